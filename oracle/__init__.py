@@ -1,0 +1,198 @@
+"""fp64 CPU oracle for the GLMB step core -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import this package.  The
+product path (``paper_2512_06230_b200``) never imports it and shares no code
+with it.  The arithmetic lives in ``glmb_oracle.c`` (plain C, fp64, every
+function cites the PAPER.md passage it follows); this module only builds it
+with gcc and marshals numpy arrays through ctypes.
+
+Parity status: every function here is pinned by ``tests/test_oracle_*.py``
+(see DESIGN.md "Oracle pins"); nothing is "parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "glmb_oracle.c")
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile glmb_oracle.c -> oracle/liboracle.so (gcc -O2, OpenMP, no fast-math)."""
+    if (not force and os.path.exists(_LIB_PATH)
+            and os.path.getmtime(_LIB_PATH) >= os.path.getmtime(_SRC)):
+        return _LIB_PATH
+    tmp = _LIB_PATH + f".tmp{os.getpid()}"
+    cmd = ["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fopenmp",
+           "-fno-fast-math", "-ffp-contract=off", _SRC, "-o", tmp, "-lm"]
+    subprocess.check_call(cmd)
+    os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            L = C.CDLL(_LIB_PATH)
+            P = np.ctypeslib.ndpointer
+            f32 = P(np.float32, flags="C_CONTIGUOUS")
+            f64 = P(np.float64, flags="C_CONTIGUOUS")
+            i32 = P(np.int32, flags="C_CONTIGUOUS")
+            u32 = P(np.uint32, flags="C_CONTIGUOUS")
+            L.oracle_philox_batch.argtypes = [C.c_uint64, u32, C.c_int64, u32]
+            L.oracle_uniform_u32.argtypes = [C.c_uint32]
+            L.oracle_uniform_u32.restype = C.c_double
+            L.oracle_normals4.argtypes = [C.c_uint64, u32, f64]
+            L.oracle_normals_batch.argtypes = [C.c_uint64, u32, C.c_int64, f64]
+            L.oracle_wrap.argtypes = [C.c_double]
+            L.oracle_wrap.restype = C.c_double
+            L.oracle_ctrv.argtypes = [f64, C.c_double, C.c_double, C.c_double, f64]
+            L.oracle_gauss2.argtypes = [C.c_double] * 7
+            L.oracle_gauss2.restype = C.c_double
+            L.oracle_loggauss2.argtypes = [C.c_double] * 7
+            L.oracle_loggauss2.restype = C.c_double
+            L.oracle_predict.argtypes = (
+                [C.c_int32, C.c_int32, C.c_int64] + [f32] * 5 + [i32]
+                + [C.c_float] * 3 + [C.c_uint64, C.c_uint32] + [f64] * 5)
+            L.oracle_birth.argtypes = (
+                [C.c_int32, C.c_int32, C.c_int64, f32, f32, i32, C.c_uint64,
+                 C.c_uint32] + [f64] * 6)
+            L.oracle_compat.argtypes = (
+                [C.c_int32, C.c_int32, C.c_int64, f32, f32, f32, C.c_int32, f32]
+                + [C.c_float] * 6 + [f64, f64, f64, C.c_int64, u32, C.c_int64])
+            L.oracle_reweight.argtypes = (
+                [C.c_int32, C.c_int32, C.c_int64, f32, f32, f32, C.c_int32, f32]
+                + [C.c_float] * 3 + [i32, C.c_int32, f64, f64, u32])
+            L.oracle_num_threads.restype = C.c_int
+            L.oracle_set_num_threads.argtypes = [C.c_int]
+            _lib = L
+    return _lib
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def set_num_threads(n: int) -> None:
+    lib().oracle_set_num_threads(int(n))
+
+
+def num_threads() -> int:
+    return int(lib().oracle_num_threads())
+
+
+# ----------------------------------------------------------------- O1-O4
+def philox(seed: int, ctr: np.ndarray) -> np.ndarray:
+    """Philox4x32-10 blocks for counters ctr [N,4] u32, key = (lo32, hi32)(seed)."""
+    ctr = np.ascontiguousarray(ctr, dtype=np.uint32).reshape(-1, 4)
+    out = np.empty_like(ctr)
+    lib().oracle_philox_batch(C.c_uint64(seed), ctr, ctr.shape[0], out)
+    return out
+
+
+def uniform_u32(r: int) -> float:
+    return float(lib().oracle_uniform_u32(int(r)))
+
+
+def normals4(seed: int, ctr) -> np.ndarray:
+    out = np.empty(4, np.float64)
+    lib().oracle_normals4(C.c_uint64(seed), np.ascontiguousarray(ctr, np.uint32), out)
+    return out
+
+
+def normals_batch(seed: int, ctr: np.ndarray) -> np.ndarray:
+    """Four normals per counter row (Box-Muller on words (0,1) and (2,3)) -> [N,4] fp64."""
+    ctr = np.ascontiguousarray(ctr, dtype=np.uint32).reshape(-1, 4)
+    out = np.empty(ctr.shape, np.float64)
+    lib().oracle_normals_batch(C.c_uint64(seed), ctr, ctr.shape[0], out)
+    return out
+
+
+def wrap(a: float) -> float:
+    return float(lib().oracle_wrap(float(a)))
+
+
+# ----------------------------------------------------------------- O5
+def ctrv(state, dt: float, nu_a: float = 0.0, nu_w: float = 0.0) -> np.ndarray:
+    s = np.ascontiguousarray(state, np.float64)
+    out = np.empty(5, np.float64)
+    lib().oracle_ctrv(s, float(dt), float(nu_a), float(nu_w), out)
+    return out
+
+
+def predict(x, y, v, psi, omega, gid, dt, sigma_a, sigma_w, seed, step):
+    """Arrays [T][ld] fp32; returns five fp64 arrays [T][ld] (P = ld)."""
+    x, y, v, psi, omega = (_f32(a) for a in (x, y, v, psi, omega))
+    T, ld = x.shape
+    outs = [np.zeros((T, ld), np.float64) for _ in range(5)]
+    lib().oracle_predict(T, ld, ld, x, y, v, psi, omega,
+                         np.ascontiguousarray(gid, np.int32), float(dt),
+                         float(sigma_a), float(sigma_w), C.c_uint64(seed),
+                         C.c_uint32(step), *outs)
+    return outs
+
+
+# ----------------------------------------------------------------- O6
+def birth(mean, chol, gid, P, seed, step):
+    """mean [B,5], chol [B,15] fp32 -> six fp64 arrays [B][P] (x,y,v,psi,omega,w)."""
+    mean, chol = _f32(mean), _f32(chol)
+    B = mean.shape[0]
+    outs = [np.zeros((B, P), np.float64) for _ in range(6)]
+    lib().oracle_birth(B, P, P, mean, chol, np.ascontiguousarray(gid, np.int32),
+                       C.c_uint64(seed), C.c_uint32(step), *outs)
+    return outs
+
+
+# ----------------------------------------------------------------- O7
+def gauss2(z, p, R) -> float:
+    return float(lib().oracle_gauss2(float(z[0]), float(z[1]), float(p[0]), float(p[1]),
+                                     float(R[0]), float(R[1]), float(R[2])))
+
+
+def loggauss2(z, p, R) -> float:
+    return float(lib().oracle_loggauss2(float(z[0]), float(z[1]), float(p[0]), float(p[1]),
+                                        float(R[0]), float(R[1]), float(R[2])))
+
+
+def compat(x, y, w, Z, R, p_d, kappa, gamma):
+    """x,y,w [T][P] fp32, Z [M,2] fp32, R = (Rxx,Rxy,Ryy).
+    Returns dict: L [T][M] (no P_D), C_clutter [M], C_tracks [T][M], gate [T][ceil(M/32)]."""
+    x, y, w = (_f32(a).reshape(np.shape(a)[0], -1) if np.size(a) else
+               np.zeros((np.shape(a)[0] if np.ndim(a) else 0, 4), np.float32) for a in (x, y, w))
+    Z = _f32(Z).reshape(-1, 2)
+    T, P = x.shape
+    M = Z.shape[0]
+    ldg = (M + 31) // 32
+    Lik = np.zeros((T, M), np.float64)
+    Ccl = np.zeros(M, np.float64)
+    Ctr = np.zeros((T, M), np.float64)
+    gate = np.zeros((T, ldg), np.uint32)
+    lib().oracle_compat(T, P, P, x, y, w, M, Z, float(R[0]), float(R[1]), float(R[2]),
+                        float(p_d), float(kappa), float(gamma), Lik, Ccl, Ctr, M, gate, ldg)
+    return {"L": Lik, "C_clutter": Ccl, "C_tracks": Ctr, "gate": gate}
+
+
+# ----------------------------------------------------------------- O8
+def reweight(x, y, w, Z, R, theta, col_offset=0):
+    """Returns (w' [T][P] fp64, logZ [T] fp64, flags [T] u32)."""
+    x, y, w = _f32(x), _f32(y), _f32(w)
+    Z = _f32(Z).reshape(-1, 2)
+    T, P = x.shape
+    M = Z.shape[0]
+    wo = np.zeros((T, P), np.float64)
+    lz = np.zeros(T, np.float64)
+    fl = np.zeros(T, np.uint32)
+    lib().oracle_reweight(T, P, P, x, y, w, M, Z, float(R[0]), float(R[1]), float(R[2]),
+                          np.ascontiguousarray(theta, np.int32), int(col_offset), wo, lz, fl)
+    return wo, lz, fl

@@ -1,0 +1,338 @@
+/*
+ * glmb_oracle.c -- plain, slow, fp64 CPU ORACLE for the GLMB step core.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * The product path (paper_2512_06230_b200/, libglmb.so) never links, loads
+ * or calls it, and shares no code, header, table or constant generator with
+ * it.  This file follows the paper's definitions written out directly, in
+ * the paper's order and notation, with no blocking, fusion or reordering.
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n (section named beside it);
+ * DESIGN.md "Readings" R1..R22 = the ambiguity register.
+ *
+ * Precision: every float input (states, weights, z, R, P_D, kappa, gamma, dt,
+ * sigmas) is the fp32 value the GPU sees, widened exactly to double; every
+ * arithmetic step below is fp64 (libm sin/cos/exp/log, correctly rounded or
+ * within 1 ulp).  Outputs are fp64.
+ *
+ * Functions and the passage each follows:
+ *   O1 oracle_philox4x32_10  -- Philox4x32-10 (Salmon et al., SC'11), R9
+ *   O2 keying                -- (seed; p, gid, step, tag) counter layout, R9
+ *   O3 oracle_uniform_u32    -- u = (2*(r>>9)+1) * 2^-24, R9
+ *   O4 Box-Muller            -- n0 = sqrt(-2 ln ua) cos(2 pi ub), n1 = ... sin, R9
+ *   O5 oracle_ctrv / oracle_predict -- CTRV survival propagation, P:3, P:24 (§Approach), R7, R8
+ *   O6 oracle_birth          -- LMB birth sampling, P:24 (§Approach), R10
+ *   O7 oracle_compat         -- C_k equation, P:26-38 (§Approach), R1-R6, R12
+ *   O8 oracle_reweight       -- particle update, P:53 (§Approach), R13, R14, R16
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define OR_PI 3.14159265358979323846
+
+int oracle_version(void) { return 1; }
+
+int oracle_num_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
+void oracle_set_num_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
+/* ------------------------------------------------------------------ O1 */
+/* Philox4x32-10: ten rounds of
+ *   (c0,c1,c2,c3) -> (hi(M1*c2)^c1^k0, lo(M1*c2), hi(M0*c0)^c3^k1, lo(M0*c0))
+ * with the key bumped by the Weyl constants (W0,W1) between rounds.
+ * Constants: Salmon, Moraes, Dror, Shaw, "Parallel random numbers: as easy
+ * as 1, 2, 3", SC'11, Philox4x32 (M0=0xD2511F53, M1=0xCD9E8D57,
+ * W0=0x9E3779B9, W1=0xBB67AE85). */
+void oracle_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2],
+                          uint32_t out[4]) {
+  const uint64_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+  const uint32_t W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+  uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+  uint32_t k0 = key_in[0], k1 = key_in[1];
+  for (int round = 0; round < 10; ++round) {
+    if (round > 0) {
+      k0 += W0;
+      k1 += W1;
+    }
+    uint64_t p0 = M0 * (uint64_t)c0;
+    uint64_t p1 = M1 * (uint64_t)c2;
+    uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0;
+    uint32_t n1 = (uint32_t)p1;
+    uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+    uint32_t n3 = (uint32_t)p0;
+    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* batched form: key = (lo32(seed), hi32(seed)) (O2) */
+void oracle_philox_batch(uint64_t seed, const uint32_t *ctr, int64_t n,
+                         uint32_t *out) {
+  uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  for (int64_t i = 0; i < n; ++i) oracle_philox4x32_10(ctr + 4 * i, key, out + 4 * i);
+}
+
+/* ------------------------------------------------------------------ O3 */
+/* u = (2*(r>>9) + 1) * 2^-24, an odd multiple of 2^-24 in [2^-24, 1-2^-24]. */
+double oracle_uniform_u32(uint32_t r) {
+  return (2.0 * (double)(r >> 9) + 1.0) * (1.0 / 16777216.0);
+}
+
+/* ------------------------------------------------------------------ O4 */
+static void box_muller(uint32_t ra, uint32_t rb, double *n0, double *n1) {
+  double ua = oracle_uniform_u32(ra);
+  double ub = oracle_uniform_u32(rb);
+  double rho = sqrt(-2.0 * log(ua));
+  *n0 = rho * cos(2.0 * OR_PI * ub);
+  *n1 = rho * sin(2.0 * OR_PI * ub);
+}
+
+/* four standard normals from one Philox block: words (0,1) -> (n0,n1),
+ * words (2,3) -> (n2,n3). */
+void oracle_normals4(uint64_t seed, const uint32_t ctr[4], double n[4]) {
+  uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  uint32_t r[4];
+  oracle_philox4x32_10(ctr, key, r);
+  box_muller(r[0], r[1], &n[0], &n[1]);
+  box_muller(r[2], r[3], &n[2], &n[3]);
+}
+
+void oracle_normals_batch(uint64_t seed, const uint32_t *ctr, int64_t n,
+                          double *out) {
+  for (int64_t i = 0; i < n; ++i) oracle_normals4(seed, ctr + 4 * i, out + 4 * i);
+}
+
+/* ------------------------------------------------------------------ O5 */
+/* wrap(a) = a - 2 pi * ceil((a - pi) / (2 pi)) in (-pi, pi] (R7). */
+double oracle_wrap(double a) {
+  return a - 2.0 * OR_PI * ceil((a - OR_PI) / (2.0 * OR_PI));
+}
+
+/* CTRV ("constant turn rate and velocity", P:3, §Approach) with the
+ * acceleration / yaw-acceleration noise terms of R7:
+ *   |omega| > 1e-4:  dx = (v/omega)(sin(psi+omega dt) - sin psi)
+ *                    dy = (v/omega)(cos psi - cos(psi+omega dt))
+ *   else (2nd-order Taylor of the same flow):
+ *                    dx = v dt cos psi - 1/2 v omega dt^2 sin psi
+ *                    dy = v dt sin psi + 1/2 v omega dt^2 cos psi
+ *   x+ = x + dx + 1/2 dt^2 cos psi nu_a
+ *   y+ = y + dy + 1/2 dt^2 sin psi nu_a
+ *   v+ = v + dt nu_a
+ *   psi+ = wrap(psi + omega dt + 1/2 dt^2 nu_w)
+ *   omega+ = omega + dt nu_w
+ * s_in/s_out: [x, y, v, psi, omega]. */
+void oracle_ctrv(const double s_in[5], double dt, double nu_a, double nu_w,
+                 double s_out[5]) {
+  double x = s_in[0], y = s_in[1], v = s_in[2], psi = s_in[3], om = s_in[4];
+  double dx, dy;
+  if (fabs(om) > 1e-4) {
+    dx = (v / om) * (sin(psi + om * dt) - sin(psi));
+    dy = (v / om) * (cos(psi) - cos(psi + om * dt));
+  } else {
+    dx = v * dt * cos(psi) - 0.5 * v * om * dt * dt * sin(psi);
+    dy = v * dt * sin(psi) + 0.5 * v * om * dt * dt * cos(psi);
+  }
+  s_out[0] = x + dx + 0.5 * dt * dt * cos(psi) * nu_a;
+  s_out[1] = y + dy + 0.5 * dt * dt * sin(psi) * nu_a;
+  s_out[2] = v + dt * nu_a;
+  s_out[3] = oracle_wrap(psi + om * dt + 0.5 * dt * dt * nu_w);
+  s_out[4] = om + dt * nu_w;
+}
+
+/* Survival prediction: "particles representing targets that have survived
+ * from step k-1 are propagated forward using the constant turn rate and
+ * velocity kinematics model ... as a batch operation over all particles and
+ * surviving tracks" (§Approach).  Noise: Philox block with counter
+ * (p, gid_j, step, tag=0) (O2, domain 0 = predict); nu_a = sigma_a n0,
+ * nu_w = sigma_w n1.  Element (j,p) at j*ld + p.  Outputs fp64 [T][ld]. */
+void oracle_predict(int32_t T, int32_t P, int64_t ld, const float *x,
+                    const float *y, const float *v, const float *psi,
+                    const float *omega, const int32_t *gid, float dt,
+                    float sigma_a, float sigma_w, uint64_t seed, uint32_t step,
+                    double *ox, double *oy, double *ov, double *opsi,
+                    double *oomega) {
+#pragma omp parallel for schedule(dynamic)
+  for (int32_t j = 0; j < T; ++j) {
+    for (int32_t p = 0; p < P; ++p) {
+      int64_t e = (int64_t)j * ld + p;
+      uint32_t ctr[4] = {(uint32_t)p, (uint32_t)gid[j], step, 0u};
+      double n[4];
+      oracle_normals4(seed, ctr, n);
+      double s[5] = {x[e], y[e], v[e], psi[e], omega[e]}, o[5];
+      oracle_ctrv(s, (double)dt, (double)sigma_a * n[0], (double)sigma_w * n[1], o);
+      ox[e] = o[0]; oy[e] = o[1]; ov[e] = o[2]; opsi[e] = o[3]; oomega[e] = o[4];
+    }
+  }
+}
+
+/* ------------------------------------------------------------------ O6 */
+/* LMB birth: "a set of particles is sampled from the birth probability
+ * distribution for each new track" (§Approach); distribution
+ * N(mu_b, L_b L_b^T) (R10).  Draws: block tag (1<<8|0) gives n0..n3, block
+ * tag (1<<8|1) words (0,1) give n4.  x = mu_b + L_b n, psi wrapped, w = 1/P.
+ * mean: [B][5]; chol: [B][15] row-major packed lower triangle. */
+void oracle_birth(int32_t B, int32_t P, int64_t ld, const float *mean,
+                  const float *chol, const int32_t *gid, uint64_t seed,
+                  uint32_t step, double *ox, double *oy, double *ov,
+                  double *opsi, double *oomega, double *ow) {
+#pragma omp parallel for schedule(dynamic)
+  for (int32_t b = 0; b < B; ++b) {
+    for (int32_t p = 0; p < P; ++p) {
+      int64_t e = (int64_t)b * ld + p;
+      uint32_t c0[4] = {(uint32_t)p, (uint32_t)gid[b], step, (1u << 8) | 0u};
+      uint32_t c1[4] = {(uint32_t)p, (uint32_t)gid[b], step, (1u << 8) | 1u};
+      double na[4], nb[4];
+      oracle_normals4(seed, c0, na);
+      oracle_normals4(seed, c1, nb);
+      double n[5] = {na[0], na[1], na[2], na[3], nb[0]};
+      double s[5];
+      int idx = 0;
+      for (int r = 0; r < 5; ++r) {
+        double acc = (double)mean[b * 5 + r];
+        for (int c = 0; c <= r; ++c) acc += (double)chol[b * 15 + idx + c] * n[c];
+        idx += r + 1;
+        s[r] = acc;
+      }
+      ox[e] = s[0]; oy[e] = s[1]; ov[e] = s[2];
+      opsi[e] = oracle_wrap(s[3]);
+      oomega[e] = s[4];
+      ow[e] = 1.0 / (double)P;
+    }
+  }
+}
+
+/* ------------------------------------------------------------------ O7 */
+/* N(z; (px,py), R) for a 2x2 SPD R = [[Rxx,Rxy],[Rxy,Ryy]]:
+ *   exp(-1/2 d^T R^-1 d) / (2 pi sqrt(det R)),  d = z - (px,py),
+ *   R^-1 = [[Ryy, -Rxy], [-Rxy, Rxx]] / det R. */
+double oracle_gauss2(double zx, double zy, double px, double py, double Rxx,
+                     double Rxy, double Ryy) {
+  double det = Rxx * Ryy - Rxy * Rxy;
+  double dx = zx - px, dy = zy - py;
+  double q = (Ryy * dx * dx - 2.0 * Rxy * dx * dy + Rxx * dy * dy) / det;
+  return exp(-0.5 * q) / (2.0 * OR_PI * sqrt(det));
+}
+
+/* ln N(z; (px,py), R) = -1/2 d^T R^-1 d - ln(2 pi sqrt(det R)), the same
+ * density in log form (no underflow for far-away particles). */
+double oracle_loggauss2(double zx, double zy, double px, double py, double Rxx,
+                        double Rxy, double Ryy) {
+  double det = Rxx * Ryy - Rxy * Rxy;
+  double dx = zx - px, dy = zy - py;
+  double q = (Ryy * dx * dx - 2.0 * Rxy * dx * dy + Rxx * dy * dy) / det;
+  return -0.5 * q - log(2.0 * OR_PI * sqrt(det));
+}
+
+/* Compatibility matrix, P:26-38 (§Approach, equation for C_k):
+ *   C[i,j] = g_ij * P_D * L(z_i | x_j)   for j = 1..T_k   (R1: P_D factor)
+ *   C[i,0] = kappa                                         (clutter, R5)
+ *   g_ij   = [L(z_i | x_j) >= gamma]                       (R2)
+ *   L(z | x_j) = sum_p w_jp N(z; H x_jp, R), H = [I2 0]    (R3)
+ * Weights are used as supplied (R12).  Sum over p is sequential fp64.
+ * Outputs: Lik [T][M] (L without P_D, for the gate band), C_clutter [M],
+ * C_tracks [T][ldc] (column-major C: column j+1 of C is row j here),
+ * gate [T][ldg] u32 words, bit (i%32) of word i/32. */
+void oracle_compat(int32_t T, int32_t P, int64_t ld, const float *x,
+                   const float *y, const float *w, int32_t M, const float *Z,
+                   float Rxx, float Rxy, float Ryy, float p_d, float kappa,
+                   float gamma, double *Lik, double *C_clutter,
+                   double *C_tracks, int64_t ldc, uint32_t *gate,
+                   int64_t ldg) {
+  for (int32_t i = 0; i < M; ++i) C_clutter[i] = (double)kappa;
+#pragma omp parallel for schedule(dynamic)
+  for (int32_t j = 0; j < T; ++j) {
+    for (int64_t k = 0; k < ldg; ++k) gate[(int64_t)j * ldg + k] = 0u;
+    for (int32_t i = 0; i < M; ++i) {
+      double L = 0.0;
+      for (int32_t p = 0; p < P; ++p) {
+        int64_t e = (int64_t)j * ld + p;
+        L += (double)w[e] * oracle_gauss2(Z[2 * i], Z[2 * i + 1], x[e], y[e],
+                                          Rxx, Rxy, Ryy);
+      }
+      int g = (L >= (double)gamma);
+      Lik[(int64_t)j * M + i] = L;
+      C_tracks[(int64_t)j * ldc + i] = g ? (double)p_d * L : 0.0;
+      if (g) gate[(int64_t)j * ldg + i / 32] |= (1u << (i % 32));
+    }
+  }
+}
+
+/* ------------------------------------------------------------------ O8 */
+/* Particle update, P:53 (§Approach): "The particle weights are updated
+ * according to the measurement likelihood" -- Bayes' rule on the weights of
+ * track j for every measurement the association map theta assigns to it
+ * (R13, R14: theta[i] = 0 clutter, theta[i] = c >= 1 means C column c;
+ * local track j is column col_offset + j + 1):
+ *   S_j = {i : theta_i = col_offset + j + 1}
+ *   S_j empty : w unchanged, logZ_j = ln sum_p w_p, flag 0
+ *   otherwise : l_p = ln w_p + sum_{i in S_j} ln N(z_i; (x_p,y_p), R)
+ *               (ln N via oracle_loggauss2, the log of the same density)
+ *               m = max_p l_p ; m = -inf -> w' = 1/P, flag bit0 (R16)
+ *               w'_p = exp(l_p - m) / sum_q exp(l_q - m)
+ *               logZ_j = m + ln sum_q exp(l_q - m)
+ * (logZ_j = ln sum_p w_p prod_i N(z_i; .), the log normaliser; the max
+ * shift is only fp64 range safety). */
+void oracle_reweight(int32_t T, int32_t P, int64_t ld, const float *x,
+                     const float *y, const float *w, int32_t M, const float *Z,
+                     float Rxx, float Rxy, float Ryy, const int32_t *theta,
+                     int32_t col_offset, double *w_out, double *logZ,
+                     uint32_t *flags) {
+#pragma omp parallel for schedule(dynamic)
+  for (int32_t j = 0; j < T; ++j) {
+    int32_t col = col_offset + j + 1;
+    int nS = 0;
+    for (int32_t i = 0; i < M; ++i) nS += (theta[i] == col);
+    int64_t base = (int64_t)j * ld;
+    flags[j] = 0u;
+    if (nS == 0) {
+      double s = 0.0;
+      for (int32_t p = 0; p < P; ++p) {
+        w_out[base + p] = (double)w[base + p];
+        s += (double)w[base + p];
+      }
+      logZ[j] = log(s);
+      continue;
+    }
+    double *l = (double *)malloc(sizeof(double) * (size_t)(P > 0 ? P : 1));
+    double m = -INFINITY;
+    for (int32_t p = 0; p < P; ++p) {
+      double lp = log((double)w[base + p]);
+      for (int32_t i = 0; i < M; ++i)
+        if (theta[i] == col)
+          lp += oracle_loggauss2(Z[2 * i], Z[2 * i + 1], x[base + p],
+                                 y[base + p], Rxx, Rxy, Ryy);
+      l[p] = lp;
+      if (lp > m) m = lp;
+    }
+    if (m == -INFINITY) {
+      for (int32_t p = 0; p < P; ++p) w_out[base + p] = 1.0 / (double)P;
+      logZ[j] = -INFINITY;
+      flags[j] = 1u;
+    } else {
+      double s = 0.0;
+      for (int32_t p = 0; p < P; ++p) s += exp(l[p] - m);
+      for (int32_t p = 0; p < P; ++p) w_out[base + p] = exp(l[p] - m) / s;
+      logZ[j] = m + log(s);
+    }
+    free(l);
+  }
+}
