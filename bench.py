@@ -1,0 +1,398 @@
+#!/usr/bin/env python
+"""bench.py -- one GLMB step core (predict + birth + compat + reweight) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl glmb|reference]
+
+Metric (BASELINE.json): particle-measurement likelihood evals/s (whole job,
+all ranks) and ms per GLMB step.  Evals per step = M_k*T_k*P (compat, the
+dense mixture) + P*#{i: theta_i != 0} (reweight).  Workload: BASELINE config 3
+(T=1024+16 births, P=8192, M~1200) at N=1; config 4 (T=4096, P=8192, M~4800,
+tracks sharded, Z/theta broadcast, C all-gathered over NCCL) at N>1.
+
+Timing: W untimed warm-up steps, then K steps bracketed by barrier +
+synchronize, CUDA events on the launching stream, max over ranks.  Inputs
+(particle state 204 MB at cfg3, > 126 MB L2) stream through HBM every step.
+Rank 0 prints one JSON line.  The oracle (oracle/, fp64 CPU) is executed only
+in the cpu_baseline leg and in --impl reference.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particle-measurement likelihood evals/s (GLMB step: predict+birth+compat+reweight)"
+SFU_EX2_PER_CLK_PER_SM = 16          # MUFU.EX2 lanes/clk/SM on sm_100
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=None)
+    ap.add_argument("--impl", default="glmb", choices=["glmb", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """Polls NVML every 5 ms while active: SM clock, max clock, throttle reasons."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.ok = [], set(), False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # noqa: BLE001
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": float(self.max_mhz),
+                "samples": len(self.samples), "reasons": sorted(self.reasons)}
+
+
+# ------------------------------------------------------------------ CPU oracle legs
+def oracle_sample(cfg_id: int, seconds: float, cores: int):
+    """Time the fp64 oracle (as it stands) on a bounded sample of the workload:
+    the first n tracks of the config -- predict, compat over all M, reweight --
+    with OpenMP over tracks.  n is calibrated so the run takes ~`seconds`."""
+    import oracle
+    from paper_2512_06230_b200.scenes import make_scene
+    oracle.set_num_threads(cores)
+    base = make_scene(cfg_id, rows=range(0), steps=1)
+    c = base.cfg
+    Z, th = base.Z[0], base.theta[0]
+
+    def run(n):
+        s = make_scene(cfg_id, rows=range(n), steps=1)
+        t0 = time.perf_counter()
+        px, py, pv, pp, po = oracle.predict(s.x, s.y, s.v, s.psi, s.omega, s.gid, c.dt, c.sigma_a,
+                                            c.sigma_w, c.seed, 0)
+        x32, y32 = px.astype(np.float32), py.astype(np.float32)
+        oracle.compat(x32, y32, s.w, Z, c.R, c.p_d, c.kappa, c.gamma)
+        oracle.reweight(x32, y32, s.w, Z, c.R, th, 0)
+        dt = time.perf_counter() - t0
+        n_assigned = int(((th >= 1) & (th <= n)).sum())
+        return dt, len(Z) * n * c.P + c.P * n_assigned
+
+    n0 = max(1, min(c.T, cores))
+    t0, _ = run(n0)
+    n = int(min(c.T, max(n0, n0 * seconds / max(t0, 1e-3))))
+    n = max(n0, (n // n0) * n0)
+    dt, evals = run(n)
+    return {"value": evals / dt, "unit": "evals/s", "cores": cores, "kind": "oracle",
+            "sample": f"cfg{cfg_id}: first {n} of {c.T + c.B} tracks x all M={len(Z)} x P={c.P} "
+                      f"(predict+compat+reweight, fp64, OpenMP over tracks), {dt:.2f} s",
+            "seconds": dt, "evals": evals}
+
+
+def reference_arm(a, cfg_id):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2512_06230_b200.scenes import make_scene
+    cores = host_cores()
+    full = make_scene(cfg_id, rows=range(0), steps=1)
+    c = full.cfg
+    th = full.theta[0]
+    full_evals = len(full.Z[0]) * (c.T + c.B) * c.P + c.P * int((th != 0).sum())
+    per_step = max(2.0, 120.0 / max(1, a.steps + a.warmup))
+    times, evals = [], []
+    for k in range(a.warmup + a.steps):
+        r = oracle_sample(cfg_id, per_step, cores)
+        if k >= a.warmup:
+            times.append(r["seconds"])
+            evals.append(r["evals"])
+    value = sum(evals) / sum(times)
+    ms = full_evals / value * 1e3
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s",
+            "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"cfg{cfg_id}", "T": c.T, "B": c.B, "P": c.P,
+                       "M": len(full.Z[0]), "note": "oracle on a bounded sample per step; "
+                       "ms_per_step extrapolated to the full step at the sampled rate"},
+            "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "oracle",
+                             "sample": r["sample"]},
+            "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    a = parse()
+    rank, world, local = dist_env()
+    cfg_id = a.config if a.config is not None else (3 if world == 1 else 4)
+    if a.impl == "reference":
+        return reference_arm(a, cfg_id)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2512_06230_b200 import _lib as L
+    from paper_2512_06230_b200.build import build
+    from paper_2512_06230_b200.scenes import CONFIGS, make_scene
+    from paper_2512_06230_b200.step import GlmbStep, shard_range
+
+    if rank == 0:
+        build()
+    if world > 1:
+        dist.init_process_group("nccl")
+        dist.barrier()
+        build()  # no-op once rank 0 has built
+    torch.cuda.set_device(local)
+    L.glmb_init(local)
+    dev = torch.device("cuda", local)
+    cfg = CONFIGS[cfg_id]
+    Tk = cfg.T + cfg.B
+    cols = shard_range(Tk, rank, world)
+    per = (Tk + world - 1) // world
+    n_steps_scene = min(cfg.steps, a.warmup + a.steps)
+    scene = make_scene(cfg_id, rows=range(cols.start, min(cols.stop, cfg.T)), steps=n_steps_scene)
+    st = GlmbStep(scene, cols=cols, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    # W>1: Z/theta live on rank 0 and are broadcast inside the timed region;
+    # column blocks of C (+ gate words) are all-gathered into the full matrix.
+    if world > 1:
+        if per * world != Tk:
+            raise SystemExit("config 4 sharding expects T_k divisible by the world size")
+        Zbuf = torch.zeros(st.M_max, 2, device=dev)
+        thbuf = torch.zeros(st.M_max, dtype=torch.int32, device=dev)
+        C_full = torch.empty(Tk, st.ldc, device=dev)
+        G_full = torch.empty(Tk, st.ldg, dtype=torch.int32, device=dev)
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    stage_names = ["predict", "birth", "compat", "reweight"]
+    stage_ms = {n: [] for n in stage_names}
+
+    def one_step(k, timed):
+        zi = k % len(st.Z)
+        with torch.cuda.stream(stream):
+            if world > 1:
+                M = st.Z[zi].shape[0]
+                if rank == 0:
+                    Zbuf[:M].copy_(st.Z[zi]); thbuf[:M].copy_(st.theta[zi])
+                dist.broadcast(Zbuf[:M], src=0)
+                dist.broadcast(thbuf[:M], src=0)
+                Zk, thk = Zbuf[:M], thbuf[:M]
+            else:
+                Zk, thk = st.Z[zi], st.theta[zi]
+            marks = [ev() for _ in range(5)] if timed else None
+            if timed:
+                marks[0].record(stream)
+            st.predict(k, stream)
+            if timed:
+                marks[1].record(stream)
+            st.birth(k, stream)
+            if timed:
+                marks[2].record(stream)
+            st.compat(k, stream, Z=Zk)
+            if timed:
+                marks[3].record(stream)
+            st.reweight(k, stream, Z=Zk, theta=thk)
+            if timed:
+                marks[4].record(stream)
+            if world > 1:
+                dist.all_gather_into_tensor(C_full, st.out.C_tracks)
+                dist.all_gather_into_tensor(G_full, st.out.gate)
+        return marks
+
+    for k in range(a.warmup):
+        one_step(k, False)
+    torch.cuda.synchronize(dev)
+    sampler = ClockSampler(local)
+    all_marks = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t_start, t_end = ev(), ev()
+    with sampler:
+        t_start.record(stream)
+        for k in range(a.warmup, a.warmup + a.steps):
+            all_marks.append(one_step(k, True))
+        t_end.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    for m in all_marks:
+        for i, n in enumerate(stage_names):
+            stage_ms[n].append(m[i].elapsed_time(m[i + 1]))
+    evals_local = sum(st.evals(k) for k in range(a.warmup, a.warmup + a.steps))
+    pairs_local = sum(len(scene.Z[k % len(scene.Z)]) * st.T_local * st.P
+                      for k in range(a.warmup, a.warmup + a.steps))
+    if world > 1:
+        t = torch.tensor([elapsed_ms, float(evals_local)], dtype=torch.float64, device=dev)
+        tmax = t.clone(); dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
+        tsum = t.clone(); dist.all_reduce(tsum[1:], op=dist.ReduceOp.SUM)
+        elapsed_ms, evals_total = float(tmax[0]), float(tsum[1])
+    else:
+        evals_total = float(evals_local)
+
+    # ---- end to end through the public C-ABI entry with host buffers (N=1 leg per rank)
+    e2e = None
+    if not a.no_e2e:
+        M_max = st.M_max
+        pin = lambda t: t.pin_memory()
+        Zh = [pin(torch.from_numpy(z)) for z in scene.Z]
+        thh = [pin(torch.from_numpy(t)) for t in scene.theta]
+        Zd = torch.empty(M_max, 2, device=dev)
+        thd = torch.empty(M_max, dtype=torch.int32, device=dev)
+        o = st.out
+        Cc_h = pin(torch.empty(M_max))
+        Ct_h = pin(torch.empty(st.T_local, st.ldc))
+        G_h = pin(torch.empty(st.T_local, st.ldg, dtype=torch.int32))
+        ln_h = pin(torch.empty(st.T_local))
+        fl_h = pin(torch.empty(st.T_local, dtype=torch.int32))
+        h2d = d2h = 0
+
+        def host_step(k):
+            zi = k % len(Zh)
+            L.glmb_step_host(st.step_params(k), Zh[zi], thh[zi], Zd, thd, o.C_clutter, o.C_tracks,
+                             o.gate, o.log_norm, o.flags, Cc_h, Ct_h, G_h, ln_h, fl_h, stream)
+            M = Zh[zi].shape[0]
+            return M * 8 + M * 4, M * 4 + st.T_local * st.ldc * 4 + st.T_local * st.ldg * 4 + st.T_local * 8
+
+        for k in range(a.warmup):
+            host_step(k)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for k in range(a.warmup, a.warmup + a.steps):
+            hb, db = host_step(k)
+            h2d += hb
+            d2h += db
+        e2e_s = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t[0])
+        e2e = {"value": evals_total / e2e_s, "unit": "evals/s",
+               "h2d_bytes_per_step": h2d // a.steps, "d2h_bytes_per_step": d2h // a.steps,
+               "ms_per_step": e2e_s * 1e3 / a.steps,
+               "note": "glmb_step_host: pinned H2D of Z_k, theta_k; step; D2H of C_k, gate, "
+                       "log_norm, flags; stream synchronised each step; particle state resident"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (compat): SFU-bound, one MUFU.EX2 per pair
+    sm_count = L.glmb_sm_count(local)
+    clocks = sampler.summary()
+    f_max = (clocks["sm_max_mhz"] or 1965.0) * 1e6
+    peak = sm_count * SFU_EX2_PER_CLK_PER_SM * f_max
+    compat_ms = statistics.mean(stage_ms["compat"])
+    pairs_per_launch = pairs_local / a.steps
+    achieved = pairs_per_launch / (compat_ms * 1e-3)
+    stage_mean = {n: statistics.mean(v) for n, v in stage_ms.items()}
+    predict_bytes = st.T_surv * st.P * 40
+    reweight_bytes = st.T_local * st.P * 16
+    launches_per_step = (1 if st.T_surv else 0) + (1 if st.B_local else 0) + 1 + 1
+    cpu = None
+    if world == 1 and not a.no_cpu_baseline:
+        cpu = oracle_sample(cfg_id, a.cpu_seconds, host_cores())
+        cpu = {k: v for k, v in cpu.items() if k in ("value", "unit", "cores", "kind", "sample")}
+    Ms = [len(scene.Z[k % len(scene.Z)]) for k in range(a.warmup, a.warmup + a.steps)]
+    line = {
+        "metric": METRIC,
+        "value": evals_total / (elapsed_ms * 1e-3),
+        "unit": "evals/s",
+        "n_gpus": world,
+        "steps": a.steps,
+        "warmup": a.warmup,
+        "ms_per_step": elapsed_ms / a.steps,
+        "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": f"cfg{cfg_id} ({cfg.name})", "T": cfg.T, "B": cfg.B, "P": cfg.P,
+                   "M_mean": float(np.mean(Ms)), "parallelism": f"tracks sharded x{world}",
+                   "l2": "particle state 24 B x T_k x P > 126 MB L2 streams from HBM every step",
+                   "evals_per_step": evals_total / a.steps},
+        "roofline": {"bound": "alu", "kernel": "compat (MUFU.EX2 SFU pipe)",
+                     "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Geval/s",
+                     "frac": achieved / peak,
+                     "peak_basis": f"{sm_count} SM x {SFU_EX2_PER_CLK_PER_SM} ex2/clk x "
+                                   f"{f_max / 1e6:.0f} MHz (max SM clock)",
+                     "frac_at_measured_clock": (achieved / (sm_count * SFU_EX2_PER_CLK_PER_SM *
+                                                            clocks["sm_mhz"] * 1e6)
+                                                if clocks["sm_mhz"] else None),
+                     "traffic": None},
+        "stages_ms": stage_mean,
+        "hbm": {"predict_GBps": predict_bytes / (stage_mean["predict"] * 1e-3) / 1e9,
+                "reweight_GBps": reweight_bytes / (stage_mean["reweight"] * 1e-3) / 1e9},
+        "gpu_launches": launches_per_step * a.steps,
+        "clocks": clocks,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

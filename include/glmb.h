@@ -1,0 +1,250 @@
+/*
+ * glmb.h -- C ABI of the B200-native GLMB step core (arXiv 2512.06230).
+ *
+ * The library (paper_2512_06230_b200/libglmb.so, sm_100a) implements the
+ * data-parallel core of one step of the paper's particle GLMB tracker:
+ *
+ *   glmb_predict   CTRV survival propagation of every particle of every
+ *                  surviving track, with Philox4x32-10 process noise
+ *                  (§Approach "propagated forward using the
+ *                  constant turn rate and velocity kinematics model ... a
+ *                  batch operation over all particles and surviving tracks").
+ *   glmb_birth     LMB birth sampling, P particles per new track from
+ *                  N(mu_b, L_b L_b^T)  ("a set of particles is sampled
+ *                  from the birth probability distribution for each new track").
+ *   glmb_compat    the M_k x (T_k+1) compatibility matrix C_k with gate bits
+ *                  (equation for C_k; P:37 gate g = [L >= gamma];
+ *                  P:39 "the entire construction ... can be performed in
+ *                  parallel").
+ *   glmb_reweight  per-track particle reweighting under a supplied
+ *                  association map theta_k (P:42 theta_k; "The particle
+ *                  weights are updated according to the measurement likelihood").
+ *
+ * Readings of the paper where it is silent or ambiguous (P_D factor in C,
+ * gate on L without P_D, kappa as an intensity, the CTRV noise terms, the
+ * Philox keying, theta encoding) are listed in DESIGN.md ("Readings").
+ *
+ * Conventions shared by every call
+ * --------------------------------
+ *  - Every pointer argument is a DEVICE pointer (cudaMalloc / torch CUDA
+ *    memory) owned by the caller, unless the parameter name ends in _host.
+ *    The library never allocates, frees or retains a pointer.
+ *  - Calls validate their arguments, enqueue kernels on `stream` and return
+ *    without synchronising (except glmb_step_host, which is synchronous).
+ *    Launch failures return GLMB_ERR_CUDA; execution faults surface at the
+ *    caller's next synchronisation.  No call ever aborts the process.
+ *  - `stream` is a cudaStream_t (ABI-compatible typedef below).  A non-NULL
+ *    stream selects the device; NULL means the legacy default stream of the
+ *    calling thread's current device.
+ *  - Particle arrays are SoA, track-major fp32: element (j, p) of each array
+ *    is at j*ld + p.  Requirements: n_particles >= 4 and a multiple of 4,
+ *    ld >= n_particles and a multiple of 4, every array 16-byte aligned
+ *    (GLMB_ERR_ALIGNMENT otherwise).  Elements p in [n_particles, ld) are
+ *    never read or written.
+ *  - M == 0 gives a 0-row C (glmb_compat writes nothing); glmb_reweight
+ *    with M == 0 leaves every weight untouched and writes log_norm = ln sum w.
+ *    n_tracks == 0 is a no-op for predict/birth/reweight; glmb_compat with
+ *    n_tracks == 0 writes only C_clutter (the clutter-only matrix).
+ *  - Coordinates are metres in a local frame; |x|,|y| <= 1e4 m keeps the
+ *    fp32 contract of DESIGN.md (fp32 resolution 1e-3 m at 1e4 m).
+ *  - NaN inputs are not flagged: a NaN likelihood compares false against
+ *    gamma, so g = 0 and C = 0 for that entry.
+ */
+#ifndef GLMB_H_
+#define GLMB_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *glmb_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  GLMB_OK = 0,
+  GLMB_ERR_INVALID_ARG = -1,        /* a size, parameter or null pointer violates the contract */
+  GLMB_ERR_ALIGNMENT = -2,          /* an array is not 16-B aligned or ld/P not multiples of 4 */
+  GLMB_ERR_UNSUPPORTED_DEVICE = -3, /* device is not compute capability 10.0 (sm_100a) */
+  GLMB_ERR_CUDA = -4                /* a CUDA runtime call or kernel launch failed */
+} glmb_status;
+
+/* Particle set: T tracks x P particles, SoA fp32 [T][ld] per array.
+ * Pointers may alias none of each other.  `w` are the particle weights
+ * w_j^p of P:21 (used as supplied: compat does not renormalise them). */
+typedef struct {
+  float *x, *y, *v, *psi, *omega, *w;
+  int32_t n_tracks;    /* T >= 0                                 */
+  int32_t n_particles; /* P >= 4, P % 4 == 0                      */
+  int64_t ld;          /* >= P, ld % 4 == 0                       */
+} glmb_particles;
+
+/* Library version (major*10000 + minor*100 + patch). */
+int glmb_version(void);
+
+/* Human-readable text of a status code (static storage, never NULL). */
+const char *glmb_status_string(glmb_status s);
+
+/* Checks that `device` is compute capability 10.0 and caches its SM count.
+ * Optional: every other call performs the same check lazily.
+ * Returns GLMB_ERR_UNSUPPORTED_DEVICE on any other device. */
+glmb_status glmb_init(int device);
+
+/* Number of streaming multiprocessors of `device` (0 on error). */
+int glmb_sm_count(int device);
+
+/* ---------------------------------------------------------------------
+ * glmb_predict -- CTRV survival propagation (P:3, §Approach).
+ *
+ * For every track j < in->n_tracks and particle p < P:
+ *   (n0, n1) = Box-Muller(Philox4x32-10(key = (lo32 seed, hi32 seed),
+ *                                      counter = (p, gid[j], step, 0)))
+ *   nu_a = sigma_a * n0,  nu_w = sigma_w * n1
+ *   h = omega dt / 2
+ *   x'     = x + v dt sinc(h) cos(psi + h) + 1/2 dt^2 cos(psi) nu_a
+ *   y'     = y + v dt sinc(h) sin(psi + h) + 1/2 dt^2 sin(psi) nu_a
+ *   v'     = v + dt nu_a
+ *   psi'   = wrap(psi + omega dt + 1/2 dt^2 nu_w)   in (-pi, pi]
+ *   omega' = omega + dt nu_w
+ * (the half-angle form of the CTRV flow; identical to
+ *  (v/omega)(sin(psi+omega dt) - sin psi) etc., stable as omega -> 0.)
+ * Weights are not touched.  `out` may equal `in` (in place); otherwise
+ * in/out must not overlap and must have the same n_tracks / n_particles.
+ * gid: [n_tracks] int32 global track ids (the Philox key word; makes the
+ * draws independent of sharding and column position).
+ * Errors: INVALID_ARG if dt <= 0, sigma_a < 0, sigma_w < 0, shape mismatch,
+ * or a NULL pointer with n_tracks > 0.
+ * --------------------------------------------------------------------- */
+glmb_status glmb_predict(const glmb_particles *in, const glmb_particles *out,
+                         const int32_t *gid, float dt, float sigma_a,
+                         float sigma_w, uint64_t seed, uint32_t step,
+                         glmb_stream_t stream);
+
+/* ---------------------------------------------------------------------
+ * glmb_birth -- LMB birth sampling (§Approach).
+ *
+ * For every birth track b < out->n_tracks and particle p < P:
+ *   n0..n3 = Box-Muller normals of Philox(counter = (p, gid[b], step, 0x100))
+ *   n4     = first normal of Philox(counter = (p, gid[b], step, 0x101))
+ *   s = mean[b] + L_b n          (L_b = chol[b], packed row-major lower
+ *                                 triangle: L00, L10 L11, L20 L21 L22, ...)
+ *   (x, y, v, psi, omega) = (s0, s1, s2, wrap(s3), s4),  w = 1/P
+ * `out` describes the B birth rows (typically the particle arrays offset to
+ * row T, so births follow the survivors: C column T+b+1).
+ * mean: [B][5] fp32, chol: [B][15] fp32, gid: [B] int32 (device).
+ * Errors: INVALID_ARG on NULL pointers with B > 0.
+ * --------------------------------------------------------------------- */
+glmb_status glmb_birth(const glmb_particles *out, const int32_t *gid,
+                       const float *mean, const float *chol, uint64_t seed,
+                       uint32_t step, glmb_stream_t stream);
+
+/* ---------------------------------------------------------------------
+ * glmb_compat -- compatibility matrix C_k (§Approach).
+ *
+ *   L_ij = sum_p w_jp N(z_i; (x_jp, y_jp), R)         (H = [I2 0])
+ *   g_ij = [L_ij >= gamma]                             (inclusive)
+ *   C[i, j+1] = g_ij ? p_d * L_ij : 0
+ *   C[i, 0]   = kappa                                  (clutter)
+ * for i < M, j < trk->n_tracks.  The sum is the dense mixture over all P
+ * particles (the gate is applied after L).
+ *
+ * Z: [M][2] fp32 measurements z_i (x, y).
+ * R = [[Rxx, Rxy], [Rxy, Ryy]] must be SPD.
+ * Outputs (column-major C, each column contiguous over measurements):
+ *   C_clutter [M] fp32      = kappa (may be NULL: not written)
+ *   C_tracks  [T][ldc] fp32, entry (j, i) = C[i, j+1]; ldc >= M.
+ *             Entries i in [M, ldc) are not written.
+ *   gate      [T][ldg] u32, bit (i % 32) of word (j, i / 32) = g_ij;
+ *             ldg >= ceil(M/32); bits i >= M of the last word are 0;
+ *             words >= ceil(M/32) are not written.
+ * Results are bit-identical for any n_tracks split (sharding) and any row
+ * permutation of Z (each entry is computed independently, in a fixed
+ * particle order).
+ * Errors: INVALID_ARG if R is not SPD, p_d not in (0,1], kappa < 0,
+ * gamma < 1e-30 (the fp32 exactness precondition), ldc < M,
+ * ldg < ceil(M/32), or NULL outputs with T > 0 and M > 0.
+ * --------------------------------------------------------------------- */
+glmb_status glmb_compat(const glmb_particles *trk, const float *Z, int32_t M,
+                        float Rxx, float Rxy, float Ryy, float p_d,
+                        float kappa, float gamma, float *C_clutter,
+                        float *C_tracks, int64_t ldc, uint32_t *gate,
+                        int64_t ldg, glmb_stream_t stream);
+
+/* ---------------------------------------------------------------------
+ * glmb_reweight -- particle update under theta_k (§Approach).
+ *
+ * theta: [M] int32, theta[i] = 0 means clutter, c >= 1 means C column c
+ * (values outside [0, col_offset + T] are ignored).  Local track j is C
+ * column col_offset + j + 1 (col_offset = global index of local track 0).
+ *   S_j = { i : theta[i] == col_offset + j + 1 }
+ *   S_j empty: w unchanged, log_norm[j] = ln sum_p w_p, flags[j] = 0
+ *   else:      l_p = ln w_p + sum_{i in S_j} ln N(z_i; (x_p, y_p), R)
+ *              w'_p = exp(l_p - m) / sum_q exp(l_q - m),  m = max_p l_p
+ *              log_norm[j] = m + ln sum_q exp(l_q - m)
+ *              if every w_p == 0: w'_p = 1/P, log_norm = -inf, flags[j] = 1
+ * w is updated in place.  log_norm: [T] fp32, flags: [T] u32 (bit 0 =
+ * degenerate track reset to uniform).
+ * Errors: INVALID_ARG if R is not SPD or a needed pointer is NULL.
+ * --------------------------------------------------------------------- */
+glmb_status glmb_reweight(const glmb_particles *trk, const float *Z,
+                          int32_t M, float Rxx, float Rxy, float Ryy,
+                          const int32_t *theta, int32_t col_offset,
+                          float *log_norm, uint32_t *flags,
+                          glmb_stream_t stream);
+
+/* ---------------------------------------------------------------------
+ * One whole step: predict (rows [0, n_survivors)) -> birth (rows
+ * [n_survivors, tracks.n_tracks)) -> compat (all rows) -> reweight (all
+ * rows), enqueued on `stream`.  Exactly the four calls above, in order.
+ * --------------------------------------------------------------------- */
+typedef struct {
+  glmb_particles tracks;   /* T_k = T + B rows: survivors then births   */
+  int32_t n_survivors;     /* T                                          */
+  const int32_t *gid;      /* [T_k] global ids (device)                  */
+  const float *birth_mean; /* [B][5] (device)                            */
+  const float *birth_chol; /* [B][15] (device)                           */
+  float dt, sigma_a, sigma_w;
+  uint64_t seed;
+  uint32_t step;
+  float Rxx, Rxy, Ryy, p_d, kappa, gamma;
+  int32_t col_offset;      /* global column offset of local row 0        */
+} glmb_step_params;
+
+glmb_status glmb_step(const glmb_step_params *prm, const float *Z, int32_t M,
+                      const int32_t *theta, float *C_clutter, float *C_tracks,
+                      int64_t ldc, uint32_t *gate, int64_t ldg,
+                      float *log_norm, uint32_t *flags, glmb_stream_t stream);
+
+/* End-to-end step with HOST inputs and outputs (synchronous).
+ * Copies Z_host [M][2] and theta_host [M] (pinned host memory recommended)
+ * into the device workspaces Z_dev / theta_dev (capacity >= M), runs
+ * glmb_step, copies C_clutter, C_tracks ([T_k][ldc]), gate ([T_k][ldg]),
+ * log_norm and flags back into the *_host buffers, then synchronises
+ * `stream`.  The particle state stays resident on the device. */
+glmb_status glmb_step_host(const glmb_step_params *prm, const float *Z_host,
+                           int32_t M, const int32_t *theta_host, float *Z_dev,
+                           int32_t *theta_dev, float *C_clutter_dev,
+                           float *C_tracks_dev, int64_t ldc, uint32_t *gate_dev,
+                           int64_t ldg, float *log_norm_dev,
+                           uint32_t *flags_dev, float *C_clutter_host,
+                           float *C_tracks_host, uint32_t *gate_host,
+                           float *log_norm_host, uint32_t *flags_host,
+                           glmb_stream_t stream);
+
+/* ---------------------------------------------------------------------
+ * Test hooks (not on the hot path; same device code as predict/birth).
+ * glmb_philox_dump: out[n] = Philox4x32-10(key(seed), ctr[n]) for n < N.
+ * glmb_normals_dump: out[n] = the four Box-Muller normals of that block
+ * (words (0,1) -> out[n][0..1], words (2,3) -> out[n][2..3]).
+ * ctr, out: [N][4] device arrays.
+ * --------------------------------------------------------------------- */
+glmb_status glmb_philox_dump(uint64_t seed, const uint32_t *ctr, int32_t N,
+                             uint32_t *out, glmb_stream_t stream);
+glmb_status glmb_normals_dump(uint64_t seed, const uint32_t *ctr, int32_t N,
+                              float *out, glmb_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GLMB_H_ */

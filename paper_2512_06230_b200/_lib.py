@@ -1,0 +1,221 @@
+"""Thin ctypes binding of libglmb.so (include/glmb.h).  Argument marshalling only.
+
+Every function here has the name of the C entry point it calls and takes
+torch CUDA tensors (device memory allocated by torch) plus an optional
+``torch.cuda.Stream``.  No arithmetic of the method happens in Python, and
+there is no CPU fallback: if the library is missing or the device is not
+sm_100a, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libglmb.so")
+
+GLMB_OK = 0
+_lock = threading.Lock()
+_lib = None
+
+
+class GlmbError(RuntimeError):
+    def __init__(self, status: int, text: str):
+        super().__init__(f"{text} (status {status})")
+        self.status = status
+
+
+class glmb_particles(C.Structure):
+    _fields_ = [("x", C.c_void_p), ("y", C.c_void_p), ("v", C.c_void_p), ("psi", C.c_void_p),
+                ("omega", C.c_void_p), ("w", C.c_void_p), ("n_tracks", C.c_int32),
+                ("n_particles", C.c_int32), ("ld", C.c_int64)]
+
+
+class glmb_step_params(C.Structure):
+    _fields_ = [("tracks", glmb_particles), ("n_survivors", C.c_int32), ("gid", C.c_void_p),
+                ("birth_mean", C.c_void_p), ("birth_chol", C.c_void_p), ("dt", C.c_float),
+                ("sigma_a", C.c_float), ("sigma_w", C.c_float), ("seed", C.c_uint64),
+                ("step", C.c_uint32), ("Rxx", C.c_float), ("Rxy", C.c_float), ("Ryy", C.c_float),
+                ("p_d", C.c_float), ("kappa", C.c_float), ("gamma", C.c_float),
+                ("col_offset", C.c_int32)]
+
+
+EXPORTED = ["glmb_version", "glmb_status_string", "glmb_init", "glmb_sm_count", "glmb_predict",
+            "glmb_birth", "glmb_compat", "glmb_reweight", "glmb_step", "glmb_step_host",
+            "glmb_philox_dump", "glmb_normals_dump"]
+
+
+def load(path: str = LIB_PATH):
+    """dlopen libglmb.so and declare every signature.  Raises if it is missing."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise GlmbError(-100, f"libglmb.so not built at {path}: run "
+                                  f"`python -m paper_2512_06230_b200.build` (no CPU fallback exists)")
+        L = C.CDLL(path)
+        vp, i32, i64, u32, u64, f32 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32, C.c_uint64, C.c_float
+        PP = C.POINTER(glmb_particles)
+        L.glmb_version.restype = C.c_int
+        L.glmb_status_string.restype = C.c_char_p
+        L.glmb_status_string.argtypes = [C.c_int]
+        L.glmb_init.argtypes = [C.c_int]
+        L.glmb_sm_count.argtypes = [C.c_int]
+        L.glmb_predict.argtypes = [PP, PP, vp, f32, f32, f32, u64, u32, vp]
+        L.glmb_birth.argtypes = [PP, vp, vp, vp, u64, u32, vp]
+        L.glmb_compat.argtypes = [PP, vp, i32, f32, f32, f32, f32, f32, f32, vp, vp, i64, vp, i64, vp]
+        L.glmb_reweight.argtypes = [PP, vp, i32, f32, f32, f32, vp, i32, vp, vp, vp]
+        SP = C.POINTER(glmb_step_params)
+        L.glmb_step.argtypes = [SP, vp, i32, vp, vp, vp, i64, vp, i64, vp, vp, vp]
+        L.glmb_step_host.argtypes = [SP, vp, i32, vp, vp, vp, vp, vp, i64, vp, i64, vp, vp,
+                                     vp, vp, vp, vp, vp, vp]
+        L.glmb_philox_dump.argtypes = [u64, vp, i32, vp, vp]
+        L.glmb_normals_dump.argtypes = [u64, vp, i32, vp, vp]
+        for name in EXPORTED:
+            if name not in ("glmb_version", "glmb_status_string", "glmb_sm_count"):
+                getattr(L, name).restype = C.c_int
+        _lib = L
+        return L
+
+
+def _check(status: int) -> None:
+    if status != GLMB_OK:
+        raise GlmbError(status, load().glmb_status_string(status).decode())
+
+
+def _ptr(t) -> int:
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise GlmbError(-1, "expected a CUDA tensor (the GLMB path has no CPU fallback)")
+    if not t.is_contiguous():
+        raise GlmbError(-1, "expected a contiguous tensor")
+    return t.data_ptr()
+
+
+def _stream(stream):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+class Particles:
+    """SoA particle storage: one tensor [6, T, ld] fp32 (x, y, v, psi, omega, w)."""
+
+    FIELDS = ("x", "y", "v", "psi", "omega", "w")
+
+    def __init__(self, data: torch.Tensor, n_particles: int):
+        assert data.dim() == 3 and data.shape[0] == 6 and data.dtype == torch.float32
+        self.data = data
+        self.T = data.shape[1]
+        self.ld = data.shape[2]
+        self.P = n_particles
+
+    @classmethod
+    def empty(cls, T: int, P: int, device="cuda", ld: int | None = None):
+        ld = P if ld is None else ld
+        return cls(torch.empty(6, T, ld, dtype=torch.float32, device=device), P)
+
+    @classmethod
+    def from_arrays(cls, arrays, device="cuda"):
+        """arrays: six [T, P] array-likes (x, y, v, psi, omega, w)."""
+        t = torch.stack([torch.as_tensor(a, dtype=torch.float32) for a in arrays]).contiguous()
+        return cls(t.to(device), t.shape[2])
+
+    def rows(self, start: int, stop: int) -> "Particles":
+        return Particles(self.data[:, start:stop], self.P)
+
+    def field(self, name: str) -> torch.Tensor:
+        return self.data[self.FIELDS.index(name)]
+
+    def struct(self) -> glmb_particles:
+        d = self.data
+        T = d.shape[1]
+        if T == 0:
+            return glmb_particles(None, None, None, None, None, None, 0, self.P, self.ld)
+        if d.stride(2) != 1 or d.stride(1) != self.ld:
+            raise GlmbError(-1, "particle storage must be [6][T][ld] with unit stride")
+        ptrs = [d[k].data_ptr() for k in range(6)]
+        if not d.is_cuda:
+            raise GlmbError(-1, "particles must live in CUDA memory")
+        return glmb_particles(*ptrs, T, self.P, self.ld)
+
+
+# --------------------------------------------------------------- entry points
+def glmb_version() -> int:
+    return load().glmb_version()
+
+
+def glmb_init(device: int = 0) -> None:
+    _check(load().glmb_init(device))
+
+
+def glmb_sm_count(device: int = 0) -> int:
+    return load().glmb_sm_count(device)
+
+
+def glmb_predict(inp: Particles, out: Particles, gid, dt, sigma_a, sigma_w, seed, step, stream=None):
+    a, b = inp.struct(), out.struct()
+    _check(load().glmb_predict(C.byref(a), C.byref(b), _ptr(gid), dt, sigma_a, sigma_w,
+                               int(seed) & 0xFFFFFFFFFFFFFFFF, int(step), _stream(stream)))
+
+
+def glmb_birth(out: Particles, gid, mean, chol, seed, step, stream=None):
+    b = out.struct()
+    _check(load().glmb_birth(C.byref(b), _ptr(gid), _ptr(mean), _ptr(chol),
+                             int(seed) & 0xFFFFFFFFFFFFFFFF, int(step), _stream(stream)))
+
+
+def glmb_compat(trk: Particles, Z, R, p_d, kappa, gamma, C_clutter, C_tracks, gate, stream=None):
+    """Z [M,2] fp32; C_tracks [T, ldc] fp32; gate [T, ldg] int32 (u32 words); C_clutter [M] or None."""
+    t = trk.struct()
+    M = Z.shape[0]
+    _check(load().glmb_compat(C.byref(t), _ptr(Z), M, R[0], R[1], R[2], p_d, kappa, gamma,
+                              _ptr(C_clutter), _ptr(C_tracks), C_tracks.shape[1], _ptr(gate),
+                              gate.shape[1], _stream(stream)))
+
+
+def glmb_reweight(trk: Particles, Z, R, theta, col_offset, log_norm, flags, stream=None):
+    t = trk.struct()
+    _check(load().glmb_reweight(C.byref(t), _ptr(Z), Z.shape[0], R[0], R[1], R[2], _ptr(theta),
+                                int(col_offset), _ptr(log_norm), _ptr(flags), _stream(stream)))
+
+
+def make_step_params(tracks: Particles, n_survivors, gid, birth_mean, birth_chol, dt, sigma_a,
+                     sigma_w, seed, step, R, p_d, kappa, gamma, col_offset=0) -> glmb_step_params:
+    return glmb_step_params(tracks.struct(), int(n_survivors), _ptr(gid), _ptr(birth_mean),
+                            _ptr(birth_chol), dt, sigma_a, sigma_w, int(seed) & 0xFFFFFFFFFFFFFFFF,
+                            int(step), R[0], R[1], R[2], p_d, kappa, gamma, int(col_offset))
+
+
+def glmb_step(prm: glmb_step_params, Z, theta, C_clutter, C_tracks, gate, log_norm, flags,
+              stream=None):
+    _check(load().glmb_step(C.byref(prm), _ptr(Z), Z.shape[0], _ptr(theta), _ptr(C_clutter),
+                            _ptr(C_tracks), C_tracks.shape[1], _ptr(gate), gate.shape[1],
+                            _ptr(log_norm), _ptr(flags), _stream(stream)))
+
+
+def glmb_step_host(prm: glmb_step_params, Z_host, theta_host, Z_dev, theta_dev, C_clutter,
+                   C_tracks, gate, log_norm, flags, C_clutter_host, C_tracks_host, gate_host,
+                   log_norm_host, flags_host, stream=None):
+    """Host tensors (pinned recommended) in and out; synchronous."""
+    hp = lambda t: None if t is None else t.data_ptr()
+    M = Z_host.shape[0]
+    _check(load().glmb_step_host(C.byref(prm), hp(Z_host), M, hp(theta_host), _ptr(Z_dev),
+                                 _ptr(theta_dev), _ptr(C_clutter), _ptr(C_tracks), C_tracks.shape[1],
+                                 _ptr(gate), gate.shape[1], _ptr(log_norm), _ptr(flags),
+                                 hp(C_clutter_host), hp(C_tracks_host), hp(gate_host),
+                                 hp(log_norm_host), hp(flags_host), _stream(stream)))
+
+
+def glmb_philox_dump(seed, ctr, out, stream=None):
+    _check(load().glmb_philox_dump(int(seed) & 0xFFFFFFFFFFFFFFFF, _ptr(ctr), ctr.shape[0],
+                                   _ptr(out), _stream(stream)))
+
+
+def glmb_normals_dump(seed, ctr, out, stream=None):
+    _check(load().glmb_normals_dump(int(seed) & 0xFFFFFFFFFFFFFFFF, _ptr(ctr), ctr.shape[0],
+                                    _ptr(out), _stream(stream)))

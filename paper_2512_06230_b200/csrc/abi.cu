@@ -1,0 +1,298 @@
+// abi.cu -- the extern "C" boundary of libglmb.so (declared in include/glmb.h).
+//
+// Validation, device selection from the caller's stream, launch planning.
+// Every entry point is asynchronous on the caller's stream (glmb_step_host
+// excepted), never allocates, never aborts.
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+
+#include "../../include/glmb.h"
+#include "glmb_internal.h"
+
+namespace {
+
+constexpr int kMaxDevices = 64;
+int g_sm_count[kMaxDevices] = {0};
+int g_checked[kMaxDevices] = {0};  // 0 unknown, 1 ok, -1 unsupported
+
+glmb_status check_device(int dev) {
+  if (dev < 0 || dev >= kMaxDevices) return GLMB_ERR_UNSUPPORTED_DEVICE;
+  if (g_checked[dev] == 0) {
+    int major = 0, minor = 0, sms = 0;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+      cudaGetLastError();
+      return GLMB_ERR_CUDA;
+    }
+    g_sm_count[dev] = sms;
+    g_checked[dev] = (major == 10 && minor == 0) ? 1 : -1;
+  }
+  return g_checked[dev] == 1 ? GLMB_OK : GLMB_ERR_UNSUPPORTED_DEVICE;
+}
+
+// Make the stream's device current in this library's runtime instance.
+glmb_status bind_stream(cudaStream_t s, int *dev_out) {
+  int dev = 0;
+  if (s != nullptr) {
+    if (cudaStreamGetDevice(s, &dev) != cudaSuccess) {
+      cudaGetLastError();
+      return GLMB_ERR_CUDA;
+    }
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess || cur != dev) {
+      if (cudaSetDevice(dev) != cudaSuccess) {
+        cudaGetLastError();
+        return GLMB_ERR_CUDA;
+      }
+    }
+  } else if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return GLMB_ERR_CUDA;
+  }
+  if (dev_out) *dev_out = dev;
+  return check_device(dev);
+}
+
+inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+glmb_status check_particles(const glmb_particles *p, bool need_w, bool need_vpo) {
+  if (p == nullptr) return GLMB_ERR_INVALID_ARG;
+  if (p->n_tracks < 0) return GLMB_ERR_INVALID_ARG;
+  if (p->n_tracks == 0) return GLMB_OK;
+  if (p->n_particles < 4 || p->ld < p->n_particles) return GLMB_ERR_INVALID_ARG;
+  if ((p->n_particles & 3) || (p->ld & 3)) return GLMB_ERR_ALIGNMENT;
+  if (static_cast<int64_t>(p->n_tracks) * p->ld > (int64_t(1) << 40)) return GLMB_ERR_INVALID_ARG;
+  const float *arr[6] = {p->x, p->y, p->v, p->psi, p->omega, p->w};
+  const bool need[6] = {true, true, need_vpo, need_vpo, need_vpo, need_w};
+  for (int k = 0; k < 6; ++k) {
+    if (!need[k]) continue;
+    if (arr[k] == nullptr) return GLMB_ERR_INVALID_ARG;
+    if (!aligned16(arr[k])) return GLMB_ERR_ALIGNMENT;
+  }
+  return GLMB_OK;
+}
+
+bool spd(float Rxx, float Rxy, float Ryy) {
+  const double det = static_cast<double>(Rxx) * Ryy - static_cast<double>(Rxy) * Rxy;
+  return std::isfinite(det) && Rxx > 0.f && det > 0.0;
+}
+
+inline glmb_status from_cuda(cudaError_t e) { return e == cudaSuccess ? GLMB_OK : GLMB_ERR_CUDA; }
+
+#define GLMB_TRY(expr)                    \
+  do {                                    \
+    const glmb_status st_ = (expr);       \
+    if (st_ != GLMB_OK) return st_;       \
+  } while (0)
+
+}  // namespace
+
+extern "C" {
+
+int glmb_version(void) { return 10000; }
+
+const char *glmb_status_string(glmb_status s) {
+  switch (s) {
+    case GLMB_OK: return "GLMB_OK";
+    case GLMB_ERR_INVALID_ARG: return "GLMB_ERR_INVALID_ARG: argument violates the contract in glmb.h";
+    case GLMB_ERR_ALIGNMENT: return "GLMB_ERR_ALIGNMENT: array not 16-B aligned or P/ld not a multiple of 4";
+    case GLMB_ERR_UNSUPPORTED_DEVICE: return "GLMB_ERR_UNSUPPORTED_DEVICE: needs compute capability 10.0 (sm_100a)";
+    case GLMB_ERR_CUDA: return "GLMB_ERR_CUDA: a CUDA call or kernel launch failed";
+  }
+  return "GLMB: unknown status";
+}
+
+glmb_status glmb_init(int device) {
+  if (cudaSetDevice(device) != cudaSuccess) {
+    cudaGetLastError();
+    return GLMB_ERR_CUDA;
+  }
+  return check_device(device);
+}
+
+int glmb_sm_count(int device) {
+  if (check_device(device) != GLMB_OK) return 0;
+  return g_sm_count[device];
+}
+
+glmb_status glmb_predict(const glmb_particles *in, const glmb_particles *out, const int32_t *gid, float dt,
+                         float sigma_a, float sigma_w, uint64_t seed, uint32_t step, glmb_stream_t stream) {
+  GLMB_TRY(check_particles(in, false, true));
+  GLMB_TRY(check_particles(out, false, true));
+  if (in->n_tracks != out->n_tracks) return GLMB_ERR_INVALID_ARG;
+  if (in->n_tracks > 0 && (in->n_particles != out->n_particles || in->ld != out->ld)) return GLMB_ERR_INVALID_ARG;
+  if (!(dt > 0.f) || !(sigma_a >= 0.f) || !(sigma_w >= 0.f)) return GLMB_ERR_INVALID_ARG;
+  if (in->n_tracks == 0) return GLMB_OK;
+  if (gid == nullptr) return GLMB_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int dev = 0;
+  GLMB_TRY(bind_stream(s, &dev));
+  glmb::PredictArgs a{in->x, in->y, in->v, in->psi, in->omega, out->x, out->y, out->v, out->psi, out->omega,
+                      gid, in->n_tracks, in->n_particles, in->ld, dt, sigma_a, sigma_w,
+                      static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32), step};
+  return from_cuda(glmb::launch_predict(a, g_sm_count[dev], s));
+}
+
+glmb_status glmb_birth(const glmb_particles *out, const int32_t *gid, const float *mean, const float *chol,
+                       uint64_t seed, uint32_t step, glmb_stream_t stream) {
+  GLMB_TRY(check_particles(out, true, true));
+  if (out->n_tracks == 0) return GLMB_OK;
+  if (gid == nullptr || mean == nullptr || chol == nullptr) return GLMB_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int dev = 0;
+  GLMB_TRY(bind_stream(s, &dev));
+  glmb::BirthArgs a{out->x, out->y, out->v, out->psi, out->omega, out->w, gid, mean, chol,
+                    out->n_tracks, out->n_particles, out->ld,
+                    static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32), step};
+  return from_cuda(glmb::launch_birth(a, g_sm_count[dev], s));
+}
+
+glmb_status glmb_compat(const glmb_particles *trk, const float *Z, int32_t M, float Rxx, float Rxy, float Ryy,
+                        float p_d, float kappa, float gamma, float *C_clutter, float *C_tracks, int64_t ldc,
+                        uint32_t *gate, int64_t ldg, glmb_stream_t stream) {
+  GLMB_TRY(check_particles(trk, true, false));
+  if (M < 0) return GLMB_ERR_INVALID_ARG;
+  if (!spd(Rxx, Rxy, Ryy) || !(p_d > 0.f && p_d <= 1.f) || !(kappa >= 0.f) || !(gamma >= 1e-30f))
+    return GLMB_ERR_INVALID_ARG;
+  if (M == 0) return GLMB_OK;
+  if (Z == nullptr) return GLMB_ERR_INVALID_ARG;
+  if ((reinterpret_cast<uintptr_t>(Z) & 7u) != 0) return GLMB_ERR_ALIGNMENT;
+  const int32_t T = trk->n_tracks;
+  if (T > 0) {
+    if (C_tracks == nullptr || gate == nullptr) return GLMB_ERR_INVALID_ARG;
+    if (ldc < M || ldg < (M + 31) / 32) return GLMB_ERR_INVALID_ARG;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  GLMB_TRY(bind_stream(s, nullptr));
+  if (T == 0) return from_cuda(glmb::launch_clutter_fill(C_clutter, M, kappa, s));
+
+  // whitening: 1/2 log2(e) d^T R^-1 d = (a1 dx + a2 dy)^2 + (b2 dy)^2
+  const double rxx = Rxx, rxy = Rxy, ryy = Ryy;
+  const double det = rxx * ryy - rxy * rxy;
+  const double s0 = std::sqrt(0.5 * 1.4426950408889634074);  // sqrt(1/2 log2 e)
+  const double a1 = s0 * std::sqrt(ryy / det);
+  const double a2 = -a1 * (rxy / ryy);
+  const double b2 = s0 / std::sqrt(ryy);
+  glmb::CompatArgs a{};
+  a.x = trk->x; a.y = trk->y; a.w = trk->w; a.ld = trk->ld; a.T = T; a.P = trk->n_particles;
+  a.Z = Z; a.M = M;
+  a.a1 = static_cast<float>(a1); a.a2 = static_cast<float>(a2); a.b2 = static_cast<float>(b2);
+  a.norm = static_cast<float>(1.0 / (2.0 * 3.14159265358979323846 * std::sqrt(det)));
+  a.p_d = p_d; a.kappa = kappa; a.gamma = gamma;
+  a.C_clutter = C_clutter; a.C_tracks = C_tracks; a.ldc = ldc; a.gate = gate; a.ldg = ldg;
+  glmb::compat_plan(M, a.P, &a.K, &a.n_mtiles);
+  if (static_cast<int64_t>(T) * a.n_mtiles > 0x7fffffffLL) return GLMB_ERR_INVALID_ARG;
+  return from_cuda(glmb::launch_compat(a, s));
+}
+
+glmb_status glmb_reweight(const glmb_particles *trk, const float *Z, int32_t M, float Rxx, float Rxy, float Ryy,
+                          const int32_t *theta, int32_t col_offset, float *log_norm, uint32_t *flags,
+                          glmb_stream_t stream) {
+  GLMB_TRY(check_particles(trk, true, false));
+  if (M < 0 || !spd(Rxx, Rxy, Ryy)) return GLMB_ERR_INVALID_ARG;
+  const int32_t T = trk->n_tracks;
+  if (T == 0) return GLMB_OK;
+  if (log_norm == nullptr || flags == nullptr) return GLMB_ERR_INVALID_ARG;
+  if (M > 0 && (Z == nullptr || theta == nullptr)) return GLMB_ERR_INVALID_ARG;
+  if (M > 0 && (reinterpret_cast<uintptr_t>(Z) & 7u) != 0) return GLMB_ERR_ALIGNMENT;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  GLMB_TRY(bind_stream(s, nullptr));
+  const double rxx = Rxx, rxy = Rxy, ryy = Ryy;
+  const double det = rxx * ryy - rxy * rxy;
+  const double h = 0.5 * 1.4426950408889634074;  // 1/2 log2(e)
+  glmb::ReweightArgs a{};
+  a.x = trk->x; a.y = trk->y; a.w = trk->w; a.ld = trk->ld; a.T = T; a.P = trk->n_particles;
+  a.Z = Z; a.M = M; a.theta = theta; a.col_offset = col_offset;
+  a.qa = h * ryy / det;
+  a.qb = -2.0 * h * rxy / det;
+  a.qc = h * rxx / det;
+  a.log_norm1 = std::log(2.0 * 3.14159265358979323846 * std::sqrt(det));
+  a.log_norm = log_norm; a.flags = flags;
+  return from_cuda(glmb::launch_reweight(a, s));
+}
+
+glmb_status glmb_step(const glmb_step_params *prm, const float *Z, int32_t M, const int32_t *theta,
+                      float *C_clutter, float *C_tracks, int64_t ldc, uint32_t *gate, int64_t ldg, float *log_norm,
+                      uint32_t *flags, glmb_stream_t stream) {
+  if (prm == nullptr) return GLMB_ERR_INVALID_ARG;
+  const glmb_particles &all = prm->tracks;
+  GLMB_TRY(check_particles(&all, true, true));
+  const int32_t T = prm->n_survivors, Tk = all.n_tracks;
+  if (T < 0 || T > Tk) return GLMB_ERR_INVALID_ARG;
+  glmb_particles surv = all;
+  surv.n_tracks = T;
+  glmb_particles births = all;
+  births.n_tracks = Tk - T;
+  const int64_t off = static_cast<int64_t>(T) * all.ld;
+  if (Tk > 0) {
+    births.x = all.x + off; births.y = all.y + off; births.v = all.v + off;
+    births.psi = all.psi + off; births.omega = all.omega + off; births.w = all.w + off;
+  }
+  GLMB_TRY(glmb_predict(&surv, &surv, prm->gid, prm->dt, prm->sigma_a, prm->sigma_w, prm->seed, prm->step, stream));
+  GLMB_TRY(glmb_birth(&births, prm->gid ? prm->gid + T : nullptr, prm->birth_mean, prm->birth_chol, prm->seed,
+                      prm->step, stream));
+  GLMB_TRY(glmb_compat(&all, Z, M, prm->Rxx, prm->Rxy, prm->Ryy, prm->p_d, prm->kappa, prm->gamma, C_clutter,
+                       C_tracks, ldc, gate, ldg, stream));
+  return glmb_reweight(&all, Z, M, prm->Rxx, prm->Rxy, prm->Ryy, theta, prm->col_offset, log_norm, flags,
+                       stream);
+}
+
+glmb_status glmb_step_host(const glmb_step_params *prm, const float *Z_host, int32_t M, const int32_t *theta_host,
+                           float *Z_dev, int32_t *theta_dev, float *C_clutter_dev, float *C_tracks_dev, int64_t ldc,
+                           uint32_t *gate_dev, int64_t ldg, float *log_norm_dev, uint32_t *flags_dev,
+                           float *C_clutter_host, float *C_tracks_host, uint32_t *gate_host, float *log_norm_host,
+                           uint32_t *flags_host, glmb_stream_t stream) {
+  if (prm == nullptr || M < 0) return GLMB_ERR_INVALID_ARG;
+  if (M > 0 && (Z_host == nullptr || theta_host == nullptr || Z_dev == nullptr || theta_dev == nullptr))
+    return GLMB_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  GLMB_TRY(bind_stream(s, nullptr));
+  const int64_t Tk = prm->tracks.n_tracks;
+  if (M > 0) {
+    if (cudaMemcpyAsync(Z_dev, Z_host, sizeof(float) * 2 * M, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(theta_dev, theta_host, sizeof(int32_t) * M, cudaMemcpyHostToDevice, s) != cudaSuccess)
+      return GLMB_ERR_CUDA;
+  }
+  GLMB_TRY(glmb_step(prm, Z_dev, M, theta_dev, C_clutter_dev, C_tracks_dev, ldc, gate_dev, ldg, log_norm_dev,
+                     flags_dev, stream));
+  if (M > 0 && C_clutter_host && C_clutter_dev &&
+      cudaMemcpyAsync(C_clutter_host, C_clutter_dev, sizeof(float) * M, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return GLMB_ERR_CUDA;
+  if (Tk > 0 && M > 0) {
+    if (C_tracks_host && cudaMemcpyAsync(C_tracks_host, C_tracks_dev, sizeof(float) * Tk * ldc,
+                                         cudaMemcpyDeviceToHost, s) != cudaSuccess)
+      return GLMB_ERR_CUDA;
+    if (gate_host && cudaMemcpyAsync(gate_host, gate_dev, sizeof(uint32_t) * Tk * ldg, cudaMemcpyDeviceToHost, s) !=
+                         cudaSuccess)
+      return GLMB_ERR_CUDA;
+  }
+  if (Tk > 0) {
+    if (log_norm_host && cudaMemcpyAsync(log_norm_host, log_norm_dev, sizeof(float) * Tk, cudaMemcpyDeviceToHost,
+                                         s) != cudaSuccess)
+      return GLMB_ERR_CUDA;
+    if (flags_host &&
+        cudaMemcpyAsync(flags_host, flags_dev, sizeof(uint32_t) * Tk, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+      return GLMB_ERR_CUDA;
+  }
+  return from_cuda(cudaStreamSynchronize(s));
+}
+
+glmb_status glmb_philox_dump(uint64_t seed, const uint32_t *ctr, int32_t N, uint32_t *out, glmb_stream_t stream) {
+  if (N < 0 || (N > 0 && (ctr == nullptr || out == nullptr))) return GLMB_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  GLMB_TRY(bind_stream(s, nullptr));
+  return from_cuda(glmb::launch_philox_dump(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32), ctr, N,
+                                            out, s));
+}
+
+glmb_status glmb_normals_dump(uint64_t seed, const uint32_t *ctr, int32_t N, float *out, glmb_stream_t stream) {
+  if (N < 0 || (N > 0 && (ctr == nullptr || out == nullptr))) return GLMB_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  GLMB_TRY(bind_stream(s, nullptr));
+  return from_cuda(glmb::launch_normals_dump(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32), ctr, N,
+                                             out, s));
+}
+
+}  // extern "C"

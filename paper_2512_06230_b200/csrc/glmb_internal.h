@@ -1,0 +1,74 @@
+// glmb_internal.h -- launcher interfaces between the C ABI (abi.cu) and the
+// kernel translation units.  Arguments are already validated by abi.cu.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace glmb {
+
+struct PredictArgs {
+  const float *x, *y, *v, *psi, *omega;
+  float *ox, *oy, *ov, *opsi, *oomega;
+  const int32_t *gid;
+  int32_t T, P;
+  int64_t ld;
+  float dt, sigma_a, sigma_w;
+  uint32_t key0, key1, step;
+};
+
+struct BirthArgs {
+  float *x, *y, *v, *psi, *omega, *w;
+  const int32_t *gid;
+  const float *mean, *chol;
+  int32_t B, P;
+  int64_t ld;
+  uint32_t key0, key1, step;
+};
+
+// Whitened, centred measurement geometry for compat:
+//   X' = a1 (x - cx) + a2 (y - cy),  Y' = b2 (y - cy)
+// so that  1/2 log2(e) d^T R^-1 d = |(dX', dY')|^2  and  L = norm * sum w 2^-|d'|^2.
+struct CompatArgs {
+  const float *x, *y, *w;
+  int64_t ld;
+  int32_t T, P;
+  const float *Z;
+  int32_t M;
+  float a1, a2, b2, norm;
+  float p_d, kappa, gamma;
+  float *C_clutter, *C_tracks;
+  int64_t ldc;
+  uint32_t *gate;
+  int64_t ldg;
+  int32_t n_mtiles;  // measurement tiles per track
+  int32_t K;         // measurements per thread (tile = 128*K)
+};
+
+struct ReweightArgs {
+  const float *x, *y;
+  float *w;
+  int64_t ld;
+  int32_t T, P;
+  const float *Z;
+  int32_t M;
+  const int32_t *theta;
+  int32_t col_offset;
+  double qa, qb, qc;   // q' = qa dx^2 + qb dx dy + qc dy^2 = 1/2 log2(e) d^T R^-1 d
+  double log_norm1;    // ln(2 pi sqrt(det R))
+  float *log_norm;
+  uint32_t *flags;
+};
+
+cudaError_t launch_predict(const PredictArgs &a, int sm_count, cudaStream_t s);
+cudaError_t launch_birth(const BirthArgs &a, int sm_count, cudaStream_t s);
+cudaError_t launch_philox_dump(uint32_t k0, uint32_t k1, const uint32_t *ctr, int32_t n, uint32_t *out,
+                               cudaStream_t s);
+cudaError_t launch_normals_dump(uint32_t k0, uint32_t k1, const uint32_t *ctr, int32_t n, float *out,
+                                cudaStream_t s);
+// chooses K / n_mtiles from (M, P) only (never from T: bit-identical sharding)
+void compat_plan(int32_t M, int32_t P, int32_t *K, int32_t *n_mtiles);
+cudaError_t launch_compat(const CompatArgs &a, cudaStream_t s);
+cudaError_t launch_clutter_fill(float *C_clutter, int32_t M, float kappa, cudaStream_t s);
+cudaError_t launch_reweight(const ReweightArgs &a, cudaStream_t s);
+
+}  // namespace glmb

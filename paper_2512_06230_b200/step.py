@@ -1,0 +1,142 @@
+"""Step driver: device-resident buffers for one (shard of a) scene and the
+four C-ABI calls of one GLMB step (predict -> birth -> compat -> reweight).
+
+A rank owns the contiguous block [lo, hi) of the T_k = T + B global columns
+(survivors first, then births -- P:24 "superposition of these surviving
+predicted and newborn tracks"); column c of C_k (c >= 1) is global track
+c - 1.  All arithmetic runs in libglmb.so; this module only allocates torch
+CUDA memory and passes pointers.
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .scenes import Scene
+
+
+def shard_range(n: int, rank: int, world: int) -> range:
+    """Contiguous, as-even-as-possible block of n items for rank."""
+    per = (n + world - 1) // world
+    lo = min(n, rank * per)
+    hi = min(n, lo + per)
+    return range(lo, hi)
+
+
+@dataclasses.dataclass
+class StepOutputs:
+    C_clutter: torch.Tensor
+    C_tracks: torch.Tensor   # [T_local, ldc]
+    gate: torch.Tensor       # [T_local, ldg] int32 words (u32 bit pattern)
+    log_norm: torch.Tensor   # [T_local]
+    flags: torch.Tensor      # [T_local] int32
+
+
+class GlmbStep:
+    """Buffers + launch sequence for one rank.
+
+    scene: generated with rows = this rank's survivor rows (global ids in scene.gid).
+    cols:  this rank's global column block [lo, hi) of the T_k columns.
+    """
+
+    def __init__(self, scene: Scene, cols: Optional[range] = None, device="cuda",
+                 seed: Optional[int] = None):
+        cfg = scene.cfg
+        self.scene = scene
+        self.cfg = cfg
+        self.device = torch.device(device)
+        Tk = cfg.T + cfg.B
+        self.cols = range(0, Tk) if cols is None else cols
+        lo, hi = self.cols.start, self.cols.stop
+        surv = range(lo, min(hi, cfg.T))
+        births = range(max(lo, cfg.T), hi)
+        if list(scene.gid) != list(surv):
+            raise ValueError("scene rows must equal this rank's survivor columns")
+        self.T_surv = len(surv)
+        self.B_local = len(births)
+        self.T_local = self.T_surv + self.B_local
+        P = cfg.P
+        self.P = P
+        dev = self.device
+        self.particles = L.Particles.empty(self.T_local, P, device=dev)
+        if self.T_surv:
+            init = np.stack([scene.x, scene.y, scene.v, scene.psi, scene.omega, scene.w])
+            self.particles.data[:, :self.T_surv].copy_(torch.from_numpy(init))
+        self.init_state = None
+        b_idx = [b - cfg.T for b in births]
+        gid = np.concatenate([np.asarray(scene.gid, np.int32),
+                              scene.birth_gid[b_idx].astype(np.int32)])
+        self.gid = torch.from_numpy(gid).to(dev)
+        self.birth_mean = torch.from_numpy(np.ascontiguousarray(scene.birth_mean[b_idx])).to(dev)
+        self.birth_chol = torch.from_numpy(np.ascontiguousarray(scene.birth_chol[b_idx])).to(dev)
+        # measurements of every step resident in HBM (inputs of the timed region)
+        self.M_max = max([len(z) for z in scene.Z] + [1])
+        self.ldc = ((self.M_max + 31) // 32) * 32
+        self.ldg = (self.M_max + 31) // 32
+        self.Z = [torch.from_numpy(z).to(dev) for z in scene.Z]
+        self.theta = [torch.from_numpy(t).to(dev) for t in scene.theta]
+        self.out = StepOutputs(
+            C_clutter=torch.zeros(self.M_max, dtype=torch.float32, device=dev),
+            C_tracks=torch.zeros(self.T_local, self.ldc, dtype=torch.float32, device=dev),
+            gate=torch.zeros(self.T_local, self.ldg, dtype=torch.int32, device=dev),
+            log_norm=torch.zeros(self.T_local, dtype=torch.float32, device=dev),
+            flags=torch.zeros(self.T_local, dtype=torch.int32, device=dev))
+        self.seed = cfg.seed if seed is None else seed
+        self.R = cfg.R
+
+    # ---- the four stages (each is one C-ABI call) ----
+    def survivors(self) -> L.Particles:
+        return self.particles.rows(0, self.T_surv)
+
+    def births(self) -> L.Particles:
+        return self.particles.rows(self.T_surv, self.T_local)
+
+    def predict(self, k: int, stream=None):
+        s = self.survivors()
+        L.glmb_predict(s, s, self.gid[:self.T_surv], self.cfg.dt, self.cfg.sigma_a,
+                       self.cfg.sigma_w, self.seed, k, stream)
+
+    def birth(self, k: int, stream=None):
+        if self.B_local:
+            L.glmb_birth(self.births(), self.gid[self.T_surv:], self.birth_mean, self.birth_chol,
+                         self.seed, k, stream)
+
+    def compat(self, k: int, stream=None, Z=None):
+        zi = k % len(self.Z)
+        o = self.out
+        L.glmb_compat(self.particles, self.Z[zi] if Z is None else Z, self.R, self.cfg.p_d, self.cfg.kappa,
+                      self.cfg.gamma, o.C_clutter, o.C_tracks, o.gate, stream)
+
+    def reweight(self, k: int, stream=None, Z=None, theta=None):
+        zi = k % len(self.Z)
+        o = self.out
+        L.glmb_reweight(self.particles, self.Z[zi] if Z is None else Z, self.R,
+                        self.theta[zi] if theta is None else theta, self.cols.start,
+                        o.log_norm, o.flags, stream)
+
+    def run(self, k: int, stream=None):
+        """One whole step through the fused glmb_step entry point."""
+        zi = k % len(self.Z)
+        o = self.out
+        prm = self.step_params(k)
+        L.glmb_step(prm, self.Z[zi], self.theta[zi], o.C_clutter, o.C_tracks, o.gate, o.log_norm,
+                    o.flags, stream)
+
+    def step_params(self, k: int) -> L.glmb_step_params:
+        c = self.cfg
+        return L.make_step_params(self.particles, self.T_surv, self.gid, self.birth_mean,
+                                  self.birth_chol, c.dt, c.sigma_a, c.sigma_w, self.seed, k,
+                                  self.R, c.p_d, c.kappa, c.gamma, self.cols.start)
+
+    def evals(self, k: int) -> int:
+        """Algorithmic particle-measurement likelihood evaluations of step k on this rank:
+        M_k * T_k * P (compat, dense) + P * #{i : theta_i in this rank's columns} (reweight)."""
+        zi = k % len(self.Z)
+        M = len(self.scene.Z[zi])
+        th = self.scene.theta[zi]
+        n_assigned = int(((th >= self.cols.start + 1) & (th <= self.cols.stop)).sum())
+        return M * self.T_local * self.P + self.P * n_assigned

@@ -1,0 +1,392 @@
+"""GPU parity: every stage of the CUDA path (through the C ABI) vs the fp64 oracle
+on identical seeded fp32 inputs."""
+import numpy as np
+import pytest
+
+from conftest import gpu_available
+from _parity import (check_compat, check_log_norm, check_state, check_weights)
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not gpu_available(), reason="needs a CUDA GPU")]
+
+
+@pytest.fixture(scope="module")
+def L():
+    import torch
+    from paper_2512_06230_b200 import _lib
+    from paper_2512_06230_b200.build import build
+    build()
+    _lib.glmb_init(0)
+    torch.cuda.set_device(0)
+    return _lib
+
+
+def _dev(a, dtype=None):
+    import torch
+    t = torch.as_tensor(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.cuda()
+
+
+def _host(t):
+    import torch
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+# ------------------------------------------------------------------ Philox
+def test_philox_bit_exact(L, orc):
+    import torch
+    r = np.random.default_rng(0)
+    n = 200_000
+    ctr = r.integers(0, 2**32, (n, 4), dtype=np.uint64).astype(np.uint32)
+    # every counter configs 0-1 use in predict / birth
+    p = np.arange(1024, dtype=np.uint32)
+    for gid, tag in [(0, 0), (3, 0), (63, 0), (64, 0x100), (67, 0x101)]:
+        blk = np.stack([p, np.full_like(p, gid), np.zeros_like(p), np.full_like(p, tag)], 1)
+        ctr = np.concatenate([ctr, blk])
+    ctr[:2] = [[0, 0, 0, 0], [0xFFFFFFFF] * 4]
+    for seed in (0, 7, 0xFFFFFFFFFFFFFFFF, 0x123456789ABCDEF0):
+        out = torch.empty(ctr.shape, dtype=torch.int32, device="cuda")
+        L.glmb_philox_dump(seed, _dev(ctr.view(np.int32)), out)
+        got = _host(out).view(np.uint32)
+        np.testing.assert_array_equal(got, orc.philox(seed, ctr))
+
+
+def test_box_muller_normals(L, orc):
+    import torch
+    n = 100_000
+    ctr = np.zeros((n, 4), np.uint32)
+    ctr[:, 0] = np.arange(n)
+    ctr[:, 1] = 5
+    out = torch.empty((n, 4), dtype=torch.float32, device="cuda")
+    L.glmb_normals_dump(11, _dev(ctr.view(np.int32)), out)
+    g = _host(out).astype(np.float64)
+    ref = orc.normals_batch(11, ctr)
+    assert np.abs(g - ref).max() < 1e-5
+
+
+# ------------------------------------------------------------------ predict / birth
+def _predict_gpu(L, arrs, gid, dt, sa, sw, seed, step):
+    from paper_2512_06230_b200._lib import Particles
+    T, P = arrs[0].shape
+    w = np.full((T, P), 1.0 / P, np.float32)
+    pin = Particles.from_arrays(list(arrs) + [w])
+    pout = Particles.empty(T, P)
+    L.glmb_predict(pin, pout, _dev(gid), dt, sa, sw, seed, step)
+    res = _host(pout.data)
+    # in place gives the same bits
+    L.glmb_predict(pin, pin, _dev(gid), dt, sa, sw, seed, step)
+    np.testing.assert_array_equal(_host(pin.data)[:5], res[:5])
+    return res
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2])
+def test_predict_parity_configs(L, orc, cfg):
+    from paper_2512_06230_b200.scenes import make_scene
+    s = make_scene(cfg, steps=1)
+    c = s.cfg
+    arrs = (s.x, s.y, s.v, s.psi, s.omega)
+    g = _predict_gpu(L, arrs, s.gid, c.dt, c.sigma_a, c.sigma_w, c.seed, 3)
+    ref = orc.predict(*arrs, s.gid, c.dt, c.sigma_a, c.sigma_w, c.seed, 3)
+    check_state(g[:5], ref)
+
+
+def test_predict_edge_kinematics(L, orc):
+    """omega at and around 0 and the oracle's 1e-4 branch, large dt, headings near +-pi."""
+    T, P = 2, 64
+    r = np.random.default_rng(1)
+    om = np.concatenate([np.array([0, 1e-7, -1e-7, 1e-5, -1e-5, 1e-4, -1e-4, 1.0001e-4, 3e-3, -0.5, 2.0, -4.0]),
+                         r.normal(0, 1, T * P - 12)]).reshape(T, P).astype(np.float32)
+    psi = r.uniform(-np.pi, np.pi, (T, P)).astype(np.float32)
+    psi[0, :6] = [np.pi, -np.pi, 3.1415925, -3.1415925, 0.0, 1.5707964]
+    arrs = (r.uniform(-3000, 3000, (T, P)).astype(np.float32), r.uniform(-3000, 3000, (T, P)).astype(np.float32),
+            r.uniform(0, 30, (T, P)).astype(np.float32), psi, om)
+    gid = np.array([0, 12345], np.int32)
+    for dt in (0.1, 1.0):
+        g = _predict_gpu(L, arrs, gid, dt, 2.0, 0.5, 99, 7)
+        ref = orc.predict(*arrs, gid, dt, 2.0, 0.5, 99, 7)
+        check_state(g[:5], ref)
+        assert np.all((g[3] > -np.float32(np.pi)) & (g[3] <= np.float32(np.pi)))
+
+
+def test_predict_noise_free_matches_flow(L, orc):
+    from paper_2512_06230_b200.scenes import random_cloud
+    x, y, v, psi, om, _ = random_cloud(3, 128, seed=4)
+    g = _predict_gpu(L, (x, y, v, psi, om), np.arange(3, dtype=np.int32), 0.1, 0.0, 0.0, 1, 0)
+    ref = orc.predict(x, y, v, psi, om, np.arange(3, dtype=np.int32), 0.1, 0.0, 0.0, 1, 0)
+    check_state(g[:5], ref)
+    np.testing.assert_array_equal(g[2], v)          # speed untouched without noise
+    np.testing.assert_array_equal(g[4], om)
+
+
+@pytest.mark.parametrize("cfg", [1, 3])
+def test_birth_parity(L, orc, cfg):
+    from paper_2512_06230_b200._lib import Particles
+    from paper_2512_06230_b200.scenes import make_scene
+    s = make_scene(cfg, rows=range(0), steps=1)
+    B, P = s.birth_mean.shape[0], s.cfg.P
+    out = Particles.empty(B, P)
+    L.glmb_birth(out, _dev(s.birth_gid), _dev(s.birth_mean), _dev(s.birth_chol), s.cfg.seed, 2)
+    g = _host(out.data)
+    ref = orc.birth(s.birth_mean, s.birth_chol, s.birth_gid, P, s.cfg.seed, 2)
+    check_state(g[:5], ref[:5])
+    np.testing.assert_array_equal(g[5], np.float32(1.0 / P))
+
+
+def test_birth_full_covariance(L, orc):
+    from paper_2512_06230_b200._lib import Particles
+    mean = np.array([[10, 20, 5, 3.1, 0.1], [-5, 0, 1, -3.1, 0]], np.float32)
+    Lm = np.array([[2, 0, 0, 0, 0], [0.5, 1, 0, 0, 0], [0.1, 0.2, 0.3, 0, 0],
+                   [0.0, 0.1, 0.0, 0.8, 0], [0.05, 0, 0.02, 0.01, 0.2]])
+    chol = np.stack([Lm[np.tril_indices(5)]] * 2).astype(np.float32)
+    gid = np.array([100, 101], np.int32)
+    out = Particles.empty(2, 256)
+    L.glmb_birth(out, _dev(gid), _dev(mean), _dev(chol), 3, 9)
+    g = _host(out.data)
+    ref = orc.birth(mean, chol, gid, 256, 3, 9)
+    check_state(g[:5], ref[:5])
+
+
+# ------------------------------------------------------------------ compat
+def _compat_gpu(L, x, y, w, Z, R, p_d, kappa, gamma, ld=None, ldc=None, ldg=None):
+    import torch
+    from paper_2512_06230_b200._lib import Particles
+    T, P = x.shape
+    M = Z.shape[0]
+    ld = P if ld is None else ld
+    ldc = max(M, 1) if ldc is None else ldc
+    ldg = max((M + 31) // 32, 1) if ldg is None else ldg
+    data = np.zeros((6, T, ld), np.float32)
+    data[0, :, :P], data[1, :, :P], data[5, :, :P] = x, y, w
+    data[0, :, P:] = np.nan   # padding beyond P must never be read
+    trk = Particles(_dev(data), P)
+    C = torch.full((T, ldc), -7.0, dtype=torch.float32, device="cuda")
+    G = torch.full((T, ldg), -1, dtype=torch.int32, device="cuda")
+    Cc = torch.full((max(M, 1),), -7.0, dtype=torch.float32, device="cuda")
+    Zd = _dev(Z.reshape(-1, 2).astype(np.float32)) if M else torch.zeros((0, 2), device="cuda")
+    L.glmb_compat(trk, Zd, R, p_d, kappa, gamma, Cc, C, G)
+    return _host(C), _host(G).view(np.uint32), _host(Cc)
+
+
+@pytest.mark.parametrize("cfg", [0, 1])
+def test_compat_parity_configs(L, orc, cfg):
+    from paper_2512_06230_b200.scenes import make_scene
+    s = make_scene(cfg, steps=1)
+    c = s.cfg
+    Z = s.Z[0]
+    C, G, Cc = _compat_gpu(L, s.x, s.y, s.w, Z, c.R, c.p_d, c.kappa, c.gamma)
+    ref = orc.compat(s.x, s.y, s.w, Z, c.R, c.p_d, c.kappa, c.gamma)
+    nband, rel = check_compat(C, G, Cc, ref, c.gamma, len(Z))
+    assert rel < 1e-5 and nband <= max(1, 1e-3 * (ref["L"] >= c.gamma).sum())
+    assert (ref["L"] >= c.gamma).sum() > 0
+
+
+def test_compat_parity_cfg2_sampled(L, orc):
+    from paper_2512_06230_b200.scenes import make_scene
+    s = make_scene(2, rows=range(40, 72), steps=1)
+    c = s.cfg
+    C, G, Cc = _compat_gpu(L, s.x, s.y, s.w, s.Z[0], c.R, c.p_d, c.kappa, c.gamma)
+    ref = orc.compat(s.x, s.y, s.w, s.Z[0], c.R, c.p_d, c.kappa, c.gamma)
+    check_compat(C, G, Cc, ref, c.gamma, len(s.Z[0]))
+
+
+@pytest.mark.parametrize("T,P,M,ld", [(1, 4, 1, 4), (2, 260, 33, 264), (3, 1028, 129, 1028),
+                                      (2, 516, 1025, 520), (1, 512, 2049, 512), (5, 8, 7, 12)])
+def test_compat_ragged_shapes(L, orc, T, P, M, ld):
+    r = np.random.default_rng(T * 1000 + M)
+    cen = r.uniform(0, 50, (T, 2))
+    x = (cen[:, :1] + r.normal(0, 2, (T, P))).astype(np.float32)
+    y = (cen[:, 1:] + r.normal(0, 2, (T, P))).astype(np.float32)
+    w = r.dirichlet(np.ones(P), T).astype(np.float32)
+    Z = r.uniform(-5, 55, (M, 2)).astype(np.float32)
+    R = (1.3, 0.4, 0.9)
+    C, G, Cc = _compat_gpu(L, x, y, w, Z, R, 0.85, 3e-4, 1e-6, ld=ld, ldc=M + 5, ldg=(M + 31) // 32 + 2)
+    ref = orc.compat(x, y, w, Z, R, 0.85, 3e-4, 1e-6)
+    check_compat(C, G, Cc, ref, 1e-6, M)
+    assert np.all(C[:, M:] == -7.0)                      # entries past M untouched
+    assert np.all(G[:, (M + 31) // 32:] == 0xFFFFFFFF)   # words past ceil(M/32) untouched
+
+
+def test_compat_large_coordinates_general_R(L, orc):
+    """Tracks near 4 km (cfg4 scale) with a correlated R: whitening + centring keep 1e-4."""
+    r = np.random.default_rng(5)
+    T, P, M = 4, 1024, 300
+    cen = r.uniform(3500, 4000, (T, 2))
+    x = (cen[:, :1] + r.normal(0, 2, (T, P))).astype(np.float32)
+    y = (cen[:, 1:] + r.normal(0, 2, (T, P))).astype(np.float32)
+    w = np.full((T, P), 1.0 / P, np.float32)
+    Z = (cen[r.integers(0, T, M)] + r.normal(0, 4, (M, 2))).astype(np.float32)
+    R = (0.7, -0.3, 1.6)
+    C, G, Cc = _compat_gpu(L, x, y, w, Z, R, 0.9, 6.25e-5, 1e-8)
+    ref = orc.compat(x, y, w, Z, R, 0.9, 6.25e-5, 1e-8)
+    nb, rel = check_compat(C, G, Cc, ref, 1e-8, M)
+    assert (ref["L"] >= 1e-8).sum() > 50
+
+
+def test_compat_edge_cases(L, orc):
+    import torch
+    from paper_2512_06230_b200._lib import Particles
+    Z = np.array([[1, 2], [3, 4], [5, 6]], np.float32)
+    # T = 0: clutter-only matrix
+    trk = Particles.empty(0, 4)
+    Cc = torch.full((3,), -1.0, device="cuda")
+    L.glmb_compat(trk, _dev(Z), (1, 0, 1), 0.9, 5e-5, 1e-6, Cc, torch.empty((0, 3), device="cuda"),
+                  torch.empty((0, 1), dtype=torch.int32, device="cuda"))
+    np.testing.assert_array_equal(_host(Cc), np.float32(5e-5))
+    # M = 0: no-op
+    x = np.zeros((1, 4), np.float32)
+    C, G, _ = _compat_gpu(L, x, x, x + 0.25, np.zeros((0, 2), np.float32), (1, 0, 1), 0.9, 1e-3, 1e-6)
+    assert np.all(C == -7.0)
+    # all gated out
+    C, G, Cc = _compat_gpu(L, x + 500, x + 500, x + 0.25, Z, (1, 0, 1), 0.9, 1e-3, 1e-6)
+    assert np.all(C[:, :3] == 0) and np.all(G[:, 0] == 0)
+    # NaN particle -> L NaN -> g = 0, C = 0
+    xn = x.copy(); xn[0, 0] = np.nan
+    C, G, _ = _compat_gpu(L, xn, x, x + 0.25, np.zeros((1, 2), np.float32), (1, 0, 1), 0.9, 1e-3, 1e-6)
+    assert C[0, 0] == 0 and G[0, 0] == 0
+    # the gate radius closed form: single particle, R = I
+    g = 1e-6
+    d = np.sqrt(-2 * np.log(2 * np.pi * float(np.float32(g))))
+    Zg = np.array([[d - 1e-3, 0], [d + 1e-3, 0]], np.float32)
+    C, G, _ = _compat_gpu(L, x[:, :4] * 0, x[:, :4] * 0, np.array([[1, 0, 0, 0]], np.float32), Zg,
+                          (1, 0, 1), 0.9, 1e-3, g)
+    assert int(G[0, 0]) == 0b01
+
+
+def test_compat_invariances(L, orc):
+    """Row permutation of Z permutes C rows bit-exactly; splitting the tracks (sharding) is
+    bit-identical; particle permutation changes C by fp32 reduction order only."""
+    from paper_2512_06230_b200.scenes import make_scene
+    s = make_scene(1, steps=1)
+    c = s.cfg
+    Z = s.Z[0]
+    C, G, _ = _compat_gpu(L, s.x, s.y, s.w, Z, c.R, c.p_d, c.kappa, c.gamma)
+    perm = np.random.default_rng(0).permutation(len(Z))
+    C2, _, _ = _compat_gpu(L, s.x, s.y, s.w, Z[perm], c.R, c.p_d, c.kappa, c.gamma)
+    np.testing.assert_array_equal(C2[:, :len(Z)], C[:, perm])
+    for lo, hi in [(0, 17), (17, 40), (40, 64)]:
+        Cs, Gs, _ = _compat_gpu(L, s.x[lo:hi], s.y[lo:hi], s.w[lo:hi], Z, c.R, c.p_d, c.kappa, c.gamma)
+        np.testing.assert_array_equal(Cs, C[lo:hi])
+        np.testing.assert_array_equal(Gs, G[lo:hi])
+    pp = np.random.default_rng(1).permutation(s.cfg.P)
+    pp = np.concatenate([[0], pp[pp != 0]])   # keep the centring particle first
+    C3, _, _ = _compat_gpu(L, s.x[:, pp], s.y[:, pp], s.w[:, pp], Z, c.R, c.p_d, c.kappa, c.gamma)
+    nz = C != 0
+    np.testing.assert_allclose(C3[nz], C[nz], rtol=1e-5)
+
+
+# ------------------------------------------------------------------ reweight
+def _reweight_gpu(L, x, y, w, Z, R, theta, col_offset=0):
+    import torch
+    from paper_2512_06230_b200._lib import Particles
+    T, P = x.shape
+    data = np.zeros((6, T, P), np.float32)
+    data[0], data[1], data[5] = x, y, w
+    trk = Particles(_dev(data), P)
+    ln = torch.zeros(T, device="cuda")
+    fl = torch.full((T,), -1, dtype=torch.int32, device="cuda")
+    Zd = _dev(Z.reshape(-1, 2).astype(np.float32))
+    L.glmb_reweight(trk, Zd, R, _dev(theta.astype(np.int32)), col_offset, ln, fl)
+    return _host(trk.data)[5], _host(ln), _host(fl)
+
+
+@pytest.mark.parametrize("cfg", [0, 1])
+def test_reweight_parity_configs(L, orc, cfg):
+    from paper_2512_06230_b200.scenes import make_scene
+    s = make_scene(cfg, steps=1)
+    c = s.cfg
+    w, ln, fl = _reweight_gpu(L, s.x, s.y, s.w, s.Z[0], c.R, s.theta[0])
+    rw, rln, rfl = orc.reweight(s.x, s.y, s.w, s.Z[0], c.R, s.theta[0])
+    check_weights(w, rw)
+    check_log_norm(ln, rln)
+    np.testing.assert_array_equal(fl.view(np.uint32), rfl)
+
+
+@pytest.mark.parametrize("P", [4, 1024, 4096, 8192, 12288])
+def test_reweight_paths_and_multi_detection(L, orc, P):
+    """Register-cached paths (P <= 8192) and the generic path (P > 8192); several
+    detections per track (P:46-48 multiple detections per object), a far-away
+    measurement, an empty track, theta values out of range and a column offset."""
+    r = np.random.default_rng(P)
+    T = 5
+    x = r.normal(100, 1.5, (T, P)).astype(np.float32)
+    y = r.normal(-40, 1.5, (T, P)).astype(np.float32)
+    w = r.dirichlet(np.ones(P), T).astype(np.float32)
+    Z = np.array([[100.5, -40], [99, -41], [101, -39.5], [130, -40], [100, -40.2], [0, 0]], np.float32)
+    # col_offset 10: local j -> column 11 + j
+    theta = np.array([11, 11, 11, 12, 14, 99], np.int32)
+    wg, ln, fl = _reweight_gpu(L, x, y, w, Z, (0.8, 0.1, 1.1), theta, col_offset=10)
+    rw, rln, rfl = orc.reweight(x, y, w, Z, (0.8, 0.1, 1.1), theta, col_offset=10)
+    check_weights(wg, rw)
+    check_log_norm(ln, rln)
+    np.testing.assert_array_equal(wg[2], w[2])     # column 13: no measurement -> untouched
+    np.testing.assert_array_equal(fl, 0)
+
+
+def test_reweight_degenerate_and_many_assigned(L, orc):
+    r = np.random.default_rng(3)
+    T, P, M = 2, 256, 1500          # > 1024 assigned measurements: generic S path
+    x = r.normal(0, 1, (T, P)).astype(np.float32)
+    y = r.normal(0, 1, (T, P)).astype(np.float32)
+    w = r.dirichlet(np.ones(P), T).astype(np.float32)
+    w[1] = 0.0                      # degenerate track: uniform reset + flag
+    Z = r.normal(0, 0.3, (M, 2)).astype(np.float32)
+    theta = np.where(np.arange(M) % 2 == 0, 1, 2).astype(np.int32)
+    wg, ln, fl = _reweight_gpu(L, x, y, w, Z, (50.0, 0, 50.0), theta)
+    rw, rln, rfl = orc.reweight(x, y, w, Z, (50.0, 0, 50.0), theta)
+    check_weights(wg, rw)
+    check_log_norm(ln, rln)
+    np.testing.assert_array_equal(fl.view(np.uint32), rfl)
+    assert rfl[1] == 1
+
+
+# ------------------------------------------------------------------ whole step
+def test_step_composition_and_host_entry(L):
+    """glmb_step == the four calls in sequence (bit-exact); glmb_step_host == glmb_step."""
+    import torch
+    from paper_2512_06230_b200.scenes import make_scene
+    from paper_2512_06230_b200.step import GlmbStep
+    s = make_scene(1, steps=1)
+    a = GlmbStep(s)
+    b = GlmbStep(s)
+    a.predict(0); a.birth(0); a.compat(0); a.reweight(0)
+    b.run(0)
+    torch.cuda.synchronize()
+    for f in ("C_tracks", "gate", "log_norm", "flags", "C_clutter"):
+        np.testing.assert_array_equal(getattr(a.out, f).cpu().numpy(), getattr(b.out, f).cpu().numpy())
+    np.testing.assert_array_equal(a.particles.data.cpu().numpy(), b.particles.data.cpu().numpy())
+    c = GlmbStep(s)
+    M = len(s.Z[0])
+    pin = lambda arr: torch.from_numpy(arr).pin_memory()
+    Zh, th = pin(s.Z[0]), pin(s.theta[0])
+    Cc_h = torch.empty(c.M_max).pin_memory()
+    Ct_h = torch.empty(c.T_local, c.ldc).pin_memory()
+    G_h = torch.empty(c.T_local, c.ldg, dtype=torch.int32).pin_memory()
+    ln_h = torch.empty(c.T_local).pin_memory()
+    fl_h = torch.empty(c.T_local, dtype=torch.int32).pin_memory()
+    o = c.out
+    L.glmb_step_host(c.step_params(0), Zh, th, torch.empty(M, 2, device="cuda"),
+                     torch.empty(M, dtype=torch.int32, device="cuda"), o.C_clutter, o.C_tracks,
+                     o.gate, o.log_norm, o.flags, Cc_h, Ct_h, G_h, ln_h, fl_h)
+    np.testing.assert_array_equal(Ct_h.numpy()[:, :M], b.out.C_tracks.cpu().numpy()[:, :M])
+    np.testing.assert_array_equal(G_h.numpy(), b.out.gate.cpu().numpy())
+    np.testing.assert_array_equal(ln_h.numpy(), b.out.log_norm.cpu().numpy())
+
+
+def test_status_errors(L):
+    import torch
+    from paper_2512_06230_b200._lib import GlmbError, Particles
+    trk = Particles.empty(2, 8)
+    Z = torch.zeros(3, 2, device="cuda")
+    C = torch.zeros(2, 3, device="cuda")
+    G = torch.zeros(2, 1, dtype=torch.int32, device="cuda")
+    with pytest.raises(GlmbError) as e:
+        L.glmb_compat(trk, Z, (1, 2, 1), 0.9, 1e-3, 1e-6, None, C, G)    # R not SPD
+    assert e.value.status == -1
+    with pytest.raises(GlmbError):
+        L.glmb_compat(trk, Z, (1, 0, 1), 0.9, 1e-3, 1e-31, None, C, G)   # gamma < 1e-30
+    with pytest.raises(GlmbError) as e:
+        L.glmb_compat(Particles(trk.data, 6), Z, (1, 0, 1), 0.9, 1e-3, 1e-6, None, C, G)
+    assert e.value.status == -2                                           # P % 4 != 0
