@@ -16,7 +16,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libglmb.so")
 SOURCES = ["abi.cu", "kernels_rng.cu", "compat.cu", "reweight.cu"]
-HEADERS = ["glmb_device.cuh", "glmb_internal.h"]
+HEADERS = ["glmb_device.cuh", "glmb_internal.h", "peaks.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
@@ -54,6 +54,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, LIB)
+    peaks = os.path.join(HERE, "glmb_peaks")
+    r = subprocess.run([NVCC] + ARCH + ["-O3", "-o", peaks, os.path.join(CSRC, "peaks.cu")],
+                       capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"peaks build failed:\n{r.stdout}\n{r.stderr}")
     return LIB
 
 

@@ -1,0 +1,106 @@
+// peaks.cu -- micro-benchmark of the issue pipes the GLMB kernels are bound by
+// (standalone executable, not part of libglmb.so).  Prints one JSON object:
+// MUFU.EX2, FFMA2 (packed fp32x2), FFMA throughput per SM per clock and the
+// SM count / clock seen, so every roofline in bench.py uses measured numbers.
+#include <cstdio>
+#include <cuda_runtime.h>
+
+constexpr int kChains = 8;
+
+__global__ void ex2_kernel(float *out, int iters, float seed, long long *cyc) {
+  float v[kChains];
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) v[c] = seed * (c + 1) * 1e-3f - 0.5f;
+  const long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(v[c]));
+  }
+  const long long t1 = clock64();
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) s += v[c];
+  if (s == 12345.f) out[0] = s;
+  if (threadIdx.x == 0 && blockIdx.x == 0) cyc[0] = t1 - t0;
+}
+
+__global__ void ffma2_kernel(float *out, int iters, float seed, long long *cyc) {
+  unsigned long long v[kChains], m, a;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(m) : "f"(0.999f));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(a) : "f"(seed * 1e-3f));
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) asm("mov.b64 %0, {%1, %2};" : "=l"(v[c]) : "f"(seed + c), "f"(seed - c));
+  const long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(v[c]) : "l"(m), "l"(a));
+  }
+  const long long t1 = clock64();
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v[c]));
+    s += lo + hi;
+  }
+  if (s == 12345.f) out[0] = s;
+  if (threadIdx.x == 0 && blockIdx.x == 0) cyc[0] = t1 - t0;
+}
+
+__global__ void ffma_kernel(float *out, int iters, float seed, long long *cyc) {
+  float v[kChains];
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) v[c] = seed + c;
+  const float m = 0.999f, a = seed * 1e-3f;
+  const long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(v[c]) : "f"(m), "f"(a));
+  }
+  const long long t1 = clock64();
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) s += v[c];
+  if (s == 12345.f) out[0] = s;
+  if (threadIdx.x == 0 && blockIdx.x == 0) cyc[0] = t1 - t0;
+}
+
+template <typename F>
+void run(const char *name, F kern, int sms, float *out, long long *cyc, bool last) {
+  const int threads = 256, blocks_per_sm = 8, iters = 4096;
+  const int blocks = sms * blocks_per_sm;
+  kern<<<blocks, threads>>>(out, 16, 1.0f, cyc);  // warm up
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  kern<<<blocks, threads>>>(out, iters, 1.0f, cyc);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  long long c = 0;
+  cudaMemcpy(&c, cyc, sizeof(c), cudaMemcpyDeviceToHost);
+  const double ops = double(blocks) * threads * iters * kChains;  // thread-level instructions
+  const double per_sm_per_clk = ops / sms / double(c) * ((double)blocks_per_sm / blocks_per_sm);
+  // one block's clock64 span ~ the whole kernel when all blocks are co-resident
+  printf("  \"%s\": {\"ops_per_s\": %.6e, \"ms\": %.4f, \"block_cycles\": %lld, \"lanes_per_clk_per_sm\": %.3f}%s\n",
+         name, ops / (ms * 1e-3), ms, c, per_sm_per_clk, last ? "" : ",");
+}
+
+int main() {
+  int dev = 0, sms = 0, clk_khz = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev);
+  float *out;
+  long long *cyc;
+  cudaMalloc(&out, 16);
+  cudaMalloc(&cyc, 16);
+  printf("{\n  \"sm_count\": %d,\n  \"attr_clock_mhz\": %.1f,\n", sms, clk_khz / 1e3);
+  run("mufu_ex2", ex2_kernel, sms, out, cyc, false);
+  run("ffma2_f32x2", ffma2_kernel, sms, out, cyc, false);
+  run("ffma", ffma_kernel, sms, out, cyc, true);
+  printf("}\n");
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}

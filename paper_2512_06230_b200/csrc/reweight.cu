@@ -25,7 +25,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kSCap = 1024;  // assigned measurements held in shared memory
+constexpr int kSCap = 256;   // assigned measurements held in shared memory (more: global rescan)
 
 struct SList {
   double2 z[kSCap];
@@ -33,28 +33,41 @@ struct SList {
   int in_smem;     // 1 if all of S_j fits in z[]
 };
 
-// Collect S_j in ascending i with warp 0 (ballot + popc prefix).
-__device__ void collect_S(const ReweightArgs &a, int col, SList &S) {
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    int n = 0;
-    for (int base = 0; base < a.M; base += 32) {
+// Collect S_j in ascending i: each warp scans a contiguous chunk of theta
+// (ballot + popc), then the per-warp counts are prefix-summed so the list keeps
+// the ascending order of i (deterministic fp64 accumulation order).
+__device__ void collect_S(const ReweightArgs &a, int col, SList &S, int *warp_cnt) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int chunk = ((a.M + kWarps - 1) / kWarps + 31) & ~31;
+  const int lo = warp * chunk, hi = min(a.M, lo + chunk);
+  int n = 0;
+  for (int base = lo; base < hi; base += 32) {
+    const int i = base + lane;
+    n += __popc(__ballot_sync(0xffffffffu, i < hi && __ldg(a.theta + i) == col));
+  }
+  if (lane == 0) warp_cnt[warp] = n;
+  __syncthreads();
+  int off = 0, total = 0;
+#pragma unroll
+  for (int k = 0; k < kWarps; ++k) {
+    off += (k < warp) ? warp_cnt[k] : 0;
+    total += warp_cnt[k];
+  }
+  if (total > 0 && total <= kSCap) {
+    for (int base = lo; base < hi; base += 32) {
       const int i = base + lane;
-      const bool hit = (i < a.M) && (__ldg(a.theta + i) == col);
+      const bool hit = i < hi && __ldg(a.theta + i) == col;
       const uint32_t mask = __ballot_sync(0xffffffffu, hit);
       if (hit) {
-        const int pos = n + __popc(mask & ((1u << lane) - 1u));
-        if (pos < kSCap) {
-          const float2 z = __ldg(reinterpret_cast<const float2 *>(a.Z) + i);
-          S.z[pos] = make_double2(z.x, z.y);
-        }
+        const float2 z = __ldg(reinterpret_cast<const float2 *>(a.Z) + i);
+        S.z[off + __popc(mask & ((1u << lane) - 1u))] = make_double2(z.x, z.y);
       }
-      n += __popc(mask);
+      off += __popc(mask);
     }
-    if (lane == 0) {
-      S.n = n;
-      S.in_smem = n <= kSCap;
-    }
+  }
+  if (threadIdx.x == 0) {
+    S.n = total;
+    S.in_smem = total <= kSCap;
   }
   __syncthreads();
 }
@@ -105,25 +118,29 @@ __device__ double block_sum(double v, double *red) {
 
 __device__ __forceinline__ float &q4(float4 &v, int q) { return (&v.x)[q]; }
 
-// R > 0: register-cached path (P <= 1024 R).  R == 0: generic recompute path.
-template <int R>
+// CACHED: l_p (fp64) cached in dynamic shared memory (P * 8 bytes), so the
+// particles are read from HBM once; otherwise l_p is recomputed per pass.
+template <bool CACHED>
 __global__ void __launch_bounds__(kThreads) reweight_kernel(const ReweightArgs a) {
+  extern __shared__ __align__(16) double lcache[];
   __shared__ SList S;
   __shared__ double red[kWarps];
+  __shared__ int warp_cnt[kWarps];
   const int j = blockIdx.x;
   const int col = a.col_offset + j + 1;
   const int64_t base = static_cast<int64_t>(j) * a.ld;
-  const float *xs = a.x + base, *ys = a.y + base;
-  float *ws = a.w + base;
+  const float4 *xs = reinterpret_cast<const float4 *>(a.x + base);
+  const float4 *ys = reinterpret_cast<const float4 *>(a.y + base);
+  float4 *ws = reinterpret_cast<float4 *>(a.w + base);
   const int quads = a.P >> 2;
 
-  collect_S(a, col, S);
+  collect_S(a, col, S, warp_cnt);
   const int nS = S.n;
 
   if (nS == 0) {  // untouched; log_norm = ln sum w
     double s = 0.0;
     for (int g = threadIdx.x; g < quads; g += kThreads) {
-      const float4 w4 = __ldcs(reinterpret_cast<const float4 *>(ws) + g);
+      const float4 w4 = __ldcs(ws + g);
       s += (static_cast<double>(w4.x) + w4.y) + (static_cast<double>(w4.z) + w4.w);
     }
     s = block_sum(s, red);
@@ -134,41 +151,23 @@ __global__ void __launch_bounds__(kThreads) reweight_kernel(const ReweightArgs a
     return;
   }
 
-  double m;
-  double lc[R > 0 ? 4 * R : 1];
-  if constexpr (R > 0) {
-    double lm = -INFINITY;
+  // pass 1: l_p and the block max
+  double lm = -INFINITY;
+#pragma unroll 4
+  for (int g = threadIdx.x; g < quads; g += kThreads) {
+    float4 X = __ldcs(xs + g), Y = __ldcs(ys + g), Wv = __ldcs(ws + g);
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int g = threadIdx.x + r * kThreads;
-      if (g < quads) {
-        float4 X = __ldcs(reinterpret_cast<const float4 *>(xs) + g);
-        float4 Y = __ldcs(reinterpret_cast<const float4 *>(ys) + g);
-        float4 Wv = __ldcs(reinterpret_cast<const float4 *>(ws) + g);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          lc[4 * r + q] = log_weight(a, S, col, q4(X, q), q4(Y, q), q4(Wv, q));
-          lm = fmax(lm, lc[4 * r + q]);
-        }
-      }
+    for (int q = 0; q < 4; ++q) {
+      const double l = log_weight(a, S, col, q4(X, q), q4(Y, q), q4(Wv, q));
+      if constexpr (CACHED) lcache[4 * g + q] = l;
+      lm = fmax(lm, l);
     }
-    m = block_max(lm, red);
-  } else {
-    double lm = -INFINITY;
-    for (int g = threadIdx.x; g < quads; g += kThreads) {
-      float4 X = __ldcs(reinterpret_cast<const float4 *>(xs) + g);
-      float4 Y = __ldcs(reinterpret_cast<const float4 *>(ys) + g);
-      float4 Wv = __ldcs(reinterpret_cast<const float4 *>(ws) + g);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) lm = fmax(lm, log_weight(a, S, col, q4(X, q), q4(Y, q), q4(Wv, q)));
-    }
-    m = block_max(lm, red);
   }
+  const double m = block_max(lm, red);
 
   if (m == -INFINITY) {  // every weight zero: uniform reset, flagged (never abort)
     const float u = 1.0f / static_cast<float>(a.P);
-    for (int g = threadIdx.x; g < quads; g += kThreads)
-      __stcs(reinterpret_cast<float4 *>(ws) + g, make_float4(u, u, u, u));
+    for (int g = threadIdx.x; g < quads; g += kThreads) __stcs(ws + g, make_float4(u, u, u, u));
     if (threadIdx.x == 0) {
       a.log_norm[j] = -INFINITY;
       a.flags[j] = 1u;
@@ -176,57 +175,41 @@ __global__ void __launch_bounds__(kThreads) reweight_kernel(const ReweightArgs a
     return;
   }
 
-  // pass 2: s = sum 2^(l - m)
+  // pass 2: e_p = 2^(l_p - m) (kept in place of l_p) and s = sum e_p
   double s = 0.0;
-  if constexpr (R > 0) {
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int g = threadIdx.x + r * kThreads;
-      if (g < quads) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float e = ex2_approx(static_cast<float>(lc[4 * r + q] - m));
-          lc[4 * r + q] = e;
-          s += e;
-        }
-      }
+  for (int g = threadIdx.x; g < quads; g += kThreads) {
+    float4 X, Y, Wv;
+    if constexpr (!CACHED) {
+      X = __ldcs(xs + g);
+      Y = __ldcs(ys + g);
+      Wv = __ldcs(ws + g);
     }
-  } else {
-    for (int g = threadIdx.x; g < quads; g += kThreads) {
-      float4 X = __ldcs(reinterpret_cast<const float4 *>(xs) + g);
-      float4 Y = __ldcs(reinterpret_cast<const float4 *>(ys) + g);
-      float4 Wv = __ldcs(reinterpret_cast<const float4 *>(ws) + g);
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        s += ex2_approx(static_cast<float>(log_weight(a, S, col, q4(X, q), q4(Y, q), q4(Wv, q)) - m));
+    for (int q = 0; q < 4; ++q) {
+      double l;
+      if constexpr (CACHED) l = lcache[4 * g + q];
+      else l = log_weight(a, S, col, q4(X, q), q4(Y, q), q4(Wv, q));
+      const float e = ex2_approx(static_cast<float>(l - m));
+      if constexpr (CACHED) lcache[4 * g + q] = e;
+      s += e;
     }
   }
   s = block_sum(s, red);
   const float inv_s = static_cast<float>(1.0 / s);
 
-  // pass 3: write w'
-  if constexpr (R > 0) {
+  // pass 3: w'_p = e_p / s
+  for (int g = threadIdx.x; g < quads; g += kThreads) {
+    float4 o;
+    if constexpr (CACHED) {
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int g = threadIdx.x + r * kThreads;
-      if (g < quads) {
-        float4 o;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) q4(o, q) = static_cast<float>(lc[4 * r + q]) * inv_s;
-        __stcs(reinterpret_cast<float4 *>(ws) + g, o);
-      }
-    }
-  } else {
-    for (int g = threadIdx.x; g < quads; g += kThreads) {
-      float4 X = __ldcs(reinterpret_cast<const float4 *>(xs) + g);
-      float4 Y = __ldcs(reinterpret_cast<const float4 *>(ys) + g);
-      float4 Wv = __ldcs(reinterpret_cast<const float4 *>(ws) + g);
-      float4 o;
+      for (int q = 0; q < 4; ++q) q4(o, q) = static_cast<float>(lcache[4 * g + q]) * inv_s;
+    } else {
+      float4 X = __ldcs(xs + g), Y = __ldcs(ys + g), Wv = __ldcs(ws + g);
 #pragma unroll
       for (int q = 0; q < 4; ++q)
         q4(o, q) = ex2_approx(static_cast<float>(log_weight(a, S, col, q4(X, q), q4(Y, q), q4(Wv, q)) - m)) * inv_s;
-      __stcs(reinterpret_cast<float4 *>(ws) + g, o);
     }
+    __stcs(ws + g, o);
   }
   if (threadIdx.x == 0) {
     const double ln2 = 0.69314718055994530942;
@@ -235,22 +218,28 @@ __global__ void __launch_bounds__(kThreads) reweight_kernel(const ReweightArgs a
   }
 }
 
-template <int R>
-cudaError_t launch_r(const ReweightArgs &a, cudaStream_t s) {
-  reweight_kernel<R><<<a.T, kThreads, 0, s>>>(a);
-  return cudaGetLastError();
-}
+constexpr int kMaxCacheBytes = 100 * 1024;
 
 }  // namespace
 
 cudaError_t launch_reweight(const ReweightArgs &a, cudaStream_t s) {
   if (a.T == 0) return cudaSuccess;
-  const int quads_per_thread = ((a.P >> 2) + kThreads - 1) / kThreads;
-  if (quads_per_thread <= 1) return launch_r<1>(a, s);
-  if (quads_per_thread <= 2) return launch_r<2>(a, s);
-  if (quads_per_thread <= 4) return launch_r<4>(a, s);
-  if (quads_per_thread <= 8) return launch_r<8>(a, s);
-  return launch_r<0>(a, s);
+  const size_t cache = static_cast<size_t>(a.P) * sizeof(double);
+  if (cache <= kMaxCacheBytes) {
+    static bool attr_set[64] = {};  // per device; benign race: idempotent attribute
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+      cudaError_t e = cudaFuncSetAttribute(reweight_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           kMaxCacheBytes);
+      if (e != cudaSuccess) return e;
+      if (dev >= 0 && dev < 64) attr_set[dev] = true;
+    }
+    reweight_kernel<true><<<a.T, kThreads, cache, s>>>(a);
+  } else {
+    reweight_kernel<false><<<a.T, kThreads, 0, s>>>(a);
+  }
+  return cudaGetLastError();
 }
 
 }  // namespace glmb

@@ -304,9 +304,9 @@ def test_reweight_parity_configs(L, orc, cfg):
     np.testing.assert_array_equal(fl.view(np.uint32), rfl)
 
 
-@pytest.mark.parametrize("P", [4, 1024, 4096, 8192, 12288])
+@pytest.mark.parametrize("P", [4, 1024, 4096, 8192, 12288, 16384])
 def test_reweight_paths_and_multi_detection(L, orc, P):
-    """Register-cached paths (P <= 8192) and the generic path (P > 8192); several
+    """Shared-memory-cached path (P <= 12800) and the recompute path (P = 16384); several
     detections per track (P:46-48 multiple detections per object), a far-away
     measurement, an empty track, theta values out of range and a column offset."""
     r = np.random.default_rng(P)
@@ -327,7 +327,7 @@ def test_reweight_paths_and_multi_detection(L, orc, P):
 
 def test_reweight_degenerate_and_many_assigned(L, orc):
     r = np.random.default_rng(3)
-    T, P, M = 2, 256, 1500          # > 1024 assigned measurements: generic S path
+    T, P, M = 2, 256, 1500          # > 256 assigned measurements: generic S path
     x = r.normal(0, 1, (T, P)).astype(np.float32)
     y = r.normal(0, 1, (T, P)).astype(np.float32)
     w = r.dirichlet(np.ones(P), T).astype(np.float32)
