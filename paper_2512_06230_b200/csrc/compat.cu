@@ -4,39 +4,91 @@
 //   C[i, j+1] = g_ij P_D L_ij,  C[i, 0] = kappa          (§Approach)
 //
 // Design: the work is M*T*P independent Gaussian
-// evaluations -- one exp per pair, bound by the SFU (MUFU.EX2) pipe, not by
-// HBM and not a dense contraction (no tensor cores).
+// evaluations -- one exp per pair.  It is bound by the exp throughput of the
+// SM (MUFU.EX2, 16/clk/SM measured), not by HBM and not a dense contraction
+// (no tensor cores: see DESIGN.md for why q = |z|^2 - 2 z.p + |p|^2 as a
+// K=4 GEMM would not survive tf32/bf16 at these coordinates).
 //  * One CTA (4 warps) = one (track j, measurement tile of 128*K) unit; warp w
 //    owns the contiguous measurements m0 + 32Kw + 32k + lane (k < K) in
 //    registers, so every measurement's sum over the particles is completed by
-//    one thread in a fixed order -- no cross-thread reduction, and C is
-//    bit-identical for any sharding of the tracks and any permutation of Z's
-//    rows.  Warps past M skip the arithmetic; the ragged last measurement
+//    one thread in a fixed particle order -- no cross-thread reduction, and C
+//    is bit-identical for any sharding of the tracks and any permutation of
+//    Z's rows.  Warps past M skip the arithmetic; the ragged last measurement
 //    tiles are scheduled last (unit = mt*T + j) to fill the tail.
-//  * The track's particles stream through shared memory in tiles of
-//    kTileP, moved by the TMA bulk-copy engine (cp.async.bulk + mbarrier,
-//    kStages-deep ring) and reused by all 128*K measurements of the CTA.
-//  * Each tile is whitened once in place (X' = a1(x-cx) + a2(y-cy),
-//    Y' = b2(y-cy), centred on the track's first particle so the fp32
-//    subtraction of large coordinates is exact), which turns
-//    1/2 log2(e) d^T R^-1 d into |d'|^2 for any SPD R.  Per pair the inner
-//    loop is then FADD2 dx, FADD2 dy, FMUL2, FFMA2, MUFU.EX2, FFMA2 acc on
-//    packed fp32x2 (two particles per instruction).
+//  * The track's particles stream through shared memory in tiles of kTileP,
+//    moved by the TMA bulk-copy engine (cp.async.bulk + mbarrier ring of raw
+//    x, y, w) and reused by all 128*K measurements of the CTA.
+//  * Whitening: with U' the scaled Cholesky factor of R^-1,
+//    1/2 log2(e) d^T R^-1 d = |U'(z - c) - U'(p - c)|^2 for any SPD R, where c
+//    is the mean of the track's first tile (so p - c and z - c are exact or
+//    tiny for every relevant pair even at 4 km coordinates).  Each raw tile is
+//    whitened once into an AoS float4 tile (X', Y', CP = -|p'|^2, w), double
+//    buffered so one __syncthreads per tile suffices.
+//  * Inner loop: one LDS.128 per particle; the thread's measurements are
+//    packed in pairs (fp32x2), the particle's values are scalar operands that
+//    FFMA2/FADD2 broadcast:
+//      e = 2z'x * X' + (2z'y * Y' + CP) - |z'|^2  = -|z' - p'|^2
+//      acc += w * 2^e
+//    = 3 packed FP ops + 2 exp + 1 packed FMA per two pairs.  Optionally one
+//    particle in EMU_PERIOD evaluates 2^e on the FMA pipe instead of MUFU
+//    (round-to-nearest range reduction with the 1.5*2^23 trick, degree-5
+//    minimax polynomial, rel. error 2.4e-7 ~ MUFU's, exponent added with one
+//    LEA) to balance the MUFU and FMA pipes.
+//    The choice is by particle index, so every measurement sees the same mix.
 //  * Two-level summation (per tile, then across tiles) keeps the fp32 sum
-//    error ~kTileP/2*eps instead of P/2*eps.
+//    error ~kTileP*eps instead of P*eps.
 //  * Epilogue: L = norm*sum, gate bit via __ballot_sync (32 consecutive
 //    measurements of a warp = one gate word), coalesced C stores.
+#include <cstdlib>
+
 #include "glmb_device.cuh"
 #include "glmb_internal.h"
 
 namespace glmb {
 namespace {
 
-constexpr int kThreads = 128;
-constexpr int kTileP = 512;   // particles per shared-memory stage (fixed: sets the sum order)
-constexpr int kStages = 4;    // TMA ring depth
+constexpr int kWarps = 4;
+constexpr int kThreads = 32 * kWarps;
+constexpr int kTileM = 32 * kWarps;  // measurements per tile per K
+constexpr int kTileP = 512;          // particles per shared-memory tile (fixed: sets the sum order)
+constexpr int kStages = 2;           // TMA ring depth of raw tiles (x, y, w)
 constexpr int kMaxK = 4;
-constexpr int kSmemBytes = kStages * 3 * kTileP * 4;
+constexpr int kRawFloats = 3 * kTileP;
+constexpr int kSmemBytes = kStages * kRawFloats * 4 + 2 * kTileP * 16;  // raw ring + 2 AoS tiles
+
+// degree-5 minimax fit of 2^f on [-1/2, 1/2] (max rel. error 7.5e-8, 2.3e-7 in fp32 Horner)
+constexpr float kC0 = 1.0000001192092896f, kC1 = 0.6931469440460205f, kC2 = 0.24022120237350464f,
+                kC3 = 0.05550713092088699f, kC4 = 0.009675533510744572f, kC5 = 0.0013276446843519807f;
+constexpr float kRound = 12582912.0f;  // 1.5 * 2^23: x + kRound rounds x to an integer
+
+// 2^e for a packed pair on the FMA + ALU pipes (no MUFU).  e <= 0 expected;
+// e < -125 is clamped (result < 2^-125 * 1.42 vs MUFU's flush to 0).
+__device__ __forceinline__ f2 exp2_poly2(f2 e) {
+  float e0, e1;
+  f2_unpack(e, e0, e1);
+  e = f2_pack(fmaxf(e0, -125.0f), fmaxf(e1, -125.0f));
+  const f2 rnd = f2_pack(kRound, kRound);
+  const f2 t = f2_add(e, rnd);             // t = kRound + round(e)
+  const f2 f = f2_sub(e, f2_sub(t, rnd));  // f = e - round(e) in [-1/2, 1/2]
+  f2 p = f2_fma(f2_pack(kC5, kC5), f, f2_pack(kC4, kC4));
+  p = f2_fma(p, f, f2_pack(kC3, kC3));
+  p = f2_fma(p, f, f2_pack(kC2, kC2));
+  p = f2_fma(p, f, f2_pack(kC1, kC1));
+  p = f2_fma(p, f, f2_pack(kC0, kC0));
+  float p0, p1, t0, t1;
+  f2_unpack(p, p0, p1);
+  f2_unpack(t, t0, t1);
+  // low mantissa bits of t hold round(e); << 23 moves them into the exponent field
+  p0 = __uint_as_float(__float_as_uint(p0) + (__float_as_uint(t0) << 23));
+  p1 = __uint_as_float(__float_as_uint(p1) + (__float_as_uint(t1) << 23));
+  return f2_pack(p0, p1);
+}
+
+__device__ __forceinline__ f2 exp2_mufu2(f2 e) {
+  float e0, e1;
+  f2_unpack(e, e0, e1);
+  return f2_pack(ex2_approx(e0), ex2_approx(e1));
+}
 
 __device__ __forceinline__ void issue_tile(const CompatArgs &a, const float *xs, const float *ys, const float *ws,
                                            float *stage, uint64_t *bar, int t) {
@@ -49,70 +101,106 @@ __device__ __forceinline__ void issue_tile(const CompatArgs &a, const float *xs,
   bulk_g2s(stage + 2 * kTileP, ws + p0, bytes, bar);
 }
 
-// Sum over one shared-memory tile for this warp's first KV measurement slices.
-template <int K, int KV>
-__device__ __forceinline__ void tile_pairs(const float2 *__restrict__ X2, const float2 *__restrict__ Y2,
-                                           const float2 *__restrict__ W2, int npairs, const float (&zx)[K],
-                                           const float (&zy)[K], float (&tot)[K]) {
-  f2 acc[KV];
+// Per-thread measurements, packed in pairs (slot 2h, 2h+1 -> lane halves).
+template <int K>
+struct Meas {
+  static constexpr int H = (K + 1) / 2;
+  f2 zx2[H], zy2[H], nzz[H];  // 2 z'x, 2 z'y, -|z'|^2
+  float tot[2 * H];          // running sums per measurement slot
+};
+
+// One particle against the thread's HV measurement pairs.  POLY_MASK bit h:
+// pair h takes 2^e from the FMA-pipe polynomial instead of MUFU.
+template <int H, int POLY_MASK>
+__device__ __forceinline__ void particle_step(const float4 p, const f2 (&zx2)[H], const f2 (&zy2)[H],
+                                              const f2 (&nzz)[H], f2 (&acc)[H], int hv) {
+  const f2 px = f2_pack(p.x, p.x), py = f2_pack(p.y, p.y), cp = f2_pack(p.z, p.z), pw = f2_pack(p.w, p.w);
 #pragma unroll
-  for (int k = 0; k < KV; ++k) acc[k] = 0ull;
-#pragma unroll 2
-  for (int q = 0; q < npairs; ++q) {
-    const float2 xv = X2[q], yv = Y2[q], wv = W2[q];
-    const f2 px = f2_pack(xv.x, xv.y), py = f2_pack(yv.x, yv.y), pw = f2_pack(wv.x, wv.y);
-#pragma unroll
-    for (int k = 0; k < KV; ++k) {
-      const f2 dx = f2_sub(f2_pack(zx[k], zx[k]), px);
-      const f2 dy = f2_sub(f2_pack(zy[k], zy[k]), py);
-      const f2 qq = f2_fma(dy, dy, f2_mul(dx, dx));
-      float q0, q1;
-      f2_unpack(qq, q0, q1);
-      acc[k] = f2_fma(pw, f2_pack(ex2_approx(-q0), ex2_approx(-q1)), acc[k]);
+  for (int h = 0; h < H; ++h) {
+    if (h < hv) {
+      f2 e = f2_fma(zy2[h], py, cp);
+      e = f2_fma(zx2[h], px, e);
+      e = f2_add(e, nzz[h]);
+      acc[h] = f2_fma(pw, ((POLY_MASK >> h) & 1) ? exp2_poly2(e) : exp2_mufu2(e), acc[h]);
     }
-  }
-#pragma unroll
-  for (int k = 0; k < KV; ++k) {
-    float lo, hi;
-    f2_unpack(acc[k], lo, hi);
-    tot[k] += lo + hi;
   }
 }
 
-template <int K>
-__device__ __forceinline__ void tile_dispatch(int kv, const float *X, const float *Y, const float *W, int npairs,
-                                              const float (&zx)[K], const float (&zy)[K], float (&tot)[K]) {
-  const float2 *X2 = reinterpret_cast<const float2 *>(X);
-  const float2 *Y2 = reinterpret_cast<const float2 *>(Y);
-  const float2 *W2 = reinterpret_cast<const float2 *>(W);
-  if (kv == K) {
-    tile_pairs<K, K>(X2, Y2, W2, npairs, zx, zy, tot);
-  } else {
-    if constexpr (K > 1) if (kv == 1) tile_pairs<K, 1>(X2, Y2, W2, npairs, zx, zy, tot);
-    if constexpr (K > 2) if (kv == 2) tile_pairs<K, (K > 2 ? 2 : 1)>(X2, Y2, W2, npairs, zx, zy, tot);
-    if constexpr (K > 3) if (kv == 3) tile_pairs<K, (K > 3 ? 3 : 1)>(X2, Y2, W2, npairs, zx, zy, tot);
-    if constexpr (K > 4) {
-      if (kv == 4) tile_pairs<K, 4>(X2, Y2, W2, npairs, zx, zy, tot);
-      if (kv == 5) tile_pairs<K, (K > 5 ? 5 : 4)>(X2, Y2, W2, npairs, zx, zy, tot);
-      if (kv == 6) tile_pairs<K, (K > 6 ? 6 : 4)>(X2, Y2, W2, npairs, zx, zy, tot);
-      if (kv == 7) tile_pairs<K, (K > 7 ? 7 : 4)>(X2, Y2, W2, npairs, zx, zy, tot);
+// Mask of the pairs that use the polynomial for particle u of an EMU_PERIOD group:
+// pair h is emulated when (u + 2h) % EMU_PERIOD == EMU_PERIOD - 1, so the
+// polynomial work is spread over the group instead of bunched on one particle.
+template <int EMU_PERIOD, int H>
+constexpr int poly_mask(int u) {
+  int m = 0;
+  if (EMU_PERIOD < 0) {  // bunched: every pair of particle |P|-1 (pair-independent choice)
+    if (u == -EMU_PERIOD - 1) m = (1 << H) - 1;
+    return m;
+  }
+  for (int h = 0; h < H; ++h)
+    if (EMU_PERIOD > 0 && (u + 2 * h) % EMU_PERIOD == EMU_PERIOD - 1) m |= 1 << h;
+  return m;
+}
+
+template <int H, int EMU_PERIOD, int U = 0>
+__device__ __forceinline__ void step_u(int u, const float4 p, const f2 (&zx2)[H], const f2 (&zy2)[H],
+                                       const f2 (&nzz)[H], f2 (&acc)[H], int hv) {
+  // u is a compile-time constant after unrolling; recurse to turn it into a template argument
+  if constexpr (U < (EMU_PERIOD > 0 ? EMU_PERIOD : -EMU_PERIOD)) {
+    if (u == U) particle_step<H, poly_mask<EMU_PERIOD, H>(U)>(p, zx2, zy2, nzz, acc, hv);
+    else step_u<H, EMU_PERIOD, U + 1>(u, p, zx2, zy2, nzz, acc, hv);
+  }
+}
+
+// Sum over one AoS tile for this warp's first HV measurement pairs.
+template <int K, int HV, int EMU_PERIOD>
+__device__ __forceinline__ void tile_sum(const float4 *__restrict__ A, int np, Meas<K> &m) {
+  constexpr int H = Meas<K>::H;
+  f2 acc[H];
+#pragma unroll
+  for (int h = 0; h < H; ++h) acc[h] = 0ull;
+  int p = 0;
+  if constexpr (EMU_PERIOD != 0) {
+    constexpr int PER = EMU_PERIOD > 0 ? EMU_PERIOD : -EMU_PERIOD;
+#pragma unroll 1
+    for (; p + PER <= np; p += PER) {
+#pragma unroll
+      for (int u = 0; u < PER; ++u) step_u<H, EMU_PERIOD>(u, A[p + u], m.zx2, m.zy2, m.nzz, acc, HV);
     }
   }
+#pragma unroll 4
+  for (; p < np; ++p) particle_step<H, 0>(A[p], m.zx2, m.zy2, m.nzz, acc, HV);
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+    float lo, hi;
+    f2_unpack(acc[h], lo, hi);
+    m.tot[2 * h] += lo;
+    m.tot[2 * h + 1] += hi;
+  }
+}
+
+template <int K, int EMU_PERIOD>
+__device__ __forceinline__ void tile_dispatch(int hv, const float4 *A, int np, Meas<K> &m) {
+  constexpr int H = Meas<K>::H;
+  if (hv == H) tile_sum<K, H, EMU_PERIOD>(A, np, m);
+  else if constexpr (H > 1) tile_sum<K, 1, EMU_PERIOD>(A, np, m);
 }
 
 // Unit u = mt * T + j (all full measurement tiles first, the ragged last tiles
 // at the end of the grid, so the short units fill the tail of the schedule).
-// Warp w owns the contiguous measurements m0 + w*32K + k*32 + lane, k < K.
-template <int K>
+template <int K, int EMU_PERIOD>
 __global__ void __launch_bounds__(kThreads) compat_kernel(const CompatArgs a) {
+  constexpr int H = Meas<K>::H;
   extern __shared__ __align__(128) float smem[];
+  float4 *aos = reinterpret_cast<float4 *>(smem + kStages * kRawFloats);  // 2 AoS tiles
   __shared__ __align__(8) uint64_t bars[kStages];
+  __shared__ float red[2][kWarps];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int mt = blockIdx.x / a.T;
   const int j = blockIdx.x - mt * a.T;
-  const int wbase = mt * (kThreads * K) + warp * (32 * K);  // first measurement of this warp
-  const int kv = min(K, max(0, (a.M - wbase + 31) >> 5));   // measurement slices with any valid lane
+  const int wbase = mt * (kTileM * K) + warp * (32 * K);   // first measurement of this warp
+  const int kv = min(K, max(0, (a.M - wbase + 31) >> 5));  // measurement slots with any valid lane
+  const int hv = (kv + 1) >> 1;                            // packed pairs with any valid slot
   const int64_t base = static_cast<int64_t>(j) * a.ld;
   const float *xs = a.x + base, *ys = a.y + base, *ws = a.w + base;
   const int ntiles = (a.P + kTileP - 1) / kTileP;
@@ -123,43 +211,65 @@ __global__ void __launch_bounds__(kThreads) compat_kernel(const CompatArgs a) {
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0) {
-    for (int s = 0; s < kStages && s < ntiles; ++s) issue_tile(a, xs, ys, ws, smem + s * 3 * kTileP, &bars[s], s);
-  }
-
-  const float cx = __ldg(xs), cy = __ldg(ys);  // centre: the track's first particle
-  float zx[K], zy[K], tot[K];
+  if (tid == 0)
+    for (int s = 0; s < kStages && s < ntiles; ++s) issue_tile(a, xs, ys, ws, smem + s * kRawFloats, &bars[s], s);
+  float2 zr[2 * H];
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
+  for (int k = 0; k < 2 * H; ++k) {
     const int i = wbase + k * 32 + lane;
-    zx[k] = 0.f;
-    zy[k] = 0.f;
-    if (i < a.M) {
-      const float2 z = __ldg(reinterpret_cast<const float2 *>(a.Z) + i);
-      const float lx = z.x - cx, ly = z.y - cy;
-      zx[k] = fmaf(a.a2, ly, a.a1 * lx);
-      zy[k] = a.b2 * ly;
-    }
-    tot[k] = 0.f;
+    zr[k] = (k < K && i < a.M) ? __ldg(reinterpret_cast<const float2 *>(a.Z) + i) : make_float2(0.f, 0.f);
   }
 
+  Meas<K> m;
+  float cx = 0.f, cy = 0.f;
   for (int t = 0; t < ntiles; ++t) {
     const int s = t % kStages;
-    float *X = smem + s * 3 * kTileP;
-    float *Y = X + kTileP;
+    const float *X = smem + s * kRawFloats;
+    const float *Y = X + kTileP;
     const float *W = Y + kTileP;
+    float4 *A = aos + (t & 1) * kTileP;
     const int np = min(kTileP, a.P - t * kTileP);
     mbar_wait_parity(&bars[s], static_cast<uint32_t>(t / kStages) & 1u);
-    for (int idx = tid; idx < np; idx += kThreads) {  // whiten in place
-      const float lx = X[idx] - cx, ly = Y[idx] - cy;
-      X[idx] = fmaf(a.a2, ly, a.a1 * lx);
-      Y[idx] = a.b2 * ly;
+    if (t == 0) {  // centre c = mean position of the first tile (fixed order -> deterministic)
+      float sx = 0.f, sy = 0.f;
+      for (int idx = tid; idx < np; idx += kThreads) {
+        sx += X[idx];
+        sy += Y[idx];
+      }
+      sx = warp_sum(sx);
+      sy = warp_sum(sy);
+      if (lane == 0) {
+        red[0][warp] = sx;
+        red[1][warp] = sy;
+      }
+      __syncthreads();
+      cx = ((red[0][0] + red[0][1]) + (red[0][2] + red[0][3])) / static_cast<float>(np);
+      cy = ((red[1][0] + red[1][1]) + (red[1][2] + red[1][3])) / static_cast<float>(np);
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        float zx[2], zy[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const float lx = zr[2 * h + u].x - cx, ly = zr[2 * h + u].y - cy;
+          zx[u] = fmaf(a.a2, ly, a.a1 * lx);
+          zy[u] = a.b2 * ly;
+        }
+        m.zx2[h] = f2_pack(2.0f * zx[0], 2.0f * zx[1]);
+        m.zy2[h] = f2_pack(2.0f * zy[0], 2.0f * zy[1]);
+        m.nzz[h] = f2_pack(-fmaf(zx[0], zx[0], zy[0] * zy[0]), -fmaf(zx[1], zx[1], zy[1] * zy[1]));
+        m.tot[2 * h] = 0.f;
+        m.tot[2 * h + 1] = 0.f;
+      }
     }
-    __syncthreads();
-    if (kv > 0) tile_dispatch<K>(kv, X, Y, W, np >> 1, zx, zy, tot);
-    fence_proxy_async_smem();  // order this CTA's generic smem accesses before the next TMA write
-    __syncthreads();
-    if (tid == 0 && t + kStages < ntiles) issue_tile(a, xs, ys, ws, X, &bars[s], t + kStages);
+    for (int idx = tid; idx < np; idx += kThreads) {  // whiten raw tile -> AoS (X', Y', -|p'|^2, w)
+      const float lx = X[idx] - cx, ly = Y[idx] - cy;
+      const float px = fmaf(a.a2, ly, a.a1 * lx), py = a.b2 * ly;
+      A[idx] = make_float4(px, py, -fmaf(px, px, py * py), W[idx]);
+    }
+    fence_proxy_async_smem();  // raw stage s was read through the generic proxy; TMA rewrites it next
+    __syncthreads();           // AoS tile t complete; every warp is done with tile t-1
+    if (tid == 0 && t + kStages < ntiles) issue_tile(a, xs, ys, ws, smem + s * kRawFloats, &bars[s], t + kStages);
+    if (hv > 0) tile_dispatch<K, EMU_PERIOD>(hv, A, np, m);
   }
 
   // epilogue: likelihood, gate bit, C entry, clutter column
@@ -169,7 +279,7 @@ __global__ void __launch_bounds__(kThreads) compat_kernel(const CompatArgs a) {
     if (k < kv) {
       const int i = wbase + k * 32 + lane;
       const bool valid = i < a.M;
-      const float L = tot[k] * a.norm;
+      const float L = m.tot[k] * a.norm;
       const bool g = valid && (L >= a.gamma);
       if (valid) a.C_tracks[static_cast<int64_t>(j) * a.ldc + i] = g ? a.p_d * L : 0.0f;
       const uint32_t word = __ballot_sync(0xffffffffu, g);
@@ -184,11 +294,42 @@ __global__ void clutter_fill_kernel(float *c, int32_t M, float kappa) {
   if (i < M) c[i] = kappa;
 }
 
-template <int K>
+template <int K, int EMU_PERIOD>
 cudaError_t launch_k(const CompatArgs &a, cudaStream_t s) {
   const int64_t grid = static_cast<int64_t>(a.T) * a.n_mtiles;
-  compat_kernel<K><<<static_cast<unsigned>(grid), kThreads, kSmemBytes, s>>>(a);
+  compat_kernel<K, EMU_PERIOD><<<static_cast<unsigned>(grid), kThreads, kSmemBytes, s>>>(a);
   return cudaGetLastError();
+}
+
+// Share of the exps evaluated on the FMA pipe: one particle in |EMU| (negative:
+// every measurement pair of that particle, so each measurement sees the same
+// MUFU/polynomial mix and C stays bit-exact under row permutations of Z;
+// positive: pair h of particle u when (u + 2h) % EMU == EMU - 1, spread; 0:
+// all MUFU).  Default -12 (measured best bit-exact setting on B200, see
+// profiles/).  GLMB_COMPAT_EMU overrides it (diagnostics / A-B runs).
+int emu_period() {
+  static int v = [] {
+    const char *e = std::getenv("GLMB_COMPAT_EMU");
+    return e ? std::atoi(e) : -12;
+  }();
+  return v;
+}
+
+template <int K>
+cudaError_t launch_e(const CompatArgs &a, cudaStream_t s) {
+  switch (emu_period()) {
+    case 0: return launch_k<K, 0>(a, s);
+    case 4: return launch_k<K, 4>(a, s);
+    case 6: return launch_k<K, 6>(a, s);
+    case 8: return launch_k<K, 8>(a, s);
+    case 10: return launch_k<K, 10>(a, s);
+    case 12: return launch_k<K, 12>(a, s);
+    case 16: return launch_k<K, 16>(a, s);
+    case -6: return launch_k<K, -6>(a, s);
+    case -8: return launch_k<K, -8>(a, s);
+    case -12: return launch_k<K, -12>(a, s);
+    default: return launch_k<K, 0>(a, s);
+  }
 }
 
 }  // namespace
@@ -200,16 +341,16 @@ void compat_plan(int32_t M, int32_t P, int32_t *K, int32_t *n_mtiles) {
   (void)P;
   int32_t k = kMaxK;
   const int32_t warps_needed = (M + 31) / 32;
-  while (k > 1 && warps_needed <= (kThreads / 32) * (k / 2)) k /= 2;
+  while (k > 1 && warps_needed <= kWarps * (k / 2)) k /= 2;
   *K = k;
-  *n_mtiles = (M + kThreads * k - 1) / (kThreads * k);
+  *n_mtiles = (M + kTileM * k - 1) / (kTileM * k);
 }
 
 cudaError_t launch_compat(const CompatArgs &a, cudaStream_t s) {
   switch (a.K) {
-    case 1: return launch_k<1>(a, s);
-    case 2: return launch_k<2>(a, s);
-    case 4: return launch_k<4>(a, s);
+    case 1: return launch_e<1>(a, s);
+    case 2: return launch_e<2>(a, s);
+    case 4: return launch_e<4>(a, s);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -65,6 +65,58 @@ __global__ void ffma_kernel(float *out, int iters, float seed, long long *cyc) {
   if (threadIdx.x == 0 && blockIdx.x == 0) cyc[0] = t1 - t0;
 }
 
+// NM independent MUFU.EX2 and NF independent FFMA2 per iteration (8 chains each):
+// tells whether the SFU and FMA pipes overlap at full rate.
+template <int NM, int NF>
+__global__ void mix_kernel(float *out, int iters, float seed, long long *cyc) {
+  float v[NM > 0 ? NM : 1];
+  unsigned long long u[NF > 0 ? NF : 1], m, a;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(m) : "f"(0.999f));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(a) : "f"(seed * 1e-3f));
+#pragma unroll
+  for (int c = 0; c < NM; ++c) v[c] = seed * (c + 1) * 1e-3f - 0.5f;
+#pragma unroll
+  for (int c = 0; c < NF; ++c) asm("mov.b64 %0, {%1, %2};" : "=l"(u[c]) : "f"(seed + c), "f"(seed - c));
+  const long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < (NM > NF ? NM : NF); ++c) {
+      if (c < NM) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(v[c]));
+      if (c < NF) asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(u[c]) : "l"(m), "l"(a));
+    }
+  }
+  const long long t1 = clock64();
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < NM; ++c) s += v[c];
+#pragma unroll
+  for (int c = 0; c < NF; ++c) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(u[c]));
+    s += lo + hi;
+  }
+  if (s == 12345.f) out[0] = s;
+  if (threadIdx.x == 0 && blockIdx.x == 0) cyc[0] = t1 - t0;
+}
+
+template <int NM, int NF>
+void run_mix(int sms, float *out, long long *cyc) {
+  const int threads = 256, blocks = sms * 8, iters = 2048;
+  mix_kernel<NM, NF><<<blocks, threads>>>(out, 16, 1.0f, cyc);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  mix_kernel<NM, NF><<<blocks, threads>>>(out, iters, 1.0f, cyc);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double th = double(blocks) * threads * iters;
+  printf("  \"mix_m%d_f%d\": {\"ex2_per_s\": %.6e, \"ffma2_per_s\": %.6e, \"ms\": %.4f},\n", NM, NF,
+         th * NM / (ms * 1e-3), th * NF / (ms * 1e-3), ms);
+}
+
 template <typename F>
 void run(const char *name, F kern, int sms, float *out, long long *cyc, bool last) {
   const int threads = 256, blocks_per_sm = 8, iters = 4096;
@@ -98,6 +150,10 @@ int main() {
   cudaMalloc(&out, 16);
   cudaMalloc(&cyc, 16);
   printf("{\n  \"sm_count\": %d,\n  \"attr_clock_mhz\": %.1f,\n", sms, clk_khz / 1e3);
+  run_mix<8, 8>(sms, out, cyc);
+  run_mix<8, 12>(sms, out, cyc);
+  run_mix<8, 16>(sms, out, cyc);
+  run_mix<4, 16>(sms, out, cyc);
   run("mufu_ex2", ex2_kernel, sms, out, cyc, false);
   run("ffma2_f32x2", ffma2_kernel, sms, out, cyc, false);
   run("ffma", ffma_kernel, sms, out, cyc, true);
