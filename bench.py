@@ -191,7 +191,8 @@ def main():
     from paper_2512_06230_b200 import _lib as L
     from paper_2512_06230_b200.build import build
     from paper_2512_06230_b200.scenes import CONFIGS, make_scene
-    from paper_2512_06230_b200.step import GlmbStep, shard_range
+    from paper_2512_06230_b200.dist import ShardPlan, allgather_columns, broadcast_measurements
+    from paper_2512_06230_b200.step import GlmbStep
 
     if rank == 0:
         build()
@@ -204,21 +205,20 @@ def main():
     dev = torch.device("cuda", local)
     cfg = CONFIGS[cfg_id]
     Tk = cfg.T + cfg.B
-    cols = shard_range(Tk, rank, world)
-    per = (Tk + world - 1) // world
+    plan = ShardPlan(Tk, world)
+    cols = plan.cols(rank)
+    per = plan.per_rank
     n_steps_scene = min(cfg.steps, a.warmup + a.steps)
     scene = make_scene(cfg_id, rows=range(cols.start, min(cols.stop, cfg.T)), steps=n_steps_scene)
-    st = GlmbStep(scene, cols=cols, device=dev)
+    st = GlmbStep(scene, cols=cols, device=dev, rows_alloc=per)
     stream = torch.cuda.Stream(device=dev)
     # W>1: Z/theta live on rank 0 and are broadcast inside the timed region;
     # column blocks of C (+ gate words) are all-gathered into the full matrix.
     if world > 1:
-        if per * world != Tk:
-            raise SystemExit("config 4 sharding expects T_k divisible by the world size")
         Zbuf = torch.zeros(st.M_max, 2, device=dev)
         thbuf = torch.zeros(st.M_max, dtype=torch.int32, device=dev)
-        C_full = torch.empty(Tk, st.ldc, device=dev)
-        G_full = torch.empty(Tk, st.ldg, dtype=torch.int32, device=dev)
+        C_full = torch.empty(per * world, st.ldc, device=dev)
+        G_full = torch.empty(per * world, st.ldg, dtype=torch.int32, device=dev)
 
     ev = lambda: torch.cuda.Event(enable_timing=True)
     stage_names = ["predict", "birth", "compat", "reweight"]
@@ -231,8 +231,7 @@ def main():
                 M = st.Z[zi].shape[0]
                 if rank == 0:
                     Zbuf[:M].copy_(st.Z[zi]); thbuf[:M].copy_(st.theta[zi])
-                dist.broadcast(Zbuf[:M], src=0)
-                dist.broadcast(thbuf[:M], src=0)
+                broadcast_measurements(Zbuf[:M], thbuf[:M], src=0)
                 Zk, thk = Zbuf[:M], thbuf[:M]
             else:
                 Zk, thk = st.Z[zi], st.theta[zi]
@@ -252,8 +251,8 @@ def main():
             if timed:
                 marks[4].record(stream)
             if world > 1:
-                dist.all_gather_into_tensor(C_full, st.out.C_tracks)
-                dist.all_gather_into_tensor(G_full, st.out.gate)
+                allgather_columns(st.out.C_tracks, C_full)
+                allgather_columns(st.out.gate, G_full)
         return marks
 
     for k in range(a.warmup):

@@ -20,11 +20,9 @@ from .scenes import Scene
 
 
 def shard_range(n: int, rank: int, world: int) -> range:
-    """Contiguous, as-even-as-possible block of n items for rank."""
-    per = (n + world - 1) // world
-    lo = min(n, rank * per)
-    hi = min(n, lo + per)
-    return range(lo, hi)
+    """Contiguous block of the n global columns owned by rank (dist.ShardPlan)."""
+    from .dist import ShardPlan
+    return ShardPlan(n, world).cols(rank)
 
 
 @dataclasses.dataclass
@@ -44,7 +42,7 @@ class GlmbStep:
     """
 
     def __init__(self, scene: Scene, cols: Optional[range] = None, device="cuda",
-                 seed: Optional[int] = None):
+                 seed: Optional[int] = None, rows_alloc: Optional[int] = None):
         cfg = scene.cfg
         self.scene = scene
         self.cfg = cfg
@@ -79,10 +77,13 @@ class GlmbStep:
         self.ldg = (self.M_max + 31) // 32
         self.Z = [torch.from_numpy(z).to(dev) for z in scene.Z]
         self.theta = [torch.from_numpy(t).to(dev) for t in scene.theta]
+        # rows_alloc >= T_local pads the column block to the common all-gather size
+        ra = self.T_local if rows_alloc is None else max(rows_alloc, self.T_local)
+        self.rows_alloc = ra
         self.out = StepOutputs(
             C_clutter=torch.zeros(self.M_max, dtype=torch.float32, device=dev),
-            C_tracks=torch.zeros(self.T_local, self.ldc, dtype=torch.float32, device=dev),
-            gate=torch.zeros(self.T_local, self.ldg, dtype=torch.int32, device=dev),
+            C_tracks=torch.zeros(ra, self.ldc, dtype=torch.float32, device=dev),
+            gate=torch.zeros(ra, self.ldg, dtype=torch.int32, device=dev),
             log_norm=torch.zeros(self.T_local, dtype=torch.float32, device=dev),
             flags=torch.zeros(self.T_local, dtype=torch.int32, device=dev))
         self.seed = cfg.seed if seed is None else seed
