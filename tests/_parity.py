@@ -75,6 +75,7 @@ def check_log_norm(gpu, ref):
     g = np.asarray(gpu, np.float64)
     r = np.asarray(ref, np.float64)
     same_inf = np.isinf(g) & np.isinf(r) & (np.sign(g) == np.sign(r))
-    d = np.abs(g - r)
+    with np.errstate(invalid="ignore"):
+        d = np.abs(g - r)
     ok = same_inf | (d <= REL_C * np.maximum(np.abs(r), 1.0))
     assert ok.all(), f"log_norm off: worst d={d[~ok].max():.3e}"

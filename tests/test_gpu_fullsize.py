@@ -125,8 +125,7 @@ def test_compat_large_M_row_permutation_bit_exact(L):
     from paper_2512_06230_b200.scenes import make_scene
     from paper_2512_06230_b200.step import GlmbStep
     s = make_scene(3, rows=range(0, 24), steps=1)
-    c = s.cfg
-    st = GlmbStep(s)
+    st = GlmbStep(s, cols=range(0, 24))
     st.compat(0)
     C = st.out.C_tracks.clone()
     M = len(s.Z[0])
