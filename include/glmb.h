@@ -97,9 +97,10 @@ int glmb_sm_count(int device);
  * glmb_predict -- CTRV survival propagation (P:3, §Approach).
  *
  * For every track j < in->n_tracks and particle p < P:
- *   (n0, n1) = Box-Muller(Philox4x32-10(key = (lo32 seed, hi32 seed),
- *                                      counter = (p, gid[j], step, 0)))
- *   nu_a = sigma_a * n0,  nu_w = sigma_w * n1
+ *   (n0, n1, n2, n3) = Box-Muller normals of Philox4x32-10(
+ *        key = (lo32 seed, hi32 seed), counter = (p / 2, gid[j], step, 0))
+ *   (na, nw) = (n0, n1) for even p, (n2, n3) for odd p
+ *   nu_a = sigma_a * na,  nu_w = sigma_w * nw
  *   h = omega dt / 2
  *   x'     = x + v dt sinc(h) cos(psi + h) + 1/2 dt^2 cos(psi) nu_a
  *   y'     = y + v dt sinc(h) sin(psi + h) + 1/2 dt^2 sin(psi) nu_a

@@ -161,9 +161,10 @@ void oracle_ctrv(const double s_in[5], double dt, double nu_a, double nu_w,
 /* Survival prediction: "particles representing targets that have survived
  * from step k-1 are propagated forward using the constant turn rate and
  * velocity kinematics model ... as a batch operation over all particles and
- * surviving tracks" (§Approach).  Noise: Philox block with counter
- * (p, gid_j, step, tag=0) (O2, domain 0 = predict); nu_a = sigma_a n0,
- * nu_w = sigma_w n1.  Element (j,p) at j*ld + p.  Outputs fp64 [T][ld]. */
+ * surviving tracks" (§Approach).  Noise (O2, R9): Philox block with
+ * counter (p/2, gid_j, step, tag=0) (domain 0 = predict); particle p takes
+ * (n0, n1) if p is even, (n2, n3) if odd; nu_a = sigma_a n_a, nu_w = sigma_w n_w.
+ * Element (j,p) at j*ld + p.  Outputs fp64 [T][ld]. */
 void oracle_predict(int32_t T, int32_t P, int64_t ld, const float *x,
                     const float *y, const float *v, const float *psi,
                     const float *omega, const int32_t *gid, float dt,
@@ -174,11 +175,15 @@ void oracle_predict(int32_t T, int32_t P, int64_t ld, const float *x,
   for (int32_t j = 0; j < T; ++j) {
     for (int32_t p = 0; p < P; ++p) {
       int64_t e = (int64_t)j * ld + p;
-      uint32_t ctr[4] = {(uint32_t)p, (uint32_t)gid[j], step, 0u};
+      /* one Philox block per particle pair (R9): counter (p/2, gid, step, 0);
+       * the even particle takes normals (n0, n1), the odd one (n2, n3) */
+      uint32_t ctr[4] = {(uint32_t)p / 2u, (uint32_t)gid[j], step, 0u};
       double n[4];
       oracle_normals4(seed, ctr, n);
+      double na = (p % 2 == 0) ? n[0] : n[2];
+      double nw = (p % 2 == 0) ? n[1] : n[3];
       double s[5] = {x[e], y[e], v[e], psi[e], omega[e]}, o[5];
-      oracle_ctrv(s, (double)dt, (double)sigma_a * n[0], (double)sigma_w * n[1], o);
+      oracle_ctrv(s, (double)dt, (double)sigma_a * na, (double)sigma_w * nw, o);
       ox[e] = o[0]; oy[e] = o[1]; ov[e] = o[2]; opsi[e] = o[3]; oomega[e] = o[4];
     }
   }

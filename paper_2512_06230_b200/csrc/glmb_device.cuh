@@ -37,14 +37,16 @@ __device__ __forceinline__ float uniform24(uint32_t r) {
 }
 
 // Box-Muller pair from two raw words: rho = sqrt(-2 ln ua), (rho cos 2pi ub, rho sin 2pi ub).
-// Accurate libdevice logf / sqrtf / sincospif (predict and birth are HBM-bound).
+// logf / sqrtf are the accurate libdevice versions (ln ua near 1 needs them);
+// the angle goes to MUFU sin/cos as 2 pi ub - pi in (-pi, pi) (abs. error ~2^-21,
+// i.e. < 3e-6 on n) with cos(t + pi) = -cos t, sin(t + pi) = -sin t.
 __device__ __forceinline__ void box_muller(uint32_t ra, uint32_t rb, float &n0, float &n1) {
   const float ua = uniform24(ra), ub = uniform24(rb);
   const float rho = sqrtf(-2.0f * logf(ua));
   float s, c;
-  sincospif(2.0f * ub, &s, &c);
-  n0 = rho * c;
-  n1 = rho * s;
+  __sincosf(fmaf(6.28318530717958647692f, ub, -3.14159265358979323846f), &s, &c);
+  n0 = -rho * c;
+  n1 = -rho * s;
 }
 
 // wrap(a) = a - 2 pi ceil((a - pi) / 2 pi)  -> (-pi, pi]

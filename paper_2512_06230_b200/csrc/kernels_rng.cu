@@ -3,7 +3,8 @@
 // Both passes are HBM-bound streams over SoA fp32 particle arrays: each
 // thread owns 4 consecutive particles of one track (one 128-bit load / store
 // per array), draws their process noise from Philox4x32-10 keyed by
-// (seed; p, gid, step, tag) and writes the result.  Grid: grid-stride over
+// (seed; counter, gid, step, tag) and writes the result.  Predict uses one
+// Philox block per particle pair (counter p >> 1, words (0,1) / (2,3)).  Grid: grid-stride over
 // the T*P/4 particle quads with 256-thread blocks, sized to 148 SMs x 8.
 #include "glmb_device.cuh"
 #include "glmb_internal.h"
@@ -32,11 +33,16 @@ __global__ void __launch_bounds__(kThreads) predict_kernel(const PredictArgs a) 
     float4 X = ld_stream(a.x + e), Y = ld_stream(a.y + e), V = ld_stream(a.v + e);
     float4 PS = ld_stream(a.psi + e), OM = ld_stream(a.omega + e);
     const uint32_t gid = static_cast<uint32_t>(__ldg(a.gid + j));
+    // one Philox block per particle pair: counter (p >> 1, gid, step, 0);
+    // words (0,1) drive the even particle, words (2,3) the odd one
+    const u32x4 r01 = philox4x32_10(u32x4{static_cast<uint32_t>(p0 >> 1), gid, a.step, 0u}, a.key0, a.key1);
+    const u32x4 r23 = philox4x32_10(u32x4{static_cast<uint32_t>((p0 >> 1) + 1), gid, a.step, 0u}, a.key0, a.key1);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const u32x4 r = philox4x32_10(u32x4{static_cast<uint32_t>(p0 + q), gid, a.step, 0u}, a.key0, a.key1);
+      const u32x4 &r = q < 2 ? r01 : r23;
       float n0, n1;
-      box_muller(r.a, r.b, n0, n1);
+      if (q & 1) box_muller(r.c, r.d, n0, n1);
+      else box_muller(r.a, r.b, n0, n1);
       const float nu_a = a.sigma_a * n0, nu_w = a.sigma_w * n1;
       const float x = at(X, q), y = at(Y, q), v = at(V, q), psi = at(PS, q), om = at(OM, q);
       const float h = om * half_dt;

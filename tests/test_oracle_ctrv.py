@@ -94,7 +94,8 @@ def test_wrap(orc):
 
 
 def test_predict_uses_keyed_philox_noise(orc):
-    """predict(j,p) == ctrv(state, dt, sigma_a n0, sigma_w n1) with n from counter (p, gid, step, 0)."""
+    """predict(j,p) == ctrv(state, dt, sigma_a n_a, sigma_w n_w) with (n_a, n_w) = normals (0,1)
+    (p even) or (2,3) (p odd) of the block with counter (p // 2, gid, step, 0)."""
     T, P = 3, 8
     r = np.random.default_rng(0)
     st = [r.uniform(0, 50, (T, P)).astype(np.float32) for _ in range(2)] + [
@@ -104,10 +105,11 @@ def test_predict_uses_keyed_philox_noise(orc):
     out = orc.predict(*st, gid, 0.1, 1.0, 0.1, seed=99, step=4)
     for j in range(T):
         for p in range(P):
-            n = orc.normals4(99, [p, gid[j], 4, 0])
+            n = orc.normals4(99, [p // 2, gid[j], 4, 0])
+            na, nw = (n[0], n[1]) if p % 2 == 0 else (n[2], n[3])
             s = [float(a[j, p]) for a in st]
-            ref = orc.ctrv(s, float(np.float32(0.1)), float(np.float32(1.0)) * n[0],
-                           float(np.float32(0.1)) * n[1])
+            ref = orc.ctrv(s, float(np.float32(0.1)), float(np.float32(1.0)) * na,
+                           float(np.float32(0.1)) * nw)
             np.testing.assert_array_equal([o[j, p] for o in out], ref)
 
 
