@@ -31,7 +31,12 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "particle-measurement likelihood evals/s (GLMB step: predict+birth+compat+reweight)"
-SFU_EX2_PER_CLK_PER_SM = 16          # MUFU.EX2 lanes/clk/SM on sm_100
+SFU_EX2_PER_CLK_PER_SM = 16          # MUFU.EX2 lanes/clk/SM on sm_100 (measured: glmb_peaks)
+FMA_LANES_PER_CLK_PER_SM = 128       # FP32 FMA lanes/clk/SM (FFMA or FFMA2 x 2), measured: glmb_peaks
+# compat, per pair: 4 FMA-pipe ops + one exp; an exp moved to the FMA pipe costs 8 FMA-pipe ops.
+# Best split f of exps on the FMA pipe: x(1-f) = E, x(4+8f) = F  ->  x = (F + 8E) / 12 pairs/clk/SM.
+COMPAT_PAIRS_PER_CLK_PER_SM = (FMA_LANES_PER_CLK_PER_SM + 8 * SFU_EX2_PER_CLK_PER_SM) / 12.0
+HBM_PEAK_GBPS_FALLBACK = 6556.5      # MEASURED_PEAKS.json hbm_gbs (read at run time when present)
 
 
 def parse():
@@ -111,41 +116,55 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU oracle legs
-def oracle_sample(cfg_id: int, seconds: float, cores: int):
-    """Time the fp64 oracle (as it stands) on a bounded sample of the workload:
-    the first n tracks of the config -- predict, compat over all M, reweight --
-    with OpenMP over tracks.  n is calibrated so the run takes ~`seconds`."""
-    import oracle
-    from paper_2512_06230_b200.scenes import make_scene
-    oracle.set_num_threads(cores)
-    base = make_scene(cfg_id, rows=range(0), steps=1)
-    c = base.cfg
-    Z, th = base.Z[0], base.theta[0]
+class OracleSample:
+    """The fp64 oracle (as it stands) on a bounded sample of the workload: the
+    first n tracks of the config -- predict, compat over all M, reweight -- with
+    OpenMP over tracks.  n is calibrated once so one run takes ~`seconds`."""
 
-    def run(n):
-        s = make_scene(cfg_id, rows=range(n), steps=1)
+    def __init__(self, cfg_id: int, seconds: float, cores: int):
+        import oracle
+        from paper_2512_06230_b200.scenes import make_scene
+        self.oracle, self.make_scene = oracle, make_scene
+        oracle.set_num_threads(cores)
+        self.cfg_id, self.cores = cfg_id, cores
+        base = make_scene(cfg_id, rows=range(0), steps=1)
+        self.c = base.cfg
+        self.Z, self.th = base.Z[0], base.theta[0]
+        n0 = max(1, min(self.c.T, cores))
+        t0, _ = self.run(n0)
+        n = int(min(self.c.T, max(n0, n0 * seconds / max(t0, 1e-3))))
+        self.n = max(n0, (n // n0) * n0)
+
+    def run(self, n: int = None):
+        n = self.n if n is None else n
+        c, o = self.c, self.oracle
+        s = self.make_scene(self.cfg_id, rows=range(n), steps=1)
         t0 = time.perf_counter()
-        px, py, pv, pp, po = oracle.predict(s.x, s.y, s.v, s.psi, s.omega, s.gid, c.dt, c.sigma_a,
-                                            c.sigma_w, c.seed, 0)
+        px, py, _, _, _ = o.predict(s.x, s.y, s.v, s.psi, s.omega, s.gid, c.dt, c.sigma_a,
+                                    c.sigma_w, c.seed, 0)
         x32, y32 = px.astype(np.float32), py.astype(np.float32)
-        oracle.compat(x32, y32, s.w, Z, c.R, c.p_d, c.kappa, c.gamma)
-        oracle.reweight(x32, y32, s.w, Z, c.R, th, 0)
+        o.compat(x32, y32, s.w, self.Z, c.R, c.p_d, c.kappa, c.gamma)
+        o.reweight(x32, y32, s.w, self.Z, c.R, self.th, 0)
         dt = time.perf_counter() - t0
-        n_assigned = int(((th >= 1) & (th <= n)).sum())
-        return dt, len(Z) * n * c.P + c.P * n_assigned
+        n_assigned = int(((self.th >= 1) & (self.th <= n)).sum())
+        return dt, len(self.Z) * n * c.P + c.P * n_assigned
 
-    n0 = max(1, min(c.T, cores))
-    t0, _ = run(n0)
-    n = int(min(c.T, max(n0, n0 * seconds / max(t0, 1e-3))))
-    n = max(n0, (n // n0) * n0)
-    dt, evals = run(n)
+    def describe(self, dt):
+        c = self.c
+        return (f"cfg{self.cfg_id}: first {self.n} of {c.T + c.B} tracks x all M={len(self.Z)} x "
+                f"P={c.P} (predict+compat+reweight, fp64, OpenMP over tracks), {dt:.2f} s")
+
+
+def oracle_sample(cfg_id: int, seconds: float, cores: int):
+    smp = OracleSample(cfg_id, seconds, cores)
+    dt, evals = smp.run()
     return {"value": evals / dt, "unit": "evals/s", "cores": cores, "kind": "oracle",
-            "sample": f"cfg{cfg_id}: first {n} of {c.T + c.B} tracks x all M={len(Z)} x P={c.P} "
-                      f"(predict+compat+reweight, fp64, OpenMP over tracks), {dt:.2f} s",
-            "seconds": dt, "evals": evals}
+            "sample": smp.describe(dt)}
 
 
 def reference_arm(a, cfg_id):
+    """--impl reference: this tier's reference is the fp64 oracle (there is no reference
+    implementation, only the paper).  Rank 0 alone runs it; other ranks exit 0."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
@@ -155,24 +174,26 @@ def reference_arm(a, cfg_id):
     c = full.cfg
     th = full.theta[0]
     full_evals = len(full.Z[0]) * (c.T + c.B) * c.P + c.P * int((th != 0).sum())
-    per_step = max(2.0, 120.0 / max(1, a.steps + a.warmup))
+    per_step = min(20.0, max(1.0, 150.0 / max(1, a.steps + a.warmup)))
+    smp = OracleSample(cfg_id, per_step, cores)
     times, evals = [], []
     for k in range(a.warmup + a.steps):
-        r = oracle_sample(cfg_id, per_step, cores)
+        dt, ev = smp.run()
         if k >= a.warmup:
-            times.append(r["seconds"])
-            evals.append(r["evals"])
+            times.append(dt)
+            evals.append(ev)
     value = sum(evals) / sum(times)
     ms = full_evals / value * 1e3
+    sample = smp.describe(statistics.mean(times)) + " per step"
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s",
             "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"cfg{cfg_id}", "T": c.T, "B": c.B, "P": c.P,
-                       "M": len(full.Z[0]), "note": "oracle on a bounded sample per step; "
+            "config": {"workload": f"cfg{cfg_id} ({c.name})", "T": c.T, "B": c.B, "P": c.P,
+                       "M": len(full.Z[0]), "note": "fp64 CPU oracle on a bounded sample per step; "
                        "ms_per_step extrapolated to the full step at the sampled rate"},
             "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "oracle",
-                             "sample": r["sample"]},
+                             "sample": sample},
             "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -337,11 +358,13 @@ def main():
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (compat): SFU-bound, one MUFU.EX2 per pair
+    # ---- roofline of the dominant kernel (compat): exp-throughput bound (MUFU.EX2 + the
+    # FMA-pipe polynomial share), DESIGN.md "compat roofline"
     sm_count = L.glmb_sm_count(local)
     clocks = sampler.summary()
     f_max = (clocks["sm_max_mhz"] or 1965.0) * 1e6
-    peak = sm_count * SFU_EX2_PER_CLK_PER_SM * f_max
+    peak = sm_count * COMPAT_PAIRS_PER_CLK_PER_SM * f_max
+    peak_sfu = sm_count * SFU_EX2_PER_CLK_PER_SM * f_max
     compat_ms = statistics.mean(stage_ms["compat"])
     pairs_per_launch = pairs_local / a.steps
     achieved = pairs_per_launch / (compat_ms * 1e-3)
@@ -371,18 +394,24 @@ def main():
                    "M_mean": float(np.mean(Ms)), "parallelism": f"tracks sharded x{world}",
                    "l2": "particle state 24 B x T_k x P > 126 MB L2 streams from HBM every step",
                    "evals_per_step": evals_total / a.steps},
-        "roofline": {"bound": "alu", "kernel": "compat (MUFU.EX2 SFU pipe)",
+        "roofline": {"bound": "alu", "kernel": "compat (exp: MUFU.EX2 + FMA-pipe polynomial)",
                      "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Geval/s",
                      "frac": achieved / peak,
-                     "peak_basis": f"{sm_count} SM x {SFU_EX2_PER_CLK_PER_SM} ex2/clk x "
-                                   f"{f_max / 1e6:.0f} MHz (max SM clock)",
-                     "frac_at_measured_clock": (achieved / (sm_count * SFU_EX2_PER_CLK_PER_SM *
+                     "peak_basis": f"{sm_count} SM x {COMPAT_PAIRS_PER_CLK_PER_SM:.2f} pairs/clk "
+                                   f"(16 ex2/clk + 128 FMA lanes/clk, measured) x {f_max / 1e6:.0f} MHz",
+                     "frac_of_mufu_only_bound": achieved / peak_sfu,
+                     "frac_at_measured_clock": (achieved / (sm_count * COMPAT_PAIRS_PER_CLK_PER_SM *
                                                             clocks["sm_mhz"] * 1e6)
                                                 if clocks["sm_mhz"] else None),
-                     "traffic": None},
+                     "traffic": compat_traffic(st, scene)},
+        "hbm_kernels": {
+            "predict": {"bound": "hbm", "bytes_per_launch": predict_bytes,
+                        "achieved_GBps": predict_bytes / (stage_mean["predict"] * 1e-3) / 1e9,
+                        "peak_GBps": hbm_peak(), "frac": predict_bytes / (stage_mean["predict"] * 1e-3) / 1e9 / hbm_peak()},
+            "reweight": {"bound": "hbm", "bytes_per_launch": reweight_bytes,
+                         "achieved_GBps": reweight_bytes / (stage_mean["reweight"] * 1e-3) / 1e9,
+                         "peak_GBps": hbm_peak(), "frac": reweight_bytes / (stage_mean["reweight"] * 1e-3) / 1e9 / hbm_peak()}},
         "stages_ms": stage_mean,
-        "hbm": {"predict_GBps": predict_bytes / (stage_mean["predict"] * 1e-3) / 1e9,
-                "reweight_GBps": reweight_bytes / (stage_mean["reweight"] * 1e-3) / 1e9},
         "gpu_launches": launches_per_step * a.steps,
         "clocks": clocks,
         "e2e": e2e,
