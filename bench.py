@@ -199,6 +199,80 @@ def reference_arm(a, cfg_id):
     print(json.dumps(line), flush=True)
 
 
+def hbm_peak() -> float:
+    """MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth), else the fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except Exception:  # noqa: BLE001
+        return HBM_PEAK_GBPS_FALLBACK
+
+
+def compat_traffic(T: int, P: int, M: int):
+    """DRAM bytes per compat launch for this workload from the committed
+    ncu --set full capture (profiles/compat_traffic.json), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "compat_traffic.json")) as f:
+            return json.load(f).get(f"T{T}_P{P}_M{M}")
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def make_line(*, cfg_id, cfg, world, steps, warmup, elapsed_ms, evals_total, pairs_per_launch,
+              stage_ms, sm_count, clocks, T_surv, B_local, T_local, P, M_mean, traffic, e2e, cpu):
+    """The one JSON line of the GPU arm (pure function of the measurements)."""
+    f_max = (clocks.get("sm_max_mhz") or 1965.0) * 1e6
+    peak = sm_count * COMPAT_PAIRS_PER_CLK_PER_SM * f_max
+    peak_sfu = sm_count * SFU_EX2_PER_CLK_PER_SM * f_max
+    stage_mean = {n: statistics.mean(v) for n, v in stage_ms.items()}
+    achieved = pairs_per_launch / (stage_mean["compat"] * 1e-3)
+    hbm = hbm_peak()
+
+    def hbm_kernel(name, nbytes):
+        gbps = nbytes / (stage_mean[name] * 1e-3) / 1e9 if stage_mean[name] > 0 else 0.0
+        return {"bound": "hbm", "bytes_per_launch": nbytes, "achieved_GBps": gbps,
+                "peak_GBps": hbm, "frac": gbps / hbm}
+
+    sm_mhz = clocks.get("sm_mhz")
+    return {
+        "metric": METRIC,
+        "value": evals_total / (elapsed_ms * 1e-3),
+        "unit": "evals/s",
+        "n_gpus": world,
+        "steps": steps,
+        "warmup": warmup,
+        "ms_per_step": elapsed_ms / steps,
+        "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": f"cfg{cfg_id} ({cfg.name})", "T": cfg.T, "B": cfg.B, "P": cfg.P,
+                   "M_mean": M_mean, "parallelism": f"tracks sharded x{world}",
+                   "l2": "inputs larger than L2: particle state 24 B x T_k x P (204 MB at cfg3) "
+                         "streams from HBM every step",
+                   "evals_per_step": evals_total / steps},
+        "roofline": {"bound": "alu", "kernel": "compat (exp: MUFU.EX2 + FMA-pipe polynomial)",
+                     "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Geval/s",
+                     "frac": achieved / peak,
+                     "peak_basis": f"{sm_count} SM x {COMPAT_PAIRS_PER_CLK_PER_SM:.2f} pairs/clk "
+                                   f"(16 ex2/clk + 128 FMA lanes/clk, measured) x {f_max / 1e6:.0f} MHz",
+                     "frac_of_mufu_only_bound": achieved / peak_sfu,
+                     "frac_at_measured_clock": (achieved / (sm_count * COMPAT_PAIRS_PER_CLK_PER_SM * sm_mhz * 1e6)
+                                                if sm_mhz else None),
+                     "traffic": traffic},
+        "hbm_kernels": {"predict": hbm_kernel("predict", T_surv * P * 40),
+                        "birth": hbm_kernel("birth", B_local * P * 24),
+                        "reweight": hbm_kernel("reweight", T_local * P * 16)},
+        "stages_ms": stage_mean,
+        "gpu_launches": ((1 if T_surv else 0) + (1 if B_local else 0) + 2) * steps,
+        "clocks": clocks,
+        "e2e": e2e,
+        "cpu_baseline": None if cpu is None else
+        {k: v for k, v in cpu.items() if k in ("value", "unit", "cores", "kind", "sample")},
+    }
+
+
 # ------------------------------------------------------------------ GPU arm
 def main():
     a = parse()
@@ -358,65 +432,16 @@ def main():
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (compat): exp-throughput bound (MUFU.EX2 + the
-    # FMA-pipe polynomial share), DESIGN.md "compat roofline"
-    sm_count = L.glmb_sm_count(local)
-    clocks = sampler.summary()
-    f_max = (clocks["sm_max_mhz"] or 1965.0) * 1e6
-    peak = sm_count * COMPAT_PAIRS_PER_CLK_PER_SM * f_max
-    peak_sfu = sm_count * SFU_EX2_PER_CLK_PER_SM * f_max
-    compat_ms = statistics.mean(stage_ms["compat"])
-    pairs_per_launch = pairs_local / a.steps
-    achieved = pairs_per_launch / (compat_ms * 1e-3)
-    stage_mean = {n: statistics.mean(v) for n, v in stage_ms.items()}
-    predict_bytes = st.T_surv * st.P * 40
-    reweight_bytes = st.T_local * st.P * 16
-    launches_per_step = (1 if st.T_surv else 0) + (1 if st.B_local else 0) + 1 + 1
     cpu = None
     if world == 1 and not a.no_cpu_baseline:
         cpu = oracle_sample(cfg_id, a.cpu_seconds, host_cores())
-        cpu = {k: v for k, v in cpu.items() if k in ("value", "unit", "cores", "kind", "sample")}
     Ms = [len(scene.Z[k % len(scene.Z)]) for k in range(a.warmup, a.warmup + a.steps)]
-    line = {
-        "metric": METRIC,
-        "value": evals_total / (elapsed_ms * 1e-3),
-        "unit": "evals/s",
-        "n_gpus": world,
-        "steps": a.steps,
-        "warmup": a.warmup,
-        "ms_per_step": elapsed_ms / a.steps,
-        "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "weak",
-        "vs_baseline": None,
-        "dtype": "f32",
-        "data": "synthetic",
-        "config": {"workload": f"cfg{cfg_id} ({cfg.name})", "T": cfg.T, "B": cfg.B, "P": cfg.P,
-                   "M_mean": float(np.mean(Ms)), "parallelism": f"tracks sharded x{world}",
-                   "l2": "particle state 24 B x T_k x P > 126 MB L2 streams from HBM every step",
-                   "evals_per_step": evals_total / a.steps},
-        "roofline": {"bound": "alu", "kernel": "compat (exp: MUFU.EX2 + FMA-pipe polynomial)",
-                     "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Geval/s",
-                     "frac": achieved / peak,
-                     "peak_basis": f"{sm_count} SM x {COMPAT_PAIRS_PER_CLK_PER_SM:.2f} pairs/clk "
-                                   f"(16 ex2/clk + 128 FMA lanes/clk, measured) x {f_max / 1e6:.0f} MHz",
-                     "frac_of_mufu_only_bound": achieved / peak_sfu,
-                     "frac_at_measured_clock": (achieved / (sm_count * COMPAT_PAIRS_PER_CLK_PER_SM *
-                                                            clocks["sm_mhz"] * 1e6)
-                                                if clocks["sm_mhz"] else None),
-                     "traffic": compat_traffic(st, scene)},
-        "hbm_kernels": {
-            "predict": {"bound": "hbm", "bytes_per_launch": predict_bytes,
-                        "achieved_GBps": predict_bytes / (stage_mean["predict"] * 1e-3) / 1e9,
-                        "peak_GBps": hbm_peak(), "frac": predict_bytes / (stage_mean["predict"] * 1e-3) / 1e9 / hbm_peak()},
-            "reweight": {"bound": "hbm", "bytes_per_launch": reweight_bytes,
-                         "achieved_GBps": reweight_bytes / (stage_mean["reweight"] * 1e-3) / 1e9,
-                         "peak_GBps": hbm_peak(), "frac": reweight_bytes / (stage_mean["reweight"] * 1e-3) / 1e9 / hbm_peak()}},
-        "stages_ms": stage_mean,
-        "gpu_launches": launches_per_step * a.steps,
-        "clocks": clocks,
-        "e2e": e2e,
-        "cpu_baseline": cpu,
-    }
+    line = make_line(
+        cfg_id=cfg_id, cfg=cfg, world=world, steps=a.steps, warmup=a.warmup,
+        elapsed_ms=elapsed_ms, evals_total=evals_total, pairs_per_launch=pairs_local / a.steps,
+        stage_ms=stage_ms, sm_count=L.glmb_sm_count(local), clocks=sampler.summary(),
+        T_surv=st.T_surv, B_local=st.B_local, T_local=st.T_local, P=st.P, M_mean=float(np.mean(Ms)),
+        traffic=compat_traffic(st.T_local, st.P, len(scene.Z[0])), e2e=e2e, cpu=cpu)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -1,0 +1,48 @@
+"""CPU checks of bench.py's host logic: the JSON line contract and the reference arm."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def test_make_line_contract():
+    import bench
+    from paper_2512_06230_b200.scenes import CONFIGS
+    line = bench.make_line(
+        cfg_id=3, cfg=CONFIGS[3], world=1, steps=4, warmup=3, elapsed_ms=10.0, evals_total=4.0e10,
+        pairs_per_launch=1.0e10, stage_ms={"predict": [0.06] * 4, "birth": [0.01] * 4,
+                                           "compat": [2.4] * 4, "reweight": [0.08] * 4},
+        sm_count=148, clocks={"sm_mhz": 1965.0, "sm_max_mhz": 1965.0, "reasons": []},
+        T_surv=1024, B_local=16, T_local=1040, P=8192, M_mean=1198.0, traffic=None,
+        e2e={"value": 1.0, "unit": "evals/s", "h2d_bytes_per_step": 1, "d2h_bytes_per_step": 1},
+        cpu={"value": 1.0, "unit": "evals/s", "cores": 8, "kind": "oracle", "sample": "x", "seconds": 1})
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
+                "gpu_launches", "clocks"):
+        assert key in line
+    assert line["value"] == pytest.approx(4.0e12)
+    assert line["ms_per_step"] == pytest.approx(2.5)
+    r = line["roofline"]
+    assert r["bound"] == "alu" and 0 < r["frac"] < 1 and r["frac"] == pytest.approx(r["achieved"] / r["peak"])
+    assert r["peak"] == pytest.approx(148 * (128 + 8 * 16) / 12 * 1.965e9 / 1e9)
+    assert line["gpu_launches"] == 16
+    assert line["cpu_baseline"]["cores"] == 8 and "seconds" not in line["cpu_baseline"]
+    assert "workload" in line["config"]
+    json.dumps(line)
+
+
+@pytest.mark.slow
+def test_reference_arm_runs_on_cpu():
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                          "--steps", "1", "--warmup", "0", "--config", "0"],
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "oracle"
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
