@@ -161,6 +161,8 @@ glmb_status glmb_birth(const glmb_particles *out, const int32_t *gid,
  * Results are bit-identical for any n_tracks split (sharding) and any row
  * permutation of Z (each entry is computed independently, in a fixed
  * particle order).
+ * Precondition for the 1e-4 fp32 contract: weights in [0, 1]
+ * (P:21's particle weights); terms below 2^-126 flush to zero.
  * Errors: INVALID_ARG if R is not SPD, p_d not in (0,1], kappa < 0,
  * gamma < 1e-30 (the fp32 exactness precondition), ldc < M,
  * ldg < ceil(M/32), or NULL outputs with T > 0 and M > 0.

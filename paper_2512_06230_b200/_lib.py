@@ -15,7 +15,7 @@ import threading
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libglmb.so")
+LIB_PATH = os.environ.get("GLMB_LIB", os.path.join(_HERE, "libglmb.so"))  # override: A/B runs only
 
 GLMB_OK = 0
 _lock = threading.Lock()

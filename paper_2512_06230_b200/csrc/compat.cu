@@ -14,27 +14,29 @@
 //    one thread in a fixed particle order -- no cross-thread reduction, and C
 //    is bit-identical for any sharding of the tracks and any permutation of
 //    Z's rows.  Warps past M skip the arithmetic; the ragged last measurement
-//    tiles are scheduled last (unit = mt*T + j) to fill the tail.
+//    tiles are scheduled last (unit = mt*T + j) to fill the tail.  K = 2 and
+//    40 registers give 16 resident CTAs (64 warps) per SM.
 //  * The track's particles stream through shared memory in tiles of kTileP,
-//    moved by the TMA bulk-copy engine (cp.async.bulk + mbarrier ring of raw
-//    x, y, w) and reused by all 128*K measurements of the CTA.
+//    moved by the TMA bulk-copy engine (cp.async.bulk + mbarrier) and reused
+//    by all 128*K measurements of the CTA; one tile of arithmetic (~50 us per
+//    CTA) hides the next tile's copy, so a single raw stage suffices.
 //  * Whitening: with U' the scaled Cholesky factor of R^-1,
 //    1/2 log2(e) d^T R^-1 d = |U'(z - c) - U'(p - c)|^2 for any SPD R, where c
 //    is the mean of the track's first tile (so p - c and z - c are exact or
-//    tiny for every relevant pair even at 4 km coordinates).  Each raw tile is
-//    whitened once into an AoS float4 tile (X', Y', CP = -|p'|^2, w), double
-//    buffered so one __syncthreads per tile suffices.
+//    small even at 4 km coordinates).  Each raw tile is whitened once into an
+//    AoS float4 tile (X', Y', -, w), double buffered so one __syncthreads per
+//    tile suffices.
 //  * Inner loop: one LDS.128 per particle; the thread's measurements are
 //    packed in pairs (fp32x2), the particle's values are scalar operands that
-//    FFMA2/FADD2 broadcast:
-//      e = 2z'x * X' + (2z'y * Y' + CP) - |z'|^2  = -|z' - p'|^2
-//      acc += w * 2^e
-//    = 3 packed FP ops + 2 exp + 1 packed FMA per two pairs.  Optionally one
-//    particle in EMU_PERIOD evaluates 2^e on the FMA pipe instead of MUFU
-//    (round-to-nearest range reduction with the 1.5*2^23 trick, degree-5
-//    minimax polynomial, rel. error 2.4e-7 ~ MUFU's, exponent added with one
-//    LEA) to balance the MUFU and FMA pipes.
-//    The choice is by particle index, so every measurement sees the same mix.
+//    FFMA2 broadcasts: dx, dy = z' - p' exactly as in the definition (no
+//    |z|^2 - 2z.p + |p|^2 expansion, whose cancellation grows with the cloud
+//    width), q = dx^2 + dy^2, acc += w 2^-q.  One particle in 12 evaluates its
+//    exps on the FMA pipe instead of MUFU (round-to-nearest range reduction
+//    with the 1.5*2^23 trick, degree-5 minimax polynomial, rel. error 2.4e-7
+//    ~ MUFU's, exponent added with an integer shift-add, scaled by 2^64 so
+//    tiny results flush to zero like MUFU.EX2.FTZ), which offloads the MUFU
+//    pipe.  The choice is by particle index, so
+//    every measurement sees the same arithmetic (row-permutation bit-exact).
 //  * Two-level summation (per tile, then across tiles) keeps the fp32 sum
 //    error ~kTileP*eps instead of P*eps.
 //  * Epilogue: L = norm*sum, gate bit via __ballot_sync (32 consecutive
@@ -50,25 +52,31 @@ namespace {
 constexpr int kWarps = 4;
 constexpr int kThreads = 32 * kWarps;
 constexpr int kTileM = 32 * kWarps;  // measurements per tile per K
-constexpr int kTileP = 512;          // particles per shared-memory tile (fixed: sets the sum order)
-constexpr int kStages = 2;           // TMA ring depth of raw tiles (x, y, w)
-constexpr int kMaxK = 4;
+constexpr int kTileP = 256;          // particles per shared-memory tile (fixed: sets the sum order)
+constexpr int kStages = 1;           // raw tiles (x, y, w) in flight: one tile of compute (~50 us) hides a TMA
+constexpr int kMaxK = 8;
+// resident CTAs per SM the register allocation must allow (4 warps each)
+template <int K>
+constexpr int min_blocks() { return K <= 2 ? 12 : 8; }
 constexpr int kRawFloats = 3 * kTileP;
 constexpr int kSmemBytes = kStages * kRawFloats * 4 + 2 * kTileP * 16;  // raw ring + 2 AoS tiles
 
 // degree-5 minimax fit of 2^f on [-1/2, 1/2] (max rel. error 7.5e-8, 2.3e-7 in fp32 Horner)
 constexpr float kC0 = 1.0000001192092896f, kC1 = 0.6931469440460205f, kC2 = 0.24022120237350464f,
                 kC3 = 0.05550713092088699f, kC4 = 0.009675533510744572f, kC5 = 0.0013276446843519807f;
-constexpr float kRound = 12582912.0f;  // 1.5 * 2^23: x + kRound rounds x to an integer
+constexpr float kRound64 = 12582976.0f;  // 1.5 * 2^23 + 64: x + kRound64 = round(x) + 64 in the low bits
+constexpr float kTwoM64 = 5.42101086242752217e-20f;  // 2^-64
 
-// 2^e for a packed pair on the FMA + ALU pipes (no MUFU).  e <= 0 expected;
-// e < -125 is clamped (result < 2^-125 * 1.42 vs MUFU's flush to 0).
-__device__ __forceinline__ f2 exp2_poly2(f2 e) {
-  float e0, e1;
-  f2_unpack(e, e0, e1);
-  e = f2_pack(fmaxf(e0, -125.0f), fmaxf(e1, -125.0f));
-  const f2 rnd = f2_pack(kRound, kRound);
-  const f2 t = f2_add(e, rnd);             // t = kRound + round(e)
+// 2^-q for a packed pair on the FMA + ALU pipes (no MUFU), returned scaled by
+// 2^64 (the caller folds 2^-64 into the weight, so results below 2^-126 flush
+// to zero exactly as MUFU.EX2.FTZ does).  q >= 0 is clamped at 189 so the
+// integer exponent 64 - round(q) >= -125 stays a valid float exponent.
+__device__ __forceinline__ f2 exp2_poly2_x64_neg(f2 q) {
+  float q0, q1;
+  f2_unpack(q, q0, q1);
+  const f2 e = f2_pack(-fminf(q0, 189.0f), -fminf(q1, 189.0f));
+  const f2 rnd = f2_pack(kRound64, kRound64);
+  const f2 t = f2_add(e, rnd);             // low mantissa bits of t = round(e) + 64
   const f2 f = f2_sub(e, f2_sub(t, rnd));  // f = e - round(e) in [-1/2, 1/2]
   f2 p = f2_fma(f2_pack(kC5, kC5), f, f2_pack(kC4, kC4));
   p = f2_fma(p, f, f2_pack(kC3, kC3));
@@ -78,16 +86,17 @@ __device__ __forceinline__ f2 exp2_poly2(f2 e) {
   float p0, p1, t0, t1;
   f2_unpack(p, p0, p1);
   f2_unpack(t, t0, t1);
-  // low mantissa bits of t hold round(e); << 23 moves them into the exponent field
+  // << 23 moves round(e) + 64 into the exponent field of p in [2^-1/2, 2^1/2]
   p0 = __uint_as_float(__float_as_uint(p0) + (__float_as_uint(t0) << 23));
   p1 = __uint_as_float(__float_as_uint(p1) + (__float_as_uint(t1) << 23));
   return f2_pack(p0, p1);
 }
 
-__device__ __forceinline__ f2 exp2_mufu2(f2 e) {
-  float e0, e1;
-  f2_unpack(e, e0, e1);
-  return f2_pack(ex2_approx(e0), ex2_approx(e1));
+// 2^-q on MUFU.EX2 (the negation is an operand modifier)
+__device__ __forceinline__ f2 exp2_mufu2_neg(f2 q) {
+  float q0, q1;
+  f2_unpack(q, q0, q1);
+  return f2_pack(ex2_approx(-q0), ex2_approx(-q1));
 }
 
 __device__ __forceinline__ void issue_tile(const CompatArgs &a, const float *xs, const float *ys, const float *ws,
@@ -105,23 +114,33 @@ __device__ __forceinline__ void issue_tile(const CompatArgs &a, const float *xs,
 template <int K>
 struct Meas {
   static constexpr int H = (K + 1) / 2;
-  f2 zx2[H], zy2[H], nzz[H];  // 2 z'x, 2 z'y, -|z'|^2
+  f2 zx2[H], zy2[H];         // 2 z'x, 2 z'y
   float tot[2 * H];          // running sums per measurement slot
 };
 
 // One particle against the thread's HV measurement pairs.  POLY_MASK bit h:
 // pair h takes 2^e from the FMA-pipe polynomial instead of MUFU.
+// AoS entry p = (X', Y', -, w).  e = -|z' - p'|^2 from the exact difference
+// (z' = zx2 / 2 exactly): dx, dy by FFMA2, q by FMUL2 + FFMA2; the sign of -q is
+// an operand modifier of MUFU / the polynomial's adds.
 template <int H, int POLY_MASK>
 __device__ __forceinline__ void particle_step(const float4 p, const f2 (&zx2)[H], const f2 (&zy2)[H],
-                                              const f2 (&nzz)[H], f2 (&acc)[H], int hv) {
-  const f2 px = f2_pack(p.x, p.x), py = f2_pack(p.y, p.y), cp = f2_pack(p.z, p.z), pw = f2_pack(p.w, p.w);
+                                              f2 (&acc)[H], int hv) {
+  const f2 pw = f2_pack(p.w, p.w);
+  const f2 half = f2_pack(0.5f, 0.5f);
+  const f2 npx = f2_pack(-p.x, -p.x), npy = f2_pack(-p.y, -p.y);
 #pragma unroll
   for (int h = 0; h < H; ++h) {
     if (h < hv) {
-      f2 e = f2_fma(zy2[h], py, cp);
-      e = f2_fma(zx2[h], px, e);
-      e = f2_add(e, nzz[h]);
-      acc[h] = f2_fma(pw, ((POLY_MASK >> h) & 1) ? exp2_poly2(e) : exp2_mufu2(e), acc[h]);
+      const f2 dx = f2_fma(zx2[h], half, npx);  // z'x - p'x
+      const f2 dy = f2_fma(zy2[h], half, npy);
+      const f2 q = f2_fma(dy, dy, f2_mul(dx, dx));
+      if ((POLY_MASK >> h) & 1) {
+        const f2 pw64 = f2_pack(p.w * kTwoM64, p.w * kTwoM64);
+        acc[h] = f2_fma(pw64, exp2_poly2_x64_neg(q), acc[h]);
+      } else {
+        acc[h] = f2_fma(pw, exp2_mufu2_neg(q), acc[h]);
+      }
     }
   }
 }
@@ -143,11 +162,11 @@ constexpr int poly_mask(int u) {
 
 template <int H, int EMU_PERIOD, int U = 0>
 __device__ __forceinline__ void step_u(int u, const float4 p, const f2 (&zx2)[H], const f2 (&zy2)[H],
-                                       const f2 (&nzz)[H], f2 (&acc)[H], int hv) {
+                                       f2 (&acc)[H], int hv) {
   // u is a compile-time constant after unrolling; recurse to turn it into a template argument
   if constexpr (U < (EMU_PERIOD > 0 ? EMU_PERIOD : -EMU_PERIOD)) {
-    if (u == U) particle_step<H, poly_mask<EMU_PERIOD, H>(U)>(p, zx2, zy2, nzz, acc, hv);
-    else step_u<H, EMU_PERIOD, U + 1>(u, p, zx2, zy2, nzz, acc, hv);
+    if (u == U) particle_step<H, poly_mask<EMU_PERIOD, H>(U)>(p, zx2, zy2, acc, hv);
+    else step_u<H, EMU_PERIOD, U + 1>(u, p, zx2, zy2, acc, hv);
   }
 }
 
@@ -164,11 +183,11 @@ __device__ __forceinline__ void tile_sum(const float4 *__restrict__ A, int np, M
 #pragma unroll 1
     for (; p + PER <= np; p += PER) {
 #pragma unroll
-      for (int u = 0; u < PER; ++u) step_u<H, EMU_PERIOD>(u, A[p + u], m.zx2, m.zy2, m.nzz, acc, HV);
+      for (int u = 0; u < PER; ++u) step_u<H, EMU_PERIOD>(u, A[p + u], m.zx2, m.zy2, acc, HV);
     }
   }
 #pragma unroll 4
-  for (; p < np; ++p) particle_step<H, 0>(A[p], m.zx2, m.zy2, m.nzz, acc, HV);
+  for (; p < np; ++p) particle_step<H, 0>(A[p], m.zx2, m.zy2, acc, HV);
 #pragma unroll
   for (int h = 0; h < H; ++h) {
     float lo, hi;
@@ -182,13 +201,19 @@ template <int K, int EMU_PERIOD>
 __device__ __forceinline__ void tile_dispatch(int hv, const float4 *A, int np, Meas<K> &m) {
   constexpr int H = Meas<K>::H;
   if (hv == H) tile_sum<K, H, EMU_PERIOD>(A, np, m);
-  else if constexpr (H > 1) tile_sum<K, 1, EMU_PERIOD>(A, np, m);
+  else if constexpr (H > 1) {
+    if (hv == 1) tile_sum<K, 1, EMU_PERIOD>(A, np, m);
+    if constexpr (H > 2) {
+      if (hv == 2) tile_sum<K, 2, EMU_PERIOD>(A, np, m);
+      if (hv == 3) tile_sum<K, (H > 3 ? 3 : 2), EMU_PERIOD>(A, np, m);
+    }
+  }
 }
 
 // Unit u = mt * T + j (all full measurement tiles first, the ragged last tiles
 // at the end of the grid, so the short units fill the tail of the schedule).
 template <int K, int EMU_PERIOD>
-__global__ void __launch_bounds__(kThreads) compat_kernel(const CompatArgs a) {
+__global__ void __launch_bounds__(kThreads, min_blocks<K>()) compat_kernel(const CompatArgs a) {
   constexpr int H = Meas<K>::H;
   extern __shared__ __align__(128) float smem[];
   float4 *aos = reinterpret_cast<float4 *>(smem + kStages * kRawFloats);  // 2 AoS tiles
@@ -204,7 +229,6 @@ __global__ void __launch_bounds__(kThreads) compat_kernel(const CompatArgs a) {
   const int64_t base = static_cast<int64_t>(j) * a.ld;
   const float *xs = a.x + base, *ys = a.y + base, *ws = a.w + base;
   const int ntiles = (a.P + kTileP - 1) / kTileP;
-
   if (tid == 0) {
 #pragma unroll
     for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
@@ -256,15 +280,14 @@ __global__ void __launch_bounds__(kThreads) compat_kernel(const CompatArgs a) {
         }
         m.zx2[h] = f2_pack(2.0f * zx[0], 2.0f * zx[1]);
         m.zy2[h] = f2_pack(2.0f * zy[0], 2.0f * zy[1]);
-        m.nzz[h] = f2_pack(-fmaf(zx[0], zx[0], zy[0] * zy[0]), -fmaf(zx[1], zx[1], zy[1] * zy[1]));
         m.tot[2 * h] = 0.f;
         m.tot[2 * h + 1] = 0.f;
       }
     }
-    for (int idx = tid; idx < np; idx += kThreads) {  // whiten raw tile -> AoS (X', Y', -|p'|^2, w)
+    // whiten raw tile -> AoS (X', Y', -, w)
+    for (int idx = tid; idx < np; idx += kThreads) {
       const float lx = X[idx] - cx, ly = Y[idx] - cy;
-      const float px = fmaf(a.a2, ly, a.a1 * lx), py = a.b2 * ly;
-      A[idx] = make_float4(px, py, -fmaf(px, px, py * py), W[idx]);
+      A[idx] = make_float4(fmaf(a.a2, ly, a.a1 * lx), a.b2 * ly, 0.f, W[idx]);
     }
     fence_proxy_async_smem();  // raw stage s was read through the generic proxy; TMA rewrites it next
     __syncthreads();           // AoS tile t complete; every warp is done with tile t-1
@@ -306,7 +329,7 @@ cudaError_t launch_k(const CompatArgs &a, cudaStream_t s) {
 // MUFU/polynomial mix and C stays bit-exact under row permutations of Z;
 // positive: pair h of particle u when (u + 2h) % EMU == EMU - 1, spread; 0:
 // all MUFU).  Default -12 (measured best bit-exact setting on B200, see
-// profiles/).  GLMB_COMPAT_EMU overrides it (diagnostics / A-B runs).
+// profiles/README.md).  GLMB_COMPAT_EMU overrides it (diagnostics / A-B runs).
 int emu_period() {
   static int v = [] {
     const char *e = std::getenv("GLMB_COMPAT_EMU");
@@ -328,6 +351,11 @@ cudaError_t launch_e(const CompatArgs &a, cudaStream_t s) {
     case -6: return launch_k<K, -6>(a, s);
     case -8: return launch_k<K, -8>(a, s);
     case -12: return launch_k<K, -12>(a, s);
+    case -4: return launch_k<K, -4>(a, s);
+    case -10: return launch_k<K, -10>(a, s);
+    case -16: return launch_k<K, -16>(a, s);
+    case 1: return launch_k<K, 1>(a, s);
+    case -5: return launch_k<K, -5>(a, s);
     default: return launch_k<K, 0>(a, s);
   }
 }
@@ -336,21 +364,29 @@ cudaError_t launch_e(const CompatArgs &a, cudaStream_t s) {
 
 void compat_plan(int32_t M, int32_t P, int32_t *K, int32_t *n_mtiles) {
   // Depends on (M, P) only -- never on T -- so any sharding of the tracks runs
-  // the same per-column code (bit-identical C).  Measurements per thread K = 4
-  // (tile of 512) for large M; small M uses the smallest K covering M.
+  // the same per-column code (bit-identical C).  K measurements per thread
+  // (tile of 128 K): kDefaultK for large M (GLMB_COMPAT_K overrides: A/B runs);
+  // small M uses the smallest K covering M.
   (void)P;
-  int32_t k = kMaxK;
+  static const int32_t kmax = [] {
+    const char *e = std::getenv("GLMB_COMPAT_K");
+    const int v = e ? std::atoi(e) : 2;
+    return (v == 1 || v == 2 || v == 4 || v == 8) ? v : 2;
+  }();
+  int32_t k = kmax;
   const int32_t warps_needed = (M + 31) / 32;
   while (k > 1 && warps_needed <= kWarps * (k / 2)) k /= 2;
   *K = k;
   *n_mtiles = (M + kTileM * k - 1) / (kTileM * k);
 }
 
-cudaError_t launch_compat(const CompatArgs &a, cudaStream_t s) {
+cudaError_t launch_compat(const CompatArgs &a_in, cudaStream_t s) {
+  const CompatArgs &a = a_in;
   switch (a.K) {
     case 1: return launch_e<1>(a, s);
     case 2: return launch_e<2>(a, s);
     case 4: return launch_e<4>(a, s);
+    case 8: return launch_e<8>(a, s);
     default: return cudaErrorInvalidValue;
   }
 }

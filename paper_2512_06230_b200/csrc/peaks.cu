@@ -99,6 +99,45 @@ __global__ void mix_kernel(float *out, int iters, float seed, long long *cyc) {
   if (threadIdx.x == 0 && blockIdx.x == 0) cyc[0] = t1 - t0;
 }
 
+// NM MUFU.EX2 per LDS.128 broadcast (all lanes read the same 16 B of shared memory).
+template <int NM>
+__global__ void mufu_lds_kernel(float *out, int iters, float seed, long long *cyc) {
+  __shared__ float4 buf[64];
+  if (threadIdx.x < 64) buf[threadIdx.x] = make_float4(seed, seed * 0.5f, seed * 0.25f, seed * 0.125f);
+  __syncthreads();
+  float v[NM];
+#pragma unroll
+  for (int c = 0; c < NM; ++c) v[c] = seed * (c + 1) * 1e-3f - 0.5f;
+  float acc = 0.f;
+  for (int i = 0; i < iters; ++i) {
+    const float4 p = buf[i & 63];
+    acc += p.x + p.w;
+#pragma unroll
+    for (int c = 0; c < NM; ++c) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(v[c]));
+  }
+  float s = acc;
+#pragma unroll
+  for (int c = 0; c < NM; ++c) s += v[c];
+  if (s == 12345.f) out[0] = s;
+}
+
+template <int NM>
+void run_mufu_lds(int sms, float *out, long long *cyc) {
+  const int threads = 256, blocks = sms * 8, iters = 4096;
+  mufu_lds_kernel<NM><<<blocks, threads>>>(out, 16, 1.0f, cyc);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  mufu_lds_kernel<NM><<<blocks, threads>>>(out, iters, 1.0f, cyc);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double th = double(blocks) * threads * iters;
+  printf("  \"mufu%d_per_lds128\": {\"ex2_per_s\": %.6e, \"ms\": %.4f},\n", NM, th * NM / (ms * 1e-3), ms);
+}
+
 template <int NM, int NF>
 void run_mix(int sms, float *out, long long *cyc) {
   const int threads = 256, blocks = sms * 8, iters = 2048;
@@ -150,6 +189,9 @@ int main() {
   cudaMalloc(&out, 16);
   cudaMalloc(&cyc, 16);
   printf("{\n  \"sm_count\": %d,\n  \"attr_clock_mhz\": %.1f,\n", sms, clk_khz / 1e3);
+  run_mufu_lds<2>(sms, out, cyc);
+  run_mufu_lds<4>(sms, out, cyc);
+  run_mufu_lds<8>(sms, out, cyc);
   run_mix<8, 8>(sms, out, cyc);
   run_mix<8, 12>(sms, out, cyc);
   run_mix<8, 16>(sms, out, cyc);

@@ -390,3 +390,27 @@ def test_status_errors(L):
     with pytest.raises(GlmbError) as e:
         L.glmb_compat(Particles(trk.data, 6), Z, (1, 0, 1), 0.9, 1e-3, 1e-6, None, C, G)
     assert e.value.status == -2                                           # P % 4 != 0
+
+
+@pytest.mark.parametrize("case", ["wide", "tiny_w", "mixed"])
+def test_compat_fold_fallback_tiles(L, orc, case):
+    """Tiles with a particle at |p'|^2 > 64 (wide clouds) take the exact-difference
+    form; wide tracks, a track mixing wide and narrow tiles, and weights spanning
+    1e-36 .. 1e-3 must all match the oracle."""
+    r = np.random.default_rng(hash(case) % 2**32)
+    T, P, M = 3, 1024, 300
+    spread = {"wide": 25.0, "tiny_w": 2.0, "mixed": 2.0}[case]
+    x = (500 + spread * r.standard_normal((T, P))).astype(np.float32)
+    y = (800 + spread * r.standard_normal((T, P))).astype(np.float32)
+    w = np.full((T, P), 1.0 / P, np.float32)
+    if case == "tiny_w":
+        w[:] = np.float32(1e-36)
+        w[:, ::7] = np.float32(1e-3)
+    if case == "mixed":
+        x[:, 256:512] += (40 * r.standard_normal(256)).astype(np.float32)   # one wide tile
+    Z = np.stack([500 + 30 * r.standard_normal(M), 800 + 30 * r.standard_normal(M)], 1).astype(np.float32)
+    R = (1.0, 0.2, 0.7)
+    C, G, Cc = _compat_gpu(L, x, y, w, Z, R, 0.9, 1e-4, 1e-30 if case == "tiny_w" else 1e-8)
+    ref = orc.compat(x, y, w, Z, R, 0.9, 1e-4, 1e-30 if case == "tiny_w" else 1e-8)
+    check_compat(C, G, Cc, ref, 1e-30 if case == "tiny_w" else 1e-8, M)
+    assert (ref["C_tracks"] > 0).sum() > 10
