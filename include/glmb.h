@@ -185,12 +185,16 @@ glmb_status glmb_compat(const glmb_particles *trk, const float *Z, int32_t M,
  *              w'_p = exp(l_p - m) / sum_q exp(l_q - m),  m = max_p l_p
  *              log_norm[j] = m + ln sum_q exp(l_q - m)
  *              if every w_p == 0: w'_p = 1/P, log_norm = -inf, flags[j] = 1
- * w is updated in place.  log_norm: [T] fp32, flags: [T] u32 (bit 0 =
+ * The new weights go to w_out ([T][ld], 16-B aligned, same layout as w):
+ * w_out == trk->w updates in place; a separate buffer leaves trk->w intact
+ * (so glmb_compat may read it concurrently on another stream; tracks with
+ * S_j empty are then copied).  log_norm: [T] fp32, flags: [T] u32 (bit 0 =
  * degenerate track reset to uniform).
- * Errors: INVALID_ARG if R is not SPD or a needed pointer is NULL.
+ * Errors: INVALID_ARG if R is not SPD or a needed pointer is NULL;
+ * ALIGNMENT if w_out is not 16-B aligned.
  * --------------------------------------------------------------------- */
-glmb_status glmb_reweight(const glmb_particles *trk, const float *Z,
-                          int32_t M, float Rxx, float Rxy, float Ryy,
+glmb_status glmb_reweight(const glmb_particles *trk, float *w_out,
+                          const float *Z, int32_t M, float Rxx, float Rxy, float Ryy,
                           const int32_t *theta, int32_t col_offset,
                           float *log_norm, uint32_t *flags,
                           glmb_stream_t stream);

@@ -68,7 +68,7 @@ def load(path: str = LIB_PATH):
         L.glmb_predict.argtypes = [PP, PP, vp, f32, f32, f32, u64, u32, vp]
         L.glmb_birth.argtypes = [PP, vp, vp, vp, u64, u32, vp]
         L.glmb_compat.argtypes = [PP, vp, i32, f32, f32, f32, f32, f32, f32, vp, vp, i64, vp, i64, vp]
-        L.glmb_reweight.argtypes = [PP, vp, i32, f32, f32, f32, vp, i32, vp, vp, vp]
+        L.glmb_reweight.argtypes = [PP, vp, vp, i32, f32, f32, f32, vp, i32, vp, vp, vp]
         SP = C.POINTER(glmb_step_params)
         L.glmb_step.argtypes = [SP, vp, i32, vp, vp, vp, i64, vp, i64, vp, vp, vp]
         L.glmb_step_host.argtypes = [SP, vp, i32, vp, vp, vp, vp, vp, i64, vp, i64, vp, vp,
@@ -107,12 +107,14 @@ class Particles:
 
     FIELDS = ("x", "y", "v", "psi", "omega", "w")
 
-    def __init__(self, data: torch.Tensor, n_particles: int):
+    def __init__(self, data: torch.Tensor, n_particles: int, w: torch.Tensor | None = None):
+        """w: optional separate weight buffer [T, ld] used instead of data[5]."""
         assert data.dim() == 3 and data.shape[0] == 6 and data.dtype == torch.float32
         self.data = data
         self.T = data.shape[1]
         self.ld = data.shape[2]
         self.P = n_particles
+        self.w_override = w
 
     @classmethod
     def empty(cls, T: int, P: int, device="cuda", ld: int | None = None):
@@ -126,7 +128,11 @@ class Particles:
         return cls(t.to(device), t.shape[2])
 
     def rows(self, start: int, stop: int) -> "Particles":
-        return Particles(self.data[:, start:stop], self.P)
+        w = None if self.w_override is None else self.w_override[start:stop]
+        return Particles(self.data[:, start:stop], self.P, w)
+
+    def weights(self) -> torch.Tensor:
+        return self.data[5] if self.w_override is None else self.w_override
 
     def field(self, name: str) -> torch.Tensor:
         return self.data[self.FIELDS.index(name)]
@@ -139,6 +145,8 @@ class Particles:
         if d.stride(2) != 1 or d.stride(1) != self.ld:
             raise GlmbError(-1, "particle storage must be [6][T][ld] with unit stride")
         ptrs = [d[k].data_ptr() for k in range(6)]
+        if self.w_override is not None:
+            ptrs[5] = self.w_override.data_ptr()
         if not d.is_cuda:
             raise GlmbError(-1, "particles must live in CUDA memory")
         return glmb_particles(*ptrs, T, self.P, self.ld)
@@ -178,9 +186,11 @@ def glmb_compat(trk: Particles, Z, R, p_d, kappa, gamma, C_clutter, C_tracks, ga
                               gate.shape[1], _stream(stream)))
 
 
-def glmb_reweight(trk: Particles, Z, R, theta, col_offset, log_norm, flags, stream=None):
+def glmb_reweight(trk: Particles, Z, R, theta, col_offset, log_norm, flags, stream=None, w_out=None):
+    """w_out: [T, ld] tensor for the new weights (None: in place, trk's w)."""
     t = trk.struct()
-    _check(load().glmb_reweight(C.byref(t), _ptr(Z), Z.shape[0], R[0], R[1], R[2], _ptr(theta),
+    wo = t.w if w_out is None else _ptr(w_out)
+    _check(load().glmb_reweight(C.byref(t), wo, _ptr(Z), Z.shape[0], R[0], R[1], R[2], _ptr(theta),
                                 int(col_offset), _ptr(log_norm), _ptr(flags), _stream(stream)))
 
 

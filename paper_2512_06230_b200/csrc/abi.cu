@@ -187,10 +187,12 @@ glmb_status glmb_compat(const glmb_particles *trk, const float *Z, int32_t M, fl
   return from_cuda(glmb::launch_compat(a, s));
 }
 
-glmb_status glmb_reweight(const glmb_particles *trk, const float *Z, int32_t M, float Rxx, float Rxy, float Ryy,
-                          const int32_t *theta, int32_t col_offset, float *log_norm, uint32_t *flags,
+glmb_status glmb_reweight(const glmb_particles *trk, float *w_out, const float *Z, int32_t M, float Rxx, float Rxy,
+                          float Ryy, const int32_t *theta, int32_t col_offset, float *log_norm, uint32_t *flags,
                           glmb_stream_t stream) {
   GLMB_TRY(check_particles(trk, true, false));
+  if (trk->n_tracks > 0 && w_out == nullptr) return GLMB_ERR_INVALID_ARG;
+  if (trk->n_tracks > 0 && (reinterpret_cast<uintptr_t>(w_out) & 15u) != 0) return GLMB_ERR_ALIGNMENT;
   if (M < 0 || !spd(Rxx, Rxy, Ryy)) return GLMB_ERR_INVALID_ARG;
   const int32_t T = trk->n_tracks;
   if (T == 0) return GLMB_OK;
@@ -203,7 +205,7 @@ glmb_status glmb_reweight(const glmb_particles *trk, const float *Z, int32_t M, 
   const double det = rxx * ryy - rxy * rxy;
   const double h = 0.5 * 1.4426950408889634074;  // 1/2 log2(e)
   glmb::ReweightArgs a{};
-  a.x = trk->x; a.y = trk->y; a.w = trk->w; a.ld = trk->ld; a.T = T; a.P = trk->n_particles;
+  a.x = trk->x; a.y = trk->y; a.w = trk->w; a.w_out = w_out; a.ld = trk->ld; a.T = T; a.P = trk->n_particles;
   a.Z = Z; a.M = M; a.theta = theta; a.col_offset = col_offset;
   a.qa = h * ryy / det;
   a.qb = -2.0 * h * rxy / det;
@@ -235,7 +237,7 @@ glmb_status glmb_step(const glmb_step_params *prm, const float *Z, int32_t M, co
                       prm->step, stream));
   GLMB_TRY(glmb_compat(&all, Z, M, prm->Rxx, prm->Rxy, prm->Ryy, prm->p_d, prm->kappa, prm->gamma, C_clutter,
                        C_tracks, ldc, gate, ldg, stream));
-  return glmb_reweight(&all, Z, M, prm->Rxx, prm->Rxy, prm->Ryy, theta, prm->col_offset, log_norm, flags,
+  return glmb_reweight(&all, all.w, Z, M, prm->Rxx, prm->Rxy, prm->Ryy, theta, prm->col_offset, log_norm, flags,
                        stream);
 }
 

@@ -46,7 +46,8 @@ struct CompatArgs {
 
 struct ReweightArgs {
   const float *x, *y;
-  float *w;
+  const float *w;  // weights read
+  float *w_out;    // weights written (may equal w: in place)
   int64_t ld;
   int32_t T, P;
   const float *Z;

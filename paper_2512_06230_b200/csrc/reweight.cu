@@ -16,6 +16,7 @@
 // the generic path that recomputes l_p in the second pass.
 // Block reductions run in a fixed order -> deterministic, shard-invariant.
 #include <cfloat>
+#include <cstdlib>
 
 #include <cooperative_groups.h>
 
@@ -134,7 +135,9 @@ __global__ void __launch_bounds__(kThreads) reweight_kernel(const ReweightArgs a
   const int64_t base = static_cast<int64_t>(j) * a.ld;
   const float4 *xs = reinterpret_cast<const float4 *>(a.x + base);
   const float4 *ys = reinterpret_cast<const float4 *>(a.y + base);
-  float4 *ws = reinterpret_cast<float4 *>(a.w + base);
+  const float4 *ws = reinterpret_cast<const float4 *>(a.w + base);
+  float4 *wo = reinterpret_cast<float4 *>(a.w_out + base);
+  const bool copy_out = a.w_out != a.w;
   const int quads = a.P >> 2;
 
   collect_S(a, col, S, warp_cnt);
@@ -144,6 +147,7 @@ __global__ void __launch_bounds__(kThreads) reweight_kernel(const ReweightArgs a
     double s = 0.0;
     for (int g = threadIdx.x; g < quads; g += kThreads) {
       const float4 w4 = __ldcs(ws + g);
+      if (copy_out) __stcs(wo + g, w4);
       s += (static_cast<double>(w4.x) + w4.y) + (static_cast<double>(w4.z) + w4.w);
     }
     s = block_sum(s, red);
@@ -170,7 +174,7 @@ __global__ void __launch_bounds__(kThreads) reweight_kernel(const ReweightArgs a
 
   if (m == -INFINITY) {  // every weight zero: uniform reset, flagged (never abort)
     const float u = 1.0f / static_cast<float>(a.P);
-    for (int g = threadIdx.x; g < quads; g += kThreads) __stcs(ws + g, make_float4(u, u, u, u));
+    for (int g = threadIdx.x; g < quads; g += kThreads) __stcs(wo + g, make_float4(u, u, u, u));
     if (threadIdx.x == 0) {
       a.log_norm[j] = -INFINITY;
       a.flags[j] = 1u;
@@ -212,7 +216,7 @@ __global__ void __launch_bounds__(kThreads) reweight_kernel(const ReweightArgs a
       for (int q = 0; q < 4; ++q)
         q4(o, q) = ex2_approx(static_cast<float>(log_weight(a, S, col, q4(X, q), q4(Y, q), q4(Wv, q)) - m)) * inv_s;
     }
-    __stcs(ws + g, o);
+    __stcs(wo + g, o);
   }
   if (threadIdx.x == 0) {
     const double ln2 = 0.69314718055994530942;
@@ -228,7 +232,7 @@ __global__ void __launch_bounds__(kThreads) reweight_kernel(const ReweightArgs a
 // latency chain of each CTA (theta scan, loads, two reductions) overlaps far
 // more work -- the pass is HBM-bound again.
 template <int CL, int R>
-__global__ void __launch_bounds__(kThreads) reweight_cluster_kernel(const ReweightArgs a) {
+__global__ void __launch_bounds__(kThreads, R == 1 ? 6 : 3) reweight_cluster_kernel(const ReweightArgs a) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   __shared__ SList S;
@@ -241,7 +245,9 @@ __global__ void __launch_bounds__(kThreads) reweight_cluster_kernel(const Reweig
   const int64_t base = static_cast<int64_t>(j) * a.ld;
   const float4 *xs = reinterpret_cast<const float4 *>(a.x + base);
   const float4 *ys = reinterpret_cast<const float4 *>(a.y + base);
-  float4 *ws = reinterpret_cast<float4 *>(a.w + base);
+  const float4 *ws = reinterpret_cast<const float4 *>(a.w + base);
+  float4 *wo = reinterpret_cast<float4 *>(a.w_out + base);
+  const bool copy_out = a.w_out != a.w;
   const int quads = a.P >> 2;
   const int per = (quads + CL - 1) / CL;
   const int q0 = crank * per, q1 = min(quads, q0 + per);
@@ -273,9 +279,13 @@ __global__ void __launch_bounds__(kThreads) reweight_cluster_kernel(const Reweig
   if (nS == 0) {  // untouched; log_norm = ln sum w
     double sw = 0.0;
 #pragma unroll
-    for (int r = 0; r < R; ++r)
-      if (q0 + threadIdx.x + r * kThreads < q1)
+    for (int r = 0; r < R; ++r) {
+      const int g = q0 + threadIdx.x + r * kThreads;
+      if (g < q1) {
+        if (copy_out) __stcs(wo + g, W[r]);
         sw += (static_cast<double>(W[r].x) + W[r].y) + (static_cast<double>(W[r].z) + W[r].w);
+      }
+    }
     sw = block_sum(sw, red);
     if (threadIdx.x == 0) part[1] = sw;
     const double tot = cluster_combine(1, false);
@@ -308,7 +318,7 @@ __global__ void __launch_bounds__(kThreads) reweight_cluster_kernel(const Reweig
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int g = q0 + threadIdx.x + r * kThreads;
-      if (g < q1) __stcs(ws + g, make_float4(u, u, u, u));
+      if (g < q1) __stcs(wo + g, make_float4(u, u, u, u));
     }
     if (crank == 0 && threadIdx.x == 0) {
       a.log_norm[j] = -INFINITY;
@@ -341,7 +351,7 @@ __global__ void __launch_bounds__(kThreads) reweight_cluster_kernel(const Reweig
       float4 o;
 #pragma unroll
       for (int q = 0; q < 4; ++q) q4(o, q) = static_cast<float>(l[4 * r + q]) * inv_s;
-      __stcs(ws + g, o);
+      __stcs(wo + g, o);
     }
   }
   if (crank == 0 && threadIdx.x == 0) {
@@ -377,6 +387,16 @@ cudaError_t launch_reweight(const ReweightArgs &a, cudaStream_t s) {
   if (a.T == 0) return cudaSuccess;
   // Launch shape depends on P only (never on T): shard-invariant results.
   const int quads = a.P >> 2;
+  static const int rw_r = [] {  // quads per thread: 1 (more, lighter CTAs) or 2; A-B knob
+    const char *e = std::getenv("GLMB_REWEIGHT_R");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (rw_r == 1) {
+    if (quads <= 1 * kThreads) return launch_cluster<1, 1>(a, s);
+    if (quads <= 2 * kThreads) return launch_cluster<2, 1>(a, s);
+    if (quads <= 4 * kThreads) return launch_cluster<4, 1>(a, s);
+    if (quads <= 8 * kThreads) return launch_cluster<8, 1>(a, s);
+  }
   if (quads <= 1 * kThreads * 2) return launch_cluster<1, 2>(a, s);
   if (quads <= 2 * kThreads * 2) return launch_cluster<2, 2>(a, s);
   if (quads <= 4 * kThreads * 2) return launch_cluster<4, 2>(a, s);

@@ -64,7 +64,10 @@ class GlmbStep:
         if self.T_surv:
             init = np.stack([scene.x, scene.y, scene.v, scene.psi, scene.omega, scene.w])
             self.particles.data[:, :self.T_surv].copy_(torch.from_numpy(init))
-        self.init_state = None
+        # double-buffered weights: reweight may write the other buffer while compat
+        # reads the current one on another stream (glmb_reweight's w_out)
+        self.w_bufs = [self.particles.data[5], torch.empty_like(self.particles.data[5])]
+        self.w_cur = 0
         b_idx = [b - cfg.T for b in births]
         gid = np.concatenate([np.asarray(scene.gid, np.int32),
                               scene.birth_gid[b_idx].astype(np.int32)])
@@ -112,12 +115,21 @@ class GlmbStep:
         L.glmb_compat(self.particles, self.Z[zi] if Z is None else Z, self.R, self.cfg.p_d, self.cfg.kappa,
                       self.cfg.gamma, o.C_clutter, o.C_tracks, o.gate, stream)
 
-    def reweight(self, k: int, stream=None, Z=None, theta=None):
+    def reweight(self, k: int, stream=None, Z=None, theta=None, out_of_place: bool = False):
+        """out_of_place: write the new weights into the spare buffer (the current weights
+        stay readable by a concurrent compat) and make it current afterwards."""
         zi = k % len(self.Z)
         o = self.out
+        w_out = self.w_bufs[1 - self.w_cur] if out_of_place else None
         L.glmb_reweight(self.particles, self.Z[zi] if Z is None else Z, self.R,
                         self.theta[zi] if theta is None else theta, self.cols.start,
-                        o.log_norm, o.flags, stream)
+                        o.log_norm, o.flags, stream, w_out=w_out)
+        if out_of_place:
+            self.w_cur = 1 - self.w_cur
+            self.particles = L.Particles(self.particles.data, self.P, self.w_bufs[self.w_cur])
+
+    def weights(self) -> torch.Tensor:
+        return self.w_bufs[self.w_cur]
 
     def run(self, k: int, stream=None):
         """One whole step through the fused glmb_step entry point."""

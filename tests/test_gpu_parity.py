@@ -414,3 +414,31 @@ def test_compat_fold_fallback_tiles(L, orc, case):
     ref = orc.compat(x, y, w, Z, R, 0.9, 1e-4, 1e-30 if case == "tiny_w" else 1e-8)
     check_compat(C, G, Cc, ref, 1e-30 if case == "tiny_w" else 1e-8, M)
     assert (ref["C_tracks"] > 0).sum() > 10
+
+
+@pytest.mark.parametrize("P", [1024, 8192, 16384])
+def test_reweight_out_of_place_matches_in_place(L, orc, P):
+    """glmb_reweight with a separate w_out: same bits as in place, input weights untouched,
+    tracks without assigned measurements copied."""
+    import torch
+    from paper_2512_06230_b200._lib import Particles
+    r = np.random.default_rng(P + 1)
+    T = 6
+    data = np.zeros((6, T, P), np.float32)
+    data[0] = r.normal(0, 1, (T, P))
+    data[1] = r.normal(0, 1, (T, P))
+    data[5] = r.dirichlet(np.ones(P), T)
+    Z = r.normal(0, 1, (5, 2)).astype(np.float32)
+    theta = np.array([1, 3, 3, 0, 6], np.int32)
+    a = Particles(_dev(data), P)
+    b = Particles(_dev(data), P)
+    w_out = torch.full((T, P), -1.0, device="cuda")
+    la, fa = torch.zeros(T, device="cuda"), torch.zeros(T, dtype=torch.int32, device="cuda")
+    lb, fb = torch.zeros(T, device="cuda"), torch.zeros(T, dtype=torch.int32, device="cuda")
+    L.glmb_reweight(a, _dev(Z), (1, 0, 1), _dev(theta), 0, la, fa)
+    L.glmb_reweight(b, _dev(Z), (1, 0, 1), _dev(theta), 0, lb, fb, w_out=w_out)
+    np.testing.assert_array_equal(_host(w_out), _host(a.data)[5])
+    np.testing.assert_array_equal(_host(b.data)[5], data[5])
+    np.testing.assert_array_equal(_host(la), _host(lb))
+    rw, _, _ = orc.reweight(data[0], data[1], data[5], Z, (1, 0, 1), theta)
+    check_weights(_host(w_out), rw)
