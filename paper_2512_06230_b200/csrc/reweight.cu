@@ -36,37 +36,65 @@ struct SList {
   int in_smem;     // 1 if all of S_j fits in z[]
 };
 
-// Collect S_j in ascending i: each warp scans a contiguous chunk of theta
-// (ballot + popc), then the per-warp counts are prefix-summed so the list keeps
-// the ascending order of i (deterministic fp64 accumulation order).
-__device__ void collect_S(const ReweightArgs &a, int col, SList &S, int *warp_cnt) {
+// Collect S_j in ascending i.  Chunks of 8 * kThreads indices: every thread
+// issues its 8 theta loads at once (one L2 round trip per chunk, not one per
+// 32 indices), each warp ballots per row, and warp 0 turns the 64 (row, warp)
+// masks -- already in ascending-i order -- into list positions with a
+// warp-shuffle prefix sum and fetches the hit measurements.
+constexpr int kRows = 8;
+__device__ void collect_S(const ReweightArgs &a, int col, SList &S, uint32_t *masks /* [kRows * kWarps] */) {
+  static_assert(kRows * kWarps == 64, "warp 0 scans two masks per lane");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int chunk = ((a.M + kWarps - 1) / kWarps + 31) & ~31;
-  const int lo = warp * chunk, hi = min(a.M, lo + chunk);
-  int n = 0;
-  for (int base = lo; base < hi; base += 32) {
-    const int i = base + lane;
-    n += __popc(__ballot_sync(0xffffffffu, i < hi && __ldg(a.theta + i) == col));
-  }
-  if (lane == 0) warp_cnt[warp] = n;
-  __syncthreads();
-  int off = 0, total = 0;
+  int total = 0;  // maintained by warp 0
+  for (int base = 0; base < a.M; base += kRows * kThreads) {
+    int th[kRows];
 #pragma unroll
-  for (int k = 0; k < kWarps; ++k) {
-    off += (k < warp) ? warp_cnt[k] : 0;
-    total += warp_cnt[k];
-  }
-  if (total > 0 && total <= kSCap) {
-    for (int base = lo; base < hi; base += 32) {
-      const int i = base + lane;
-      const bool hit = i < hi && __ldg(a.theta + i) == col;
-      const uint32_t mask = __ballot_sync(0xffffffffu, hit);
-      if (hit) {
-        const float2 z = __ldg(reinterpret_cast<const float2 *>(a.Z) + i);
-        S.z[off + __popc(mask & ((1u << lane) - 1u))] = make_double2(z.x, z.y);
-      }
-      off += __popc(mask);
+    for (int r = 0; r < kRows; ++r) {
+      const int i = base + r * kThreads + threadIdx.x;
+      th[r] = i < a.M ? __ldg(a.theta + i) : -1;
     }
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) {
+      const uint32_t m = __ballot_sync(0xffffffffu, th[r] == col);
+      if (lane == 0) masks[r * kWarps + warp] = m;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t m0 = masks[lane], m1 = masks[lane + 32];  // mask k covers i = base + 32 k + bit
+      const int c0 = __popc(m0), c1 = __popc(m1);
+      int s0 = c0, s1 = c1;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t0 = __shfl_up_sync(0xffffffffu, s0, o), t1 = __shfl_up_sync(0xffffffffu, s1, o);
+        if (lane >= o) {
+          s0 += t0;
+          s1 += t1;
+        }
+      }
+      const int tot0 = __shfl_sync(0xffffffffu, s0, 31), tot1 = __shfl_sync(0xffffffffu, s1, 31);
+      int off0 = total + s0 - c0, off1 = total + tot0 + s1 - c1;
+      const float2 *Z2 = reinterpret_cast<const float2 *>(a.Z);
+      while (m0) {
+        const int i = base + 32 * lane + __ffs(m0) - 1;
+        m0 &= m0 - 1;
+        if (off0 < kSCap) {
+          const float2 z = __ldg(Z2 + i);
+          S.z[off0] = make_double2(z.x, z.y);
+        }
+        ++off0;
+      }
+      while (m1) {
+        const int i = base + 32 * (lane + 32) + __ffs(m1) - 1;
+        m1 &= m1 - 1;
+        if (off1 < kSCap) {
+          const float2 z = __ldg(Z2 + i);
+          S.z[off1] = make_double2(z.x, z.y);
+        }
+        ++off1;
+      }
+      total += tot0 + tot1;
+    }
+    __syncthreads();  // masks are rewritten by the next chunk
   }
   if (threadIdx.x == 0) {
     S.n = total;
@@ -129,7 +157,7 @@ __global__ void __launch_bounds__(kThreads) reweight_kernel(const ReweightArgs a
   extern __shared__ __align__(16) double lcache[];
   __shared__ SList S;
   __shared__ double red[kWarps];
-  __shared__ int warp_cnt[kWarps];
+  __shared__ uint32_t masks[kRows * kWarps];
   const int j = blockIdx.x;
   const int col = a.col_offset + j + 1;
   const int64_t base = static_cast<int64_t>(j) * a.ld;
@@ -140,7 +168,7 @@ __global__ void __launch_bounds__(kThreads) reweight_kernel(const ReweightArgs a
   const bool copy_out = a.w_out != a.w;
   const int quads = a.P >> 2;
 
-  collect_S(a, col, S, warp_cnt);
+  collect_S(a, col, S, masks);
   const int nS = S.n;
 
   if (nS == 0) {  // untouched; log_norm = ln sum w
@@ -225,19 +253,40 @@ __global__ void __launch_bounds__(kThreads) reweight_kernel(const ReweightArgs a
   }
 }
 
+// Split cluster barrier: arrive without a release fence, wait at exit.
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
+
+// (max, sum) pairs combined exactly as one pass over all terms would give up
+// to rounding: (m, s) + (m', s') = (M, s 2^(m-M) + s' 2^(m'-M)), M = max(m, m').
+// Applied by one thread in a fixed order, so the reduction is deterministic.
+__device__ __forceinline__ void ms_merge(double &m, double &s, double m2, double s2) {
+  const double M = fmax(m, m2);
+  if (M == -INFINITY) {
+    s = 0.0;
+    return;
+  }
+  s = s * ex2_approx(static_cast<float>(m - M)) + s2 * ex2_approx(static_cast<float>(m2 - M));
+  m = M;
+}
+
 // Thread-block-cluster variant (P <= 8 * 1024 * R): the CL CTAs of a cluster
-// split one track's particles, keep them in registers, and combine the block
-// max / block sum through distributed shared memory (DSMEM) in cluster-rank
-// order (deterministic).  4x the CTAs of the one-CTA-per-track kernel, so the
-// latency chain of each CTA (theta scan, loads, two reductions) overlaps far
-// more work -- the pass is HBM-bound again.
+// split one track's particles and keep them in registers.  One pass computes
+// l_p, each warp's (max m_w, sum 2^(l - m_w)) by shuffles, and one thread per
+// CTA merges the warps and then the cluster's CTAs (DSMEM, rank order:
+// deterministic) -- one reduction and one cluster barrier instead of a max
+// pass and a sum pass, and no per-thread rescaling.  w'_p = 2^(l_p - m_w) *
+// 2^(m_w - m) / s.  Particle loads are issued
+// before the theta scan so the two latencies overlap.
 template <int CL, int R>
-__global__ void __launch_bounds__(kThreads, R == 1 ? 6 : 3) reweight_cluster_kernel(const ReweightArgs a) {
+__global__ void __launch_bounds__(kThreads, R == 1 ? 5 : (R == 2 ? 3 : 2)) reweight_cluster_kernel(const ReweightArgs a) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   __shared__ SList S;
-  __shared__ double red[kWarps];
-  __shared__ int warp_cnt[kWarps];
+  __shared__ double red[2][kWarps];
+  __shared__ uint32_t masks[kRows * kWarps];
   __shared__ double part[2];  // this CTA's (max, sum), read by the peers
   const int crank = static_cast<int>(cluster.block_rank());
   const int j = blockIdx.x / CL;
@@ -251,6 +300,7 @@ __global__ void __launch_bounds__(kThreads, R == 1 ? 6 : 3) reweight_cluster_ker
   const int quads = a.P >> 2;
   const int per = (quads + CL - 1) / CL;
   const int q0 = crank * per, q1 = min(quads, q0 + per);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
   float4 X[R], Y[R], W[R];
 #pragma unroll
@@ -262,58 +312,94 @@ __global__ void __launch_bounds__(kThreads, R == 1 ? 6 : 3) reweight_cluster_ker
       W[r] = __ldcs(ws + g);
     }
   }
-  collect_S(a, col, S, warp_cnt);
+  collect_S(a, col, S, masks);
   const int nS = S.n;
-
-  auto cluster_combine = [&](int slot, bool take_max) -> double {
-    cluster.sync();
-    double v = take_max ? -INFINITY : 0.0;
-#pragma unroll
-    for (int r = 0; r < CL; ++r) {
-      const double pv = cluster.map_shared_rank(part, r)[slot];
-      v = take_max ? fmax(v, pv) : v + pv;
-    }
-    return v;
-  };
 
   if (nS == 0) {  // untouched; log_norm = ln sum w
     double sw = 0.0;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int g = q0 + threadIdx.x + r * kThreads;
-      if (g < q1) {
-        if (copy_out) __stcs(wo + g, W[r]);
-        sw += (static_cast<double>(W[r].x) + W[r].y) + (static_cast<double>(W[r].z) + W[r].w);
+      if (g < q1) sw += (static_cast<double>(W[r].x) + W[r].y) + (static_cast<double>(W[r].z) + W[r].w);
+    }
+    sw = block_sum(sw, red[0]);
+    if (threadIdx.x == 0) part[1] = sw;
+    cluster.sync();
+    if (copy_out) {  // after the barrier: the copy does not sit behind its release fence
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int g = q0 + threadIdx.x + r * kThreads;
+        if (g < q1) __stcs(wo + g, W[r]);
       }
     }
-    sw = block_sum(sw, red);
-    if (threadIdx.x == 0) part[1] = sw;
-    const double tot = cluster_combine(1, false);
     if (crank == 0 && threadIdx.x == 0) {
+      double tot = 0.0;
+#pragma unroll
+      for (int r = 0; r < CL; ++r) tot += cluster.map_shared_rank(part, r)[1];
       a.log_norm[j] = static_cast<float>(log(tot));
       a.flags[j] = 0u;
     }
-    cluster.sync();  // peers' shared memory stays alive until every read is done
+    if (crank == 0) __syncthreads();
+    cluster_arrive_relaxed();  // done with the peers' shared memory
+    cluster_wait();            // ... and they with ours
     return;
   }
 
   double l[4 * R];
-  double lm = -INFINITY;
+  double mw = -INFINITY;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    if (q0 + threadIdx.x + r * kThreads < q1) {
+    const bool ok = q0 + threadIdx.x + r * kThreads < q1;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        l[4 * r + q] = log_weight(a, S, col, q4(X[r], q), q4(Y[r], q), q4(W[r], q));
-        lm = fmax(lm, l[4 * r + q]);
-      }
+    for (int q = 0; q < 4; ++q) {
+      l[4 * r + q] = ok ? log_weight(a, S, col, q4(X[r], q), q4(Y[r], q), q4(W[r], q)) : -INFINITY;
+      mw = fmax(mw, l[4 * r + q]);
     }
   }
-  lm = block_max(lm, red);
-  if (threadIdx.x == 0) part[0] = lm;
-  const double m = cluster_combine(0, true);
+  // warp max (fp64 shuffles, no conversions), then terms relative to it
+  mw = warp_max_d(mw);
+  float e[4 * R];
+  float sw = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 4 * R; ++k) {
+    e[k] = mw == -INFINITY ? 0.0f : ex2_approx(static_cast<float>(l[k] - mw));
+    sw += e[k];
+  }
+  sw = warp_sum(sw);
+  // block: thread 0 merges the warps in order; cluster: thread 0 of every CTA
+  // merges the CL parts in rank order (all CTAs get the same (m, s))
+  __shared__ double bc[2];
+  if (lane == 0) {
+    red[0][warp] = mw;
+    red[1][warp] = sw;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double mb = red[0][0], sb = red[1][0];
+#pragma unroll
+    for (int k = 1; k < kWarps; ++k) ms_merge(mb, sb, red[0][k], red[1][k]);
+    part[0] = mb;
+    part[1] = sb;
+  }
+  cluster.sync();
+  if (threadIdx.x == 0) {
+    double mc = -INFINITY, sc = 0.0;
+#pragma unroll
+    for (int r = 0; r < CL; ++r) {
+      const double *pr = cluster.map_shared_rank(part, r);
+      ms_merge(mc, sc, pr[0], pr[1]);
+    }
+    bc[0] = mc;
+    bc[1] = sc;
+  }
+  __syncthreads();
+  const double mc = bc[0], sc = bc[1];
+  // every read of a peer's shared memory is done: arrive now (relaxed: no
+  // memory ordering needed), wait only at exit so the stores below do not
+  // sit behind a release fence
+  cluster_arrive_relaxed();
 
-  if (m == -INFINITY) {  // every weight zero: uniform reset, flagged (never abort)
+  if (mc == -INFINITY) {  // every weight zero: uniform reset, flagged (never abort)
     const float u = 1.0f / static_cast<float>(a.P);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -324,42 +410,23 @@ __global__ void __launch_bounds__(kThreads, R == 1 ? 6 : 3) reweight_cluster_ker
       a.log_norm[j] = -INFINITY;
       a.flags[j] = 1u;
     }
-    cluster.sync();
+    cluster_wait();
     return;
   }
-
-  double sl = 0.0;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    if (q0 + threadIdx.x + r * kThreads < q1) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float e = ex2_approx(static_cast<float>(l[4 * r + q] - m));
-        l[4 * r + q] = e;
-        sl += e;
-      }
-    }
-  }
-  sl = block_sum(sl, red);
-  if (threadIdx.x == 0) part[1] = sl;
-  const double s = cluster_combine(1, false);
-  const float inv_s = static_cast<float>(1.0 / s);
+  // w'_p = 2^(l_p - m_w) 2^(m_w - m) / s; a factor below FLT_MIN flushes only
+  // weights whose exact value is below FLT_MIN as well
+  const float f = mw == -INFINITY ? 0.0f : ex2_approx(static_cast<float>(mw - mc)) * static_cast<float>(1.0 / sc);
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int g = q0 + threadIdx.x + r * kThreads;
-    if (g < q1) {
-      float4 o;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) q4(o, q) = static_cast<float>(l[4 * r + q]) * inv_s;
-      __stcs(wo + g, o);
-    }
+    if (g < q1) __stcs(wo + g, make_float4(e[4 * r] * f, e[4 * r + 1] * f, e[4 * r + 2] * f, e[4 * r + 3] * f));
   }
   if (crank == 0 && threadIdx.x == 0) {
     const double ln2 = 0.69314718055994530942;
-    a.log_norm[j] = static_cast<float>((m + log2(s)) * ln2 - nS * a.log_norm1);
+    a.log_norm[j] = static_cast<float>((mc + log2(sc)) * ln2 - nS * a.log_norm1);
     a.flags[j] = 0u;
   }
-  cluster.sync();
+  cluster_wait();
 }
 
 template <int CL, int R>
@@ -397,10 +464,15 @@ cudaError_t launch_reweight(const ReweightArgs &a, cudaStream_t s) {
     if (quads <= 4 * kThreads) return launch_cluster<4, 1>(a, s);
     if (quads <= 8 * kThreads) return launch_cluster<8, 1>(a, s);
   }
-  if (quads <= 1 * kThreads * 2) return launch_cluster<1, 2>(a, s);
-  if (quads <= 2 * kThreads * 2) return launch_cluster<2, 2>(a, s);
-  if (quads <= 4 * kThreads * 2) return launch_cluster<4, 2>(a, s);
-  if (quads <= 8 * kThreads * 2) return launch_cluster<8, 2>(a, s);
+  if (rw_r != 4) {
+    if (quads <= 1 * kThreads * 2) return launch_cluster<1, 2>(a, s);
+    if (quads <= 2 * kThreads * 2) return launch_cluster<2, 2>(a, s);
+    if (quads <= 4 * kThreads * 2) return launch_cluster<4, 2>(a, s);
+    if (quads <= 8 * kThreads * 2) return launch_cluster<8, 2>(a, s);
+  }
+  if (quads <= 1 * kThreads * 4) return launch_cluster<1, 4>(a, s);
+  if (quads <= 2 * kThreads * 4) return launch_cluster<2, 4>(a, s);
+  if (quads <= 4 * kThreads * 4) return launch_cluster<4, 4>(a, s);
   if (quads <= 8 * kThreads * 4) return launch_cluster<8, 4>(a, s);
   const size_t cache = static_cast<size_t>(a.P) * sizeof(double);
   if (cache <= kMaxCacheBytes) {
