@@ -74,6 +74,17 @@ def lib():
             L.oracle_reweight.argtypes = (
                 [C.c_int32, C.c_int32, C.c_int64, f32, f32, f32, C.c_int32, f32]
                 + [C.c_float] * 3 + [i32, C.c_int32, f64, f64, u32])
+            u8 = P(np.uint8, flags="C_CONTIGUOUS")
+            L.oracle_death_prob.argtypes = [C.c_int32, C.c_int32, f32, C.c_int64, u32, C.c_int64,
+                                            C.c_float, C.c_float, f32, f64]
+            L.oracle_compat_rows.argtypes = [C.c_int32, C.c_int32, f32, C.c_int64, u32, C.c_int64,
+                                             i32, i32, f32, f64]
+            L.oracle_assoc_sample.argtypes = (
+                [C.c_int32] * 4 + [u32, C.c_int64, f64, f32, f32, C.c_float, C.c_float,
+                                   i32, i32, f32, f64, C.c_uint64, C.c_uint32, u32, i32, C.c_int64, f64])
+            L.oracle_dedup.argtypes = [C.c_int32] * 3 + [u32, C.c_int64, i32, C.c_int64, u8]
+            L.oracle_prune.argtypes = [C.c_int32, f64, u8, C.c_double, C.c_int32, i32, f64]
+            L.oracle_prune.restype = C.c_int32
             L.oracle_num_threads.restype = C.c_int
             L.oracle_set_num_threads.argtypes = [C.c_int]
             _lib = L
@@ -196,3 +207,85 @@ def reweight(x, y, w, Z, R, theta, col_offset=0):
     lib().oracle_reweight(T, P, P, x, y, w, M, Z, float(R[0]), float(R[1]), float(R[2]),
                           np.ascontiguousarray(theta, np.int32), int(col_offset), wo, lz, fl)
     return wo, lz, fl
+
+
+# ----------------------------------------------------------------- O9-O13 (hypothesis machinery)
+def _gate_words(gate, T, M):
+    ldg = (M + 31) // 32
+    if T == 0:
+        return np.zeros((1, 1), np.uint32), ldg
+    g = np.ascontiguousarray(gate, np.uint32).reshape(T, -1)
+    return g, g.shape[1]
+
+
+def death_prob(C_tracks, gate, p_d, kappa, p_s):
+    """C_tracks fp32 [T][ldc] (column-major C), gate u32 [T][ldg]; p_s [T] -> d [T] fp64 (O9)."""
+    C = _f32(C_tracks)
+    T = C.shape[0]
+    ldc = C.shape[1] if T else 0
+    g, ldg = _gate_words(gate, T, ldc)
+    M = ldc
+    d = np.zeros(T, np.float64)
+    lib().oracle_death_prob(T, M, C, ldc, g, ldg, float(p_d), float(kappa), _f32(p_s), d)
+    return d
+
+
+def compat_rows(C_tracks, gate, M):
+    """Row-wise (CSR) view of C: (row_ptr [M+1] i32, col [nnz] i32, val [nnz] f32, ln_val [nnz] f64) (O10)."""
+    C = _f32(C_tracks)
+    T = C.shape[0]
+    ldc = C.shape[1] if T else M
+    g, ldg = _gate_words(gate, T, M)
+    cap = max(1, T * M)
+    rp = np.zeros(M + 1, np.int32)
+    col = np.zeros(cap, np.int32)
+    val = np.zeros(cap, np.float32)
+    lv = np.zeros(cap, np.float64)
+    lib().oracle_compat_rows(T, M, C if T else np.zeros((1, 1), np.float32), ldc,
+                             g if T else np.zeros((1, 1), np.uint32), ldg, rp, col, val, lv)
+    n = int(rp[M])
+    return rp, col[:n].copy(), val[:n].copy(), lv[:n].copy()
+
+
+def assoc_sample(parent_mask, parent_logw, H_up, d_prob, p_s, p_d, kappa, rows, M, seed, step):
+    """Two-stage sampler (O11).  parent_mask u32 [H_old][ldt]; rows = compat_rows(...).
+    Returns (alive u32 [H_old*H_up][ldt], theta i32 [H_old*H_up][M], logw f64 [H_old*H_up])."""
+    pm = np.ascontiguousarray(parent_mask, np.uint32)
+    H_old, ldt = pm.shape
+    T = len(d_prob)
+    rp, col, val, lv = rows
+    n = H_old * H_up
+    alive = np.zeros((n, ldt), np.uint32)
+    theta = np.zeros((n, max(M, 1)), np.int32)
+    logw = np.zeros(n, np.float64)
+    one = lambda a, dt: np.ascontiguousarray(a if len(a) else np.zeros(1, dt), dt)
+    lib().oracle_assoc_sample(H_old, H_up, T, M, pm, ldt, np.ascontiguousarray(parent_logw, np.float64),
+                              one(d_prob, np.float32), one(p_s, np.float32), float(p_d), float(kappa),
+                              np.ascontiguousarray(rp, np.int32), one(col, np.int32), one(val, np.float32),
+                              one(lv, np.float64), C.c_uint64(seed), C.c_uint32(step), alive, theta,
+                              theta.shape[1], logw)
+    return alive, theta[:, :M], logw
+
+
+def dedup(alive, theta, H_old, H_up):
+    """unique u8 [H_old*H_up]: 1 for the first occurrence of each (alive, theta) within a parent (O12)."""
+    al = np.ascontiguousarray(alive, np.uint32)
+    th = np.ascontiguousarray(theta, np.int32)
+    M = th.shape[1]
+    if M == 0:
+        th = np.zeros((th.shape[0], 1), np.int32)
+    u = np.zeros(H_old * H_up, np.uint8)
+    lib().oracle_dedup(H_old, H_up, M, al, al.shape[1], th, th.shape[1], u)
+    return u
+
+
+def prune(logw, unique, tau, h_max):
+    """(keep_idx i32 [k], keep_w f64 [k]) after normalisation, tau and H_max (O13)."""
+    lw = np.ascontiguousarray(logw, np.float64)
+    u = np.ascontiguousarray(unique, np.uint8)
+    n = len(lw)
+    idx = np.zeros(max(1, n), np.int32)
+    w = np.zeros(max(1, n), np.float64)
+    k = lib().oracle_prune(n, lw if n else np.zeros(1), u if n else np.zeros(1, np.uint8),
+                           float(tau), int(h_max), idx, w)
+    return idx[:k].copy(), w[:k].copy()

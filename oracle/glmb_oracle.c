@@ -25,6 +25,11 @@
  *   O6 oracle_birth          -- LMB birth sampling, P:24 (§Approach), R10
  *   O7 oracle_compat         -- C_k equation, P:26-38 (§Approach), R1-R6, R12
  *   O8 oracle_reweight       -- particle update, P:53 (§Approach), R13, R14, R16
+ *   O9 oracle_death_prob     -- posterior death probability, P:44 (§Approach), R23
+ *   O10 oracle_compat_rows   -- row-wise (CSR) view of C_k, R26
+ *   O11 oracle_assoc_sample  -- two-stage sampler + hypothesis weight, R24-R26, R28
+ *   O12 oracle_dedup         -- unique successor hypotheses, R27
+ *   O13 oracle_prune         -- normalise, tau threshold, H_max, R29
  */
 #include <math.h>
 #include <stdint.h>
@@ -340,4 +345,225 @@ void oracle_reweight(int32_t T, int32_t P, int64_t ld, const float *x,
     }
     free(l);
   }
+}
+
+/* ==================================================================
+ * Hypothesis machinery: death probability, the
+ * row-wise view of C_k, the two-stage association sampler with de-duplication,
+ * the successor hypothesis weight, and pruning.  P:44-53 (§Approach).
+ * ================================================================== */
+
+/* O9 Posterior death probability, P:44 (§Approach: "We compute a posterior
+ * probability of track death for each track d_prob(x_j), balancing its prior
+ * survival probability against the likelihood of it being detected"; the
+ * formula is deferred to a citation -- reading R23):
+ *   e_j = max_{i : g_ij} C[i,j] / (C[i,j] + kappa)     (0 if no gated i)
+ *   d_j = (1 - P_S) / ((1 - P_S) + P_S ((1 - P_D) + P_D e_j)),  d_j = 0 if P_S = 1.
+ * C_tracks fp32 [T][ldc] (column-major C, as glmb_compat writes it), gate
+ * [T][ldg] bits. */
+void oracle_death_prob(int32_t T, int32_t M, const float *C_tracks, int64_t ldc,
+                       const uint32_t *gate, int64_t ldg, float p_d, float kappa,
+                       const float *p_s, double *d_out) {
+  for (int32_t j = 0; j < T; ++j) {
+    double e = 0.0;
+    for (int32_t i = 0; i < M; ++i) {
+      if ((gate[(int64_t)j * ldg + i / 32] >> (i % 32)) & 1u) {
+        double c = (double)C_tracks[(int64_t)j * ldc + i];
+        double r = c / (c + (double)kappa);
+        if (r > e) e = r;
+      }
+    }
+    double ps = (double)p_s[j], pd = (double)p_d;
+    if (ps == 1.0) {
+      d_out[j] = 0.0;
+    } else {
+      d_out[j] = (1.0 - ps) / ((1.0 - ps) + ps * ((1.0 - pd) + pd * e));
+    }
+  }
+}
+
+/* O10 Row-wise (CSR) view of C_k: row i lists the gated track columns j
+ * (ascending) with C[i, j+1] -- the rows the categorical of P:46 normalises.
+ * row_ptr [M+1]; col [nnz] (0-based track index j, i.e. C column j+1);
+ * val [nnz] (the fp32 entry, copied); ln_val [nnz] = ln(val) in fp64. */
+void oracle_compat_rows(int32_t T, int32_t M, const float *C_tracks, int64_t ldc,
+                        const uint32_t *gate, int64_t ldg, int32_t *row_ptr,
+                        int32_t *col, float *val, double *ln_val) {
+  int32_t n = 0;
+  for (int32_t i = 0; i < M; ++i) {
+    row_ptr[i] = n;
+    for (int32_t j = 0; j < T; ++j) {
+      if ((gate[(int64_t)j * ldg + i / 32] >> (i % 32)) & 1u) {
+        col[n] = j;
+        val[n] = C_tracks[(int64_t)j * ldc + i];
+        ln_val[n] = log((double)val[n]);
+        ++n;
+      }
+    }
+  }
+  row_ptr[M] = n;
+}
+
+/* one uniform for (index n, parent h, sample s, domain): Philox4x32-10 block
+ * with counter (n/4, h, step, domain<<24 | s), word n%4, mapped by O3
+ * (reading R24) */
+static double sampler_uniform(uint64_t seed, uint32_t step, uint32_t domain,
+                              int64_t n, int32_t h, int32_t s) {
+  uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  uint32_t ctr[4] = {(uint32_t)(n / 4), (uint32_t)h, step, (domain << 24) | (uint32_t)s};
+  uint32_t r[4];
+  oracle_philox4x32_10(ctr, key, r);
+  return oracle_uniform_u32(r[n % 4]);
+}
+
+/* O11 Two-stage association sampler, P:44-48 (§Approach), one sample (h, s)
+ * of parent hypothesis h:
+ *  stage 1 ("Bernoulli sampling step using d_prob to determine which
+ *   tracks survive"): track j of the parent survives iff u_j < 1 - d_j,
+ *   decided in fp32 as the kernel does (R25);
+ *  stage 2 ("for each measurement i, an association is sampled from a
+ *   categorical distribution defined by normalizing the corresponding row in
+ *   the modified matrix C'_k"; dead columns zeroed): theta_i = 0 with weight
+ *   kappa, theta_i = j+1 with weight C[i, j+1] for surviving j -- inverse CDF
+ *   in fp32 in ascending column order (R26): total = kappa + sum, t = u*total,
+ *   first column whose running sum exceeds t (the last positive one if
+ *   rounding leaves none).
+ *  weight ("multiplying its parent's weight with the joint likelihood of
+ *   the sampled survival/death events and data associations", R28):
+ *   ln w = ln w_parent + sum_{j in parent} (alive ? ln P_S : ln(1 - P_S))
+ *        + sum_i ln C'[i, theta_i] + #(alive j with no measurement) ln(1 - P_D).
+ * Outputs for sample q = h*H_up + s: alive [q][ldt] bits, theta [q][ldm],
+ * logw [q]. */
+void oracle_assoc_sample(int32_t H_old, int32_t H_up, int32_t T, int32_t M,
+                         const uint32_t *parent_mask, int64_t ldt,
+                         const double *parent_logw, const float *d_prob,
+                         const float *p_s, float p_d, float kappa,
+                         const int32_t *row_ptr, const int32_t *col,
+                         const float *val, const double *ln_val, uint64_t seed,
+                         uint32_t step, uint32_t *alive, int32_t *theta,
+                         int64_t ldm, double *logw) {
+#pragma omp parallel for schedule(dynamic)
+  for (int64_t q = 0; q < (int64_t)H_old * H_up; ++q) {
+    int32_t h = (int32_t)(q / H_up), s = (int32_t)(q % H_up);
+    const uint32_t *pm = parent_mask + (int64_t)h * ldt;
+    uint32_t *al = alive + q * ldt;
+    int32_t *th = theta + q * ldm;
+    int *detected = (int *)calloc((size_t)(T > 0 ? T : 1), sizeof(int));
+    double lw = parent_logw[h];
+    for (int64_t k = 0; k < ldt; ++k) al[k] = 0u;
+    /* stage 1 */
+    for (int32_t j = 0; j < T; ++j) {
+      if (!((pm[j / 32] >> (j % 32)) & 1u)) continue;
+      float u = (float)sampler_uniform(seed, step, 2u, j, h, s);
+      float thr = 1.0f - d_prob[j];
+      int a = u < thr;
+      if (a) al[j / 32] |= 1u << (j % 32);
+      lw += a ? log((double)p_s[j]) : log(1.0 - (double)p_s[j]);
+    }
+    /* stage 2 */
+    for (int32_t i = 0; i < M; ++i) {
+      float u = (float)sampler_uniform(seed, step, 3u, i, h, s);
+      float total = kappa;
+      for (int32_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e)
+        if ((al[col[e] / 32] >> (col[e] % 32)) & 1u) total = total + val[e];
+      float t = u * total;
+      float acc = kappa;
+      int32_t pick = -1, last = 0;
+      double lpick = log((double)kappa), llast = lpick;
+      if (t < acc) {
+        pick = 0;
+      } else {
+        for (int32_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+          if (!((al[col[e] / 32] >> (col[e] % 32)) & 1u)) continue;
+          acc = acc + val[e];
+          last = col[e] + 1;
+          llast = ln_val[e];
+          if (t < acc) {
+            pick = col[e] + 1;
+            lpick = ln_val[e];
+            break;
+          }
+        }
+        if (pick < 0) {
+          pick = last;
+          lpick = llast;
+        }
+      }
+      th[i] = pick;
+      lw += lpick;
+      if (pick > 0) detected[pick - 1] = 1;
+    }
+    int missed = 0;
+    for (int32_t j = 0; j < T; ++j)
+      if (((al[j / 32] >> (j % 32)) & 1u) && !detected[j]) ++missed;
+    lw += (double)missed * log(1.0 - (double)p_d);
+    logw[q] = lw;
+    free(detected);
+  }
+}
+
+/* O12 De-duplication, P:46 ("yielding a large set of new assignment
+ * hypotheses from which only the unique hypotheses are retained"): within a
+ * parent, sample s is unique iff no earlier sample s' < s has the same
+ * surviving-track set and the same association map (R27). */
+void oracle_dedup(int32_t H_old, int32_t H_up, int32_t M, const uint32_t *alive,
+                  int64_t ldt, const int32_t *theta, int64_t ldm, uint8_t *unique) {
+#pragma omp parallel for schedule(dynamic)
+  for (int32_t h = 0; h < H_old; ++h) {
+    for (int32_t s = 0; s < H_up; ++s) {
+      int64_t q = (int64_t)h * H_up + s;
+      int dup = 0;
+      for (int32_t s2 = 0; s2 < s && !dup; ++s2) {
+        int64_t q2 = (int64_t)h * H_up + s2;
+        int same = 1;
+        for (int64_t k = 0; k < ldt && same; ++k) same = alive[q * ldt + k] == alive[q2 * ldt + k];
+        for (int32_t i = 0; i < M && same; ++i) same = theta[q * ldm + i] == theta[q2 * ldm + i];
+        dup = same;
+      }
+      unique[q] = (uint8_t)!dup;
+    }
+  }
+}
+
+/* O13 Normalisation and pruning, P:53 (§Approach: "hypotheses with weights
+ * below a predefined threshold tau are discarded. Finally, the H_max most
+ * likely hypotheses are retained"): over the unique candidates,
+ * w_c = exp(lw_c - max) / sum; keep w_c >= tau (the largest is always kept);
+ * order by (w descending, index ascending); keep the first h_max; renormalise
+ * the kept weights to sum 1 (R29).  Returns the kept count. */
+int32_t oracle_prune(int32_t n, const double *logw, const uint8_t *unique, double tau,
+                     int32_t h_max, int32_t *keep_idx, double *keep_w) {
+  double m = -INFINITY;
+  int32_t arg = -1;
+  for (int32_t c = 0; c < n; ++c)
+    if (unique[c] && logw[c] > m) { m = logw[c]; arg = c; }
+  if (arg < 0 || h_max <= 0) return 0;
+  double s = 0.0;
+  for (int32_t c = 0; c < n; ++c)
+    if (unique[c]) s += exp(logw[c] - m);
+  int32_t *idx = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+  double *w = (double *)malloc(sizeof(double) * (size_t)n);
+  int32_t k = 0;
+  for (int32_t c = 0; c < n; ++c) {
+    if (!unique[c]) continue;
+    double wc = exp(logw[c] - m) / s;
+    if (wc >= tau || c == arg) { idx[k] = c; w[k] = wc; ++k; }
+  }
+  /* insertion sort by (w desc, index asc) */
+  for (int32_t a = 1; a < k; ++a) {
+    int32_t ia = idx[a];
+    double wa = w[a];
+    int32_t b = a - 1;
+    while (b >= 0 && (w[b] < wa || (w[b] == wa && idx[b] > ia))) {
+      idx[b + 1] = idx[b]; w[b + 1] = w[b]; --b;
+    }
+    idx[b + 1] = ia; w[b + 1] = wa;
+  }
+  int32_t nk = k < h_max ? k : h_max;
+  double sk = 0.0;
+  for (int32_t a = 0; a < nk; ++a) sk += w[a];
+  for (int32_t a = 0; a < nk; ++a) { keep_idx[a] = idx[a]; keep_w[a] = w[a] / sk; }
+  free(idx);
+  free(w);
+  return nk;
 }
