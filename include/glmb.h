@@ -238,6 +238,126 @@ glmb_status glmb_step_host(const glmb_step_params *prm, const float *Z_host,
                            float *log_norm_host, uint32_t *flags_host,
                            glmb_stream_t stream);
 
+/* =====================================================================
+ * Hypothesis machinery: the consumers of C_k.
+ * P:44-53 §Approach.  Readings R23-R29 in DESIGN.md §3.
+ * ===================================================================== */
+
+/* ---------------------------------------------------------------------
+ * glmb_death_prob -- posterior death probability d_prob(x_j) (P:44:
+ * "balancing its prior survival probability against the likelihood of it
+ * being detected"; the formula is deferred to a citation -- reading R23):
+ *   e_j = max_{i : g_ij} C[i, j+1] / (C[i, j+1] + kappa)   (0 if no gated i)
+ *   d_j = (1 - P_S,j) / ((1 - P_S,j) + P_S,j ((1 - P_D) + P_D e_j)),
+ *   d_j = 0 when P_S,j == 1.
+ * C_tracks [T][ldc] fp32 and gate [T][ldg] u32 exactly as glmb_compat writes
+ * them; p_s [T] fp32 prior survival probabilities; d_out [T] fp32 (computed
+ * in fp64, rounded once).
+ * Errors: INVALID_ARG on T < 0, M < 0, p_d not in (0,1], kappa < 0, ldc < M,
+ * ldg < ceil(M/32), NULL pointers with T > 0.
+ * --------------------------------------------------------------------- */
+glmb_status glmb_death_prob(int32_t T, int32_t M, const float *C_tracks,
+                            int64_t ldc, const uint32_t *gate, int64_t ldg,
+                            float p_d, float kappa, const float *p_s,
+                            float *d_out, glmb_stream_t stream);
+
+/* ---------------------------------------------------------------------
+ * glmb_compat_rows -- row-wise (CSR) copy of the gated entries of C_k: the
+ * rows that the categorical of P:44 ("normalizing the corresponding row in
+ * the modified matrix C'_k") is drawn from.
+ *   row_ptr [M+1] int32: row i's entries are [row_ptr[i], row_ptr[i+1]);
+ *           row_ptr[M] = nnz = number of set gate bits (always written,
+ *           even when nnz > cap)
+ *   col [cap] int32   track index j (C column j+1), ascending within a row
+ *   val [cap] fp32    C[i, j+1] copied bit-exactly
+ *   ln_val [cap] fp64 ln(val) (used by the hypothesis weight)
+ * Entries past `cap` are not written: the caller checks row_ptr[M] <= cap
+ * after the stream synchronises and re-runs with a larger cap otherwise.
+ * Errors: INVALID_ARG on negative sizes, NULL row_ptr, NULL outputs with
+ * cap > 0, or bad ldc / ldg.
+ * --------------------------------------------------------------------- */
+glmb_status glmb_compat_rows(int32_t T, int32_t M, const float *C_tracks,
+                             int64_t ldc, const uint32_t *gate, int64_t ldg,
+                             int32_t *row_ptr, int32_t *col, float *val,
+                             double *ln_val, int32_t cap, glmb_stream_t stream);
+
+/* ---------------------------------------------------------------------
+ * glmb_assoc_sample -- the two-stage association sampler and the
+ * successor hypothesis weight, for H_old parents x H_up samples.
+ * Sample q = h*H_up + s of parent h:
+ *  stage 1 ("a Bernoulli sampling step using d_prob to determine which
+ *   tracks survive"): for every track j set in parent_mask[h],
+ *   u = uniform24(word j%4 of Philox4x32-10(key(seed),
+ *                 counter (j/4, h, step, 2<<24 | s)))
+ *   alive_j = (u < 1.0f - d_prob[j])              (fp32 compare, R24/R25)
+ *  stage 2 ("for each measurement i, an association is sampled from a
+ *   categorical distribution defined by normalizing the corresponding row in
+ *   the modified matrix C'_k"): u_i from counter (i/4, h, step, 3<<24 | s),
+ *   word i%4; in fp32 with round-to-nearest adds in ascending column order,
+ *   total = kappa + sum_{alive gated j} C[i, j+1], t = u_i * total, theta_i =
+ *   the first column whose running sum (starting at kappa for column 0)
+ *   exceeds t; if rounding leaves none, the last alive gated column (R26).
+ *  weight ("multiplying its parent's weight with the joint likelihood of
+ *   the sampled survival/death events and data associations", R28), fp64:
+ *   logw = parent_logw[h] + sum_{j in parent} (alive ? ln P_S,j : ln(1-P_S,j))
+ *        + sum_i ln C'[i, theta_i] + #(alive j with no measurement) ln(1-P_D)
+ *   (ln C'[i, 0] = ln kappa; ln C'[i, j+1] = ln_val of the CSR entry).
+ * Inputs: parent_mask [H_old][ldt] u32 (bit j%32 of word j/32: track j is in
+ * parent h), ldt >= ceil(T/32), 1 <= ldt <= 12288; parent_logw [H_old] fp64;
+ * d_prob, p_s [T] fp32; the CSR of glmb_compat_rows (row_ptr [M+1], col,
+ * val, ln_val).
+ * Outputs: alive [H_old*H_up][ldt] u32 (bits of dead / absent tracks 0);
+ *   theta [H_old*H_up][ldm] int32 (0 = clutter, c >= 1 = C column c;
+ *   entries [M, ldm) not written; ldm % 4 == 0, theta 16-B aligned);
+ *   logw [H_old*H_up] fp64; hash [H_old*H_up] u64 (optional, may be NULL): a
+ *   64-bit fingerprint of (alive, theta) consumed by glmb_dedup.
+ * Results do not depend on the launch configuration (bit-exact integers).
+ * Errors: INVALID_ARG on negative sizes, H_up >= 2^24, H_old*H_up >= 2^31,
+ * p_d not in (0,1], kappa < 0, bad ldt / ldm, NULL pointers;
+ * ALIGNMENT on ldm % 4 != 0 or a misaligned theta.
+ * --------------------------------------------------------------------- */
+glmb_status glmb_assoc_sample(int32_t H_old, int32_t H_up, int32_t T, int32_t M,
+                              const uint32_t *parent_mask, int32_t ldt,
+                              const double *parent_logw, const float *d_prob,
+                              const float *p_s, float p_d, float kappa,
+                              const int32_t *row_ptr, const int32_t *col,
+                              const float *val, const double *ln_val,
+                              uint64_t seed, uint32_t step, uint32_t *alive,
+                              int32_t *theta, int64_t ldm, double *logw,
+                              uint64_t *hash, glmb_stream_t stream);
+
+/* ---------------------------------------------------------------------
+ * glmb_dedup -- unique successors ("only the unique hypotheses are
+ * retained", R27): unique[q] = 1 iff no earlier sample s2 < s of the same
+ * parent has identical alive words (ldt) and theta entries (M); exact (the
+ * fingerprints from glmb_assoc_sample only select the pairs compared).
+ * Errors: INVALID_ARG on negative sizes, ldt < 1, ldm < M, NULL pointers.
+ * --------------------------------------------------------------------- */
+glmb_status glmb_dedup(int32_t H_old, int32_t H_up, int32_t M,
+                       const uint32_t *alive, int32_t ldt, const int32_t *theta,
+                       int64_t ldm, const uint64_t *hash, uint8_t *unique,
+                       glmb_stream_t stream);
+
+/* ---------------------------------------------------------------------
+ * glmb_prune -- normalisation and pruning ("hypotheses with weights
+ * below a predefined threshold tau are discarded. Finally, the H_max most
+ * likely hypotheses are retained", R29), over the n candidates with
+ * unique[c] != 0:
+ *   w_c = exp(logw_c - max) / sum_c' exp(logw_c' - max)      (fp64)
+ *   keep w_c >= tau (the first maximiser is always kept); order by
+ *   (w desc, index asc); keep the first h_max; renormalise to sum 1.
+ * Outputs: keep_idx [h_max] int32 (candidate indices), keep_w [h_max] fp64,
+ * *n_kept (device int32) = the kept count k <= h_max (entries >= k untouched).
+ * workspace: [n] u64 device scratch.
+ * Errors: INVALID_ARG on n < 0, tau < 0 or NaN, h_max < 0 or
+ * h_max > GLMB_PRUNE_HMAX_LIMIT, NULL pointers.
+ * --------------------------------------------------------------------- */
+#define GLMB_PRUNE_HMAX_LIMIT 16384
+glmb_status glmb_prune(int32_t n, const double *logw, const uint8_t *unique,
+                       double tau, int32_t h_max, uint64_t *workspace,
+                       int32_t *keep_idx, double *keep_w, int32_t *n_kept,
+                       glmb_stream_t stream);
+
 /* ---------------------------------------------------------------------
  * Test hooks (not on the hot path; same device code as predict/birth).
  * glmb_philox_dump: out[n] = Philox4x32-10(key(seed), ctr[n]) for n < N.

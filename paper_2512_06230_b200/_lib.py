@@ -45,7 +45,8 @@ class glmb_step_params(C.Structure):
 
 EXPORTED = ["glmb_version", "glmb_status_string", "glmb_init", "glmb_sm_count", "glmb_predict",
             "glmb_birth", "glmb_compat", "glmb_reweight", "glmb_step", "glmb_step_host",
-            "glmb_philox_dump", "glmb_normals_dump"]
+            "glmb_philox_dump", "glmb_normals_dump", "glmb_death_prob", "glmb_compat_rows",
+            "glmb_assoc_sample", "glmb_dedup", "glmb_prune"]
 
 
 def load(path: str = LIB_PATH):
@@ -75,6 +76,12 @@ def load(path: str = LIB_PATH):
                                      vp, vp, vp, vp, vp, vp]
         L.glmb_philox_dump.argtypes = [u64, vp, i32, vp, vp]
         L.glmb_normals_dump.argtypes = [u64, vp, i32, vp, vp]
+        L.glmb_death_prob.argtypes = [i32, i32, vp, i64, vp, i64, f32, f32, vp, vp, vp]
+        L.glmb_compat_rows.argtypes = [i32, i32, vp, i64, vp, i64, vp, vp, vp, vp, i32, vp]
+        L.glmb_assoc_sample.argtypes = [i32, i32, i32, i32, vp, i32, vp, vp, vp, f32, f32, vp, vp, vp,
+                                        vp, u64, u32, vp, vp, i64, vp, vp, vp]
+        L.glmb_dedup.argtypes = [i32, i32, i32, vp, i32, vp, i64, vp, vp, vp]
+        L.glmb_prune.argtypes = [i32, vp, vp, C.c_double, i32, vp, vp, vp, vp, vp]
         for name in EXPORTED:
             if name not in ("glmb_version", "glmb_status_string", "glmb_sm_count"):
                 getattr(L, name).restype = C.c_int
@@ -229,3 +236,40 @@ def glmb_philox_dump(seed, ctr, out, stream=None):
 def glmb_normals_dump(seed, ctr, out, stream=None):
     _check(load().glmb_normals_dump(int(seed) & 0xFFFFFFFFFFFFFFFF, _ptr(ctr), ctr.shape[0],
                                     _ptr(out), _stream(stream)))
+
+
+# --------------------------------------------------------------- hypothesis machinery (f1, f3)
+def glmb_death_prob(C_tracks, gate, M, p_d, kappa, p_s, d_out, stream=None):
+    """C_tracks [T, ldc] fp32, gate [T, ldg] int32 words, p_s [T] fp32 -> d_out [T] fp32."""
+    T = C_tracks.shape[0]
+    _check(load().glmb_death_prob(T, int(M), _ptr(C_tracks), C_tracks.shape[1], _ptr(gate), gate.shape[1],
+                                  p_d, kappa, _ptr(p_s), _ptr(d_out), _stream(stream)))
+
+
+def glmb_compat_rows(C_tracks, gate, M, row_ptr, col, val, ln_val, stream=None):
+    """CSR of the gated entries: row_ptr [M+1] int32, col [cap] int32, val [cap] fp32, ln_val [cap] fp64."""
+    T = C_tracks.shape[0]
+    _check(load().glmb_compat_rows(T, int(M), _ptr(C_tracks), C_tracks.shape[1], _ptr(gate), gate.shape[1],
+                                   _ptr(row_ptr), _ptr(col), _ptr(val), _ptr(ln_val), col.shape[0],
+                                   _stream(stream)))
+
+
+def glmb_assoc_sample(H_up, parent_mask, parent_logw, d_prob, p_s, p_d, kappa, row_ptr, col, val, ln_val,
+                      M, seed, step, alive, theta, logw, hash=None, stream=None):
+    """parent_mask [H_old, ldt] int32 words; alive [H_old*H_up, ldt]; theta [H_old*H_up, ldm] int32."""
+    H_old, ldt = parent_mask.shape
+    T = d_prob.shape[0]
+    _check(load().glmb_assoc_sample(H_old, int(H_up), T, int(M), _ptr(parent_mask), ldt, _ptr(parent_logw),
+                                    _ptr(d_prob), _ptr(p_s), p_d, kappa, _ptr(row_ptr), _ptr(col), _ptr(val),
+                                    _ptr(ln_val), int(seed) & 0xFFFFFFFFFFFFFFFF, int(step), _ptr(alive),
+                                    _ptr(theta), theta.shape[1], _ptr(logw), _ptr(hash), _stream(stream)))
+
+
+def glmb_dedup(H_old, H_up, M, alive, theta, hash, unique, stream=None):
+    _check(load().glmb_dedup(int(H_old), int(H_up), int(M), _ptr(alive), alive.shape[1], _ptr(theta),
+                             theta.shape[1], _ptr(hash), _ptr(unique), _stream(stream)))
+
+
+def glmb_prune(logw, unique, tau, h_max, workspace, keep_idx, keep_w, n_kept, stream=None):
+    _check(load().glmb_prune(logw.shape[0], _ptr(logw), _ptr(unique), float(tau), int(h_max), _ptr(workspace),
+                             _ptr(keep_idx), _ptr(keep_w), _ptr(n_kept), _stream(stream)))

@@ -281,6 +281,88 @@ glmb_status glmb_step_host(const glmb_step_params *prm, const float *Z_host, int
   return from_cuda(cudaStreamSynchronize(s));
 }
 
+// ------------------------------------------------------------------ hypothesis machinery
+glmb_status glmb_death_prob(int32_t T, int32_t M, const float *C_tracks, int64_t ldc, const uint32_t *gate,
+                            int64_t ldg, float p_d, float kappa, const float *p_s, float *d_out,
+                            glmb_stream_t stream) {
+  if (T < 0 || M < 0 || !(p_d > 0.f && p_d <= 1.f) || !(kappa >= 0.f)) return GLMB_ERR_INVALID_ARG;
+  if (T == 0) return GLMB_OK;
+  if (p_s == nullptr || d_out == nullptr) return GLMB_ERR_INVALID_ARG;
+  if (M > 0 && (C_tracks == nullptr || gate == nullptr || ldc < M || ldg < (M + 31) / 32))
+    return GLMB_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  GLMB_TRY(bind_stream(s, nullptr));
+  glmb::DeathArgs a{T, M, C_tracks, ldc, gate, ldg, p_d, kappa, p_s, d_out};
+  return from_cuda(glmb::launch_death_prob(a, s));
+}
+
+glmb_status glmb_compat_rows(int32_t T, int32_t M, const float *C_tracks, int64_t ldc, const uint32_t *gate,
+                             int64_t ldg, int32_t *row_ptr, int32_t *col, float *val, double *ln_val, int32_t cap,
+                             glmb_stream_t stream) {
+  if (T < 0 || M < 0 || cap < 0) return GLMB_ERR_INVALID_ARG;
+  if (row_ptr == nullptr) return GLMB_ERR_INVALID_ARG;
+  if (T > 0 && M > 0 && (C_tracks == nullptr || gate == nullptr || ldc < M || ldg < (M + 31) / 32))
+    return GLMB_ERR_INVALID_ARG;
+  if (cap > 0 && (col == nullptr || val == nullptr || ln_val == nullptr)) return GLMB_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  GLMB_TRY(bind_stream(s, nullptr));
+  glmb::RowsArgs a{T, M, gate, ldg, C_tracks, ldc, row_ptr, col, val, ln_val, cap};
+  return from_cuda(glmb::launch_compat_rows(a, s));
+}
+
+glmb_status glmb_assoc_sample(int32_t H_old, int32_t H_up, int32_t T, int32_t M, const uint32_t *parent_mask,
+                              int32_t ldt, const double *parent_logw, const float *d_prob, const float *p_s,
+                              float p_d, float kappa, const int32_t *row_ptr, const int32_t *col, const float *val,
+                              const double *ln_val, uint64_t seed, uint32_t step, uint32_t *alive, int32_t *theta,
+                              int64_t ldm, double *logw, uint64_t *hash, glmb_stream_t stream) {
+  if (H_old < 0 || H_up < 0 || T < 0 || M < 0) return GLMB_ERR_INVALID_ARG;
+  if (H_up >= (1 << 24) || static_cast<int64_t>(H_old) * H_up > 0x7fffffffLL) return GLMB_ERR_INVALID_ARG;
+  if (!(p_d > 0.f && p_d <= 1.f) || !(kappa >= 0.f)) return GLMB_ERR_INVALID_ARG;
+  if (ldt < (T + 31) / 32 || ldt < 1 || ldt > 12 * 1024 || ldm < M) return GLMB_ERR_INVALID_ARG;
+  if (static_cast<int64_t>(H_old) * H_up == 0) return GLMB_OK;
+  if (parent_mask == nullptr || parent_logw == nullptr || alive == nullptr || logw == nullptr || row_ptr == nullptr)
+    return GLMB_ERR_INVALID_ARG;
+  if (T > 0 && (d_prob == nullptr || p_s == nullptr)) return GLMB_ERR_INVALID_ARG;
+  if (M > 0 && (theta == nullptr || col == nullptr || val == nullptr || ln_val == nullptr))
+    return GLMB_ERR_INVALID_ARG;
+  if (M > 0 && ((ldm & 3) || (reinterpret_cast<uintptr_t>(theta) & 15u))) return GLMB_ERR_ALIGNMENT;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  GLMB_TRY(bind_stream(s, nullptr));
+  glmb::SampleArgs a{H_old, H_up, T, M, parent_mask, ldt, parent_logw, d_prob, p_s, p_d, kappa, row_ptr, col, val,
+                     ln_val, static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32), step, alive, theta, ldm,
+                     logw, reinterpret_cast<unsigned long long *>(hash)};
+  return from_cuda(glmb::launch_assoc_sample(a, s));
+}
+
+glmb_status glmb_dedup(int32_t H_old, int32_t H_up, int32_t M, const uint32_t *alive, int32_t ldt,
+                       const int32_t *theta, int64_t ldm, const uint64_t *hash, uint8_t *unique,
+                       glmb_stream_t stream) {
+  if (H_old < 0 || H_up < 0 || M < 0 || ldt < 1 || ldm < M) return GLMB_ERR_INVALID_ARG;
+  if (static_cast<int64_t>(H_old) * H_up == 0) return GLMB_OK;
+  if (alive == nullptr || hash == nullptr || unique == nullptr || (M > 0 && theta == nullptr))
+    return GLMB_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  GLMB_TRY(bind_stream(s, nullptr));
+  glmb::DedupArgs a{H_old, H_up, M, ldt, ldm, alive, theta, reinterpret_cast<const unsigned long long *>(hash),
+                    unique};
+  return from_cuda(glmb::launch_dedup(a, s));
+}
+
+glmb_status glmb_prune(int32_t n, const double *logw, const uint8_t *unique, double tau, int32_t h_max,
+                       uint64_t *workspace, int32_t *keep_idx, double *keep_w, int32_t *n_kept,
+                       glmb_stream_t stream) {
+  if (n < 0 || h_max < 0 || h_max > GLMB_PRUNE_HMAX_LIMIT || !(tau >= 0.0)) return GLMB_ERR_INVALID_ARG;
+  if (n_kept == nullptr) return GLMB_ERR_INVALID_ARG;
+  if (n > 0 && (logw == nullptr || unique == nullptr || workspace == nullptr)) return GLMB_ERR_INVALID_ARG;
+  if (h_max > 0 && (keep_idx == nullptr || keep_w == nullptr)) return GLMB_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  GLMB_TRY(bind_stream(s, nullptr));
+  if (n == 0 || h_max == 0) return from_cuda(cudaMemsetAsync(n_kept, 0, sizeof(int32_t), s));
+  glmb::PruneArgs a{n, logw, unique, tau, h_max, glmb::prune_capacity(h_max),
+                    reinterpret_cast<unsigned long long *>(workspace), keep_idx, keep_w, n_kept};
+  return from_cuda(glmb::launch_prune(a, s));
+}
+
 glmb_status glmb_philox_dump(uint64_t seed, const uint32_t *ctr, int32_t N, uint32_t *out, glmb_stream_t stream) {
   if (N < 0 || (N > 0 && (ctr == nullptr || out == nullptr))) return GLMB_ERR_INVALID_ARG;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);

@@ -60,6 +60,69 @@ struct ReweightArgs {
   uint32_t *flags;
 };
 
+// ---- hypothesis machinery (hyp.cu)
+struct DeathArgs {
+  int32_t T, M;
+  const float *C_tracks;
+  int64_t ldc;
+  const uint32_t *gate;
+  int64_t ldg;
+  float p_d, kappa;
+  const float *p_s;
+  float *d_out;
+};
+
+struct RowsArgs {
+  int32_t T, M;
+  const uint32_t *gate;
+  int64_t ldg;
+  const float *C_tracks;
+  int64_t ldc;
+  int32_t *row_ptr, *col;
+  float *val;
+  double *ln_val;
+  int32_t cap;
+};
+
+struct SampleArgs {
+  int32_t H_old, H_up, T, M;
+  const uint32_t *parent_mask;
+  int32_t ldt;
+  const double *parent_logw;
+  const float *d_prob, *p_s;
+  float p_d, kappa;
+  const int32_t *row_ptr, *col;
+  const float *val;
+  const double *ln_val;
+  uint32_t key0, key1, step;
+  uint32_t *alive;
+  int32_t *theta;
+  int64_t ldm;
+  double *logw;
+  unsigned long long *hash;
+};
+
+struct DedupArgs {
+  int32_t H_old, H_up, M, ldt;
+  int64_t ldm;
+  const uint32_t *alive;
+  const int32_t *theta;
+  const unsigned long long *hash;
+  uint8_t *unique;
+};
+
+struct PruneArgs {
+  int32_t n;
+  const double *logw;
+  const uint8_t *unique;
+  double tau;
+  int32_t h_max, cap2;
+  unsigned long long *keys;  // workspace [n]
+  int32_t *keep_idx;
+  double *keep_w;
+  int32_t *n_kept;
+};
+
 cudaError_t launch_predict(const PredictArgs &a, int sm_count, cudaStream_t s);
 cudaError_t launch_birth(const BirthArgs &a, int sm_count, cudaStream_t s);
 cudaError_t launch_philox_dump(uint32_t k0, uint32_t k1, const uint32_t *ctr, int32_t n, uint32_t *out,
@@ -71,5 +134,11 @@ void compat_plan(int32_t M, int32_t P, int32_t *K, int32_t *n_mtiles);
 cudaError_t launch_compat(const CompatArgs &a, cudaStream_t s);
 cudaError_t launch_clutter_fill(float *C_clutter, int32_t M, float kappa, cudaStream_t s);
 cudaError_t launch_reweight(const ReweightArgs &a, cudaStream_t s);
+cudaError_t launch_death_prob(const DeathArgs &a, cudaStream_t s);
+cudaError_t launch_compat_rows(const RowsArgs &a, cudaStream_t s);
+cudaError_t launch_assoc_sample(const SampleArgs &a, cudaStream_t s);
+cudaError_t launch_dedup(const DedupArgs &a, cudaStream_t s);
+int32_t prune_capacity(int32_t h_max);
+cudaError_t launch_prune(const PruneArgs &a, cudaStream_t s);
 
 }  // namespace glmb

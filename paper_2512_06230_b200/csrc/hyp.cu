@@ -1,0 +1,599 @@
+// hyp.cu -- the hypothesis machinery that consumes C_k (
+// PAPER.md P:44-53 §Approach):
+//
+//   death_prob     d_j from the best gated entry of column j        (reading R23)
+//   compat_rows    row-wise (CSR) copy of the gated entries of C_k   (the rows P:46 normalises)
+//   assoc_sample   two-stage sampler: Bernoulli survival, then one categorical
+//                  per measurement row of C'_k; log-weight of each sample
+//   dedup          first occurrence of each (alive set, theta) within a parent
+//   prune          normalise, drop w < tau, keep the H_max most likely
+//
+// Integer outcomes (alive bits, theta) are decided in fp32 exactly as the
+// readings R25/R26 state, so they are bit-identical to any implementation that
+// follows them; log-weights accumulate in fp64.
+#include "glmb_device.cuh"
+#include "glmb_internal.h"
+
+namespace glmb {
+namespace {
+
+constexpr uint32_t kDomainSurvive = 2u, kDomainAssoc = 3u;
+
+// ------------------------------------------------------------------ death probability
+// One warp per track column: e_j = max over gated i of r_i = C[i, j+1] / (C[i, j+1] + kappa),
+// then d_j = (1 - P_S) / ((1 - P_S) + P_S ((1 - P_D) + P_D e_j)).  fp64 with explicitly
+// rounded operations (no FMA contraction): IEEE-exact steps, so d_j is reproducible.
+__global__ void __launch_bounds__(256) death_prob_kernel(DeathArgs a) {
+  const int32_t j = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (j >= a.T) return;
+  const float *col = a.C_tracks + static_cast<int64_t>(j) * a.ldc;
+  const uint32_t *g = a.gate + static_cast<int64_t>(j) * a.ldg;
+  const double kappa = static_cast<double>(a.kappa);
+  double e = 0.0;
+  for (int32_t i0 = 0; i0 < a.M; i0 += 32) {
+    const uint32_t word = __ldg(g + (i0 >> 5));
+    const int32_t i = i0 + lane;
+    if (i < a.M && ((word >> lane) & 1u)) {
+      const double c = static_cast<double>(__ldg(col + i));
+      e = fmax(e, __ddiv_rn(c, __dadd_rn(c, kappa)));
+    }
+  }
+  e = warp_max_d(e);
+  if (lane == 0) {
+    const double ps = static_cast<double>(__ldg(a.p_s + j)), pd = static_cast<double>(a.p_d);
+    const double dead = __dsub_rn(1.0, ps);
+    const double detect = __dadd_rn(__dsub_rn(1.0, pd), __dmul_rn(pd, e));
+    a.d_out[j] = ps == 1.0 ? 0.0f : __double2float_rn(__ddiv_rn(dead, __dadd_rn(dead, __dmul_rn(ps, detect))));
+  }
+}
+
+// ------------------------------------------------------------------ CSR of the gated entries
+// CTA = 32 consecutive rows (one gate word column w), 8 warps; warp k owns the
+// contiguous track chunk [k*ch, (k+1)*ch) so entries come out in ascending j.
+constexpr int kRowWarps = 8;
+
+__device__ __forceinline__ void row_chunk(int32_t T, int k, int32_t &j0, int32_t &j1) {
+  const int32_t ch = (T + kRowWarps - 1) / kRowWarps;
+  j0 = min(T, k * ch);
+  j1 = min(T, j0 + ch);
+}
+
+__global__ void __launch_bounds__(kRowWarps * 32) rows_count_kernel(RowsArgs a) {
+  __shared__ int32_t cnt[kRowWarps][32];
+  const int w = blockIdx.x, lane = threadIdx.x & 31, k = threadIdx.x >> 5;
+  int32_t j0, j1;
+  row_chunk(a.T, k, j0, j1);
+  int32_t c = 0;
+  for (int32_t j = j0; j < j1; ++j) c += (__ldg(a.gate + static_cast<int64_t>(j) * a.ldg + w) >> lane) & 1u;
+  cnt[k][lane] = c;
+  __syncthreads();
+  if (k == 0) {
+    int32_t s = 0;
+#pragma unroll
+    for (int q = 0; q < kRowWarps; ++q) s += cnt[q][lane];
+    const int32_t i = w * 32 + lane;
+    if (i < a.M) a.row_ptr[i] = s;
+  }
+}
+
+// exclusive scan of row_ptr[0..M) in place, row_ptr[M] = total (one CTA)
+__global__ void __launch_bounds__(1024) rows_scan_kernel(int32_t *row_ptr, int32_t M) {
+  __shared__ int32_t wsum[32];
+  __shared__ int32_t carry_s;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry_s = 0;
+  __syncthreads();
+  for (int32_t base = 0; base < M; base += 1024) {
+    const int32_t i = base + threadIdx.x;
+    const int32_t v = i < M ? row_ptr[i] : 0;
+    int32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      int32_t s = wsum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, s, o);
+        if (lane >= o) s += y;
+      }
+      wsum[lane] = s;  // inclusive warp-total prefix
+    }
+    __syncthreads();
+    const int32_t carry = carry_s;
+    const int32_t excl = carry + (wid ? wsum[wid - 1] : 0) + x - v;
+    if (i < M) row_ptr[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == 0) carry_s = carry + wsum[31];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) row_ptr[M] = carry_s;
+}
+
+__global__ void __launch_bounds__(kRowWarps * 32) rows_fill_kernel(RowsArgs a) {
+  __shared__ int32_t cnt[kRowWarps][32];
+  const int w = blockIdx.x, lane = threadIdx.x & 31, k = threadIdx.x >> 5;
+  int32_t j0, j1;
+  row_chunk(a.T, k, j0, j1);
+  int32_t c = 0;
+  for (int32_t j = j0; j < j1; ++j) c += (__ldg(a.gate + static_cast<int64_t>(j) * a.ldg + w) >> lane) & 1u;
+  cnt[k][lane] = c;
+  __syncthreads();
+  const int32_t i = w * 32 + lane;
+  if (i >= a.M) return;
+  int32_t pos = a.row_ptr[i];
+  for (int q = 0; q < k; ++q) pos += cnt[q][lane];
+  for (int32_t j = j0; j < j1; ++j) {
+    if ((__ldg(a.gate + static_cast<int64_t>(j) * a.ldg + w) >> lane) & 1u) {
+      if (pos < a.cap) {
+        const float v = __ldg(a.C_tracks + static_cast<int64_t>(j) * a.ldc + i);
+        a.col[pos] = j;
+        a.val[pos] = v;
+        a.ln_val[pos] = log(static_cast<double>(v));
+      }
+      ++pos;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ two-stage sampler
+// One CTA per sample q = h * H_up + s.  Shared memory: the sample's alive set
+// and its detected-track set (ldt words each).
+constexpr int kSampThreads = 128;
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {  // SplitMix64 finaliser
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t fp_term(uint32_t v, uint64_t idx) {
+  return mix64((idx << 32) ^ v ^ 0x9E3779B97F4A7C15ull);
+}
+
+template <typename Tv>
+__device__ __forceinline__ Tv block_sum_128(Tv v, Tv *red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  const Tv r = (red[0] + red[1]) + (red[2] + red[3]);
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a) {
+  extern __shared__ uint32_t sm[];
+  uint32_t *alive = sm, *det = sm + a.ldt;
+  __shared__ double red_d[4];
+  __shared__ unsigned long long red_u[4];
+  __shared__ int32_t red_i[4];
+  const int64_t q = blockIdx.x;
+  const int32_t h = static_cast<int32_t>(q / a.H_up), s = static_cast<int32_t>(q - static_cast<int64_t>(h) * a.H_up);
+  const uint32_t *pm = a.parent_mask + static_cast<int64_t>(h) * a.ldt;
+  for (int32_t k = threadIdx.x; k < a.ldt; k += kSampThreads) {
+    alive[k] = 0u;
+    det[k] = 0u;
+  }
+  __syncthreads();
+
+  // stage 1: track j of the parent survives iff u_j < 1 - d_j (fp32, R25);
+  // Philox block (j/4, h, step, 2<<24 | s), word j%4
+  double lw = 0.0;
+  const int32_t tquads = (a.T + 3) >> 2;
+  for (int32_t t = threadIdx.x; t < tquads; t += kSampThreads) {
+    const u32x4 r = philox4x32_10(
+        u32x4{static_cast<uint32_t>(t), static_cast<uint32_t>(h), a.step, (kDomainSurvive << 24) | static_cast<uint32_t>(s)},
+        a.key0, a.key1);
+    const uint32_t pmw = __ldg(pm + ((4 * t) >> 5));
+    uint32_t bits = 0u;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int32_t j = 4 * t + e;
+      if (j >= a.T || !((pmw >> (j & 31)) & 1u)) continue;
+      const float thr = __fsub_rn(1.0f, __ldg(a.d_prob + j));
+      const bool al = uniform24(e == 0 ? r.a : e == 1 ? r.b : e == 2 ? r.c : r.d) < thr;
+      const double ps = static_cast<double>(__ldg(a.p_s + j));
+      lw += al ? log(ps) : log(1.0 - ps);
+      bits |= static_cast<uint32_t>(al) << e;
+    }
+    if (bits) atomicOr(alive + ((4 * t) >> 5), bits << ((4 * t) & 31));
+  }
+  __syncthreads();
+
+  // stage 2: each row i draws theta_i from the row of C'_k (clutter kappa,
+  // surviving gated columns in ascending order), inverse CDF in fp32 (R26);
+  // Philox block (i/4, h, step, 3<<24 | s), word i%4
+  const double ln_kappa = log(static_cast<double>(a.kappa));
+  int32_t *th = a.theta + q * a.ldm;
+  uint64_t fp = 0ull;
+  const int32_t mquads = (a.M + 3) >> 2;
+  for (int32_t t = threadIdx.x; t < mquads; t += kSampThreads) {
+    const u32x4 r = philox4x32_10(
+        u32x4{static_cast<uint32_t>(t), static_cast<uint32_t>(h), a.step, (kDomainAssoc << 24) | static_cast<uint32_t>(s)},
+        a.key0, a.key1);
+    int32_t pick4[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int32_t i = 4 * t + e;
+      if (i >= a.M) continue;
+      const uint32_t rwe = e == 0 ? r.a : e == 1 ? r.b : e == 2 ? r.c : r.d;
+      const int32_t e0 = __ldg(a.row_ptr + i), e1 = __ldg(a.row_ptr + i + 1);
+      float total = a.kappa;
+      for (int32_t x = e0; x < e1; ++x) {
+        const int32_t j = __ldg(a.col + x);
+        if ((alive[j >> 5] >> (j & 31)) & 1u) total = __fadd_rn(total, __ldg(a.val + x));
+      }
+      const float tt = __fmul_rn(uniform24(rwe), total);
+      float acc = a.kappa;
+      int32_t pick = -1, last = 0;
+      double lpick = ln_kappa, llast = ln_kappa;
+      if (tt < acc) {
+        pick = 0;
+      } else {
+        for (int32_t x = e0; x < e1; ++x) {
+          const int32_t j = __ldg(a.col + x);
+          if (!((alive[j >> 5] >> (j & 31)) & 1u)) continue;
+          acc = __fadd_rn(acc, __ldg(a.val + x));
+          last = j + 1;
+          llast = __ldg(a.ln_val + x);
+          if (tt < acc) {
+            pick = j + 1;
+            lpick = llast;
+            break;
+          }
+        }
+        if (pick < 0) {
+          pick = last;
+          lpick = llast;
+        }
+      }
+      pick4[e] = pick;
+      lw += lpick;
+      if (pick > 0) atomicOr(det + ((pick - 1) >> 5), 1u << ((pick - 1) & 31));
+      fp += fp_term(static_cast<uint32_t>(pick), static_cast<uint64_t>(a.ldt) + i);
+    }
+    const int32_t i0 = 4 * t;
+    if (i0 + 3 < a.M) {
+      *reinterpret_cast<int4 *>(th + i0) = make_int4(pick4[0], pick4[1], pick4[2], pick4[3]);
+    } else {
+      for (int e = 0; e < 4 && i0 + e < a.M; ++e) th[i0 + e] = pick4[e];
+    }
+  }
+  __syncthreads();
+
+  // missed detections: alive tracks with no measurement; fingerprint of the alive words
+  int32_t missed = 0;
+  uint32_t *al_out = a.alive + q * a.ldt;
+  for (int32_t k = threadIdx.x; k < a.ldt; k += kSampThreads) {
+    const uint32_t av = alive[k];
+    missed += __popc(av & ~det[k]);
+    al_out[k] = av;
+    fp += fp_term(av, static_cast<uint64_t>(k));
+  }
+  lw = block_sum_128(lw, red_d);
+  const unsigned long long fps = block_sum_128(static_cast<unsigned long long>(fp), red_u);
+  missed = block_sum_128(missed, red_i);
+  if (threadIdx.x == 0) {
+    a.logw[q] = __ldg(a.parent_logw + h) + lw + static_cast<double>(missed) * log(1.0 - static_cast<double>(a.p_d));
+    if (a.hash) a.hash[q] = fps;
+  }
+}
+
+// ------------------------------------------------------------------ dedup
+// One CTA per parent: sample s is a duplicate iff some s2 < s of the same parent
+// has the same fingerprint and the same (alive, theta) words.
+constexpr int kDedupThreads = 256, kDedupTile = 2048;
+
+__device__ bool same_sample(const DedupArgs &a, int64_t q1, int64_t q2) {
+  const uint32_t *A1 = a.alive + q1 * a.ldt, *A2 = a.alive + q2 * a.ldt;
+  for (int32_t k = 0; k < a.ldt; ++k)
+    if (A1[k] != A2[k]) return false;
+  const int32_t *T1 = a.theta + q1 * a.ldm, *T2 = a.theta + q2 * a.ldm;
+  for (int32_t i = 0; i < a.M; ++i)
+    if (T1[i] != T2[i]) return false;
+  return true;
+}
+
+__global__ void __launch_bounds__(kDedupThreads) dedup_kernel(DedupArgs a) {
+  __shared__ unsigned long long hs[kDedupTile];
+  const int32_t h = blockIdx.x;
+  const int64_t base = static_cast<int64_t>(h) * a.H_up;
+  for (int32_t s0 = 0; s0 < a.H_up; s0 += kDedupThreads) {
+    const int32_t s = s0 + threadIdx.x;
+    const unsigned long long mine = s < a.H_up ? a.hash[base + s] : 0ull;
+    bool dup = false;
+    const int32_t s_hi = min(a.H_up, s0 + kDedupThreads);  // largest s of this chunk + 1
+    for (int32_t t0 = 0; t0 < s_hi; t0 += kDedupTile) {
+      __syncthreads();
+      for (int32_t k = threadIdx.x; k < kDedupTile && t0 + k < s_hi; k += kDedupThreads) hs[k] = a.hash[base + t0 + k];
+      __syncthreads();
+      if (s < a.H_up && !dup) {
+        const int32_t lim = min(kDedupTile, s - t0);
+        for (int32_t k = 0; k < lim; ++k) {
+          if (hs[k] == mine && same_sample(a, base + s, base + t0 + k)) {
+            dup = true;
+            break;
+          }
+        }
+      }
+    }
+    if (s < a.H_up) a.unique[base + s] = dup ? 0 : 1;
+  }
+}
+
+// ------------------------------------------------------------------ prune
+// One CTA.  Keys: candidate c gets key = bits(w_c) + 1 (w_c >= 0, so the IEEE
+// bit pattern orders like the value), 0 otherwise.  The H_max largest keys are
+// found by an MSB-first radix select; ties at the threshold are taken in index
+// order; the kept set is bitonic-sorted by (w desc, index asc) in shared memory.
+constexpr int kPruneThreads = 1024;
+
+struct MaxArg {
+  double v;
+  int32_t i;
+};
+__device__ __forceinline__ MaxArg better(MaxArg x, MaxArg y) {
+  if (y.i < 0) return x;
+  if (x.i < 0) return y;
+  if (y.v > x.v || (y.v == x.v && y.i < x.i)) return y;
+  return x;
+}
+
+__global__ void __launch_bounds__(kPruneThreads) prune_kernel(PruneArgs a) {
+  extern __shared__ unsigned char psm[];
+  unsigned long long *skey = reinterpret_cast<unsigned long long *>(psm);  // [cap2]
+  int32_t *sidx = reinterpret_cast<int32_t *>(skey + a.cap2);              // [cap2]
+  __shared__ double sd[32];
+  __shared__ int32_t si[32];
+  __shared__ uint32_t hist[256];
+  __shared__ unsigned long long prefix_s;
+  __shared__ int32_t need_s, carry_s, tiecarry_s;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int32_t n = a.n;
+
+  // (1) max / first argmax over unique candidates
+  MaxArg m{-INFINITY, -1};
+  for (int32_t c = threadIdx.x; c < n; c += kPruneThreads)
+    if (a.unique[c]) m = better(m, MaxArg{a.logw[c], c});
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    MaxArg y{__shfl_xor_sync(0xffffffffu, m.v, o), __shfl_xor_sync(0xffffffffu, m.i, o)};
+    m = better(m, y);
+  }
+  if (lane == 0) { sd[wid] = m.v; si[wid] = m.i; }
+  __syncthreads();
+  if (wid == 0) {
+    m = MaxArg{sd[lane], si[lane]};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      MaxArg y{__shfl_xor_sync(0xffffffffu, m.v, o), __shfl_xor_sync(0xffffffffu, m.i, o)};
+      m = better(m, y);
+    }
+    if (lane == 0) { sd[0] = m.v; si[0] = m.i; }
+  }
+  __syncthreads();
+  const double mx = sd[0];
+  const int32_t arg = si[0];
+  __syncthreads();
+  if (arg < 0 || a.h_max <= 0) {
+    if (threadIdx.x == 0) *a.n_kept = 0;
+    return;
+  }
+  // (2) s = sum exp(lw - max), fixed order
+  double acc = 0.0;
+  for (int32_t c = threadIdx.x; c < n; c += kPruneThreads)
+    if (a.unique[c]) acc += exp(a.logw[c] - mx);
+  acc = warp_sum_d(acc);
+  if (lane == 0) sd[wid] = acc;
+  __syncthreads();
+  if (wid == 0) {
+    acc = warp_sum_d(sd[lane]);
+    if (lane == 0) sd[0] = acc;
+  }
+  __syncthreads();
+  const double ssum = sd[0];
+  // (3) keys
+  int32_t cnt = 0;
+  for (int32_t c = threadIdx.x; c < n; c += kPruneThreads) {
+    unsigned long long key = 0ull;
+    if (a.unique[c]) {
+      const double w = exp(a.logw[c] - mx) / ssum;
+      if (w >= a.tau || c == arg) key = static_cast<unsigned long long>(__double_as_longlong(w)) + 1ull;
+    }
+    a.keys[c] = key;
+    cnt += key != 0ull;
+  }
+  __syncthreads();
+  // total candidates
+  {
+    int32_t v = cnt;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) si[wid] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int32_t t = 0;
+      for (int q = 0; q < 32; ++q) t += si[q];
+      need_s = t;
+    }
+    __syncthreads();
+  }
+  const int32_t K = need_s;
+  const int32_t nk = min(K, a.h_max);
+  // (4) radix select of the nk-th largest key (threshold thr: keep key > thr, plus
+  //     the first `ties` keys == thr in index order)
+  unsigned long long thr = 1ull;  // K <= h_max: keep every key >= 1
+  int32_t ties = 0;
+  bool select = K > a.h_max;
+  if (select) {
+    if (threadIdx.x == 0) { prefix_s = 0ull; need_s = a.h_max; }
+    __syncthreads();
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      for (int b = threadIdx.x; b < 256; b += kPruneThreads) hist[b] = 0u;
+      __syncthreads();
+      const unsigned long long pre = prefix_s;
+      const unsigned long long hmask = shift == 56 ? 0ull : (~0ull << (shift + 8));
+      for (int32_t c = threadIdx.x; c < n; c += kPruneThreads) {
+        const unsigned long long key = a.keys[c];
+        if ((key & hmask) == pre) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int32_t need = need_s;
+        int b = 255;
+        for (; b > 0; --b) {
+          if (static_cast<int32_t>(hist[b]) >= need) break;
+          need -= static_cast<int32_t>(hist[b]);
+        }
+        need_s = need;
+        prefix_s = pre | (static_cast<unsigned long long>(b) << shift);
+      }
+      __syncthreads();
+    }
+    thr = prefix_s;
+    ties = need_s;  // how many keys == thr to keep
+    __syncthreads();
+  }
+  // (5) compaction in index order: kept = key > thr (select) or key >= thr (no select)
+  if (threadIdx.x == 0) { carry_s = 0; tiecarry_s = 0; }
+  __syncthreads();
+  for (int32_t base = 0; base < n; base += kPruneThreads) {
+    const int32_t c = base + threadIdx.x;
+    const unsigned long long key = c < n ? a.keys[c] : 0ull;
+    const bool gt = select ? key > thr : key >= thr;
+    const bool tie = select && key == thr;
+    // rank of this tie among ties (index order)
+    const uint32_t tb = __ballot_sync(0xffffffffu, tie);
+    __syncthreads();
+    if (lane == 0) { si[wid] = __popc(tb); }
+    __syncthreads();
+    int32_t tie_before = tiecarry_s;
+    for (int q = 0; q < wid; ++q) tie_before += si[q];
+    tie_before += __popc(tb & ((1u << lane) - 1u));
+    int32_t tie_tot = 0;
+    for (int q = 0; q < 32; ++q) tie_tot += si[q];
+    const bool keep = gt || (tie && tie_before < ties);
+    const uint32_t kb = __ballot_sync(0xffffffffu, keep);
+    __syncthreads();
+    if (lane == 0) si[wid] = __popc(kb);
+    __syncthreads();
+    int32_t pos = carry_s;
+    for (int q = 0; q < wid; ++q) pos += si[q];
+    pos += __popc(kb & ((1u << lane) - 1u));
+    int32_t keep_tot = 0;
+    for (int q = 0; q < 32; ++q) keep_tot += si[q];
+    if (keep && pos < a.cap2) {
+      skey[pos] = key;
+      sidx[pos] = c;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) { carry_s += keep_tot; tiecarry_s += tie_tot; }
+    __syncthreads();
+  }
+  // pad to cap2 with sentinels (key 0 sorts last)
+  for (int32_t p = nk + threadIdx.x; p < a.cap2; p += kPruneThreads) {
+    skey[p] = 0ull;
+    sidx[p] = 0x7fffffff;
+  }
+  __syncthreads();
+  // (6) bitonic sort, descending by key, ascending by index
+  for (int32_t size = 2; size <= a.cap2; size <<= 1) {
+    for (int32_t stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int32_t p = threadIdx.x; p < a.cap2; p += kPruneThreads) {
+        const int32_t o = p ^ stride;
+        if (o > p) {
+          const bool desc = (p & size) == 0;
+          const unsigned long long k1 = skey[p], k2 = skey[o];
+          const int32_t i1 = sidx[p], i2 = sidx[o];
+          // "p before o" in the target order (key desc, idx asc)
+          const bool before = k1 > k2 || (k1 == k2 && i1 < i2);
+          if (before != desc) {
+            skey[p] = k2; skey[o] = k1;
+            sidx[p] = i2; sidx[o] = i1;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // (7) renormalise the kept weights
+  double ws = 0.0;
+  for (int32_t p = threadIdx.x; p < nk; p += kPruneThreads)
+    ws += __longlong_as_double(static_cast<long long>(skey[p] - 1ull));
+  ws = warp_sum_d(ws);
+  if (lane == 0) sd[wid] = ws;
+  __syncthreads();
+  if (wid == 0) {
+    ws = warp_sum_d(sd[lane]);
+    if (lane == 0) sd[0] = ws;
+  }
+  __syncthreads();
+  const double wsum = sd[0];
+  for (int32_t p = threadIdx.x; p < nk; p += kPruneThreads) {
+    a.keep_idx[p] = sidx[p];
+    a.keep_w[p] = __longlong_as_double(static_cast<long long>(skey[p] - 1ull)) / wsum;
+  }
+  if (threadIdx.x == 0) *a.n_kept = nk;
+}
+
+}  // namespace
+
+cudaError_t launch_death_prob(const DeathArgs &a, cudaStream_t s) {
+  death_prob_kernel<<<(a.T + 7) / 8, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compat_rows(const RowsArgs &a, cudaStream_t s) {
+  const int32_t words = (a.M + 31) / 32;
+  if (a.T > 0 && words > 0) {
+    rows_count_kernel<<<words, kRowWarps * 32, 0, s>>>(a);
+  } else if (a.M > 0) {
+    cudaError_t e = cudaMemsetAsync(a.row_ptr, 0, sizeof(int32_t) * a.M, s);
+    if (e != cudaSuccess) return e;
+  }
+  rows_scan_kernel<<<1, 1024, 0, s>>>(a.row_ptr, a.M);
+  if (a.T > 0 && words > 0) rows_fill_kernel<<<words, kRowWarps * 32, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_assoc_sample(const SampleArgs &a, cudaStream_t s) {
+  const int64_t n = static_cast<int64_t>(a.H_old) * a.H_up;
+  const size_t smem = sizeof(uint32_t) * 2 * static_cast<size_t>(a.ldt);
+  if (smem > 40 * 1024) {  // dynamic + static shared memory past the 48 KB default
+    cudaError_t e = cudaFuncSetAttribute(assoc_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  assoc_sample_kernel<<<static_cast<unsigned>(n), kSampThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dedup(const DedupArgs &a, cudaStream_t s) {
+  dedup_kernel<<<a.H_old, kDedupThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+int32_t prune_capacity(int32_t h_max) {
+  int32_t c = 1;
+  while (c < h_max) c <<= 1;
+  return c;
+}
+
+cudaError_t launch_prune(const PruneArgs &a, cudaStream_t s) {
+  const size_t smem = static_cast<size_t>(a.cap2) * (sizeof(unsigned long long) + sizeof(int32_t));
+  if (smem > 40 * 1024) {  // dynamic + static shared memory past the 48 KB default
+    cudaError_t e =
+        cudaFuncSetAttribute(prune_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  prune_kernel<<<1, kPruneThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace glmb

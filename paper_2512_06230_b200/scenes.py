@@ -214,3 +214,47 @@ def random_cloud(T: int, P: int, seed: int, center_scale: float = 100.0,
     else:
         w = np.full((T, P), 1.0 / P, np.float32)
     return x, y, v, psi, om, w
+
+
+# ------------------------------------------------------------------ hypothesis-machinery inputs
+_S_HYP, _S_SYNC = 7, 8
+
+
+def hypothesis_inputs(T: int, B: int, H_old: int, seed: int, p_s_survivor: float = 0.99,
+                      p_s_birth: float = 0.1, p_in_parent: float = 0.9):
+    """Parent hypotheses over the T_k = T + B columns of C_k:
+    survivor j is in parent h with probability p_in_parent, births are in every parent
+    (LMB birth is added to each hypothesis); parent log-weights = ln of a sorted
+    Dirichlet(1) draw; prior survival p_s = p_s_survivor (survivors), p_s_birth (births).
+    Returns (parent_mask u32 [H_old][ldt], parent_logw f64 [H_old], p_s f32 [T+B])."""
+    Tk = T + B
+    ldt = max(1, (Tk + 31) // 32)
+    r = _rng(seed, _S_HYP, 0)
+    member = np.zeros((H_old, Tk), bool)
+    member[:, :T] = r.random((H_old, T)) < p_in_parent
+    member[:, T:] = True
+    mask = np.zeros((H_old, ldt), np.uint32)
+    for j in range(Tk):
+        mask[:, j // 32] |= (member[:, j].astype(np.uint32) << np.uint32(j % 32))
+    w = np.sort(r.dirichlet(np.ones(H_old)))[::-1] if H_old else np.zeros(0)
+    logw = np.log(np.maximum(w, 1e-300)).astype(np.float64)
+    p_s = np.concatenate([np.full(T, p_s_survivor), np.full(B, p_s_birth)]).astype(np.float32)
+    return mask, np.ascontiguousarray(logw), p_s
+
+
+def synthetic_compat(T: int, M: int, seed: int, p_d: float = 0.9, mean_gated: float = 1.5):
+    """A C_k-shaped sparse matrix without running the likelihood: each measurement row is
+    gated to Poisson(mean_gated) distinct random tracks with entries p_d * 10^U(-8, 0.3).
+    Returns (C_tracks fp32 [T][M], gate u32 [T][ceil(M/32)]) in glmb_compat's layout."""
+    r = _rng(seed, _S_SYNC, 0)
+    ldg = max(1, (M + 31) // 32)
+    C = np.zeros((max(T, 0), M), np.float32)
+    g = np.zeros((max(T, 0), ldg), np.uint32)
+    for i in range(M):
+        n = min(T, r.poisson(mean_gated))
+        if n == 0:
+            continue
+        js = r.choice(T, size=n, replace=False)
+        C[js, i] = (p_d * 10.0 ** r.uniform(-8, 0.3, n)).astype(np.float32)
+        g[js, i // 32] |= np.uint32(1 << (i % 32))
+    return C, g
