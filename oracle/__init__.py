@@ -85,6 +85,13 @@ def lib():
             L.oracle_dedup.argtypes = [C.c_int32] * 3 + [u32, C.c_int64, i32, C.c_int64, u8]
             L.oracle_prune.argtypes = [C.c_int32, f64, u8, C.c_double, C.c_int32, i32, f64]
             L.oracle_prune.restype = C.c_int32
+            L.oracle_assoc_pairs.argtypes = [C.c_int32, i32, u32, C.c_int64, i32, C.c_int64, C.c_int32,
+                                             C.c_int32, i32, i32, i32, i32]
+            L.oracle_assoc_pairs.restype = C.c_int32
+            L.oracle_reweight_pairs.argtypes = ([C.c_int32, C.c_int64, f32, f32, f32, f32]
+                                                + [C.c_float] * 3 + [C.c_int32, i32, i32, i32, f64, f64, u32, f64])
+            L.oracle_resample.argtypes = [C.c_int32, f32, C.c_uint64, C.c_uint32, C.c_int32, i32]
+            L.oracle_resample.restype = C.c_int
             L.oracle_num_threads.restype = C.c_int
             L.oracle_set_num_threads.argtypes = [C.c_int]
             _lib = L
@@ -289,3 +296,51 @@ def prune(logw, unique, tau, h_max):
     k = lib().oracle_prune(n, lw if n else np.zeros(1), u if n else np.zeros(1, np.uint8),
                            float(tau), int(h_max), idx, w)
     return idx[:k].copy(), w[:k].copy()
+
+
+# ----------------------------------------------------------------- O14-O16 (particle loop)
+def assoc_pairs(hyp_idx, alive, theta, T, M):
+    """Unique (track, measurement-set) pairs over the hypotheses hyp_idx (O14).
+    Returns (pair_track [K], pair_ptr [K+1], pair_meas [nnz], pair_of [n_hyp][T])."""
+    hi = np.ascontiguousarray(hyp_idx, np.int32)
+    al = np.ascontiguousarray(alive, np.uint32)
+    th = np.ascontiguousarray(theta, np.int32)
+    if th.shape[1] == 0:
+        th = np.zeros((th.shape[0], 1), np.int32)
+    n = len(hi)
+    cap = max(1, n * T)
+    pt = np.zeros(cap, np.int32)
+    pp = np.zeros(cap + 1, np.int32)
+    pm = np.zeros(max(1, n * M), np.int32)
+    po = np.zeros((max(n, 1), max(T, 1)), np.int32)
+    K = lib().oracle_assoc_pairs(n, hi if n else np.zeros(1, np.int32), al, al.shape[1], th, th.shape[1],
+                                 T, M, pt, pp, pm, po)
+    return pt[:K].copy(), pp[:K + 1].copy(), pm[:pp[K]].copy(), po[:n, :T].copy()
+
+
+def reweight_pairs(x, y, w, Z, R, pair_track, pair_ptr, pair_meas):
+    """Per-pair Bayes update (O15): (w' [K][P] fp64, logZ [K], flags [K] u32, ess [K])."""
+    x, y, w = _f32(x), _f32(y), _f32(w)
+    Z = _f32(Z).reshape(-1, 2)
+    if Z.shape[0] == 0:
+        Z = np.zeros((1, 2), np.float32)
+    P = x.shape[1]
+    K = len(pair_track)
+    wo = np.zeros((max(K, 1), P), np.float64)
+    lz = np.zeros(max(K, 1), np.float64)
+    fl = np.zeros(max(K, 1), np.uint32)
+    es = np.zeros(max(K, 1), np.float64)
+    pm = np.ascontiguousarray(pair_meas, np.int32)
+    lib().oracle_reweight_pairs(P, P, x, y, w, Z, float(R[0]), float(R[1]), float(R[2]), K,
+                                np.ascontiguousarray(pair_track if K else np.zeros(1), np.int32),
+                                np.ascontiguousarray(pair_ptr, np.int32),
+                                pm if len(pm) else np.zeros(1, np.int32), wo, lz, fl, es)
+    return wo[:K], lz[:K], fl[:K], es[:K]
+
+
+def resample(w, seed, step, k):
+    """Systematic resampling decision + ancestors of one weight vector (O16): (resampled, anc [P])."""
+    w = _f32(w)
+    anc = np.full(len(w), -1, np.int32)
+    r = lib().oracle_resample(len(w), w, C.c_uint64(seed), C.c_uint32(step), int(k), anc)
+    return bool(r), anc

@@ -567,3 +567,161 @@ int32_t oracle_prune(int32_t n, const double *logw, const uint8_t *unique, doubl
   free(w);
   return nk;
 }
+
+/* ==================================================================
+ * Particle loop after the hypothesis update: unique
+ * (track, measurement-set) pairs, the batched per-pair Bayes update with its
+ * effective sample size, and systematic resampling.  P:53 (§Approach).
+ * ================================================================== */
+
+/* O14 Unique association pairs, P:53 ("we perform a batched particle update
+ * for all unique (track, measurement) association pairs generated across the
+ * new set of hypotheses"), reading R30: for r = 0..n_hyp-1 (the given order,
+ * e.g. the pruned ranking) and hypothesis q = hyp_idx[r], every track j
+ * (ascending) alive in q gets the set S = {i : theta_q[i] = j+1} (ascending
+ * i).  The pair (j, S) is numbered on its first occurrence in that scan;
+ * pair_of[r][j] = its number, -1 for tracks not alive in q.
+ * Outputs: pair_track [n_pairs], pair_ptr [n_pairs+1], pair_meas [nnz]
+ * (capacities n_hyp*T and n_hyp*M suffice).  Returns n_pairs. */
+int32_t oracle_assoc_pairs(int32_t n_hyp, const int32_t *hyp_idx, const uint32_t *alive,
+                           int64_t ldt, const int32_t *theta, int64_t ldm, int32_t T,
+                           int32_t M, int32_t *pair_track, int32_t *pair_ptr,
+                           int32_t *pair_meas, int32_t *pair_of) {
+  int32_t K = 0, nnz = 0;
+  int32_t *S = (int32_t *)malloc(sizeof(int32_t) * (size_t)(M > 0 ? M : 1));
+  pair_ptr[0] = 0;
+  for (int32_t r = 0; r < n_hyp; ++r) {
+    int64_t q = hyp_idx[r];
+    const uint32_t *al = alive + q * ldt;
+    const int32_t *th = theta + q * ldm;
+    for (int32_t j = 0; j < T; ++j) {
+      if (!((al[j / 32] >> (j % 32)) & 1u)) {
+        pair_of[(int64_t)r * T + j] = -1;
+        continue;
+      }
+      int32_t n = 0;
+      for (int32_t i = 0; i < M; ++i)
+        if (th[i] == j + 1) S[n++] = i;
+      int32_t found = -1;
+      for (int32_t k = 0; k < K && found < 0; ++k) {
+        if (pair_track[k] != j || pair_ptr[k + 1] - pair_ptr[k] != n) continue;
+        int same = 1;
+        for (int32_t e = 0; e < n && same; ++e) same = pair_meas[pair_ptr[k] + e] == S[e];
+        if (same) found = k;
+      }
+      if (found < 0) {
+        found = K;
+        pair_track[K] = j;
+        for (int32_t e = 0; e < n; ++e) pair_meas[nnz + e] = S[e];
+        nnz += n;
+        pair_ptr[K + 1] = nnz;
+        ++K;
+      }
+      pair_of[(int64_t)r * T + j] = found;
+    }
+  }
+  free(S);
+  return K;
+}
+
+/* O15 Batched particle update over pairs, P:53 ("The particle weights are
+ * updated according to the measurement likelihood"): pair k updates the
+ * particles of track pair_track[k] with its set S_k exactly as O8 does for
+ * S_j (Bayes' rule, log normaliser, uniform reset + flag when every weight
+ * is zero; S_k empty: weights copied, logZ = ln sum w), and reports the
+ * effective sample size ESS_k = (sum_p w'_p)^2 / sum_p w'_p^2 of the new
+ * weights (Kong-Liu; reading R31).  w_out [K][P] fp64. */
+void oracle_reweight_pairs(int32_t P, int64_t ld, const float *x, const float *y,
+                           const float *w, const float *Z, float Rxx, float Rxy, float Ryy,
+                           int32_t K, const int32_t *pair_track, const int32_t *pair_ptr,
+                           const int32_t *pair_meas, double *w_out, double *logZ,
+                           uint32_t *flags, double *ess) {
+#pragma omp parallel for schedule(dynamic)
+  for (int32_t k = 0; k < K; ++k) {
+    int64_t base = (int64_t)pair_track[k] * ld;
+    double *wo = w_out + (int64_t)k * P;
+    int32_t e0 = pair_ptr[k], e1 = pair_ptr[k + 1];
+    flags[k] = 0u;
+    if (e1 == e0) {
+      double s = 0.0;
+      for (int32_t p = 0; p < P; ++p) {
+        wo[p] = (double)w[base + p];
+        s += wo[p];
+      }
+      logZ[k] = log(s);
+    } else {
+      double *l = (double *)malloc(sizeof(double) * (size_t)P);
+      double m = -INFINITY;
+      for (int32_t p = 0; p < P; ++p) {
+        double lp = log((double)w[base + p]);
+        for (int32_t e = e0; e < e1; ++e) {
+          int32_t i = pair_meas[e];
+          lp += oracle_loggauss2(Z[2 * i], Z[2 * i + 1], x[base + p], y[base + p], Rxx, Rxy, Ryy);
+        }
+        l[p] = lp;
+        if (lp > m) m = lp;
+      }
+      if (m == -INFINITY) {
+        for (int32_t p = 0; p < P; ++p) wo[p] = 1.0 / (double)P;
+        logZ[k] = -INFINITY;
+        flags[k] = 1u;
+      } else {
+        double s = 0.0;
+        for (int32_t p = 0; p < P; ++p) s += exp(l[p] - m);
+        for (int32_t p = 0; p < P; ++p) wo[p] = exp(l[p] - m) / s;
+        logZ[k] = m + log(s);
+      }
+      free(l);
+    }
+    double s1 = 0.0, s2 = 0.0;
+    for (int32_t p = 0; p < P; ++p) {
+      s1 += wo[p];
+      s2 += wo[p] * wo[p];
+    }
+    ess[k] = s2 > 0.0 ? s1 * s1 / s2 : 0.0;
+  }
+}
+
+/* O16 Systematic resampling of one weight vector, P:53 ("a resampling step
+ * is performed if necessary to prevent particle degeneracy"), readings R31,
+ * R32.  Weights are taken in units of 2^-26: W_m = floor(w_m 2^26) (exact
+ * for fp32 w in [0, 1]), S = sum W, Q = sum W^2 (exact integers).
+ *  - resample iff 2 S^2 < P Q, i.e. ESS = S^2/Q < P/2 (S = 0: no resample);
+ *  - U = 2 (r >> 9) + 1 with r = word 0 of Philox4x32-10(key(seed),
+ *    counter (k, 0, step, 4 << 24)) -- the same odd 24-bit integer as O3's
+ *    uniform u = U 2^-24 -- and V = floor(U S / 2^24);
+ *  - position n = 0..P-1: t_n = floor((n S + V) / P), the systematic grid
+ *    (u + n)/P of the total mass; ancestor a_n = min{m : W_0 + ... + W_m > t_n}.
+ * Returns 1 and fills anc [P] when it resamples, else returns 0 (anc
+ * untouched).  Requires P <= 2^14 (so every product fits 64 bits). */
+int oracle_resample(int32_t P, const float *w, uint64_t seed, uint32_t step, int32_t k,
+                    int32_t *anc) {
+  unsigned __int128 S = 0, Q = 0;
+  uint64_t *W = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)P);
+  for (int32_t m = 0; m < P; ++m) {
+    W[m] = (uint64_t)floor((double)w[m] * 67108864.0);
+    S += W[m];
+    Q += (unsigned __int128)W[m] * W[m];
+  }
+  int res = S > 0 && 2 * S * S < (unsigned __int128)P * Q;
+  if (res) {
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    uint32_t ctr[4] = {(uint32_t)k, 0u, step, 4u << 24};
+    uint32_t r[4];
+    oracle_philox4x32_10(ctr, key, r);
+    uint64_t U = 2ull * (r[0] >> 9) + 1ull;
+    uint64_t V = (uint64_t)((U * S) >> 24);
+    for (int32_t n = 0; n < P; ++n) {
+      uint64_t t = (uint64_t)(((unsigned __int128)n * S + V) / (unsigned)P);
+      uint64_t cum = 0;
+      int32_t a = P - 1;
+      for (int32_t m = 0; m < P; ++m) {
+        cum += W[m];
+        if (cum > t) { a = m; break; }
+      }
+      anc[n] = a;
+    }
+  }
+  free(W);
+  return res;
+}
