@@ -53,6 +53,7 @@
 #ifndef GLMB_H_
 #define GLMB_H_
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -357,6 +358,83 @@ glmb_status glmb_prune(int32_t n, const double *logw, const uint8_t *unique,
                        double tau, int32_t h_max, uint64_t *workspace,
                        int32_t *keep_idx, double *keep_w, int32_t *n_kept,
                        glmb_stream_t stream);
+
+/* =====================================================================
+ * Particle loop: unique association pairs, the batched
+ * per-pair particle update, systematic resampling.  P:53 §Approach.
+ * Readings R30-R32 in DESIGN.md §3.
+ * ===================================================================== */
+#define GLMB_PAIRS_PMAX 16384 /* particles per track for reweight_pairs / resample */
+
+/* ---------------------------------------------------------------------
+ * glmb_assoc_pairs -- the unique (track, measurement set) pairs of P:53 ("a
+ * batched particle update for all unique (track, measurement) association
+ * pairs generated across the new set of hypotheses", R30).
+ * For r = 0..n_hyp-1, hypothesis q = hyp_idx[r] (rows of the sampler's alive
+ * [.][ldt] / theta [.][ldm] outputs, e.g. glmb_prune's keep_idx), every track
+ * j < T alive in q has S = {i < M : theta_q[i] == j+1} (ascending).  Pairs
+ * are numbered by first occurrence in (r, j) order:
+ *   pair_track [K] int32, pair_ptr [K+1] int32 (pair k's measurements are
+ *   pair_meas[pair_ptr[k] .. pair_ptr[k+1])), pair_of [n_hyp][T] int32 (the
+ *   pair of (r, j), -1 if j is not alive in q), *n_pairs = K (device int32).
+ * Capacities: pair_track n_hyp*T, pair_ptr n_hyp*T + 1, pair_meas n_hyp*M.
+ * workspace: device scratch of glmb_assoc_pairs_workspace_size(n_hyp, T, M)
+ * bytes.  Exact (fingerprints only preselect the compared lists).
+ * Errors: INVALID_ARG on negative sizes, T > 17066, bad ldt / ldm, NULL
+ * pointers, a short workspace.
+ * --------------------------------------------------------------------- */
+size_t glmb_assoc_pairs_workspace_size(int32_t n_hyp, int32_t T, int32_t M);
+glmb_status glmb_assoc_pairs(int32_t n_hyp, const int32_t *hyp_idx,
+                             const uint32_t *alive, int32_t ldt,
+                             const int32_t *theta, int64_t ldm, int32_t T,
+                             int32_t M, int32_t *pair_track, int32_t *pair_ptr,
+                             int32_t *pair_meas, int32_t *pair_of,
+                             int32_t *n_pairs, void *workspace,
+                             size_t workspace_bytes, glmb_stream_t stream);
+
+/* ---------------------------------------------------------------------
+ * glmb_reweight_pairs -- the batched particle update over pairs: pair
+ * k updates the particles of source track pair_track[k] with S_k exactly as
+ * glmb_reweight does for S_j, writing row k of w_out ([K][ld_out] fp32),
+ * log_norm[k], flags[k] (bit 0: all weights zero, reset to uniform) and
+ * ess[k] = (sum w')^2 / sum w'^2 (fp32; R31).  S_k empty: weights copied.
+ * K is the capacity (grid size); n_pairs (device int32, may be NULL) limits
+ * the work to the first *n_pairs pairs, so the call can follow
+ * glmb_assoc_pairs without a host round trip.  src->n_particles <=
+ * GLMB_PAIRS_PMAX.
+ * Errors: INVALID_ARG (R not SPD, NULL pointers, P too large);
+ * ALIGNMENT (w_out, ld_out).
+ * --------------------------------------------------------------------- */
+glmb_status glmb_reweight_pairs(const glmb_particles *src, const float *Z,
+                                int32_t M, float Rxx, float Rxy, float Ryy,
+                                int32_t K, const int32_t *n_pairs,
+                                const int32_t *pair_track,
+                                const int32_t *pair_ptr,
+                                const int32_t *pair_meas, float *w_out,
+                                int64_t ld_out, float *log_norm,
+                                uint32_t *flags, float *ess,
+                                glmb_stream_t stream);
+
+/* ---------------------------------------------------------------------
+ * glmb_resample -- systematic resampling "if necessary" (R31/R32).
+ * For pair k (< K, and < *n_pairs if n_pairs != NULL), weights w[k][.]
+ * (fp32 in [0, 1], stride ldw) are taken as integers W_m = floor(w_m 2^26);
+ * S = sum W, Q = sum W^2 (exact).  If S > 0 and 2 S^2 < P Q (ESS < P/2):
+ *   U = 2 (r >> 9) + 1, r = word 0 of Philox4x32-10(key(seed), counter
+ *   (k, 0, step, 4 << 24)); V = floor(U S / 2^24);
+ *   slot n < P takes ancestor a_n = min{m : W_0 + ... + W_m > floor((n S + V) / P)}
+ *   out row k: (x, y, v, psi, omega) of src row pair_track[k] at a_n, w = 1/P;
+ *   flags[k] |= 2.
+ * Otherwise out row k = the source particles with weights w[k] (flags bit 1
+ * cleared).  `out` describes >= K rows (a new particle set, one row per pair);
+ * flags may be NULL.  P <= GLMB_PAIRS_PMAX.
+ * Errors: INVALID_ARG / ALIGNMENT as for the other particle calls.
+ * --------------------------------------------------------------------- */
+glmb_status glmb_resample(const glmb_particles *src, int32_t K,
+                          const int32_t *n_pairs, const int32_t *pair_track,
+                          const float *w, int64_t ldw,
+                          const glmb_particles *out, uint64_t seed,
+                          uint32_t step, uint32_t *flags, glmb_stream_t stream);
 
 /* ---------------------------------------------------------------------
  * Test hooks (not on the hot path; same device code as predict/birth).

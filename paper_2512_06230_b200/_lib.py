@@ -46,7 +46,8 @@ class glmb_step_params(C.Structure):
 EXPORTED = ["glmb_version", "glmb_status_string", "glmb_init", "glmb_sm_count", "glmb_predict",
             "glmb_birth", "glmb_compat", "glmb_reweight", "glmb_step", "glmb_step_host",
             "glmb_philox_dump", "glmb_normals_dump", "glmb_death_prob", "glmb_compat_rows",
-            "glmb_assoc_sample", "glmb_dedup", "glmb_prune"]
+            "glmb_assoc_sample", "glmb_dedup", "glmb_prune", "glmb_assoc_pairs_workspace_size",
+            "glmb_assoc_pairs", "glmb_reweight_pairs", "glmb_resample"]
 
 
 def load(path: str = LIB_PATH):
@@ -82,8 +83,16 @@ def load(path: str = LIB_PATH):
                                         vp, u64, u32, vp, vp, i64, vp, vp, vp]
         L.glmb_dedup.argtypes = [i32, i32, i32, vp, i32, vp, i64, vp, vp, vp]
         L.glmb_prune.argtypes = [i32, vp, vp, C.c_double, i32, vp, vp, vp, vp, vp]
+        L.glmb_assoc_pairs_workspace_size.argtypes = [i32, i32, i32]
+        L.glmb_assoc_pairs_workspace_size.restype = C.c_size_t
+        L.glmb_assoc_pairs.argtypes = [i32, vp, vp, i32, vp, i64, i32, i32, vp, vp, vp, vp, vp, vp,
+                                       C.c_size_t, vp]
+        L.glmb_reweight_pairs.argtypes = [PP, vp, i32, f32, f32, f32, i32, vp, vp, vp, vp, vp, i64, vp, vp,
+                                          vp, vp]
+        L.glmb_resample.argtypes = [PP, i32, vp, vp, vp, i64, PP, u64, u32, vp, vp]
         for name in EXPORTED:
-            if name not in ("glmb_version", "glmb_status_string", "glmb_sm_count"):
+            if name not in ("glmb_version", "glmb_status_string", "glmb_sm_count",
+                            "glmb_assoc_pairs_workspace_size"):
                 getattr(L, name).restype = C.c_int
         _lib = L
         return L
@@ -273,3 +282,34 @@ def glmb_dedup(H_old, H_up, M, alive, theta, hash, unique, stream=None):
 def glmb_prune(logw, unique, tau, h_max, workspace, keep_idx, keep_w, n_kept, stream=None):
     _check(load().glmb_prune(logw.shape[0], _ptr(logw), _ptr(unique), float(tau), int(h_max), _ptr(workspace),
                              _ptr(keep_idx), _ptr(keep_w), _ptr(n_kept), _stream(stream)))
+
+
+# --------------------------------------------------------------- particle loop (f2)
+def glmb_assoc_pairs_workspace_size(n_hyp, T, M) -> int:
+    return int(load().glmb_assoc_pairs_workspace_size(int(n_hyp), int(T), int(M)))
+
+
+def glmb_assoc_pairs(hyp_idx, alive, theta, T, M, pair_track, pair_ptr, pair_meas, pair_of, n_pairs,
+                     workspace, stream=None):
+    """hyp_idx [n_hyp] int32 rows of alive [., ldt] / theta [., ldm]; outputs as in glmb.h."""
+    n_hyp = hyp_idx.shape[0]
+    _check(load().glmb_assoc_pairs(n_hyp, _ptr(hyp_idx), _ptr(alive), alive.shape[1], _ptr(theta),
+                                   theta.shape[1], int(T), int(M), _ptr(pair_track), _ptr(pair_ptr),
+                                   _ptr(pair_meas), _ptr(pair_of), _ptr(n_pairs), _ptr(workspace),
+                                   workspace.numel() * workspace.element_size(), _stream(stream)))
+
+
+def glmb_reweight_pairs(src: Particles, Z, R, K, n_pairs, pair_track, pair_ptr, pair_meas, w_out, log_norm,
+                        flags, ess, stream=None):
+    t = src.struct()
+    _check(load().glmb_reweight_pairs(C.byref(t), _ptr(Z), Z.shape[0], R[0], R[1], R[2], int(K), _ptr(n_pairs),
+                                      _ptr(pair_track), _ptr(pair_ptr), _ptr(pair_meas), _ptr(w_out),
+                                      w_out.shape[1], _ptr(log_norm), _ptr(flags), _ptr(ess), _stream(stream)))
+
+
+def glmb_resample(src: Particles, K, n_pairs, pair_track, w, out: Particles, seed, step, flags=None,
+                  stream=None):
+    a, b = src.struct(), out.struct()
+    _check(load().glmb_resample(C.byref(a), int(K), _ptr(n_pairs), _ptr(pair_track), _ptr(w), w.shape[1],
+                                C.byref(b), int(seed) & 0xFFFFFFFFFFFFFFFF, int(step), _ptr(flags),
+                                _stream(stream)))

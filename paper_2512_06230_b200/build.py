@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libglmb.so")
-SOURCES = ["abi.cu", "kernels_rng.cu", "compat.cu", "reweight.cu", "hyp.cu"]
+SOURCES = ["abi.cu", "kernels_rng.cu", "compat.cu", "reweight.cu", "hyp.cu", "pairs.cu"]
 HEADERS = ["glmb_device.cuh", "glmb_internal.h", "peaks.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -212,6 +212,7 @@ glmb_status glmb_reweight(const glmb_particles *trk, float *w_out, const float *
   a.qc = h * rxx / det;
   a.log_norm1 = std::log(2.0 * 3.14159265358979323846 * std::sqrt(det));
   a.log_norm = log_norm; a.flags = flags;
+  a.ld_out = trk->ld;
   return from_cuda(glmb::launch_reweight(a, s));
 }
 
@@ -361,6 +362,93 @@ glmb_status glmb_prune(int32_t n, const double *logw, const uint8_t *unique, dou
   glmb::PruneArgs a{n, logw, unique, tau, h_max, glmb::prune_capacity(h_max),
                     reinterpret_cast<unsigned long long *>(workspace), keep_idx, keep_w, n_kept};
   return from_cuda(glmb::launch_prune(a, s));
+}
+
+// ------------------------------------------------------------------ particle loop (f2)
+size_t glmb_assoc_pairs_workspace_size(int32_t n_hyp, int32_t T, int32_t M) {
+  if (n_hyp < 0 || T < 0 || M < 0) return 0;
+  return glmb::pairs_workspace_bytes(n_hyp, T, M);
+}
+
+glmb_status glmb_assoc_pairs(int32_t n_hyp, const int32_t *hyp_idx, const uint32_t *alive, int32_t ldt,
+                             const int32_t *theta, int64_t ldm, int32_t T, int32_t M, int32_t *pair_track,
+                             int32_t *pair_ptr, int32_t *pair_meas, int32_t *pair_of, int32_t *n_pairs,
+                             void *workspace, size_t workspace_bytes, glmb_stream_t stream) {
+  if (n_hyp < 0 || T < 0 || M < 0 || ldt < (T + 31) / 32 || ldt < 1 || ldm < M) return GLMB_ERR_INVALID_ARG;
+  if (static_cast<int64_t>(n_hyp) * (T > M ? T : M) > 0x7fffffffLL) return GLMB_ERR_INVALID_ARG;
+  if (static_cast<size_t>(T) * 12 > 200 * 1024) return GLMB_ERR_INVALID_ARG;  // per-track shared-memory tables
+  if (n_pairs == nullptr || pair_ptr == nullptr) return GLMB_ERR_INVALID_ARG;
+  if (n_hyp > 0 && T > 0) {
+    if (hyp_idx == nullptr || alive == nullptr || pair_track == nullptr || pair_of == nullptr ||
+        (M > 0 && (theta == nullptr || pair_meas == nullptr)))
+      return GLMB_ERR_INVALID_ARG;
+    if (workspace == nullptr || workspace_bytes < glmb::pairs_workspace_bytes(n_hyp, T, M))
+      return GLMB_ERR_INVALID_ARG;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  GLMB_TRY(bind_stream(s, nullptr));
+  glmb::PairsArgs a{};
+  a.n_hyp = n_hyp; a.T = T; a.M = M; a.ldt = ldt; a.ldm = ldm; a.hyp_idx = hyp_idx; a.alive = alive;
+  a.theta = theta; a.pair_track = pair_track; a.pair_ptr = pair_ptr; a.pair_meas = pair_meas;
+  a.pair_of = pair_of; a.n_pairs = n_pairs;
+  return from_cuda(glmb::launch_assoc_pairs(a, workspace, s));
+}
+
+glmb_status glmb_reweight_pairs(const glmb_particles *src, const float *Z, int32_t M, float Rxx, float Rxy,
+                                float Ryy, int32_t K, const int32_t *n_pairs, const int32_t *pair_track,
+                                const int32_t *pair_ptr, const int32_t *pair_meas, float *w_out, int64_t ld_out,
+                                float *log_norm, uint32_t *flags, float *ess, glmb_stream_t stream) {
+  GLMB_TRY(check_particles(src, true, false));
+  if (K < 0 || M < 0 || !spd(Rxx, Rxy, Ryy)) return GLMB_ERR_INVALID_ARG;
+  if (K == 0) return GLMB_OK;
+  if (src->n_tracks == 0 || src->n_particles > GLMB_PAIRS_PMAX) return GLMB_ERR_INVALID_ARG;
+  if (pair_track == nullptr || pair_ptr == nullptr || w_out == nullptr || log_norm == nullptr ||
+      flags == nullptr || ess == nullptr)
+    return GLMB_ERR_INVALID_ARG;
+  if (M > 0 && (Z == nullptr || pair_meas == nullptr)) return GLMB_ERR_INVALID_ARG;
+  if (ld_out < src->n_particles || (ld_out & 3)) return GLMB_ERR_ALIGNMENT;
+  if ((reinterpret_cast<uintptr_t>(w_out) & 15u) != 0) return GLMB_ERR_ALIGNMENT;
+  if (M > 0 && (reinterpret_cast<uintptr_t>(Z) & 7u) != 0) return GLMB_ERR_ALIGNMENT;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  GLMB_TRY(bind_stream(s, nullptr));
+  const double rxx = Rxx, rxy = Rxy, ryy = Ryy;
+  const double det = rxx * ryy - rxy * rxy;
+  const double h = 0.5 * 1.4426950408889634074;
+  glmb::ReweightArgs a{};
+  a.x = src->x; a.y = src->y; a.w = src->w; a.w_out = w_out; a.ld = src->ld; a.T = K; a.P = src->n_particles;
+  a.Z = Z; a.M = M; a.theta = nullptr; a.col_offset = 0;
+  a.qa = h * ryy / det;
+  a.qb = -2.0 * h * rxy / det;
+  a.qc = h * rxx / det;
+  a.log_norm1 = std::log(2.0 * 3.14159265358979323846 * std::sqrt(det));
+  a.log_norm = log_norm; a.flags = flags;
+  a.pair_track = pair_track; a.pair_ptr = pair_ptr; a.pair_meas = pair_meas; a.n_units_dev = n_pairs;
+  a.ld_out = ld_out; a.ess = ess;
+  return from_cuda(glmb::launch_reweight(a, s));
+}
+
+glmb_status glmb_resample(const glmb_particles *src, int32_t K, const int32_t *n_pairs, const int32_t *pair_track,
+                          const float *w, int64_t ldw, const glmb_particles *out, uint64_t seed, uint32_t step,
+                          uint32_t *flags, glmb_stream_t stream) {
+  GLMB_TRY(check_particles(src, false, true));
+  GLMB_TRY(check_particles(out, true, true));
+  if (K < 0) return GLMB_ERR_INVALID_ARG;
+  if (K == 0) return GLMB_OK;
+  if (src->n_tracks == 0 || out->n_tracks < K || out->n_particles != src->n_particles ||
+      src->n_particles > GLMB_PAIRS_PMAX)
+    return GLMB_ERR_INVALID_ARG;
+  if (pair_track == nullptr || w == nullptr) return GLMB_ERR_INVALID_ARG;
+  if (ldw < src->n_particles || (ldw & 3) || (reinterpret_cast<uintptr_t>(w) & 15u)) return GLMB_ERR_ALIGNMENT;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  GLMB_TRY(bind_stream(s, nullptr));
+  glmb::ResampleArgs a{};
+  a.x = src->x; a.y = src->y; a.v = src->v; a.psi = src->psi; a.omega = src->omega; a.ld = src->ld;
+  a.P = src->n_particles; a.pair_track = pair_track; a.w = w; a.ldw = ldw; a.K = K; a.n_units_dev = n_pairs;
+  a.ox = out->x; a.oy = out->y; a.ov = out->v; a.opsi = out->psi; a.oomega = out->omega; a.ow = out->w;
+  a.ld_out = out->ld;
+  a.key0 = static_cast<uint32_t>(seed); a.key1 = static_cast<uint32_t>(seed >> 32); a.step = step;
+  a.flags = flags;
+  return from_cuda(glmb::launch_resample(a, s));
 }
 
 glmb_status glmb_philox_dump(uint64_t seed, const uint32_t *ctr, int32_t N, uint32_t *out, glmb_stream_t stream) {

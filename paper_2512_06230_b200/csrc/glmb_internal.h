@@ -58,6 +58,14 @@ struct ReweightArgs {
   double log_norm1;    // ln(2 pi sqrt(det R))
   float *log_norm;
   uint32_t *flags;
+  // pair mode (glmb_reweight_pairs): unit k updates source row pair_track[k] with
+  // S_k = pair_meas[pair_ptr[k] .. pair_ptr[k+1]) and writes row k of w_out (stride
+  // ld_out), log_norm[k], flags[k], ess[k].  theta mode: pair_track == nullptr,
+  // unit j = row j, ld_out = ld, ess == nullptr.
+  const int32_t *pair_track, *pair_ptr, *pair_meas;
+  const int32_t *n_units_dev;  // optional device count of valid units (<= T)
+  int64_t ld_out;
+  float *ess;
 };
 
 // ---- hypothesis machinery (hyp.cu)
@@ -140,5 +148,36 @@ cudaError_t launch_assoc_sample(const SampleArgs &a, cudaStream_t s);
 cudaError_t launch_dedup(const DedupArgs &a, cudaStream_t s);
 int32_t prune_capacity(int32_t h_max);
 cudaError_t launch_prune(const PruneArgs &a, cudaStream_t s);
+
+// ---- particle loop (pairs.cu)
+struct PairsArgs {
+  int32_t n_hyp, T, M, ldt;
+  int64_t ldm;
+  const int32_t *hyp_idx;
+  const uint32_t *alive;
+  const int32_t *theta;
+  int32_t *pair_track, *pair_ptr, *pair_meas, *pair_of, *n_pairs;
+  // workspace (n_hyp*T entries each, and n_hyp*M for the lists)
+  int32_t *cnt, *off, *first, *list;
+  unsigned long long *fp;
+};
+size_t pairs_workspace_bytes(int32_t n_hyp, int32_t T, int32_t M);
+cudaError_t launch_assoc_pairs(const PairsArgs &a, void *ws, cudaStream_t s);
+
+struct ResampleArgs {
+  const float *x, *y, *v, *psi, *omega;  // source particles [.][ld]
+  int64_t ld;
+  int32_t P;
+  const int32_t *pair_track;
+  const float *w;                        // reweighted weights [K][ldw]
+  int64_t ldw;
+  int32_t K;
+  const int32_t *n_units_dev;
+  float *ox, *oy, *ov, *opsi, *oomega, *ow;  // output particles [K][ld_out]
+  int64_t ld_out;
+  uint32_t key0, key1, step;
+  uint32_t *flags;                       // bit 1 set when unit k was resampled
+};
+cudaError_t launch_resample(const ResampleArgs &a, cudaStream_t s);
 
 }  // namespace glmb

@@ -1,0 +1,375 @@
+// pairs.cu -- the particle loop after the hypothesis update (
+// PAPER.md P:53 §Approach):
+//
+//   assoc_pairs   unique (track, measurement set) pairs over the kept hypotheses
+//                 ("a batched particle update for all unique (track, measurement)
+//                 association pairs", reading R30)
+//   resample      systematic resampling of each pair's reweighted particles when
+//                 ESS < P/2 ("a resampling step is performed if necessary", R31, R32)
+//
+// (the per-pair Bayes update itself is reweight.cu's cluster kernel in pair mode.)
+// The resampling CDF is built from integer weights W = floor(w 2^26), so the
+// prefix sums, the ESS decision and the ancestors are exact integers: the same
+// on any hardware and in any summation order.
+#include "glmb_device.cuh"
+#include "glmb_internal.h"
+
+namespace glmb {
+namespace {
+
+__device__ __forceinline__ unsigned long long mix64p(unsigned long long z) {  // SplitMix64 finaliser
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// block-wide exclusive scan of one int per thread (blockDim.x == 1024 or less, multiple of 32)
+template <typename Ti>
+__device__ Ti block_excl_scan(Ti v, Ti *wsum /* [32] */, Ti &total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  Ti x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const Ti y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    Ti s = lane < nw ? wsum[lane] : Ti(0);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const Ti y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    wsum[lane] = s;
+  }
+  __syncthreads();
+  total = wsum[nw - 1];
+  const Ti r = (wid ? wsum[wid - 1] : Ti(0)) + x - v;
+  __syncthreads();
+  return r;
+}
+
+// ------------------------------------------------------------------ per-hypothesis inversion of theta
+// One CTA per kept hypothesis r: |S| and a fingerprint of S for every track,
+// the per-track offsets, and the lists S (ascending i) in list[r][0..M).
+constexpr int kInvThreads = 256;
+
+__global__ void __launch_bounds__(kInvThreads) invert_kernel(PairsArgs a) {
+  extern __shared__ unsigned char smraw[];
+  unsigned long long *fp = reinterpret_cast<unsigned long long *>(smraw);  // [T]
+  int32_t *cnt = reinterpret_cast<int32_t *>(fp + a.T);                   // [T]
+  __shared__ int32_t wsum[32];
+  const int32_t r = blockIdx.x;
+  const int64_t q = __ldg(a.hyp_idx + r);
+  const uint32_t *al = a.alive + q * a.ldt;
+  const int32_t *th = a.theta + q * a.ldm;
+  for (int32_t j = threadIdx.x; j < a.T; j += kInvThreads) {
+    cnt[j] = 0;
+    fp[j] = 0ull;
+  }
+  __syncthreads();
+  for (int32_t i = threadIdx.x; i < a.M; i += kInvThreads) {
+    const int32_t c = __ldg(th + i);
+    if (c >= 1 && c <= a.T) {
+      const int32_t j = c - 1;
+      if ((__ldg(al + (j >> 5)) >> (j & 31)) & 1u) {
+        atomicAdd(cnt + j, 1);
+        atomicAdd(fp + j, mix64p(static_cast<unsigned long long>(i) + 0x632BE59BD9B4E019ull));
+      }
+    }
+  }
+  __syncthreads();
+  // per-track outputs and the exclusive scan of the counts (offsets into list[r])
+  int32_t carry = 0;
+  const int64_t rb = static_cast<int64_t>(r) * a.T;
+  for (int32_t j0 = 0; j0 < a.T; j0 += kInvThreads) {
+    const int32_t j = j0 + threadIdx.x;
+    int32_t c = 0;
+    if (j < a.T) {
+      const bool alive = (__ldg(al + (j >> 5)) >> (j & 31)) & 1u;
+      c = cnt[j];
+      a.cnt[rb + j] = alive ? c : -1;
+      a.fp[rb + j] = mix64p(fp[j] ^ (static_cast<unsigned long long>(c) << 40));
+    }
+    int32_t tot;
+    const int32_t ex = block_excl_scan(c, wsum, tot);
+    if (j < a.T) {
+      a.off[rb + j] = carry + ex;
+      cnt[j] = carry + ex;  // becomes the list cursor of track j
+    }
+    carry += tot;
+  }
+  __syncthreads();
+  // lists in ascending i: warp 0 walks the rows 32 at a time; lanes with the same
+  // track are ranked by lane, and the group's leader advances the cursor
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int32_t *list = a.list + static_cast<int64_t>(r) * a.M;
+    for (int32_t i0 = 0; i0 < a.M; i0 += 32) {
+      const int32_t i = i0 + lane;
+      int32_t key = -1 - lane;  // unique per lane when the row is not listed
+      if (i < a.M) {
+        const int32_t c = __ldg(th + i);
+        if (c >= 1 && c <= a.T && ((__ldg(al + ((c - 1) >> 5)) >> ((c - 1) & 31)) & 1u)) key = c - 1;
+      }
+      const uint32_t grp = __match_any_sync(0xffffffffu, key);
+      const int leader = __ffs(grp) - 1;
+      int32_t b = 0;
+      if (key >= 0 && lane == leader) {
+        b = cnt[key];
+        cnt[key] = b + __popc(grp);
+      }
+      b = __shfl_sync(0xffffffffu, b, leader);
+      if (key >= 0) list[b + __popc(grp & ((1u << lane) - 1u))] = i;
+    }
+  }
+}
+
+// first occurrence of each (j, S): the earliest r' <= r with the same list
+__global__ void __launch_bounds__(256) first_kernel(PairsArgs a) {
+  const int32_t r = blockIdx.y;
+  const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= a.T) return;
+  const int64_t e = static_cast<int64_t>(r) * a.T + j;
+  const int32_t c = a.cnt[e];
+  if (c < 0) {
+    a.first[e] = -1;
+    return;
+  }
+  const unsigned long long f = a.fp[e];
+  const int32_t *mine = a.list + static_cast<int64_t>(r) * a.M + a.off[e];
+  int32_t first = r;
+  for (int32_t r2 = 0; r2 < r; ++r2) {
+    const int64_t e2 = static_cast<int64_t>(r2) * a.T + j;
+    if (a.cnt[e2] != c || a.fp[e2] != f) continue;
+    const int32_t *other = a.list + static_cast<int64_t>(r2) * a.M + a.off[e2];
+    bool same = true;
+    for (int32_t k = 0; k < c && same; ++k) same = mine[k] == other[k];
+    if (same) {
+      first = r2;
+      break;
+    }
+  }
+  a.first[e] = first;
+}
+
+// numbering in (r, j) order: pair index and list offset of each first occurrence (one CTA)
+__global__ void __launch_bounds__(1024) number_kernel(PairsArgs a) {
+  __shared__ int32_t wsum[32];
+  const int64_t n = static_cast<int64_t>(a.n_hyp) * a.T;
+  int32_t kc = 0, mc = 0;
+  for (int64_t e0 = 0; e0 < n; e0 += 1024) {
+    const int64_t e = e0 + threadIdx.x;
+    int32_t isnew = 0, c = 0;
+    if (e < n) {
+      const int32_t r = static_cast<int32_t>(e / a.T);
+      isnew = a.first[e] == r;
+      c = isnew ? a.cnt[e] : 0;
+    }
+    int32_t ktot, mtot;
+    const int32_t k = kc + block_excl_scan(isnew, wsum, ktot);
+    const int32_t m = mc + block_excl_scan(c, wsum, mtot);
+    if (isnew) {
+      const int32_t j = static_cast<int32_t>(e % a.T);
+      a.pair_track[k] = j;
+      a.pair_ptr[k] = m;
+      a.pair_of[e] = k;
+    }
+    kc += ktot;
+    mc += mtot;
+  }
+  if (threadIdx.x == 0) {
+    a.pair_ptr[kc] = mc;
+    *a.n_pairs = kc;
+  }
+}
+
+// pair_of for repeats and the measurement lists of the new pairs
+__global__ void __launch_bounds__(256) finish_kernel(PairsArgs a) {
+  const int32_t r = blockIdx.y;
+  const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= a.T) return;
+  const int64_t e = static_cast<int64_t>(r) * a.T + j;
+  const int32_t f = a.first[e];
+  if (f < 0) {
+    a.pair_of[e] = -1;
+    return;
+  }
+  if (f != r) {
+    a.pair_of[e] = a.pair_of[static_cast<int64_t>(f) * a.T + j];
+    return;
+  }
+  const int32_t k = a.pair_of[e];
+  const int32_t c = a.cnt[e];
+  const int32_t *src = a.list + static_cast<int64_t>(r) * a.M + a.off[e];
+  int32_t *dst = a.pair_meas + a.pair_ptr[k];
+  for (int32_t t = 0; t < c; ++t) dst[t] = src[t];
+}
+
+// ------------------------------------------------------------------ systematic resampling
+// One CTA per pair k.  W_m = floor(w_m 2^26) in shared memory, cum_m = W_0 + ...
+// + W_m (u64, exact), S = cum_{P-1}, Q = sum W_m^2 (u128, exact).  Resample iff
+// 2 S^2 < P Q (ESS < P/2).  Output slot n takes ancestor a_n = min{m : cum_m > t_n},
+// t_n = floor((n S + V) / P), V = floor(U S 2^-24), U = 2 (r >> 9) + 1 from
+// Philox(counter (k, 0, step, 4 << 24)) word 0.  Ancestors are non-decreasing in n,
+// so the gathers of consecutive slots hit neighbouring addresses.
+constexpr int kResThreads = 256;
+
+__global__ void __launch_bounds__(kResThreads) resample_kernel(ResampleArgs a) {
+  extern __shared__ __align__(16) unsigned char rs[];
+  unsigned long long *cum = reinterpret_cast<unsigned long long *>(rs);  // [P]
+  uint32_t *Wsm = reinterpret_cast<uint32_t *>(cum + a.P);              // [P]
+  __shared__ unsigned long long wsum[32];
+  __shared__ unsigned long long qlo[kResThreads / 32], qhi[kResThreads / 32];
+  __shared__ int do_res;
+  const int k = blockIdx.x;
+  if (a.n_units_dev != nullptr && k >= __ldg(a.n_units_dev)) return;
+  const int j = __ldg(a.pair_track + k);
+  const int64_t src = static_cast<int64_t>(j) * a.ld, dst = static_cast<int64_t>(k) * a.ld_out;
+  const float *wk = a.w + static_cast<int64_t>(k) * a.ldw;
+  const int quads = a.P >> 2;
+  // integer weights (2^26 scaling of an fp32 in [0, 1] is exact; floor by conversion)
+  unsigned __int128 qsum = 0;
+  for (int g = threadIdx.x; g < quads; g += kResThreads) {
+    const float4 w4 = __ldg(reinterpret_cast<const float4 *>(wk) + g);
+    const uint32_t W0 = __float2uint_rd(w4.x * 67108864.0f), W1 = __float2uint_rd(w4.y * 67108864.0f),
+                   W2 = __float2uint_rd(w4.z * 67108864.0f), W3 = __float2uint_rd(w4.w * 67108864.0f);
+    reinterpret_cast<uint4 *>(Wsm)[g] = make_uint4(W0, W1, W2, W3);
+    qsum += static_cast<unsigned long long>(W0) * W0 + static_cast<unsigned long long>(W1) * W1 +
+            static_cast<unsigned long long>(W2) * W2 + static_cast<unsigned long long>(W3) * W3;
+  }
+  __syncthreads();
+  // contiguous chunk per thread -> local sums -> block exclusive scan -> cum
+  const int per = (a.P + kResThreads - 1) / kResThreads;
+  const int m0 = min(a.P, threadIdx.x * per), m1 = min(a.P, m0 + per);
+  unsigned long long loc = 0;
+  for (int m = m0; m < m1; ++m) loc += Wsm[m];
+  unsigned long long S;
+  unsigned long long run = block_excl_scan(loc, wsum, S);
+  for (int m = m0; m < m1; ++m) {
+    run += Wsm[m];
+    cum[m] = run;
+  }
+  // Q: exact 128-bit sum (lo/hi halves reduced with carries by one thread)
+  {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned long long lo = static_cast<unsigned long long>(qsum), hi = static_cast<unsigned long long>(qsum >> 64);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long lo2 = __shfl_xor_sync(0xffffffffu, lo, o), hi2 = __shfl_xor_sync(0xffffffffu, hi, o);
+      const unsigned long long s = lo + lo2;
+      hi += hi2 + (s < lo);
+      lo = s;
+    }
+    if (lane == 0) {
+      qlo[wid] = lo;
+      qhi[wid] = hi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned __int128 Q = 0;
+      for (int w = 0; w < kResThreads / 32; ++w) Q += (static_cast<unsigned __int128>(qhi[w]) << 64) | qlo[w];
+      const unsigned __int128 S2 = static_cast<unsigned __int128>(S) * S;
+      do_res = S > 0 && 2 * S2 < static_cast<unsigned __int128>(a.P) * Q;
+      if (a.flags != nullptr) a.flags[k] = (a.flags[k] & ~2u) | (do_res ? 2u : 0u);
+    }
+    __syncthreads();
+  }
+  float4 *ox = reinterpret_cast<float4 *>(a.ox + dst), *oy = reinterpret_cast<float4 *>(a.oy + dst),
+         *ov = reinterpret_cast<float4 *>(a.ov + dst), *op = reinterpret_cast<float4 *>(a.opsi + dst),
+         *oo = reinterpret_cast<float4 *>(a.oomega + dst), *ow = reinterpret_cast<float4 *>(a.ow + dst);
+  if (!do_res) {  // keep the particles with their new weights
+    for (int g = threadIdx.x; g < quads; g += kResThreads) {
+      __stcs(ox + g, __ldg(reinterpret_cast<const float4 *>(a.x + src) + g));
+      __stcs(oy + g, __ldg(reinterpret_cast<const float4 *>(a.y + src) + g));
+      __stcs(ov + g, __ldg(reinterpret_cast<const float4 *>(a.v + src) + g));
+      __stcs(op + g, __ldg(reinterpret_cast<const float4 *>(a.psi + src) + g));
+      __stcs(oo + g, __ldg(reinterpret_cast<const float4 *>(a.omega + src) + g));
+      __stcs(ow + g, __ldg(reinterpret_cast<const float4 *>(wk) + g));
+    }
+    return;
+  }
+  const u32x4 r = philox4x32_10(u32x4{static_cast<uint32_t>(k), 0u, a.step, 4u << 24}, a.key0, a.key1);
+  const unsigned long long U = 2ull * (r.a >> 9) + 1ull;
+  const unsigned long long V = (U * S) >> 24;  // U < 2^24, S <= 2^40: no overflow
+  const float inv_p = 1.0f / static_cast<float>(a.P);
+  for (int g = threadIdx.x; g < quads; g += kResThreads) {
+    float4 X, Y, Vv, Ps, Om;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int n = 4 * g + e;
+      const unsigned long long t = (static_cast<unsigned long long>(n) * S + V) / static_cast<unsigned>(a.P);
+      int lo = 0, hi = a.P - 1;  // first m with cum[m] > t (exists: cum[P-1] = S > t)
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (cum[mid] > t) hi = mid;
+        else lo = mid + 1;
+      }
+      const int64_t m = src + lo;
+      (&X.x)[e] = __ldg(a.x + m);
+      (&Y.x)[e] = __ldg(a.y + m);
+      (&Vv.x)[e] = __ldg(a.v + m);
+      (&Ps.x)[e] = __ldg(a.psi + m);
+      (&Om.x)[e] = __ldg(a.omega + m);
+    }
+    __stcs(ox + g, X);
+    __stcs(oy + g, Y);
+    __stcs(ov + g, Vv);
+    __stcs(op + g, Ps);
+    __stcs(oo + g, Om);
+    __stcs(ow + g, make_float4(inv_p, inv_p, inv_p, inv_p));
+  }
+}
+
+}  // namespace
+
+size_t pairs_workspace_bytes(int32_t n_hyp, int32_t T, int32_t M) {
+  const size_t nt = static_cast<size_t>(n_hyp) * T;
+  return nt * (3 * sizeof(int32_t) + sizeof(unsigned long long)) + static_cast<size_t>(n_hyp) * M * sizeof(int32_t) +
+         64;
+}
+
+cudaError_t launch_assoc_pairs(const PairsArgs &in, void *ws, cudaStream_t s) {
+  PairsArgs a = in;
+  const size_t nt = static_cast<size_t>(a.n_hyp) * a.T;
+  unsigned char *p = static_cast<unsigned char *>(ws);
+  p = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+  a.fp = reinterpret_cast<unsigned long long *>(p);
+  a.cnt = reinterpret_cast<int32_t *>(a.fp + nt);
+  a.off = a.cnt + nt;
+  a.first = a.off + nt;
+  a.list = a.first + nt;
+  if (a.n_hyp == 0 || a.T == 0) {
+    cudaError_t e = cudaMemsetAsync(a.n_pairs, 0, sizeof(int32_t), s);
+    if (e != cudaSuccess) return e;
+    return cudaMemsetAsync(a.pair_ptr, 0, sizeof(int32_t), s);
+  }
+  const size_t smem = static_cast<size_t>(a.T) * (sizeof(unsigned long long) + sizeof(int32_t));
+  if (smem > 40 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(invert_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  invert_kernel<<<a.n_hyp, kInvThreads, smem, s>>>(a);
+  const dim3 g2((a.T + 255) / 256, a.n_hyp);
+  first_kernel<<<g2, 256, 0, s>>>(a);
+  number_kernel<<<1, 1024, 0, s>>>(a);
+  finish_kernel<<<g2, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_resample(const ResampleArgs &a, cudaStream_t s) {
+  if (a.K == 0) return cudaSuccess;
+  const size_t smem = static_cast<size_t>(a.P) * (sizeof(unsigned long long) + sizeof(uint32_t));
+  if (smem > 40 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(resample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  resample_kernel<<<a.K, kResThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace glmb

@@ -34,7 +34,24 @@ struct SList {
   double2 z[kSCap];
   int n;           // |S_j|
   int in_smem;     // 1 if all of S_j fits in z[]
+  int e0;          // pair mode: first index of S_k in pair_meas
 };
+
+// Pair mode: S_k is given explicitly (ascending i) -- fetch its measurements.
+__device__ void collect_S_pair(const ReweightArgs &a, int k, SList &S) {
+  const int e0 = __ldg(a.pair_ptr + k), n = __ldg(a.pair_ptr + k + 1) - e0;
+  const float2 *Z2 = reinterpret_cast<const float2 *>(a.Z);
+  for (int e = threadIdx.x; e < n && e < kSCap; e += blockDim.x) {
+    const float2 z = __ldg(Z2 + __ldg(a.pair_meas + e0 + e));
+    S.z[e] = make_double2(z.x, z.y);
+  }
+  if (threadIdx.x == 0) {
+    S.n = n;
+    S.in_smem = n <= kSCap;
+    S.e0 = e0;
+  }
+  __syncthreads();
+}
 
 // Collect S_j in ascending i.  Chunks of 8 * kThreads indices: every thread
 // issues its 8 theta loads at once (one L2 round trip per chunk, not one per
@@ -116,6 +133,11 @@ __device__ __forceinline__ double log_weight(const ReweightArgs &a, const SList 
   const double dpx = px, dpy = py;
   if (S.in_smem) {
     for (int s = 0; s < S.n; ++s) l -= qform(a, S.z[s].x, S.z[s].y, dpx, dpy);
+  } else if (a.pair_meas != nullptr) {
+    for (int e = S.e0; e < S.e0 + S.n; ++e) {
+      const float2 z = __ldg(reinterpret_cast<const float2 *>(a.Z) + __ldg(a.pair_meas + e));
+      l -= qform(a, z.x, z.y, dpx, dpy);
+    }
   } else {
     for (int i = 0; i < a.M; ++i)
       if (__ldg(a.theta + i) == col) {
@@ -262,13 +284,16 @@ __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.w
 // (max, sum) pairs combined exactly as one pass over all terms would give up
 // to rounding: (m, s) + (m', s') = (M, s 2^(m-M) + s' 2^(m'-M)), M = max(m, m').
 // Applied by one thread in a fixed order, so the reduction is deterministic.
-__device__ __forceinline__ void ms_merge(double &m, double &s, double m2, double s2) {
+__device__ __forceinline__ void ms_merge(double &m, double &s, double &s2, double m2, double t, double t2) {
   const double M = fmax(m, m2);
   if (M == -INFINITY) {
     s = 0.0;
+    s2 = 0.0;
     return;
   }
-  s = s * ex2_approx(static_cast<float>(m - M)) + s2 * ex2_approx(static_cast<float>(m2 - M));
+  const double f1 = ex2_approx(static_cast<float>(m - M)), f2 = ex2_approx(static_cast<float>(m2 - M));
+  s = s * f1 + t * f2;
+  s2 = s2 * (f1 * f1) + t2 * (f2 * f2);
   m = M;
 }
 
@@ -285,18 +310,21 @@ __global__ void __launch_bounds__(kThreads, R == 1 ? 5 : (R == 2 ? 3 : 2)) rewei
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   __shared__ SList S;
-  __shared__ double red[2][kWarps];
+  __shared__ double red[3][kWarps];
   __shared__ uint32_t masks[kRows * kWarps];
-  __shared__ double part[2];  // this CTA's (max, sum), read by the peers
+  __shared__ double part[3];  // this CTA's (max, sum, sum of squares), read by the peers
   const int crank = static_cast<int>(cluster.block_rank());
-  const int j = blockIdx.x / CL;
+  const int u = blockIdx.x / CL;  // unit: track j (theta mode) or pair k (pair mode)
+  const bool pairs = a.pair_track != nullptr;
+  if (a.n_units_dev != nullptr && u >= __ldg(a.n_units_dev)) return;  // whole cluster exits together
+  const int j = pairs ? __ldg(a.pair_track + u) : u;
   const int col = a.col_offset + j + 1;
   const int64_t base = static_cast<int64_t>(j) * a.ld;
   const float4 *xs = reinterpret_cast<const float4 *>(a.x + base);
   const float4 *ys = reinterpret_cast<const float4 *>(a.y + base);
   const float4 *ws = reinterpret_cast<const float4 *>(a.w + base);
-  float4 *wo = reinterpret_cast<float4 *>(a.w_out + base);
-  const bool copy_out = a.w_out != a.w;
+  float4 *wo = reinterpret_cast<float4 *>(a.w_out + static_cast<int64_t>(u) * a.ld_out);
+  const bool copy_out = pairs || a.w_out != a.w;
   const int quads = a.P >> 2;
   const int per = (quads + CL - 1) / CL;
   const int q0 = crank * per, q1 = min(quads, q0 + per);
@@ -312,18 +340,27 @@ __global__ void __launch_bounds__(kThreads, R == 1 ? 5 : (R == 2 ? 3 : 2)) rewei
       W[r] = __ldcs(ws + g);
     }
   }
-  collect_S(a, col, S, masks);
+  if (pairs) collect_S_pair(a, u, S);
+  else collect_S(a, col, S, masks);
   const int nS = S.n;
 
-  if (nS == 0) {  // untouched; log_norm = ln sum w
-    double sw = 0.0;
+  if (nS == 0) {  // untouched; log_norm = ln sum w; ESS = (sum w)^2 / sum w^2
+    double sw = 0.0, sw2 = 0.0;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int g = q0 + threadIdx.x + r * kThreads;
-      if (g < q1) sw += (static_cast<double>(W[r].x) + W[r].y) + (static_cast<double>(W[r].z) + W[r].w);
+      if (g < q1) {
+        sw += (static_cast<double>(W[r].x) + W[r].y) + (static_cast<double>(W[r].z) + W[r].w);
+        sw2 += (static_cast<double>(W[r].x) * W[r].x + static_cast<double>(W[r].y) * W[r].y) +
+               (static_cast<double>(W[r].z) * W[r].z + static_cast<double>(W[r].w) * W[r].w);
+      }
     }
     sw = block_sum(sw, red[0]);
-    if (threadIdx.x == 0) part[1] = sw;
+    if (a.ess != nullptr) sw2 = block_sum(sw2, red[1]);
+    if (threadIdx.x == 0) {
+      part[1] = sw;
+      part[2] = sw2;
+    }
     cluster.sync();
     if (copy_out) {  // after the barrier: the copy does not sit behind its release fence
 #pragma unroll
@@ -333,11 +370,16 @@ __global__ void __launch_bounds__(kThreads, R == 1 ? 5 : (R == 2 ? 3 : 2)) rewei
       }
     }
     if (crank == 0 && threadIdx.x == 0) {
-      double tot = 0.0;
+      double tot = 0.0, tot2 = 0.0;
 #pragma unroll
-      for (int r = 0; r < CL; ++r) tot += cluster.map_shared_rank(part, r)[1];
-      a.log_norm[j] = static_cast<float>(log(tot));
-      a.flags[j] = 0u;
+      for (int r = 0; r < CL; ++r) {
+        const double *pr = cluster.map_shared_rank(part, r);
+        tot += pr[1];
+        tot2 += pr[2];
+      }
+      a.log_norm[u] = static_cast<float>(log(tot));
+      a.flags[u] = 0u;
+      if (a.ess != nullptr) a.ess[u] = tot2 > 0.0 ? static_cast<float>(tot * tot / tot2) : 0.0f;
     }
     if (crank == 0) __syncthreads();
     cluster_arrive_relaxed();  // done with the peers' shared memory
@@ -359,56 +401,62 @@ __global__ void __launch_bounds__(kThreads, R == 1 ? 5 : (R == 2 ? 3 : 2)) rewei
   // warp max (fp64 shuffles, no conversions), then terms relative to it
   mw = warp_max_d(mw);
   float e[4 * R];
-  float sw = 0.0f;
+  float sw = 0.0f, sw2 = 0.0f;
 #pragma unroll
   for (int k = 0; k < 4 * R; ++k) {
     e[k] = mw == -INFINITY ? 0.0f : ex2_approx(static_cast<float>(l[k] - mw));
     sw += e[k];
+    sw2 = fmaf(e[k], e[k], sw2);
   }
   sw = warp_sum(sw);
+  if (a.ess != nullptr) sw2 = warp_sum(sw2);
   // block: thread 0 merges the warps in order; cluster: thread 0 of every CTA
   // merges the CL parts in rank order (all CTAs get the same (m, s))
-  __shared__ double bc[2];
+  __shared__ double bc[3];
   if (lane == 0) {
     red[0][warp] = mw;
     red[1][warp] = sw;
+    red[2][warp] = sw2;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double mb = red[0][0], sb = red[1][0];
+    double mb = red[0][0], sb = red[1][0], s2b = red[2][0];
 #pragma unroll
-    for (int k = 1; k < kWarps; ++k) ms_merge(mb, sb, red[0][k], red[1][k]);
+    for (int k = 1; k < kWarps; ++k) ms_merge(mb, sb, s2b, red[0][k], red[1][k], red[2][k]);
     part[0] = mb;
     part[1] = sb;
+    part[2] = s2b;
   }
   cluster.sync();
   if (threadIdx.x == 0) {
-    double mc = -INFINITY, sc = 0.0;
+    double mc = -INFINITY, sc = 0.0, s2c = 0.0;
 #pragma unroll
     for (int r = 0; r < CL; ++r) {
       const double *pr = cluster.map_shared_rank(part, r);
-      ms_merge(mc, sc, pr[0], pr[1]);
+      ms_merge(mc, sc, s2c, pr[0], pr[1], pr[2]);
     }
     bc[0] = mc;
     bc[1] = sc;
+    bc[2] = s2c;
   }
   __syncthreads();
-  const double mc = bc[0], sc = bc[1];
+  const double mc = bc[0], sc = bc[1], s2c = bc[2];
   // every read of a peer's shared memory is done: arrive now (relaxed: no
   // memory ordering needed), wait only at exit so the stores below do not
   // sit behind a release fence
   cluster_arrive_relaxed();
 
   if (mc == -INFINITY) {  // every weight zero: uniform reset, flagged (never abort)
-    const float u = 1.0f / static_cast<float>(a.P);
+    const float uw = 1.0f / static_cast<float>(a.P);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int g = q0 + threadIdx.x + r * kThreads;
-      if (g < q1) __stcs(wo + g, make_float4(u, u, u, u));
+      if (g < q1) __stcs(wo + g, make_float4(uw, uw, uw, uw));
     }
     if (crank == 0 && threadIdx.x == 0) {
-      a.log_norm[j] = -INFINITY;
-      a.flags[j] = 1u;
+      a.log_norm[u] = -INFINITY;
+      a.flags[u] = 1u;
+      if (a.ess != nullptr) a.ess[u] = static_cast<float>(a.P);
     }
     cluster_wait();
     return;
@@ -423,8 +471,9 @@ __global__ void __launch_bounds__(kThreads, R == 1 ? 5 : (R == 2 ? 3 : 2)) rewei
   }
   if (crank == 0 && threadIdx.x == 0) {
     const double ln2 = 0.69314718055994530942;
-    a.log_norm[j] = static_cast<float>((mc + log2(sc)) * ln2 - nS * a.log_norm1);
-    a.flags[j] = 0u;
+    a.log_norm[u] = static_cast<float>((mc + log2(sc)) * ln2 - nS * a.log_norm1);
+    a.flags[u] = 0u;
+    if (a.ess != nullptr) a.ess[u] = static_cast<float>(sc * sc / s2c);  // (sum w')^2 / sum w'^2
   }
   cluster_wait();
 }

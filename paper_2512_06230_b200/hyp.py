@@ -1,9 +1,13 @@
-"""Hypothesis update on the GPU (§Approach).
+"""Hypothesis update and particle loop on the GPU (§Approach).
 
 ``HypothesisUpdate`` owns the device buffers of one rank and issues, on one
 stream, the five C-ABI calls that turn C_k into the pruned successor set:
 
     glmb_death_prob -> glmb_compat_rows -> glmb_assoc_sample -> glmb_dedup -> glmb_prune
+
+``ParticleUpdate`` then closes the particle loop for the kept hypotheses:
+
+    glmb_assoc_pairs -> glmb_reweight_pairs -> glmb_resample
 
 Argument marshalling only: every step runs in libglmb.so's kernels.
 """
@@ -53,3 +57,52 @@ class HypothesisUpdate:
                         self.unique[:n], stream)
         _lib.glmb_prune(self.logw[:n], self.unique[:n], tau, self.h_max, self.keys[:n], self.keep_idx,
                         self.keep_w, self.n_kept, stream)
+
+
+class ParticleUpdate:
+    """Unique (track, measurement set) pairs of the kept hypotheses, their particle update and
+    resampling into a new particle set with one row per pair."""
+
+    def __init__(self, T: int, M_max: int, n_hyp_max: int, P: int, K_cap: int | None = None, device="cuda"):
+        """K_cap: rows of the new particle set (default min(n_hyp_max, 4) * T); the pair lists
+        themselves are sized for the worst case n_hyp_max * T."""
+        from ._lib import Particles
+        dev = torch.device(device)
+        self.T, self.M_max, self.n_hyp_max, self.P = T, M_max, n_hyp_max, P
+        K = max(1, n_hyp_max * T)
+        Kc = max(1, min(n_hyp_max, 4) * T) if K_cap is None else max(1, int(K_cap))
+        i32 = torch.int32
+        self.K_cap = Kc
+        self.pair_track = torch.empty(K, dtype=i32, device=dev)
+        self.pair_ptr = torch.empty(K + 1, dtype=i32, device=dev)
+        self.pair_meas = torch.empty(max(1, n_hyp_max * M_max), dtype=i32, device=dev)
+        self.pair_of = torch.empty(max(1, n_hyp_max), max(1, T), dtype=i32, device=dev)
+        self.n_pairs = torch.zeros(1, dtype=i32, device=dev)
+        nb = _lib.glmb_assoc_pairs_workspace_size(n_hyp_max, T, M_max)
+        self.ws = torch.empty(max(16, nb), dtype=torch.uint8, device=dev)
+        self.w_new = torch.empty(Kc, P, dtype=torch.float32, device=dev)
+        self.log_norm = torch.empty(Kc, dtype=torch.float32, device=dev)
+        self.flags = torch.empty(Kc, dtype=i32, device=dev)
+        self.ess = torch.empty(Kc, dtype=torch.float32, device=dev)
+        self.out = Particles.empty(Kc, P, device=dev)
+
+    def run(self, src, Z, R, hyp_idx, n_hyp, alive, theta, M, seed, step, stream=None):
+        """src: Particles of the T_k predicted tracks; hyp_idx [>= n_hyp] device int32 (e.g. the
+        pruned keep_idx); alive / theta: the sampler's outputs.  New set: self.out rows < n_pairs."""
+        assert n_hyp <= self.n_hyp_max and M <= self.M_max
+        hi = hyp_idx[:n_hyp]
+        _lib.glmb_assoc_pairs(hi, alive, theta, self.T, M, self.pair_track, self.pair_ptr, self.pair_meas,
+                              self.pair_of, self.n_pairs, self.ws, stream)
+        K = min(self.K_cap, max(1, n_hyp * self.T))
+        _lib.glmb_reweight_pairs(src, Z, R, K, self.n_pairs, self.pair_track, self.pair_ptr, self.pair_meas,
+                                 self.w_new[:K], self.log_norm, self.flags, self.ess, stream)
+        _lib.glmb_resample(src, K, self.n_pairs, self.pair_track, self.w_new[:K], self.out, seed, step,
+                           self.flags, stream)
+
+    def n_pairs_checked(self) -> int:
+        """Synchronises and returns K; raises if the pairs overflowed K_cap (rows past it were not updated)."""
+        torch.cuda.synchronize()
+        K = int(self.n_pairs.item())
+        if K > self.K_cap:
+            raise RuntimeError(f"{K} unique pairs exceed K_cap = {self.K_cap}")
+        return K
