@@ -49,6 +49,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
+    ap.add_argument("--no-update", action="store_true", help="skip the GLMB update (f1-f3) timing")
+    ap.add_argument("--h-old", type=int, default=100)
+    ap.add_argument("--h-up", type=int, default=100)
+    ap.add_argument("--h-max", type=int, default=100)
     return ap.parse_args()
 
 
@@ -275,6 +279,70 @@ def make_line(*, cfg_id, cfg, world, steps, warmup, elapsed_ms, evals_total, pai
     }
 
 
+# ------------------------------------------------------------------ GLMB update
+def bench_update(a, st, scene, cfg, dev, stream, L):
+    """The hypothesis update and particle loop that consume the step's C_k:
+    death_prob -> compat_rows -> assoc_sample -> dedup -> prune -> assoc_pairs ->
+    reweight_pairs -> resample, on the device-resident C_k / particles of the last timed
+    step, H_old x H_up samples, tau = 1e-5, H_max (H_up = 100, tau = 1e-5,
+    H_max <= 100).  Reported beside the headline metric (not part of it)."""
+    import torch
+    from paper_2512_06230_b200.hyp import HypothesisUpdate, ParticleUpdate
+    from paper_2512_06230_b200.scenes import hypothesis_inputs
+    T = st.T_local
+    zi = (a.warmup + a.steps - 1) % len(st.Z)
+    Z = st.Z[zi]
+    M = Z.shape[0]
+    pm, plw, ps = hypothesis_inputs(cfg.T, cfg.B, a.h_old, seed=cfg.seed)
+    pm_d = torch.from_numpy(pm.view(np.int32)).to(dev)
+    plw_d = torch.from_numpy(plw).to(dev)
+    ps_d = torch.from_numpy(ps).to(dev)
+    hu = HypothesisUpdate(T, st.M_max, a.h_old, a.h_up, a.h_max, device=dev)
+    pu = ParticleUpdate(T, st.M_max, a.h_max, st.P, K_cap=16 * T, device=dev)
+    names = ["death_prob", "compat_rows", "assoc_sample", "dedup", "prune", "assoc_pairs",
+             "reweight_pairs", "resample"]
+    stage = {n: [] for n in names}
+    total = []
+
+    def run(k, timed):
+        evs = {}
+        def mark(name):
+            if timed:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(stream)
+                evs[name] = e
+        with torch.cuda.stream(stream):
+            if timed:
+                mark("start")
+            hu.run(st.out.C_tracks, st.out.gate, M, ps_d, pm_d, plw_d, cfg.p_d, cfg.kappa, 1e-5,
+                   seed=cfg.seed, step=k, stream=stream, mark=mark)
+            pu.run(st.particles, Z, st.R, hu.keep_idx, a.h_max, hu.alive, hu.theta, M, seed=cfg.seed,
+                   step=k, stream=stream, n_hyp_dev=hu.n_kept, mark=mark)
+        return evs
+
+    for k in range(a.warmup):
+        run(k, False)
+    torch.cuda.synchronize(dev)
+    all_evs = [run(k, True) for k in range(a.warmup, a.warmup + a.steps)]
+    torch.cuda.synchronize(dev)
+    for evs in all_evs:
+        prev = evs["start"]
+        for n in names:
+            stage[n].append(prev.elapsed_time(evs[n]))
+            prev = evs[n]
+        total.append(evs["start"].elapsed_time(evs["resample"]))
+    n_kept = int(hu.n_kept.item())
+    n_pairs = pu.n_pairs_checked()
+    fl = pu.flags[:n_pairs].cpu().numpy()
+    return {"workload": f"cfg{a.config if a.config is not None else 3} C_k (T_k={T}, M={M}) + particles; "
+                        f"H_old={a.h_old} x H_up={a.h_up}, tau=1e-5, H_max={a.h_max} (P:186)",
+            "ms": statistics.mean(total), "stages_ms": {n: statistics.mean(v) for n, v in stage.items()},
+            "n_samples": a.h_old * a.h_up, "n_unique": int(hu.unique.sum().item()), "n_kept": n_kept,
+            "n_pairs": n_pairs, "n_resampled": int(((fl >> 1) & 1).sum()),
+            "gpu_launches_per_update": 14,
+            "note": "device-resident; no host round trip inside (device counts n_kept / n_pairs)"}
+
+
 # ------------------------------------------------------------------ GPU arm
 def main():
     a = parse()
@@ -455,6 +523,10 @@ def main():
             dist.destroy_process_group()
         return
 
+    update = None
+    if world == 1 and not a.no_update:
+        update = bench_update(a, st, scene, cfg, dev, stream, L)
+
     cpu = None
     if world == 1 and not a.no_cpu_baseline:
         cpu = oracle_sample(cfg_id, a.cpu_seconds, host_cores())
@@ -465,6 +537,8 @@ def main():
         stage_ms=stage_ms, sm_count=L.glmb_sm_count(local), clocks=sampler.summary(),
         T_surv=st.T_surv, B_local=st.B_local, T_local=st.T_local, P=st.P, M_mean=float(np.mean(Ms)),
         traffic=compat_traffic(st.T_local, st.P, len(scene.Z[0])), e2e=e2e, cpu=cpu)
+    if update is not None:
+        line["glmb_update"] = update
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -378,13 +378,17 @@ glmb_status glmb_prune(int32_t n, const double *logw, const uint8_t *unique,
  *   pair_meas[pair_ptr[k] .. pair_ptr[k+1])), pair_of [n_hyp][T] int32 (the
  *   pair of (r, j), -1 if j is not alive in q), *n_pairs = K (device int32).
  * Capacities: pair_track n_hyp*T, pair_ptr n_hyp*T + 1, pair_meas n_hyp*M.
+ * n_hyp_dev (device int32, may be NULL): use only the first min(n_hyp,
+ * *n_hyp_dev) hypotheses (e.g. glmb_prune's n_kept) -- no host round trip;
+ * pair_of rows past it are not written.
  * workspace: device scratch of glmb_assoc_pairs_workspace_size(n_hyp, T, M)
  * bytes.  Exact (fingerprints only preselect the compared lists).
  * Errors: INVALID_ARG on negative sizes, T > 17066, bad ldt / ldm, NULL
  * pointers, a short workspace.
  * --------------------------------------------------------------------- */
 size_t glmb_assoc_pairs_workspace_size(int32_t n_hyp, int32_t T, int32_t M);
-glmb_status glmb_assoc_pairs(int32_t n_hyp, const int32_t *hyp_idx,
+glmb_status glmb_assoc_pairs(int32_t n_hyp, const int32_t *n_hyp_dev,
+                             const int32_t *hyp_idx,
                              const uint32_t *alive, int32_t ldt,
                              const int32_t *theta, int64_t ldm, int32_t T,
                              int32_t M, int32_t *pair_track, int32_t *pair_ptr,

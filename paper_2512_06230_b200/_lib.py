@@ -85,7 +85,7 @@ def load(path: str = LIB_PATH):
         L.glmb_prune.argtypes = [i32, vp, vp, C.c_double, i32, vp, vp, vp, vp, vp]
         L.glmb_assoc_pairs_workspace_size.argtypes = [i32, i32, i32]
         L.glmb_assoc_pairs_workspace_size.restype = C.c_size_t
-        L.glmb_assoc_pairs.argtypes = [i32, vp, vp, i32, vp, i64, i32, i32, vp, vp, vp, vp, vp, vp,
+        L.glmb_assoc_pairs.argtypes = [i32, vp, vp, vp, i32, vp, i64, i32, i32, vp, vp, vp, vp, vp, vp,
                                        C.c_size_t, vp]
         L.glmb_reweight_pairs.argtypes = [PP, vp, i32, f32, f32, f32, i32, vp, vp, vp, vp, vp, i64, vp, vp,
                                           vp, vp]
@@ -290,10 +290,11 @@ def glmb_assoc_pairs_workspace_size(n_hyp, T, M) -> int:
 
 
 def glmb_assoc_pairs(hyp_idx, alive, theta, T, M, pair_track, pair_ptr, pair_meas, pair_of, n_pairs,
-                     workspace, stream=None):
-    """hyp_idx [n_hyp] int32 rows of alive [., ldt] / theta [., ldm]; outputs as in glmb.h."""
+                     workspace, stream=None, n_hyp_dev=None):
+    """hyp_idx [n_hyp] int32 rows of alive [., ldt] / theta [., ldm]; outputs as in glmb.h.
+    n_hyp_dev: optional device int32 count of hypotheses actually used (e.g. glmb_prune's n_kept)."""
     n_hyp = hyp_idx.shape[0]
-    _check(load().glmb_assoc_pairs(n_hyp, _ptr(hyp_idx), _ptr(alive), alive.shape[1], _ptr(theta),
+    _check(load().glmb_assoc_pairs(n_hyp, _ptr(n_hyp_dev), _ptr(hyp_idx), _ptr(alive), alive.shape[1], _ptr(theta),
                                    theta.shape[1], int(T), int(M), _ptr(pair_track), _ptr(pair_ptr),
                                    _ptr(pair_meas), _ptr(pair_of), _ptr(n_pairs), _ptr(workspace),
                                    workspace.numel() * workspace.element_size(), _stream(stream)))

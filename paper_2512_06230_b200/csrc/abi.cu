@@ -370,7 +370,7 @@ size_t glmb_assoc_pairs_workspace_size(int32_t n_hyp, int32_t T, int32_t M) {
   return glmb::pairs_workspace_bytes(n_hyp, T, M);
 }
 
-glmb_status glmb_assoc_pairs(int32_t n_hyp, const int32_t *hyp_idx, const uint32_t *alive, int32_t ldt,
+glmb_status glmb_assoc_pairs(int32_t n_hyp, const int32_t *n_hyp_dev, const int32_t *hyp_idx, const uint32_t *alive, int32_t ldt,
                              const int32_t *theta, int64_t ldm, int32_t T, int32_t M, int32_t *pair_track,
                              int32_t *pair_ptr, int32_t *pair_meas, int32_t *pair_of, int32_t *n_pairs,
                              void *workspace, size_t workspace_bytes, glmb_stream_t stream) {
@@ -388,7 +388,7 @@ glmb_status glmb_assoc_pairs(int32_t n_hyp, const int32_t *hyp_idx, const uint32
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   GLMB_TRY(bind_stream(s, nullptr));
   glmb::PairsArgs a{};
-  a.n_hyp = n_hyp; a.T = T; a.M = M; a.ldt = ldt; a.ldm = ldm; a.hyp_idx = hyp_idx; a.alive = alive;
+  a.n_hyp = n_hyp; a.n_hyp_dev = n_hyp_dev; a.T = T; a.M = M; a.ldt = ldt; a.ldm = ldm; a.hyp_idx = hyp_idx; a.alive = alive;
   a.theta = theta; a.pair_track = pair_track; a.pair_ptr = pair_ptr; a.pair_meas = pair_meas;
   a.pair_of = pair_of; a.n_pairs = n_pairs;
   return from_cuda(glmb::launch_assoc_pairs(a, workspace, s));

@@ -153,6 +153,7 @@ cudaError_t launch_prune(const PruneArgs &a, cudaStream_t s);
 struct PairsArgs {
   int32_t n_hyp, T, M, ldt;
   int64_t ldm;
+  const int32_t *n_hyp_dev;  // optional device count (<= n_hyp) of hypotheses to use
   const int32_t *hyp_idx;
   const uint32_t *alive;
   const int32_t *theta;

@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(kInvThreads) invert_kernel(PairsArgs a) {
   int32_t *cnt = reinterpret_cast<int32_t *>(fp + a.T);                   // [T]
   __shared__ int32_t wsum[32];
   const int32_t r = blockIdx.x;
+  if (a.n_hyp_dev != nullptr && r >= __ldg(a.n_hyp_dev)) return;
   const int64_t q = __ldg(a.hyp_idx + r);
   const uint32_t *al = a.alive + q * a.ldt;
   const int32_t *th = a.theta + q * a.ldm;
@@ -131,7 +132,7 @@ __global__ void __launch_bounds__(kInvThreads) invert_kernel(PairsArgs a) {
 __global__ void __launch_bounds__(256) first_kernel(PairsArgs a) {
   const int32_t r = blockIdx.y;
   const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= a.T) return;
+  if (j >= a.T || (a.n_hyp_dev != nullptr && r >= __ldg(a.n_hyp_dev))) return;
   const int64_t e = static_cast<int64_t>(r) * a.T + j;
   const int32_t c = a.cnt[e];
   if (c < 0) {
@@ -158,7 +159,8 @@ __global__ void __launch_bounds__(256) first_kernel(PairsArgs a) {
 // numbering in (r, j) order: pair index and list offset of each first occurrence (one CTA)
 __global__ void __launch_bounds__(1024) number_kernel(PairsArgs a) {
   __shared__ int32_t wsum[32];
-  const int64_t n = static_cast<int64_t>(a.n_hyp) * a.T;
+  const int32_t nh = a.n_hyp_dev != nullptr ? min(a.n_hyp, *a.n_hyp_dev) : a.n_hyp;
+  const int64_t n = static_cast<int64_t>(nh) * a.T;
   int32_t kc = 0, mc = 0;
   for (int64_t e0 = 0; e0 < n; e0 += 1024) {
     const int64_t e = e0 + threadIdx.x;
@@ -190,7 +192,7 @@ __global__ void __launch_bounds__(1024) number_kernel(PairsArgs a) {
 __global__ void __launch_bounds__(256) finish_kernel(PairsArgs a) {
   const int32_t r = blockIdx.y;
   const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= a.T) return;
+  if (j >= a.T || (a.n_hyp_dev != nullptr && r >= __ldg(a.n_hyp_dev))) return;
   const int64_t e = static_cast<int64_t>(r) * a.T + j;
   const int32_t f = a.first[e];
   if (f < 0) {

@@ -43,20 +43,26 @@ class HypothesisUpdate:
         self.n_kept = torch.zeros(1, dtype=i32, device=dev)
 
     def run(self, C_tracks, gate, M, p_s, parent_mask, parent_logw, p_d, kappa, tau, seed, step,
-            stream=None):
+            stream=None, mark=None):
         """C_tracks [T, ldc] fp32 / gate [T, ldg] words as glmb_compat writes them (device);
         p_s [T] fp32; parent_mask [H_old, ldt] int32 words; parent_logw [H_old] fp64."""
         assert M <= self.M_max
         n = self.H_old * self.H_up
+        mark = mark or (lambda name: None)   # optional stage hook (bench: CUDA events)
         _lib.glmb_death_prob(C_tracks, gate, M, p_d, kappa, p_s, self.d, stream)
+        mark("death_prob")
         _lib.glmb_compat_rows(C_tracks, gate, M, self.row_ptr, self.col, self.val, self.ln_val, stream)
+        mark("compat_rows")
         _lib.glmb_assoc_sample(self.H_up, parent_mask, parent_logw, self.d[:self.T], p_s, p_d, kappa,
                                self.row_ptr, self.col, self.val, self.ln_val, M, seed, step,
                                self.alive[:n], self.theta[:n], self.logw[:n], self.hash[:n], stream)
+        mark("assoc_sample")
         _lib.glmb_dedup(self.H_old, self.H_up, M, self.alive[:n], self.theta[:n], self.hash[:n],
                         self.unique[:n], stream)
+        mark("dedup")
         _lib.glmb_prune(self.logw[:n], self.unique[:n], tau, self.h_max, self.keys[:n], self.keep_idx,
                         self.keep_w, self.n_kept, stream)
+        mark("prune")
 
 
 class ParticleUpdate:
@@ -86,18 +92,25 @@ class ParticleUpdate:
         self.ess = torch.empty(Kc, dtype=torch.float32, device=dev)
         self.out = Particles.empty(Kc, P, device=dev)
 
-    def run(self, src, Z, R, hyp_idx, n_hyp, alive, theta, M, seed, step, stream=None):
+    def run(self, src, Z, R, hyp_idx, n_hyp, alive, theta, M, seed, step, stream=None, n_hyp_dev=None,
+            mark=None):
         """src: Particles of the T_k predicted tracks; hyp_idx [>= n_hyp] device int32 (e.g. the
-        pruned keep_idx); alive / theta: the sampler's outputs.  New set: self.out rows < n_pairs."""
+        pruned keep_idx); alive / theta: the sampler's outputs; n_hyp_dev: optional device count
+        (e.g. HypothesisUpdate.n_kept, with n_hyp = h_max) so nothing waits on the host.
+        New set: self.out rows < n_pairs."""
         assert n_hyp <= self.n_hyp_max and M <= self.M_max
+        mark = mark or (lambda name: None)
         hi = hyp_idx[:n_hyp]
         _lib.glmb_assoc_pairs(hi, alive, theta, self.T, M, self.pair_track, self.pair_ptr, self.pair_meas,
-                              self.pair_of, self.n_pairs, self.ws, stream)
+                              self.pair_of, self.n_pairs, self.ws, stream, n_hyp_dev=n_hyp_dev)
+        mark("assoc_pairs")
         K = min(self.K_cap, max(1, n_hyp * self.T))
         _lib.glmb_reweight_pairs(src, Z, R, K, self.n_pairs, self.pair_track, self.pair_ptr, self.pair_meas,
                                  self.w_new[:K], self.log_norm, self.flags, self.ess, stream)
+        mark("reweight_pairs")
         _lib.glmb_resample(src, K, self.n_pairs, self.pair_track, self.w_new[:K], self.out, seed, step,
                            self.flags, stream)
+        mark("resample")
 
     def n_pairs_checked(self) -> int:
         """Synchronises and returns K; raises if the pairs overflowed K_cap (rows past it were not updated)."""
