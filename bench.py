@@ -33,9 +33,10 @@ sys.path.insert(0, ROOT)
 METRIC = "particle-measurement likelihood evals/s (GLMB step: predict+birth+compat+reweight)"
 SFU_EX2_PER_CLK_PER_SM = 16          # MUFU.EX2 lanes/clk/SM on sm_100 (measured: glmb_peaks)
 FMA_LANES_PER_CLK_PER_SM = 128       # FP32 FMA lanes/clk/SM (FFMA or FFMA2 x 2), measured: glmb_peaks
-# compat, per pair: 4 FMA-pipe ops + one exp; an exp moved to the FMA pipe costs 8 FMA-pipe ops.
-# Best split f of exps on the FMA pipe: x(1-f) = E, x(4+8f) = F  ->  x = (F + 8E) / 12 pairs/clk/SM.
-COMPAT_PAIRS_PER_CLK_PER_SM = (FMA_LANES_PER_CLK_PER_SM + 8 * SFU_EX2_PER_CLK_PER_SM) / 12.0
+# compat, per pair (exact-difference form): 5 FP32 lane-ops (dx, dy, dx^2, +dy^2, acc) + one exp;
+# an exp moved to the FMA pipe costs 8 FP32 lane-ops.
+# Best split f of exps on the FMA pipe: x(1-f) = E, x(5+8f) = F  ->  x = (F + 8E) / 13 pairs/clk/SM.
+COMPAT_PAIRS_PER_CLK_PER_SM = (FMA_LANES_PER_CLK_PER_SM + 8 * SFU_EX2_PER_CLK_PER_SM) / 13.0
 HBM_PEAK_GBPS_FALLBACK = 6556.5      # MEASURED_PEAKS.json hbm_gbs (read at run time when present)
 
 
@@ -262,7 +263,7 @@ def make_line(*, cfg_id, cfg, world, steps, warmup, elapsed_ms, evals_total, pai
                      "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Geval/s",
                      "frac": achieved / peak,
                      "peak_basis": f"{sm_count} SM x {COMPAT_PAIRS_PER_CLK_PER_SM:.2f} pairs/clk "
-                                   f"(16 ex2/clk + 128 FMA lanes/clk, measured) x {f_max / 1e6:.0f} MHz",
+                                   f"(16 ex2/clk + 128 FP32 lanes/clk, measured; 5 lanes + 1 exp per pair) x {f_max / 1e6:.0f} MHz",
                      "frac_of_mufu_only_bound": achieved / peak_sfu,
                      "frac_at_measured_clock": (achieved / (sm_count * COMPAT_PAIRS_PER_CLK_PER_SM * sm_mhz * 1e6)
                                                 if sm_mhz else None),

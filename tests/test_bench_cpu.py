@@ -29,7 +29,7 @@ def test_make_line_contract():
     assert line["ms_per_step"] == pytest.approx(2.5)
     r = line["roofline"]
     assert r["bound"] == "alu" and 0 < r["frac"] < 1 and r["frac"] == pytest.approx(r["achieved"] / r["peak"])
-    assert r["peak"] == pytest.approx(148 * (128 + 8 * 16) / 12 * 1.965e9 / 1e9)
+    assert r["peak"] == pytest.approx(148 * (128 + 8 * 16) / 13 * 1.965e9 / 1e9)   # 5 lanes + 1 exp per pair
     assert line["gpu_launches"] == 16
     assert line["cpu_baseline"]["cores"] == 8 and "seconds" not in line["cpu_baseline"]
     assert "workload" in line["config"]
