@@ -92,6 +92,10 @@ def lib():
                                                 + [C.c_float] * 3 + [C.c_int32, i32, i32, i32, f64, f64, u32, f64])
             L.oracle_resample.argtypes = [C.c_int32, f32, C.c_uint64, C.c_uint32, C.c_int32, i32]
             L.oracle_resample.restype = C.c_int
+            L.oracle_next_parents.argtypes = [C.c_int32, f64, i32, C.c_int32, C.c_int32, C.c_int32,
+                                              C.c_int32, C.c_int64, u32, f64]
+            L.oracle_map_estimate.argtypes = [C.c_int32, i32, C.c_int32, C.c_int32, C.c_int64, f32, f32,
+                                              f32, f64]
             L.oracle_num_threads.restype = C.c_int
             L.oracle_set_num_threads.argtypes = [C.c_int]
             _lib = L
@@ -344,3 +348,26 @@ def resample(w, seed, step, k):
     anc = np.full(len(w), -1, np.int32)
     r = lib().oracle_resample(len(w), w, C.c_uint64(seed), C.c_uint32(step), int(k), anc)
     return bool(r), anc
+
+
+# ----------------------------------------------------------------- O17-O18 (tracker loop)
+def next_parents(keep_w, pair_of, T, K_cap, B, birth_col0, ldt):
+    """(mask u32 [n_kept][ldt], logw f64 [n_kept]) of the next step's parents (O17)."""
+    kw = np.ascontiguousarray(keep_w, np.float64)
+    n = len(kw)
+    po = np.ascontiguousarray(pair_of, np.int32).reshape(max(n, 1), -1) if n else np.zeros((1, max(T, 1)), np.int32)
+    mask = np.zeros((max(n, 1), ldt), np.uint32)
+    lw = np.zeros(max(n, 1), np.float64)
+    lib().oracle_next_parents(n, kw if n else np.zeros(1), po, T, K_cap, B, birth_col0, ldt, mask, lw)
+    return mask[:n], lw[:n]
+
+
+def map_estimate(n_kept, pair_of0, x, y, w):
+    """est [T][3] = (x, y, 1) weighted mean of row pair_of0[j] of (x, y, w), or (nan, nan, 0) (O18)."""
+    x, y, w = _f32(x), _f32(y), _f32(w)
+    po = np.ascontiguousarray(pair_of0, np.int32)
+    T = len(po)
+    P = x.shape[1]
+    est = np.zeros((max(T, 1), 3), np.float64)
+    lib().oracle_map_estimate(int(n_kept), po if T else np.zeros(1, np.int32), T, P, P, x, y, w, est)
+    return est[:T]

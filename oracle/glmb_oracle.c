@@ -725,3 +725,58 @@ int oracle_resample(int32_t P, const float *w, uint64_t seed, uint32_t step, int
   free(W);
   return res;
 }
+
+/* ==================================================================
+ * Closing the tracker loop: the kept hypotheses become
+ * the next step's parents, and the MAP hypothesis gives the state estimate.
+ * ================================================================== */
+
+/* O17 Next parents, P:44 ("For each of the H_old hypotheses from the
+ * previous timestep k-1, a new set of H_up hypotheses is generated") with
+ * P:24 (births are superposed on every hypothesis), reading R33: kept
+ * hypothesis r (< n_kept, in pruned order) becomes parent r of the next
+ * step; its tracks are the pairs it uses, pair_of[r][j] >= 0 (their rows in
+ * the new particle set, < K_cap), plus the B birth columns birth_col0 ..
+ * birth_col0+B-1; its log-weight is ln keep_w[r]. */
+void oracle_next_parents(int32_t n_kept, const double *keep_w, const int32_t *pair_of,
+                         int32_t T, int32_t K_cap, int32_t B, int32_t birth_col0,
+                         int64_t ldt, uint32_t *mask, double *logw) {
+  for (int32_t r = 0; r < n_kept; ++r) {
+    uint32_t *m = mask + (int64_t)r * ldt;
+    for (int64_t k = 0; k < ldt; ++k) m[k] = 0u;
+    for (int32_t j = 0; j < T; ++j) {
+      int32_t k = pair_of[(int64_t)r * T + j];
+      if (k >= 0 && k < K_cap) m[k / 32] |= 1u << (k % 32);
+    }
+    for (int32_t b = 0; b < B; ++b) {
+      int32_t c = birth_col0 + b;
+      m[c / 32] |= 1u << (c % 32);
+    }
+    logw[r] = log(keep_w[r]);
+  }
+}
+
+/* O18 State estimate of the most likely hypothesis (reading R34): for every
+ * track j alive in kept hypothesis 0 (pair_of row 0 >= 0), the weighted mean
+ * position of its updated particles, sum_p w_p (x_p, y_p) / sum_p w_p, of row
+ * pair_of[0][j] of the new particle set; est [T][3] = (x, y, 1), or
+ * (NaN, NaN, 0) for tracks not in the hypothesis. */
+void oracle_map_estimate(int32_t n_kept, const int32_t *pair_of0, int32_t T, int32_t P,
+                         int64_t ld, const float *x, const float *y, const float *w,
+                         double *est) {
+  for (int32_t j = 0; j < T; ++j) {
+    int32_t k = n_kept > 0 ? pair_of0[j] : -1;
+    if (k < 0) {
+      est[3 * j] = NAN; est[3 * j + 1] = NAN; est[3 * j + 2] = 0.0;
+      continue;
+    }
+    double sw = 0.0, sx = 0.0, sy = 0.0;
+    for (int32_t p = 0; p < P; ++p) {
+      double wp = (double)w[(int64_t)k * ld + p];
+      sw += wp;
+      sx += wp * (double)x[(int64_t)k * ld + p];
+      sy += wp * (double)y[(int64_t)k * ld + p];
+    }
+    est[3 * j] = sx / sw; est[3 * j + 1] = sy / sw; est[3 * j + 2] = 1.0;
+  }
+}
