@@ -81,7 +81,8 @@ def lib():
                                              i32, i32, f32, f64]
             L.oracle_assoc_sample.argtypes = (
                 [C.c_int32] * 4 + [u32, C.c_int64, f64, f32, f32, C.c_float, C.c_float,
-                                   i32, i32, f32, f64, C.c_uint64, C.c_uint32, u32, i32, C.c_int64, f64])
+                                   i32, i32, f32, f64, f64, C.c_int32, C.c_uint64, C.c_uint32, u32, i32,
+                                   C.c_int64, f64])
             L.oracle_dedup.argtypes = [C.c_int32] * 3 + [u32, C.c_int64, i32, C.c_int64, u8]
             L.oracle_prune.argtypes = [C.c_int32, f64, u8, C.c_double, C.c_int32, i32, f64]
             L.oracle_prune.restype = C.c_int32
@@ -258,9 +259,13 @@ def compat_rows(C_tracks, gate, M):
     return rp, col[:n].copy(), val[:n].copy(), lv[:n].copy()
 
 
-def assoc_sample(parent_mask, parent_logw, H_up, d_prob, p_s, p_d, kappa, rows, M, seed, step):
-    """Two-stage sampler (O11).  parent_mask u32 [H_old][ldt]; rows = compat_rows(...).
+def assoc_sample(parent_mask, parent_logw, H_up, d_prob, p_s, p_d, kappa, rows, M, seed, step,
+                 count_lp=None):
+    """Two-stage sampler (O11).  parent_mask u32 [H_old][ldt]; rows = compat_rows(...);
+    count_lp: optional ln prior of the number of measurements per alive track (index min(n, len-1)).
     Returns (alive u32 [H_old*H_up][ldt], theta i32 [H_old*H_up][M], logw f64 [H_old*H_up])."""
+    clp = np.ascontiguousarray(count_lp if count_lp is not None else np.zeros(1), np.float64)
+    n_count = 0 if count_lp is None else len(clp)
     pm = np.ascontiguousarray(parent_mask, np.uint32)
     H_old, ldt = pm.shape
     T = len(d_prob)
@@ -273,7 +278,8 @@ def assoc_sample(parent_mask, parent_logw, H_up, d_prob, p_s, p_d, kappa, rows, 
     lib().oracle_assoc_sample(H_old, H_up, T, M, pm, ldt, np.ascontiguousarray(parent_logw, np.float64),
                               one(d_prob, np.float32), one(p_s, np.float32), float(p_d), float(kappa),
                               np.ascontiguousarray(rp, np.int32), one(col, np.int32), one(val, np.float32),
-                              one(lv, np.float64), C.c_uint64(seed), C.c_uint32(step), alive, theta,
+                              one(lv, np.float64), clp, n_count, C.c_uint64(seed), C.c_uint32(step),
+                              alive, theta,
                               theta.shape[1], logw)
     return alive, theta[:, :M], logw
 

@@ -431,7 +431,11 @@ static double sampler_uniform(uint64_t seed, uint32_t step, uint32_t domain,
  *  weight ("multiplying its parent's weight with the joint likelihood of
  *   the sampled survival/death events and data associations", R28):
  *   ln w = ln w_parent + sum_{j in parent} (alive ? ln P_S : ln(1 - P_S))
- *        + sum_i ln C'[i, theta_i] + #(alive j with no measurement) ln(1 - P_D).
+ *        + sum_i ln C'[i, theta_i] + sum_{alive j} lc(n_j),
+ *   n_j = #{i : theta_i = j+1}; lc(0) = ln(1 - P_D), lc(n >= 1) = 0 by default;
+ *   with a count table (n_count > 0) lc(n) = count_lp[min(n, n_count - 1)]:
+ *   the cardinality prior on the number of measurements per object that the
+ *   independent proposal ignores and the importance weight restores.
  * Outputs for sample q = h*H_up + s: alive [q][ldt] bits, theta [q][ldm],
  * logw [q]. */
 void oracle_assoc_sample(int32_t H_old, int32_t H_up, int32_t T, int32_t M,
@@ -439,7 +443,8 @@ void oracle_assoc_sample(int32_t H_old, int32_t H_up, int32_t T, int32_t M,
                          const double *parent_logw, const float *d_prob,
                          const float *p_s, float p_d, float kappa,
                          const int32_t *row_ptr, const int32_t *col,
-                         const float *val, const double *ln_val, uint64_t seed,
+                         const float *val, const double *ln_val,
+                         const double *count_lp, int32_t n_count, uint64_t seed,
                          uint32_t step, uint32_t *alive, int32_t *theta,
                          int64_t ldm, double *logw) {
 #pragma omp parallel for schedule(dynamic)
@@ -491,12 +496,15 @@ void oracle_assoc_sample(int32_t H_old, int32_t H_up, int32_t T, int32_t M,
       }
       th[i] = pick;
       lw += lpick;
-      if (pick > 0) detected[pick - 1] = 1;
+      if (pick > 0) detected[pick - 1] += 1;
     }
-    int missed = 0;
-    for (int32_t j = 0; j < T; ++j)
-      if (((al[j / 32] >> (j % 32)) & 1u) && !detected[j]) ++missed;
-    lw += (double)missed * log(1.0 - (double)p_d);
+    for (int32_t j = 0; j < T; ++j) {
+      if (!((al[j / 32] >> (j % 32)) & 1u)) continue;
+      if (n_count > 0)
+        lw += count_lp[detected[j] < n_count ? detected[j] : n_count - 1];
+      else if (detected[j] == 0)
+        lw += log(1.0 - (double)p_d);
+    }
     logw[q] = lw;
     free(detected);
   }

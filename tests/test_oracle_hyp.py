@@ -89,7 +89,8 @@ def test_compat_rows_round_trip(orc):
 
 
 # ------------------------------------------------------------------ O11
-def _sampler(orc, C, g, d, ps, pd, kappa, H_up, seed=1, step=0, parent_mask=None, parent_logw=None):
+def _sampler(orc, C, g, d, ps, pd, kappa, H_up, seed=1, step=0, parent_mask=None, parent_logw=None,
+             count_lp=None):
     T, M = C.shape[0], C.shape[1]
     ldt = max(1, (T + 31) // 32)
     if parent_mask is None:
@@ -100,7 +101,7 @@ def _sampler(orc, C, g, d, ps, pd, kappa, H_up, seed=1, step=0, parent_mask=None
         parent_logw = np.zeros(parent_mask.shape[0])
     rows = orc.compat_rows(C, g, M)
     return orc.assoc_sample(parent_mask, parent_logw, H_up, np.asarray(d, np.float32), np.asarray(ps, np.float32),
-                            pd, kappa, rows, M, seed, step), rows
+                            pd, kappa, rows, M, seed, step, count_lp=count_lp), rows
 
 
 def test_sampler_forced_outcomes(orc):
@@ -271,3 +272,53 @@ def test_prune_spec_and_edges(orc):
     idx2, kw2 = orc.prune(np.log([0.2, 0.4, 0.4]) - 2000.0, np.ones(3, np.uint8), 0.0, 2)
     np.testing.assert_array_equal(idx, idx2)
     np.testing.assert_allclose(kw, kw2, rtol=1e-12)
+
+
+def _exact_posterior_counts(C, ps, kappa, lc):
+    """Enumeration with a per-track measurement-count prior exp(lc[min(n, len-1)]) for alive tracks."""
+    T, M = C.shape
+    out = {}
+    for alive in itertools.product([0, 1], repeat=T):
+        choices = [[0] + [j + 1 for j in range(T) if alive[j]] for _ in range(M)]
+        for th in itertools.product(*choices):
+            w = 1.0
+            for j in range(T):
+                w *= ps[j] if alive[j] else 1 - ps[j]
+                if alive[j]:
+                    n = sum(1 for c in th if c == j + 1)
+                    w *= math.exp(lc[min(n, len(lc) - 1)])
+            for i, c in enumerate(th):
+                w *= kappa if c == 0 else float(C[c - 1, i])
+            out[(alive, th)] = w
+    z = sum(out.values())
+    return {k: v / z for k, v in out.items()}
+
+
+def test_successors_with_count_prior(orc):
+    """the proposal ignores the per-object measurement-count prior, the importance weight
+    restores it.  With a Poisson(D) count table (combined with C's P_D factor: e^-D D^n / P_D^n)
+    the unique weighted samples reproduce the exact enumerated posterior of that target."""
+    T, M = 2, 3
+    C = np.array([[0.8, 0.05, 0.4], [0.3, 0.6, 0.5]], np.float32)
+    g = np.array([[0b111], [0b111]], np.uint32)
+    ps, pd, kappa, D = np.array([0.9, 0.7], np.float32), 0.8, 0.2, 1.5
+    lc = np.array([-D + n * math.log(D) - n * math.log(pd) for n in range(M + 1)])
+    d = np.array([0.3, 0.4], np.float32)
+    H = 4000
+    (al, th, lw), _ = _sampler(orc, C, g, d, ps, pd, kappa, H, seed=12, count_lp=lc)
+    u = orc.dedup(al, th, 1, H)
+    keys = [(tuple(int((al[q, 0] >> j) & 1) for j in range(T)), tuple(int(t) for t in th[q])) for q in range(H)]
+    exact = _exact_posterior_counts(C, [float(v) for v in ps], kappa, lc)
+    idx, w = orc.prune(lw, u, 0.0, 10 ** 6)
+    got = {keys[q]: wq for q, wq in zip(idx, w)}
+    tv = 0.5 * sum(abs(got.get(k, 0.0) - p) for k, p in exact.items())
+    assert tv < 0.02
+    uniq = [q for q in range(H) if u[q]]
+    ratios = [math.exp(lw[q]) / exact[keys[q]] for q in uniq]
+    np.testing.assert_allclose(ratios, ratios[0], rtol=1e-6)
+    # the default (no table) is the table [ln(1 - P_D), 0, 0, ...]
+    (al1, th1, lw1), _ = _sampler(orc, C, g, d, ps, pd, kappa, 50, seed=3)
+    (al2, th2, lw2), _ = _sampler(orc, C, g, d, ps, pd, kappa, 50, seed=3,
+                                 count_lp=np.array([math.log(1 - float(np.float32(pd))), 0.0]))
+    np.testing.assert_array_equal(th1, th2)
+    np.testing.assert_allclose(lw1, lw2, rtol=1e-15)
