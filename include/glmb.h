@@ -301,8 +301,13 @@ glmb_status glmb_compat_rows(int32_t T, int32_t M, const float *C_tracks,
  *  weight ("multiplying its parent's weight with the joint likelihood of
  *   the sampled survival/death events and data associations", R28), fp64:
  *   logw = parent_logw[h] + sum_{j in parent} (alive ? ln P_S,j : ln(1-P_S,j))
- *        + sum_i ln C'[i, theta_i] + #(alive j with no measurement) ln(1-P_D)
- *   (ln C'[i, 0] = ln kappa; ln C'[i, j+1] = ln_val of the CSR entry).
+ *        + sum_i ln C'[i, theta_i] + sum_{alive j} lc(n_j)
+ *   (ln C'[i, 0] = ln kappa; ln C'[i, j+1] = ln_val of the CSR entry;
+ *   n_j = #{i : theta_i = j+1}).  lc: with n_count == 0 (count_lp may be
+ *   NULL) lc(0) = ln(1-P_D), lc(n >= 1) = 0; with n_count > 0 (device
+ *   count_lp [n_count] fp64, T <= 32768) lc(n) = count_lp[min(n, n_count-1)]:
+ *   the prior on the number of measurements per object that the independent
+ *   proposal ignores and the importance weight restores.
  * Inputs: parent_mask [H_old][ldt] u32 (bit j%32 of word j/32: track j is in
  * parent h), ldt >= ceil(T/32), 1 <= ldt <= 12288; parent_logw [H_old] fp64;
  * d_prob, p_s [T] fp32; the CSR of glmb_compat_rows (row_ptr [M+1], col,
@@ -312,17 +317,21 @@ glmb_status glmb_compat_rows(int32_t T, int32_t M, const float *C_tracks,
  *   entries [M, ldm) not written; ldm % 4 == 0, theta 16-B aligned);
  *   logw [H_old*H_up] fp64; hash [H_old*H_up] u64 (optional, may be NULL): a
  *   64-bit fingerprint of (alive, theta) consumed by glmb_dedup.
+ * n_parents (device int32, may be NULL): only parents h < *n_parents are
+ * sampled (the rest of the H_old slots are skipped; their outputs untouched).
  * Results do not depend on the launch configuration (bit-exact integers).
  * Errors: INVALID_ARG on negative sizes, H_up >= 2^24, H_old*H_up >= 2^31,
  * p_d not in (0,1], kappa < 0, bad ldt / ldm, NULL pointers;
  * ALIGNMENT on ldm % 4 != 0 or a misaligned theta.
  * --------------------------------------------------------------------- */
-glmb_status glmb_assoc_sample(int32_t H_old, int32_t H_up, int32_t T, int32_t M,
+glmb_status glmb_assoc_sample(int32_t H_old, const int32_t *n_parents,
+                              int32_t H_up, int32_t T, int32_t M,
                               const uint32_t *parent_mask, int32_t ldt,
                               const double *parent_logw, const float *d_prob,
                               const float *p_s, float p_d, float kappa,
                               const int32_t *row_ptr, const int32_t *col,
                               const float *val, const double *ln_val,
+                              const double *count_lp, int32_t n_count,
                               uint64_t seed, uint32_t step, uint32_t *alive,
                               int32_t *theta, int64_t ldm, double *logw,
                               uint64_t *hash, glmb_stream_t stream);
@@ -332,9 +341,12 @@ glmb_status glmb_assoc_sample(int32_t H_old, int32_t H_up, int32_t T, int32_t M,
  * retained", R27): unique[q] = 1 iff no earlier sample s2 < s of the same
  * parent has identical alive words (ldt) and theta entries (M); exact (the
  * fingerprints from glmb_assoc_sample only select the pairs compared).
+ * n_parents (device int32, may be NULL): samples of parents h >= *n_parents
+ * get unique = 0.
  * Errors: INVALID_ARG on negative sizes, ldt < 1, ldm < M, NULL pointers.
  * --------------------------------------------------------------------- */
-glmb_status glmb_dedup(int32_t H_old, int32_t H_up, int32_t M,
+glmb_status glmb_dedup(int32_t H_old, const int32_t *n_parents, int32_t H_up,
+                       int32_t M,
                        const uint32_t *alive, int32_t ldt, const int32_t *theta,
                        int64_t ldm, const uint64_t *hash, uint8_t *unique,
                        glmb_stream_t stream);
@@ -439,6 +451,39 @@ glmb_status glmb_resample(const glmb_particles *src, int32_t K,
                           const float *w, int64_t ldw,
                           const glmb_particles *out, uint64_t seed,
                           uint32_t step, uint32_t *flags, glmb_stream_t stream);
+
+/* =====================================================================
+ * Tracker loop: the kept hypotheses become the next
+ * step's parents; the most likely hypothesis gives the state estimate.
+ * Readings R33, R34 in DESIGN.md §3.
+ * ===================================================================== */
+
+/* glmb_next_parents -- P:44 ("For each of the H_old hypotheses from the
+ * previous timestep ...") with P:24 (births superposed on every hypothesis):
+ * for r < *n_kept (the kept hypotheses in pruned order, as glmb_prune and
+ * glmb_assoc_pairs leave them): parent_mask[r] ([ldt] u32 words) = bits of
+ * the pairs pair_of[r][j] >= 0 with index < K_cap (their rows in the new
+ * particle set) and of the birth columns birth_col0 .. birth_col0+B-1;
+ * parent_logw[r] = ln keep_w[r]; *n_parents = min(*n_kept, n_hyp_cap).
+ * Rows r >= *n_kept are not written.  All pointers device memory.
+ * Errors: INVALID_ARG on negative sizes, K_cap or birth columns beyond
+ * 32*ldt, ldt > 12288, NULL pointers. */
+glmb_status glmb_next_parents(int32_t n_hyp_cap, const int32_t *n_kept,
+                              const double *keep_w, const int32_t *pair_of,
+                              int32_t T, int32_t K_cap, int32_t B,
+                              int32_t birth_col0, uint32_t *parent_mask,
+                              int32_t ldt, double *parent_logw,
+                              int32_t *n_parents, glmb_stream_t stream);
+
+/* glmb_map_estimate -- the state estimate of the most likely hypothesis
+ * (R34): for every old track j < T with k = pair_of0[j] >= 0 (row 0 of
+ * glmb_assoc_pairs' pair_of, i.e. the best kept hypothesis) and *n_kept > 0,
+ * est[j] = (sum_p w_p x_p / sum_p w_p, ... y ..., 1) over row k of `set` (the
+ * new particle set); otherwise est[j] = (NaN, NaN, 0).  est: [T][3] fp64,
+ * sums in fp64.  Errors: INVALID_ARG on NULL pointers / bad particle set. */
+glmb_status glmb_map_estimate(const int32_t *n_kept, const int32_t *pair_of0,
+                              int32_t T, const glmb_particles *set, double *est,
+                              glmb_stream_t stream);
 
 /* ---------------------------------------------------------------------
  * Test hooks (not on the hot path; same device code as predict/birth).

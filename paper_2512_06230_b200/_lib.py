@@ -47,7 +47,8 @@ EXPORTED = ["glmb_version", "glmb_status_string", "glmb_init", "glmb_sm_count", 
             "glmb_birth", "glmb_compat", "glmb_reweight", "glmb_step", "glmb_step_host",
             "glmb_philox_dump", "glmb_normals_dump", "glmb_death_prob", "glmb_compat_rows",
             "glmb_assoc_sample", "glmb_dedup", "glmb_prune", "glmb_assoc_pairs_workspace_size",
-            "glmb_assoc_pairs", "glmb_reweight_pairs", "glmb_resample"]
+            "glmb_assoc_pairs", "glmb_reweight_pairs", "glmb_resample", "glmb_next_parents",
+            "glmb_map_estimate"]
 
 
 def load(path: str = LIB_PATH):
@@ -79,9 +80,11 @@ def load(path: str = LIB_PATH):
         L.glmb_normals_dump.argtypes = [u64, vp, i32, vp, vp]
         L.glmb_death_prob.argtypes = [i32, i32, vp, i64, vp, i64, f32, f32, vp, vp, vp]
         L.glmb_compat_rows.argtypes = [i32, i32, vp, i64, vp, i64, vp, vp, vp, vp, i32, vp]
-        L.glmb_assoc_sample.argtypes = [i32, i32, i32, i32, vp, i32, vp, vp, vp, f32, f32, vp, vp, vp,
-                                        vp, u64, u32, vp, vp, i64, vp, vp, vp]
-        L.glmb_dedup.argtypes = [i32, i32, i32, vp, i32, vp, i64, vp, vp, vp]
+        L.glmb_assoc_sample.argtypes = [i32, vp, i32, i32, i32, vp, i32, vp, vp, vp, f32, f32, vp, vp, vp,
+                                        vp, vp, i32, u64, u32, vp, vp, i64, vp, vp, vp]
+        L.glmb_dedup.argtypes = [i32, vp, i32, i32, vp, i32, vp, i64, vp, vp, vp]
+        L.glmb_next_parents.argtypes = [i32, vp, vp, vp, i32, i32, i32, i32, vp, i32, vp, vp, vp]
+        L.glmb_map_estimate.argtypes = [vp, vp, i32, PP, vp, vp]
         L.glmb_prune.argtypes = [i32, vp, vp, C.c_double, i32, vp, vp, vp, vp, vp]
         L.glmb_assoc_pairs_workspace_size.argtypes = [i32, i32, i32]
         L.glmb_assoc_pairs_workspace_size.restype = C.c_size_t
@@ -264,18 +267,21 @@ def glmb_compat_rows(C_tracks, gate, M, row_ptr, col, val, ln_val, stream=None):
 
 
 def glmb_assoc_sample(H_up, parent_mask, parent_logw, d_prob, p_s, p_d, kappa, row_ptr, col, val, ln_val,
-                      M, seed, step, alive, theta, logw, hash=None, stream=None):
-    """parent_mask [H_old, ldt] int32 words; alive [H_old*H_up, ldt]; theta [H_old*H_up, ldm] int32."""
+                      M, seed, step, alive, theta, logw, hash=None, stream=None, n_parents=None,
+                      count_lp=None):
+    """parent_mask [H_old, ldt] int32 words; alive [H_old*H_up, ldt]; theta [H_old*H_up, ldm] int32.
+    n_parents: optional device int32 count of valid parent rows."""
     H_old, ldt = parent_mask.shape
     T = d_prob.shape[0]
-    _check(load().glmb_assoc_sample(H_old, int(H_up), T, int(M), _ptr(parent_mask), ldt, _ptr(parent_logw),
+    _check(load().glmb_assoc_sample(H_old, _ptr(n_parents), int(H_up), T, int(M), _ptr(parent_mask), ldt, _ptr(parent_logw),
                                     _ptr(d_prob), _ptr(p_s), p_d, kappa, _ptr(row_ptr), _ptr(col), _ptr(val),
-                                    _ptr(ln_val), int(seed) & 0xFFFFFFFFFFFFFFFF, int(step), _ptr(alive),
+                                    _ptr(ln_val), _ptr(count_lp), 0 if count_lp is None else count_lp.shape[0],
+                                    int(seed) & 0xFFFFFFFFFFFFFFFF, int(step), _ptr(alive),
                                     _ptr(theta), theta.shape[1], _ptr(logw), _ptr(hash), _stream(stream)))
 
 
-def glmb_dedup(H_old, H_up, M, alive, theta, hash, unique, stream=None):
-    _check(load().glmb_dedup(int(H_old), int(H_up), int(M), _ptr(alive), alive.shape[1], _ptr(theta),
+def glmb_dedup(H_old, H_up, M, alive, theta, hash, unique, stream=None, n_parents=None):
+    _check(load().glmb_dedup(int(H_old), _ptr(n_parents), int(H_up), int(M), _ptr(alive), alive.shape[1], _ptr(theta),
                              theta.shape[1], _ptr(hash), _ptr(unique), _stream(stream)))
 
 
@@ -314,3 +320,20 @@ def glmb_resample(src: Particles, K, n_pairs, pair_track, w, out: Particles, see
     _check(load().glmb_resample(C.byref(a), int(K), _ptr(n_pairs), _ptr(pair_track), _ptr(w), w.shape[1],
                                 C.byref(b), int(seed) & 0xFFFFFFFFFFFFFFFF, int(step), _ptr(flags),
                                 _stream(stream)))
+
+
+# --------------------------------------------------------------- tracker loop (f4)
+def glmb_next_parents(n_kept, keep_w, pair_of, K_cap, B, birth_col0, parent_mask, parent_logw, n_parents,
+                      stream=None):
+    """pair_of [n_hyp_cap, T] int32; parent_mask [n_hyp_cap, ldt] int32 words (outputs on device)."""
+    n_hyp_cap, T = pair_of.shape
+    _check(load().glmb_next_parents(n_hyp_cap, _ptr(n_kept), _ptr(keep_w), _ptr(pair_of), T, int(K_cap), int(B),
+                                    int(birth_col0), _ptr(parent_mask), parent_mask.shape[1], _ptr(parent_logw),
+                                    _ptr(n_parents), _stream(stream)))
+
+
+def glmb_map_estimate(n_kept, pair_of0, new_set: Particles, est, stream=None):
+    """pair_of0 [T] int32 (row 0 of pair_of); est [T, 3] fp64."""
+    t = new_set.struct()
+    _check(load().glmb_map_estimate(_ptr(n_kept), _ptr(pair_of0), pair_of0.shape[0], C.byref(t), _ptr(est),
+                                    _stream(stream)))

@@ -311,15 +311,18 @@ glmb_status glmb_compat_rows(int32_t T, int32_t M, const float *C_tracks, int64_
   return from_cuda(glmb::launch_compat_rows(a, s));
 }
 
-glmb_status glmb_assoc_sample(int32_t H_old, int32_t H_up, int32_t T, int32_t M, const uint32_t *parent_mask,
+glmb_status glmb_assoc_sample(int32_t H_old, const int32_t *n_parents, int32_t H_up, int32_t T, int32_t M,
+                              const uint32_t *parent_mask,
                               int32_t ldt, const double *parent_logw, const float *d_prob, const float *p_s,
                               float p_d, float kappa, const int32_t *row_ptr, const int32_t *col, const float *val,
-                              const double *ln_val, uint64_t seed, uint32_t step, uint32_t *alive, int32_t *theta,
-                              int64_t ldm, double *logw, uint64_t *hash, glmb_stream_t stream) {
+                              const double *ln_val, const double *count_lp, int32_t n_count, uint64_t seed,
+                              uint32_t step, uint32_t *alive, int32_t *theta, int64_t ldm, double *logw,
+                              uint64_t *hash, glmb_stream_t stream) {
   if (H_old < 0 || H_up < 0 || T < 0 || M < 0) return GLMB_ERR_INVALID_ARG;
   if (H_up >= (1 << 24) || static_cast<int64_t>(H_old) * H_up > 0x7fffffffLL) return GLMB_ERR_INVALID_ARG;
   if (!(p_d > 0.f && p_d <= 1.f) || !(kappa >= 0.f)) return GLMB_ERR_INVALID_ARG;
   if (ldt < (T + 31) / 32 || ldt < 1 || ldt > 12 * 1024 || ldm < M) return GLMB_ERR_INVALID_ARG;
+  if (n_count < 0 || (n_count > 0 && (count_lp == nullptr || T > 32768))) return GLMB_ERR_INVALID_ARG;
   if (static_cast<int64_t>(H_old) * H_up == 0) return GLMB_OK;
   if (parent_mask == nullptr || parent_logw == nullptr || alive == nullptr || logw == nullptr || row_ptr == nullptr)
     return GLMB_ERR_INVALID_ARG;
@@ -329,13 +332,15 @@ glmb_status glmb_assoc_sample(int32_t H_old, int32_t H_up, int32_t T, int32_t M,
   if (M > 0 && ((ldm & 3) || (reinterpret_cast<uintptr_t>(theta) & 15u))) return GLMB_ERR_ALIGNMENT;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   GLMB_TRY(bind_stream(s, nullptr));
-  glmb::SampleArgs a{H_old, H_up, T, M, parent_mask, ldt, parent_logw, d_prob, p_s, p_d, kappa, row_ptr, col, val,
-                     ln_val, static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32), step, alive, theta, ldm,
+  glmb::SampleArgs a{H_old, H_up, T, M, n_parents, parent_mask, ldt, parent_logw, d_prob, p_s, p_d, kappa, row_ptr, col, val,
+                     ln_val, count_lp, n_count, static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32), step,
+                     alive, theta, ldm,
                      logw, reinterpret_cast<unsigned long long *>(hash)};
   return from_cuda(glmb::launch_assoc_sample(a, s));
 }
 
-glmb_status glmb_dedup(int32_t H_old, int32_t H_up, int32_t M, const uint32_t *alive, int32_t ldt,
+glmb_status glmb_dedup(int32_t H_old, const int32_t *n_parents, int32_t H_up, int32_t M, const uint32_t *alive,
+                       int32_t ldt,
                        const int32_t *theta, int64_t ldm, const uint64_t *hash, uint8_t *unique,
                        glmb_stream_t stream) {
   if (H_old < 0 || H_up < 0 || M < 0 || ldt < 1 || ldm < M) return GLMB_ERR_INVALID_ARG;
@@ -344,7 +349,7 @@ glmb_status glmb_dedup(int32_t H_old, int32_t H_up, int32_t M, const uint32_t *a
     return GLMB_ERR_INVALID_ARG;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   GLMB_TRY(bind_stream(s, nullptr));
-  glmb::DedupArgs a{H_old, H_up, M, ldt, ldm, alive, theta, reinterpret_cast<const unsigned long long *>(hash),
+  glmb::DedupArgs a{H_old, H_up, M, ldt, n_parents, ldm, alive, theta, reinterpret_cast<const unsigned long long *>(hash),
                     unique};
   return from_cuda(glmb::launch_dedup(a, s));
 }
@@ -449,6 +454,37 @@ glmb_status glmb_resample(const glmb_particles *src, int32_t K, const int32_t *n
   a.key0 = static_cast<uint32_t>(seed); a.key1 = static_cast<uint32_t>(seed >> 32); a.step = step;
   a.flags = flags;
   return from_cuda(glmb::launch_resample(a, s));
+}
+
+// ------------------------------------------------------------------ tracker loop (f4)
+glmb_status glmb_next_parents(int32_t n_hyp_cap, const int32_t *n_kept, const double *keep_w, const int32_t *pair_of,
+                              int32_t T, int32_t K_cap, int32_t B, int32_t birth_col0, uint32_t *parent_mask,
+                              int32_t ldt, double *parent_logw, int32_t *n_parents, glmb_stream_t stream) {
+  if (n_hyp_cap < 0 || T < 0 || K_cap < 0 || B < 0 || birth_col0 < 0 || ldt < 1) return GLMB_ERR_INVALID_ARG;
+  if (static_cast<int64_t>(K_cap) > 32LL * ldt || static_cast<int64_t>(birth_col0) + B > 32LL * ldt ||
+      ldt > 12 * 1024)
+    return GLMB_ERR_INVALID_ARG;
+  if (n_kept == nullptr || n_parents == nullptr) return GLMB_ERR_INVALID_ARG;
+  if (n_hyp_cap > 0 && (keep_w == nullptr || parent_mask == nullptr || parent_logw == nullptr ||
+                        (T > 0 && pair_of == nullptr)))
+    return GLMB_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  GLMB_TRY(bind_stream(s, nullptr));
+  glmb::NextParentsArgs a{n_hyp_cap, n_kept, keep_w, pair_of, T, K_cap, B, birth_col0, ldt, parent_mask,
+                          parent_logw, n_parents};
+  return from_cuda(glmb::launch_next_parents(a, s));
+}
+
+glmb_status glmb_map_estimate(const int32_t *n_kept, const int32_t *pair_of0, int32_t T, const glmb_particles *set,
+                              double *est, glmb_stream_t stream) {
+  if (T < 0 || n_kept == nullptr) return GLMB_ERR_INVALID_ARG;
+  if (T == 0) return GLMB_OK;
+  GLMB_TRY(check_particles(set, true, false));
+  if (pair_of0 == nullptr || est == nullptr || set->n_tracks == 0) return GLMB_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  GLMB_TRY(bind_stream(s, nullptr));
+  glmb::MapEstimateArgs a{n_kept, pair_of0, T, set->n_particles, set->ld, set->x, set->y, set->w, est};
+  return from_cuda(glmb::launch_map_estimate(a, s));
 }
 
 glmb_status glmb_philox_dump(uint64_t seed, const uint32_t *ctr, int32_t N, uint32_t *out, glmb_stream_t stream) {

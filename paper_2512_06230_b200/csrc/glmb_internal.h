@@ -94,6 +94,7 @@ struct RowsArgs {
 
 struct SampleArgs {
   int32_t H_old, H_up, T, M;
+  const int32_t *n_parents;  // optional device count (<= H_old) of valid parents
   const uint32_t *parent_mask;
   int32_t ldt;
   const double *parent_logw;
@@ -102,6 +103,8 @@ struct SampleArgs {
   const int32_t *row_ptr, *col;
   const float *val;
   const double *ln_val;
+  const double *count_lp;  // optional per-track measurement-count log prior (n_count entries)
+  int32_t n_count;
   uint32_t key0, key1, step;
   uint32_t *alive;
   int32_t *theta;
@@ -112,6 +115,7 @@ struct SampleArgs {
 
 struct DedupArgs {
   int32_t H_old, H_up, M, ldt;
+  const int32_t *n_parents;  // optional device count of valid parents (others: unique = 0)
   int64_t ldm;
   const uint32_t *alive;
   const int32_t *theta;
@@ -180,5 +184,27 @@ struct ResampleArgs {
   uint32_t *flags;                       // bit 1 set when unit k was resampled
 };
 cudaError_t launch_resample(const ResampleArgs &a, cudaStream_t s);
+
+// ---- tracker loop (pairs.cu)
+struct NextParentsArgs {
+  int32_t n_hyp_cap;
+  const int32_t *n_kept;
+  const double *keep_w;
+  const int32_t *pair_of;  // [n_hyp_cap][T]
+  int32_t T, K_cap, B, birth_col0, ldt;
+  uint32_t *parent_mask;   // [n_hyp_cap][ldt]
+  double *parent_logw;
+  int32_t *n_parents;
+};
+cudaError_t launch_next_parents(const NextParentsArgs &a, cudaStream_t s);
+
+struct MapEstimateArgs {
+  const int32_t *n_kept, *pair_of0;
+  int32_t T, P;
+  int64_t ld;
+  const float *x, *y, *w;
+  double *est;  // [T][3]
+};
+cudaError_t launch_map_estimate(const MapEstimateArgs &a, cudaStream_t s);
 
 }  // namespace glmb

@@ -170,16 +170,20 @@ __device__ __forceinline__ Tv block_sum_128(Tv v, Tv *red) {
 __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a) {
   extern __shared__ uint32_t sm[];
   uint32_t *alive = sm, *det = sm + a.ldt;
+  int32_t *cnt = reinterpret_cast<int32_t *>(sm + 2 * a.ldt);  // [T] when a count prior is given
   __shared__ double red_d[4];
   __shared__ unsigned long long red_u[4];
   __shared__ int32_t red_i[4];
   const int64_t q = blockIdx.x;
   const int32_t h = static_cast<int32_t>(q / a.H_up), s = static_cast<int32_t>(q - static_cast<int64_t>(h) * a.H_up);
+  if (a.n_parents != nullptr && h >= __ldg(a.n_parents)) return;  // inactive parent slot
   const uint32_t *pm = a.parent_mask + static_cast<int64_t>(h) * a.ldt;
   for (int32_t k = threadIdx.x; k < a.ldt; k += kSampThreads) {
     alive[k] = 0u;
     det[k] = 0u;
   }
+  if (a.n_count > 0)
+    for (int32_t j = threadIdx.x; j < a.T; j += kSampThreads) cnt[j] = 0;
   __syncthreads();
 
   // stage 1: track j of the parent survives iff u_j < 1 - d_j (fp32, R25);
@@ -255,7 +259,10 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
       }
       pick4[e] = pick;
       lw += lpick;
-      if (pick > 0) atomicOr(det + ((pick - 1) >> 5), 1u << ((pick - 1) & 31));
+      if (pick > 0) {
+        atomicOr(det + ((pick - 1) >> 5), 1u << ((pick - 1) & 31));
+        if (a.n_count > 0) atomicAdd(cnt + pick - 1, 1);
+      }
       fp += fp_term(static_cast<uint32_t>(pick), static_cast<uint64_t>(a.ldt) + i);
     }
     const int32_t i0 = 4 * t;
@@ -267,7 +274,8 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
   }
   __syncthreads();
 
-  // missed detections: alive tracks with no measurement; fingerprint of the alive words
+  // missed detections: alive tracks with no measurement (or, with a count prior,
+  // lc(n_j) for every alive track); fingerprint of the alive words
   int32_t missed = 0;
   uint32_t *al_out = a.alive + q * a.ldt;
   for (int32_t k = threadIdx.x; k < a.ldt; k += kSampThreads) {
@@ -275,6 +283,11 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
     missed += __popc(av & ~det[k]);
     al_out[k] = av;
     fp += fp_term(av, static_cast<uint64_t>(k));
+  }
+  if (a.n_count > 0) {
+    missed = 0;
+    for (int32_t j = threadIdx.x; j < a.T; j += kSampThreads)
+      if ((alive[j >> 5] >> (j & 31)) & 1u) lw += __ldg(a.count_lp + min(cnt[j], a.n_count - 1));
   }
   lw = block_sum_128(lw, red_d);
   const unsigned long long fps = block_sum_128(static_cast<unsigned long long>(fp), red_u);
@@ -304,6 +317,10 @@ __global__ void __launch_bounds__(kDedupThreads) dedup_kernel(DedupArgs a) {
   __shared__ unsigned long long hs[kDedupTile];
   const int32_t h = blockIdx.x;
   const int64_t base = static_cast<int64_t>(h) * a.H_up;
+  if (a.n_parents != nullptr && h >= __ldg(a.n_parents)) {  // inactive parent slot: no candidates
+    for (int32_t s = threadIdx.x; s < a.H_up; s += kDedupThreads) a.unique[base + s] = 0;
+    return;
+  }
   for (int32_t s0 = 0; s0 < a.H_up; s0 += kDedupThreads) {
     const int32_t s = s0 + threadIdx.x;
     const unsigned long long mine = s < a.H_up ? a.hash[base + s] : 0ull;
@@ -564,7 +581,8 @@ cudaError_t launch_compat_rows(const RowsArgs &a, cudaStream_t s) {
 
 cudaError_t launch_assoc_sample(const SampleArgs &a, cudaStream_t s) {
   const int64_t n = static_cast<int64_t>(a.H_old) * a.H_up;
-  const size_t smem = sizeof(uint32_t) * 2 * static_cast<size_t>(a.ldt);
+  const size_t smem = sizeof(uint32_t) * 2 * static_cast<size_t>(a.ldt) +
+                      (a.n_count > 0 ? sizeof(int32_t) * static_cast<size_t>(a.T) : 0);
   if (smem > 40 * 1024) {  // dynamic + static shared memory past the 48 KB default
     cudaError_t e = cudaFuncSetAttribute(assoc_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));

@@ -325,6 +325,77 @@ __global__ void __launch_bounds__(kResThreads) resample_kernel(ResampleArgs a) {
   }
 }
 
+// ------------------------------------------------------------------ tracker loop (f4)
+// Kept hypothesis r -> parent r of the next step: bits of the pairs it uses
+// (rows of the new particle set) plus the birth columns; ln of its weight.
+__global__ void __launch_bounds__(128) next_parents_kernel(NextParentsArgs a) {
+  extern __shared__ uint32_t msk[];  // [ldt]
+  const int32_t r = blockIdx.x;
+  const int32_t nk = __ldg(a.n_kept);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *a.n_parents = min(nk, a.n_hyp_cap);
+  if (r >= nk) return;
+  for (int32_t k = threadIdx.x; k < a.ldt; k += blockDim.x) msk[k] = 0u;
+  __syncthreads();
+  const int32_t *po = a.pair_of + static_cast<int64_t>(r) * a.T;
+  for (int32_t j = threadIdx.x; j < a.T; j += blockDim.x) {
+    const int32_t k = __ldg(po + j);
+    if (k >= 0 && k < a.K_cap) atomicOr(msk + (k >> 5), 1u << (k & 31));
+  }
+  for (int32_t b = threadIdx.x; b < a.B; b += blockDim.x) {
+    const int32_t c = a.birth_col0 + b;
+    atomicOr(msk + (c >> 5), 1u << (c & 31));
+  }
+  __syncthreads();
+  uint32_t *out = a.parent_mask + static_cast<int64_t>(r) * a.ldt;
+  for (int32_t k = threadIdx.x; k < a.ldt; k += blockDim.x) out[k] = msk[k];
+  if (threadIdx.x == 0) a.parent_logw[r] = log(__ldg(a.keep_w + r));
+}
+
+// MAP estimate: weighted mean position of each track of kept hypothesis 0 (fp64 sums)
+__global__ void __launch_bounds__(256) map_estimate_kernel(MapEstimateArgs a) {
+  __shared__ double red[3][8];
+  const int32_t j = blockIdx.x;
+  const int32_t k = __ldg(a.n_kept) > 0 ? __ldg(a.pair_of0 + j) : -1;
+  double *e = a.est + 3 * static_cast<int64_t>(j);
+  if (k < 0) {
+    if (threadIdx.x == 0) {
+      e[0] = __longlong_as_double(0x7ff8000000000000ll);
+      e[1] = e[0];
+      e[2] = 0.0;
+    }
+    return;
+  }
+  const int64_t base = static_cast<int64_t>(k) * a.ld;
+  double sw = 0.0, sx = 0.0, sy = 0.0;
+  for (int32_t p = threadIdx.x; p < a.P; p += blockDim.x) {
+    const double w = __ldg(a.w + base + p);
+    sw += w;
+    sx += w * static_cast<double>(__ldg(a.x + base + p));
+    sy += w * static_cast<double>(__ldg(a.y + base + p));
+  }
+  sw = warp_sum_d(sw);
+  sx = warp_sum_d(sx);
+  sy = warp_sum_d(sy);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[0][wid] = sw;
+    red[1][wid] = sx;
+    red[2][wid] = sy;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tw = 0.0, tx = 0.0, ty = 0.0;
+    for (int q = 0; q < 8; ++q) {
+      tw += red[0][q];
+      tx += red[1][q];
+      ty += red[2][q];
+    }
+    e[0] = tx / tw;
+    e[1] = ty / tw;
+    e[2] = 1.0;
+  }
+}
+
 }  // namespace
 
 size_t pairs_workspace_bytes(int32_t n_hyp, int32_t T, int32_t M) {
@@ -371,6 +442,22 @@ cudaError_t launch_resample(const ResampleArgs &a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
   }
   resample_kernel<<<a.K, kResThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace glmb
+
+namespace glmb {
+
+cudaError_t launch_next_parents(const NextParentsArgs &a, cudaStream_t s) {
+  if (a.n_hyp_cap == 0) return cudaMemsetAsync(a.n_parents, 0, sizeof(int32_t), s);
+  next_parents_kernel<<<a.n_hyp_cap, 128, sizeof(uint32_t) * a.ldt, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_map_estimate(const MapEstimateArgs &a, cudaStream_t s) {
+  if (a.T == 0) return cudaSuccess;
+  map_estimate_kernel<<<a.T, 256, 0, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -43,7 +43,9 @@ class HypothesisUpdate:
         self.n_kept = torch.zeros(1, dtype=i32, device=dev)
 
     def run(self, C_tracks, gate, M, p_s, parent_mask, parent_logw, p_d, kappa, tau, seed, step,
-            stream=None, mark=None):
+            stream=None, mark=None, n_parents=None, count_lp=None):
+        """n_parents: optional device int32 count of valid rows of parent_mask (<= H_old);
+        count_lp: optional device fp64 measurement-count log prior per alive track."""
         """C_tracks [T, ldc] fp32 / gate [T, ldg] words as glmb_compat writes them (device);
         p_s [T] fp32; parent_mask [H_old, ldt] int32 words; parent_logw [H_old] fp64."""
         assert M <= self.M_max
@@ -55,10 +57,11 @@ class HypothesisUpdate:
         mark("compat_rows")
         _lib.glmb_assoc_sample(self.H_up, parent_mask, parent_logw, self.d[:self.T], p_s, p_d, kappa,
                                self.row_ptr, self.col, self.val, self.ln_val, M, seed, step,
-                               self.alive[:n], self.theta[:n], self.logw[:n], self.hash[:n], stream)
+                               self.alive[:n], self.theta[:n], self.logw[:n], self.hash[:n], stream,
+                               n_parents=n_parents, count_lp=count_lp)
         mark("assoc_sample")
         _lib.glmb_dedup(self.H_old, self.H_up, M, self.alive[:n], self.theta[:n], self.hash[:n],
-                        self.unique[:n], stream)
+                        self.unique[:n], stream, n_parents=n_parents)
         mark("dedup")
         _lib.glmb_prune(self.logw[:n], self.unique[:n], tau, self.h_max, self.keys[:n], self.keep_idx,
                         self.keep_w, self.n_kept, stream)
@@ -69,7 +72,8 @@ class ParticleUpdate:
     """Unique (track, measurement set) pairs of the kept hypotheses, their particle update and
     resampling into a new particle set with one row per pair."""
 
-    def __init__(self, T: int, M_max: int, n_hyp_max: int, P: int, K_cap: int | None = None, device="cuda"):
+    def __init__(self, T: int, M_max: int, n_hyp_max: int, P: int, K_cap: int | None = None, device="cuda",
+                 own_out: bool = True):
         """K_cap: rows of the new particle set (default min(n_hyp_max, 4) * T); the pair lists
         themselves are sized for the worst case n_hyp_max * T."""
         from ._lib import Particles
@@ -90,14 +94,14 @@ class ParticleUpdate:
         self.log_norm = torch.empty(Kc, dtype=torch.float32, device=dev)
         self.flags = torch.empty(Kc, dtype=i32, device=dev)
         self.ess = torch.empty(Kc, dtype=torch.float32, device=dev)
-        self.out = Particles.empty(Kc, P, device=dev)
+        self.out = Particles.empty(Kc, P, device=dev) if own_out else None
 
     def run(self, src, Z, R, hyp_idx, n_hyp, alive, theta, M, seed, step, stream=None, n_hyp_dev=None,
-            mark=None):
+            mark=None, out=None):
         """src: Particles of the T_k predicted tracks; hyp_idx [>= n_hyp] device int32 (e.g. the
         pruned keep_idx); alive / theta: the sampler's outputs; n_hyp_dev: optional device count
         (e.g. HypothesisUpdate.n_kept, with n_hyp = h_max) so nothing waits on the host.
-        New set: self.out rows < n_pairs."""
+        New set: rows < n_pairs of `out` (default self.out; any Particles with >= K_cap rows)."""
         assert n_hyp <= self.n_hyp_max and M <= self.M_max
         mark = mark or (lambda name: None)
         hi = hyp_idx[:n_hyp]
@@ -108,8 +112,8 @@ class ParticleUpdate:
         _lib.glmb_reweight_pairs(src, Z, R, K, self.n_pairs, self.pair_track, self.pair_ptr, self.pair_meas,
                                  self.w_new[:K], self.log_norm, self.flags, self.ess, stream)
         mark("reweight_pairs")
-        _lib.glmb_resample(src, K, self.n_pairs, self.pair_track, self.w_new[:K], self.out, seed, step,
-                           self.flags, stream)
+        _lib.glmb_resample(src, K, self.n_pairs, self.pair_track, self.w_new[:K], self.out if out is None else out,
+                           seed, step, self.flags, stream)
         mark("resample")
 
     def n_pairs_checked(self) -> int:

@@ -1,0 +1,208 @@
+"""The whole GLMB tracker loop on the GPU (§Approach,
+the convoy benchmark of P:182-186 §Experiments).
+
+One update per time step, every stage a libglmb.so kernel behind the C ABI:
+
+    predict (survivors) -> birth -> compat -> death_prob -> compat_rows -> assoc_sample
+    -> dedup -> prune -> assoc_pairs -> reweight_pairs -> resample -> map_estimate
+    -> next_parents
+
+The kept hypotheses' unique (track, measurement set) pairs become the next
+step's tracks (rows of the new particle set), each kept hypothesis becomes a
+parent over those rows plus the birth columns (R33).  Counts stay on the
+device between stages; the host reads one int per step (the number of pairs,
+which fixes the next step's track count and birth column) -- the only
+synchronisation.  Python does argument marshalling and buffer bookkeeping only.
+"""
+from __future__ import annotations
+
+import dataclasses
+import time
+from typing import List
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import Particles
+from .hyp import HypothesisUpdate, ParticleUpdate
+from .scenes import ConvoyConfig
+
+
+@dataclasses.dataclass
+class UpdateRecord:
+    step: int
+    M: int
+    T_k: int
+    n_parents: int
+    n_kept: int
+    n_pairs: int
+    device_ms: float
+    wall_ms: float
+
+
+def count_log_prior(cfg: ConvoyConfig, M_max: int) -> np.ndarray:
+    """lc(n), n = 0..n_max, for glmb_assoc_sample (reading R36): the set likelihood of n
+    detections from one object is pi(n) n! prod L(z_i) for a count distribution pi; C already
+    carries one P_D per measurement, so lc(n) = ln pi(n) + ln n! - n ln P_D.
+    poisson:  pi = Poisson(D)            -> ln pi(n) + ln n! = -D + n ln D
+    binomial: pi = Binomial(n_max, q), n_max = round(D / q) (mean ~D, variance D (1 - q))
+              -> ln C(n_max, n) + n ln q + (n_max - n) ln(1 - q) + ln n!   (n > n_max: -1e4)"""
+    from math import lgamma, log
+    pd = float(np.float32(cfg.p_d))
+    D = cfg.D
+    if cfg.count_model == "poisson":
+        n = np.arange(M_max + 1, dtype=np.float64)
+        return -D + n * log(D) - n * log(pd)
+    q = cfg.count_q
+    nmax = int(round(D / q))
+    lc = np.full(nmax + 2, -1e4)
+    for n in range(nmax + 1):
+        lc[n] = (lgamma(nmax + 1) - lgamma(n + 1) - lgamma(nmax - n + 1) + n * log(q)
+                 + (nmax - n) * log(1.0 - q) + lgamma(n + 1) - n * log(pd))
+    return lc
+
+
+class ConvoyTracker:
+    def __init__(self, cfg: ConvoyConfig, M_max: int, K_cap: int = 1024, device="cuda"):
+        self.cfg = cfg
+        dev = torch.device(device)
+        self.dev = dev
+        B, P = cfg.B, cfg.P
+        self.K_cap, self.M_max = K_cap, M_max
+        self.T_cap = K_cap + B
+        rows = self.T_cap
+        # two particle sets: [survivors | births]; the particle update writes the other one
+        self.bufs = [Particles.empty(rows, P, device=dev), Particles.empty(rows, P, device=dev)]
+        for b in self.bufs:
+            b.data.zero_()
+        self.cur = 0
+        self.gid = torch.arange(rows, dtype=torch.int32, device=dev)
+        self.p_s = torch.empty(rows, dtype=torch.float32, device=dev)
+        self.ldc = max(32, (M_max + 31) // 32 * 32)
+        self.ldg = max(1, (M_max + 31) // 32)
+        self.C_clutter = torch.empty(max(M_max, 1), dtype=torch.float32, device=dev)
+        self.C_tracks = torch.empty(rows, self.ldc, dtype=torch.float32, device=dev)
+        self.gate = torch.empty(rows, self.ldg, dtype=torch.int32, device=dev)
+        self.Z = torch.empty(max(M_max, 1), 2, dtype=torch.float32, device=dev)
+        H = cfg.H_max
+        self.hu = HypothesisUpdate(rows, M_max, H, cfg.H_up, H, device=dev)
+        self.pu = ParticleUpdate(rows, M_max, H, P, K_cap=K_cap, device=dev, own_out=False)
+        self.ldt = self.hu.ldt
+        self.parent_mask = torch.zeros(H, self.ldt, dtype=torch.int32, device=dev)
+        self.parent_logw = torch.zeros(H, dtype=torch.float64, device=dev)
+        self.n_parents = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.est = torch.empty(rows, 3, dtype=torch.float64, device=dev)
+        self.count_lp = torch.from_numpy(count_log_prior(cfg, M_max)).to(dev) if cfg.count_prior else None
+        self.birth_mean = None
+        self.birth_chol = None
+        self.n_surv = 0
+        self.stream = torch.cuda.Stream(device=dev)
+        self.counts = torch.zeros(3, dtype=torch.int32, device=dev)
+        self.counts_host = torch.zeros(3, dtype=torch.int32).pin_memory()
+        self.est_host = torch.zeros(rows, 3, dtype=torch.float64).pin_memory()
+
+    def reset(self, birth_mean: np.ndarray, birth_chol: np.ndarray):
+        """Empty track set; one parent (the empty hypothesis, weight 1) over the birth columns."""
+        cfg = self.cfg
+        self.birth_mean = torch.from_numpy(np.ascontiguousarray(birth_mean, np.float32)).to(self.dev)
+        self.birth_chol = torch.from_numpy(np.ascontiguousarray(birth_chol, np.float32)).to(self.dev)
+        self.n_surv = 0
+        self.cur = 0
+        one = torch.ones(1, dtype=torch.float64, device=self.dev)
+        n1 = torch.ones(1, dtype=torch.int32, device=self.dev)
+        none = torch.full((1, 1), -1, dtype=torch.int32, device=self.dev)
+        _lib.glmb_next_parents(n1, one, none, 0, cfg.B, 0, self.parent_mask[:1], self.parent_logw[:1],
+                               self.n_parents, self.stream)
+
+    def update(self, k: int, Z: np.ndarray, host_Z: bool = True) -> UpdateRecord:
+        cfg, s = self.cfg, self.stream
+        M = Z.shape[0]
+        assert M <= self.M_max
+        t0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        src = self.bufs[self.cur]
+        dst = self.bufs[1 - self.cur]
+        T, B = self.n_surv, cfg.B
+        Tk = T + B
+        with torch.cuda.stream(s):
+            e0.record(s)
+            self.Z[:M].copy_(torch.from_numpy(Z), non_blocking=True)
+            Zk = self.Z[:M]
+            self.p_s[:T].fill_(cfg.p_s)
+            self.p_s[T:Tk].fill_(cfg.r_birth)
+            if T:
+                surv = src.rows(0, T)
+                _lib.glmb_predict(surv, surv, self.gid[:T], cfg.dt, cfg.sigma_a, cfg.sigma_w, cfg.seed, k, s)
+            _lib.glmb_birth(src.rows(T, Tk), self.gid[T:Tk], self.birth_mean, self.birth_chol, cfg.seed, k, s)
+            trk = src.rows(0, Tk)
+            _lib.glmb_compat(trk, Zk, cfg.R, cfg.p_d, cfg.kappa, cfg.gamma, self.C_clutter[:M],
+                             self.C_tracks[:Tk], self.gate[:Tk], s)
+            hu = self.hu
+            # the hypothesis machinery works on T_k columns (capacity-sized buffers, views)
+            hu.T = Tk
+            hu.run(self.C_tracks[:Tk], self.gate[:Tk], M, self.p_s[:Tk], self.parent_mask,
+                   self.parent_logw, cfg.p_d, cfg.kappa, cfg.tau, cfg.seed, k, s, n_parents=self.n_parents,
+                   count_lp=self.count_lp)
+            pu = self.pu
+            pu.T = Tk
+            pu.run(trk, Zk, cfg.R, hu.keep_idx, cfg.H_max, hu.alive, hu.theta, M, cfg.seed, k, s,
+                   n_hyp_dev=hu.n_kept, out=dst.rows(0, self.K_cap))
+            po = pu.pair_of.view(-1)[:cfg.H_max * Tk].view(cfg.H_max, Tk)   # packed [H][T_k]
+            _lib.glmb_map_estimate(hu.n_kept, po[0], dst.rows(0, self.K_cap), self.est[:Tk], s)
+            self.counts[0:1].copy_(pu.n_pairs)
+            self.counts[1:2].copy_(hu.n_kept)
+            self.counts[2:3].copy_(self.n_parents)
+            self.counts_host.copy_(self.counts, non_blocking=True)
+            e1.record(s)
+        s.synchronize()
+        K, n_kept, n_par = (int(v) for v in self.counts_host)
+        if K > self.K_cap:
+            raise RuntimeError(f"step {k}: {K} unique pairs exceed K_cap = {self.K_cap}")
+        with torch.cuda.stream(s):
+            # kept hypotheses -> parents over the new rows [0, K) and the next births at [K, K + B)
+            _lib.glmb_next_parents(hu.n_kept, hu.keep_w, po, self.K_cap, B, K,
+                                   self.parent_mask, self.parent_logw, self.n_parents, s)
+        wall = (time.perf_counter() - t0) * 1e3
+        self.n_surv = K
+        self.cur = 1 - self.cur
+        return UpdateRecord(k, M, Tk, n_par, n_kept, K, e0.elapsed_time(e1), wall)
+
+    def estimate(self, T_k: int) -> np.ndarray:
+        """MAP positions [n, 2] of the last update (host copy; evaluation only)."""
+        e = self.est[:T_k].cpu().numpy()
+        return e[e[:, 2] > 0, :2]
+
+
+def run_convoy(cfg: ConvoyConfig, steps: int | None = None, K_cap: int = 1024, device="cuda",
+               with_estimates: bool = True):
+    """Runs the tracker over the convoy scene; returns (records, estimates, truth)."""
+    from .scenes import convoy_scene
+    Zs, truth, bm, bc = convoy_scene(cfg)
+    n = len(Zs) if steps is None else min(steps, len(Zs))
+    M_max = max(len(z) for z in Zs[:n])
+    tr = ConvoyTracker(cfg, M_max, K_cap=K_cap, device=device)
+    tr.reset(bm, bc)
+    recs: List[UpdateRecord] = []
+    ests = []
+    for k in range(n):
+        rec = tr.update(k, Zs[k])
+        recs.append(rec)
+        if with_estimates:
+            ests.append(tr.estimate(rec.T_k))
+    return recs, ests, truth[:n]
+
+
+def convoy_metrics(ests, truth):
+    """mean relative absolute cardinality error, and the mean distance of the
+    Hungarian (minimum-distance) matching between estimated and true positions."""
+    from scipy.optimize import linear_sum_assignment
+    card, dist = [], []
+    for e, t in zip(ests, truth):
+        n = len(t)
+        card.append(abs(len(e) - n) / max(n, 1))
+        if len(e) and n:
+            Dm = np.linalg.norm(e[:, None, :] - t[None, :, :], axis=2)
+            r, c = linear_sum_assignment(Dm)
+            dist.append(float(Dm[r, c].mean()))
+    return float(np.mean(card)), float(np.mean(dist)) if dist else float("nan")

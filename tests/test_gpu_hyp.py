@@ -68,7 +68,7 @@ def _gpu_rows(L, C, g, M, cap=None):
     return _host(rp), _host(col), _host(val), _host(lv)
 
 
-def _gpu_sample(L, H_up, pm, plw, d, ps, p_d, kappa, rows, M, seed, step, ldm=None):
+def _gpu_sample(L, H_up, pm, plw, d, ps, p_d, kappa, rows, M, seed, step, ldm=None, count_lp=None):
     import torch
     H_old, ldt = pm.shape
     n = H_old * H_up
@@ -82,7 +82,7 @@ def _gpu_sample(L, H_up, pm, plw, d, ps, p_d, kappa, rows, M, seed, step, ldm=No
     L.glmb_assoc_sample(H_up, _dev(pm.view(np.int32)), _dev(plw), _dev(np.asarray(d, np.float32)),
                         _dev(np.asarray(ps, np.float32)), p_d, kappa, _dev(rp), _dev(one(col, np.int32)),
                         _dev(one(val, np.float32)), _dev(one(lv, np.float64)), M, seed, step,
-                        alive, theta, logw, hsh)
+                        alive, theta, logw, hsh, count_lp=None if count_lp is None else _dev(count_lp))
     return (_host(alive).view(np.uint32), _host(theta), _host(logw), _host(hsh))
 
 
@@ -348,3 +348,19 @@ def test_hypothesis_update_chain(L, orc):
     k = int(_host(hu.n_kept)[0])
     np.testing.assert_array_equal(_host(hu.keep_idx)[:k], r_idx)
     np.testing.assert_allclose(_host(hu.keep_w)[:k], r_w, rtol=1e-9)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "dense-rows", "cfg3-shaped"])
+def test_assoc_sample_count_prior(L, orc, name):
+    """The per-track measurement-count prior (Poisson(D) over C's P_D factor) vs O11."""
+    import math
+    C, g, M, pm, plw, ps, d, p_d, kappa, H_up = _sample_case(orc, name)
+    D = 2.5
+    pd32 = float(np.float32(p_d))
+    lc = np.array([-D + n * math.log(D) - n * math.log(pd32) for n in range(12)])
+    rows = orc.compat_rows(C, g, M)
+    al, th, lw, hs = _gpu_sample(L, H_up, pm, plw, d, ps, p_d, kappa, rows, M, 31, 2, count_lp=lc)
+    r_al, r_th, r_lw = orc.assoc_sample(pm, plw, H_up, d, ps, p_d, kappa, rows, M, 31, 2, count_lp=lc)
+    np.testing.assert_array_equal(al, r_al)
+    np.testing.assert_array_equal(th[:, :M], r_th)
+    _check_logw(lw, r_lw)
