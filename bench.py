@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--h-old", type=int, default=100)
     ap.add_argument("--h-up", type=int, default=100)
     ap.add_argument("--h-max", type=int, default=100)
+    ap.add_argument("--no-convoy", action="store_true", help="skip the paper-shaped convoy run (f4)")
     return ap.parse_args()
 
 
@@ -344,6 +345,31 @@ def bench_update(a, st, scene, cfg, dev, stream, L):
             "note": "device-resident; no host round trip inside (device counts n_kept / n_pairs)"}
 
 
+# ------------------------------------------------------------------ the paper's convoy
+def bench_convoy(dev):
+    """The paper's own benchmark shape: N = 20 objects, D = 5, sigma = 0.25, delta = 2,
+    H_up = 100, tau = 1e-5, H_max = 100, 548 updates, through tracker.ConvoyTracker (every stage a
+    libglmb kernel; the host copies Z_k in and reads one count per update).  Per-update time is
+    wall clock around the whole update (what the paper's 0.1 s real-time line refers to),
+    plus the device time between the first and last kernel; accuracy by P:213-215's metrics."""
+    from paper_2512_06230_b200.scenes import ConvoyConfig
+    from paper_2512_06230_b200.tracker import convoy_metrics, run_convoy
+    cfg = ConvoyConfig(N=20, H_max=100)
+    run_convoy(ConvoyConfig(N=2, H_max=10, K=20), K_cap=256, device=dev)     # warm-up (module load, allocator)
+    recs, ests, truth = run_convoy(cfg, K_cap=4096, device=dev)
+    card, dist = convoy_metrics(ests, truth)
+    wall = np.array([r.wall_ms for r in recs])
+    devms = np.array([r.device_ms for r in recs])
+    return {"workload": "convoy N=20, D=5, sigma=0.25 m, delta=2, lambda=0, H_up=100, tau=1e-5, H_max=100, "
+                        "548 updates (P:182-186; synthetic figure-eight ground track, R35)",
+            "update_ms_mean": float(wall.mean()), "update_ms_p95": float(np.percentile(wall, 95)),
+            "update_ms_max": float(wall.max()), "device_ms_mean": float(devms.mean()),
+            "realtime_budget_ms": 100.0, "card_err": card, "track_err_m": dist,
+            "pairs_max": max(r.n_pairs for r in recs),
+            "paper": "L40S: 'under the threshold of 0.1 seconds per update ... almost always' (P:211), "
+                     "card. error low at H_max=100, matched error < 0.15 m (P:213-215)"}
+
+
 # ------------------------------------------------------------------ GPU arm
 def main():
     a = parse()
@@ -527,6 +553,9 @@ def main():
     update = None
     if world == 1 and not a.no_update:
         update = bench_update(a, st, scene, cfg, dev, stream, L)
+    convoy = None
+    if world == 1 and not a.no_convoy:
+        convoy = bench_convoy(dev)
 
     cpu = None
     if world == 1 and not a.no_cpu_baseline:
@@ -540,6 +569,8 @@ def main():
         traffic=compat_traffic(st.T_local, st.P, len(scene.Z[0])), e2e=e2e, cpu=cpu)
     if update is not None:
         line["glmb_update"] = update
+    if convoy is not None:
+        line["convoy"] = convoy
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
