@@ -329,12 +329,12 @@ cudaError_t launch_k(const CompatArgs &a, cudaStream_t s) {
 // every measurement pair of that particle, so each measurement sees the same
 // MUFU/polynomial mix and C stays bit-exact under row permutations of Z;
 // positive: pair h of particle u when (u + 2h) % EMU == EMU - 1, spread; 0:
-// all MUFU).  Default -12 (measured best bit-exact setting on B200, see
+// all MUFU).  Default -10 (measured best bit-exact setting on B200, see
 // profiles/README.md).  GLMB_COMPAT_EMU overrides it (diagnostics / A-B runs).
 int emu_period() {
   static int v = [] {
     const char *e = std::getenv("GLMB_COMPAT_EMU");
-    return e ? std::atoi(e) : -12;
+    return e ? std::atoi(e) : -10;
   }();
   return v;
 }

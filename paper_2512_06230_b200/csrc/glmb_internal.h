@@ -111,6 +111,7 @@ struct SampleArgs {
   int64_t ldm;
   double *logw;
   unsigned long long *hash;
+  int32_t row_cap;  // set by the launcher: filtered row entries that fit in shared memory
 };
 
 struct DedupArgs {
@@ -163,7 +164,7 @@ struct PairsArgs {
   const int32_t *theta;
   int32_t *pair_track, *pair_ptr, *pair_meas, *pair_of, *n_pairs;
   // workspace (n_hyp*T entries each, and n_hyp*M for the lists)
-  int32_t *cnt, *off, *first, *list;
+  int32_t *cnt, *off, *first, *list, *row_k, *row_m;
   unsigned long long *fp;
 };
 size_t pairs_workspace_bytes(int32_t n_hyp, int32_t T, int32_t M);

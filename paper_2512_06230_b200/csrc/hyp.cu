@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(256) death_prob_kernel(DeathArgs a) {
 // ------------------------------------------------------------------ CSR of the gated entries
 // CTA = 32 consecutive rows (one gate word column w), 8 warps; warp k owns the
 // contiguous track chunk [k*ch, (k+1)*ch) so entries come out in ascending j.
-constexpr int kRowWarps = 8;
+constexpr int kRowWarps = 32;
 
 __device__ __forceinline__ void row_chunk(int32_t T, int k, int32_t &j0, int32_t &j1) {
   const int32_t ch = (T + kRowWarps - 1) / kRowWarps;
@@ -167,71 +167,162 @@ __device__ __forceinline__ Tv block_sum_128(Tv v, Tv *red) {
   return r;
 }
 
+// Block-wide exclusive scan of one int32 per thread (kSampThreads threads).
+__device__ __forceinline__ int32_t block_excl_scan_128(int32_t v, int32_t *red, int32_t &total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) red[wid] = x;
+  __syncthreads();
+  const int32_t w0 = red[0], w1 = red[1], w2 = red[2], w3 = red[3];
+  total = w0 + w1 + w2 + w3;
+  const int32_t before = wid == 0 ? 0 : wid == 1 ? w0 : wid == 2 ? w0 + w1 : w0 + w1 + w2;
+  __syncthreads();
+  return before + x - v;
+}
+
+// CTA = (parent h, group of kSampPerCta samples).  The parent's rows of C'_k --
+// the gated entries whose column is in the parent, in ascending column order --
+// are filtered once into shared memory (when they fit, else the CTA walks the
+// global CSR) and reused by the group's samples; stage 1 visits only the
+// parent's tracks.  Same draws and the same fp32 operation order as a walk of
+// the full rows (columns outside the parent are never alive), so the integer
+// outcomes do not depend on this.
+constexpr int kSampPerCta = 16;
+constexpr int kRowCapMax = 2048;  // filtered entries held in shared memory (32 KB: ~6 CTAs per SM)
+
 __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a) {
-  extern __shared__ uint32_t sm[];
-  uint32_t *alive = sm, *det = sm + a.ldt;
-  int32_t *cnt = reinterpret_cast<int32_t *>(sm + 2 * a.ldt);  // [T] when a count prior is given
+  extern __shared__ __align__(16) unsigned char smraw[];
+  double *flv = reinterpret_cast<double *>(smraw);                 // [row_cap]
+  float *fval = reinterpret_cast<float *>(flv + a.row_cap);        // [row_cap]
+  int32_t *fcol = reinterpret_cast<int32_t *>(fval + a.row_cap);   // [row_cap]
+  int32_t *frp = fcol + a.row_cap;                                 // [M + 1]
+  uint32_t *pmask = reinterpret_cast<uint32_t *>(frp + a.M + 1);   // [ldt]
+  uint32_t *alive = pmask + a.ldt, *det = alive + a.ldt;            // [ldt] each
+  int32_t *cnt = reinterpret_cast<int32_t *>(det + a.ldt);         // [T] when a count prior is given
   __shared__ double red_d[4];
   __shared__ unsigned long long red_u[4];
   __shared__ int32_t red_i[4];
-  const int64_t q = blockIdx.x;
-  const int32_t h = static_cast<int32_t>(q / a.H_up), s = static_cast<int32_t>(q - static_cast<int64_t>(h) * a.H_up);
+  __shared__ int32_t use_smem;
+  const int n_groups = (a.H_up + kSampPerCta - 1) / kSampPerCta;
+  const int32_t h = static_cast<int32_t>(blockIdx.x / n_groups);
+  const int32_t s0 = static_cast<int32_t>(blockIdx.x - static_cast<int64_t>(h) * n_groups) * kSampPerCta;
+  const int32_t s1 = min(a.H_up, s0 + kSampPerCta);
   if (a.n_parents != nullptr && h >= __ldg(a.n_parents)) return;  // inactive parent slot
   const uint32_t *pm = a.parent_mask + static_cast<int64_t>(h) * a.ldt;
-  for (int32_t k = threadIdx.x; k < a.ldt; k += kSampThreads) {
-    alive[k] = 0u;
-    det[k] = 0u;
-  }
-  if (a.n_count > 0)
-    for (int32_t j = threadIdx.x; j < a.T; j += kSampThreads) cnt[j] = 0;
+  for (int32_t k = threadIdx.x; k < a.ldt; k += kSampThreads) pmask[k] = __ldg(pm + k);
   __syncthreads();
 
-  // stage 1: track j of the parent survives iff u_j < 1 - d_j (fp32, R25);
-  // Philox block (j/4, h, step, 2<<24 | s), word j%4
-  double lw = 0.0;
-  const int32_t tquads = (a.T + 3) >> 2;
-  for (int32_t t = threadIdx.x; t < tquads; t += kSampThreads) {
-    const u32x4 r = philox4x32_10(
-        u32x4{static_cast<uint32_t>(t), static_cast<uint32_t>(h), a.step, (kDomainSurvive << 24) | static_cast<uint32_t>(s)},
-        a.key0, a.key1);
-    const uint32_t pmw = __ldg(pm + ((4 * t) >> 5));
-    uint32_t bits = 0u;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int32_t j = 4 * t + e;
-      if (j >= a.T || !((pmw >> (j & 31)) & 1u)) continue;
-      const float thr = __fsub_rn(1.0f, __ldg(a.d_prob + j));
-      const bool al = uniform24(e == 0 ? r.a : e == 1 ? r.b : e == 2 ? r.c : r.d) < thr;
-      const double ps = static_cast<double>(__ldg(a.p_s + j));
-      lw += al ? log(ps) : log(1.0 - ps);
-      bits |= static_cast<uint32_t>(al) << e;
+  // ---- the parent's rows (shared memory), filtered in ascending column order
+  {
+    int32_t carry = 0;
+    for (int32_t i0 = 0; i0 < a.M; i0 += kSampThreads) {
+      const int32_t i = i0 + threadIdx.x;
+      int32_t c = 0;
+      if (i < a.M) {
+        const int32_t e1 = __ldg(a.row_ptr + i + 1);
+        for (int32_t x = __ldg(a.row_ptr + i); x < e1; ++x) {
+          const int32_t j = __ldg(a.col + x);
+          c += (pmask[j >> 5] >> (j & 31)) & 1u;
+        }
+      }
+      int32_t tot;
+      const int32_t ex = block_excl_scan_128(c, red_i, tot);
+      if (i < a.M) frp[i] = carry + ex;
+      carry += tot;
     }
-    if (bits) atomicOr(alive + ((4 * t) >> 5), bits << ((4 * t) & 31));
+    if (threadIdx.x == 0) {
+      frp[a.M] = carry;
+      use_smem = carry <= a.row_cap;
+    }
+    __syncthreads();
+    if (use_smem) {
+      for (int32_t i = threadIdx.x; i < a.M; i += kSampThreads) {
+        int32_t o = frp[i];
+        const int32_t e1 = __ldg(a.row_ptr + i + 1);
+        for (int32_t x = __ldg(a.row_ptr + i); x < e1; ++x) {
+          const int32_t j = __ldg(a.col + x);
+          if ((pmask[j >> 5] >> (j & 31)) & 1u) {
+            fcol[o] = j;
+            fval[o] = __ldg(a.val + x);
+            flv[o] = __ldg(a.ln_val + x);
+            ++o;
+          }
+        }
+      }
+    }
+    __syncthreads();
   }
-  __syncthreads();
-
-  // stage 2: each row i draws theta_i from the row of C'_k (clutter kappa,
-  // surviving gated columns in ascending order), inverse CDF in fp32 (R26);
-  // Philox block (i/4, h, step, 3<<24 | s), word i%4
+  const bool sm_rows = use_smem;
+  const int32_t *rp = sm_rows ? frp : a.row_ptr;
+  const int32_t *cl = sm_rows ? fcol : a.col;
+  const float *vl = sm_rows ? fval : a.val;
+  const double *lvl = sm_rows ? flv : a.ln_val;
   const double ln_kappa = log(static_cast<double>(a.kappa));
-  int32_t *th = a.theta + q * a.ldm;
-  uint64_t fp = 0ull;
-  const int32_t mquads = (a.M + 3) >> 2;
-  for (int32_t t = threadIdx.x; t < mquads; t += kSampThreads) {
-    const u32x4 r = philox4x32_10(
-        u32x4{static_cast<uint32_t>(t), static_cast<uint32_t>(h), a.step, (kDomainAssoc << 24) | static_cast<uint32_t>(s)},
-        a.key0, a.key1);
-    int32_t pick4[4] = {0, 0, 0, 0};
+  const double ln_miss = log(1.0 - static_cast<double>(a.p_d));
+  for (int32_t s = s0; s < s1; ++s) {
+    const int64_t q = static_cast<int64_t>(h) * a.H_up + s;
+    // stage 1: track j of the parent survives iff u_j < 1 - d_j (fp32, R25);
+    // Philox block (j/4, h, step, 2<<24 | s), word j%4 -- only quads holding parent tracks
+    double lw = 0.0;
+    for (int32_t k = threadIdx.x; k < a.ldt; k += kSampThreads) {
+      const uint32_t pw = pmask[k];
+      uint32_t aw = 0u;
+      for (uint32_t rest = pw; rest != 0u;) {
+        const int nib = (__ffs(rest) - 1) >> 2;                  // next quad with a parent track
+        const uint32_t qbits = (pw >> (4 * nib)) & 0xFu;
+        rest &= ~(0xFu << (4 * nib));
+        const int32_t t = 8 * k + nib;
+        const u32x4 r = philox4x32_10(
+            u32x4{static_cast<uint32_t>(t), static_cast<uint32_t>(h), a.step,
+                  (kDomainSurvive << 24) | static_cast<uint32_t>(s)},
+            a.key0, a.key1);
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int32_t i = 4 * t + e;
+        for (int e = 0; e < 4; ++e) {
+          if (!((qbits >> e) & 1u)) continue;
+          const int32_t j = 4 * t + e;
+          const float thr = __fsub_rn(1.0f, __ldg(a.d_prob + j));
+          const bool al = uniform24(e == 0 ? r.a : e == 1 ? r.b : e == 2 ? r.c : r.d) < thr;
+          const double ps = static_cast<double>(__ldg(a.p_s + j));
+          lw += al ? log(ps) : log(1.0 - ps);
+          aw |= static_cast<uint32_t>(al) << (4 * nib + e);
+          if (a.n_count > 0) cnt[j] = 0;
+        }
+      }
+      alive[k] = aw;
+      det[k] = 0u;
+    }
+    __syncthreads();
+
+    // stage 2: each row i draws theta_i from the row of C'_k (clutter kappa,
+    // surviving gated columns in ascending order), inverse CDF in fp32 (R26);
+    // Philox block (i/4, h, step, 3<<24 | s), word i%4
+    int32_t *th = a.theta + q * a.ldm;
+    uint64_t fp = 0ull;
+    // one row per thread; the Philox block of rows 4t..4t+3 is computed by the lane
+    // holding row 4t and shuffled to the three lanes after it (rows are lane-contiguous)
+    const int lane = threadIdx.x & 31;
+    for (int32_t i0 = 0; i0 < a.M; i0 += kSampThreads) {
+      const int32_t i = i0 + threadIdx.x;
+      u32x4 r{0u, 0u, 0u, 0u};
+      if ((i & 3) == 0 && i < a.M)
+        r = philox4x32_10(u32x4{static_cast<uint32_t>(i >> 2), static_cast<uint32_t>(h), a.step,
+                                (kDomainAssoc << 24) | static_cast<uint32_t>(s)},
+                          a.key0, a.key1);
+      const int src = lane & ~3, e = i & 3;
+      const uint32_t w0 = __shfl_sync(0xffffffffu, r.a, src), w1 = __shfl_sync(0xffffffffu, r.b, src);
+      const uint32_t w2 = __shfl_sync(0xffffffffu, r.c, src), w3 = __shfl_sync(0xffffffffu, r.d, src);
       if (i >= a.M) continue;
-      const uint32_t rwe = e == 0 ? r.a : e == 1 ? r.b : e == 2 ? r.c : r.d;
-      const int32_t e0 = __ldg(a.row_ptr + i), e1 = __ldg(a.row_ptr + i + 1);
+      const uint32_t rwe = e == 0 ? w0 : e == 1 ? w1 : e == 2 ? w2 : w3;
+      const int32_t e0 = rp[i], e1 = rp[i + 1];
       float total = a.kappa;
       for (int32_t x = e0; x < e1; ++x) {
-        const int32_t j = __ldg(a.col + x);
-        if ((alive[j >> 5] >> (j & 31)) & 1u) total = __fadd_rn(total, __ldg(a.val + x));
+        const int32_t j = cl[x];
+        if ((alive[j >> 5] >> (j & 31)) & 1u) total = __fadd_rn(total, vl[x]);
       }
       const float tt = __fmul_rn(uniform24(rwe), total);
       float acc = a.kappa;
@@ -241,11 +332,11 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
         pick = 0;
       } else {
         for (int32_t x = e0; x < e1; ++x) {
-          const int32_t j = __ldg(a.col + x);
+          const int32_t j = cl[x];
           if (!((alive[j >> 5] >> (j & 31)) & 1u)) continue;
-          acc = __fadd_rn(acc, __ldg(a.val + x));
+          acc = __fadd_rn(acc, vl[x]);
           last = j + 1;
-          llast = __ldg(a.ln_val + x);
+          llast = lvl[x];
           if (tt < acc) {
             pick = j + 1;
             lpick = llast;
@@ -257,44 +348,40 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
           lpick = llast;
         }
       }
-      pick4[e] = pick;
       lw += lpick;
       if (pick > 0) {
         atomicOr(det + ((pick - 1) >> 5), 1u << ((pick - 1) & 31));
         if (a.n_count > 0) atomicAdd(cnt + pick - 1, 1);
       }
       fp += fp_term(static_cast<uint32_t>(pick), static_cast<uint64_t>(a.ldt) + i);
+      th[i] = pick;
     }
-    const int32_t i0 = 4 * t;
-    if (i0 + 3 < a.M) {
-      *reinterpret_cast<int4 *>(th + i0) = make_int4(pick4[0], pick4[1], pick4[2], pick4[3]);
-    } else {
-      for (int e = 0; e < 4 && i0 + e < a.M; ++e) th[i0 + e] = pick4[e];
-    }
-  }
-  __syncthreads();
+    __syncthreads();
 
-  // missed detections: alive tracks with no measurement (or, with a count prior,
-  // lc(n_j) for every alive track); fingerprint of the alive words
-  int32_t missed = 0;
-  uint32_t *al_out = a.alive + q * a.ldt;
-  for (int32_t k = threadIdx.x; k < a.ldt; k += kSampThreads) {
-    const uint32_t av = alive[k];
-    missed += __popc(av & ~det[k]);
-    al_out[k] = av;
-    fp += fp_term(av, static_cast<uint64_t>(k));
-  }
-  if (a.n_count > 0) {
-    missed = 0;
-    for (int32_t j = threadIdx.x; j < a.T; j += kSampThreads)
-      if ((alive[j >> 5] >> (j & 31)) & 1u) lw += __ldg(a.count_lp + min(cnt[j], a.n_count - 1));
-  }
-  lw = block_sum_128(lw, red_d);
-  const unsigned long long fps = block_sum_128(static_cast<unsigned long long>(fp), red_u);
-  missed = block_sum_128(missed, red_i);
-  if (threadIdx.x == 0) {
-    a.logw[q] = __ldg(a.parent_logw + h) + lw + static_cast<double>(missed) * log(1.0 - static_cast<double>(a.p_d));
-    if (a.hash) a.hash[q] = fps;
+    // missed detections (alive tracks with no measurement) or, with a count prior,
+    // lc(n_j) for every alive track; fingerprint of the alive words
+    int32_t missed = 0;
+    uint32_t *al_out = a.alive + q * a.ldt;
+    for (int32_t k = threadIdx.x; k < a.ldt; k += kSampThreads) {
+      const uint32_t av = alive[k];
+      al_out[k] = av;
+      fp += fp_term(av, static_cast<uint64_t>(k));
+      if (a.n_count > 0) {
+        for (uint32_t rest = av; rest != 0u; rest &= rest - 1u) {
+          const int32_t j = 32 * k + __ffs(rest) - 1;
+          lw += __ldg(a.count_lp + min(cnt[j], a.n_count - 1));
+        }
+      } else {
+        missed += __popc(av & ~det[k]);
+      }
+    }
+    lw = block_sum_128(lw, red_d);
+    const unsigned long long fps = block_sum_128(static_cast<unsigned long long>(fp), red_u);
+    missed = block_sum_128(missed, red_i);
+    if (threadIdx.x == 0) {
+      a.logw[q] = __ldg(a.parent_logw + h) + lw + static_cast<double>(missed) * ln_miss;
+      if (a.hash) a.hash[q] = fps;
+    }
   }
 }
 
@@ -580,15 +667,20 @@ cudaError_t launch_compat_rows(const RowsArgs &a, cudaStream_t s) {
 }
 
 cudaError_t launch_assoc_sample(const SampleArgs &a, cudaStream_t s) {
-  const int64_t n = static_cast<int64_t>(a.H_old) * a.H_up;
-  const size_t smem = sizeof(uint32_t) * 2 * static_cast<size_t>(a.ldt) +
-                      (a.n_count > 0 ? sizeof(int32_t) * static_cast<size_t>(a.T) : 0);
-  if (smem > 40 * 1024) {  // dynamic + static shared memory past the 48 KB default
-    cudaError_t e = cudaFuncSetAttribute(assoc_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-  }
-  assoc_sample_kernel<<<static_cast<unsigned>(n), kSampThreads, smem, s>>>(a);
+  const int64_t groups = (a.H_up + kSampPerCta - 1) / kSampPerCta;
+  const int64_t n = static_cast<int64_t>(a.H_old) * groups;
+  SampleArgs b = a;
+  const size_t fixed = sizeof(int32_t) * (static_cast<size_t>(a.M) + 1) + sizeof(uint32_t) * 3 * static_cast<size_t>(a.ldt) +
+                       (a.n_count > 0 ? sizeof(int32_t) * static_cast<size_t>(a.T) : 0) + 16;
+  const size_t budget = 200 * 1024;
+  if (fixed > budget) return cudaErrorInvalidValue;
+  const size_t per = sizeof(double) + sizeof(float) + sizeof(int32_t);
+  b.row_cap = static_cast<int32_t>(min(static_cast<size_t>(kRowCapMax), (budget - fixed) / per));
+  const size_t smem = static_cast<size_t>(b.row_cap) * per + fixed;
+  cudaError_t e = cudaFuncSetAttribute(assoc_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  assoc_sample_kernel<<<static_cast<unsigned>(n), kSampThreads, smem, s>>>(b);
   return cudaGetLastError();
 }
 

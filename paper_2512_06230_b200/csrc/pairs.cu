@@ -156,28 +156,58 @@ __global__ void __launch_bounds__(256) first_kernel(PairsArgs a) {
   a.first[e] = first;
 }
 
-// numbering in (r, j) order: pair index and list offset of each first occurrence (one CTA)
-__global__ void __launch_bounds__(1024) number_kernel(PairsArgs a) {
-  __shared__ int32_t wsum[32];
-  const int32_t nh = a.n_hyp_dev != nullptr ? min(a.n_hyp, *a.n_hyp_dev) : a.n_hyp;
-  const int64_t n = static_cast<int64_t>(nh) * a.T;
-  int32_t kc = 0, mc = 0;
-  for (int64_t e0 = 0; e0 < n; e0 += 1024) {
-    const int64_t e = e0 + threadIdx.x;
-    int32_t isnew = 0, c = 0;
-    if (e < n) {
-      const int32_t r = static_cast<int32_t>(e / a.T);
-      isnew = a.first[e] == r;
-      c = isnew ? a.cnt[e] : 0;
+// numbering in (r, j) order: pair index and list offset of each first occurrence.
+// (1) per hypothesis row: how many new pairs and list entries; (2) one small CTA
+// scans the rows; (3) per row: a block scan places the row's new pairs.
+__device__ __forceinline__ int32_t n_hyp_used(const PairsArgs &a) {
+  return a.n_hyp_dev != nullptr ? min(a.n_hyp, __ldg(a.n_hyp_dev)) : a.n_hyp;
+}
+
+__global__ void __launch_bounds__(256) row_count_kernel(PairsArgs a) {
+  __shared__ int32_t rk[8], rm[8];
+  const int32_t r = blockIdx.x;
+  int32_t k = 0, m = 0;
+  if (r < n_hyp_used(a)) {
+    const int64_t rb = static_cast<int64_t>(r) * a.T;
+    for (int32_t j = threadIdx.x; j < a.T; j += blockDim.x) {
+      const bool isnew = a.first[rb + j] == r;
+      k += isnew;
+      m += isnew ? a.cnt[rb + j] : 0;
     }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    k += __shfl_xor_sync(0xffffffffu, k, o);
+    m += __shfl_xor_sync(0xffffffffu, m, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    rk[threadIdx.x >> 5] = k;
+    rm[threadIdx.x >> 5] = m;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t tk = 0, tm = 0;
+    for (int q = 0; q < 8; ++q) {
+      tk += rk[q];
+      tm += rm[q];
+    }
+    a.row_k[r] = tk;
+    a.row_m[r] = tm;
+  }
+}
+
+__global__ void __launch_bounds__(1024) row_scan_kernel(PairsArgs a) {
+  __shared__ int32_t wsum[32];
+  int32_t kc = 0, mc = 0;
+  for (int32_t r0 = 0; r0 < a.n_hyp; r0 += 1024) {
+    const int32_t r = r0 + threadIdx.x;
+    const int32_t k = r < a.n_hyp ? a.row_k[r] : 0, m = r < a.n_hyp ? a.row_m[r] : 0;
     int32_t ktot, mtot;
-    const int32_t k = kc + block_excl_scan(isnew, wsum, ktot);
-    const int32_t m = mc + block_excl_scan(c, wsum, mtot);
-    if (isnew) {
-      const int32_t j = static_cast<int32_t>(e % a.T);
-      a.pair_track[k] = j;
-      a.pair_ptr[k] = m;
-      a.pair_of[e] = k;
+    const int32_t ko = kc + block_excl_scan(k, wsum, ktot);
+    const int32_t mo = mc + block_excl_scan(m, wsum, mtot);
+    if (r < a.n_hyp) {
+      a.row_k[r] = ko;  // in place: becomes the row's first pair index / list offset
+      a.row_m[r] = mo;
     }
     kc += ktot;
     mc += mtot;
@@ -185,6 +215,32 @@ __global__ void __launch_bounds__(1024) number_kernel(PairsArgs a) {
   if (threadIdx.x == 0) {
     a.pair_ptr[kc] = mc;
     *a.n_pairs = kc;
+  }
+}
+
+__global__ void __launch_bounds__(256) number_kernel(PairsArgs a) {
+  __shared__ int32_t wsum[32];
+  const int32_t r = blockIdx.x;
+  if (r >= n_hyp_used(a)) return;
+  const int64_t rb = static_cast<int64_t>(r) * a.T;
+  int32_t kc = a.row_k[r], mc = a.row_m[r];
+  for (int32_t j0 = 0; j0 < a.T; j0 += blockDim.x) {
+    const int32_t j = j0 + threadIdx.x;
+    int32_t isnew = 0, c = 0;
+    if (j < a.T) {
+      isnew = a.first[rb + j] == r;
+      c = isnew ? a.cnt[rb + j] : 0;
+    }
+    int32_t ktot, mtot;
+    const int32_t k = kc + block_excl_scan(isnew, wsum, ktot);
+    const int32_t m = mc + block_excl_scan(c, wsum, mtot);
+    if (isnew) {
+      a.pair_track[k] = j;
+      a.pair_ptr[k] = m;
+      a.pair_of[rb + j] = k;
+    }
+    kc += ktot;
+    mc += mtot;
   }
 }
 
@@ -401,7 +457,7 @@ __global__ void __launch_bounds__(256) map_estimate_kernel(MapEstimateArgs a) {
 size_t pairs_workspace_bytes(int32_t n_hyp, int32_t T, int32_t M) {
   const size_t nt = static_cast<size_t>(n_hyp) * T;
   return nt * (3 * sizeof(int32_t) + sizeof(unsigned long long)) + static_cast<size_t>(n_hyp) * M * sizeof(int32_t) +
-         64;
+         2 * static_cast<size_t>(n_hyp) * sizeof(int32_t) + 64;
 }
 
 cudaError_t launch_assoc_pairs(const PairsArgs &in, void *ws, cudaStream_t s) {
@@ -414,6 +470,8 @@ cudaError_t launch_assoc_pairs(const PairsArgs &in, void *ws, cudaStream_t s) {
   a.off = a.cnt + nt;
   a.first = a.off + nt;
   a.list = a.first + nt;
+  a.row_k = a.list + static_cast<size_t>(a.n_hyp) * a.M;
+  a.row_m = a.row_k + a.n_hyp;
   if (a.n_hyp == 0 || a.T == 0) {
     cudaError_t e = cudaMemsetAsync(a.n_pairs, 0, sizeof(int32_t), s);
     if (e != cudaSuccess) return e;
@@ -428,7 +486,9 @@ cudaError_t launch_assoc_pairs(const PairsArgs &in, void *ws, cudaStream_t s) {
   invert_kernel<<<a.n_hyp, kInvThreads, smem, s>>>(a);
   const dim3 g2((a.T + 255) / 256, a.n_hyp);
   first_kernel<<<g2, 256, 0, s>>>(a);
-  number_kernel<<<1, 1024, 0, s>>>(a);
+  row_count_kernel<<<a.n_hyp, 256, 0, s>>>(a);
+  row_scan_kernel<<<1, 1024, 0, s>>>(a);
+  number_kernel<<<a.n_hyp, 256, 0, s>>>(a);
   finish_kernel<<<g2, 256, 0, s>>>(a);
   return cudaGetLastError();
 }
