@@ -49,15 +49,13 @@
 namespace glmb {
 namespace {
 
-constexpr int kWarps = 4;
-constexpr int kThreads = 32 * kWarps;
-constexpr int kTileM = 32 * kWarps;  // measurements per tile per K
+constexpr int kVWarps = 4;  // the centre sum is defined over 4 (virtual) warps of 32 threads
 constexpr int kTileP = 256;          // particles per shared-memory tile (fixed: sets the sum order)
 constexpr int kStages = 1;           // raw tiles (x, y, w) in flight: one tile of compute (~50 us) hides a TMA
 constexpr int kMaxK = 8;
 // resident CTAs per SM the register allocation must allow (4 warps each)
-template <int K>
-constexpr int min_blocks() { return K <= 2 ? 12 : 8; }
+template <int NW, int K>
+constexpr int min_blocks() { return NW == 4 ? (K <= 2 ? 12 : 8) : (NW == 2 ? 20 : 28); }
 constexpr int kRawFloats = 3 * kTileP;
 constexpr int kSmemBytes = kStages * kRawFloats * 4 + 2 * kTileP * 16;  // raw ring + 2 AoS tiles
 
@@ -213,13 +211,15 @@ __device__ __forceinline__ void tile_dispatch(int hv, const float4 *A, int np, M
 
 // Unit u = mt * T + j (all full measurement tiles first, the ragged last tiles
 // at the end of the grid, so the short units fill the tail of the schedule).
-template <int K, int EMU_PERIOD>
-__global__ void __launch_bounds__(kThreads, min_blocks<K>()) compat_kernel(const CompatArgs a) {
+template <int NW, int K, int EMU_PERIOD>
+__global__ void __launch_bounds__(32 * NW, min_blocks<NW, K>()) compat_kernel(const CompatArgs a) {
   constexpr int H = Meas<K>::H;
+  constexpr int kThreads = 32 * NW;
+  constexpr int kTileM = 32 * NW;  // measurements per tile per K
   extern __shared__ __align__(128) float smem[];
   float4 *aos = reinterpret_cast<float4 *>(smem + kStages * kRawFloats);  // 2 AoS tiles
   __shared__ __align__(8) uint64_t bars[kStages];
-  __shared__ float red[2][kWarps];
+  __shared__ float red[2][kVWarps];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int mt = blockIdx.x / a.T;
@@ -256,16 +256,22 @@ __global__ void __launch_bounds__(kThreads, min_blocks<K>()) compat_kernel(const
     const int np = min(kTileP, a.P - t * kTileP);
     mbar_wait_parity(&bars[s], static_cast<uint32_t>(t / kStages) & 1u);
     if (t == 0) {  // centre c = mean position of the first tile (fixed order -> deterministic)
-      float sx = 0.f, sy = 0.f;
-      for (int idx = tid; idx < np; idx += kThreads) {
-        sx += X[idx];
-        sy += Y[idx];
-      }
-      sx = warp_sum(sx);
-      sy = warp_sum(sy);
-      if (lane == 0) {
-        red[0][warp] = sx;
-        red[1][warp] = sy;
+      // summed as 128 virtual threads in 4 virtual warps whatever NW is, so the centre
+      // (and hence C) is the same for every launch shape
+#pragma unroll
+      for (int v = 0; v < kVWarps / NW; ++v) {
+        const int vt = tid + v * kThreads;
+        float sx = 0.f, sy = 0.f;
+        for (int idx = vt; idx < np; idx += 32 * kVWarps) {
+          sx += X[idx];
+          sy += Y[idx];
+        }
+        sx = warp_sum(sx);
+        sy = warp_sum(sy);
+        if (lane == 0) {
+          red[0][vt >> 5] = sx;
+          red[1][vt >> 5] = sy;
+        }
       }
       __syncthreads();
       cx = ((red[0][0] + red[0][1]) + (red[0][2] + red[0][3])) / static_cast<float>(np);
@@ -318,10 +324,10 @@ __global__ void clutter_fill_kernel(float *c, int32_t M, float kappa) {
   if (i < M) c[i] = kappa;
 }
 
-template <int K, int EMU_PERIOD>
+template <int NW, int K, int EMU_PERIOD>
 cudaError_t launch_k(const CompatArgs &a, cudaStream_t s) {
   const int64_t grid = static_cast<int64_t>(a.T) * a.n_mtiles;
-  compat_kernel<K, EMU_PERIOD><<<static_cast<unsigned>(grid), kThreads, kSmemBytes, s>>>(a);
+  compat_kernel<NW, K, EMU_PERIOD><<<static_cast<unsigned>(grid), 32 * NW, kSmemBytes, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -339,55 +345,61 @@ int emu_period() {
   return v;
 }
 
-template <int K>
+template <int NW, int K>
 cudaError_t launch_e(const CompatArgs &a, cudaStream_t s) {
   switch (emu_period()) {
-    case 0: return launch_k<K, 0>(a, s);
-    case 4: return launch_k<K, 4>(a, s);
-    case 6: return launch_k<K, 6>(a, s);
-    case 8: return launch_k<K, 8>(a, s);
-    case 10: return launch_k<K, 10>(a, s);
-    case 12: return launch_k<K, 12>(a, s);
-    case 16: return launch_k<K, 16>(a, s);
-    case -6: return launch_k<K, -6>(a, s);
-    case -8: return launch_k<K, -8>(a, s);
-    case -12: return launch_k<K, -12>(a, s);
-    case -4: return launch_k<K, -4>(a, s);
-    case -10: return launch_k<K, -10>(a, s);
-    case -16: return launch_k<K, -16>(a, s);
-    case 1: return launch_k<K, 1>(a, s);
-    case -5: return launch_k<K, -5>(a, s);
-    default: return launch_k<K, 0>(a, s);
+    case 0: return launch_k<NW, K, 0>(a, s);
+    case -6: return launch_k<NW, K, -6>(a, s);
+    case -8: return launch_k<NW, K, -8>(a, s);
+    case -12: return launch_k<NW, K, -12>(a, s);
+    case -16: return launch_k<NW, K, -16>(a, s);
+    case 10: return launch_k<NW, K, 10>(a, s);
+    default: return launch_k<NW, K, -10>(a, s);
   }
 }
 
 }  // namespace
 
-void compat_plan(int32_t M, int32_t P, int32_t *K, int32_t *n_mtiles) {
+void compat_plan(int32_t M, int32_t P, int32_t *K, int32_t *NW, int32_t *n_mtiles) {
   // Depends on (M, P) only -- never on T -- so any sharding of the tracks runs
-  // the same per-column code (bit-identical C).  K measurements per thread
-  // (tile of 128 K): kDefaultK for large M (GLMB_COMPAT_K overrides: A/B runs);
-  // small M uses the smallest K covering M.
+  // the same per-column code (bit-identical C).  A warp holds 32 K measurements;
+  // K = 2 (one packed pair per thread) wherever M allows, NW warps per CTA:
+  //   M > 128: NW = 4, K = kDefaultK (GLMB_COMPAT_K overrides: A/B runs)
+  //   64 < M <= 128: NW = 2, K = 2;  32 < M <= 64: NW = 1, K = 2;  M <= 32: NW = 1, K = 1
   (void)P;
   static const int32_t kmax = [] {
     const char *e = std::getenv("GLMB_COMPAT_K");
     const int v = e ? std::atoi(e) : 2;
     return (v == 1 || v == 2 || v == 4 || v == 8) ? v : 2;
   }();
-  int32_t k = kmax;
-  const int32_t warps_needed = (M + 31) / 32;
-  while (k > 1 && warps_needed <= kWarps * (k / 2)) k /= 2;
+  int32_t k = kmax, nw = 4;
+  if (M <= 32) {
+    k = 1;
+    nw = 1;
+  } else if (M <= 64) {
+    k = 2;
+    nw = 1;
+  } else if (M <= 128) {
+    k = 2;
+    nw = 2;
+  } else {
+    const int32_t warps_needed = (M + 31) / 32;
+    while (k > 2 && warps_needed <= 4 * (k / 2)) k /= 2;
+  }
   *K = k;
-  *n_mtiles = (M + kTileM * k - 1) / (kTileM * k);
+  *NW = nw;
+  *n_mtiles = (M + 32 * nw * k - 1) / (32 * nw * k);
 }
 
 cudaError_t launch_compat(const CompatArgs &a_in, cudaStream_t s) {
   const CompatArgs &a = a_in;
+  if (a.NW == 1) return a.K == 1 ? launch_e<1, 1>(a, s) : launch_e<1, 2>(a, s);
+  if (a.NW == 2) return launch_e<2, 2>(a, s);
   switch (a.K) {
-    case 1: return launch_e<1>(a, s);
-    case 2: return launch_e<2>(a, s);
-    case 4: return launch_e<4>(a, s);
-    case 8: return launch_e<8>(a, s);
+    case 1: return launch_e<4, 1>(a, s);
+    case 2: return launch_e<4, 2>(a, s);
+    case 4: return launch_e<4, 4>(a, s);
+    case 8: return launch_e<4, 8>(a, s);
     default: return cudaErrorInvalidValue;
   }
 }

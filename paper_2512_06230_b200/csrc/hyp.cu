@@ -548,15 +548,40 @@ __global__ void __launch_bounds__(kPruneThreads) prune_kernel(PruneArgs a) {
         if ((key & hmask) == pre) atomicAdd(&hist[(key >> shift) & 255u], 1u);
       }
       __syncthreads();
-      if (threadIdx.x == 0) {
-        int32_t need = need_s;
-        int b = 255;
-        for (; b > 0; --b) {
-          if (static_cast<int32_t>(hist[b]) >= need) break;
-          need -= static_cast<int32_t>(hist[b]);
+      if (threadIdx.x < 32) {  // warp 0: the largest bin b whose count reaches the remaining need
+        const int l = threadIdx.x;
+        const int32_t need = need_s;
+        int32_t hb[8], sl = 0;  // lane l holds bins 255 - 8l - k, k = 0..7 (descending)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          hb[k] = static_cast<int32_t>(hist[255 - 8 * l - k]);
+          sl += hb[k];
         }
-        need_s = need;
-        prefix_s = pre | (static_cast<unsigned long long>(b) << shift);
+        int32_t incl = sl;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (l >= o) incl += y;
+        }
+        const uint32_t hit = __ballot_sync(0xffffffffu, incl >= need);
+        const int L = hit ? __ffs(hit) - 1 : 31;
+        if (l == L) {
+          int32_t above = incl - sl;  // bins above this lane's first bin
+          int b = 255 - 8 * l - 7;
+          int32_t rem = need - above;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            if (hb[k] >= need - above) {
+              b = 255 - 8 * l - k;
+              rem = need - above;
+              break;
+            }
+            above += hb[k];
+            rem = need - above;
+          }
+          need_s = rem;
+          prefix_s = pre | (static_cast<unsigned long long>(b) << shift);
+        }
       }
       __syncthreads();
     }
