@@ -331,12 +331,13 @@ glmb_status glmb_assoc_sample(int32_t H_old, const int32_t *n_parents, int32_t H
     return GLMB_ERR_INVALID_ARG;
   if (M > 0 && ((ldm & 3) || (reinterpret_cast<uintptr_t>(theta) & 15u))) return GLMB_ERR_ALIGNMENT;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  GLMB_TRY(bind_stream(s, nullptr));
+  int dev = 0;
+  GLMB_TRY(bind_stream(s, &dev));
   glmb::SampleArgs a{H_old, H_up, T, M, n_parents, parent_mask, ldt, parent_logw, d_prob, p_s, p_d, kappa, row_ptr, col, val,
                      ln_val, count_lp, n_count, static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32), step,
                      alive, theta, ldm,
                      logw, reinterpret_cast<unsigned long long *>(hash)};
-  return from_cuda(glmb::launch_assoc_sample(a, s));
+  return from_cuda(glmb::launch_assoc_sample(a, g_sm_count[dev], s));
 }
 
 glmb_status glmb_dedup(int32_t H_old, const int32_t *n_parents, int32_t H_up, int32_t M, const uint32_t *alive,

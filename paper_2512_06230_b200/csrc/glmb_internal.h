@@ -113,6 +113,7 @@ struct SampleArgs {
   double *logw;
   unsigned long long *hash;
   int32_t row_cap;  // set by the launcher: filtered row entries that fit in shared memory
+  int32_t spc;      // set by the launcher: samples per CTA
 };
 
 struct DedupArgs {
@@ -150,7 +151,7 @@ cudaError_t launch_clutter_fill(float *C_clutter, int32_t M, float kappa, cudaSt
 cudaError_t launch_reweight(const ReweightArgs &a, cudaStream_t s);
 cudaError_t launch_death_prob(const DeathArgs &a, cudaStream_t s);
 cudaError_t launch_compat_rows(const RowsArgs &a, cudaStream_t s);
-cudaError_t launch_assoc_sample(const SampleArgs &a, cudaStream_t s);
+cudaError_t launch_assoc_sample(const SampleArgs &a, int sm_count, cudaStream_t s);
 cudaError_t launch_dedup(const DedupArgs &a, cudaStream_t s);
 int32_t prune_capacity(int32_t h_max);
 cudaError_t launch_prune(const PruneArgs &a, cudaStream_t s);

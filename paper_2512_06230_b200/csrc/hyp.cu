@@ -11,6 +11,8 @@
 // Integer outcomes (alive bits, theta) are decided in fp32 exactly as the
 // readings R25/R26 state, so they are bit-identical to any implementation that
 // follows them; log-weights accumulate in fp64.
+#include <cstdlib>
+
 #include "glmb_device.cuh"
 #include "glmb_internal.h"
 
@@ -192,8 +194,8 @@ __device__ __forceinline__ int32_t block_excl_scan_128(int32_t v, int32_t *red, 
 // parent's tracks.  Same draws and the same fp32 operation order as a walk of
 // the full rows (columns outside the parent are never alive), so the integer
 // outcomes do not depend on this.
-constexpr int kSampPerCta = 16;
-constexpr int kRowCapMax = 2048;  // filtered entries held in shared memory (32 KB: ~6 CTAs per SM)
+constexpr int kSampPerCtaMax = 16;
+constexpr int kRowCapMax = 1024;  // filtered entries held in shared memory (16 KB: ~10 CTAs per SM)
 
 __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -208,10 +210,10 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
   __shared__ unsigned long long red_u[4];
   __shared__ int32_t red_i[4];
   __shared__ int32_t use_smem;
-  const int n_groups = (a.H_up + kSampPerCta - 1) / kSampPerCta;
+  const int n_groups = (a.H_up + a.spc - 1) / a.spc;
   const int32_t h = static_cast<int32_t>(blockIdx.x / n_groups);
-  const int32_t s0 = static_cast<int32_t>(blockIdx.x - static_cast<int64_t>(h) * n_groups) * kSampPerCta;
-  const int32_t s1 = min(a.H_up, s0 + kSampPerCta);
+  const int32_t s0 = static_cast<int32_t>(blockIdx.x - static_cast<int64_t>(h) * n_groups) * a.spc;
+  const int32_t s1 = min(a.H_up, s0 + a.spc);
   if (a.n_parents != nullptr && h >= __ldg(a.n_parents)) return;  // inactive parent slot
   const uint32_t *pm = a.parent_mask + static_cast<int64_t>(h) * a.ldt;
   for (int32_t k = threadIdx.x; k < a.ldt; k += kSampThreads) pmask[k] = __ldg(pm + k);
@@ -270,31 +272,30 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
     // Philox block (j/4, h, step, 2<<24 | s), word j%4 -- only quads holding parent tracks
     double lw = 0.0;
     for (int32_t k = threadIdx.x; k < a.ldt; k += kSampThreads) {
-      const uint32_t pw = pmask[k];
-      uint32_t aw = 0u;
-      for (uint32_t rest = pw; rest != 0u;) {
-        const int nib = (__ffs(rest) - 1) >> 2;                  // next quad with a parent track
-        const uint32_t qbits = (pw >> (4 * nib)) & 0xFu;
-        rest &= ~(0xFu << (4 * nib));
-        const int32_t t = 8 * k + nib;
-        const u32x4 r = philox4x32_10(
-            u32x4{static_cast<uint32_t>(t), static_cast<uint32_t>(h), a.step,
-                  (kDomainSurvive << 24) | static_cast<uint32_t>(s)},
-            a.key0, a.key1);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          if (!((qbits >> e) & 1u)) continue;
-          const int32_t j = 4 * t + e;
-          const float thr = __fsub_rn(1.0f, __ldg(a.d_prob + j));
-          const bool al = uniform24(e == 0 ? r.a : e == 1 ? r.b : e == 2 ? r.c : r.d) < thr;
-          const double ps = static_cast<double>(__ldg(a.p_s + j));
-          lw += al ? log(ps) : log(1.0 - ps);
-          aw |= static_cast<uint32_t>(al) << (4 * nib + e);
-          if (a.n_count > 0) cnt[j] = 0;
-        }
-      }
-      alive[k] = aw;
+      alive[k] = 0u;
       det[k] = 0u;
+    }
+    __syncthreads();
+    const int32_t tquads = (a.T + 3) >> 2;
+    for (int32_t t = threadIdx.x; t < tquads; t += kSampThreads) {
+      const uint32_t qbits = (pmask[t >> 3] >> (4 * (t & 7))) & 0xFu;
+      if (qbits == 0u) continue;
+      const u32x4 r = philox4x32_10(
+          u32x4{static_cast<uint32_t>(t), static_cast<uint32_t>(h), a.step, (kDomainSurvive << 24) | static_cast<uint32_t>(s)},
+          a.key0, a.key1);
+      uint32_t bits = 0u;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (!((qbits >> e) & 1u)) continue;
+        const int32_t j = 4 * t + e;
+        const float thr = __fsub_rn(1.0f, __ldg(a.d_prob + j));
+        const bool al = uniform24(e == 0 ? r.a : e == 1 ? r.b : e == 2 ? r.c : r.d) < thr;
+        const double ps = static_cast<double>(__ldg(a.p_s + j));
+        lw += al ? log(ps) : log(1.0 - ps);
+        bits |= static_cast<uint32_t>(al) << e;
+        if (a.n_count > 0) cnt[j] = 0;
+      }
+      if (bits) atomicOr(alive + (t >> 3), bits << (4 * (t & 7)));
     }
     __syncthreads();
 
@@ -375,12 +376,25 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
         missed += __popc(av & ~det[k]);
       }
     }
-    lw = block_sum_128(lw, red_d);
-    const unsigned long long fps = block_sum_128(static_cast<unsigned long long>(fp), red_u);
-    missed = block_sum_128(missed, red_i);
+    // one reduction round for (lw, fingerprint, missed): shuffles, one barrier, thread 0
+    unsigned long long fpu = static_cast<unsigned long long>(fp);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lw += __shfl_xor_sync(0xffffffffu, lw, o);
+      fpu += __shfl_xor_sync(0xffffffffu, fpu, o);
+      missed += __shfl_xor_sync(0xffffffffu, missed, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      red_d[threadIdx.x >> 5] = lw;
+      red_u[threadIdx.x >> 5] = fpu;
+      red_i[threadIdx.x >> 5] = missed;
+    }
+    __syncthreads();
     if (threadIdx.x == 0) {
-      a.logw[q] = __ldg(a.parent_logw + h) + lw + static_cast<double>(missed) * ln_miss;
-      if (a.hash) a.hash[q] = fps;
+      const double lws = (red_d[0] + red_d[1]) + (red_d[2] + red_d[3]);
+      const int32_t ms = (red_i[0] + red_i[1]) + (red_i[2] + red_i[3]);
+      a.logw[q] = __ldg(a.parent_logw + h) + lws + static_cast<double>(ms) * ln_miss;
+      if (a.hash) a.hash[q] = (red_u[0] + red_u[1]) + (red_u[2] + red_u[3]);
     }
   }
 }
@@ -691,10 +705,19 @@ cudaError_t launch_compat_rows(const RowsArgs &a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_assoc_sample(const SampleArgs &a, cudaStream_t s) {
-  const int64_t groups = (a.H_up + kSampPerCta - 1) / kSampPerCta;
-  const int64_t n = static_cast<int64_t>(a.H_old) * groups;
+cudaError_t launch_assoc_sample(const SampleArgs &a, int sm_count, cudaStream_t s) {
   SampleArgs b = a;
+  // samples per CTA: enough CTAs to fill the GPU ~8 deep, at most kSampPerCtaMax (the
+  // parent's rows are filtered once per CTA)
+  static const int spc_env = [] {
+    const char *e = std::getenv("GLMB_SAMPLES_PER_CTA");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int64_t total = static_cast<int64_t>(a.H_old) * a.H_up;
+  int64_t spc = spc_env > 0 ? spc_env : total / (static_cast<int64_t>(sm_count > 0 ? sm_count : 148) * 8);
+  b.spc = static_cast<int32_t>(spc < 1 ? 1 : spc > kSampPerCtaMax ? kSampPerCtaMax : spc);
+  const int64_t groups = (a.H_up + b.spc - 1) / b.spc;
+  const int64_t n = static_cast<int64_t>(a.H_old) * groups;
   const size_t fixed = sizeof(int32_t) * (static_cast<size_t>(a.M) + 1) + sizeof(uint32_t) * 3 * static_cast<size_t>(a.ldt) +
                        (a.n_count > 0 ? sizeof(int32_t) * static_cast<size_t>(a.T) : 0) + 16;
   const size_t budget = 200 * 1024;
