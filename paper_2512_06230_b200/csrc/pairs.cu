@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(256) finish_kernel(PairsArgs a) {
 // t_n = floor((n S + V) / P), V = floor(U S 2^-24), U = 2 (r >> 9) + 1 from
 // Philox(counter (k, 0, step, 4 << 24)) word 0.  Ancestors are non-decreasing in n,
 // so the gathers of consecutive slots hit neighbouring addresses.
-constexpr int kResThreads = 256;
+constexpr int kResThreads = 1024;
 
 __global__ void __launch_bounds__(kResThreads) resample_kernel(ResampleArgs a) {
   extern __shared__ __align__(16) unsigned char rs[];
@@ -355,15 +355,27 @@ __global__ void __launch_bounds__(kResThreads) resample_kernel(ResampleArgs a) {
   const float inv_p = 1.0f / static_cast<float>(a.P);
   for (int g = threadIdx.x; g < quads; g += kResThreads) {
     float4 X, Y, Vv, Ps, Om;
+    int lo = 0;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int n = 4 * g + e;
       const unsigned long long t = (static_cast<unsigned long long>(n) * S + V) / static_cast<unsigned>(a.P);
-      int lo = 0, hi = a.P - 1;  // first m with cum[m] > t (exists: cum[P-1] = S > t)
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (cum[mid] > t) hi = mid;
-        else lo = mid + 1;
+      // first m with cum[m] > t (exists: cum[P-1] = S > t).  Slots are non-decreasing in
+      // their ancestor: the quad's first slot binary-searches, the next ones step forward
+      // from the previous ancestor (a binary search again after 8 steps)
+      int steps = 0;
+      if (e > 0)
+        while (cum[lo] <= t && steps < 8) {
+          ++lo;
+          ++steps;
+        }
+      if (e == 0 || steps == 8) {
+        int hi = a.P - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (cum[mid] > t) hi = mid;
+          else lo = mid + 1;
+        }
       }
       const int64_t m = src + lo;
       (&X.x)[e] = __ldg(a.x + m);
