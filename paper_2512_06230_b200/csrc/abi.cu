@@ -182,8 +182,8 @@ glmb_status glmb_compat(const glmb_particles *trk, const float *Z, int32_t M, fl
   a.norm = static_cast<float>(1.0 / (2.0 * 3.14159265358979323846 * std::sqrt(det)));
   a.p_d = p_d; a.kappa = kappa; a.gamma = gamma;
   a.C_clutter = C_clutter; a.C_tracks = C_tracks; a.ldc = ldc; a.gate = gate; a.ldg = ldg;
-  glmb::compat_plan(M, a.P, &a.K, &a.NW, &a.n_mtiles);
-  if (static_cast<int64_t>(T) * a.n_mtiles > 0x7fffffffLL) return GLMB_ERR_INVALID_ARG;
+  glmb::compat_plan(M, a.P, &a.K, &a.NW, &a.CL, &a.n_mtiles);
+  if (static_cast<int64_t>(T) * a.n_mtiles * a.CL > 0x7fffffffLL) return GLMB_ERR_INVALID_ARG;
   return from_cuda(glmb::launch_compat(a, s));
 }
 

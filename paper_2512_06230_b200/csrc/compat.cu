@@ -43,6 +43,8 @@
 //    measurements of a warp = one gate word), coalesced C stores.
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "glmb_device.cuh"
 #include "glmb_internal.h"
 
@@ -211,33 +213,44 @@ __device__ __forceinline__ void tile_dispatch(int hv, const float4 *A, int np, M
 
 // Unit u = mt * T + j (all full measurement tiles first, the ragged last tiles
 // at the end of the grid, so the short units fill the tail of the schedule).
-template <int NW, int K, int EMU_PERIOD>
+// CL > 1: a thread-block cluster of CL CTAs shares one (track, measurement tile)
+// unit, CTA rank c summing the particle tiles [c tpc, (c+1) tpc); rank 0 adds the
+// ranks' partial sums in rank order through DSMEM and writes the epilogue.  Each
+// CTA does 1/CL of the unit's work, so the last wave of the grid is CL times
+// shorter (the tail of a 2.2-wave grid cost ~12 % of the launch).
+template <int NW, int K, int EMU_PERIOD, int CL>
 __global__ void __launch_bounds__(32 * NW, min_blocks<NW, K>()) compat_kernel(const CompatArgs a) {
   constexpr int H = Meas<K>::H;
   constexpr int kThreads = 32 * NW;
   constexpr int kTileM = 32 * NW;  // measurements per tile per K
+  __shared__ float part[CL > 1 ? K : 1][CL > 1 ? kThreads : 1];  // this CTA's partial sums
   extern __shared__ __align__(128) float smem[];
   float4 *aos = reinterpret_cast<float4 *>(smem + kStages * kRawFloats);  // 2 AoS tiles
   __shared__ __align__(8) uint64_t bars[kStages];
   __shared__ float red[2][kVWarps];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int mt = blockIdx.x / a.T;
-  const int j = blockIdx.x - mt * a.T;
+  const int unit = blockIdx.x / CL;
+  const int crank = CL > 1 ? static_cast<int>(blockIdx.x - unit * CL) : 0;
+  const int mt = unit / a.T;
+  const int j = unit - mt * a.T;
   const int wbase = mt * (kTileM * K) + warp * (32 * K);   // first measurement of this warp
   const int kv = min(K, max(0, (a.M - wbase + 31) >> 5));  // measurement slots with any valid lane
   const int hv = (kv + 1) >> 1;                            // packed pairs with any valid slot
   const int64_t base = static_cast<int64_t>(j) * a.ld;
   const float *xs = a.x + base, *ys = a.y + base, *ws = a.w + base;
   const int ntiles = (a.P + kTileP - 1) / kTileP;
+  const int tpc = (ntiles + CL - 1) / CL;                 // tiles per cluster rank
+  const int t_begin = min(ntiles, crank * tpc), t_end = min(ntiles, t_begin + tpc);
+  static_assert(kStages == 1, "the chunked tile schedule below assumes one raw stage");
   if (tid == 0) {
-#pragma unroll
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    mbar_init(&bars[0], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0)
-    for (int s = 0; s < kStages && s < ntiles; ++s) issue_tile(a, xs, ys, ws, smem + s * kRawFloats, &bars[s], s);
+  // the first tile is always tile 0 (the centre); ranks > 0 then jump to their own chunk
+  if (tid == 0) issue_tile(a, xs, ys, ws, smem, &bars[0], 0);
+  uint32_t phase = 0;
   float2 zr[2 * H];
 #pragma unroll
   for (int k = 0; k < 2 * H; ++k) {
@@ -247,15 +260,18 @@ __global__ void __launch_bounds__(32 * NW, min_blocks<NW, K>()) compat_kernel(co
 
   Meas<K> m;
   float cx = 0.f, cy = 0.f;
-  for (int t = 0; t < ntiles; ++t) {
-    const int s = t % kStages;
-    const float *X = smem + s * kRawFloats;
+  // ranks > 0: tile 0 only for the centre, then the rank's first tile
+  int t = crank == 0 ? 0 : -1;
+  for (; t < t_end; ++t) {
+    const float *X = smem;
     const float *Y = X + kTileP;
     const float *W = Y + kTileP;
     float4 *A = aos + (t & 1) * kTileP;
-    const int np = min(kTileP, a.P - t * kTileP);
-    mbar_wait_parity(&bars[s], static_cast<uint32_t>(t / kStages) & 1u);
-    if (t == 0) {  // centre c = mean position of the first tile (fixed order -> deterministic)
+    const int tt = t < 0 ? 0 : t;                         // the tile in the raw stage
+    const int np = min(kTileP, a.P - tt * kTileP);
+    mbar_wait_parity(&bars[0], phase);
+    phase ^= 1u;
+    if (tt == 0 && (t == 0 || t < 0)) {  // centre c = mean position of the first tile (fixed order -> deterministic)
       // summed as 128 virtual threads in 4 virtual warps whatever NW is, so the centre
       // (and hence C) is the same for every launch shape
 #pragma unroll
@@ -291,15 +307,40 @@ __global__ void __launch_bounds__(32 * NW, min_blocks<NW, K>()) compat_kernel(co
         m.tot[2 * h + 1] = 0.f;
       }
     }
-    // whiten raw tile -> AoS (X', Y', -, w)
+    if (t < 0) {  // centre only: load the rank's first own tile next
+      fence_proxy_async_smem();
+      __syncthreads();
+      if (tid == 0 && t_begin < t_end) issue_tile(a, xs, ys, ws, smem, &bars[0], t_begin);
+      t = t_begin - 1;
+      continue;
+    }
+    // whiten raw tile -> AoS (X', Y', w 2^-64, w)
     for (int idx = tid; idx < np; idx += kThreads) {
       const float lx = X[idx] - cx, ly = Y[idx] - cy;
       A[idx] = make_float4(fmaf(a.a2, ly, a.a1 * lx), a.b2 * ly, W[idx] * kTwoM64, W[idx]);
     }
-    fence_proxy_async_smem();  // raw stage s was read through the generic proxy; TMA rewrites it next
+    fence_proxy_async_smem();  // the raw stage was read through the generic proxy; TMA rewrites it next
     __syncthreads();           // AoS tile t complete; every warp is done with tile t-1
-    if (tid == 0 && t + kStages < ntiles) issue_tile(a, xs, ys, ws, smem + s * kRawFloats, &bars[s], t + kStages);
+    if (tid == 0 && t + 1 < t_end) issue_tile(a, xs, ys, ws, smem, &bars[0], t + 1);
     if (hv > 0) tile_dispatch<K, EMU_PERIOD>(hv, A, np, m);
+  }
+
+  if constexpr (CL > 1) {  // rank 0 adds the ranks' partial sums in rank order (DSMEM)
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+#pragma unroll
+    for (int k = 0; k < K; ++k) part[k][tid] = m.tot[k];
+    cluster.sync();
+    if (crank == 0) {
+#pragma unroll
+      for (int r = 1; r < CL; ++r) {
+        const float(*pp)[kThreads] = reinterpret_cast<const float(*)[kThreads]>(cluster.map_shared_rank(&part[0][0], r));
+#pragma unroll
+        for (int k = 0; k < K; ++k) m.tot[k] += pp[k][tid];
+      }
+    }
+    cluster.sync();  // peers keep their shared memory until rank 0 has read it
+    if (crank != 0) return;
   }
 
   // epilogue: likelihood, gate bit, C entry, clutter column
@@ -324,11 +365,35 @@ __global__ void clutter_fill_kernel(float *c, int32_t M, float kappa) {
   if (i < M) c[i] = kappa;
 }
 
+template <int NW, int K, int EMU_PERIOD, int CL>
+cudaError_t launch_kc(const CompatArgs &a, cudaStream_t s) {
+  const int64_t grid = static_cast<int64_t>(a.T) * a.n_mtiles * CL;
+  if (CL == 1) {
+    compat_kernel<NW, K, EMU_PERIOD, CL><<<static_cast<unsigned>(grid), 32 * NW, kSmemBytes, s>>>(a);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(32 * NW);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, compat_kernel<NW, K, EMU_PERIOD, CL>, a);
+}
+
 template <int NW, int K, int EMU_PERIOD>
 cudaError_t launch_k(const CompatArgs &a, cudaStream_t s) {
-  const int64_t grid = static_cast<int64_t>(a.T) * a.n_mtiles;
-  compat_kernel<NW, K, EMU_PERIOD><<<static_cast<unsigned>(grid), 32 * NW, kSmemBytes, s>>>(a);
-  return cudaGetLastError();
+  switch (a.CL) {
+    case 2: return launch_kc<NW, K, EMU_PERIOD, 2>(a, s);
+    case 4: return launch_kc<NW, K, EMU_PERIOD, 4>(a, s);
+    default: return launch_kc<NW, K, EMU_PERIOD, 1>(a, s);
+  }
 }
 
 // Share of the exps evaluated on the FMA pipe: one particle in |EMU| (negative:
@@ -360,13 +425,22 @@ cudaError_t launch_e(const CompatArgs &a, cudaStream_t s) {
 
 }  // namespace
 
-void compat_plan(int32_t M, int32_t P, int32_t *K, int32_t *NW, int32_t *n_mtiles) {
+void compat_plan(int32_t M, int32_t P, int32_t *K, int32_t *NW, int32_t *CL, int32_t *n_mtiles) {
   // Depends on (M, P) only -- never on T -- so any sharding of the tracks runs
   // the same per-column code (bit-identical C).  A warp holds 32 K measurements;
   // K = 2 (one packed pair per thread) wherever M allows, NW warps per CTA:
   //   M > 128: NW = 4, K = kDefaultK (GLMB_COMPAT_K overrides: A/B runs)
   //   64 < M <= 128: NW = 2, K = 2;  32 < M <= 64: NW = 1, K = 2;  M <= 32: NW = 1, K = 1
-  (void)P;
+  // CL: particle chunks per (track, measurement tile), a thread-block cluster (>= 8
+  // particle tiles per CTA); GLMB_COMPAT_CL overrides (A/B runs)
+  static const int32_t cl_env = [] {
+    const char *e = std::getenv("GLMB_COMPAT_CL");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int32_t ptiles = (P + kTileP - 1) / kTileP;
+  int32_t cl = ptiles >= 16 ? 2 : 1;  // measured (cfg3): CL = 1 14.5, 2 15.3, 4 14.9 pairs/clk/SM
+  if (cl_env == 1 || cl_env == 2 || cl_env == 4) cl = cl_env;
+  *CL = cl;
   static const int32_t kmax = [] {
     const char *e = std::getenv("GLMB_COMPAT_K");
     const int v = e ? std::atoi(e) : 2;

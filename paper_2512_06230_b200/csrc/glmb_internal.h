@@ -43,6 +43,7 @@ struct CompatArgs {
   int32_t n_mtiles;  // measurement tiles per track
   int32_t K;         // measurements per thread (tile = 32 * NW * K)
   int32_t NW;        // warps per CTA
+  int32_t CL;        // CTAs (particle chunks) per (track, measurement tile): cluster size
 };
 
 struct ReweightArgs {
@@ -145,7 +146,7 @@ cudaError_t launch_philox_dump(uint32_t k0, uint32_t k1, const uint32_t *ctr, in
 cudaError_t launch_normals_dump(uint32_t k0, uint32_t k1, const uint32_t *ctr, int32_t n, float *out,
                                 cudaStream_t s);
 // chooses K / n_mtiles from (M, P) only (never from T: bit-identical sharding)
-void compat_plan(int32_t M, int32_t P, int32_t *K, int32_t *NW, int32_t *n_mtiles);
+void compat_plan(int32_t M, int32_t P, int32_t *K, int32_t *NW, int32_t *CL, int32_t *n_mtiles);
 cudaError_t launch_compat(const CompatArgs &a, cudaStream_t s);
 cudaError_t launch_clutter_fill(float *C_clutter, int32_t M, float kappa, cudaStream_t s);
 cudaError_t launch_reweight(const ReweightArgs &a, cudaStream_t s);
