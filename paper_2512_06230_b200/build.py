@@ -37,12 +37,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     bdir = os.path.join(ROOT, "build", "glmb")
     os.makedirs(bdir, exist_ok=True)
-    objs = []
-    for src in SOURCES:
+    def compile_one(src):
         obj = os.path.join(bdir, src.replace(".cu", ".o"))
         cmd = [NVCC] + FLAGS + (["-Xptxas", "-v"] if verbose else []) + [
             "-I", os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, src), "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        return obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    # the translation units are independent: compile them concurrently
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    objs = []
+    for src, (obj, r) in zip(SOURCES, results):
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
         if verbose and r.stderr:

@@ -389,11 +389,7 @@ cudaError_t launch_kc(const CompatArgs &a, cudaStream_t s) {
 
 template <int NW, int K, int EMU_PERIOD>
 cudaError_t launch_k(const CompatArgs &a, cudaStream_t s) {
-  switch (a.CL) {
-    case 2: return launch_kc<NW, K, EMU_PERIOD, 2>(a, s);
-    case 4: return launch_kc<NW, K, EMU_PERIOD, 4>(a, s);
-    default: return launch_kc<NW, K, EMU_PERIOD, 1>(a, s);
-  }
+  return a.CL == 2 ? launch_kc<NW, K, EMU_PERIOD, 2>(a, s) : launch_kc<NW, K, EMU_PERIOD, 1>(a, s);
 }
 
 // Share of the exps evaluated on the FMA pipe: one particle in |EMU| (negative:
@@ -412,13 +408,10 @@ int emu_period() {
 
 template <int NW, int K>
 cudaError_t launch_e(const CompatArgs &a, cudaStream_t s) {
-  switch (emu_period()) {
+  switch (emu_period()) {  // the measured neighbourhood of the default (profiles/README.md)
     case 0: return launch_k<NW, K, 0>(a, s);
-    case -6: return launch_k<NW, K, -6>(a, s);
     case -8: return launch_k<NW, K, -8>(a, s);
     case -12: return launch_k<NW, K, -12>(a, s);
-    case -16: return launch_k<NW, K, -16>(a, s);
-    case 10: return launch_k<NW, K, 10>(a, s);
     default: return launch_k<NW, K, -10>(a, s);
   }
 }
@@ -439,12 +432,12 @@ void compat_plan(int32_t M, int32_t P, int32_t *K, int32_t *NW, int32_t *CL, int
   }();
   const int32_t ptiles = (P + kTileP - 1) / kTileP;
   int32_t cl = ptiles >= 16 ? 2 : 1;  // measured (cfg3): CL = 1 14.5, 2 15.3, 4 14.9 pairs/clk/SM
-  if (cl_env == 1 || cl_env == 2 || cl_env == 4) cl = cl_env;
+  if (cl_env == 1 || cl_env == 2) cl = cl_env;
   *CL = cl;
   static const int32_t kmax = [] {
     const char *e = std::getenv("GLMB_COMPAT_K");
     const int v = e ? std::atoi(e) : 2;
-    return (v == 1 || v == 2 || v == 4 || v == 8) ? v : 2;
+    return (v == 1 || v == 2) ? v : 2;
   }();
   int32_t k = kmax, nw = 4;
   if (M <= 32) {
@@ -472,8 +465,6 @@ cudaError_t launch_compat(const CompatArgs &a_in, cudaStream_t s) {
   switch (a.K) {
     case 1: return launch_e<4, 1>(a, s);
     case 2: return launch_e<4, 2>(a, s);
-    case 4: return launch_e<4, 4>(a, s);
-    case 8: return launch_e<4, 8>(a, s);
     default: return cudaErrorInvalidValue;
   }
 }
