@@ -93,3 +93,52 @@ def test_validation_without_gpu(lib):
     empty = glmb_particles(None, None, None, None, None, None, 0, 8, 8)
     assert L.glmb_predict(C.byref(empty), C.byref(empty), None, 0.1, 1.0, 0.1, 0, 0, None) == 0
     assert L.glmb_compat(C.byref(p), None, 0, 1.0, 0.0, 1.0, 0.9, 1e-3, 1e-6, None, None, 0, None, 0, None) == 0
+
+
+def test_validation_hypothesis_calls_without_gpu():
+    """The f1-f4 entry points reject bad arguments on the host (status -1 / -2) and treat
+    empty work as a successful no-op, before any CUDA call."""
+    from paper_2512_06230_b200 import _lib
+    L = _lib.load()
+    fake = 0x1000
+    # death_prob: p_d out of range, kappa < 0, ldc < M
+    assert L.glmb_death_prob(3, 40, fake, 40, fake, 2, 1.5, 1e-3, fake, fake, None) == -1
+    assert L.glmb_death_prob(3, 40, fake, 40, fake, 2, 0.9, -1.0, fake, fake, None) == -1
+    assert L.glmb_death_prob(3, 40, fake, 39, fake, 2, 0.9, 1e-3, fake, fake, None) == -1
+    assert L.glmb_death_prob(0, 40, None, 0, None, 0, 0.9, 1e-3, None, None, None) == 0
+    # compat_rows: NULL row_ptr, NULL outputs with cap > 0
+    assert L.glmb_compat_rows(3, 40, fake, 40, fake, 2, None, fake, fake, fake, 8, None) == -1
+    assert L.glmb_compat_rows(3, 40, fake, 40, fake, 2, fake, None, fake, fake, 8, None) == -1
+    # assoc_sample: H_up >= 2^24, ldt too small, misaligned theta / ldm % 4, count prior without a table
+    args = lambda **kw: dict(dict(H_old=2, n_par=None, H_up=8, T=40, M=10, pm=fake, ldt=2, plw=fake, d=fake,
+                                  ps=fake, pd=0.9, kappa=1e-3, rp=fake, col=fake, val=fake, lv=fake, clp=None,
+                                  ncount=0, seed=0, step=0, alive=fake, theta=fake, ldm=12, logw=fake,
+                                  hash=None, s=None), **kw)
+    call = lambda a: L.glmb_assoc_sample(*a.values())
+    assert call(args(H_up=1 << 24)) == -1
+    assert call(args(ldt=1)) == -1
+    assert call(args(ldm=10)) == -2
+    assert call(args(theta=fake + 4)) == -2
+    assert call(args(ncount=3)) == -1
+    assert call(args(H_old=0)) == 0
+    # dedup / prune
+    assert L.glmb_dedup(2, None, 8, 10, fake, 0, fake, 12, fake, fake, None) == -1      # ldt < 1
+    assert L.glmb_prune(10, fake, fake, -1.0, 5, fake, fake, fake, fake, None) == -1    # tau < 0
+    assert L.glmb_prune(10, fake, fake, 0.0, 16385, fake, fake, fake, fake, None) == -1  # h_max > limit
+    # pairs / particle loop
+    assert L.glmb_assoc_pairs(2, None, fake, fake, 2, fake, 12, 40, 10, fake, fake, fake, fake, fake,
+                              fake, 1, None) == -1                                     # short workspace
+    assert L.glmb_assoc_pairs_workspace_size(-1, 4, 4) == 0
+    p = _lib.glmb_particles(fake, fake, fake, fake, fake, fake, 2, 8, 8)
+    big = _lib.glmb_particles(fake, fake, fake, fake, fake, fake, 2, 16388, 16388)
+    assert L.glmb_reweight_pairs(C.byref(big), fake, 3, 1.0, 0.0, 1.0, 4, None, fake, fake, fake, fake, 16388,
+                                 fake, fake, fake, None) == -1                         # P > GLMB_PAIRS_PMAX
+    assert L.glmb_reweight_pairs(C.byref(p), fake, 3, 1.0, 0.0, 1.0, 4, None, fake, fake, fake, fake + 4, 8,
+                                 fake, fake, fake, None) == -2                         # misaligned w_out
+    assert L.glmb_reweight_pairs(C.byref(p), fake, 3, 1.0, 0.0, 1.0, 0, None, None, None, None, None, 8,
+                                 None, None, None, None) == 0                          # K = 0
+    assert L.glmb_resample(C.byref(p), 2, None, fake, fake, 6, C.byref(p), 0, 0, None, None) == -2   # ldw % 4
+    assert L.glmb_resample(C.byref(p), 3, None, fake, fake, 8, C.byref(p), 0, 0, None, None) == -1   # out too small
+    # tracker loop
+    assert L.glmb_next_parents(4, fake, fake, fake, 10, 64, 1, 0, fake, 1, fake, fake, None) == -1  # K_cap > 32 ldt
+    assert L.glmb_map_estimate(None, fake, 3, C.byref(p), fake, None) == -1
