@@ -486,6 +486,67 @@ glmb_status glmb_map_estimate(const int32_t *n_kept, const int32_t *pair_of0,
                               glmb_stream_t stream);
 
 /* ---------------------------------------------------------------------
+ * glmb_update -- the whole update after C_k in one call: the
+ * calls glmb_death_prob -> glmb_compat_rows -> glmb_assoc_sample ->
+ * glmb_dedup -> glmb_prune -> glmb_assoc_pairs -> glmb_reweight_pairs ->
+ * glmb_resample (-> glmb_map_estimate when est != NULL), enqueued in that
+ * order on `stream` with the counts passed between them on the device (no
+ * host round trip).  Each field has the meaning, layout and requirements of
+ * the same argument of those calls; the first failing call's status is
+ * returned (earlier calls stay enqueued).
+ * --------------------------------------------------------------------- */
+typedef struct {
+  /* sizes and model */
+  int32_t T, M, H_old, H_up, h_max, K_cap;
+  float p_d, kappa, Rxx, Rxy, Ryy;
+  double tau;
+  uint64_t seed;
+  uint32_t step;
+  /* inputs (device) */
+  glmb_particles tracks;         /* the T_k predicted tracks (x, y, w read; all read by resample) */
+  const float *C_tracks;         /* [T][ldc] as glmb_compat writes it */
+  int64_t ldc;
+  const uint32_t *gate;          /* [T][ldg] */
+  int64_t ldg;
+  const float *Z;                /* [M][2] */
+  const float *p_s;              /* [T] */
+  const uint32_t *parent_mask;   /* [H_old][ldt] */
+  int32_t ldt;
+  const double *parent_logw;     /* [H_old] */
+  const int32_t *n_parents;      /* device count or NULL */
+  const double *count_lp;        /* [n_count] or NULL */
+  int32_t n_count;
+  /* workspaces and outputs (device) */
+  float *d_prob;                 /* [T] */
+  int32_t *row_ptr, *col;        /* [M+1], [rows_cap] */
+  float *val;                    /* [rows_cap] */
+  double *ln_val;                /* [rows_cap] */
+  int32_t rows_cap;
+  uint32_t *alive;               /* [H_old*H_up][ldt] */
+  int32_t *theta;                /* [H_old*H_up][ldm] */
+  int64_t ldm;
+  double *logw;                  /* [H_old*H_up] */
+  uint64_t *hash;                /* [H_old*H_up] */
+  uint8_t *unique;               /* [H_old*H_up] */
+  uint64_t *prune_ws;            /* [H_old*H_up] */
+  int32_t *keep_idx;             /* [h_max] */
+  double *keep_w;                /* [h_max] */
+  int32_t *n_kept;               /* device int32 */
+  int32_t *pair_track, *pair_ptr, *pair_meas, *pair_of, *n_pairs;  /* as glmb_assoc_pairs (n_hyp = h_max) */
+  void *pairs_ws;
+  size_t pairs_ws_bytes;
+  float *w_new;                  /* [K_cap][ld_new] */
+  int64_t ld_new;
+  float *log_norm;               /* [K_cap] */
+  uint32_t *flags;               /* [K_cap] */
+  float *ess;                    /* [K_cap] */
+  glmb_particles out;            /* the new particle set, >= K_cap rows */
+  double *est;                   /* [T][3] MAP estimate, or NULL */
+} glmb_update_params;
+
+glmb_status glmb_update(const glmb_update_params *u, glmb_stream_t stream);
+
+/* ---------------------------------------------------------------------
  * Test hooks (not on the hot path; same device code as predict/birth).
  * glmb_philox_dump: out[n] = Philox4x32-10(key(seed), ctr[n]) for n < N.
  * glmb_normals_dump: out[n] = the four Box-Muller normals of that block

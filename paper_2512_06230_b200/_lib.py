@@ -43,12 +43,27 @@ class glmb_step_params(C.Structure):
                 ("col_offset", C.c_int32)]
 
 
+class glmb_update_params(C.Structure):
+    vp, i32, i64, f32, f64 = C.c_void_p, C.c_int32, C.c_int64, C.c_float, C.c_double
+    _fields_ = [("T", i32), ("M", i32), ("H_old", i32), ("H_up", i32), ("h_max", i32), ("K_cap", i32),
+                ("p_d", f32), ("kappa", f32), ("Rxx", f32), ("Rxy", f32), ("Ryy", f32), ("tau", f64),
+                ("seed", C.c_uint64), ("step", C.c_uint32), ("tracks", glmb_particles),
+                ("C_tracks", vp), ("ldc", i64), ("gate", vp), ("ldg", i64), ("Z", vp), ("p_s", vp),
+                ("parent_mask", vp), ("ldt", i32), ("parent_logw", vp), ("n_parents", vp), ("count_lp", vp),
+                ("n_count", i32), ("d_prob", vp), ("row_ptr", vp), ("col", vp), ("val", vp), ("ln_val", vp),
+                ("rows_cap", i32), ("alive", vp), ("theta", vp), ("ldm", i64), ("logw", vp), ("hash", vp),
+                ("unique", vp), ("prune_ws", vp), ("keep_idx", vp), ("keep_w", vp), ("n_kept", vp),
+                ("pair_track", vp), ("pair_ptr", vp), ("pair_meas", vp), ("pair_of", vp), ("n_pairs", vp),
+                ("pairs_ws", vp), ("pairs_ws_bytes", C.c_size_t), ("w_new", vp), ("ld_new", i64),
+                ("log_norm", vp), ("flags", vp), ("ess", vp), ("out", glmb_particles), ("est", vp)]
+
+
 EXPORTED = ["glmb_version", "glmb_status_string", "glmb_init", "glmb_sm_count", "glmb_predict",
             "glmb_birth", "glmb_compat", "glmb_reweight", "glmb_step", "glmb_step_host",
             "glmb_philox_dump", "glmb_normals_dump", "glmb_death_prob", "glmb_compat_rows",
             "glmb_assoc_sample", "glmb_dedup", "glmb_prune", "glmb_assoc_pairs_workspace_size",
             "glmb_assoc_pairs", "glmb_reweight_pairs", "glmb_resample", "glmb_next_parents",
-            "glmb_map_estimate"]
+            "glmb_map_estimate", "glmb_update"]
 
 
 def load(path: str = LIB_PATH):
@@ -85,6 +100,7 @@ def load(path: str = LIB_PATH):
         L.glmb_dedup.argtypes = [i32, vp, i32, i32, vp, i32, vp, i64, vp, vp, vp]
         L.glmb_next_parents.argtypes = [i32, vp, vp, vp, i32, i32, i32, i32, vp, i32, vp, vp, vp]
         L.glmb_map_estimate.argtypes = [vp, vp, i32, PP, vp, vp]
+        L.glmb_update.argtypes = [C.POINTER(glmb_update_params), vp]
         L.glmb_prune.argtypes = [i32, vp, vp, C.c_double, i32, vp, vp, vp, vp, vp]
         L.glmb_assoc_pairs_workspace_size.argtypes = [i32, i32, i32]
         L.glmb_assoc_pairs_workspace_size.restype = C.c_size_t
@@ -337,3 +353,8 @@ def glmb_map_estimate(n_kept, pair_of0, new_set: Particles, est, stream=None):
     t = new_set.struct()
     _check(load().glmb_map_estimate(_ptr(n_kept), _ptr(pair_of0), pair_of0.shape[0], C.byref(t), _ptr(est),
                                     _stream(stream)))
+
+
+def glmb_update(params: "glmb_update_params", stream=None):
+    """The whole update after C_k in one C call (include/glmb.h glmb_update)."""
+    _check(load().glmb_update(C.byref(params), _stream(stream)))

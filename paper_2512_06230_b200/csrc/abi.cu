@@ -3,6 +3,7 @@
 // Validation, device selection from the caller's stream, launch planning.
 // Every entry point is asynchronous on the caller's stream (glmb_step_host
 // excepted), never allocates, never aborts.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -486,6 +487,33 @@ glmb_status glmb_map_estimate(const int32_t *n_kept, const int32_t *pair_of0, in
   GLMB_TRY(bind_stream(s, nullptr));
   glmb::MapEstimateArgs a{n_kept, pair_of0, T, set->n_particles, set->ld, set->x, set->y, set->w, est};
   return from_cuda(glmb::launch_map_estimate(a, s));
+}
+
+glmb_status glmb_update(const glmb_update_params *u, glmb_stream_t stream) {
+  if (u == nullptr) return GLMB_ERR_INVALID_ARG;
+  const int64_t n = static_cast<int64_t>(u->H_old) * u->H_up;
+  GLMB_TRY(glmb_death_prob(u->T, u->M, u->C_tracks, u->ldc, u->gate, u->ldg, u->p_d, u->kappa, u->p_s, u->d_prob,
+                           stream));
+  GLMB_TRY(glmb_compat_rows(u->T, u->M, u->C_tracks, u->ldc, u->gate, u->ldg, u->row_ptr, u->col, u->val, u->ln_val,
+                            u->rows_cap, stream));
+  GLMB_TRY(glmb_assoc_sample(u->H_old, u->n_parents, u->H_up, u->T, u->M, u->parent_mask, u->ldt, u->parent_logw,
+                             u->d_prob, u->p_s, u->p_d, u->kappa, u->row_ptr, u->col, u->val, u->ln_val, u->count_lp,
+                             u->n_count, u->seed, u->step, u->alive, u->theta, u->ldm, u->logw, u->hash, stream));
+  GLMB_TRY(glmb_dedup(u->H_old, u->n_parents, u->H_up, u->M, u->alive, u->ldt, u->theta, u->ldm, u->hash, u->unique,
+                      stream));
+  if (n > 0x7fffffffLL) return GLMB_ERR_INVALID_ARG;
+  GLMB_TRY(glmb_prune(static_cast<int32_t>(n), u->logw, u->unique, u->tau, u->h_max, u->prune_ws, u->keep_idx,
+                      u->keep_w, u->n_kept, stream));
+  GLMB_TRY(glmb_assoc_pairs(u->h_max, u->n_kept, u->keep_idx, u->alive, u->ldt, u->theta, u->ldm, u->T, u->M,
+                            u->pair_track, u->pair_ptr, u->pair_meas, u->pair_of, u->n_pairs, u->pairs_ws,
+                            u->pairs_ws_bytes, stream));
+  const int32_t K = static_cast<int32_t>(std::min<int64_t>(u->K_cap, std::max<int64_t>(1, static_cast<int64_t>(u->h_max) * u->T)));
+  GLMB_TRY(glmb_reweight_pairs(&u->tracks, u->Z, u->M, u->Rxx, u->Rxy, u->Ryy, K, u->n_pairs, u->pair_track,
+                               u->pair_ptr, u->pair_meas, u->w_new, u->ld_new, u->log_norm, u->flags, u->ess, stream));
+  GLMB_TRY(glmb_resample(&u->tracks, K, u->n_pairs, u->pair_track, u->w_new, u->ld_new, &u->out, u->seed, u->step,
+                         u->flags, stream));
+  if (u->est != nullptr) GLMB_TRY(glmb_map_estimate(u->n_kept, u->pair_of, u->T, &u->out, u->est, stream));
+  return GLMB_OK;
 }
 
 glmb_status glmb_philox_dump(uint64_t seed, const uint32_t *ctr, int32_t N, uint32_t *out, glmb_stream_t stream) {

@@ -123,3 +123,24 @@ class ParticleUpdate:
         if K > self.K_cap:
             raise RuntimeError(f"{K} unique pairs exceed K_cap = {self.K_cap}")
         return K
+
+
+def update_params(hu: HypothesisUpdate, pu: ParticleUpdate, tracks, C_tracks, gate, M, Z, R, p_s, parent_mask,
+                  parent_logw, p_d, kappa, tau, seed, step, n_parents=None, count_lp=None, out=None,
+                  est=None) -> _lib.glmb_update_params:
+    """The glmb_update argument block over the buffers of hu / pu (T = hu.T columns)."""
+    T = hu.T
+    n = hu.H_old * hu.H_up
+    K = min(pu.K_cap, max(1, hu.h_max * T))
+    o = pu.out if out is None else out
+    p = _lib._ptr
+    return _lib.glmb_update_params(
+        T, int(M), hu.H_old, hu.H_up, hu.h_max, K, p_d, kappa, R[0], R[1], R[2], float(tau),
+        int(seed) & 0xFFFFFFFFFFFFFFFF, int(step), tracks.struct(), p(C_tracks), C_tracks.shape[1], p(gate),
+        gate.shape[1], p(Z), p(p_s), p(parent_mask), parent_mask.shape[1], p(parent_logw), p(n_parents),
+        p(count_lp), 0 if count_lp is None else count_lp.shape[0], p(hu.d), p(hu.row_ptr), p(hu.col),
+        p(hu.val), p(hu.ln_val), hu.col.shape[0], p(hu.alive), p(hu.theta), hu.theta.shape[1], p(hu.logw),
+        p(hu.hash), p(hu.unique), p(hu.keys), p(hu.keep_idx), p(hu.keep_w), p(hu.n_kept), p(pu.pair_track),
+        p(pu.pair_ptr), p(pu.pair_meas), p(pu.pair_of), p(pu.n_pairs), p(pu.ws),
+        pu.ws.numel() * pu.ws.element_size(), p(pu.w_new), pu.w_new.shape[1], p(pu.log_norm), p(pu.flags),
+        p(pu.ess), o.struct(), p(est))

@@ -25,7 +25,7 @@ import torch
 
 from . import _lib
 from ._lib import Particles
-from .hyp import HypothesisUpdate, ParticleUpdate
+from .hyp import HypothesisUpdate, ParticleUpdate, update_params
 from .scenes import ConvoyConfig
 
 
@@ -115,7 +115,11 @@ class ConvoyTracker:
         _lib.glmb_next_parents(n1, one, none, 0, cfg.B, 0, self.parent_mask[:1], self.parent_logw[:1],
                                self.n_parents, self.stream)
 
-    def update(self, k: int, Z: np.ndarray, host_Z: bool = True) -> UpdateRecord:
+    STAGES = ("predict", "birth", "compat", "death_prob", "compat_rows", "assoc_sample", "dedup", "prune",
+              "assoc_pairs", "reweight_pairs", "resample", "map_estimate")
+
+    def update(self, k: int, Z: np.ndarray, profile: bool = False) -> UpdateRecord:
+        """One tracker update.  profile=True records a CUDA event after every stage (self.last_events)."""
         cfg, s = self.cfg, self.stream
         M = Z.shape[0]
         assert M <= self.M_max
@@ -125,37 +129,57 @@ class ConvoyTracker:
         dst = self.bufs[1 - self.cur]
         T, B = self.n_surv, cfg.B
         Tk = T + B
+        evs = {}
+
+        def mark(name):
+            if profile:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(s)
+                evs[name] = ev
+
         with torch.cuda.stream(s):
             e0.record(s)
             self.Z[:M].copy_(torch.from_numpy(Z), non_blocking=True)
             Zk = self.Z[:M]
             self.p_s[:T].fill_(cfg.p_s)
             self.p_s[T:Tk].fill_(cfg.r_birth)
+            mark("start")
             if T:
                 surv = src.rows(0, T)
                 _lib.glmb_predict(surv, surv, self.gid[:T], cfg.dt, cfg.sigma_a, cfg.sigma_w, cfg.seed, k, s)
+            mark("predict")
             _lib.glmb_birth(src.rows(T, Tk), self.gid[T:Tk], self.birth_mean, self.birth_chol, cfg.seed, k, s)
+            mark("birth")
             trk = src.rows(0, Tk)
             _lib.glmb_compat(trk, Zk, cfg.R, cfg.p_d, cfg.kappa, cfg.gamma, self.C_clutter[:M],
                              self.C_tracks[:Tk], self.gate[:Tk], s)
-            hu = self.hu
+            mark("compat")
+            hu, pu = self.hu, self.pu
             # the hypothesis machinery works on T_k columns (capacity-sized buffers, views)
             hu.T = Tk
-            hu.run(self.C_tracks[:Tk], self.gate[:Tk], M, self.p_s[:Tk], self.parent_mask,
-                   self.parent_logw, cfg.p_d, cfg.kappa, cfg.tau, cfg.seed, k, s, n_parents=self.n_parents,
-                   count_lp=self.count_lp)
-            pu = self.pu
             pu.T = Tk
-            pu.run(trk, Zk, cfg.R, hu.keep_idx, cfg.H_max, hu.alive, hu.theta, M, cfg.seed, k, s,
-                   n_hyp_dev=hu.n_kept, out=dst.rows(0, self.K_cap))
             po = pu.pair_of.view(-1)[:cfg.H_max * Tk].view(cfg.H_max, Tk)   # packed [H][T_k]
-            _lib.glmb_map_estimate(hu.n_kept, po[0], dst.rows(0, self.K_cap), self.est[:Tk], s)
+            if profile:   # stage by stage, an event after each
+                hu.run(self.C_tracks[:Tk], self.gate[:Tk], M, self.p_s[:Tk], self.parent_mask,
+                       self.parent_logw, cfg.p_d, cfg.kappa, cfg.tau, cfg.seed, k, s, n_parents=self.n_parents,
+                       count_lp=self.count_lp, mark=mark)
+                pu.run(trk, Zk, cfg.R, hu.keep_idx, cfg.H_max, hu.alive, hu.theta, M, cfg.seed, k, s,
+                       n_hyp_dev=hu.n_kept, out=dst.rows(0, self.K_cap), mark=mark)
+                _lib.glmb_map_estimate(hu.n_kept, po[0], dst.rows(0, self.K_cap), self.est[:Tk], s)
+                mark("map_estimate")
+            else:         # one C call enqueues the whole chain (host overhead of one launch sequence)
+                prm = update_params(hu, pu, trk, self.C_tracks[:Tk], self.gate[:Tk], M, Zk, cfg.R, self.p_s[:Tk],
+                                    self.parent_mask, self.parent_logw, cfg.p_d, cfg.kappa, cfg.tau, cfg.seed, k,
+                                    n_parents=self.n_parents, count_lp=self.count_lp,
+                                    out=dst.rows(0, self.K_cap), est=self.est[:Tk])
+                _lib.glmb_update(prm, s)
             self.counts[0:1].copy_(pu.n_pairs)
             self.counts[1:2].copy_(hu.n_kept)
             self.counts[2:3].copy_(self.n_parents)
             self.counts_host.copy_(self.counts, non_blocking=True)
             e1.record(s)
         s.synchronize()
+        self.last_events = evs
         K, n_kept, n_par = (int(v) for v in self.counts_host)
         if K > self.K_cap:
             raise RuntimeError(f"step {k}: {K} unique pairs exceed K_cap = {self.K_cap}")
@@ -175,8 +199,9 @@ class ConvoyTracker:
 
 
 def run_convoy(cfg: ConvoyConfig, steps: int | None = None, K_cap: int = 1024, device="cuda",
-               with_estimates: bool = True):
-    """Runs the tracker over the convoy scene; returns (records, estimates, truth)."""
+               with_estimates: bool = True, stage_ms: dict | None = None):
+    """Runs the tracker over the convoy scene; returns (records, estimates, truth).  With a dict
+    as stage_ms, every update is profiled per stage (CUDA events) and the means are stored in it."""
     from .scenes import convoy_scene
     Zs, truth, bm, bc = convoy_scene(cfg)
     n = len(Zs) if steps is None else min(steps, len(Zs))
@@ -185,11 +210,19 @@ def run_convoy(cfg: ConvoyConfig, steps: int | None = None, K_cap: int = 1024, d
     tr.reset(bm, bc)
     recs: List[UpdateRecord] = []
     ests = []
+    acc = {name: 0.0 for name in ConvoyTracker.STAGES}
     for k in range(n):
-        rec = tr.update(k, Zs[k])
+        rec = tr.update(k, Zs[k], profile=stage_ms is not None)
         recs.append(rec)
+        if stage_ms is not None:
+            prev = tr.last_events["start"]
+            for name in ConvoyTracker.STAGES:
+                acc[name] += prev.elapsed_time(tr.last_events[name])
+                prev = tr.last_events[name]
         if with_estimates:
             ests.append(tr.estimate(rec.T_k))
+    if stage_ms is not None:
+        stage_ms.update({name: v / max(n, 1) for name, v in acc.items()})
     return recs, ests, truth[:n]
 
 
