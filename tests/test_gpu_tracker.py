@@ -133,3 +133,42 @@ def test_convoy_tracker_small(L):
     assert card <= 0.15, card
     assert dist <= 0.3, dist
     assert max(r.n_kept for r in recs) <= cfg.H_max
+
+
+def test_glmb_update_one_call_equals_stages(L, orc):
+    """glmb_update (one C call) enqueues exactly the stage-by-stage chain: identical outputs."""
+    import torch
+    from paper_2512_06230_b200 import scenes
+    from paper_2512_06230_b200._lib import Particles
+    from paper_2512_06230_b200.hyp import HypothesisUpdate, ParticleUpdate, update_params
+    sc = scenes.make_scene(1, steps=1)
+    cfg = sc.cfg
+    Z = sc.Z[0]
+    ref = orc.compat(sc.x, sc.y, sc.w, Z, cfg.R, cfg.p_d, cfg.kappa, cfg.gamma)
+    C = _dev(ref["C_tracks"].astype(np.float32))
+    g = _dev(np.ascontiguousarray(ref["gate"], np.uint32).view(np.int32))
+    T, M = C.shape[0], Z.shape[0]
+    pm, plw, ps = scenes.hypothesis_inputs(T, 0, 6, seed=2)
+    lc = _dev(np.array([-2.0, -0.5, -0.2, -1.0, -3.0]))
+    src = Particles.from_arrays([sc.x, sc.y, sc.v, sc.psi, sc.omega, sc.w])
+    outs = []
+    for one_call in (False, True):
+        hu = HypothesisUpdate(T, M, 6, 50, 12)
+        pu = ParticleUpdate(T, M, 12, cfg.P)
+        est = torch.zeros(T, 3, dtype=torch.float64, device="cuda")
+        if one_call:
+            prm = update_params(hu, pu, src, C, g, M, _dev(Z), cfg.R, _dev(ps), _dev(pm.view(np.int32)), _dev(plw),
+                                cfg.p_d, cfg.kappa, 1e-5, 9, 1, count_lp=lc, est=est)
+            L.glmb_update(prm)
+        else:
+            hu.run(C, g, M, _dev(ps), _dev(pm.view(np.int32)), _dev(plw), cfg.p_d, cfg.kappa, 1e-5, 9, 1,
+                   count_lp=lc)
+            pu.run(src, _dev(Z), cfg.R, hu.keep_idx, 12, hu.alive, hu.theta, M, 9, 1, n_hyp_dev=hu.n_kept)
+            L.glmb_map_estimate(hu.n_kept, pu.pair_of.view(-1)[:T], pu.out, est)
+        K = pu.n_pairs_checked()
+        nk = int(_host(hu.n_kept)[0])
+        outs.append([_host(hu.theta)[:, :M], _host(hu.logw), _host(hu.keep_idx)[:nk], K, _host(pu.out.data)[:, :K],
+                     _host(est)])
+    a, b = outs
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x, y)
