@@ -211,8 +211,8 @@ __device__ __forceinline__ void tile_dispatch(int hv, const float4 *A, int np, M
   }
 }
 
-// Unit u = mt * T + j (all full measurement tiles first, the ragged last tiles
-// at the end of the grid, so the short units fill the tail of the schedule).
+// Units: every track's full measurement tiles (track-major), then the ragged
+// last tiles of all tracks (so the short units fill the tail of the schedule).
 // CL > 1: a thread-block cluster of CL CTAs shares one (track, measurement tile)
 // unit, CTA rank c summing the particle tiles [c tpc, (c+1) tpc); rank 0 adds the
 // ranks' partial sums in rank order through DSMEM and writes the epilogue.  Each
@@ -232,8 +232,21 @@ __global__ void __launch_bounds__(32 * NW, min_blocks<NW, K>()) compat_kernel(co
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int unit = blockIdx.x / CL;
   const int crank = CL > 1 ? static_cast<int>(blockIdx.x - unit * CL) : 0;
-  const int mt = unit / a.T;
-  const int j = unit - mt * a.T;
+  // unit order: a track's full measurement tiles are adjacent (they run concurrently and
+  // share the particle tiles through L2: one HBM read of the state instead of one per tile),
+  // the ragged last tiles of all tracks come last (short units fill the tail of the grid)
+  const int n_full = a.M % (kTileM * K) == 0 ? a.n_mtiles : a.n_mtiles - 1;
+  int mt, j;
+  if (a.track_major == 0) {  // GLMB_COMPAT_ORDER=0: tile-major (A/B runs)
+    mt = unit / a.T;
+    j = unit - mt * a.T;
+  } else if (unit < a.T * n_full) {
+    j = unit / n_full;
+    mt = unit - j * n_full;
+  } else {
+    j = unit - a.T * n_full;
+    mt = a.n_mtiles - 1;
+  }
   const int wbase = mt * (kTileM * K) + warp * (32 * K);   // first measurement of this warp
   const int kv = min(K, max(0, (a.M - wbase + 31) >> 5));  // measurement slots with any valid lane
   const int hv = (kv + 1) >> 1;                            // packed pairs with any valid slot
@@ -459,7 +472,12 @@ void compat_plan(int32_t M, int32_t P, int32_t *K, int32_t *NW, int32_t *CL, int
 }
 
 cudaError_t launch_compat(const CompatArgs &a_in, cudaStream_t s) {
-  const CompatArgs &a = a_in;
+  static const int order_env = [] {
+    const char *e = std::getenv("GLMB_COMPAT_ORDER");
+    return e ? std::atoi(e) : 1;
+  }();
+  CompatArgs a = a_in;
+  a.track_major = order_env;
   if (a.NW == 1) return a.K == 1 ? launch_e<1, 1>(a, s) : launch_e<1, 2>(a, s);
   if (a.NW == 2) return launch_e<2, 2>(a, s);
   switch (a.K) {

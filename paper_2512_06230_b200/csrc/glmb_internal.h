@@ -44,6 +44,7 @@ struct CompatArgs {
   int32_t K;         // measurements per thread (tile = 32 * NW * K)
   int32_t NW;        // warps per CTA
   int32_t CL;        // CTAs (particle chunks) per (track, measurement tile): cluster size
+  int32_t track_major;  // unit order: 1 = a track's measurement tiles adjacent, 0 = tile-major
 };
 
 struct ReweightArgs {
