@@ -389,13 +389,13 @@ def main():
     from paper_2512_06230_b200.dist import ShardPlan, allgather_columns, broadcast_measurements
     from paper_2512_06230_b200.step import GlmbStep
 
+    torch.cuda.set_device(local)   # before NCCL init: each rank's communicator binds its own GPU
     if rank == 0:
         build()
     if world > 1:
-        dist.init_process_group("nccl")
-        dist.barrier()
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.barrier(device_ids=[local])
         build()  # no-op once rank 0 has built
-    torch.cuda.set_device(local)
     L.glmb_init(local)
     dev = torch.device("cuda", local)
     cfg = CONFIGS[cfg_id]
@@ -474,7 +474,7 @@ def main():
     torch.cuda.synchronize(dev)
     sampler = ClockSampler(local)
     if world > 1:
-        dist.barrier()
+        dist.barrier(device_ids=[local])
     torch.cuda.synchronize(dev)
     t_start, t_end = ev(), ev()
     with sampler:
@@ -484,7 +484,7 @@ def main():
         t_end.record(stream)
         torch.cuda.synchronize(dev)
     if world > 1:
-        dist.barrier()
+        dist.barrier(device_ids=[local])
     elapsed_ms = t_start.elapsed_time(t_end)
     # per-kernel durations: the same steps again, serialised (outside the timed region)
     all_marks = [isolated_step(k) for k in range(a.warmup, a.warmup + a.steps)]
@@ -530,7 +530,7 @@ def main():
         for k in range(a.warmup):
             host_step(k)
         if world > 1:
-            dist.barrier()
+            dist.barrier(device_ids=[local])
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
         for k in range(a.warmup, a.warmup + a.steps):
