@@ -273,8 +273,8 @@ __global__ void __launch_bounds__(256) finish_kernel(PairsArgs a) {
 // t_n = floor((n S + V) / P), V = floor(U S 2^-24), U = 2 (r >> 9) + 1 from
 // Philox(counter (k, 0, step, 4 << 24)) word 0.  Ancestors are non-decreasing in n,
 // so the gathers of consecutive slots hit neighbouring addresses.
-constexpr int kResThreads = 1024;
-
+// NT threads per pair: 256 for P <= 2048 (short CTAs), 1024 above (more gathers in flight)
+template <int kResThreads>
 __global__ void __launch_bounds__(kResThreads) resample_kernel(ResampleArgs a) {
   extern __shared__ __align__(16) unsigned char rs[];
   unsigned long long *cum = reinterpret_cast<unsigned long long *>(rs);  // [P]
@@ -509,11 +509,14 @@ cudaError_t launch_resample(const ResampleArgs &a, cudaStream_t s) {
   if (a.K == 0) return cudaSuccess;
   const size_t smem = static_cast<size_t>(a.P) * (sizeof(unsigned long long) + sizeof(uint32_t));
   if (smem > 40 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(resample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+    cudaError_t e = a.P <= 2048 ? cudaFuncSetAttribute(resample_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       static_cast<int>(smem))
+                                : cudaFuncSetAttribute(resample_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  resample_kernel<<<a.K, kResThreads, smem, s>>>(a);
+  if (a.P <= 2048) resample_kernel<256><<<a.K, 256, smem, s>>>(a);
+  else resample_kernel<1024><<<a.K, 1024, smem, s>>>(a);
   return cudaGetLastError();
 }
 
