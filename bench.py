@@ -519,11 +519,12 @@ def main():
         ln_h = pin(torch.empty(st.T_local))
         fl_h = pin(torch.empty(st.T_local, dtype=torch.int32))
         h2d = d2h = 0
+        copy_stream = torch.cuda.Stream(device=dev)   # read-back of C_k overlapped with compat chunks
 
         def host_step(k):
             zi = k % len(Zh)
             L.glmb_step_host(st.step_params(k), Zh[zi], thh[zi], Zd, thd, o.C_clutter, o.C_tracks,
-                             o.gate, o.log_norm, o.flags, Cc_h, Ct_h, G_h, ln_h, fl_h, stream)
+                             o.gate, o.log_norm, o.flags, Cc_h, Ct_h, G_h, ln_h, fl_h, stream, copy_stream)
             M = Zh[zi].shape[0]
             return M * 8 + M * 4, M * 4 + st.T_local * st.ldc * 4 + st.T_local * st.ldg * 4 + st.T_local * 8
 
@@ -545,8 +546,9 @@ def main():
         e2e = {"value": evals_total / e2e_s, "unit": "evals/s",
                "h2d_bytes_per_step": h2d // a.steps, "d2h_bytes_per_step": d2h // a.steps,
                "ms_per_step": e2e_s * 1e3 / a.steps,
-               "note": "glmb_step_host: pinned H2D of Z_k, theta_k; step; D2H of C_k, gate, "
-                       "log_norm, flags; stream synchronised each step; particle state resident"}
+               "note": "glmb_step_host: pinned H2D of Z_k, theta_k; step; D2H of C_k and gate on a copy "
+                       "stream overlapping reweight, log_norm, flags; synchronised each step; particle state "
+                       "resident"}
 
     if rank != 0:
         if world > 1:

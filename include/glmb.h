@@ -228,7 +228,13 @@ glmb_status glmb_step(const glmb_step_params *prm, const float *Z, int32_t M,
  * into the device workspaces Z_dev / theta_dev (capacity >= M), runs
  * glmb_step, copies C_clutter, C_tracks ([T_k][ldc]), gate ([T_k][ldg]),
  * log_norm and flags back into the *_host buffers, then synchronises
- * `stream`.  The particle state stays resident on the device. */
+ * `stream`.  The particle state stays resident on the device.
+ * copy_stream (may be NULL; needs a non-NULL `stream`): a second stream for
+ * the read-back -- C_k's columns and gate words are copied back on
+ * copy_stream while reweight runs (environment GLMB_HOST_CHUNKS = 2..4 also
+ * splits compat into track chunks so the read-back overlaps compat; results
+ * are identical either way: C is bit-identical under any split of the
+ * tracks). */
 glmb_status glmb_step_host(const glmb_step_params *prm, const float *Z_host,
                            int32_t M, const int32_t *theta_host, float *Z_dev,
                            int32_t *theta_dev, float *C_clutter_dev,
@@ -237,7 +243,7 @@ glmb_status glmb_step_host(const glmb_step_params *prm, const float *Z_host,
                            uint32_t *flags_dev, float *C_clutter_host,
                            float *C_tracks_host, uint32_t *gate_host,
                            float *log_norm_host, uint32_t *flags_host,
-                           glmb_stream_t stream);
+                           glmb_stream_t stream, glmb_stream_t copy_stream);
 
 /* =====================================================================
  * Hypothesis machinery: the consumers of C_k.

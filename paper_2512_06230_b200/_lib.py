@@ -90,7 +90,7 @@ def load(path: str = LIB_PATH):
         SP = C.POINTER(glmb_step_params)
         L.glmb_step.argtypes = [SP, vp, i32, vp, vp, vp, i64, vp, i64, vp, vp, vp]
         L.glmb_step_host.argtypes = [SP, vp, i32, vp, vp, vp, vp, vp, i64, vp, i64, vp, vp,
-                                     vp, vp, vp, vp, vp, vp]
+                                     vp, vp, vp, vp, vp, vp, vp]
         L.glmb_philox_dump.argtypes = [u64, vp, i32, vp, vp]
         L.glmb_normals_dump.argtypes = [u64, vp, i32, vp, vp]
         L.glmb_death_prob.argtypes = [i32, i32, vp, i64, vp, i64, f32, f32, vp, vp, vp]
@@ -245,15 +245,17 @@ def glmb_step(prm: glmb_step_params, Z, theta, C_clutter, C_tracks, gate, log_no
 
 def glmb_step_host(prm: glmb_step_params, Z_host, theta_host, Z_dev, theta_dev, C_clutter,
                    C_tracks, gate, log_norm, flags, C_clutter_host, C_tracks_host, gate_host,
-                   log_norm_host, flags_host, stream=None):
-    """Host tensors (pinned recommended) in and out; synchronous."""
+                   log_norm_host, flags_host, stream=None, copy_stream=None):
+    """Host tensors (pinned recommended) in and out; synchronous.  copy_stream: a second
+    torch.cuda.Stream for the overlapped read-back (see glmb.h)."""
     hp = lambda t: None if t is None else t.data_ptr()
     M = Z_host.shape[0]
     _check(load().glmb_step_host(C.byref(prm), hp(Z_host), M, hp(theta_host), _ptr(Z_dev),
                                  _ptr(theta_dev), _ptr(C_clutter), _ptr(C_tracks), C_tracks.shape[1],
                                  _ptr(gate), gate.shape[1], _ptr(log_norm), _ptr(flags),
                                  hp(C_clutter_host), hp(C_tracks_host), hp(gate_host),
-                                 hp(log_norm_host), hp(flags_host), _stream(stream)))
+                                 hp(log_norm_host), hp(flags_host), _stream(stream),
+                                 None if copy_stream is None else copy_stream.cuda_stream))
 
 
 def glmb_philox_dump(seed, ctr, out, stream=None):

@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "../../include/glmb.h"
 #include "glmb_internal.h"
@@ -87,6 +88,17 @@ inline glmb_status from_cuda(cudaError_t e) { return e == cudaSuccess ? GLMB_OK 
     const glmb_status st_ = (expr);       \
     if (st_ != GLMB_OK) return st_;       \
   } while (0)
+
+// glmb_step_host with the C_k read-back overlapped: compat runs in track chunks
+// (the same per-column arithmetic as one launch -- C is bit-identical under any
+// split of the tracks), and each chunk's columns and gate words go back on
+// copy_stream while the next chunk computes.
+glmb_status step_host_overlapped(const glmb_step_params *prm, const float *Z_host, int32_t M,
+                                 const int32_t *theta_host, float *Z_dev, int32_t *theta_dev, float *C_clutter_dev,
+                                 float *C_tracks_dev, int64_t ldc, uint32_t *gate_dev, int64_t ldg,
+                                 float *log_norm_dev, uint32_t *flags_dev, float *C_clutter_host,
+                                 float *C_tracks_host, uint32_t *gate_host, float *log_norm_host,
+                                 uint32_t *flags_host, cudaStream_t s, cudaStream_t cs);
 
 }  // namespace
 
@@ -247,8 +259,13 @@ glmb_status glmb_step_host(const glmb_step_params *prm, const float *Z_host, int
                            float *Z_dev, int32_t *theta_dev, float *C_clutter_dev, float *C_tracks_dev, int64_t ldc,
                            uint32_t *gate_dev, int64_t ldg, float *log_norm_dev, uint32_t *flags_dev,
                            float *C_clutter_host, float *C_tracks_host, uint32_t *gate_host, float *log_norm_host,
-                           uint32_t *flags_host, glmb_stream_t stream) {
+                           uint32_t *flags_host, glmb_stream_t stream, glmb_stream_t copy_stream) {
   if (prm == nullptr || M < 0) return GLMB_ERR_INVALID_ARG;
+  if (copy_stream != nullptr && stream != nullptr)
+    return step_host_overlapped(prm, Z_host, M, theta_host, Z_dev, theta_dev, C_clutter_dev, C_tracks_dev, ldc,
+                                gate_dev, ldg, log_norm_dev, flags_dev, C_clutter_host, C_tracks_host, gate_host,
+                                log_norm_host, flags_host, reinterpret_cast<cudaStream_t>(stream),
+                                reinterpret_cast<cudaStream_t>(copy_stream));
   if (M > 0 && (Z_host == nullptr || theta_host == nullptr || Z_dev == nullptr || theta_dev == nullptr))
     return GLMB_ERR_INVALID_ARG;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -533,3 +550,95 @@ glmb_status glmb_normals_dump(uint64_t seed, const uint32_t *ctr, int32_t N, flo
 }
 
 }  // extern "C"
+
+namespace {
+
+glmb_status step_host_overlapped(const glmb_step_params *prm, const float *Z_host, int32_t M,
+                                 const int32_t *theta_host, float *Z_dev, int32_t *theta_dev, float *C_clutter_dev,
+                                 float *C_tracks_dev, int64_t ldc, uint32_t *gate_dev, int64_t ldg,
+                                 float *log_norm_dev, uint32_t *flags_dev, float *C_clutter_host,
+                                 float *C_tracks_host, uint32_t *gate_host, float *log_norm_host,
+                                 uint32_t *flags_host, cudaStream_t s, cudaStream_t cs) {
+  const glmb_particles &all = prm->tracks;
+  GLMB_TRY(check_particles(&all, true, true));
+  const int32_t T = prm->n_survivors, Tk = all.n_tracks;
+  if (T < 0 || T > Tk) return GLMB_ERR_INVALID_ARG;
+  if (M > 0 && (Z_host == nullptr || theta_host == nullptr || Z_dev == nullptr || theta_dev == nullptr))
+    return GLMB_ERR_INVALID_ARG;
+  GLMB_TRY(bind_stream(s, nullptr));
+  if (M > 0) {
+    if (cudaMemcpyAsync(Z_dev, Z_host, sizeof(float) * 2 * M, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(theta_dev, theta_host, sizeof(int32_t) * M, cudaMemcpyHostToDevice, s) != cudaSuccess)
+      return GLMB_ERR_CUDA;
+  }
+  auto rows = [&](int32_t r0, int32_t r1) {
+    glmb_particles v = all;
+    v.n_tracks = r1 - r0;
+    const int64_t off = static_cast<int64_t>(r0) * all.ld;
+    if (Tk > 0) {
+      v.x = all.x + off; v.y = all.y + off; v.v = all.v + off;
+      v.psi = all.psi + off; v.omega = all.omega + off; v.w = all.w + off;
+    }
+    return v;
+  };
+  glmb_particles surv = rows(0, T), births = rows(T, Tk);
+  glmb_stream_t st = reinterpret_cast<glmb_stream_t>(s);
+  GLMB_TRY(glmb_predict(&surv, &surv, prm->gid, prm->dt, prm->sigma_a, prm->sigma_w, prm->seed, prm->step, st));
+  GLMB_TRY(glmb_birth(&births, prm->gid ? prm->gid + T : nullptr, prm->birth_mean, prm->birth_chol, prm->seed,
+                      prm->step, st));
+  // compat chunks: GLMB_HOST_CHUNKS (1..4, default 1: one launch, its read-back overlapping
+  // reweight; more chunks overlap the read-back with compat too but pay a partial wave each)
+  static const int chunks_env = [] {
+    const char *e = std::getenv("GLMB_HOST_CHUNKS");
+    const int v = e ? std::atoi(e) : 1;
+    return v >= 1 && v <= 4 ? v : 1;
+  }();
+  constexpr int kMaxChunks = 4;
+  const int kChunks = chunks_env;
+  cudaEvent_t ev[kMaxChunks] = {};
+  glmb_status status = GLMB_OK;
+  const int32_t per = (Tk + kChunks - 1) / kChunks;
+  for (int c = 0; c < kChunks && status == GLMB_OK; ++c) {
+    const int32_t r0 = std::min(Tk, c * per), r1 = std::min(Tk, r0 + per);
+    if (r1 <= r0 && c > 0) break;
+    glmb_particles v = rows(r0, r1);
+    status = glmb_compat(&v, Z_dev, M, prm->Rxx, prm->Rxy, prm->Ryy, prm->p_d, prm->kappa, prm->gamma,
+                         c == 0 ? C_clutter_dev : nullptr, C_tracks_dev + static_cast<int64_t>(r0) * ldc, ldc,
+                         gate_dev + static_cast<int64_t>(r0) * ldg, ldg, st);
+    if (status != GLMB_OK || M == 0 || r1 <= r0) continue;
+    if (cudaEventCreateWithFlags(&ev[c], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventRecord(ev[c], s) != cudaSuccess || cudaStreamWaitEvent(cs, ev[c], 0) != cudaSuccess) {
+      status = GLMB_ERR_CUDA;
+      break;
+    }
+    if (C_tracks_host &&
+        cudaMemcpyAsync(C_tracks_host + static_cast<int64_t>(r0) * ldc, C_tracks_dev + static_cast<int64_t>(r0) * ldc,
+                        sizeof(float) * (r1 - r0) * ldc, cudaMemcpyDeviceToHost, cs) != cudaSuccess)
+      status = GLMB_ERR_CUDA;
+    if (gate_host &&
+        cudaMemcpyAsync(gate_host + static_cast<int64_t>(r0) * ldg, gate_dev + static_cast<int64_t>(r0) * ldg,
+                        sizeof(uint32_t) * (r1 - r0) * ldg, cudaMemcpyDeviceToHost, cs) != cudaSuccess)
+      status = GLMB_ERR_CUDA;
+  }
+  if (status == GLMB_OK)
+    status = glmb_reweight(&all, all.w, Z_dev, M, prm->Rxx, prm->Rxy, prm->Ryy, theta_dev, prm->col_offset,
+                           log_norm_dev, flags_dev, st);
+  if (status == GLMB_OK) {
+    if (M > 0 && C_clutter_host && C_clutter_dev &&
+        cudaMemcpyAsync(C_clutter_host, C_clutter_dev, sizeof(float) * M, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+      status = GLMB_ERR_CUDA;
+    if (Tk > 0 && log_norm_host &&
+        cudaMemcpyAsync(log_norm_host, log_norm_dev, sizeof(float) * Tk, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+      status = GLMB_ERR_CUDA;
+    if (Tk > 0 && flags_host &&
+        cudaMemcpyAsync(flags_host, flags_dev, sizeof(uint32_t) * Tk, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+      status = GLMB_ERR_CUDA;
+  }
+  const bool ok_sync = cudaStreamSynchronize(s) == cudaSuccess && cudaStreamSynchronize(cs) == cudaSuccess;
+  for (int c = 0; c < kMaxChunks; ++c)
+    if (ev[c]) cudaEventDestroy(ev[c]);
+  if (status == GLMB_OK && !ok_sync) status = GLMB_ERR_CUDA;
+  return status;
+}
+
+}  // namespace

@@ -373,6 +373,21 @@ def test_step_composition_and_host_entry(L):
     np.testing.assert_array_equal(Ct_h.numpy()[:, :M], b.out.C_tracks.cpu().numpy()[:, :M])
     np.testing.assert_array_equal(G_h.numpy(), b.out.gate.cpu().numpy())
     np.testing.assert_array_equal(ln_h.numpy(), b.out.log_norm.cpu().numpy())
+    # the overlapped read-back (compat in track chunks, D2H on a second stream) is identical
+    d = GlmbStep(s)
+    Ct2, G2, ln2, fl2, Cc2 = (torch.zeros_like(Ct_h).pin_memory(), torch.zeros_like(G_h).pin_memory(),
+                              torch.zeros_like(ln_h).pin_memory(), torch.zeros_like(fl_h).pin_memory(),
+                              torch.zeros_like(Cc_h).pin_memory())
+    st, cs = torch.cuda.Stream(), torch.cuda.Stream()
+    L.glmb_step_host(d.step_params(0), Zh, th, torch.empty(M, 2, device="cuda"),
+                     torch.empty(M, dtype=torch.int32, device="cuda"), d.out.C_clutter, d.out.C_tracks,
+                     d.out.gate, d.out.log_norm, d.out.flags, Cc2, Ct2, G2, ln2, fl2, stream=st, copy_stream=cs)
+    np.testing.assert_array_equal(Ct2.numpy()[:, :M], Ct_h.numpy()[:, :M])
+    np.testing.assert_array_equal(G2.numpy(), G_h.numpy())
+    np.testing.assert_array_equal(ln2.numpy(), ln_h.numpy())
+    np.testing.assert_array_equal(fl2.numpy(), fl_h.numpy())
+    np.testing.assert_array_equal(Cc2.numpy()[:M], Cc_h.numpy()[:M])
+    np.testing.assert_array_equal(d.particles.data.cpu().numpy(), c.particles.data.cpu().numpy())
 
 
 def test_status_errors(L):
