@@ -414,6 +414,19 @@ def main():
         thbuf = torch.zeros(st.M_max, dtype=torch.int32, device=dev)
         C_full = torch.empty(per * world, st.ldc, device=dev)
         G_full = torch.empty(per * world, st.ldg, dtype=torch.int32, device=dev)
+    # fused compat + all-gather: compat stores each column into every rank's symmetric-memory
+    # copy of C_k over NVLink, then one device barrier (GLMB_FUSED_GATHER=0: NCCL all-gather)
+    symm_cols = None
+    gather = "none (one rank)"
+    if world > 1:
+        gather = "NCCL all_gather_into_tensor of the column blocks"
+        if os.environ.get("GLMB_FUSED_GATHER", "1") != "0":
+            try:
+                from paper_2512_06230_b200.symm import SymmetricColumns
+                symm_cols = SymmetricColumns(per, st.ldc, st.ldg, dev)
+                gather = "fused: compat stores its columns into every rank's symmetric-memory C_k (NVLink), device barrier"
+            except Exception as e:  # noqa: BLE001
+                print(f"[bench] symmetric memory unavailable ({e}); NCCL all-gather", file=sys.stderr)
 
     ev = lambda: torch.cuda.Event(enable_timing=True)
     stage_names = ["predict", "birth", "compat", "reweight"]
@@ -444,10 +457,15 @@ def main():
                 st.reweight(k, side, Z=Zk, theta=thk, out_of_place=True)
                 done = ev()
                 done.record(side)
-            L.glmb_compat(p_now, Zk, st.R, st.cfg.p_d, st.cfg.kappa, st.cfg.gamma,
-                          st.out.C_clutter, st.out.C_tracks, st.out.gate, stream)
+            if symm_cols is not None:
+                symm_cols.compat(p_now, Zk, st.R, st.cfg.p_d, st.cfg.kappa, st.cfg.gamma, st.out.C_clutter, stream)
+            else:
+                L.glmb_compat(p_now, Zk, st.R, st.cfg.p_d, st.cfg.kappa, st.cfg.gamma,
+                              st.out.C_clutter, st.out.C_tracks, st.out.gate, stream)
             stream.wait_event(done)
-            if world > 1:
+            if symm_cols is not None:
+                symm_cols.barrier(stream)
+            elif world > 1:
                 allgather_columns(st.out.C_tracks, C_full)
                 allgather_columns(st.out.gate, G_full)
 
@@ -572,6 +590,7 @@ def main():
         stage_ms=stage_ms, sm_count=L.glmb_sm_count(local), clocks=sampler.summary(),
         T_surv=st.T_surv, B_local=st.B_local, T_local=st.T_local, P=st.P, M_mean=float(np.mean(Ms)),
         traffic=compat_traffic(st.T_local, st.P, len(scene.Z[0])), e2e=e2e, cpu=cpu)
+    line["config"]["gather"] = gather
     if update is not None:
         line["glmb_update"] = update
     if convoy is not None:

@@ -175,6 +175,28 @@ glmb_status glmb_compat(const glmb_particles *trk, const float *Z, int32_t M,
                         int64_t ldg, glmb_stream_t stream);
 
 /* ---------------------------------------------------------------------
+ * glmb_compat_peers -- glmb_compat fused with the all-gather of C_k's column
+ * blocks across ranks: the epilogue stores column j of this
+ * rank's tracks to row row0 + j of EVERY peer_C[r] [.][ldc] and its gate words
+ * to row row0 + j of every peer_G[r] [.][ldg], r < n_peers, instead of a local
+ * C_tracks / gate -- e.g. the peers' symmetric-memory buffers mapped over
+ * NVLink, so the transfer overlaps the likelihood tile by tile and no
+ * collective runs afterwards (the caller orders the ranks with a barrier
+ * before reading the gathered C).  peer_C / peer_G: DEVICE arrays of n_peers
+ * device pointers (1 <= n_peers <= 64).  Same arithmetic as glmb_compat, so
+ * the gathered C is bit-identical to the single-GPU C.  C_clutter is written
+ * locally (may be NULL).  Errors as glmb_compat, plus INVALID_ARG on bad
+ * n_peers / row0 / NULL pointer arrays.
+ * --------------------------------------------------------------------- */
+glmb_status glmb_compat_peers(const glmb_particles *trk, const float *Z,
+                              int32_t M, float Rxx, float Rxy, float Ryy,
+                              float p_d, float kappa, float gamma,
+                              float *C_clutter, float *const *peer_C,
+                              uint32_t *const *peer_G, int32_t n_peers,
+                              int64_t row0, int64_t ldc, int64_t ldg,
+                              glmb_stream_t stream);
+
+/* ---------------------------------------------------------------------
  * glmb_reweight -- particle update under theta_k (§Approach).
  *
  * theta: [M] int32, theta[i] = 0 means clutter, c >= 1 means C column c

@@ -63,7 +63,7 @@ EXPORTED = ["glmb_version", "glmb_status_string", "glmb_init", "glmb_sm_count", 
             "glmb_philox_dump", "glmb_normals_dump", "glmb_death_prob", "glmb_compat_rows",
             "glmb_assoc_sample", "glmb_dedup", "glmb_prune", "glmb_assoc_pairs_workspace_size",
             "glmb_assoc_pairs", "glmb_reweight_pairs", "glmb_resample", "glmb_next_parents",
-            "glmb_map_estimate", "glmb_update"]
+            "glmb_map_estimate", "glmb_update", "glmb_compat_peers"]
 
 
 def load(path: str = LIB_PATH):
@@ -101,6 +101,8 @@ def load(path: str = LIB_PATH):
         L.glmb_next_parents.argtypes = [i32, vp, vp, vp, i32, i32, i32, i32, vp, i32, vp, vp, vp]
         L.glmb_map_estimate.argtypes = [vp, vp, i32, PP, vp, vp]
         L.glmb_update.argtypes = [C.POINTER(glmb_update_params), vp]
+        L.glmb_compat_peers.argtypes = [PP, vp, i32, f32, f32, f32, f32, f32, f32, vp, vp, vp, i32, i64, i64,
+                                        i64, vp]
         L.glmb_prune.argtypes = [i32, vp, vp, C.c_double, i32, vp, vp, vp, vp, vp]
         L.glmb_assoc_pairs_workspace_size.argtypes = [i32, i32, i32]
         L.glmb_assoc_pairs_workspace_size.restype = C.c_size_t
@@ -360,3 +362,13 @@ def glmb_map_estimate(n_kept, pair_of0, new_set: Particles, est, stream=None):
 def glmb_update(params: "glmb_update_params", stream=None):
     """The whole update after C_k in one C call (include/glmb.h glmb_update)."""
     _check(load().glmb_update(C.byref(params), _stream(stream)))
+
+
+def glmb_compat_peers(trk: Particles, Z, R, p_d, kappa, gamma, C_clutter, peer_C, peer_G, row0, ldc, ldg,
+                      stream=None):
+    """Fused compat + all-gather: peer_C / peer_G are device int64 tensors [n_peers] of device pointers
+    (e.g. torch symmetric memory's buffer_ptrs_dev); column j goes to row row0 + j of every peer."""
+    t = trk.struct()
+    _check(load().glmb_compat_peers(C.byref(t), _ptr(Z), Z.shape[0], R[0], R[1], R[2], p_d, kappa, gamma,
+                                    _ptr(C_clutter), _ptr(peer_C), _ptr(peer_G), peer_C.shape[0], int(row0),
+                                    int(ldc), int(ldg), _stream(stream)))

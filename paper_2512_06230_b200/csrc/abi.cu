@@ -200,6 +200,40 @@ glmb_status glmb_compat(const glmb_particles *trk, const float *Z, int32_t M, fl
   return from_cuda(glmb::launch_compat(a, s));
 }
 
+glmb_status glmb_compat_peers(const glmb_particles *trk, const float *Z, int32_t M, float Rxx, float Rxy,
+                              float Ryy, float p_d, float kappa, float gamma, float *C_clutter,
+                              float *const *peer_C, uint32_t *const *peer_G, int32_t n_peers, int64_t row0,
+                              int64_t ldc, int64_t ldg, glmb_stream_t stream) {
+  GLMB_TRY(check_particles(trk, true, false));
+  if (M < 0 || n_peers < 1 || n_peers > 64 || row0 < 0) return GLMB_ERR_INVALID_ARG;
+  if (!spd(Rxx, Rxy, Ryy) || !(p_d > 0.f && p_d <= 1.f) || !(kappa >= 0.f) || !(gamma >= 1e-30f))
+    return GLMB_ERR_INVALID_ARG;
+  if (M == 0) return GLMB_OK;
+  if (Z == nullptr || peer_C == nullptr || peer_G == nullptr) return GLMB_ERR_INVALID_ARG;
+  if ((reinterpret_cast<uintptr_t>(Z) & 7u) != 0) return GLMB_ERR_ALIGNMENT;
+  if (ldc < M || ldg < (M + 31) / 32) return GLMB_ERR_INVALID_ARG;
+  const int32_t T = trk->n_tracks;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  GLMB_TRY(bind_stream(s, nullptr));
+  if (T == 0) return from_cuda(glmb::launch_clutter_fill(C_clutter, M, kappa, s));
+  const double rxx = Rxx, rxy = Rxy, ryy = Ryy;
+  const double det = rxx * ryy - rxy * rxy;
+  const double s0 = std::sqrt(0.5 * 1.4426950408889634074);
+  const double a1 = s0 * std::sqrt(ryy / det);
+  glmb::CompatArgs a{};
+  a.x = trk->x; a.y = trk->y; a.w = trk->w; a.ld = trk->ld; a.T = T; a.P = trk->n_particles;
+  a.Z = Z; a.M = M;
+  a.a1 = static_cast<float>(a1); a.a2 = static_cast<float>(-a1 * (rxy / ryy));
+  a.b2 = static_cast<float>(s0 / std::sqrt(ryy));
+  a.norm = static_cast<float>(1.0 / (2.0 * 3.14159265358979323846 * std::sqrt(det)));
+  a.p_d = p_d; a.kappa = kappa; a.gamma = gamma;
+  a.C_clutter = C_clutter; a.C_tracks = nullptr; a.ldc = ldc; a.gate = nullptr; a.ldg = ldg;
+  a.peer_C = peer_C; a.peer_G = peer_G; a.n_peers = n_peers; a.peer_row0 = row0;
+  glmb::compat_plan(M, a.P, &a.K, &a.NW, &a.CL, &a.n_mtiles);
+  if (static_cast<int64_t>(T) * a.n_mtiles * a.CL > 0x7fffffffLL) return GLMB_ERR_INVALID_ARG;
+  return from_cuda(glmb::launch_compat(a, s));
+}
+
 glmb_status glmb_reweight(const glmb_particles *trk, float *w_out, const float *Z, int32_t M, float Rxx, float Rxy,
                           float Ryy, const int32_t *theta, int32_t col_offset, float *log_norm, uint32_t *flags,
                           glmb_stream_t stream) {

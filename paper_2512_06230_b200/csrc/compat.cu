@@ -365,9 +365,18 @@ __global__ void __launch_bounds__(32 * NW, min_blocks<NW, K>()) compat_kernel(co
       const bool valid = i < a.M;
       const float L = m.tot[k] * a.norm;
       const bool g = valid && (L >= a.gamma);
-      if (valid) a.C_tracks[static_cast<int64_t>(j) * a.ldc + i] = g ? a.p_d * L : 0.0f;
+      const float c = g ? a.p_d * L : 0.0f;
       const uint32_t word = __ballot_sync(0xffffffffu, g);
-      if (lane == 0) a.gate[static_cast<int64_t>(j) * a.ldg + ((wbase + k * 32) >> 5)] = word;
+      if (a.n_peers == 0) {
+        if (valid) a.C_tracks[static_cast<int64_t>(j) * a.ldc + i] = c;
+        if (lane == 0) a.gate[static_cast<int64_t>(j) * a.ldg + ((wbase + k * 32) >> 5)] = word;
+      } else {  // fused all-gather: this column goes straight into every rank's copy of C_k
+        const int64_t row = a.peer_row0 + j;
+        for (int r = 0; r < a.n_peers; ++r) {
+          if (valid) a.peer_C[r][row * a.ldc + i] = c;
+          if (lane == 0) a.peer_G[r][row * a.ldg + ((wbase + k * 32) >> 5)] = word;
+        }
+      }
       if (j == 0 && a.C_clutter != nullptr && valid) a.C_clutter[i] = a.kappa;
     }
   }

@@ -45,6 +45,13 @@ struct CompatArgs {
   int32_t NW;        // warps per CTA
   int32_t CL;        // CTAs (particle chunks) per (track, measurement tile): cluster size
   int32_t track_major;  // unit order: 1 = a track's measurement tiles adjacent, 0 = tile-major
+  // fused all-gather (glmb_compat_peers): n_peers > 0 writes column j to row peer_row0 + j of
+  // every peer_C[r] / peer_G[r] (device arrays of n_peers pointers, e.g. symmetric memory
+  // mapped over NVLink) instead of C_tracks / gate
+  float *const *peer_C;
+  uint32_t *const *peer_G;
+  int32_t n_peers;
+  int64_t peer_row0;
 };
 
 struct ReweightArgs {

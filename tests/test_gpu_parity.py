@@ -457,3 +457,33 @@ def test_reweight_out_of_place_matches_in_place(L, orc, P):
     np.testing.assert_array_equal(_host(la), _host(lb))
     rw, _, _ = orc.reweight(data[0], data[1], data[5], Z, (1, 0, 1), theta)
     check_weights(_host(w_out), rw)
+
+
+def test_compat_peers_fused_gather(L):
+    """glmb_compat_peers (compat fused with the column all-gather): with one destination it
+    equals glmb_compat; with the tracks split into two blocks each written to two destination
+    buffers (two 'ranks' on one GPU, no rank waits on another) both buffers hold the whole
+    single-launch C_k and gate, bit for bit."""
+    import torch
+    from paper_2512_06230_b200._lib import Particles
+    from paper_2512_06230_b200 import scenes
+    sc = scenes.make_scene(1, steps=1)
+    cfg = sc.cfg
+    p = Particles.from_arrays([sc.x, sc.y, sc.v, sc.psi, sc.omega, sc.w])
+    Z = _dev(sc.Z[0])
+    T, M = p.T, Z.shape[0]
+    ldc, ldg = (M + 31) // 32 * 32, (M + 31) // 32
+    C0 = torch.zeros(T, ldc, device="cuda")
+    G0 = torch.zeros(T, ldg, dtype=torch.int32, device="cuda")
+    L.glmb_compat(p, Z, cfg.R, cfg.p_d, cfg.kappa, cfg.gamma, None, C0, G0)
+    bufs = [(torch.full((T, ldc), -1.0, device="cuda"), torch.full((T, ldg), -1, dtype=torch.int32, device="cuda"))
+            for _ in range(2)]
+    ptrs = lambda k: torch.tensor([b[k].data_ptr() for b in bufs], dtype=torch.int64, device="cuda")
+    half = T // 2
+    for r0, r1 in ((0, half), (half, T)):
+        L.glmb_compat_peers(p.rows(r0, r1), Z, cfg.R, cfg.p_d, cfg.kappa, cfg.gamma, None, ptrs(0), ptrs(1), r0,
+                            ldc, ldg)
+    torch.cuda.synchronize()
+    for Cb, Gb in bufs:
+        np.testing.assert_array_equal(Cb.cpu().numpy()[:, :M], C0.cpu().numpy()[:, :M])
+        np.testing.assert_array_equal(Gb.cpu().numpy(), G0.cpu().numpy())
