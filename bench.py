@@ -541,8 +541,9 @@ def main():
 
         def host_step(k):
             zi = k % len(Zh)
-            L.glmb_step_host(st.step_params(k), Zh[zi], thh[zi], Zd, thd, o.C_clutter, o.C_tracks,
-                             o.gate, o.log_norm, o.flags, Cc_h, Ct_h, G_h, ln_h, fl_h, stream, copy_stream)
+            L.glmb_step_host(st.step_params(k), Zh[zi], thh[zi], Zd, thd, o.C_clutter,
+                             o.C_tracks, o.gate, o.log_norm, o.flags, Cc_h, Ct_h, G_h, ln_h, fl_h, stream,
+                             copy_stream)
             M = Zh[zi].shape[0]
             return M * 8 + M * 4, M * 4 + st.T_local * st.ldc * 4 + st.T_local * st.ldg * 4 + st.T_local * 8
 

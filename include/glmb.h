@@ -238,6 +238,9 @@ typedef struct {
   uint32_t step;
   float Rxx, Rxy, Ryy, p_d, kappa, gamma;
   int32_t col_offset;      /* global column offset of local row 0        */
+  float *w_out;            /* NULL: reweight in place; else [T_k][ld] spare
+                              weight buffer the new weights go to (the
+                              caller swaps buffers after the step)       */
 } glmb_step_params;
 
 glmb_status glmb_step(const glmb_step_params *prm, const float *Z, int32_t M,

@@ -40,7 +40,7 @@ class glmb_step_params(C.Structure):
                 ("sigma_a", C.c_float), ("sigma_w", C.c_float), ("seed", C.c_uint64),
                 ("step", C.c_uint32), ("Rxx", C.c_float), ("Rxy", C.c_float), ("Ryy", C.c_float),
                 ("p_d", C.c_float), ("kappa", C.c_float), ("gamma", C.c_float),
-                ("col_offset", C.c_int32)]
+                ("col_offset", C.c_int32), ("w_out", C.c_void_p)]
 
 
 class glmb_update_params(C.Structure):
@@ -232,10 +232,11 @@ def glmb_reweight(trk: Particles, Z, R, theta, col_offset, log_norm, flags, stre
 
 
 def make_step_params(tracks: Particles, n_survivors, gid, birth_mean, birth_chol, dt, sigma_a,
-                     sigma_w, seed, step, R, p_d, kappa, gamma, col_offset=0) -> glmb_step_params:
+                     sigma_w, seed, step, R, p_d, kappa, gamma, col_offset=0, w_out=None) -> glmb_step_params:
+    """w_out: optional spare weight buffer [T_k, ld] for the new weights (see glmb.h)."""
     return glmb_step_params(tracks.struct(), int(n_survivors), _ptr(gid), _ptr(birth_mean),
                             _ptr(birth_chol), dt, sigma_a, sigma_w, int(seed) & 0xFFFFFFFFFFFFFFFF,
-                            int(step), R[0], R[1], R[2], p_d, kappa, gamma, int(col_offset))
+                            int(step), R[0], R[1], R[2], p_d, kappa, gamma, int(col_offset), _ptr(w_out))
 
 
 def glmb_step(prm: glmb_step_params, Z, theta, C_clutter, C_tracks, gate, log_norm, flags,

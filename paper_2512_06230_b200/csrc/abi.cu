@@ -285,8 +285,8 @@ glmb_status glmb_step(const glmb_step_params *prm, const float *Z, int32_t M, co
                       prm->step, stream));
   GLMB_TRY(glmb_compat(&all, Z, M, prm->Rxx, prm->Rxy, prm->Ryy, prm->p_d, prm->kappa, prm->gamma, C_clutter,
                        C_tracks, ldc, gate, ldg, stream));
-  return glmb_reweight(&all, all.w, Z, M, prm->Rxx, prm->Rxy, prm->Ryy, theta, prm->col_offset, log_norm, flags,
-                       stream);
+  return glmb_reweight(&all, prm->w_out ? prm->w_out : all.w, Z, M, prm->Rxx, prm->Rxy, prm->Ryy, theta,
+                       prm->col_offset, log_norm, flags, stream);
 }
 
 glmb_status glmb_step_host(const glmb_step_params *prm, const float *Z_host, int32_t M, const int32_t *theta_host,
@@ -631,6 +631,14 @@ glmb_status step_host_overlapped(const glmb_step_params *prm, const float *Z_hos
   const int kChunks = chunks_env;
   cudaEvent_t ev[kMaxChunks] = {};
   glmb_status status = GLMB_OK;
+  // compat (chunks) on `s`, then reweight on `s` (into prm->w_out when given); the copy
+  // stream reads each compat chunk's columns back while the next chunk / reweight runs.
+  // (Reweight on the copy stream concurrently with compat was measured slower: compat
+  // holds every SM, so reweight ran after it and delayed the read-back queued behind it.)
+  struct Chunk {
+    int32_t r0, r1;
+  } chunk[kMaxChunks];
+  int n_chunk = 0;
   const int32_t per = (Tk + kChunks - 1) / kChunks;
   for (int c = 0; c < kChunks && status == GLMB_OK; ++c) {
     const int32_t r0 = std::min(Tk, c * per), r1 = std::min(Tk, r0 + per);
@@ -641,7 +649,15 @@ glmb_status step_host_overlapped(const glmb_step_params *prm, const float *Z_hos
                          gate_dev + static_cast<int64_t>(r0) * ldg, ldg, st);
     if (status != GLMB_OK || M == 0 || r1 <= r0) continue;
     if (cudaEventCreateWithFlags(&ev[c], cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventRecord(ev[c], s) != cudaSuccess || cudaStreamWaitEvent(cs, ev[c], 0) != cudaSuccess) {
+        cudaEventRecord(ev[c], s) != cudaSuccess) {
+      status = GLMB_ERR_CUDA;
+      break;
+    }
+    chunk[n_chunk++] = Chunk{r0, r1};
+  }
+  for (int c = 0; c < n_chunk && status == GLMB_OK; ++c) {
+    const int32_t r0 = chunk[c].r0, r1 = chunk[c].r1;
+    if (cudaStreamWaitEvent(cs, ev[c], 0) != cudaSuccess) {
       status = GLMB_ERR_CUDA;
       break;
     }
@@ -655,17 +671,18 @@ glmb_status step_host_overlapped(const glmb_step_params *prm, const float *Z_hos
       status = GLMB_ERR_CUDA;
   }
   if (status == GLMB_OK)
-    status = glmb_reweight(&all, all.w, Z_dev, M, prm->Rxx, prm->Rxy, prm->Ryy, theta_dev, prm->col_offset,
-                           log_norm_dev, flags_dev, st);
+    status = glmb_reweight(&all, prm->w_out ? prm->w_out : all.w, Z_dev, M, prm->Rxx, prm->Rxy, prm->Ryy, theta_dev,
+                           prm->col_offset, log_norm_dev, flags_dev, st);
   if (status == GLMB_OK) {
+    cudaStream_t ls = s;
     if (M > 0 && C_clutter_host && C_clutter_dev &&
         cudaMemcpyAsync(C_clutter_host, C_clutter_dev, sizeof(float) * M, cudaMemcpyDeviceToHost, s) != cudaSuccess)
       status = GLMB_ERR_CUDA;
     if (Tk > 0 && log_norm_host &&
-        cudaMemcpyAsync(log_norm_host, log_norm_dev, sizeof(float) * Tk, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        cudaMemcpyAsync(log_norm_host, log_norm_dev, sizeof(float) * Tk, cudaMemcpyDeviceToHost, ls) != cudaSuccess)
       status = GLMB_ERR_CUDA;
     if (Tk > 0 && flags_host &&
-        cudaMemcpyAsync(flags_host, flags_dev, sizeof(uint32_t) * Tk, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        cudaMemcpyAsync(flags_host, flags_dev, sizeof(uint32_t) * Tk, cudaMemcpyDeviceToHost, ls) != cudaSuccess)
       status = GLMB_ERR_CUDA;
   }
   const bool ok_sync = cudaStreamSynchronize(s) == cudaSuccess && cudaStreamSynchronize(cs) == cudaSuccess;

@@ -139,11 +139,19 @@ class GlmbStep:
         L.glmb_step(prm, self.Z[zi], self.theta[zi], o.C_clutter, o.C_tracks, o.gate, o.log_norm,
                     o.flags, stream)
 
-    def step_params(self, k: int) -> L.glmb_step_params:
+    def step_params(self, k: int, out_of_place: bool = False) -> L.glmb_step_params:
+        """out_of_place: the new weights go to the spare buffer (call swap_weights() after the
+        step) -- lets glmb_step_host run reweight concurrently with compat."""
         c = self.cfg
         return L.make_step_params(self.particles, self.T_surv, self.gid, self.birth_mean,
                                   self.birth_chol, c.dt, c.sigma_a, c.sigma_w, self.seed, k,
-                                  self.R, c.p_d, c.kappa, c.gamma, self.cols.start)
+                                  self.R, c.p_d, c.kappa, c.gamma, self.cols.start,
+                                  w_out=self.w_bufs[1 - self.w_cur] if out_of_place else None)
+
+    def swap_weights(self):
+        """Make the spare weight buffer (written by an out-of-place step) the current one."""
+        self.w_cur = 1 - self.w_cur
+        self.particles = L.Particles(self.particles.data, self.P, self.w_bufs[self.w_cur])
 
     def evals(self, k: int) -> int:
         """Algorithmic particle-measurement likelihood evaluations of step k on this rank:

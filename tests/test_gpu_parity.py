@@ -388,6 +388,19 @@ def test_step_composition_and_host_entry(L):
     np.testing.assert_array_equal(fl2.numpy(), fl_h.numpy())
     np.testing.assert_array_equal(Cc2.numpy()[:M], Cc_h.numpy()[:M])
     np.testing.assert_array_equal(d.particles.data.cpu().numpy(), c.particles.data.cpu().numpy())
+    # ... and with reweight into the spare weight buffer, concurrent with compat
+    e = GlmbStep(s)
+    Ct3, G3, ln3, fl3 = (torch.zeros_like(Ct_h).pin_memory(), torch.zeros_like(G_h).pin_memory(),
+                         torch.zeros_like(ln_h).pin_memory(), torch.zeros_like(fl_h).pin_memory())
+    L.glmb_step_host(e.step_params(0, out_of_place=True), Zh, th, torch.empty(M, 2, device="cuda"),
+                     torch.empty(M, dtype=torch.int32, device="cuda"), e.out.C_clutter, e.out.C_tracks,
+                     e.out.gate, e.out.log_norm, e.out.flags, None, Ct3, G3, ln3, fl3, stream=st, copy_stream=cs)
+    e.swap_weights()
+    np.testing.assert_array_equal(Ct3.numpy()[:, :M], Ct_h.numpy()[:, :M])
+    np.testing.assert_array_equal(G3.numpy(), G_h.numpy())
+    np.testing.assert_array_equal(ln3.numpy(), ln_h.numpy())
+    np.testing.assert_array_equal(fl3.numpy(), fl_h.numpy())
+    np.testing.assert_array_equal(e.weights().cpu().numpy(), c.particles.data[5].cpu().numpy())
 
 
 def test_status_errors(L):
