@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--h-up", type=int, default=100)
     ap.add_argument("--h-max", type=int, default=100)
     ap.add_argument("--no-convoy", action="store_true", help="skip the paper-shaped convoy run (f4)")
+    ap.add_argument("--no-graphs", action="store_true", help="skip the CUDA-graph timing of configs 0-2")
     return ap.parse_args()
 
 
@@ -345,6 +346,49 @@ def bench_update(a, st, scene, cfg, dev, stream, L):
             "note": "device-resident; no host round trip inside (device counts n_kept / n_pairs)"}
 
 
+# ------------------------------------------------------------------ configs 0-2 (launch-bound): CUDA graphs
+def bench_graphs(dev, reps: int = 200):
+    """the small configs are launch-bound; one whole step (glmb_step: predict,
+    birth, compat, reweight) is captured once in a CUDA graph and replayed.  Reports us/step
+    eager (four C-ABI launches from Python) and replayed, and the replayed evals/s."""
+    import torch
+    from paper_2512_06230_b200.scenes import make_scene
+    from paper_2512_06230_b200.step import GlmbStep
+    out = {}
+    for cfg_id in (0, 1, 2):
+        scene = make_scene(cfg_id, steps=1)
+        st = GlmbStep(scene, device=dev)
+        s = torch.cuda.Stream(device=dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            for _ in range(3):
+                st.run(0, s)
+            s.synchronize()
+            e0.record(s)
+            for _ in range(reps):
+                st.run(0, s)
+            e1.record(s)
+            s.synchronize()
+            eager = e0.elapsed_time(e1) / reps
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                st.run(0, s)
+            for _ in range(3):
+                g.replay()
+            s.synchronize()
+            e0.record(s)
+            for _ in range(reps):
+                g.replay()
+            e1.record(s)
+            s.synchronize()
+            replay = e0.elapsed_time(e1) / reps
+        evals = st.evals(0)
+        out[f"cfg{cfg_id}"] = {"T_k": st.T_local, "P": st.P, "M": len(scene.Z[0]), "evals_per_step": evals,
+                               "us_per_step_eager": eager * 1e3, "us_per_step_graph": replay * 1e3,
+                               "evals_per_s_graph": evals / (replay * 1e-3)}
+    return out
+
+
 # ------------------------------------------------------------------ the paper's convoy (SURVEY §8f f4)
 def bench_convoy(dev):
     """The paper's own benchmark shape: N = 20 objects, D = 5, sigma = 0.25, delta = 2,
@@ -495,12 +539,18 @@ def main():
         dist.barrier(device_ids=[local])
     torch.cuda.synchronize(dev)
     t_start, t_end = ev(), ev()
+    step_marks = []
     with sampler:
         t_start.record(stream)
         for k in range(a.warmup, a.warmup + a.steps):
             one_step(k)
+            e = ev()
+            e.record(stream)
+            step_marks.append(e)
         t_end.record(stream)
         torch.cuda.synchronize(dev)
+    per_step = [(step_marks[0] if i == 0 else step_marks[i - 1]).elapsed_time(step_marks[i]) if i else
+                t_start.elapsed_time(step_marks[0]) for i in range(len(step_marks))]
     if world > 1:
         dist.barrier(device_ids=[local])
     elapsed_ms = t_start.elapsed_time(t_end)
@@ -520,6 +570,11 @@ def main():
         elapsed_ms, evals_total = float(tmax[0]), float(tsum[1])
     else:
         evals_total = float(evals_local)
+
+    # ---- launch-bound small configs: one whole step (glmb_step) captured in a CUDA graph
+    graphs = None
+    if world == 1 and not a.no_graphs:
+        graphs = bench_graphs(dev)
 
     # ---- end to end through the public C-ABI entry with host buffers (N=1 leg per rank)
     e2e = None
@@ -592,6 +647,10 @@ def main():
         T_surv=st.T_surv, B_local=st.B_local, T_local=st.T_local, P=st.P, M_mean=float(np.mean(Ms)),
         traffic=compat_traffic(st.T_local, st.P, len(scene.Z[0])), e2e=e2e, cpu=cpu)
     line["config"]["gather"] = gather
+    line["ms_per_step_p50"] = float(np.percentile(per_step, 50))
+    line["ms_per_step_p95"] = float(np.percentile(per_step, 95))
+    if graphs is not None:
+        line["small_configs_graph"] = graphs
     if update is not None:
         line["glmb_update"] = update
     if convoy is not None:

@@ -37,6 +37,17 @@ glmb_status check_device(int dev) {
 // Make the stream's device current in this library's runtime instance.
 glmb_status bind_stream(cudaStream_t s, int *dev_out) {
   int dev = 0;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (s != nullptr && cudaStreamIsCapturing(s, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone) {
+    // inside a CUDA-graph capture: no stream queries (they would invalidate the capture);
+    // the capturing thread's current device is the stream's
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+      cudaGetLastError();
+      return GLMB_ERR_CUDA;
+    }
+    if (dev_out) *dev_out = dev;
+    return check_device(dev);
+  }
   if (s != nullptr) {
     if (cudaStreamGetDevice(s, &dev) != cudaSuccess) {
       cudaGetLastError();

@@ -500,3 +500,25 @@ def test_compat_peers_fused_gather(L):
     for Cb, Gb in bufs:
         np.testing.assert_array_equal(Cb.cpu().numpy()[:, :M], C0.cpu().numpy()[:, :M])
         np.testing.assert_array_equal(Gb.cpu().numpy(), G0.cpu().numpy())
+
+
+def test_step_graph_capture(L):
+    """The C-ABI calls are CUDA-graph capturable (no stream queries during capture): a captured
+    glmb_step replays to the same outputs as the eager call."""
+    import torch
+    from paper_2512_06230_b200.scenes import make_scene
+    from paper_2512_06230_b200.step import GlmbStep
+    s = make_scene(1, steps=1)
+    a, b = GlmbStep(s), GlmbStep(s)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        a.run(0, st)
+        st.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            b.run(0, st)
+        g.replay()
+        st.synchronize()
+    for f in ("C_tracks", "gate", "log_norm", "flags"):
+        np.testing.assert_array_equal(getattr(a.out, f).cpu().numpy(), getattr(b.out, f).cpu().numpy())
+    np.testing.assert_array_equal(a.particles.data.cpu().numpy(), b.particles.data.cpu().numpy())
