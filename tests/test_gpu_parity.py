@@ -522,3 +522,32 @@ def test_step_graph_capture(L):
     for f in ("C_tracks", "gate", "log_norm", "flags"):
         np.testing.assert_array_equal(getattr(a.out, f).cpu().numpy(), getattr(b.out, f).cpu().numpy())
     np.testing.assert_array_equal(a.particles.data.cpu().numpy(), b.particles.data.cpu().numpy())
+
+
+@pytest.mark.parametrize("case", range(30))
+def test_step_kernels_random_tiny_shapes(L, orc, case):
+    """SURVEY §4 tier 5: random tiny T, P (multiple of 4), M, general SPD R, weights, gamma,
+    including T = 1 and M = 0 -- compat and reweight vs the oracle."""
+    r = np.random.default_rng(7000 + case)
+    T = int(r.integers(1, 12))
+    P = int(4 * r.integers(1, 80))
+    M = int(r.integers(0, 70)) if case % 7 else 0
+    sx, sy = r.uniform(0.2, 3.0, 2)
+    rho = r.uniform(-0.8, 0.8)
+    R = (float(np.float32(sx * sx)), float(np.float32(rho * sx * sy)), float(np.float32(sy * sy)))
+    cen = r.uniform(0, 60, (T, 2))
+    x = (cen[:, :1] + r.normal(0, r.uniform(0.3, 4), (T, P))).astype(np.float32)
+    y = (cen[:, 1:] + r.normal(0, r.uniform(0.3, 4), (T, P))).astype(np.float32)
+    w = r.dirichlet(np.ones(P) * r.uniform(0.1, 5), T).astype(np.float32)
+    Z = r.uniform(-5, 65, (M, 2)).astype(np.float32)
+    gamma = float(np.float32(10 ** r.uniform(-9, -3)))
+    p_d, kappa = float(np.float32(r.uniform(0.2, 1.0))), float(np.float32(10 ** r.uniform(-6, -2)))
+    if M:
+        C, G, Cc = _compat_gpu(L, x, y, w, Z, R, p_d, kappa, gamma)
+        check_compat(C, G, Cc, orc.compat(x, y, w, Z, R, p_d, kappa, gamma), gamma, M)
+    theta = r.integers(0, T + 1, M).astype(np.int32)
+    wg, ln, fl = _reweight_gpu(L, x, y, w, Z, R, theta)
+    rw, rln, rfl = orc.reweight(x, y, w, Z, R, theta)
+    check_weights(wg, rw)
+    check_log_norm(ln, rln)
+    np.testing.assert_array_equal(fl.view(np.uint32), rfl)
