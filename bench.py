@@ -591,38 +591,66 @@ def main():
         G_h = pin(torch.empty(st.T_local, st.ldg, dtype=torch.int32))
         ln_h = pin(torch.empty(st.T_local))
         fl_h = pin(torch.empty(st.T_local, dtype=torch.int32))
-        h2d = d2h = 0
-        copy_stream = torch.cuda.Stream(device=dev)   # read-back of C_k overlapped with compat chunks
+        copy_stream = torch.cuda.Stream(device=dev)   # dense read-back of C_k overlapping reweight
+        cap = st.T_local * M_max                       # device CSR capacity (never overflows)
+        rp_d = torch.empty(M_max + 1, dtype=torch.int32, device=dev)
+        col_d = torch.empty(cap, dtype=torch.int32, device=dev)
+        val_d = torch.empty(cap, dtype=torch.float32, device=dev)
+        lv_d = torch.empty(cap, dtype=torch.float64, device=dev)
+        cap_h = 64 * M_max                             # host CSR capacity (a second copy if exceeded)
+        rp_h = pin(torch.empty(M_max + 1, dtype=torch.int32))
+        col_h = pin(torch.empty(cap_h, dtype=torch.int32))
+        val_h = pin(torch.empty(cap_h))
 
-        def host_step(k):
+        def host_step_csr(k):
+            """C_k read back as the CSR of its gated entries (glmb_step_host_csr)."""
+            zi = k % len(Zh)
+            nnz = L.glmb_step_host_csr(st.step_params(k), Zh[zi], thh[zi], Zd, thd, o.C_tracks, o.gate,
+                                       o.log_norm, o.flags, rp_d, col_d, val_d, lv_d, rp_h, col_h, val_h, ln_h,
+                                       fl_h, stream)
+            M = Zh[zi].shape[0]
+            return M * 12, (M + 1) * 4 + nnz * 8 + st.T_local * 8
+
+        def host_step_dense(k):
+            """C_k read back dense (glmb_step_host)."""
             zi = k % len(Zh)
             L.glmb_step_host(st.step_params(k), Zh[zi], thh[zi], Zd, thd, o.C_clutter,
                              o.C_tracks, o.gate, o.log_norm, o.flags, Cc_h, Ct_h, G_h, ln_h, fl_h, stream,
                              copy_stream)
             M = Zh[zi].shape[0]
-            return M * 8 + M * 4, M * 4 + st.T_local * st.ldc * 4 + st.T_local * st.ldg * 4 + st.T_local * 8
+            return M * 12, M * 4 + st.T_local * st.ldc * 4 + st.T_local * st.ldg * 4 + st.T_local * 8
 
-        for k in range(a.warmup):
-            host_step(k)
-        if world > 1:
-            dist.barrier(device_ids=[local])
-        torch.cuda.synchronize(dev)
-        t0 = time.perf_counter()
-        for k in range(a.warmup, a.warmup + a.steps):
-            hb, db = host_step(k)
-            h2d += hb
-            d2h += db
-        e2e_s = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t[0])
+        def timed(fn):
+            h2d = d2h = 0
+            for k in range(a.warmup):
+                fn(k)
+            if world > 1:
+                dist.barrier(device_ids=[local])
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            for k in range(a.warmup, a.warmup + a.steps):
+                hb, db = fn(k)
+                h2d += hb
+                d2h += db
+            sec = time.perf_counter() - t0
+            if world > 1:
+                t = torch.tensor([sec], dtype=torch.float64, device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                sec = float(t[0])
+            return sec, h2d // a.steps, d2h // a.steps
+
+        e2e_s, h2d, d2h = timed(host_step_csr)
+        dn_s, dn_h2d, dn_d2h = timed(host_step_dense)
         e2e = {"value": evals_total / e2e_s, "unit": "evals/s",
-               "h2d_bytes_per_step": h2d // a.steps, "d2h_bytes_per_step": d2h // a.steps,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": e2e_s * 1e3 / a.steps,
-               "note": "glmb_step_host: pinned H2D of Z_k, theta_k; step; D2H of C_k and gate on a copy "
-                       "stream overlapping reweight, log_norm, flags; synchronised each step; particle state "
-                       "resident"}
+               "note": "glmb_step_host_csr: pinned H2D of Z_k, theta_k; the step; C_k's gated entries as CSR "
+                       "(row_ptr, col, val) + log_norm, flags D2H; synchronised each step; particle state "
+                       "resident on the device",
+               "dense": {"value": evals_total / dn_s, "ms_per_step": dn_s * 1e3 / a.steps,
+                         "h2d_bytes_per_step": dn_h2d, "d2h_bytes_per_step": dn_d2h,
+                         "note": "glmb_step_host: the same with C_k and the gate words read back dense "
+                                 "(on a copy stream overlapping reweight)"}}
 
     if rank != 0:
         if world > 1:

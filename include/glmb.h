@@ -270,6 +270,29 @@ glmb_status glmb_step_host(const glmb_step_params *prm, const float *Z_host,
                            float *log_norm_host, uint32_t *flags_host,
                            glmb_stream_t stream, glmb_stream_t copy_stream);
 
+/* End-to-end step returning C_k in its row-wise sparse form (synchronous): the
+ * step of glmb_step_host, then glmb_compat_rows on the device, and a read-back
+ * of the CSR of the gated entries -- row_ptr [M+1], col / val [nnz] (as
+ * glmb_compat_rows defines them; C[i][0] = kappa and every other entry is 0)
+ * -- plus log_norm and flags.  C_k is ~0.1 % dense at the BASELINE scenes, so
+ * this moves kilobytes over PCIe instead of T_k x ldc floats.  cap: device
+ * capacity of col/val/ln_val; cap_host: host capacity of col_host/val_host.
+ * The first min(cap, cap_host) entries come back with row_ptr; more (when
+ * nnz exceeds it) in a second exact-size copy.  Errors: INVALID_ARG when nnz
+ * exceeds cap or cap_host (the device or host arrays are too small). */
+glmb_status glmb_step_host_csr(const glmb_step_params *prm, const float *Z_host,
+                               int32_t M, const int32_t *theta_host,
+                               float *Z_dev, int32_t *theta_dev,
+                               float *C_tracks_dev, int64_t ldc,
+                               uint32_t *gate_dev, int64_t ldg,
+                               float *log_norm_dev, uint32_t *flags_dev,
+                               int32_t *row_ptr_dev, int32_t *col_dev,
+                               float *val_dev, double *ln_val_dev, int32_t cap,
+                               int32_t *row_ptr_host, int32_t *col_host,
+                               float *val_host, int32_t cap_host,
+                               float *log_norm_host, uint32_t *flags_host,
+                               glmb_stream_t stream);
+
 /* =====================================================================
  * Hypothesis machinery: the consumers of C_k.
  * P:44-53 §Approach.  Readings R23-R29 in DESIGN.md §3.

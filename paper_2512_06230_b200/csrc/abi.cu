@@ -578,6 +578,61 @@ glmb_status glmb_update(const glmb_update_params *u, glmb_stream_t stream) {
   return GLMB_OK;
 }
 
+glmb_status glmb_step_host_csr(const glmb_step_params *prm, const float *Z_host, int32_t M,
+                               const int32_t *theta_host, float *Z_dev, int32_t *theta_dev, float *C_tracks_dev,
+                               int64_t ldc, uint32_t *gate_dev, int64_t ldg, float *log_norm_dev, uint32_t *flags_dev,
+                               int32_t *row_ptr_dev, int32_t *col_dev, float *val_dev, double *ln_val_dev,
+                               int32_t cap, int32_t *row_ptr_host, int32_t *col_host, float *val_host,
+                               int32_t cap_host, float *log_norm_host, uint32_t *flags_host, glmb_stream_t stream) {
+  if (prm == nullptr || M < 0 || cap < 0 || cap_host < 0) return GLMB_ERR_INVALID_ARG;
+  if (M > 0 && (Z_host == nullptr || theta_host == nullptr || Z_dev == nullptr || theta_dev == nullptr))
+    return GLMB_ERR_INVALID_ARG;
+  if (row_ptr_dev == nullptr || row_ptr_host == nullptr) return GLMB_ERR_INVALID_ARG;
+  if (cap_host > 0 && (col_host == nullptr || val_host == nullptr)) return GLMB_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  GLMB_TRY(bind_stream(s, nullptr));
+  const int32_t Tk = prm->tracks.n_tracks;
+  if (M > 0) {
+    if (cudaMemcpyAsync(Z_dev, Z_host, sizeof(float) * 2 * M, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(theta_dev, theta_host, sizeof(int32_t) * M, cudaMemcpyHostToDevice, s) != cudaSuccess)
+      return GLMB_ERR_CUDA;
+  }
+  GLMB_TRY(glmb_step(prm, Z_dev, M, theta_dev, nullptr, C_tracks_dev, ldc, gate_dev, ldg, log_norm_dev, flags_dev,
+                     stream));
+  GLMB_TRY(glmb_compat_rows(Tk, M, C_tracks_dev, ldc, gate_dev, ldg, row_ptr_dev, col_dev, val_dev, ln_val_dev, cap,
+                            stream));
+  // one read-back: row_ptr, the first cap_host entries, log_norm, flags; the rest only if
+  // the gated entries outnumber cap_host (then a second, exact-size copy)
+  const int32_t first = std::min(cap_host, cap);
+  if (cudaMemcpyAsync(row_ptr_host, row_ptr_dev, sizeof(int32_t) * (M + 1), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return GLMB_ERR_CUDA;
+  if (first > 0 &&
+      (cudaMemcpyAsync(col_host, col_dev, sizeof(int32_t) * first, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+       cudaMemcpyAsync(val_host, val_dev, sizeof(float) * first, cudaMemcpyDeviceToHost, s) != cudaSuccess))
+    return GLMB_ERR_CUDA;
+  if (Tk > 0) {
+    if (log_norm_host && cudaMemcpyAsync(log_norm_host, log_norm_dev, sizeof(float) * Tk, cudaMemcpyDeviceToHost,
+                                         s) != cudaSuccess)
+      return GLMB_ERR_CUDA;
+    if (flags_host &&
+        cudaMemcpyAsync(flags_host, flags_dev, sizeof(uint32_t) * Tk, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+      return GLMB_ERR_CUDA;
+  }
+  if (cudaStreamSynchronize(s) != cudaSuccess) return GLMB_ERR_CUDA;
+  const int32_t nnz = row_ptr_host[M];
+  if (nnz > cap) return GLMB_ERR_INVALID_ARG;  /* device CSR capacity too small: entries past cap lost */
+  if (nnz > first) {
+    if (nnz > cap_host) return GLMB_ERR_INVALID_ARG;
+    if (cudaMemcpyAsync(col_host + first, col_dev + first, sizeof(int32_t) * (nnz - first), cudaMemcpyDeviceToHost,
+                        s) != cudaSuccess ||
+        cudaMemcpyAsync(val_host + first, val_dev + first, sizeof(float) * (nnz - first), cudaMemcpyDeviceToHost, s) !=
+            cudaSuccess)
+      return GLMB_ERR_CUDA;
+    if (cudaStreamSynchronize(s) != cudaSuccess) return GLMB_ERR_CUDA;
+  }
+  return GLMB_OK;
+}
+
 glmb_status glmb_philox_dump(uint64_t seed, const uint32_t *ctr, int32_t N, uint32_t *out, glmb_stream_t stream) {
   if (N < 0 || (N > 0 && (ctr == nullptr || out == nullptr))) return GLMB_ERR_INVALID_ARG;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);

@@ -551,3 +551,44 @@ def test_step_kernels_random_tiny_shapes(L, orc, case):
     check_weights(wg, rw)
     check_log_norm(ln, rln)
     np.testing.assert_array_equal(fl.view(np.uint32), rfl)
+
+
+def test_step_host_csr_matches_dense(L, orc):
+    """glmb_step_host_csr returns exactly the gated entries of the dense C_k that glmb_step_host
+    reads back (row order, ascending columns, bit-identical values), and the same log_norm."""
+    import torch
+    from paper_2512_06230_b200.scenes import make_scene
+    from paper_2512_06230_b200.step import GlmbStep
+    s = make_scene(1, steps=1)
+    a, b = GlmbStep(s), GlmbStep(s)
+    M = len(s.Z[0])
+    pin = lambda t: t.pin_memory()
+    Zh, th = pin(torch.from_numpy(s.Z[0])), pin(torch.from_numpy(s.theta[0]))
+    Zd, thd = torch.empty(M, 2, device="cuda"), torch.empty(M, dtype=torch.int32, device="cuda")
+    Ct_h = pin(torch.empty(a.T_local, a.ldc))
+    G_h = pin(torch.empty(a.T_local, a.ldg, dtype=torch.int32))
+    ln_a, fl_a = pin(torch.empty(a.T_local)), pin(torch.empty(a.T_local, dtype=torch.int32))
+    L.glmb_step_host(a.step_params(0), Zh, th, Zd, thd, a.out.C_clutter, a.out.C_tracks, a.out.gate,
+                     a.out.log_norm, a.out.flags, None, Ct_h, G_h, ln_a, fl_a)
+    cap = b.T_local * M
+    rp = torch.empty(M + 1, dtype=torch.int32, device="cuda")
+    col, val = torch.empty(cap, dtype=torch.int32, device="cuda"), torch.empty(cap, device="cuda")
+    lv = torch.empty(cap, dtype=torch.float64, device="cuda")
+    rp_h = pin(torch.empty(M + 1, dtype=torch.int32))
+    col_h, val_h = pin(torch.empty(8, dtype=torch.int32)), pin(torch.empty(8))   # small: forces the 2nd copy
+    ln_b, fl_b = pin(torch.empty(b.T_local)), pin(torch.empty(b.T_local, dtype=torch.int32))
+    with pytest.raises(Exception):   # more gated entries than the host arrays hold
+        L.glmb_step_host_csr(b.step_params(0), Zh, th, Zd, thd, b.out.C_tracks, b.out.gate, b.out.log_norm,
+                             b.out.flags, rp, col, val, lv, rp_h, col_h, val_h, ln_b, fl_b)
+    c = GlmbStep(s)
+    col_h, val_h = pin(torch.empty(4096, dtype=torch.int32)), pin(torch.empty(4096))
+    nnz = L.glmb_step_host_csr(c.step_params(0), Zh, th, Zd, thd, c.out.C_tracks, c.out.gate, c.out.log_norm,
+                               c.out.flags, rp, col, val, lv, rp_h, col_h, val_h, ln_b, fl_b)
+    C = Ct_h.numpy()[:, :M]
+    G = np.unpackbits(G_h.numpy().view(np.uint8), bitorder="little").reshape(a.T_local, -1)[:, :M].astype(bool)
+    rows = [np.nonzero(G[:, i])[0] for i in range(M)]
+    np.testing.assert_array_equal(rp_h.numpy(), np.concatenate([[0], np.cumsum([len(r) for r in rows])]))
+    assert nnz == sum(len(r) for r in rows)
+    np.testing.assert_array_equal(col_h.numpy()[:nnz], np.concatenate(rows))
+    np.testing.assert_array_equal(val_h.numpy()[:nnz], np.concatenate([C[r, i] for i, r in enumerate(rows)]))
+    np.testing.assert_array_equal(ln_b.numpy(), ln_a.numpy())
