@@ -605,9 +605,10 @@ def main():
         def host_step_csr(k):
             """C_k read back as the CSR of its gated entries (glmb_step_host_csr)."""
             zi = k % len(Zh)
-            nnz = L.glmb_step_host_csr(st.step_params(k), Zh[zi], thh[zi], Zd, thd, o.C_tracks, o.gate,
-                                       o.log_norm, o.flags, rp_d, col_d, val_d, lv_d, rp_h, col_h, val_h, ln_h,
-                                       fl_h, stream)
+            nnz = L.glmb_step_host_csr(st.step_params(k, out_of_place=True), Zh[zi], thh[zi], Zd, thd,
+                                       o.C_tracks, o.gate, o.log_norm, o.flags, rp_d, col_d, val_d, lv_d, rp_h,
+                                       col_h, val_h, ln_h, fl_h, stream, aux_stream=copy_stream)
+            st.swap_weights()
             M = Zh[zi].shape[0]
             return M * 12, (M + 1) * 4 + nnz * 8 + st.T_local * 8
 
@@ -644,9 +645,9 @@ def main():
         e2e = {"value": evals_total / e2e_s, "unit": "evals/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": e2e_s * 1e3 / a.steps,
-               "note": "glmb_step_host_csr: pinned H2D of Z_k, theta_k; the step; C_k's gated entries as CSR "
-                       "(row_ptr, col, val) + log_norm, flags D2H; synchronised each step; particle state "
-                       "resident on the device",
+               "note": "glmb_step_host_csr: pinned H2D of Z_k, theta_k; the step (reweight into the spare "
+                       "weights beside compat); C_k's gated entries as CSR (row_ptr, col, val) + log_norm, "
+                       "flags D2H; synchronised each step; particle state resident on the device",
                "dense": {"value": evals_total / dn_s, "ms_per_step": dn_s * 1e3 / a.steps,
                          "h2d_bytes_per_step": dn_h2d, "d2h_bytes_per_step": dn_d2h,
                          "note": "glmb_step_host: the same with C_k and the gate words read back dense "

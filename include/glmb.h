@@ -278,8 +278,11 @@ glmb_status glmb_step_host(const glmb_step_params *prm, const float *Z_host,
  * this moves kilobytes over PCIe instead of T_k x ldc floats.  cap: device
  * capacity of col/val/ln_val; cap_host: host capacity of col_host/val_host.
  * The first min(cap, cap_host) entries come back with row_ptr; more (when
- * nnz exceeds it) in a second exact-size copy.  Errors: INVALID_ARG when nnz
- * exceeds cap or cap_host (the device or host arrays are too small). */
+ * nnz exceeds it) in a second exact-size copy.  With prm->w_out set and an
+ * aux_stream (and a non-NULL stream), reweight runs on aux_stream beside
+ * compat (out of place: the caller swaps weight buffers afterwards); else the
+ * four calls run in order on `stream`.  Errors: INVALID_ARG when nnz exceeds
+ * cap or cap_host (the device or host arrays are too small). */
 glmb_status glmb_step_host_csr(const glmb_step_params *prm, const float *Z_host,
                                int32_t M, const int32_t *theta_host,
                                float *Z_dev, int32_t *theta_dev,
@@ -291,7 +294,7 @@ glmb_status glmb_step_host_csr(const glmb_step_params *prm, const float *Z_host,
                                int32_t *row_ptr_host, int32_t *col_host,
                                float *val_host, int32_t cap_host,
                                float *log_norm_host, uint32_t *flags_host,
-                               glmb_stream_t stream);
+                               glmb_stream_t stream, glmb_stream_t aux_stream);
 
 /* =====================================================================
  * Hypothesis machinery: the consumers of C_k.

@@ -583,7 +583,8 @@ glmb_status glmb_step_host_csr(const glmb_step_params *prm, const float *Z_host,
                                int64_t ldc, uint32_t *gate_dev, int64_t ldg, float *log_norm_dev, uint32_t *flags_dev,
                                int32_t *row_ptr_dev, int32_t *col_dev, float *val_dev, double *ln_val_dev,
                                int32_t cap, int32_t *row_ptr_host, int32_t *col_host, float *val_host,
-                               int32_t cap_host, float *log_norm_host, uint32_t *flags_host, glmb_stream_t stream) {
+                               int32_t cap_host, float *log_norm_host, uint32_t *flags_host, glmb_stream_t stream,
+                               glmb_stream_t aux_stream) {
   if (prm == nullptr || M < 0 || cap < 0 || cap_host < 0) return GLMB_ERR_INVALID_ARG;
   if (M > 0 && (Z_host == nullptr || theta_host == nullptr || Z_dev == nullptr || theta_dev == nullptr))
     return GLMB_ERR_INVALID_ARG;
@@ -597,8 +598,42 @@ glmb_status glmb_step_host_csr(const glmb_step_params *prm, const float *Z_host,
         cudaMemcpyAsync(theta_dev, theta_host, sizeof(int32_t) * M, cudaMemcpyHostToDevice, s) != cudaSuccess)
       return GLMB_ERR_CUDA;
   }
-  GLMB_TRY(glmb_step(prm, Z_dev, M, theta_dev, nullptr, C_tracks_dev, ldc, gate_dev, ldg, log_norm_dev, flags_dev,
-                     stream));
+  // out of place with an aux stream: reweight (reads w, writes prm->w_out) runs on aux_stream
+  // beside compat, enqueued first (a kernel queued behind compat only gets SMs in its tail)
+  const bool overlap = prm->w_out != nullptr && aux_stream != nullptr && stream != nullptr;
+  cudaStream_t as = reinterpret_cast<cudaStream_t>(aux_stream);
+  cudaEvent_t ev = nullptr;
+  if (!overlap) {
+    GLMB_TRY(glmb_step(prm, Z_dev, M, theta_dev, nullptr, C_tracks_dev, ldc, gate_dev, ldg, log_norm_dev, flags_dev,
+                       stream));
+  } else {
+    const glmb_particles &all = prm->tracks;
+    GLMB_TRY(check_particles(&all, true, true));
+    const int32_t T = prm->n_survivors;
+    if (T < 0 || T > Tk) return GLMB_ERR_INVALID_ARG;
+    glmb_particles surv = all, births = all;
+    surv.n_tracks = T;
+    births.n_tracks = Tk - T;
+    const int64_t off = static_cast<int64_t>(T) * all.ld;
+    if (Tk > 0) {
+      births.x = all.x + off; births.y = all.y + off; births.v = all.v + off;
+      births.psi = all.psi + off; births.omega = all.omega + off; births.w = all.w + off;
+    }
+    GLMB_TRY(glmb_predict(&surv, &surv, prm->gid, prm->dt, prm->sigma_a, prm->sigma_w, prm->seed, prm->step, stream));
+    GLMB_TRY(glmb_birth(&births, prm->gid ? prm->gid + T : nullptr, prm->birth_mean, prm->birth_chol, prm->seed,
+                        prm->step, stream));
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return GLMB_ERR_CUDA;
+    glmb_status st = GLMB_OK;
+    if (cudaEventRecord(ev, s) != cudaSuccess || cudaStreamWaitEvent(as, ev, 0) != cudaSuccess) st = GLMB_ERR_CUDA;
+    if (st == GLMB_OK)
+      st = glmb_reweight(&all, prm->w_out, Z_dev, M, prm->Rxx, prm->Rxy, prm->Ryy, theta_dev, prm->col_offset,
+                         log_norm_dev, flags_dev, aux_stream);
+    if (st == GLMB_OK)
+      st = glmb_compat(&all, Z_dev, M, prm->Rxx, prm->Rxy, prm->Ryy, prm->p_d, prm->kappa, prm->gamma, nullptr,
+                       C_tracks_dev, ldc, gate_dev, ldg, stream);
+    cudaEventDestroy(ev);
+    if (st != GLMB_OK) return st;
+  }
   GLMB_TRY(glmb_compat_rows(Tk, M, C_tracks_dev, ldc, gate_dev, ldg, row_ptr_dev, col_dev, val_dev, ln_val_dev, cap,
                             stream));
   // one read-back: row_ptr, the first cap_host entries, log_norm, flags; the rest only if
@@ -611,14 +646,16 @@ glmb_status glmb_step_host_csr(const glmb_step_params *prm, const float *Z_host,
        cudaMemcpyAsync(val_host, val_dev, sizeof(float) * first, cudaMemcpyDeviceToHost, s) != cudaSuccess))
     return GLMB_ERR_CUDA;
   if (Tk > 0) {
+    cudaStream_t ls = overlap ? as : s;  // log_norm / flags from reweight's stream
     if (log_norm_host && cudaMemcpyAsync(log_norm_host, log_norm_dev, sizeof(float) * Tk, cudaMemcpyDeviceToHost,
-                                         s) != cudaSuccess)
+                                         ls) != cudaSuccess)
       return GLMB_ERR_CUDA;
     if (flags_host &&
-        cudaMemcpyAsync(flags_host, flags_dev, sizeof(uint32_t) * Tk, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        cudaMemcpyAsync(flags_host, flags_dev, sizeof(uint32_t) * Tk, cudaMemcpyDeviceToHost, ls) != cudaSuccess)
       return GLMB_ERR_CUDA;
   }
   if (cudaStreamSynchronize(s) != cudaSuccess) return GLMB_ERR_CUDA;
+  if (overlap && cudaStreamSynchronize(as) != cudaSuccess) return GLMB_ERR_CUDA;
   const int32_t nnz = row_ptr_host[M];
   if (nnz > cap) return GLMB_ERR_INVALID_ARG;  /* device CSR capacity too small: entries past cap lost */
   if (nnz > first) {

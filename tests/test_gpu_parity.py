@@ -592,3 +592,19 @@ def test_step_host_csr_matches_dense(L, orc):
     np.testing.assert_array_equal(col_h.numpy()[:nnz], np.concatenate(rows))
     np.testing.assert_array_equal(val_h.numpy()[:nnz], np.concatenate([C[r, i] for i, r in enumerate(rows)]))
     np.testing.assert_array_equal(ln_b.numpy(), ln_a.numpy())
+    # reweight beside compat on an aux stream (out of place): same CSR, same new weights
+    d = GlmbStep(s)
+    st_, aux = torch.cuda.Stream(), torch.cuda.Stream()
+    rp2 = pin(torch.empty(M + 1, dtype=torch.int32))
+    col2, val2 = pin(torch.empty(4096, dtype=torch.int32)), pin(torch.empty(4096))
+    ln2, fl2 = pin(torch.empty(d.T_local)), pin(torch.empty(d.T_local, dtype=torch.int32))
+    nnz2 = L.glmb_step_host_csr(d.step_params(0, out_of_place=True), Zh, th, Zd, thd, d.out.C_tracks, d.out.gate,
+                                d.out.log_norm, d.out.flags, rp, col, val, lv, rp2, col2, val2, ln2, fl2,
+                                stream=st_, aux_stream=aux)
+    d.swap_weights()
+    assert nnz2 == nnz
+    np.testing.assert_array_equal(rp2.numpy(), rp_h.numpy())
+    np.testing.assert_array_equal(col2.numpy()[:nnz], col_h.numpy()[:nnz])
+    np.testing.assert_array_equal(val2.numpy()[:nnz], val_h.numpy()[:nnz])
+    np.testing.assert_array_equal(ln2.numpy(), ln_a.numpy())
+    np.testing.assert_array_equal(d.weights().cpu().numpy(), c.weights().cpu().numpy())
