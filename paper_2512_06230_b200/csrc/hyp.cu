@@ -157,17 +157,6 @@ __device__ __forceinline__ uint64_t fp_term(uint32_t v, uint64_t idx) {
   return mix64((idx << 32) ^ v ^ 0x9E3779B97F4A7C15ull);
 }
 
-template <typename Tv>
-__device__ __forceinline__ Tv block_sum_128(Tv v, Tv *red) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if (lane == 0) red[wid] = v;
-  __syncthreads();
-  const Tv r = (red[0] + red[1]) + (red[2] + red[3]);
-  __syncthreads();
-  return r;
-}
 
 // Block-wide exclusive scan of one int32 per thread (kSampThreads threads).
 __device__ __forceinline__ int32_t block_excl_scan_128(int32_t v, int32_t *red, int32_t &total) {
