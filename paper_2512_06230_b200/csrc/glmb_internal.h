@@ -123,6 +123,7 @@ struct SampleArgs {
   unsigned long long *hash;
   int32_t row_cap;  // set by the launcher: filtered row entries that fit in shared memory
   int32_t spc;      // set by the launcher: samples per CTA
+  int32_t quad_cap; // set by the launcher: parent track quads whose logs fit in shared memory
 };
 
 struct DedupArgs {

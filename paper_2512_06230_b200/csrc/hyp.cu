@@ -11,6 +11,7 @@
 // Integer outcomes (alive bits, theta) are decided in fp32 exactly as the
 // readings R25/R26 state, so they are bit-identical to any implementation that
 // follows them; log-weights accumulate in fp64.
+#include <algorithm>
 #include <cstdlib>
 
 #include "glmb_device.cuh"
@@ -176,29 +177,84 @@ __device__ __forceinline__ int32_t block_excl_scan_128(int32_t v, int32_t *red, 
   return before + x - v;
 }
 
-// CTA = (parent h, group of kSampPerCta samples).  The parent's rows of C'_k --
-// the gated entries whose column is in the parent, in ascending column order --
-// are filtered once into shared memory (when they fit, else the CTA walks the
-// global CSR) and reused by the group's samples; stage 1 visits only the
-// parent's tracks.  Same draws and the same fp32 operation order as a walk of
-// the full rows (columns outside the parent are never alive), so the integer
-// outcomes do not depend on this.
+// CTA = (parent h, group of kSampPerCta samples).  Once per CTA: the parent's rows of
+// C'_k -- the gated entries whose column is in the parent, in ascending column order --
+// are filtered into shared memory (when they fit, else the CTA walks the global CSR),
+// and the parent's track quads are listed, the first quad_cap of them with ln P_S,
+// ln(1 - P_S) of their tracks (later ones take the logs inline).  Per sample,
+// stage 1 visits only the parent's quads and, at M >= 256, stage 2 gives each thread
+// four rows (one Philox block).  Same draws and the same fp32 operation order as a walk of the full
+// rows (columns outside the parent are never alive), so the integer outcomes do not
+// depend on any of this.
 constexpr int kSampPerCtaMax = 16;
-constexpr int kRowCapMax = 1024;  // filtered entries held in shared memory (16 KB: ~10 CTAs per SM)
+constexpr int kRowCapMax = 1024;   // filtered entries held in shared memory (16 KB)
+constexpr int kQuadCapMax = 384;   // parent track quads with cached logs (26 KB)
+
+__device__ __forceinline__ uint32_t word_of(const u32x4 &r, int e) {
+  return e == 0 ? r.a : e == 1 ? r.b : e == 2 ? r.c : r.d;
+}
+
+// Row i's categorical draw (R26): clutter kappa, then the alive gated columns
+// in ascending order; inverse CDF in fp32 with the word's 24-bit uniform.  Adds the
+// picked entry's ln value to lw and returns theta_i (0 = clutter).  An empty row draws
+// the clutter entry whatever u is (u * kappa rounds to at most kappa, and the walk past
+// it falls back to column 0 as well).
+__device__ __forceinline__ int32_t draw_row(const int32_t *rp, const int32_t *cl, const float *vl,
+                                            const double *lvl, const uint32_t *alive, float kappa,
+                                            double ln_kappa, int32_t i, uint32_t word, double &lw) {
+  const int32_t e0 = rp[i], e1 = rp[i + 1];
+  int32_t pick = 0;
+  double lpick = ln_kappa;
+  if (e0 < e1) {
+    float total = kappa;
+    for (int32_t x = e0; x < e1; ++x) {
+      const int32_t j = cl[x];
+      if ((alive[j >> 5] >> (j & 31)) & 1u) total = __fadd_rn(total, vl[x]);
+    }
+    const float tt = __fmul_rn(uniform24(word), total);
+    float acc = kappa;
+    if (!(tt < acc)) {
+      int32_t last = 0;
+      double llast = ln_kappa;
+      pick = -1;
+      for (int32_t x = e0; x < e1; ++x) {
+        const int32_t j = cl[x];
+        if (!((alive[j >> 5] >> (j & 31)) & 1u)) continue;
+        acc = __fadd_rn(acc, vl[x]);
+        last = j + 1;
+        llast = lvl[x];
+        if (tt < acc) {
+          pick = j + 1;
+          lpick = llast;
+          break;
+        }
+      }
+      if (pick < 0) {
+        pick = last;
+        lpick = llast;
+      }
+    }
+  }
+  lw += lpick;
+  return pick;
+}
 
 __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   double *flv = reinterpret_cast<double *>(smraw);                 // [row_cap]
-  float *fval = reinterpret_cast<float *>(flv + a.row_cap);        // [row_cap]
+  double *qls = flv + a.row_cap;                                   // [4 quad_cap] ln P_S
+  double *qld = qls + 4 * a.quad_cap;                              // [4 quad_cap] ln(1 - P_S)
+  float *fval = reinterpret_cast<float *>(qld + 4 * a.quad_cap);   // [row_cap]
   int32_t *fcol = reinterpret_cast<int32_t *>(fval + a.row_cap);   // [row_cap]
   int32_t *frp = fcol + a.row_cap;                                 // [M + 1]
-  uint32_t *pmask = reinterpret_cast<uint32_t *>(frp + a.M + 1);   // [ldt]
+  int32_t *pq = frp + a.M + 1;                                     // [(T + 3) / 4]
+  uint32_t *pmask = reinterpret_cast<uint32_t *>(pq + ((a.T + 3) >> 2));  // [ldt]
   uint32_t *alive = pmask + a.ldt, *det = alive + a.ldt;            // [ldt] each
   int32_t *cnt = reinterpret_cast<int32_t *>(det + a.ldt);         // [T] when a count prior is given
   __shared__ double red_d[4];
   __shared__ unsigned long long red_u[4];
   __shared__ int32_t red_i[4];
-  __shared__ int32_t use_smem;
+  __shared__ int32_t use_smem, n_quads;
   const int n_groups = (a.H_up + a.spc - 1) / a.spc;
   const int32_t h = static_cast<int32_t>(blockIdx.x / n_groups);
   const int32_t s0 = static_cast<int32_t>(blockIdx.x - static_cast<int64_t>(h) * n_groups) * a.spc;
@@ -207,7 +263,31 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
   const uint32_t *pm = a.parent_mask + static_cast<int64_t>(h) * a.ldt;
   for (int32_t k = threadIdx.x; k < a.ldt; k += kSampThreads) pmask[k] = __ldg(pm + k);
   __syncthreads();
+  const int32_t tquads = (a.T + 3) >> 2;
 
+  // ---- the parent's track quads (ascending) with the logs of their tracks
+  {
+    int32_t carry = 0;
+    for (int32_t t0 = 0; t0 < tquads; t0 += kSampThreads) {
+      const int32_t t = t0 + threadIdx.x;
+      const uint32_t qbits = t < tquads ? (pmask[t >> 3] >> (4 * (t & 7))) & 0xFu : 0u;
+      int32_t tot;
+      const int32_t ex = block_excl_scan_128(qbits != 0u, red_i, tot);
+      const int32_t slot = carry + ex;
+      if (qbits != 0u) pq[slot] = t;
+      if (qbits != 0u && slot < a.quad_cap) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (!((qbits >> e) & 1u)) continue;
+          const double ps = static_cast<double>(__ldg(a.p_s + 4 * t + e));
+          qls[4 * slot + e] = log(ps);
+          qld[4 * slot + e] = log(1.0 - ps);
+        }
+      }
+      carry += tot;
+    }
+    if (threadIdx.x == 0) n_quads = carry;
+  }
   // ---- the parent's rows (shared memory), filtered in ascending column order
   {
     int32_t carry = 0;
@@ -249,12 +329,18 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
     __syncthreads();
   }
   const bool sm_rows = use_smem;
+  const int32_t nq = n_quads;
   const int32_t *rp = sm_rows ? frp : a.row_ptr;
   const int32_t *cl = sm_rows ? fcol : a.col;
   const float *vl = sm_rows ? fval : a.val;
   const double *lvl = sm_rows ? flv : a.ln_val;
   const double ln_kappa = log(static_cast<double>(a.kappa));
   const double ln_miss = log(1.0 - static_cast<double>(a.p_d));
+  const int32_t rquads = (a.M + 3) >> 2;
+  // four rows per thread once the rows outnumber the threads twice over (fewer Philox
+  // blocks per warp); below that one row per thread keeps the latency down
+  const bool rows4 = a.M >= 2 * kSampThreads;
+  const bool vec_store = ((a.ldm & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.theta) & 15) == 0);
   for (int32_t s = s0; s < s1; ++s) {
     const int64_t q = static_cast<int64_t>(h) * a.H_up + s;
     // stage 1: track j of the parent survives iff u_j < 1 - d_j (fp32, R25);
@@ -265,10 +351,9 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
       det[k] = 0u;
     }
     __syncthreads();
-    const int32_t tquads = (a.T + 3) >> 2;
-    for (int32_t t = threadIdx.x; t < tquads; t += kSampThreads) {
+    for (int32_t v = threadIdx.x; v < nq; v += kSampThreads) {
+      const int32_t t = pq[v];
       const uint32_t qbits = (pmask[t >> 3] >> (4 * (t & 7))) & 0xFu;
-      if (qbits == 0u) continue;
       const u32x4 r = philox4x32_10(
           u32x4{static_cast<uint32_t>(t), static_cast<uint32_t>(h), a.step, (kDomainSurvive << 24) | static_cast<uint32_t>(s)},
           a.key0, a.key1);
@@ -278,9 +363,13 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
         if (!((qbits >> e) & 1u)) continue;
         const int32_t j = 4 * t + e;
         const float thr = __fsub_rn(1.0f, __ldg(a.d_prob + j));
-        const bool al = uniform24(e == 0 ? r.a : e == 1 ? r.b : e == 2 ? r.c : r.d) < thr;
-        const double ps = static_cast<double>(__ldg(a.p_s + j));
-        lw += al ? log(ps) : log(1.0 - ps);
+        const bool al = uniform24(word_of(r, e)) < thr;
+        if (v < a.quad_cap) {
+          lw += al ? qls[4 * v + e] : qld[4 * v + e];
+        } else {
+          const double ps = static_cast<double>(__ldg(a.p_s + j));
+          lw += al ? log(ps) : log(1.0 - ps);
+        }
         bits |= static_cast<uint32_t>(al) << e;
         if (a.n_count > 0) cnt[j] = 0;
       }
@@ -293,58 +382,49 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
     // Philox block (i/4, h, step, 3<<24 | s), word i%4
     int32_t *th = a.theta + q * a.ldm;
     uint64_t fp = 0ull;
-    // one row per thread; the Philox block of rows 4t..4t+3 is computed by the lane
-    // holding row 4t and shuffled to the three lanes after it (rows are lane-contiguous)
-    const int lane = threadIdx.x & 31;
-    for (int32_t i0 = 0; i0 < a.M; i0 += kSampThreads) {
-      const int32_t i = i0 + threadIdx.x;
-      u32x4 r{0u, 0u, 0u, 0u};
-      if ((i & 3) == 0 && i < a.M)
-        r = philox4x32_10(u32x4{static_cast<uint32_t>(i >> 2), static_cast<uint32_t>(h), a.step,
-                                (kDomainAssoc << 24) | static_cast<uint32_t>(s)},
-                          a.key0, a.key1);
-      const int src = lane & ~3, e = i & 3;
-      const uint32_t w0 = __shfl_sync(0xffffffffu, r.a, src), w1 = __shfl_sync(0xffffffffu, r.b, src);
-      const uint32_t w2 = __shfl_sync(0xffffffffu, r.c, src), w3 = __shfl_sync(0xffffffffu, r.d, src);
-      if (i >= a.M) continue;
-      const uint32_t rwe = e == 0 ? w0 : e == 1 ? w1 : e == 2 ? w2 : w3;
-      const int32_t e0 = rp[i], e1 = rp[i + 1];
-      float total = a.kappa;
-      for (int32_t x = e0; x < e1; ++x) {
-        const int32_t j = cl[x];
-        if ((alive[j >> 5] >> (j & 31)) & 1u) total = __fadd_rn(total, vl[x]);
-      }
-      const float tt = __fmul_rn(uniform24(rwe), total);
-      float acc = a.kappa;
-      int32_t pick = -1, last = 0;
-      double lpick = ln_kappa, llast = ln_kappa;
-      if (tt < acc) {
-        pick = 0;
-      } else {
-        for (int32_t x = e0; x < e1; ++x) {
-          const int32_t j = cl[x];
-          if (!((alive[j >> 5] >> (j & 31)) & 1u)) continue;
-          acc = __fadd_rn(acc, vl[x]);
-          last = j + 1;
-          llast = lvl[x];
-          if (tt < acc) {
-            pick = j + 1;
-            lpick = llast;
-            break;
-          }
-        }
-        if (pick < 0) {
-          pick = last;
-          lpick = llast;
-        }
-      }
-      lw += lpick;
+    auto row = [&](int32_t i, uint32_t word) -> int32_t {
+      const int32_t pick = draw_row(rp, cl, vl, lvl, alive, a.kappa, ln_kappa, i, word, lw);
       if (pick > 0) {
         atomicOr(det + ((pick - 1) >> 5), 1u << ((pick - 1) & 31));
         if (a.n_count > 0) atomicAdd(cnt + pick - 1, 1);
+        // fingerprint over the detected rows only (theta is 0 elsewhere)
+        fp += fp_term(static_cast<uint32_t>(pick), static_cast<uint64_t>(a.ldt) + i);
       }
-      fp += fp_term(static_cast<uint32_t>(pick), static_cast<uint64_t>(a.ldt) + i);
-      th[i] = pick;
+      return pick;
+    };
+    if (rows4) {
+      // thread = four rows (one Philox block)
+      for (int32_t t = threadIdx.x; t < rquads; t += kSampThreads) {
+        const u32x4 r = philox4x32_10(u32x4{static_cast<uint32_t>(t), static_cast<uint32_t>(h), a.step,
+                                            (kDomainAssoc << 24) | static_cast<uint32_t>(s)},
+                                      a.key0, a.key1);
+        int32_t pk[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) pk[e] = 4 * t + e < a.M ? row(4 * t + e, word_of(r, e)) : 0;
+        if (vec_store && 4 * t + 3 < a.M) {
+          *reinterpret_cast<int4 *>(th + 4 * t) = make_int4(pk[0], pk[1], pk[2], pk[3]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (4 * t + e < a.M) th[4 * t + e] = pk[e];
+        }
+      }
+    } else {
+      // thread = one row; the Philox block of rows 4t..4t+3 is computed by the lane
+      // holding row 4t and shuffled to the three lanes after it (rows are lane-contiguous)
+      const int lane = threadIdx.x & 31;
+      for (int32_t i0 = 0; i0 < a.M; i0 += kSampThreads) {
+        const int32_t i = i0 + threadIdx.x;
+        u32x4 r{0u, 0u, 0u, 0u};
+        if ((i & 3) == 0 && i < a.M)
+          r = philox4x32_10(u32x4{static_cast<uint32_t>(i >> 2), static_cast<uint32_t>(h), a.step,
+                                  (kDomainAssoc << 24) | static_cast<uint32_t>(s)},
+                            a.key0, a.key1);
+        const int src = lane & ~3;
+        const u32x4 rr{__shfl_sync(0xffffffffu, r.a, src), __shfl_sync(0xffffffffu, r.b, src),
+                       __shfl_sync(0xffffffffu, r.c, src), __shfl_sync(0xffffffffu, r.d, src)};
+        if (i < a.M) th[i] = row(i, word_of(rr, i & 3));
+      }
     }
     __syncthreads();
 
@@ -707,13 +787,21 @@ cudaError_t launch_assoc_sample(const SampleArgs &a, int sm_count, cudaStream_t 
   b.spc = static_cast<int32_t>(spc < 1 ? 1 : spc > kSampPerCtaMax ? kSampPerCtaMax : spc);
   const int64_t groups = (a.H_up + b.spc - 1) / b.spc;
   const int64_t n = static_cast<int64_t>(a.H_old) * groups;
+  const size_t tquads = (static_cast<size_t>(a.T) + 3) / 4;
   const size_t fixed = sizeof(int32_t) * (static_cast<size_t>(a.M) + 1) + sizeof(uint32_t) * 3 * static_cast<size_t>(a.ldt) +
-                       (a.n_count > 0 ? sizeof(int32_t) * static_cast<size_t>(a.T) : 0) + 16;
-  const size_t budget = 200 * 1024;
-  if (fixed > budget) return cudaErrorInvalidValue;
+                       sizeof(int32_t) * tquads + (a.n_count > 0 ? sizeof(int32_t) * static_cast<size_t>(a.T) : 0) + 16;
+  if (fixed > 200 * 1024) return cudaErrorInvalidValue;
+  // shared memory per CTA sized so the grid runs in one wave where it can: the row
+  // cache first (up to kRowCapMax entries), then the parent quads' logs
+  const int64_t sms = sm_count > 0 ? sm_count : 148;
+  const int64_t per_sm = std::min<int64_t>(16, std::max<int64_t>(1, (n + sms - 1) / sms));
+  const size_t target = std::max(fixed, std::min<size_t>(200 * 1024, (227 * 1024) / per_sm - 2048));
   const size_t per = sizeof(double) + sizeof(float) + sizeof(int32_t);
-  b.row_cap = static_cast<int32_t>(min(static_cast<size_t>(kRowCapMax), (budget - fixed) / per));
-  const size_t smem = static_cast<size_t>(b.row_cap) * per + fixed;
+  const size_t per_q = 8 * sizeof(double);
+  b.row_cap = static_cast<int32_t>(std::min(static_cast<size_t>(kRowCapMax), (target - fixed) / per));
+  const size_t rest = target - fixed - static_cast<size_t>(b.row_cap) * per;
+  b.quad_cap = static_cast<int32_t>(std::min(std::min(tquads, static_cast<size_t>(kQuadCapMax)), rest / per_q));
+  const size_t smem = static_cast<size_t>(b.row_cap) * per + static_cast<size_t>(b.quad_cap) * per_q + fixed;
   cudaError_t e = cudaFuncSetAttribute(assoc_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
