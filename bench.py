@@ -336,12 +336,16 @@ def bench_update(a, st, scene, cfg, dev, stream, L):
         total.append(evs["start"].elapsed_time(evs["resample"]))
     n_kept = int(hu.n_kept.item())
     n_pairs = pu.n_pairs_checked()
+    rp = hu.row_ptr[:M + 1].cpu().numpy()
+    row_len = np.diff(rp)
     fl = pu.flags[:n_pairs].cpu().numpy()
     return {"workload": f"cfg{a.config if a.config is not None else 3} C_k (T_k={T}, M={M}) + particles; "
                         f"H_old={a.h_old} x H_up={a.h_up}, tau=1e-5, H_max={a.h_max} (P:186)",
             "ms": statistics.mean(total), "stages_ms": {n: statistics.mean(v) for n, v in stage.items()},
             "n_samples": a.h_old * a.h_up, "n_unique": int(hu.unique.sum().item()), "n_kept": n_kept,
             "n_pairs": n_pairs, "n_resampled": int(((fl >> 1) & 1).sum()),
+            "gated_entries": int(rp[-1]), "row_len_max": int(row_len.max()) if M else 0,
+            "rows_empty": int((row_len == 0).sum()),
             "gpu_launches_per_update": 14,
             "note": "device-resident; no host round trip inside (device counts n_kept / n_pairs)"}
 

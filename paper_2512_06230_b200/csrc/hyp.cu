@@ -181,9 +181,10 @@ __device__ __forceinline__ int32_t block_excl_scan_128(int32_t v, int32_t *red, 
 // C'_k -- the gated entries whose column is in the parent, in ascending column order --
 // are filtered into shared memory (when they fit, else the CTA walks the global CSR),
 // and the parent's track quads are listed, the first quad_cap of them with ln P_S,
-// ln(1 - P_S) of their tracks (later ones take the logs inline).  Per sample,
-// stage 1 visits only the parent's quads and, at M >= 256, stage 2 gives each thread
-// four rows (one Philox block).  Same draws and the same fp32 operation order as a walk of the full
+// ln(1 - P_S) of their tracks (later ones take the logs inline), and the rows holding
+// a parent entry are listed by Philox quad.  Per sample, stage 1 visits only the
+// parent's quads and stage 2 only those rows (a thread per quad, or per row when M <
+// 256).  Same draws and the same fp32 operation order as a walk of the full
 // rows (columns outside the parent are never alive), so the integer outcomes do not
 // depend on any of this.
 constexpr int kSampPerCtaMax = 16;
@@ -248,13 +249,16 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
   int32_t *fcol = reinterpret_cast<int32_t *>(fval + a.row_cap);   // [row_cap]
   int32_t *frp = fcol + a.row_cap;                                 // [M + 1]
   int32_t *pq = frp + a.M + 1;                                     // [(T + 3) / 4]
-  uint32_t *pmask = reinterpret_cast<uint32_t *>(pq + ((a.T + 3) >> 2));  // [ldt]
+  int32_t *nzq = pq + ((a.T + 3) >> 2);                            // [(M + 3) / 4]
+  const bool row_mode = a.M < 2 * kSampThreads;
+  int32_t *nzr = nzq + ((a.M + 3) >> 2);                            // [M] in row mode
+  uint32_t *pmask = reinterpret_cast<uint32_t *>(nzr + (row_mode ? a.M : 0));  // [ldt]
   uint32_t *alive = pmask + a.ldt, *det = alive + a.ldt;            // [ldt] each
   int32_t *cnt = reinterpret_cast<int32_t *>(det + a.ldt);         // [T] when a count prior is given
   __shared__ double red_d[4];
   __shared__ unsigned long long red_u[4];
   __shared__ int32_t red_i[4];
-  __shared__ int32_t use_smem, n_quads;
+  __shared__ int32_t use_smem, n_quads, n_nzq, n_nzr;
   const int n_groups = (a.H_up + a.spc - 1) / a.spc;
   const int32_t h = static_cast<int32_t>(blockIdx.x / n_groups);
   const int32_t s0 = static_cast<int32_t>(blockIdx.x - static_cast<int64_t>(h) * n_groups) * a.spc;
@@ -337,9 +341,42 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
   const double ln_kappa = log(static_cast<double>(a.kappa));
   const double ln_miss = log(1.0 - static_cast<double>(a.p_d));
   const int32_t rquads = (a.M + 3) >> 2;
-  // four rows per thread once the rows outnumber the threads twice over (fewer Philox
-  // blocks per warp); below that one row per thread keeps the latency down
-  const bool rows4 = a.M >= 2 * kSampThreads;
+  // ---- rows holding a parent entry, grouped by their Philox quad: nzq = (quad << 4 |
+  // mask of its non-empty rows); in row mode (few rows) also the rows themselves.  A row
+  // without one draws theta_i = 0 with ln kappa whatever its uniform (see draw_row), so
+  // the sampler only visits these.
+  {
+    int32_t cq = 0, cr = 0;
+    for (int32_t t0 = 0; t0 < rquads; t0 += kSampThreads) {
+      const int32_t t = t0 + threadIdx.x;
+      uint32_t mask = 0u;
+      if (t < rquads) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int32_t i = 4 * t + e;
+          if (i < a.M && rp[i + 1] > rp[i]) mask |= 1u << e;
+        }
+      }
+      int32_t tq, tr;
+      const int32_t exq = block_excl_scan_128(mask != 0u, red_i, tq);
+      const int32_t exr = block_excl_scan_128(__popc(mask), red_i, tr);
+      if (mask != 0u) {
+        nzq[cq + exq] = static_cast<int32_t>((static_cast<uint32_t>(t) << 4) | mask);
+        if (row_mode) {
+          int32_t k = cr + exr;
+          for (uint32_t m = mask; m != 0u; m &= m - 1u) nzr[k++] = 4 * t + __ffs(m) - 1;
+        }
+      }
+      cq += tq;
+      cr += tr;
+    }
+    if (threadIdx.x == 0) {
+      n_nzq = cq;
+      n_nzr = cr;
+    }
+    __syncthreads();
+  }
+  const int32_t nzq_n = n_nzq, nzr_n = n_nzr;
   const bool vec_store = ((a.ldm & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.theta) & 15) == 0);
   for (int32_t s = s0; s < s1; ++s) {
     const int64_t q = static_cast<int64_t>(h) * a.H_up + s;
@@ -375,55 +412,52 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
       }
       if (bits) atomicOr(alive + (t >> 3), bits << (4 * (t & 7)));
     }
+    // theta_i = 0 for every row; stage 2 (after the barrier) stores the detections
+    int32_t *th = a.theta + q * a.ldm;
+    for (int32_t t = threadIdx.x; t < rquads; t += kSampThreads) {
+      if (vec_store && 4 * t + 3 < a.M) {
+        *reinterpret_cast<int4 *>(th + 4 * t) = make_int4(0, 0, 0, 0);
+      } else {
+        for (int32_t i = 4 * t; i < min(a.M, 4 * t + 4); ++i) th[i] = 0;
+      }
+    }
     __syncthreads();
 
     // stage 2: each row i draws theta_i from the row of C'_k (clutter kappa,
     // surviving gated columns in ascending order), inverse CDF in fp32 (R26);
-    // Philox block (i/4, h, step, 3<<24 | s), word i%4
-    int32_t *th = a.theta + q * a.ldm;
+    // Philox block (i/4, h, step, 3<<24 | s), word i%4.  Rows with a parent entry only.
     uint64_t fp = 0ull;
-    auto row = [&](int32_t i, uint32_t word) -> int32_t {
+    auto row = [&](int32_t i, uint32_t word) {
       const int32_t pick = draw_row(rp, cl, vl, lvl, alive, a.kappa, ln_kappa, i, word, lw);
       if (pick > 0) {
         atomicOr(det + ((pick - 1) >> 5), 1u << ((pick - 1) & 31));
         if (a.n_count > 0) atomicAdd(cnt + pick - 1, 1);
         // fingerprint over the detected rows only (theta is 0 elsewhere)
         fp += fp_term(static_cast<uint32_t>(pick), static_cast<uint64_t>(a.ldt) + i);
+        th[i] = pick;
       }
-      return pick;
     };
-    if (rows4) {
-      // thread = four rows (one Philox block)
-      for (int32_t t = threadIdx.x; t < rquads; t += kSampThreads) {
+    if (row_mode) {
+      // thread = one row (its own Philox block: latency over issue when rows are few)
+      for (int32_t k = threadIdx.x; k < nzr_n; k += kSampThreads) {
+        const int32_t i = nzr[k];
+        const u32x4 r = philox4x32_10(u32x4{static_cast<uint32_t>(i >> 2), static_cast<uint32_t>(h), a.step,
+                                            (kDomainAssoc << 24) | static_cast<uint32_t>(s)},
+                                      a.key0, a.key1);
+        row(i, word_of(r, i & 3));
+      }
+    } else {
+      // thread = one quad of rows (one Philox block), its non-empty rows in turn
+      for (int32_t v = threadIdx.x; v < nzq_n; v += kSampThreads) {
+        const uint32_t ent = static_cast<uint32_t>(nzq[v]);
+        const int32_t t = static_cast<int32_t>(ent >> 4);
         const u32x4 r = philox4x32_10(u32x4{static_cast<uint32_t>(t), static_cast<uint32_t>(h), a.step,
                                             (kDomainAssoc << 24) | static_cast<uint32_t>(s)},
                                       a.key0, a.key1);
-        int32_t pk[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) pk[e] = 4 * t + e < a.M ? row(4 * t + e, word_of(r, e)) : 0;
-        if (vec_store && 4 * t + 3 < a.M) {
-          *reinterpret_cast<int4 *>(th + 4 * t) = make_int4(pk[0], pk[1], pk[2], pk[3]);
-        } else {
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if (4 * t + e < a.M) th[4 * t + e] = pk[e];
+        for (uint32_t m = ent & 0xFu; m != 0u; m &= m - 1u) {
+          const int e = __ffs(m) - 1;
+          row(4 * t + e, word_of(r, e));
         }
-      }
-    } else {
-      // thread = one row; the Philox block of rows 4t..4t+3 is computed by the lane
-      // holding row 4t and shuffled to the three lanes after it (rows are lane-contiguous)
-      const int lane = threadIdx.x & 31;
-      for (int32_t i0 = 0; i0 < a.M; i0 += kSampThreads) {
-        const int32_t i = i0 + threadIdx.x;
-        u32x4 r{0u, 0u, 0u, 0u};
-        if ((i & 3) == 0 && i < a.M)
-          r = philox4x32_10(u32x4{static_cast<uint32_t>(i >> 2), static_cast<uint32_t>(h), a.step,
-                                  (kDomainAssoc << 24) | static_cast<uint32_t>(s)},
-                            a.key0, a.key1);
-        const int src = lane & ~3;
-        const u32x4 rr{__shfl_sync(0xffffffffu, r.a, src), __shfl_sync(0xffffffffu, r.b, src),
-                       __shfl_sync(0xffffffffu, r.c, src), __shfl_sync(0xffffffffu, r.d, src)};
-        if (i < a.M) th[i] = row(i, word_of(rr, i & 3));
       }
     }
     __syncthreads();
@@ -462,7 +496,10 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
     if (threadIdx.x == 0) {
       const double lws = (red_d[0] + red_d[1]) + (red_d[2] + red_d[3]);
       const int32_t ms = (red_i[0] + red_i[1]) + (red_i[2] + red_i[3]);
-      a.logw[q] = __ldg(a.parent_logw + h) + lws + static_cast<double>(ms) * ln_miss;
+      // rows without a parent entry: theta_i = 0 with ln kappa each
+      const int32_t n_empty = a.M - nzr_n;
+      const double l_empty = n_empty > 0 ? static_cast<double>(n_empty) * ln_kappa : 0.0;
+      a.logw[q] = __ldg(a.parent_logw + h) + (lws + l_empty) + static_cast<double>(ms) * ln_miss;
       if (a.hash) a.hash[q] = (red_u[0] + red_u[1]) + (red_u[2] + red_u[3]);
     }
   }
@@ -789,7 +826,9 @@ cudaError_t launch_assoc_sample(const SampleArgs &a, int sm_count, cudaStream_t 
   const int64_t n = static_cast<int64_t>(a.H_old) * groups;
   const size_t tquads = (static_cast<size_t>(a.T) + 3) / 4;
   const size_t fixed = sizeof(int32_t) * (static_cast<size_t>(a.M) + 1) + sizeof(uint32_t) * 3 * static_cast<size_t>(a.ldt) +
-                       sizeof(int32_t) * tquads + (a.n_count > 0 ? sizeof(int32_t) * static_cast<size_t>(a.T) : 0) + 16;
+                       sizeof(int32_t) * tquads + sizeof(int32_t) * ((static_cast<size_t>(a.M) + 3) / 4) +
+                       (a.M < 2 * kSampThreads ? sizeof(int32_t) * static_cast<size_t>(a.M) : 0) +
+                       (a.n_count > 0 ? sizeof(int32_t) * static_cast<size_t>(a.T) : 0) + 16;
   if (fixed > 200 * 1024) return cudaErrorInvalidValue;
   // shared memory per CTA sized so the grid runs in one wave where it can: the row
   // cache first (up to kRowCapMax entries), then the parent quads' logs
