@@ -121,9 +121,8 @@ struct SampleArgs {
   int64_t ldm;
   double *logw;
   unsigned long long *hash;
-  int32_t row_cap;  // set by the launcher: filtered row entries that fit in shared memory
   int32_t spc;      // set by the launcher: samples per CTA
-  int32_t quad_cap; // set by the launcher: parent track quads whose logs fit in shared memory
+  int32_t pool;     // set by the launcher: shared-memory bytes the kernel carves at run time
 };
 
 struct DedupArgs {

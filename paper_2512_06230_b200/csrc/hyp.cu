@@ -188,8 +188,7 @@ __device__ __forceinline__ int32_t block_excl_scan_128(int32_t v, int32_t *red, 
 // rows (columns outside the parent are never alive), so the integer outcomes do not
 // depend on any of this.
 constexpr int kSampPerCtaMax = 16;
-constexpr int kRowCapMax = 1024;   // filtered entries held in shared memory (16 KB)
-constexpr int kQuadCapMax = 384;   // parent track quads with cached logs (26 KB)
+constexpr int kFilterBatch = 8;  // CSR words (32 entries) a warp loads per round of the row filter
 
 __device__ __forceinline__ uint32_t word_of(const u32x4 &r, int e) {
   return e == 0 ? r.a : e == 1 ? r.b : e == 2 ? r.c : r.d;
@@ -242,12 +241,9 @@ __device__ __forceinline__ int32_t draw_row(const int32_t *rp, const int32_t *cl
 
 __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  double *flv = reinterpret_cast<double *>(smraw);                 // [row_cap]
-  double *qls = flv + a.row_cap;                                   // [4 quad_cap] ln P_S
-  double *qld = qls + 4 * a.quad_cap;                              // [4 quad_cap] ln(1 - P_S)
-  float *fval = reinterpret_cast<float *>(qld + 4 * a.quad_cap);   // [row_cap]
-  int32_t *fcol = reinterpret_cast<int32_t *>(fval + a.row_cap);   // [row_cap]
-  int32_t *frp = fcol + a.row_cap;                                 // [M + 1]
+  // a.pool bytes at the front, carved at run time (below); fixed arrays after it
+  unsigned char *pool = smraw;
+  int32_t *frp = reinterpret_cast<int32_t *>(smraw + a.pool);      // [M + 1]
   int32_t *pq = frp + a.M + 1;                                     // [(T + 3) / 4]
   int32_t *nzq = pq + ((a.T + 3) >> 2);                            // [(M + 3) / 4]
   const bool row_mode = a.M < 2 * kSampThreads;
@@ -268,8 +264,107 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
   for (int32_t k = threadIdx.x; k < a.ldt; k += kSampThreads) pmask[k] = __ldg(pm + k);
   __syncthreads();
   const int32_t tquads = (a.T + 3) >> 2;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  auto in_parent = [&](int32_t j) { return ((pmask[j >> 5] >> (j & 31)) & 1u) != 0u; };
 
-  // ---- the parent's track quads (ascending) with the logs of their tracks
+  // ---- the parent's rows (pool), filtered in ascending column order.  A stable
+  // compaction of the CSR's entry stream: a bitmap of the kept entries (coalesced, one
+  // ballot per 32 entries) and its word prefix K give row i's start K(row_ptr[i]) and
+  // entry x's slot K(x).  Rows too many for the bitmap: a count and a fill pass per row.
+  const int32_t r0 = __ldg(a.row_ptr), r1 = __ldg(a.row_ptr + a.M);
+  const int32_t nwords = (r1 - r0 + 31) >> 5;
+  size_t rows_at = 0;  // pool offset of the filtered rows
+  int32_t kept = 0;
+  if (8 * static_cast<int64_t>(nwords) <= a.pool / 2) {
+    uint32_t *kb = reinterpret_cast<uint32_t *>(pool);
+    int32_t *kbp = reinterpret_cast<int32_t *>(kb + nwords);
+    // a warp takes kFilterBatch consecutive words per round, all loads issued first
+    for (int32_t w0 = wid * kFilterBatch; w0 < nwords; w0 += kSampThreads / 32 * kFilterBatch) {
+      int32_t jj[kFilterBatch];
+#pragma unroll
+      for (int u = 0; u < kFilterBatch; ++u) {
+        const int32_t x = r0 + 32 * (w0 + u) + lane;
+        jj[u] = x < r1 ? __ldg(a.col + x) : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < kFilterBatch; ++u) {
+        const uint32_t word = __ballot_sync(0xffffffffu, jj[u] >= 0 && in_parent(jj[u]));
+        if (lane == 0 && w0 + u < nwords) kb[w0 + u] = word;
+      }
+    }
+    __syncthreads();
+    for (int32_t w0 = 0; w0 < nwords; w0 += kSampThreads) {
+      const int32_t w = w0 + threadIdx.x;
+      int32_t tot;
+      const int32_t ex = block_excl_scan_128(w < nwords ? __popc(kb[w]) : 0, red_i, tot);
+      if (w < nwords) kbp[w] = kept + ex;
+      kept += tot;
+    }
+    __syncthreads();
+    const int32_t total = kept;
+    auto K = [&](int32_t x) -> int32_t {
+      const int32_t d = x - r0, w = d >> 5;
+      return w < nwords ? kbp[w] + __popc(kb[w] & ((1u << (d & 31)) - 1u)) : total;
+    };
+    for (int32_t i = threadIdx.x; i <= a.M; i += kSampThreads) frp[i] = K(__ldg(a.row_ptr + i));
+    rows_at = static_cast<size_t>(8) * nwords;
+    if (rows_at + 16 * static_cast<size_t>(kept) <= static_cast<size_t>(a.pool)) {
+      double *flv = reinterpret_cast<double *>(pool + rows_at);
+      float *fval = reinterpret_cast<float *>(flv + kept);
+      int32_t *fcol = reinterpret_cast<int32_t *>(fval + kept);
+      for (int32_t w = wid; w < nwords; w += kSampThreads / 32) {
+        const uint32_t word = kb[w];
+        if (!((word >> lane) & 1u)) continue;
+        const int32_t x = r0 + 32 * w + lane;
+        const int32_t o = kbp[w] + __popc(word & ((1u << lane) - 1u));
+        fcol[o] = __ldg(a.col + x);
+        fval[o] = __ldg(a.val + x);
+        flv[o] = __ldg(a.ln_val + x);
+      }
+    }
+  } else {
+    for (int32_t i0 = 0; i0 < a.M; i0 += kSampThreads) {
+      const int32_t i = i0 + threadIdx.x;
+      int32_t c = 0;
+      if (i < a.M) {
+        const int32_t e1 = __ldg(a.row_ptr + i + 1);
+        for (int32_t x = __ldg(a.row_ptr + i); x < e1; ++x) c += in_parent(__ldg(a.col + x));
+      }
+      int32_t tot;
+      const int32_t ex = block_excl_scan_128(c, red_i, tot);
+      if (i < a.M) frp[i] = kept + ex;
+      kept += tot;
+    }
+    if (threadIdx.x == 0) frp[a.M] = kept;
+    __syncthreads();
+    if (16 * static_cast<size_t>(kept) <= static_cast<size_t>(a.pool)) {
+      double *flv = reinterpret_cast<double *>(pool);
+      float *fval = reinterpret_cast<float *>(flv + kept);
+      int32_t *fcol = reinterpret_cast<int32_t *>(fval + kept);
+      for (int32_t i = threadIdx.x; i < a.M; i += kSampThreads) {
+        int32_t o = frp[i];
+        const int32_t e1 = __ldg(a.row_ptr + i + 1);
+        for (int32_t x = __ldg(a.row_ptr + i); x < e1; ++x) {
+          const int32_t j = __ldg(a.col + x);
+          if (in_parent(j)) {
+            fcol[o] = j;
+            fval[o] = __ldg(a.val + x);
+            flv[o] = __ldg(a.ln_val + x);
+            ++o;
+          }
+        }
+      }
+    }
+  }
+  if (threadIdx.x == 0) use_smem = rows_at + 16 * static_cast<size_t>(kept) <= static_cast<size_t>(a.pool);
+  __syncthreads();
+
+  // ---- the parent's track quads (ascending) with the logs of their tracks (the first
+  // quad_cap of them, in the pool after the rows)
+  const size_t quads_at = use_smem ? rows_at + 16 * static_cast<size_t>(kept) : 0;
+  const int32_t quad_cap = static_cast<int32_t>((static_cast<size_t>(a.pool) - quads_at) / 64);
+  double *qls = reinterpret_cast<double *>(pool + quads_at);   // [4 quad_cap] ln P_S
+  double *qld = qls + 4 * quad_cap;                            // [4 quad_cap] ln(1 - P_S)
   {
     int32_t carry = 0;
     for (int32_t t0 = 0; t0 < tquads; t0 += kSampThreads) {
@@ -279,7 +374,7 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
       const int32_t ex = block_excl_scan_128(qbits != 0u, red_i, tot);
       const int32_t slot = carry + ex;
       if (qbits != 0u) pq[slot] = t;
-      if (qbits != 0u && slot < a.quad_cap) {
+      if (qbits != 0u && slot < quad_cap) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           if (!((qbits >> e) & 1u)) continue;
@@ -292,48 +387,10 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
     }
     if (threadIdx.x == 0) n_quads = carry;
   }
-  // ---- the parent's rows (shared memory), filtered in ascending column order
-  {
-    int32_t carry = 0;
-    for (int32_t i0 = 0; i0 < a.M; i0 += kSampThreads) {
-      const int32_t i = i0 + threadIdx.x;
-      int32_t c = 0;
-      if (i < a.M) {
-        const int32_t e1 = __ldg(a.row_ptr + i + 1);
-        for (int32_t x = __ldg(a.row_ptr + i); x < e1; ++x) {
-          const int32_t j = __ldg(a.col + x);
-          c += (pmask[j >> 5] >> (j & 31)) & 1u;
-        }
-      }
-      int32_t tot;
-      const int32_t ex = block_excl_scan_128(c, red_i, tot);
-      if (i < a.M) frp[i] = carry + ex;
-      carry += tot;
-    }
-    if (threadIdx.x == 0) {
-      frp[a.M] = carry;
-      use_smem = carry <= a.row_cap;
-    }
-    __syncthreads();
-    if (use_smem) {
-      for (int32_t i = threadIdx.x; i < a.M; i += kSampThreads) {
-        int32_t o = frp[i];
-        const int32_t e1 = __ldg(a.row_ptr + i + 1);
-        for (int32_t x = __ldg(a.row_ptr + i); x < e1; ++x) {
-          const int32_t j = __ldg(a.col + x);
-          if ((pmask[j >> 5] >> (j & 31)) & 1u) {
-            fcol[o] = j;
-            fval[o] = __ldg(a.val + x);
-            flv[o] = __ldg(a.ln_val + x);
-            ++o;
-          }
-        }
-      }
-    }
-    __syncthreads();
-  }
   const bool sm_rows = use_smem;
-  const int32_t nq = n_quads;
+  const double *flv = reinterpret_cast<const double *>(pool + rows_at);
+  const float *fval = reinterpret_cast<const float *>(flv + kept);
+  const int32_t *fcol = reinterpret_cast<const int32_t *>(fval + kept);
   const int32_t *rp = sm_rows ? frp : a.row_ptr;
   const int32_t *cl = sm_rows ? fcol : a.col;
   const float *vl = sm_rows ? fval : a.val;
@@ -376,7 +433,7 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
     }
     __syncthreads();
   }
-  const int32_t nzq_n = n_nzq, nzr_n = n_nzr;
+  const int32_t nzq_n = n_nzq, nzr_n = n_nzr, nq = n_quads;
   const bool vec_store = ((a.ldm & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.theta) & 15) == 0);
   for (int32_t s = s0; s < s1; ++s) {
     const int64_t q = static_cast<int64_t>(h) * a.H_up + s;
@@ -401,7 +458,7 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
         const int32_t j = 4 * t + e;
         const float thr = __fsub_rn(1.0f, __ldg(a.d_prob + j));
         const bool al = uniform24(word_of(r, e)) < thr;
-        if (v < a.quad_cap) {
+        if (v < quad_cap) {
           lw += al ? qls[4 * v + e] : qld[4 * v + e];
         } else {
           const double ps = static_cast<double>(__ldg(a.p_s + j));
@@ -830,17 +887,20 @@ cudaError_t launch_assoc_sample(const SampleArgs &a, int sm_count, cudaStream_t 
                        (a.M < 2 * kSampThreads ? sizeof(int32_t) * static_cast<size_t>(a.M) : 0) +
                        (a.n_count > 0 ? sizeof(int32_t) * static_cast<size_t>(a.T) : 0) + 16;
   if (fixed > 200 * 1024) return cudaErrorInvalidValue;
-  // shared memory per CTA sized so the grid runs in one wave where it can: the row
-  // cache first (up to kRowCapMax entries), then the parent quads' logs
+  // shared memory per CTA sized so the grid runs in one wave where it can; the pool
+  // beyond the fixed arrays holds the kept-entry bitmap, the parent's rows and the
+  // parent quads' logs, carved by the kernel
   const int64_t sms = sm_count > 0 ? sm_count : 148;
   const int64_t per_sm = std::min<int64_t>(16, std::max<int64_t>(1, (n + sms - 1) / sms));
-  const size_t target = std::max(fixed, std::min<size_t>(200 * 1024, (227 * 1024) / per_sm - 2048));
-  const size_t per = sizeof(double) + sizeof(float) + sizeof(int32_t);
-  const size_t per_q = 8 * sizeof(double);
-  b.row_cap = static_cast<int32_t>(std::min(static_cast<size_t>(kRowCapMax), (target - fixed) / per));
-  const size_t rest = target - fixed - static_cast<size_t>(b.row_cap) * per;
-  b.quad_cap = static_cast<int32_t>(std::min(std::min(tquads, static_cast<size_t>(kQuadCapMax)), rest / per_q));
-  const size_t smem = static_cast<size_t>(b.row_cap) * per + static_cast<size_t>(b.quad_cap) * per_q + fixed;
+  const size_t target = std::min<size_t>(200 * 1024, (227 * 1024) / per_sm - 2048);
+  static const int pool_env = [] {  // test hook: force a small pool (every fallback path)
+    const char *e = std::getenv("GLMB_SAMPLER_POOL");
+    return e ? std::atoi(e) : 0;
+  }();
+  size_t pool = target > fixed + 1024 ? (target - fixed) & ~static_cast<size_t>(15) : 1024;
+  if (pool_env > 0) pool = static_cast<size_t>(pool_env) & ~static_cast<size_t>(15);
+  b.pool = static_cast<int32_t>(pool);
+  const size_t smem = pool + fixed;
   cudaError_t e = cudaFuncSetAttribute(assoc_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;

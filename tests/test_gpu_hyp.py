@@ -364,3 +364,22 @@ def test_assoc_sample_count_prior(L, orc, name):
     np.testing.assert_array_equal(al, r_al)
     np.testing.assert_array_equal(th[:, :M], r_th)
     _check_logw(lw, r_lw)
+
+
+@pytest.mark.parametrize("pool", [1024, 4096])
+def test_assoc_sample_small_pool(pool):
+    """The sampler's shared-memory fallbacks: GLMB_SAMPLER_POOL forces a small pool, so the
+    row filter takes the per-row passes (1 KB: no room for the kept-entry bitmap) or keeps
+    the bitmap but walks the global CSR, and the ln P_S cache covers few or no parent
+    quads.  The oracle parity tests above must pass unchanged (run in a subprocess: the
+    launcher reads the variable once)."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, GLMB_SAMPLER_POOL=str(pool))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_hyp.py"), "-k", "assoc_sample_vs_oracle or count_prior",
+                        "-m", "gpu"], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "passed" in r.stdout
