@@ -564,7 +564,11 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
 
 // ------------------------------------------------------------------ dedup
 // One CTA per parent: sample s is a duplicate iff some s2 < s of the same parent
-// has the same fingerprint and the same (alive, theta) words.
+// has the same fingerprint and the same (alive, theta) words.  Per chunk of 256
+// samples: each thread finds its sample's first earlier sample with an equal
+// fingerprint (hashes tiled through shared memory), the warps then compare those
+// pairs word by word (coalesced), and only a fingerprint collision (equal hash,
+// different sample) sends its thread on to the later candidates.
 constexpr int kDedupThreads = 256, kDedupTile = 2048;
 
 __device__ bool same_sample(const DedupArgs &a, int64_t q1, int64_t q2) {
@@ -579,8 +583,11 @@ __device__ bool same_sample(const DedupArgs &a, int64_t q1, int64_t q2) {
 
 __global__ void __launch_bounds__(kDedupThreads) dedup_kernel(DedupArgs a) {
   __shared__ unsigned long long hs[kDedupTile];
+  __shared__ int32_t cand[kDedupThreads];
+  __shared__ uint8_t same[kDedupThreads];
   const int32_t h = blockIdx.x;
   const int64_t base = static_cast<int64_t>(h) * a.H_up;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (a.n_parents != nullptr && h >= __ldg(a.n_parents)) {  // inactive parent slot: no candidates
     for (int32_t s = threadIdx.x; s < a.H_up; s += kDedupThreads) a.unique[base + s] = 0;
     return;
@@ -588,23 +595,46 @@ __global__ void __launch_bounds__(kDedupThreads) dedup_kernel(DedupArgs a) {
   for (int32_t s0 = 0; s0 < a.H_up; s0 += kDedupThreads) {
     const int32_t s = s0 + threadIdx.x;
     const unsigned long long mine = s < a.H_up ? a.hash[base + s] : 0ull;
-    bool dup = false;
+    int32_t c = -1;
     const int32_t s_hi = min(a.H_up, s0 + kDedupThreads);  // largest s of this chunk + 1
     for (int32_t t0 = 0; t0 < s_hi; t0 += kDedupTile) {
       __syncthreads();
       for (int32_t k = threadIdx.x; k < kDedupTile && t0 + k < s_hi; k += kDedupThreads) hs[k] = a.hash[base + t0 + k];
       __syncthreads();
-      if (s < a.H_up && !dup) {
+      if (s < a.H_up && c < 0) {
         const int32_t lim = min(kDedupTile, s - t0);
         for (int32_t k = 0; k < lim; ++k) {
-          if (hs[k] == mine && same_sample(a, base + s, base + t0 + k)) {
-            dup = true;
+          if (hs[k] == mine) {
+            c = t0 + k;
             break;
           }
         }
       }
     }
-    if (s < a.H_up) a.unique[base + s] = dup ? 0 : 1;
+    cand[threadIdx.x] = s < a.H_up ? c : -1;
+    __syncthreads();
+    for (int r = wid; r < kDedupThreads; r += kDedupThreads / 32) {
+      const int32_t k = cand[r];
+      if (k < 0) continue;
+      const int64_t q1 = base + s0 + r, q2 = base + k;
+      const uint32_t *A1 = a.alive + q1 * a.ldt, *A2 = a.alive + q2 * a.ldt;
+      const int32_t *T1 = a.theta + q1 * a.ldm, *T2 = a.theta + q2 * a.ldm;
+      bool diff = false;
+      for (int32_t w = lane; w < a.ldt; w += 32) diff |= A1[w] != A2[w];
+      for (int32_t i = lane; i < a.M; i += 32) diff |= T1[i] != T2[i];
+      const bool any = __any_sync(0xffffffffu, diff);
+      if (lane == 0) same[r] = !any;
+    }
+    __syncthreads();
+    if (s < a.H_up) {
+      bool dup = false;
+      if (c >= 0) {
+        dup = same[threadIdx.x];
+        for (int32_t k = c + 1; !dup && k < s; ++k)  // fingerprint collision: later candidates
+          dup = a.hash[base + k] == mine && same_sample(a, base + s, base + k);
+      }
+      a.unique[base + s] = dup ? 0 : 1;
+    }
   }
 }
 
@@ -634,7 +664,7 @@ __global__ void __launch_bounds__(kPruneThreads) prune_kernel(PruneArgs a) {
   __shared__ int32_t si[32];
   __shared__ uint32_t hist[256];
   __shared__ unsigned long long prefix_s;
-  __shared__ int32_t need_s, carry_s, tiecarry_s;
+  __shared__ int32_t need_s;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int32_t n = a.n;
 
@@ -667,9 +697,13 @@ __global__ void __launch_bounds__(kPruneThreads) prune_kernel(PruneArgs a) {
     return;
   }
   // (2) s = sum exp(lw - max), fixed order
+  // (the exponentials are parked in the key buffer for (3))
   double acc = 0.0;
-  for (int32_t c = threadIdx.x; c < n; c += kPruneThreads)
-    if (a.unique[c]) acc += exp(a.logw[c] - mx);
+  for (int32_t c = threadIdx.x; c < n; c += kPruneThreads) {
+    const double e = a.unique[c] ? exp(a.logw[c] - mx) : 0.0;
+    a.keys[c] = static_cast<unsigned long long>(__double_as_longlong(e));
+    acc += e;
+  }
   acc = warp_sum_d(acc);
   if (lane == 0) sd[wid] = acc;
   __syncthreads();
@@ -684,7 +718,7 @@ __global__ void __launch_bounds__(kPruneThreads) prune_kernel(PruneArgs a) {
   for (int32_t c = threadIdx.x; c < n; c += kPruneThreads) {
     unsigned long long key = 0ull;
     if (a.unique[c]) {
-      const double w = exp(a.logw[c] - mx) / ssum;
+      const double w = __longlong_as_double(static_cast<long long>(a.keys[c])) / ssum;
       if (w >= a.tau || c == arg) key = static_cast<unsigned long long>(__double_as_longlong(w)) + 1ull;
     }
     a.keys[c] = key;
@@ -766,41 +800,41 @@ __global__ void __launch_bounds__(kPruneThreads) prune_kernel(PruneArgs a) {
     ties = need_s;  // how many keys == thr to keep
     __syncthreads();
   }
-  // (5) compaction in index order: kept = key > thr (select) or key >= thr (no select)
-  if (threadIdx.x == 0) { carry_s = 0; tiecarry_s = 0; }
-  __syncthreads();
-  for (int32_t base = 0; base < n; base += kPruneThreads) {
-    const int32_t c = base + threadIdx.x;
-    const unsigned long long key = c < n ? a.keys[c] : 0ull;
-    const bool gt = select ? key > thr : key >= thr;
-    const bool tie = select && key == thr;
-    // rank of this tie among ties (index order)
-    const uint32_t tb = __ballot_sync(0xffffffffu, tie);
-    __syncthreads();
-    if (lane == 0) { si[wid] = __popc(tb); }
-    __syncthreads();
-    int32_t tie_before = tiecarry_s;
-    for (int q = 0; q < wid; ++q) tie_before += si[q];
-    tie_before += __popc(tb & ((1u << lane) - 1u));
-    int32_t tie_tot = 0;
-    for (int q = 0; q < 32; ++q) tie_tot += si[q];
-    const bool keep = gt || (tie && tie_before < ties);
-    const uint32_t kb = __ballot_sync(0xffffffffu, keep);
-    __syncthreads();
-    if (lane == 0) si[wid] = __popc(kb);
-    __syncthreads();
-    int32_t pos = carry_s;
-    for (int q = 0; q < wid; ++q) pos += si[q];
-    pos += __popc(kb & ((1u << lane) - 1u));
-    int32_t keep_tot = 0;
-    for (int q = 0; q < 32; ++q) keep_tot += si[q];
-    if (keep && pos < a.cap2) {
-      skey[pos] = key;
-      sidx[pos] = c;
+  // (5) compaction in index order: kept = key > thr (select) or key >= thr (no select),
+  // plus the first `ties` keys == thr.  Slot = (# gt before) + min(# ties before, ties);
+  // both counts from one per-warp round (packed in 16-bit halves), scanned by every warp.
+  {
+    int32_t carry_gt = 0, carry_tie = 0;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    for (int32_t base = 0; base < n; base += kPruneThreads) {
+      const int32_t c = base + threadIdx.x;
+      const unsigned long long key = c < n ? a.keys[c] : 0ull;
+      const bool gt = select ? key > thr : key >= thr;
+      const bool tie = select && key == thr;
+      const uint32_t gtb = __ballot_sync(0xffffffffu, gt), tb = __ballot_sync(0xffffffffu, tie);
+      if (lane == 0) si[wid] = __popc(gtb) | (__popc(tb) << 16);
+      __syncthreads();
+      const int32_t v = si[lane];
+      int32_t incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
+      const int32_t before = __shfl_sync(0xffffffffu, incl - v, wid);
+      const int32_t gt_before = carry_gt + (before & 0xffff) + __popc(gtb & lt_mask);
+      const int32_t tie_before = carry_tie + (before >> 16) + __popc(tb & lt_mask);
+      const bool keep = gt || (tie && tie_before < ties);
+      const int32_t pos = gt_before + min(tie_before, ties);
+      if (keep && pos < a.cap2) {
+        skey[pos] = key;
+        sidx[pos] = c;
+      }
+      carry_gt += total & 0xffff;
+      carry_tie += total >> 16;
+      __syncthreads();
     }
-    __syncthreads();
-    if (threadIdx.x == 0) { carry_s += keep_tot; tiecarry_s += tie_tot; }
-    __syncthreads();
   }
   // pad to cap2 with sentinels (key 0 sorts last)
   for (int32_t p = nk + threadIdx.x; p < a.cap2; p += kPruneThreads) {
