@@ -479,7 +479,8 @@ glmb_status glmb_reweight_pairs(const glmb_particles *src, const float *Z, int32
   if ((reinterpret_cast<uintptr_t>(w_out) & 15u) != 0) return GLMB_ERR_ALIGNMENT;
   if (M > 0 && (reinterpret_cast<uintptr_t>(Z) & 7u) != 0) return GLMB_ERR_ALIGNMENT;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  GLMB_TRY(bind_stream(s, nullptr));
+  int dev = 0;
+  GLMB_TRY(bind_stream(s, &dev));
   const double rxx = Rxx, rxy = Rxy, ryy = Ryy;
   const double det = rxx * ryy - rxy * rxy;
   const double h = 0.5 * 1.4426950408889634074;
@@ -493,6 +494,7 @@ glmb_status glmb_reweight_pairs(const glmb_particles *src, const float *Z, int32
   a.log_norm = log_norm; a.flags = flags;
   a.pair_track = pair_track; a.pair_ptr = pair_ptr; a.pair_meas = pair_meas; a.n_units_dev = n_pairs;
   a.ld_out = ld_out; a.ess = ess;
+  a.units_cap = 4 * (g_sm_count[dev] > 0 ? g_sm_count[dev] : 148);  // grid-stride over the device count
   return from_cuda(glmb::launch_reweight(a, s));
 }
 
@@ -509,7 +511,8 @@ glmb_status glmb_resample(const glmb_particles *src, int32_t K, const int32_t *n
   if (pair_track == nullptr || w == nullptr) return GLMB_ERR_INVALID_ARG;
   if (ldw < src->n_particles || (ldw & 3) || (reinterpret_cast<uintptr_t>(w) & 15u)) return GLMB_ERR_ALIGNMENT;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  GLMB_TRY(bind_stream(s, nullptr));
+  int dev = 0;
+  GLMB_TRY(bind_stream(s, &dev));
   glmb::ResampleArgs a{};
   a.x = src->x; a.y = src->y; a.v = src->v; a.psi = src->psi; a.omega = src->omega; a.ld = src->ld;
   a.P = src->n_particles; a.pair_track = pair_track; a.w = w; a.ldw = ldw; a.K = K; a.n_units_dev = n_pairs;
@@ -517,7 +520,7 @@ glmb_status glmb_resample(const glmb_particles *src, int32_t K, const int32_t *n
   a.ld_out = out->ld;
   a.key0 = static_cast<uint32_t>(seed); a.key1 = static_cast<uint32_t>(seed >> 32); a.step = step;
   a.flags = flags;
-  return from_cuda(glmb::launch_resample(a, s));
+  return from_cuda(glmb::launch_resample(a, g_sm_count[dev], s));
 }
 
 // ------------------------------------------------------------------ tracker loop (f4)

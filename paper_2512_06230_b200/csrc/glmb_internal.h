@@ -76,6 +76,8 @@ struct ReweightArgs {
   const int32_t *n_units_dev;  // optional device count of valid units (<= T)
   int64_t ld_out;
   float *ess;
+  int32_t units_cap;  // pair mode: > 0 caps the grid at this many units, each cluster looping
+                      // over units u, u + grid, ... < min(T, *n_units_dev) (T is a capacity there)
 };
 
 // ---- hypothesis machinery (hyp.cu)
@@ -195,7 +197,7 @@ struct ResampleArgs {
   uint32_t key0, key1, step;
   uint32_t *flags;                       // bit 1 set when unit k was resampled
 };
-cudaError_t launch_resample(const ResampleArgs &a, cudaStream_t s);
+cudaError_t launch_resample(const ResampleArgs &a, int sm_count, cudaStream_t s);
 
 // ---- tracker loop (pairs.cu)
 struct NextParentsArgs {

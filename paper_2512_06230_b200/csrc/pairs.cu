@@ -11,6 +11,8 @@
 // The resampling CDF is built from integer weights W = floor(w 2^26), so the
 // prefix sums, the ESS decision and the ancestors are exact integers: the same
 // on any hardware and in any summation order.
+#include <algorithm>
+
 #include "glmb_device.cuh"
 #include "glmb_internal.h"
 
@@ -275,15 +277,13 @@ __global__ void __launch_bounds__(256) finish_kernel(PairsArgs a) {
 // so the gathers of consecutive slots hit neighbouring addresses.
 // NT threads per pair: 256 for P <= 2048 (short CTAs), 1024 above (more gathers in flight)
 template <int kResThreads>
-__global__ void __launch_bounds__(kResThreads) resample_kernel(ResampleArgs a) {
+__device__ __forceinline__ void resample_unit(const ResampleArgs &a, const int k) {
   extern __shared__ __align__(16) unsigned char rs[];
   unsigned long long *cum = reinterpret_cast<unsigned long long *>(rs);  // [P]
   uint32_t *Wsm = reinterpret_cast<uint32_t *>(cum + a.P);              // [P]
   __shared__ unsigned long long wsum[32];
   __shared__ unsigned long long qlo[kResThreads / 32], qhi[kResThreads / 32];
   __shared__ int do_res;
-  const int k = blockIdx.x;
-  if (a.n_units_dev != nullptr && k >= __ldg(a.n_units_dev)) return;
   const int j = __ldg(a.pair_track + k);
   const int64_t src = static_cast<int64_t>(j) * a.ld, dst = static_cast<int64_t>(k) * a.ld_out;
   const float *wk = a.w + static_cast<int64_t>(k) * a.ldw;
@@ -390,6 +390,17 @@ __global__ void __launch_bounds__(kResThreads) resample_kernel(ResampleArgs a) {
     __stcs(op + g, Ps);
     __stcs(oo + g, Om);
     __stcs(ow + g, make_float4(inv_p, inv_p, inv_p, inv_p));
+  }
+}
+
+// Grid-stride over the device count of pairs (the grid is capped near the resident
+// CTA count: a capacity-sized grid of mostly empty 1024-thread CTAs cost ~0.1 ms).
+template <int kResThreads>
+__global__ void __launch_bounds__(kResThreads) resample_kernel(ResampleArgs a) {
+  const int n = a.n_units_dev != nullptr ? min(a.K, __ldg(a.n_units_dev)) : a.K;
+  for (int k = blockIdx.x; k < n; k += gridDim.x) {
+    resample_unit<kResThreads>(a, k);
+    __syncthreads();  // shared memory is reused by the next unit
   }
 }
 
@@ -505,9 +516,14 @@ cudaError_t launch_assoc_pairs(const PairsArgs &in, void *ws, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_resample(const ResampleArgs &a, cudaStream_t s) {
+cudaError_t launch_resample(const ResampleArgs &a, int sm_count, cudaStream_t s) {
   if (a.K == 0) return cudaSuccess;
   const size_t smem = static_cast<size_t>(a.P) * (sizeof(unsigned long long) + sizeof(uint32_t));
+  // about two waves of resident CTAs (shared memory bounds residency at large P)
+  const int sms = sm_count > 0 ? sm_count : 148;
+  const int per_sm = a.P <= 2048 ? std::max(1, std::min(8, static_cast<int>((200 * 1024) / (smem + 1024))))
+                                 : std::max(1, std::min(2, static_cast<int>((200 * 1024) / (smem + 1024))));
+  const int grid = std::min(a.K, 2 * sms * per_sm);
   if (smem > 40 * 1024) {
     cudaError_t e = a.P <= 2048 ? cudaFuncSetAttribute(resample_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                        static_cast<int>(smem))
@@ -515,8 +531,8 @@ cudaError_t launch_resample(const ResampleArgs &a, cudaStream_t s) {
                                                        static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  if (a.P <= 2048) resample_kernel<256><<<a.K, 256, smem, s>>>(a);
-  else resample_kernel<1024><<<a.K, 1024, smem, s>>>(a);
+  if (a.P <= 2048) resample_kernel<256><<<grid, 256, smem, s>>>(a);
+  else resample_kernel<1024><<<grid, 1024, smem, s>>>(a);
   return cudaGetLastError();
 }
 

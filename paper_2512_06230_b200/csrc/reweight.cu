@@ -305,8 +305,10 @@ __device__ __forceinline__ void ms_merge(double &m, double &s, double &s2, doubl
 // pass and a sum pass, and no per-thread rescaling.  w'_p = 2^(l_p - m_w) *
 // 2^(m_w - m) / s.  Particle loads are issued
 // before the theta scan so the two latencies overlap.
+// One unit (track j in theta mode, pair k in pair mode) by the whole cluster; every
+// path ends with a cluster barrier, so the shared memory is free for the next unit.
 template <int CL, int R>
-__global__ void __launch_bounds__(kThreads, R == 1 ? 5 : (R == 2 ? 3 : 2)) reweight_cluster_kernel(const ReweightArgs a) {
+__device__ __forceinline__ void reweight_unit(const ReweightArgs &a, const int u) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   __shared__ SList S;
@@ -314,9 +316,7 @@ __global__ void __launch_bounds__(kThreads, R == 1 ? 5 : (R == 2 ? 3 : 2)) rewei
   __shared__ uint32_t masks[kRows * kWarps];
   __shared__ double part[3];  // this CTA's (max, sum, sum of squares), read by the peers
   const int crank = static_cast<int>(cluster.block_rank());
-  const int u = blockIdx.x / CL;  // unit: track j (theta mode) or pair k (pair mode)
   const bool pairs = a.pair_track != nullptr;
-  if (a.n_units_dev != nullptr && u >= __ldg(a.n_units_dev)) return;  // whole cluster exits together
   const int j = pairs ? __ldg(a.pair_track + u) : u;
   const int col = a.col_offset + j + 1;
   const int64_t base = static_cast<int64_t>(j) * a.ld;
@@ -479,9 +479,18 @@ __global__ void __launch_bounds__(kThreads, R == 1 ? 5 : (R == 2 ? 3 : 2)) rewei
 }
 
 template <int CL, int R>
+__global__ void __launch_bounds__(kThreads, R == 1 ? 5 : (R == 2 ? 3 : 2)) reweight_cluster_kernel(const ReweightArgs a) {
+  // units u = cluster index, + clusters in the grid, ... (one pass unless the grid is capped)
+  const int n_units = a.n_units_dev != nullptr ? min(a.T, __ldg(a.n_units_dev)) : a.T;
+  const int stride = static_cast<int>(gridDim.x) / CL;
+  for (int u = static_cast<int>(blockIdx.x) / CL; u < n_units; u += stride) reweight_unit<CL, R>(a, u);
+}
+
+template <int CL, int R>
 cudaError_t launch_cluster(const ReweightArgs &a, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(a.T) * CL);
+  const int units = a.units_cap > 0 ? min(a.T, a.units_cap) : a.T;
+  cfg.gridDim = dim3(static_cast<unsigned>(units) * CL);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
