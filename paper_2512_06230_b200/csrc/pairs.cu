@@ -353,13 +353,27 @@ __device__ __forceinline__ void resample_unit(const ResampleArgs &a, const int k
   const unsigned long long U = 2ull * (r.a >> 9) + 1ull;
   const unsigned long long V = (U * S) >> 24;  // U < 2^24, S <= 2^40: no overflow
   const float inv_p = 1.0f / static_cast<float>(a.P);
+  // t_n = floor((n S + V) / P) stepped along the quad: one division per quad, then
+  // quotient and remainder advance by S = qS P + rS
+  const unsigned Pu = static_cast<unsigned>(a.P);
+  const unsigned long long qS = S / Pu;
+  const unsigned rS = static_cast<unsigned>(S - qS * Pu);
   for (int g = threadIdx.x; g < quads; g += kResThreads) {
     float4 X, Y, Vv, Ps, Om;
     int lo = 0;
+    const unsigned long long num0 = static_cast<unsigned long long>(4 * g) * S + V;
+    unsigned long long t = num0 / Pu;
+    unsigned rem = static_cast<unsigned>(num0 - t * Pu);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const int n = 4 * g + e;
-      const unsigned long long t = (static_cast<unsigned long long>(n) * S + V) / static_cast<unsigned>(a.P);
+      if (e > 0) {
+        t += qS;
+        rem += rS;
+        if (rem >= Pu) {
+          rem -= Pu;
+          ++t;
+        }
+      }
       // first m with cum[m] > t (exists: cum[P-1] = S > t).  Slots are non-decreasing in
       // their ancestor: the quad's first slot binary-searches, the next ones step forward
       // from the previous ancestor (a binary search again after 8 steps)
