@@ -283,6 +283,42 @@ def make_line(*, cfg_id, cfg, world, steps, warmup, elapsed_ms, evals_total, pai
 
 
 # ------------------------------------------------------------------ GLMB update
+def verify_fused_gather(st, symm_cols, C_full, G_full, plan, rank, world, dev, stream) -> bool:
+    """Before timing (N > 1): the fused compat + peer-store gather must give every rank
+    exactly the C_k / gate words an NCCL all-gather of glmb_compat's local columns gives
+    (bit-identical by construction).  All ranks agree on the outcome (all_reduce MIN)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2512_06230_b200 import _lib as L
+    from paper_2512_06230_b200.dist import allgather_columns
+    Zk = st.Z[0]
+    M = Zk.shape[0]
+    ok = True
+    try:
+        with torch.cuda.stream(stream):
+            symm_cols.compat(st.particles, Zk, st.R, st.cfg.p_d, st.cfg.kappa, st.cfg.gamma, st.out.C_clutter, stream)
+            symm_cols.barrier(stream)
+            L.glmb_compat(st.particles, Zk, st.R, st.cfg.p_d, st.cfg.kappa, st.cfg.gamma, st.out.C_clutter,
+                          st.out.C_tracks, st.out.gate, stream)
+        torch.cuda.synchronize(dev)
+        allgather_columns(st.out.C_tracks, C_full)
+        allgather_columns(st.out.gate, G_full)
+        torch.cuda.synchronize(dev)
+        ldg_used = (M + 31) // 32
+        for r in range(world):
+            c = plan.cols(r)
+            n_r = len(c)
+            rows = slice(r * plan.per_rank, r * plan.per_rank + n_r)
+            ok &= bool(torch.equal(symm_cols.C[rows, :M], C_full[rows, :M]))
+            ok &= bool(torch.equal(symm_cols.G[rows, :ldg_used], G_full[rows, :ldg_used]))
+    except Exception as e:  # noqa: BLE001
+        print(f"[bench] fused gather check raised {e!r}", file=sys.stderr)
+        ok = False
+    flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    return bool(flag.item())
+
+
 def bench_update(a, st, scene, cfg, dev, stream, L):
     """The hypothesis update and particle loop that consume the step's C_k:
     death_prob -> compat_rows -> assoc_sample -> dedup -> prune -> assoc_pairs ->
@@ -538,6 +574,11 @@ def main():
     for k in range(a.warmup):
         one_step(k)
     torch.cuda.synchronize(dev)
+    if symm_cols is not None and not verify_fused_gather(st, symm_cols, C_full, G_full, plan, rank, world, dev,
+                                                         stream):
+        symm_cols = None   # every rank falls back together (collective decision)
+        gather = "NCCL all_gather_into_tensor of the column blocks (fused gather failed its check)"
+        print("[bench] fused gather disagreed with the NCCL all-gather; using NCCL", file=sys.stderr)
     sampler = ClockSampler(local)
     if world > 1:
         dist.barrier(device_ids=[local])
