@@ -183,11 +183,12 @@ class Particles:
             return glmb_particles(None, None, None, None, None, None, 0, self.P, self.ld)
         if d.stride(2) != 1 or d.stride(1) != self.ld:
             raise GlmbError(-1, "particle storage must be [6][T][ld] with unit stride")
-        ptrs = [d[k].data_ptr() for k in range(6)]
-        if self.w_override is not None:
-            ptrs[5] = self.w_override.data_ptr()
         if not d.is_cuda:
             raise GlmbError(-1, "particles must live in CUDA memory")
+        base, fs = d.data_ptr(), d.stride(0) * 4   # field k at base + k * fs bytes
+        ptrs = [base + k * fs for k in range(6)]
+        if self.w_override is not None:
+            ptrs[5] = self.w_override.data_ptr()
         return glmb_particles(*ptrs, T, self.P, self.ld)
 
 

@@ -91,15 +91,21 @@ class ConvoyTracker:
         self.ldt = self.hu.ldt
         self.parent_mask = torch.zeros(H, self.ldt, dtype=torch.int32, device=dev)
         self.parent_logw = torch.zeros(H, dtype=torch.float64, device=dev)
-        self.n_parents = torch.zeros(1, dtype=torch.int32, device=dev)
         self.est = torch.empty(rows, 3, dtype=torch.float64, device=dev)
         self.count_lp = torch.from_numpy(count_log_prior(cfg, M_max)).to(dev) if cfg.count_prior else None
         self.birth_mean = None
         self.birth_chol = None
         self.n_surv = 0
         self.stream = torch.cuda.Stream(device=dev)
+        # (n_pairs, n_kept, n_parents) live side by side: one 12-byte read-back per update
         self.counts = torch.zeros(3, dtype=torch.int32, device=dev)
+        self.pu.n_pairs = self.counts[0:1]
+        self.hu.n_kept = self.counts[1:2]
+        self.n_parents = self.counts[2:3]
         self.counts_host = torch.zeros(3, dtype=torch.int32).pin_memory()
+        self.Z_host = torch.zeros(max(M_max, 1), 2, dtype=torch.float32).pin_memory()
+        self._ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        self._prm = [None, None]   # cached glmb_update argument blocks, one per particle buffer
         self.est_host = torch.zeros(rows, 3, dtype=torch.float64).pin_memory()
 
     def reset(self, birth_mean: np.ndarray, birth_chol: np.ndarray):
@@ -124,7 +130,7 @@ class ConvoyTracker:
         M = Z.shape[0]
         assert M <= self.M_max
         t0 = time.perf_counter()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0, e1 = self._ev
         src = self.bufs[self.cur]
         dst = self.bufs[1 - self.cur]
         T, B = self.n_surv, cfg.B
@@ -137,9 +143,14 @@ class ConvoyTracker:
                 ev.record(s)
                 evs[name] = ev
 
+        hu, pu = self.hu, self.pu
+        # the hypothesis machinery works on T_k columns (capacity-sized buffers, views)
+        hu.T = Tk
+        pu.T = Tk
+        self.Z_host[:M].numpy()[:] = Z      # pinned staging: the H2D copy is asynchronous
         with torch.cuda.stream(s):
             e0.record(s)
-            self.Z[:M].copy_(torch.from_numpy(Z), non_blocking=True)
+            self.Z[:M].copy_(self.Z_host[:M], non_blocking=True)
             Zk = self.Z[:M]
             self.p_s[:T].fill_(cfg.p_s)
             self.p_s[T:Tk].fill_(cfg.r_birth)
@@ -154,10 +165,6 @@ class ConvoyTracker:
             _lib.glmb_compat(trk, Zk, cfg.R, cfg.p_d, cfg.kappa, cfg.gamma, self.C_clutter[:M],
                              self.C_tracks[:Tk], self.gate[:Tk], s)
             mark("compat")
-            hu, pu = self.hu, self.pu
-            # the hypothesis machinery works on T_k columns (capacity-sized buffers, views)
-            hu.T = Tk
-            pu.T = Tk
             po = pu.pair_of.view(-1)[:cfg.H_max * Tk].view(cfg.H_max, Tk)   # packed [H][T_k]
             if profile:   # stage by stage, an event after each
                 hu.run(self.C_tracks[:Tk], self.gate[:Tk], M, self.p_s[:Tk], self.parent_mask,
@@ -168,29 +175,40 @@ class ConvoyTracker:
                 _lib.glmb_map_estimate(hu.n_kept, po[0], dst.rows(0, self.K_cap), self.est[:Tk], s)
                 mark("map_estimate")
             else:         # one C call enqueues the whole chain (host overhead of one launch sequence)
-                prm = update_params(hu, pu, trk, self.C_tracks[:Tk], self.gate[:Tk], M, Zk, cfg.R, self.p_s[:Tk],
-                                    self.parent_mask, self.parent_logw, cfg.p_d, cfg.kappa, cfg.tau, cfg.seed, k,
-                                    n_parents=self.n_parents, count_lp=self.count_lp,
-                                    out=dst.rows(0, self.K_cap), est=self.est[:Tk])
-                _lib.glmb_update(prm, s)
-            self.counts[0:1].copy_(pu.n_pairs)
-            self.counts[1:2].copy_(hu.n_kept)
-            self.counts[2:3].copy_(self.n_parents)
-            self.counts_host.copy_(self.counts, non_blocking=True)
+                _lib.glmb_update(self._update_params(trk, Tk, M, k), s)
+            self.counts_host.copy_(self.counts, non_blocking=True)   # (n_pairs, n_kept, n_parents)
             e1.record(s)
         s.synchronize()
         self.last_events = evs
         K, n_kept, n_par = (int(v) for v in self.counts_host)
         if K > self.K_cap:
             raise RuntimeError(f"step {k}: {K} unique pairs exceed K_cap = {self.K_cap}")
-        with torch.cuda.stream(s):
-            # kept hypotheses -> parents over the new rows [0, K) and the next births at [K, K + B)
-            _lib.glmb_next_parents(hu.n_kept, hu.keep_w, po, self.K_cap, B, K,
-                                   self.parent_mask, self.parent_logw, self.n_parents, s)
+        # kept hypotheses -> parents over the new rows [0, K) and the next births at [K, K + B)
+        _lib.glmb_next_parents(hu.n_kept, hu.keep_w, po, self.K_cap, B, K,
+                               self.parent_mask, self.parent_logw, self.n_parents, s)
         wall = (time.perf_counter() - t0) * 1e3
         self.n_surv = K
         self.cur = 1 - self.cur
         return UpdateRecord(k, M, Tk, n_par, n_kept, K, e0.elapsed_time(e1), wall)
+
+    def _update_params(self, trk: Particles, Tk: int, M: int, k: int) -> "_lib.glmb_update_params":
+        """The glmb_update argument block of this particle buffer, built once and then only
+        its sizes and step updated (every buffer pointer is fixed)."""
+        cfg, hu, pu = self.cfg, self.hu, self.pu
+        prm = self._prm[self.cur]
+        if prm is None:
+            dst = self.bufs[1 - self.cur]
+            prm = update_params(hu, pu, self.bufs[self.cur].rows(0, self.T_cap), self.C_tracks, self.gate, M,
+                                self.Z, cfg.R, self.p_s, self.parent_mask, self.parent_logw, cfg.p_d, cfg.kappa,
+                                cfg.tau, cfg.seed, k, n_parents=self.n_parents, count_lp=self.count_lp,
+                                out=dst.rows(0, self.K_cap), est=self.est)
+            self._prm[self.cur] = prm
+        prm.T = Tk
+        prm.M = M
+        prm.K_cap = min(pu.K_cap, max(1, hu.h_max * Tk))
+        prm.step = k
+        prm.tracks.n_tracks = Tk
+        return prm
 
     def estimate(self, T_k: int) -> np.ndarray:
         """MAP positions [n, 2] of the last update (host copy; evaluation only)."""
