@@ -369,9 +369,10 @@ glmb_status glmb_compat_rows(int32_t T, int32_t M, const float *C_tracks, int64_
     return GLMB_ERR_INVALID_ARG;
   if (cap > 0 && (col == nullptr || val == nullptr || ln_val == nullptr)) return GLMB_ERR_INVALID_ARG;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  GLMB_TRY(bind_stream(s, nullptr));
+  int dev = 0;
+  GLMB_TRY(bind_stream(s, &dev));
   glmb::RowsArgs a{T, M, gate, ldg, C_tracks, ldc, row_ptr, col, val, ln_val, cap};
-  return from_cuda(glmb::launch_compat_rows(a, s));
+  return from_cuda(glmb::launch_compat_rows(a, g_sm_count[dev], s));
 }
 
 glmb_status glmb_assoc_sample(int32_t H_old, const int32_t *n_parents, int32_t H_up, int32_t T, int32_t M,

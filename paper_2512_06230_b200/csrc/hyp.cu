@@ -52,16 +52,25 @@ __global__ void __launch_bounds__(256) death_prob_kernel(DeathArgs a) {
 }
 
 // ------------------------------------------------------------------ CSR of the gated entries
-// CTA = 32 consecutive rows (one gate word column w), 8 warps; warp k owns the
-// contiguous track chunk [k*ch, (k+1)*ch) so entries come out in ascending j.
+// CTA (w, c) = 32 consecutive rows (gate word column w) x the c-th of gridDim.y track
+// chunks; warp k owns the contiguous sub-chunk k of it, so entries come out in
+// ascending j.  Splitting the tracks over CTAs spreads the fill (and its fp64 logs)
+// over the GPU: with a few word columns (M ~ 100) one CTA per column ran on 4 SMs.
 constexpr int kRowWarps = 32;
 
-__device__ __forceinline__ void row_chunk(int32_t T, int k, int32_t &j0, int32_t &j1) {
-  const int32_t ch = (T + kRowWarps - 1) / kRowWarps;
-  j0 = min(T, k * ch);
-  j1 = min(T, j0 + ch);
+__device__ __forceinline__ void range_part(int32_t lo, int32_t hi, int parts, int k, int32_t &j0, int32_t &j1) {
+  const int32_t ch = (hi - lo + parts - 1) / parts;
+  j0 = min(hi, lo + k * ch);
+  j1 = min(hi, j0 + ch);
 }
 
+__device__ __forceinline__ void row_chunk(int32_t T, int k, int32_t &j0, int32_t &j1) {
+  int32_t c0, c1;
+  range_part(0, T, gridDim.y, blockIdx.y, c0, c1);
+  range_part(c0, c1, kRowWarps, k, j0, j1);
+}
+
+// row totals: each CTA adds its chunk's counts (row_ptr zeroed by the launcher)
 __global__ void __launch_bounds__(kRowWarps * 32) rows_count_kernel(RowsArgs a) {
   __shared__ int32_t cnt[kRowWarps][32];
   const int w = blockIdx.x, lane = threadIdx.x & 31, k = threadIdx.x >> 5;
@@ -76,7 +85,10 @@ __global__ void __launch_bounds__(kRowWarps * 32) rows_count_kernel(RowsArgs a) 
 #pragma unroll
     for (int q = 0; q < kRowWarps; ++q) s += cnt[q][lane];
     const int32_t i = w * 32 + lane;
-    if (i < a.M) a.row_ptr[i] = s;
+    if (i < a.M) {
+      if (gridDim.y == 1) a.row_ptr[i] = s;
+      else if (s) atomicAdd(a.row_ptr + i, s);
+    }
   }
 }
 
@@ -120,16 +132,23 @@ __global__ void __launch_bounds__(1024) rows_scan_kernel(int32_t *row_ptr, int32
 
 __global__ void __launch_bounds__(kRowWarps * 32) rows_fill_kernel(RowsArgs a) {
   __shared__ int32_t cnt[kRowWarps][32];
+  __shared__ int32_t pre[kRowWarps][32];
   const int w = blockIdx.x, lane = threadIdx.x & 31, k = threadIdx.x >> 5;
-  int32_t j0, j1;
-  row_chunk(a.T, k, j0, j1);
+  int32_t c0, c1, j0, j1;
+  range_part(0, a.T, gridDim.y, blockIdx.y, c0, c1);
+  range_part(c0, c1, kRowWarps, k, j0, j1);
+  // entries of this row in the tracks before the CTA's chunk (warp-strided count)
+  int32_t p = 0;
+  for (int32_t j = k; j < c0; j += kRowWarps) p += (__ldg(a.gate + static_cast<int64_t>(j) * a.ldg + w) >> lane) & 1u;
   int32_t c = 0;
   for (int32_t j = j0; j < j1; ++j) c += (__ldg(a.gate + static_cast<int64_t>(j) * a.ldg + w) >> lane) & 1u;
   cnt[k][lane] = c;
+  pre[k][lane] = p;
   __syncthreads();
   const int32_t i = w * 32 + lane;
   if (i >= a.M) return;
   int32_t pos = a.row_ptr[i];
+  for (int q = 0; q < kRowWarps; ++q) pos += pre[q][lane];
   for (int q = 0; q < k; ++q) pos += cnt[q][lane];
   for (int32_t j = j0; j < j1; ++j) {
     if ((__ldg(a.gate + static_cast<int64_t>(j) * a.ldg + w) >> lane) & 1u) {
@@ -889,16 +908,20 @@ cudaError_t launch_death_prob(const DeathArgs &a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_compat_rows(const RowsArgs &a, cudaStream_t s) {
+cudaError_t launch_compat_rows(const RowsArgs &a, int sm_count, cudaStream_t s) {
   const int32_t words = (a.M + 31) / 32;
-  if (a.T > 0 && words > 0) {
-    rows_count_kernel<<<words, kRowWarps * 32, 0, s>>>(a);
-  } else if (a.M > 0) {
+  // track chunks per word column: ~1 CTA per SM in all, >= 64 tracks per chunk
+  const int sms = sm_count > 0 ? sm_count : 148;
+  const int32_t chunks = std::max<int32_t>(1, std::min<int32_t>((sms + words - 1) / std::max<int32_t>(words, 1),
+                                                                (a.T + 63) / 64));
+  if (a.M > 0 && (chunks > 1 || a.T == 0)) {  // chunked counts accumulate atomically
     cudaError_t e = cudaMemsetAsync(a.row_ptr, 0, sizeof(int32_t) * a.M, s);
     if (e != cudaSuccess) return e;
   }
+  const dim3 grid(static_cast<unsigned>(words), static_cast<unsigned>(chunks));
+  if (a.T > 0 && words > 0) rows_count_kernel<<<grid, kRowWarps * 32, 0, s>>>(a);
   rows_scan_kernel<<<1, 1024, 0, s>>>(a.row_ptr, a.M);
-  if (a.T > 0 && words > 0) rows_fill_kernel<<<words, kRowWarps * 32, 0, s>>>(a);
+  if (a.T > 0 && words > 0) rows_fill_kernel<<<grid, kRowWarps * 32, 0, s>>>(a);
   return cudaGetLastError();
 }
 
