@@ -143,16 +143,28 @@ __global__ void __launch_bounds__(256) first_kernel(PairsArgs a) {
   }
   const unsigned long long f = a.fp[e];
   const int32_t *mine = a.list + static_cast<int64_t>(r) * a.M + a.off[e];
+  // earlier rows checked kFirstBatch at a time: their (count, fingerprint) loads are issued
+  // together (one dependent L2 round trip per earlier row was the limiter), then compared
+  // in row order, so the first match is still the smallest r2
+  constexpr int kFirstBatch = 8;
   int32_t first = r;
-  for (int32_t r2 = 0; r2 < r; ++r2) {
-    const int64_t e2 = static_cast<int64_t>(r2) * a.T + j;
-    if (a.cnt[e2] != c || a.fp[e2] != f) continue;
-    const int32_t *other = a.list + static_cast<int64_t>(r2) * a.M + a.off[e2];
-    bool same = true;
-    for (int32_t k = 0; k < c && same; ++k) same = mine[k] == other[k];
-    if (same) {
-      first = r2;
-      break;
+  for (int32_t rb = 0; rb < r && first == r; rb += kFirstBatch) {
+    int32_t cc[kFirstBatch];
+    unsigned long long ff[kFirstBatch];
+#pragma unroll
+    for (int u = 0; u < kFirstBatch; ++u) {
+      const int64_t e2 = static_cast<int64_t>(rb + u) * a.T + j;
+      cc[u] = rb + u < r ? a.cnt[e2] : -2;
+      ff[u] = rb + u < r ? a.fp[e2] : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < kFirstBatch; ++u) {
+      if (first != r || cc[u] != c || ff[u] != f) continue;
+      const int32_t r2 = rb + u;
+      const int32_t *other = a.list + static_cast<int64_t>(r2) * a.M + a.off[static_cast<int64_t>(r2) * a.T + j];
+      bool same = true;
+      for (int32_t k = 0; k < c && same; ++k) same = mine[k] == other[k];
+      if (same) first = r2;
     }
   }
   a.first[e] = first;
