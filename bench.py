@@ -616,6 +616,11 @@ def main():
     else:
         evals_total = float(evals_local)
 
+    # ---- the hypothesis update on this step's C_k (before the e2e legs step the particles on)
+    update = None
+    if world == 1 and not a.no_update:
+        update = bench_update(a, st, scene, cfg, dev, stream, L)
+
     # ---- launch-bound small configs: one whole step (glmb_step) captured in a CUDA graph
     graphs = None
     if world == 1 and not a.no_graphs:
@@ -703,9 +708,6 @@ def main():
             dist.destroy_process_group()
         return
 
-    update = None
-    if world == 1 and not a.no_update:
-        update = bench_update(a, st, scene, cfg, dev, stream, L)
     convoy = None
     if world == 1 and not a.no_convoy:
         convoy = bench_convoy(dev)
