@@ -262,7 +262,8 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
   extern __shared__ __align__(16) unsigned char smraw[];
   // a.pool bytes at the front, carved at run time (below); fixed arrays after it
   unsigned char *pool = smraw;
-  int32_t *frp = reinterpret_cast<int32_t *>(smraw + a.pool);      // [M + 1]
+  double *slc = reinterpret_cast<double *>(smraw + a.pool);         // [n_count] count prior
+  int32_t *frp = reinterpret_cast<int32_t *>(slc + max(a.n_count, 0));  // [M + 1]
   int32_t *pq = frp + a.M + 1;                                     // [(T + 3) / 4]
   int32_t *nzq = pq + ((a.T + 3) >> 2);                            // [(M + 3) / 4]
   const bool row_mode = a.M < 2 * kSampThreads;
@@ -281,6 +282,7 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
   if (a.n_parents != nullptr && h >= __ldg(a.n_parents)) return;  // inactive parent slot
   const uint32_t *pm = a.parent_mask + static_cast<int64_t>(h) * a.ldt;
   for (int32_t k = threadIdx.x; k < a.ldt; k += kSampThreads) pmask[k] = __ldg(pm + k);
+  for (int32_t k = threadIdx.x; k < a.n_count; k += kSampThreads) slc[k] = __ldg(a.count_lp + k);
   __syncthreads();
   const int32_t tquads = (a.T + 3) >> 2;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -546,13 +548,14 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
       const uint32_t av = alive[k];
       al_out[k] = av;
       fp += fp_term(av, static_cast<uint64_t>(k));
-      if (a.n_count > 0) {
-        for (uint32_t rest = av; rest != 0u; rest &= rest - 1u) {
-          const int32_t j = 32 * k + __ffs(rest) - 1;
-          lw += __ldg(a.count_lp + min(cnt[j], a.n_count - 1));
-        }
-      } else {
-        missed += __popc(av & ~det[k]);
+      if (a.n_count == 0) missed += __popc(av & ~det[k]);
+    }
+    if (a.n_count > 0) {  // lc(n_j) of every alive track, a thread per parent quad
+      for (int32_t v = threadIdx.x; v < nq; v += kSampThreads) {
+        const int32_t t = pq[v];
+        const uint32_t abits = (alive[t >> 3] >> (4 * (t & 7))) & 0xFu;
+        for (uint32_t rest = abits; rest != 0u; rest &= rest - 1u)
+          lw += slc[min(cnt[4 * t + __ffs(rest) - 1], a.n_count - 1)];
       }
     }
     // one reduction round for (lw, fingerprint, missed): shuffles, one barrier, thread 0
@@ -942,7 +945,8 @@ cudaError_t launch_assoc_sample(const SampleArgs &a, int sm_count, cudaStream_t 
   const size_t fixed = sizeof(int32_t) * (static_cast<size_t>(a.M) + 1) + sizeof(uint32_t) * 3 * static_cast<size_t>(a.ldt) +
                        sizeof(int32_t) * tquads + sizeof(int32_t) * ((static_cast<size_t>(a.M) + 3) / 4) +
                        (a.M < 2 * kSampThreads ? sizeof(int32_t) * static_cast<size_t>(a.M) : 0) +
-                       (a.n_count > 0 ? sizeof(int32_t) * static_cast<size_t>(a.T) : 0) + 16;
+                       (a.n_count > 0 ? (sizeof(int32_t) * static_cast<size_t>(a.T) +
+                                         sizeof(double) * static_cast<size_t>(a.n_count)) : 0) + 16;
   if (fixed > 200 * 1024) return cudaErrorInvalidValue;
   // shared memory per CTA sized so the grid runs in one wave where it can; the pool
   // beyond the fixed arrays holds the kept-entry bitmap, the parent's rows and the
