@@ -95,6 +95,12 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return r;
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// First statement of every kernel of the hypothesis chain: with the launch attribute
+// set (launch_pdl), the kernel's CTAs may start while the previous kernel drains and
+// wait here until its writes are visible; launched without it, this is a no-op.
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---------------------------------------------------------------- mbarrier / TMA bulk
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

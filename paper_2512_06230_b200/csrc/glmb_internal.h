@@ -6,6 +6,26 @@
 
 namespace glmb {
 
+// Kernel launch with programmatic stream serialization (the hypothesis chain: each
+// kernel starts with grid_dep_wait(), so its launch overlaps the previous kernel's
+// tail).  GLMB_PDL=0 launches plainly (A/B runs).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 struct PredictArgs {
   const float *x, *y, *v, *psi, *omega;
   float *ox, *oy, *ov, *opsi, *oomega;

@@ -27,6 +27,7 @@ constexpr uint32_t kDomainSurvive = 2u, kDomainAssoc = 3u;
 // then d_j = (1 - P_S) / ((1 - P_S) + P_S ((1 - P_D) + P_D e_j)).  fp64 with explicitly
 // rounded operations (no FMA contraction): IEEE-exact steps, so d_j is reproducible.
 __global__ void __launch_bounds__(256) death_prob_kernel(DeathArgs a) {
+  grid_dep_wait();
   const int32_t j = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (j >= a.T) return;
@@ -72,6 +73,7 @@ __device__ __forceinline__ void row_chunk(int32_t T, int k, int32_t &j0, int32_t
 
 // row totals: each CTA adds its chunk's counts (row_ptr zeroed by the launcher)
 __global__ void __launch_bounds__(kRowWarps * 32) rows_count_kernel(RowsArgs a) {
+  grid_dep_wait();
   __shared__ int32_t cnt[kRowWarps][32];
   const int w = blockIdx.x, lane = threadIdx.x & 31, k = threadIdx.x >> 5;
   int32_t j0, j1;
@@ -94,6 +96,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) rows_count_kernel(RowsArgs a) 
 
 // exclusive scan of row_ptr[0..M) in place, row_ptr[M] = total (one CTA)
 __global__ void __launch_bounds__(1024) rows_scan_kernel(int32_t *row_ptr, int32_t M) {
+  grid_dep_wait();
   __shared__ int32_t wsum[32];
   __shared__ int32_t carry_s;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -131,6 +134,7 @@ __global__ void __launch_bounds__(1024) rows_scan_kernel(int32_t *row_ptr, int32
 }
 
 __global__ void __launch_bounds__(kRowWarps * 32) rows_fill_kernel(RowsArgs a) {
+  grid_dep_wait();
   __shared__ int32_t cnt[kRowWarps][32];
   __shared__ int32_t pre[kRowWarps][32];
   const int w = blockIdx.x, lane = threadIdx.x & 31, k = threadIdx.x >> 5;
@@ -259,6 +263,7 @@ __device__ __forceinline__ int32_t draw_row(const int32_t *rp, const int32_t *cl
 }
 
 __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a) {
+  grid_dep_wait();
   extern __shared__ __align__(16) unsigned char smraw[];
   // a.pool bytes at the front, carved at run time (below); fixed arrays after it
   unsigned char *pool = smraw;
@@ -604,6 +609,7 @@ __device__ bool same_sample(const DedupArgs &a, int64_t q1, int64_t q2) {
 }
 
 __global__ void __launch_bounds__(kDedupThreads) dedup_kernel(DedupArgs a) {
+  grid_dep_wait();
   __shared__ unsigned long long hs[kDedupTile];
   __shared__ int32_t cand[kDedupThreads];
   __shared__ uint8_t same[kDedupThreads];
@@ -679,6 +685,7 @@ __device__ __forceinline__ MaxArg better(MaxArg x, MaxArg y) {
 }
 
 __global__ void __launch_bounds__(kPruneThreads) prune_kernel(PruneArgs a) {
+  grid_dep_wait();
   extern __shared__ unsigned char psm[];
   unsigned long long *skey = reinterpret_cast<unsigned long long *>(psm);  // [cap2]
   int32_t *sidx = reinterpret_cast<int32_t *>(skey + a.cap2);              // [cap2]
@@ -907,7 +914,8 @@ __global__ void __launch_bounds__(kPruneThreads) prune_kernel(PruneArgs a) {
 }  // namespace
 
 cudaError_t launch_death_prob(const DeathArgs &a, cudaStream_t s) {
-  death_prob_kernel<<<(a.T + 7) / 8, 256, 0, s>>>(a);
+  cudaError_t e0 = launch_pdl(death_prob_kernel, dim3((a.T + 7) / 8), dim3(256), 0, s, a);
+  if (e0 != cudaSuccess) return e0;
   return cudaGetLastError();
 }
 
@@ -922,10 +930,20 @@ cudaError_t launch_compat_rows(const RowsArgs &a, int sm_count, cudaStream_t s) 
     if (e != cudaSuccess) return e;
   }
   const dim3 grid(static_cast<unsigned>(words), static_cast<unsigned>(chunks));
-  if (a.T > 0 && words > 0) rows_count_kernel<<<grid, kRowWarps * 32, 0, s>>>(a);
-  rows_scan_kernel<<<1, 1024, 0, s>>>(a.row_ptr, a.M);
-  if (a.T > 0 && words > 0) rows_fill_kernel<<<grid, kRowWarps * 32, 0, s>>>(a);
+  cudaError_t e = cudaSuccess;
+  if (a.T > 0 && words > 0) e = launch_pdl(rows_count_kernel, grid, dim3(kRowWarps * 32), 0, s, a);
+  if (e == cudaSuccess) e = launch_pdl(rows_scan_kernel, dim3(1), dim3(1024), 0, s, a.row_ptr, a.M);
+  if (e == cudaSuccess && a.T > 0 && words > 0) e = launch_pdl(rows_fill_kernel, grid, dim3(kRowWarps * 32), 0, s, a);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
+}
+
+bool pdl_enabled() {
+  static const bool v = [] {
+    const char *e = std::getenv("GLMB_PDL");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return v;
 }
 
 cudaError_t launch_assoc_sample(const SampleArgs &a, int sm_count, cudaStream_t s) {
@@ -965,12 +983,14 @@ cudaError_t launch_assoc_sample(const SampleArgs &a, int sm_count, cudaStream_t 
   cudaError_t e = cudaFuncSetAttribute(assoc_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  assoc_sample_kernel<<<static_cast<unsigned>(n), kSampThreads, smem, s>>>(b);
+  e = launch_pdl(assoc_sample_kernel, dim3(static_cast<unsigned>(n)), dim3(kSampThreads), smem, s, b);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
 cudaError_t launch_dedup(const DedupArgs &a, cudaStream_t s) {
-  dedup_kernel<<<a.H_old, kDedupThreads, 0, s>>>(a);
+  cudaError_t e = launch_pdl(dedup_kernel, dim3(a.H_old), dim3(kDedupThreads), 0, s, a);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -987,7 +1007,10 @@ cudaError_t launch_prune(const PruneArgs &a, cudaStream_t s) {
         cudaFuncSetAttribute(prune_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  prune_kernel<<<1, kPruneThreads, smem, s>>>(a);
+  {
+    cudaError_t e = launch_pdl(prune_kernel, dim3(1), dim3(kPruneThreads), smem, s, a);
+    if (e != cudaSuccess) return e;
+  }
   return cudaGetLastError();
 }
 

@@ -59,6 +59,7 @@ __device__ Ti block_excl_scan(Ti v, Ti *wsum /* [32] */, Ti &total) {
 constexpr int kInvThreads = 256;
 
 __global__ void __launch_bounds__(kInvThreads) invert_kernel(PairsArgs a) {
+  grid_dep_wait();
   extern __shared__ unsigned char smraw[];
   unsigned long long *fp = reinterpret_cast<unsigned long long *>(smraw);  // [T]
   int32_t *cnt = reinterpret_cast<int32_t *>(fp + a.T);                   // [T]
@@ -132,6 +133,7 @@ __global__ void __launch_bounds__(kInvThreads) invert_kernel(PairsArgs a) {
 
 // first occurrence of each (j, S): the earliest r' <= r with the same list
 __global__ void __launch_bounds__(256) first_kernel(PairsArgs a) {
+  grid_dep_wait();
   const int32_t r = blockIdx.y;
   const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= a.T || (a.n_hyp_dev != nullptr && r >= __ldg(a.n_hyp_dev))) return;
@@ -178,6 +180,7 @@ __device__ __forceinline__ int32_t n_hyp_used(const PairsArgs &a) {
 }
 
 __global__ void __launch_bounds__(256) row_count_kernel(PairsArgs a) {
+  grid_dep_wait();
   __shared__ int32_t rk[8], rm[8];
   const int32_t r = blockIdx.x;
   int32_t k = 0, m = 0;
@@ -211,6 +214,7 @@ __global__ void __launch_bounds__(256) row_count_kernel(PairsArgs a) {
 }
 
 __global__ void __launch_bounds__(1024) row_scan_kernel(PairsArgs a) {
+  grid_dep_wait();
   __shared__ int32_t wsum[32];
   int32_t kc = 0, mc = 0;
   for (int32_t r0 = 0; r0 < a.n_hyp; r0 += 1024) {
@@ -233,6 +237,7 @@ __global__ void __launch_bounds__(1024) row_scan_kernel(PairsArgs a) {
 }
 
 __global__ void __launch_bounds__(256) number_kernel(PairsArgs a) {
+  grid_dep_wait();
   __shared__ int32_t wsum[32];
   const int32_t r = blockIdx.x;
   if (r >= n_hyp_used(a)) return;
@@ -260,6 +265,7 @@ __global__ void __launch_bounds__(256) number_kernel(PairsArgs a) {
 
 // pair_of for repeats and the measurement lists of the new pairs
 __global__ void __launch_bounds__(256) finish_kernel(PairsArgs a) {
+  grid_dep_wait();
   const int32_t r = blockIdx.y;
   const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= a.T || (a.n_hyp_dev != nullptr && r >= __ldg(a.n_hyp_dev))) return;
@@ -423,6 +429,7 @@ __device__ __forceinline__ void resample_unit(const ResampleArgs &a, const int k
 // CTA count: a capacity-sized grid of mostly empty 1024-thread CTAs cost ~0.1 ms).
 template <int kResThreads>
 __global__ void __launch_bounds__(kResThreads) resample_kernel(ResampleArgs a) {
+  grid_dep_wait();
   const int n = a.n_units_dev != nullptr ? min(a.K, __ldg(a.n_units_dev)) : a.K;
   for (int k = blockIdx.x; k < n; k += gridDim.x) {
     resample_unit<kResThreads>(a, k);
@@ -434,6 +441,7 @@ __global__ void __launch_bounds__(kResThreads) resample_kernel(ResampleArgs a) {
 // Kept hypothesis r -> parent r of the next step: bits of the pairs it uses
 // (rows of the new particle set) plus the birth columns; ln of its weight.
 __global__ void __launch_bounds__(128) next_parents_kernel(NextParentsArgs a) {
+  grid_dep_wait();
   extern __shared__ uint32_t msk[];  // [ldt]
   const int32_t r = blockIdx.x;
   const int32_t nk = __ldg(a.n_kept);
@@ -458,6 +466,7 @@ __global__ void __launch_bounds__(128) next_parents_kernel(NextParentsArgs a) {
 
 // MAP estimate: weighted mean position of each track of kept hypothesis 0 (fp64 sums)
 __global__ void __launch_bounds__(256) map_estimate_kernel(MapEstimateArgs a) {
+  grid_dep_wait();
   __shared__ double red[3][8];
   const int32_t j = blockIdx.x;
   const int32_t k = __ldg(a.n_kept) > 0 ? __ldg(a.pair_of0 + j) : -1;
@@ -532,13 +541,14 @@ cudaError_t launch_assoc_pairs(const PairsArgs &in, void *ws, cudaStream_t s) {
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  invert_kernel<<<a.n_hyp, kInvThreads, smem, s>>>(a);
+  cudaError_t e = launch_pdl(invert_kernel, dim3(a.n_hyp), dim3(kInvThreads), smem, s, a);
   const dim3 g2((a.T + 255) / 256, a.n_hyp);
-  first_kernel<<<g2, 256, 0, s>>>(a);
-  row_count_kernel<<<a.n_hyp, 256, 0, s>>>(a);
-  row_scan_kernel<<<1, 1024, 0, s>>>(a);
-  number_kernel<<<a.n_hyp, 256, 0, s>>>(a);
-  finish_kernel<<<g2, 256, 0, s>>>(a);
+  if (e == cudaSuccess) e = launch_pdl(first_kernel, g2, dim3(256), 0, s, a);
+  if (e == cudaSuccess) e = launch_pdl(row_count_kernel, dim3(a.n_hyp), dim3(256), 0, s, a);
+  if (e == cudaSuccess) e = launch_pdl(row_scan_kernel, dim3(1), dim3(1024), 0, s, a);
+  if (e == cudaSuccess) e = launch_pdl(number_kernel, dim3(a.n_hyp), dim3(256), 0, s, a);
+  if (e == cudaSuccess) e = launch_pdl(finish_kernel, g2, dim3(256), 0, s, a);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -557,8 +567,9 @@ cudaError_t launch_resample(const ResampleArgs &a, int sm_count, cudaStream_t s)
                                                        static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  if (a.P <= 2048) resample_kernel<256><<<grid, 256, smem, s>>>(a);
-  else resample_kernel<1024><<<grid, 1024, smem, s>>>(a);
+  cudaError_t e2 = a.P <= 2048 ? launch_pdl(resample_kernel<256>, dim3(grid), dim3(256), smem, s, a)
+                                : launch_pdl(resample_kernel<1024>, dim3(grid), dim3(1024), smem, s, a);
+  if (e2 != cudaSuccess) return e2;
   return cudaGetLastError();
 }
 
@@ -568,13 +579,15 @@ namespace glmb {
 
 cudaError_t launch_next_parents(const NextParentsArgs &a, cudaStream_t s) {
   if (a.n_hyp_cap == 0) return cudaMemsetAsync(a.n_parents, 0, sizeof(int32_t), s);
-  next_parents_kernel<<<a.n_hyp_cap, 128, sizeof(uint32_t) * a.ldt, s>>>(a);
+  cudaError_t e = launch_pdl(next_parents_kernel, dim3(a.n_hyp_cap), dim3(128), sizeof(uint32_t) * a.ldt, s, a);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
 cudaError_t launch_map_estimate(const MapEstimateArgs &a, cudaStream_t s) {
   if (a.T == 0) return cudaSuccess;
-  map_estimate_kernel<<<a.T, 256, 0, s>>>(a);
+  cudaError_t e = launch_pdl(map_estimate_kernel, dim3(a.T), dim3(256), 0, s, a);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

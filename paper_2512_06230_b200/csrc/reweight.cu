@@ -480,6 +480,7 @@ __device__ __forceinline__ void reweight_unit(const ReweightArgs &a, const int u
 
 template <int CL, int R>
 __global__ void __launch_bounds__(kThreads, R == 1 ? 5 : (R == 2 ? 3 : 2)) reweight_cluster_kernel(const ReweightArgs a) {
+  grid_dep_wait();  // pair mode is launched with programmatic serialization (hypothesis chain)
   // units u = cluster index, + clusters in the grid, ... (one pass unless the grid is capped)
   const int n_units = a.n_units_dev != nullptr ? min(a.T, __ldg(a.n_units_dev)) : a.T;
   const int stride = static_cast<int>(gridDim.x) / CL;
@@ -494,13 +495,15 @@ cudaError_t launch_cluster(const ReweightArgs &a, cudaStream_t s) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = (a.pair_track != nullptr && pdl_enabled()) ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, reweight_cluster_kernel<CL, R>, a);
 }
 
