@@ -220,6 +220,7 @@ __device__ __forceinline__ void tile_dispatch(int hv, const float4 *A, int np, M
 // shorter (the tail of a 2.2-wave grid cost ~12 % of the launch).
 template <int NW, int K, int EMU_PERIOD, int CL>
 __global__ void __launch_bounds__(32 * NW, min_blocks<NW, K>()) compat_kernel(const CompatArgs a) {
+  grid_dep_wait();  // launched with programmatic serialization after predict / birth
   constexpr int H = Meas<K>::H;
   constexpr int kThreads = 32 * NW;
   constexpr int kTileM = 32 * NW;  // measurements per tile per K
@@ -390,22 +391,23 @@ __global__ void clutter_fill_kernel(float *c, int32_t M, float kappa) {
 template <int NW, int K, int EMU_PERIOD, int CL>
 cudaError_t launch_kc(const CompatArgs &a, cudaStream_t s) {
   const int64_t grid = static_cast<int64_t>(a.T) * a.n_mtiles * CL;
-  if (CL == 1) {
-    compat_kernel<NW, K, EMU_PERIOD, CL><<<static_cast<unsigned>(grid), 32 * NW, kSmemBytes, s>>>(a);
-    return cudaGetLastError();
-  }
+  if (CL == 1)
+    return launch_pdl(compat_kernel<NW, K, EMU_PERIOD, CL>, dim3(static_cast<unsigned>(grid)), dim3(32 * NW),
+                      kSmemBytes, s, a);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
   cfg.blockDim = dim3(32 * NW);
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, compat_kernel<NW, K, EMU_PERIOD, CL>, a);
 }
 

@@ -21,6 +21,7 @@ __device__ __forceinline__ float &at(float4 &v, int q) { return (&v.x)[q]; }
 // CTRV survival propagation (§Approach), half-angle form:
 //   dx = v dt sinc(h) cos(psi + h), dy = v dt sinc(h) sin(psi + h), h = omega dt / 2
 __global__ void __launch_bounds__(kThreads) predict_kernel(const PredictArgs a) {
+  grid_dep_wait();
   const int32_t quads = a.P >> 2;
   const int64_t total = static_cast<int64_t>(a.T) * quads;
   const float half_dt = 0.5f * a.dt;
@@ -74,6 +75,7 @@ __global__ void __launch_bounds__(kThreads) predict_kernel(const PredictArgs a) 
 
 // LMB birth: s = mu_b + L_b n, n0..n3 from tag 0x100, n4 from tag 0x101.
 __global__ void __launch_bounds__(kThreads) birth_kernel(const BirthArgs a) {
+  grid_dep_wait();
   const int32_t quads = a.P >> 2;
   const int64_t total = static_cast<int64_t>(a.B) * quads;
   const float winit = 1.0f / static_cast<float>(a.P);
@@ -147,14 +149,20 @@ int grid_for(int64_t quads, int sm_count) {
 cudaError_t launch_predict(const PredictArgs &a, int sm_count, cudaStream_t s) {
   const int64_t quads = static_cast<int64_t>(a.T) * (a.P >> 2);
   if (quads == 0) return cudaSuccess;
-  predict_kernel<<<grid_for(quads, sm_count), kThreads, 0, s>>>(a);
+  {
+    cudaError_t e = launch_pdl(predict_kernel, dim3(grid_for(quads, sm_count)), dim3(kThreads), 0, s, a);
+    if (e != cudaSuccess) return e;
+  }
   return cudaGetLastError();
 }
 
 cudaError_t launch_birth(const BirthArgs &a, int sm_count, cudaStream_t s) {
   const int64_t quads = static_cast<int64_t>(a.B) * (a.P >> 2);
   if (quads == 0) return cudaSuccess;
-  birth_kernel<<<grid_for(quads, sm_count), kThreads, 0, s>>>(a);
+  {
+    cudaError_t e = launch_pdl(birth_kernel, dim3(grid_for(quads, sm_count)), dim3(kThreads), 0, s, a);
+    if (e != cudaSuccess) return e;
+  }
   return cudaGetLastError();
 }
 
