@@ -647,7 +647,8 @@ def main():
         col_d = torch.empty(cap, dtype=torch.int32, device=dev)
         val_d = torch.empty(cap, dtype=torch.float32, device=dev)
         lv_d = torch.empty(cap, dtype=torch.float64, device=dev)
-        cap_h = 64 * M_max                             # host CSR capacity (a second copy if exceeded)
+        cap_h = 4 * M_max                              # host CSR capacity = the speculative first copy
+                                                       # (a second, exact copy if the entries exceed it)
         rp_h = pin(torch.empty(M_max + 1, dtype=torch.int32))
         col_h = pin(torch.empty(cap_h, dtype=torch.int32))
         val_h = pin(torch.empty(cap_h))
@@ -660,7 +661,8 @@ def main():
                                        col_h, val_h, ln_h, fl_h, stream, aux_stream=copy_stream)
             st.swap_weights()
             M = Zh[zi].shape[0]
-            return M * 12, (M + 1) * 4 + nnz * 8 + st.T_local * 8
+            first = min(cap_h, cap)                    # entries copied speculatively, then the rest
+            return M * 12, (M + 1) * 4 + max(first, nnz) * 8 + st.T_local * 8
 
         def host_step_dense(k):
             """C_k read back dense (glmb_step_host)."""
