@@ -487,6 +487,182 @@ __global__ void __launch_bounds__(kThreads, R == 1 ? 5 : (R == 2 ? 3 : 2)) rewei
   for (int u = static_cast<int>(blockIdx.x) / CL; u < n_units; u += stride) reweight_unit<CL, R>(a, u);
 }
 
+// Flat two-pass variant: one 256-thread CTA per unit, no cluster.  Pass 1 streams the
+// unit's particles once from HBM and keeps a per-thread online (m, s, s2) -- s relative to
+// the thread's running max, rescaled when the max moves; the warps' and then the CTA's
+// triples merge in a fixed order.  Pass 2 re-reads x, y, w (L2-resident by then),
+// recomputes l_p bit for bit and writes w'_p = 2^(l_p - m) / s.  Nothing waits at a
+// cluster barrier holding registers, so ~8 CTAs per SM stream concurrently.
+__device__ __forceinline__ void online_add(double l, double &m, double &s, double &s2) {
+  if (l == -INFINITY) return;
+  if (l > m) {
+    const double f = m == -INFINITY ? 0.0 : static_cast<double>(ex2_approx(static_cast<float>(m - l)));
+    s = s * f + 1.0;
+    s2 = s2 * (f * f) + 1.0;
+    m = l;
+  } else {
+    const double e = ex2_approx(static_cast<float>(l - m));
+    s += e;
+    s2 += e * e;
+  }
+}
+
+template <bool LC>
+__device__ __forceinline__ void reweight_flat_unit(const ReweightArgs &a, const int u) {
+  extern __shared__ __align__(16) double lc[];  // [P] l_p when LC
+  __shared__ SList S;
+  __shared__ double red[3][kWarps];
+  __shared__ uint32_t masks[kRows * kWarps];
+  __shared__ double bc[3];
+  const bool pairs = a.pair_track != nullptr;
+  const int j = pairs ? __ldg(a.pair_track + u) : u;
+  const int col = a.col_offset + j + 1;
+  const int64_t base = static_cast<int64_t>(j) * a.ld;
+  const float4 *xs = reinterpret_cast<const float4 *>(a.x + base);
+  const float4 *ys = reinterpret_cast<const float4 *>(a.y + base);
+  const float4 *ws = reinterpret_cast<const float4 *>(a.w + base);
+  float4 *wo = reinterpret_cast<float4 *>(a.w_out + static_cast<int64_t>(u) * a.ld_out);
+  const bool copy_out = pairs || a.w_out != a.w;
+  const int quads = a.P >> 2;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (pairs) collect_S_pair(a, u, S);
+  else collect_S(a, col, S, masks);
+  const int nS = S.n;
+
+  if (nS == 0) {  // untouched; log_norm = ln sum w; ESS = (sum w)^2 / sum w^2
+    double sw = 0.0, sw2 = 0.0;
+    for (int g = threadIdx.x; g < quads; g += kThreads) {
+      const float4 w4 = __ldcs(ws + g);
+      if (copy_out) __stcs(wo + g, w4);
+      sw += (static_cast<double>(w4.x) + w4.y) + (static_cast<double>(w4.z) + w4.w);
+      sw2 += (static_cast<double>(w4.x) * w4.x + static_cast<double>(w4.y) * w4.y) +
+             (static_cast<double>(w4.z) * w4.z + static_cast<double>(w4.w) * w4.w);
+    }
+    sw = block_sum(sw, red[0]);
+    if (a.ess != nullptr) sw2 = block_sum(sw2, red[1]);
+    if (threadIdx.x == 0) {
+      a.log_norm[u] = static_cast<float>(log(sw));
+      a.flags[u] = 0u;
+      if (a.ess != nullptr) a.ess[u] = sw2 > 0.0 ? static_cast<float>(sw * sw / sw2) : 0.0f;
+    }
+    __syncthreads();
+    return;
+  }
+
+  // pass 1: online (m, s, s2) per thread; the next quad's loads are issued before this
+  // quad's arithmetic
+  double m = -INFINITY, sm = 0.0, sm2 = 0.0;
+  {
+    int g = threadIdx.x;
+    float4 X, Y, W;
+    if (g < quads) {
+      X = __ldg(xs + g);
+      Y = __ldg(ys + g);
+      W = __ldg(ws + g);
+    }
+#pragma unroll 1
+    for (; g < quads; g += kThreads) {
+      const int gn = g + kThreads;
+      float4 Xn, Yn, Wn;
+      if (gn < quads) {
+        Xn = __ldg(xs + gn);
+        Yn = __ldg(ys + gn);
+        Wn = __ldg(ws + gn);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double l = log_weight(a, S, col, q4(X, q), q4(Y, q), q4(W, q));
+        if constexpr (LC) lc[4 * g + q] = l;
+        online_add(l, m, sm, sm2);
+      }
+      X = Xn;
+      Y = Yn;
+      W = Wn;
+    }
+  }
+  // warp: max by shuffles, the lanes' sums rescaled to it; CTA: thread 0 merges the warps
+  const double mw = warp_max_d(m);
+  const double f = mw == -INFINITY || m == -INFINITY ? 0.0 : static_cast<double>(ex2_approx(static_cast<float>(m - mw)));
+  double sw = warp_sum_d(sm * f), sw2 = a.ess != nullptr ? warp_sum_d(sm2 * (f * f)) : 0.0;
+  if (lane == 0) {
+    red[0][warp] = mw;
+    red[1][warp] = sw;
+    red[2][warp] = sw2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double mb = red[0][0], sb = red[1][0], s2b = red[2][0];
+#pragma unroll
+    for (int k = 1; k < kWarps; ++k) ms_merge(mb, sb, s2b, red[0][k], red[1][k], red[2][k]);
+    bc[0] = mb;
+    bc[1] = sb;
+    bc[2] = s2b;
+  }
+  __syncthreads();
+  const double mc = bc[0], sc = bc[1], s2c = bc[2];
+  if (mc == -INFINITY) {  // every weight zero: uniform reset, flagged (never abort)
+    const float uw = 1.0f / static_cast<float>(a.P);
+    for (int g = threadIdx.x; g < quads; g += kThreads) __stcs(wo + g, make_float4(uw, uw, uw, uw));
+    if (threadIdx.x == 0) {
+      a.log_norm[u] = -INFINITY;
+      a.flags[u] = 1u;
+      if (a.ess != nullptr) a.ess[u] = static_cast<float>(a.P);
+    }
+    __syncthreads();
+    return;
+  }
+  // pass 2: w'_p = 2^(l_p - m) / s (l_p recomputed from the L2-resident particles)
+  const float inv_s = static_cast<float>(1.0 / sc);
+  if constexpr (LC) {
+    for (int g = threadIdx.x; g < quads; g += kThreads) {
+      float4 o;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) q4(o, q) = ex2_approx(static_cast<float>(lc[4 * g + q] - mc)) * inv_s;
+      __stcs(wo + g, o);
+    }
+  } else {
+    int g = threadIdx.x;
+    float4 X, Y, W;
+    if (g < quads) {
+      X = __ldcs(xs + g);
+      Y = __ldcs(ys + g);
+      W = __ldcs(ws + g);
+    }
+#pragma unroll 1
+    for (; g < quads; g += kThreads) {
+      const int gn = g + kThreads;
+      float4 Xn, Yn, Wn;
+      if (gn < quads) {
+        Xn = __ldcs(xs + gn);
+        Yn = __ldcs(ys + gn);
+        Wn = __ldcs(ws + gn);
+      }
+      float4 o;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        q4(o, q) = ex2_approx(static_cast<float>(log_weight(a, S, col, q4(X, q), q4(Y, q), q4(W, q)) - mc)) * inv_s;
+      __stcs(wo + g, o);
+      X = Xn;
+      Y = Yn;
+      W = Wn;
+    }
+  }
+  if (threadIdx.x == 0) {
+    const double ln2 = 0.69314718055994530942;
+    a.log_norm[u] = static_cast<float>((mc + log2(sc)) * ln2 - nS * a.log_norm1);
+    a.flags[u] = 0u;
+    if (a.ess != nullptr) a.ess[u] = static_cast<float>(sc * sc / s2c);
+  }
+  __syncthreads();  // S, red and bc are reused by the next unit
+}
+
+template <bool LC>
+__global__ void __launch_bounds__(kThreads, 4) reweight_flat_kernel(const ReweightArgs a) {
+  grid_dep_wait();
+  const int n_units = a.n_units_dev != nullptr ? min(a.T, __ldg(a.n_units_dev)) : a.T;
+  for (int u = blockIdx.x; u < n_units; u += gridDim.x) reweight_flat_unit<LC>(a, u);
+}
+
 template <int CL, int R>
 cudaError_t launch_cluster(const ReweightArgs &a, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
@@ -513,6 +689,35 @@ constexpr int kMaxCacheBytes = 100 * 1024;
 
 cudaError_t launch_reweight(const ReweightArgs &a, cudaStream_t s) {
   if (a.T == 0) return cudaSuccess;
+  // default: the flat kernel with l_p cached in shared memory for 2048 <= P <= 12800
+  // (measured at cfg3: 78 -> 51 us standalone; the cluster kernel stays best for small P).
+  // GLMB_REWEIGHT_FLAT: 0 = cluster kernel, 1 = flat recompute, 2 = flat cached (A/B).
+  static const int flat_env = [] {
+    const char *e = std::getenv("GLMB_REWEIGHT_FLAT");
+    return e ? std::atoi(e) : -1;
+  }();
+  const bool flat_default = flat_env < 0 && a.P >= 2048 && static_cast<size_t>(a.P) * 8 <= kMaxCacheBytes;
+  if (flat_env == 1 || flat_env == 2 || flat_default) {
+    const int units = a.units_cap > 0 ? min(a.T, a.units_cap) : a.T;
+    const bool lcache = flat_env != 1 && static_cast<size_t>(a.P) * 8 <= kMaxCacheBytes;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(units));
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = s;
+    cfg.dynamicSmemBytes = lcache ? static_cast<size_t>(a.P) * 8 : 0;
+    if (lcache) {
+      cudaError_t e = cudaFuncSetAttribute(reweight_flat_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           kMaxCacheBytes);
+      if (e != cudaSuccess) return e;
+    }
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = (a.pair_track != nullptr && pdl_enabled()) ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return lcache ? cudaLaunchKernelEx(&cfg, reweight_flat_kernel<true>, a)
+                  : cudaLaunchKernelEx(&cfg, reweight_flat_kernel<false>, a);
+  }
   // Launch shape depends on P only (never on T): shard-invariant results.
   const int quads = a.P >> 2;
   static const int rw_r = [] {  // quads per thread: 1 (more, lighter CTAs) or 2; A-B knob
