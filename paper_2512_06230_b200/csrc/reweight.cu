@@ -525,6 +525,13 @@ __device__ __forceinline__ void reweight_flat_unit(const ReweightArgs &a, const 
   const bool copy_out = pairs || a.w_out != a.w;
   const int quads = a.P >> 2;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // the first quad's loads are issued before the S scan, so the two latencies overlap
+  float4 X0, Y0, W0;
+  if (static_cast<int>(threadIdx.x) < quads) {
+    X0 = __ldg(xs + threadIdx.x);
+    Y0 = __ldg(ys + threadIdx.x);
+    W0 = __ldg(ws + threadIdx.x);
+  }
   if (pairs) collect_S_pair(a, u, S);
   else collect_S(a, col, S, masks);
   const int nS = S.n;
@@ -554,12 +561,7 @@ __device__ __forceinline__ void reweight_flat_unit(const ReweightArgs &a, const 
   double m = -INFINITY, sm = 0.0, sm2 = 0.0;
   {
     int g = threadIdx.x;
-    float4 X, Y, W;
-    if (g < quads) {
-      X = __ldg(xs + g);
-      Y = __ldg(ys + g);
-      W = __ldg(ws + g);
-    }
+    float4 X = X0, Y = Y0, W = W0;
 #pragma unroll 1
     for (; g < quads; g += kThreads) {
       const int gn = g + kThreads;
