@@ -288,17 +288,32 @@ __global__ void __launch_bounds__(256) finish_kernel(PairsArgs a) {
 
 // ------------------------------------------------------------------ systematic resampling
 // One CTA per pair k.  W_m = floor(w_m 2^26) in shared memory, cum_m = W_0 + ...
-// + W_m (u64, exact), S = cum_{P-1}, Q = sum W_m^2 (u128, exact).  Resample iff
-// 2 S^2 < P Q (ESS < P/2).  Output slot n takes ancestor a_n = min{m : cum_m > t_n},
-// t_n = floor((n S + V) / P), V = floor(U S 2^-24), U = 2 (r >> 9) + 1 from
-// Philox(counter (k, 0, step, 4 << 24)) word 0.  Ancestors are non-decreasing in n,
-// so the gathers of consecutive slots hit neighbouring addresses.
-// NT threads per pair: 256 for P <= 2048 (short CTAs), 1024 above (more gathers in flight)
+// + W_m (u64, exact, one block scan of per-thread chunk sums), S = cum_{P-1}, Q =
+// sum W_m^2 (u128, exact).  Resample iff 2 S^2 < P Q (ESS < P/2).  Output slot n
+// takes ancestor a_n = min{m : cum_m > t_n}, t_n = floor((n S + V) / P), V =
+// floor(U S 2^-24), U = 2 (r >> 9) + 1 from Philox(counter (k, 0, step, 4 << 24))
+// word 0 -- found particle-parallel (range starts marked, then a prefix max; see
+// below).  Ancestors are non-decreasing in n, so the gathers of consecutive slots
+// hit neighbouring addresses.  NT threads per pair: 256 for P <= 2048 (short CTAs),
+// 1024 above (more gathers in flight).
+// nf(c) = min{n >= 0 : n S + V >= c P}, capped at P; exact (fp64 estimate, integer
+// fix-up; c P, n S <= 2^55 for S <= P 2^26, P <= 2^14)
+__device__ __forceinline__ int res_first_slot(unsigned long long c, unsigned long long P, unsigned long long V,
+                                              unsigned long long S, double inv_s) {
+  const unsigned long long cp = c * P;
+  if (cp <= V) return 0;
+  const unsigned long long num = cp - V;
+  unsigned long long n = static_cast<unsigned long long>(static_cast<double>(num) * inv_s);
+  while (n * S < num) ++n;
+  while (n > 0 && (n - 1) * S >= num) --n;
+  return static_cast<int>(n < P ? n : P);
+}
+
 template <int kResThreads>
 __device__ __forceinline__ void resample_unit(const ResampleArgs &a, const int k) {
   extern __shared__ __align__(16) unsigned char rs[];
-  unsigned long long *cum = reinterpret_cast<unsigned long long *>(rs);  // [P]
-  uint32_t *Wsm = reinterpret_cast<uint32_t *>(cum + a.P);              // [P]
+  uint32_t *Wsm = reinterpret_cast<uint32_t *>(rs);          // [P] integer weights
+  int *anc = reinterpret_cast<int *>(Wsm + a.P);              // [P] ancestor of each slot
   __shared__ unsigned long long wsum[32];
   __shared__ unsigned long long qlo[kResThreads / 32], qhi[kResThreads / 32];
   __shared__ int do_res;
@@ -323,11 +338,7 @@ __device__ __forceinline__ void resample_unit(const ResampleArgs &a, const int k
   unsigned long long loc = 0;
   for (int m = m0; m < m1; ++m) loc += Wsm[m];
   unsigned long long S;
-  unsigned long long run = block_excl_scan(loc, wsum, S);
-  for (int m = m0; m < m1; ++m) {
-    run += Wsm[m];
-    cum[m] = run;
-  }
+  const unsigned long long run0 = block_excl_scan(loc, wsum, S);  // cum before this thread's chunk
   // Q: exact 128-bit sum (lo/hi halves reduced with carries by one thread)
   {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -371,45 +382,59 @@ __device__ __forceinline__ void resample_unit(const ResampleArgs &a, const int k
   const unsigned long long U = 2ull * (r.a >> 9) + 1ull;
   const unsigned long long V = (U * S) >> 24;  // U < 2^24, S <= 2^40: no overflow
   const float inv_p = 1.0f / static_cast<float>(a.P);
-  // t_n = floor((n S + V) / P) stepped along the quad: one division per quad, then
-  // quotient and remainder advance by S = qS P + rS
-  const unsigned Pu = static_cast<unsigned>(a.P);
-  const unsigned long long qS = S / Pu;
-  const unsigned rS = static_cast<unsigned>(S - qS * Pu);
+  // ancestors, particle-parallel: a_n = m exactly for n in [nf(cum_{m-1}), nf(cum_m)),
+  // nf(c) = min{n : t_n >= c} = ceil((c P - V) / S) (t_n = floor((n S + V) / P) is
+  // non-decreasing and t_n >= c <=> n S + V >= c P).  Each particle with offspring marks
+  // the first slot of its range; a block prefix-max over the slots then gives every slot
+  // its ancestor (ranges are ordered, so the last mark at or before n is a_n) -- no
+  // search, and a heavy particle's long range costs one write, not one per slot.
+  for (int n = threadIdx.x; n < a.P; n += kResThreads) anc[n] = -1;
+  __syncthreads();
+  {
+    const unsigned long long Pl = static_cast<unsigned long long>(a.P);
+    const double inv_s = 1.0 / static_cast<double>(S);
+    unsigned long long c = run0;
+    int lo = res_first_slot(c, Pl, V, S, inv_s);
+    for (int m = m0; m < m1; ++m) {
+      const uint32_t Wm = Wsm[m];
+      if (Wm == 0u) continue;
+      c += Wm;
+      const int hi = res_first_slot(c, Pl, V, S, inv_s);
+      if (hi > lo) anc[lo] = m;
+      lo = hi;
+    }
+  }
+  __syncthreads();
+  {  // inclusive prefix max over the slots: contiguous chunk per thread, warp + block scan
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int n0 = min(a.P, static_cast<int>(threadIdx.x) * per), n1 = min(a.P, n0 + per);
+    int cmax = -1;
+    for (int n = n0; n < n1; ++n) cmax = max(cmax, anc[n]);
+    int x = cmax;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x = max(x, y);
+    }
+    __shared__ int wmax[kResThreads / 32];
+    if (lane == 31) wmax[wid] = x;
+    __syncthreads();
+    int before = -1;
+    for (int w = 0; w < wid; ++w) before = max(before, wmax[w]);
+    const int xprev = __shfl_up_sync(0xffffffffu, x, 1);
+    int run = max(before, lane > 0 ? xprev : -1);
+    for (int n = n0; n < n1; ++n) {
+      run = max(run, anc[n]);
+      anc[n] = run;
+    }
+  }
+  __syncthreads();
   for (int g = threadIdx.x; g < quads; g += kResThreads) {
+    const int4 an = reinterpret_cast<const int4 *>(anc)[g];
     float4 X, Y, Vv, Ps, Om;
-    int lo = 0;
-    const unsigned long long num0 = static_cast<unsigned long long>(4 * g) * S + V;
-    unsigned long long t = num0 / Pu;
-    unsigned rem = static_cast<unsigned>(num0 - t * Pu);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      if (e > 0) {
-        t += qS;
-        rem += rS;
-        if (rem >= Pu) {
-          rem -= Pu;
-          ++t;
-        }
-      }
-      // first m with cum[m] > t (exists: cum[P-1] = S > t).  Slots are non-decreasing in
-      // their ancestor: the quad's first slot binary-searches, the next ones step forward
-      // from the previous ancestor (a binary search again after 8 steps)
-      int steps = 0;
-      if (e > 0)
-        while (cum[lo] <= t && steps < 8) {
-          ++lo;
-          ++steps;
-        }
-      if (e == 0 || steps == 8) {
-        int hi = a.P - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (cum[mid] > t) hi = mid;
-          else lo = mid + 1;
-        }
-      }
-      const int64_t m = src + lo;
+      const int64_t m = src + (&an.x)[e];
       (&X.x)[e] = __ldg(a.x + m);
       (&Y.x)[e] = __ldg(a.y + m);
       (&Vv.x)[e] = __ldg(a.v + m);
@@ -554,7 +579,7 @@ cudaError_t launch_assoc_pairs(const PairsArgs &in, void *ws, cudaStream_t s) {
 
 cudaError_t launch_resample(const ResampleArgs &a, int sm_count, cudaStream_t s) {
   if (a.K == 0) return cudaSuccess;
-  const size_t smem = static_cast<size_t>(a.P) * (sizeof(unsigned long long) + sizeof(uint32_t));
+  const size_t smem = static_cast<size_t>(a.P) * (sizeof(uint32_t) + sizeof(int));
   // about two waves of resident CTAs (shared memory bounds residency at large P)
   const int sms = sm_count > 0 ? sm_count : 148;
   const int per_sm = a.P <= 2048 ? std::max(1, std::min(8, static_cast<int>((200 * 1024) / (smem + 1024))))
