@@ -332,11 +332,16 @@ __device__ __forceinline__ void resample_unit(const ResampleArgs &a, const int k
             static_cast<unsigned long long>(W2) * W2 + static_cast<unsigned long long>(W3) * W3;
   }
   __syncthreads();
-  // contiguous chunk per thread -> local sums -> block exclusive scan -> cum
-  const int per = (a.P + kResThreads - 1) / kResThreads;
-  const int m0 = min(a.P, threadIdx.x * per), m1 = min(a.P, m0 + per);
+  // contiguous chunk of quads per thread (16-B shared loads) -> local sums -> block
+  // exclusive scan -> cum before the chunk
+  const int qper = (quads + kResThreads - 1) / kResThreads;
+  const int g0 = min(quads, static_cast<int>(threadIdx.x) * qper), g1 = min(quads, g0 + qper);
+  const uint4 *W4 = reinterpret_cast<const uint4 *>(Wsm);
   unsigned long long loc = 0;
-  for (int m = m0; m < m1; ++m) loc += Wsm[m];
+  for (int g = g0; g < g1; ++g) {
+    const uint4 w = W4[g];
+    loc += (static_cast<unsigned long long>(w.x) + w.y) + (static_cast<unsigned long long>(w.z) + w.w);
+  }
   unsigned long long S;
   const unsigned long long run0 = block_excl_scan(loc, wsum, S);  // cum before this thread's chunk
   // Q: exact 128-bit sum (lo/hi halves reduced with carries by one thread)
@@ -395,21 +400,28 @@ __device__ __forceinline__ void resample_unit(const ResampleArgs &a, const int k
     const double inv_s = 1.0 / static_cast<double>(S);
     unsigned long long c = run0;
     int lo = res_first_slot(c, Pl, V, S, inv_s);
-    for (int m = m0; m < m1; ++m) {
-      const uint32_t Wm = Wsm[m];
-      if (Wm == 0u) continue;
-      c += Wm;
-      const int hi = res_first_slot(c, Pl, V, S, inv_s);
-      if (hi > lo) anc[lo] = m;
-      lo = hi;
+    for (int g = g0; g < g1; ++g) {
+      const uint4 w = W4[g];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t Wm = (&w.x)[e];
+        if (Wm == 0u) continue;
+        c += Wm;
+        const int hi = res_first_slot(c, Pl, V, S, inv_s);
+        if (hi > lo) anc[lo] = 4 * g + e;
+        lo = hi;
+      }
     }
   }
   __syncthreads();
   {  // inclusive prefix max over the slots: contiguous chunk per thread, warp + block scan
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int n0 = min(a.P, static_cast<int>(threadIdx.x) * per), n1 = min(a.P, n0 + per);
+    int4 *A4 = reinterpret_cast<int4 *>(anc);
     int cmax = -1;
-    for (int n = n0; n < n1; ++n) cmax = max(cmax, anc[n]);
+    for (int g = g0; g < g1; ++g) {
+      const int4 v = A4[g];
+      cmax = max(max(cmax, max(v.x, v.y)), max(v.z, v.w));
+    }
     int x = cmax;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -419,13 +431,27 @@ __device__ __forceinline__ void resample_unit(const ResampleArgs &a, const int k
     __shared__ int wmax[kResThreads / 32];
     if (lane == 31) wmax[wid] = x;
     __syncthreads();
-    int before = -1;
-    for (int w = 0; w < wid; ++w) before = max(before, wmax[w]);
+    // exclusive max over the warps before this one: a shuffle scan of wmax[]
+    int wv = lane < kResThreads / 32 ? wmax[lane] : -1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, wv, o);
+      if (lane >= o) wv = max(wv, y);
+    }
+    const int before = wid > 0 ? __shfl_sync(0xffffffffu, wv, wid - 1) : -1;
     const int xprev = __shfl_up_sync(0xffffffffu, x, 1);
     int run = max(before, lane > 0 ? xprev : -1);
-    for (int n = n0; n < n1; ++n) {
-      run = max(run, anc[n]);
-      anc[n] = run;
+    for (int g = g0; g < g1; ++g) {
+      int4 v = A4[g];
+      run = max(run, v.x);
+      v.x = run;
+      run = max(run, v.y);
+      v.y = run;
+      run = max(run, v.z);
+      v.z = run;
+      run = max(run, v.w);
+      v.w = run;
+      A4[g] = v;
     }
   }
   __syncthreads();
