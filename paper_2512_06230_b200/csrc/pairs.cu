@@ -57,6 +57,7 @@ __device__ Ti block_excl_scan(Ti v, Ti *wsum /* [32] */, Ti &total) {
 // One CTA per kept hypothesis r: |S| and a fingerprint of S for every track,
 // the per-track offsets, and the lists S (ascending i) in list[r][0..M).
 constexpr int kInvThreads = 256;
+constexpr int kInvSortMax = 32;  // rows per track sorted by one thread; more: the warp walk
 
 __global__ void __launch_bounds__(kInvThreads) invert_kernel(PairsArgs a) {
   grid_dep_wait();
@@ -87,30 +88,59 @@ __global__ void __launch_bounds__(kInvThreads) invert_kernel(PairsArgs a) {
   __syncthreads();
   // per-track outputs and the exclusive scan of the counts (offsets into list[r])
   int32_t carry = 0;
+  bool big = false;  // some track holds more than kInvSortMax rows
   const int64_t rb = static_cast<int64_t>(r) * a.T;
+  int32_t *start = reinterpret_cast<int32_t *>(fp);  // [T] list starts (fp is consumed)
   for (int32_t j0 = 0; j0 < a.T; j0 += kInvThreads) {
     const int32_t j = j0 + threadIdx.x;
     int32_t c = 0;
+    unsigned long long f = 0ull;
     if (j < a.T) {
       const bool alive = (__ldg(al + (j >> 5)) >> (j & 31)) & 1u;
       c = cnt[j];
+      f = fp[j];
       a.cnt[rb + j] = alive ? c : -1;
-      a.fp[rb + j] = mix64p(fp[j] ^ (static_cast<unsigned long long>(c) << 40));
+      a.fp[rb + j] = mix64p(f ^ (static_cast<unsigned long long>(c) << 40));
+      big |= c > kInvSortMax;
     }
     int32_t tot;
-    const int32_t ex = block_excl_scan(c, wsum, tot);
+    const int32_t ex = block_excl_scan(c, wsum, tot);  // (its barriers order fp reads before start writes)
     if (j < a.T) {
       a.off[rb + j] = carry + ex;
       cnt[j] = carry + ex;  // becomes the list cursor of track j
+      start[j] = carry + ex;
     }
     carry += tot;
   }
-  __syncthreads();
-  // lists in ascending i: warp 0 walks the rows 32 at a time; lanes with the same
+  int32_t *list = a.list + static_cast<int64_t>(r) * a.M;
+  if (!__syncthreads_or(big)) {
+    // lists in ascending i: every listed row takes a slot of its track by an atomic
+    // cursor (any order), then each track sorts its few rows -- the same ascending list
+    // whatever order the atomics ran in
+    for (int32_t i = threadIdx.x; i < a.M; i += kInvThreads) {
+      const int32_t c = __ldg(th + i);
+      if (c >= 1 && c <= a.T && ((__ldg(al + ((c - 1) >> 5)) >> ((c - 1) & 31)) & 1u))
+        list[atomicAdd(cnt + c - 1, 1)] = i;
+    }
+    __syncthreads();
+    for (int32_t j = threadIdx.x; j < a.T; j += kInvThreads) {
+      const int32_t b = start[j], e = cnt[j];
+      for (int32_t x = b + 1; x < e; ++x) {  // insertion sort (<= kInvSortMax rows)
+        const int32_t v = list[x];
+        int32_t y = x - 1;
+        while (y >= b && list[y] > v) {
+          list[y + 1] = list[y];
+          --y;
+        }
+        list[y + 1] = v;
+      }
+    }
+    return;
+  }
+  // a track with many rows: warp 0 walks the rows 32 at a time; lanes with the same
   // track are ranked by lane, and the group's leader advances the cursor
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
-    int32_t *list = a.list + static_cast<int64_t>(r) * a.M;
     for (int32_t i0 = 0; i0 < a.M; i0 += 32) {
       const int32_t i = i0 + lane;
       int32_t key = -1 - lane;  // unique per lane when the row is not listed

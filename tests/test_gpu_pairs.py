@@ -73,7 +73,8 @@ def test_pairs_hand_example(L, orc):
 
 
 @pytest.mark.parametrize("T,M,n,seed", [(23, 40, 60, 4), (1040, 1198, 25, 3), (300, 0, 5, 1), (5, 7, 1, 2),
-                                        (70, 513, 100, 6)])
+                                        (70, 513, 100, 6),
+                                        (5, 300, 8, 7), (2, 1000, 3, 8)])   # > 32 rows per track: warp-walk lists
 def test_pairs_random(L, orc, T, M, n, seed):
     rng = np.random.default_rng(seed)
     ldt = (T + 31) // 32
