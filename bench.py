@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--h-max", type=int, default=100)
     ap.add_argument("--no-convoy", action="store_true", help="skip the paper-shaped convoy run (f4)")
     ap.add_argument("--no-graphs", action="store_true", help="skip the CUDA-graph timing of configs 0-2")
+    ap.add_argument("--no-skip-probe", action="store_true", help="skip the exact zero-tile skipping probe")
+    ap.add_argument("--compat-probe", type=int, default=None, help=argparse.SUPPRESS)  # child: predicts
     return ap.parse_args()
 
 
@@ -283,6 +285,57 @@ def make_line(*, cfg_id, cfg, world, steps, warmup, elapsed_ms, evals_total, pai
 
 
 # ------------------------------------------------------------------ GLMB update
+def compat_probe_child(cfg_id: int, n_pred: int, reps: int = 10) -> None:
+    """Child process of skip_probe: glmb_compat on config cfg_id after n_pred predicts, mean
+    launch time over `reps` (CUDA events) and a checksum of C and the gate words."""
+    import hashlib
+    import torch
+    from paper_2512_06230_b200 import _lib as L
+    from paper_2512_06230_b200.scenes import make_scene
+    from paper_2512_06230_b200.step import GlmbStep
+    torch.cuda.set_device(0)
+    L.glmb_init(0)
+    sc = make_scene(cfg_id, steps=1)
+    st = GlmbStep(sc, device="cuda:0")
+    for k in range(n_pred):
+        st.predict(k)
+    for _ in range(2):
+        st.compat(0)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        st.compat(0)
+    e1.record()
+    torch.cuda.synchronize()
+    M = len(sc.Z[0])
+    h = hashlib.sha256(st.out.C_tracks[:, :M].cpu().numpy().tobytes() + st.out.gate.cpu().numpy().tobytes())
+    print(json.dumps({"ms": e0.elapsed_time(e1) / reps, "sha": h.hexdigest()[:16]}), flush=True)
+
+
+def skip_probe(cfg_id: int) -> dict:
+    """Exact zero-tile skipping (GLMB_COMPAT_SKIP=1, opt-in, not the headline): compat with and
+    without it on the step-0 clouds and after 25 predicts (the timed steps' diffused clouds),
+    each setting in its own process; bit-identity by checksum of C and the gate words."""
+    import subprocess
+    out = {"note": "GLMB_COMPAT_SKIP=1: a warp skips a particle tile when all its measurements are >= 200 "
+                   "whitened units^2 from the tile's bounding box (contributions exactly +0 on both exp "
+                   "paths); opt-in, the headline is the dense pass"}
+    for pred in (0, 25):
+        r = {}
+        for skip in ("0", "1"):
+            env = dict(os.environ, GLMB_COMPAT_SKIP=skip)
+            p = subprocess.run([sys.executable, os.path.abspath(__file__), "--compat-probe", str(pred),
+                                "--config", str(cfg_id)], env=env, capture_output=True, text=True, timeout=600)
+            line = [l for l in p.stdout.splitlines() if l.startswith("{")]
+            if p.returncode != 0 or not line:
+                return {"error": (p.stderr or p.stdout)[-300:]}
+            r[skip] = json.loads(line[-1])
+        out[f"pred{pred}"] = {"dense_ms": r["0"]["ms"], "skip_ms": r["1"]["ms"],
+                              "speedup": r["0"]["ms"] / r["1"]["ms"], "bit_identical": r["0"]["sha"] == r["1"]["sha"]}
+    return out
+
+
 def verify_fused_gather(st, symm_cols, C_full, G_full, plan, rank, world, dev, stream) -> bool:
     """Before timing (N > 1): the fused compat + peer-store gather must give every rank
     exactly the C_k / gate words an NCCL all-gather of glmb_compat's local columns gives
@@ -464,6 +517,8 @@ def main():
     cfg_id = a.config if a.config is not None else (3 if world == 1 else 4)
     if a.impl == "reference":
         return reference_arm(a, cfg_id)
+    if a.compat_probe is not None:
+        return compat_probe_child(cfg_id, a.compat_probe)
 
     import torch
     import torch.distributed as dist
@@ -713,6 +768,9 @@ def main():
     convoy = None
     if world == 1 and not a.no_convoy:
         convoy = bench_convoy(dev)
+    skipped = None
+    if world == 1 and not a.no_skip_probe:
+        skipped = skip_probe(cfg_id)
 
     cpu = None
     if world == 1 and not a.no_cpu_baseline:
@@ -733,6 +791,8 @@ def main():
         line["glmb_update"] = update
     if convoy is not None:
         line["convoy"] = convoy
+    if skipped is not None:
+        line["compat_exact_skip"] = skipped
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

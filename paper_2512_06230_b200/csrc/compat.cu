@@ -218,7 +218,14 @@ __device__ __forceinline__ void tile_dispatch(int hv, const float4 *A, int np, M
 // ranks' partial sums in rank order through DSMEM and writes the epilogue.  Each
 // CTA does 1/CL of the unit's work, so the last wave of the grid is CL times
 // shorter (the tail of a 2.2-wave grid cost ~12 % of the launch).
-template <int NW, int K, int EMU_PERIOD, int CL>
+// SKIP (opt-in, GLMB_COMPAT_SKIP=1): a warp skips a particle tile when every one of its
+// measurements lies >= kSkipD2 whitened units^2 from the tile's bounding box.  Every pair
+// it skips has q >= 200, where both exp paths give exactly +0 (MUFU.EX2.FTZ flushes below
+// 2^-126; the polynomial clamps at q = 189 and w 2^-64 * p 2^-125 rounds to 0 below
+// 2^-150), so C and the gate words are bit-identical to the dense pass.
+constexpr float kSkipD2 = 200.0f;
+
+template <int NW, int K, int EMU_PERIOD, int CL, bool SKIP = false>
 __global__ void __launch_bounds__(32 * NW, min_blocks<NW, K>()) compat_kernel(const CompatArgs a) {
   grid_dep_wait();  // launched with programmatic serialization after predict / birth
   constexpr int H = Meas<K>::H;
@@ -229,6 +236,7 @@ __global__ void __launch_bounds__(32 * NW, min_blocks<NW, K>()) compat_kernel(co
   float4 *aos = reinterpret_cast<float4 *>(smem + kStages * kRawFloats);  // 2 AoS tiles
   __shared__ __align__(8) uint64_t bars[kStages];
   __shared__ float red[2][kVWarps];
+  __shared__ float tbox[SKIP ? 2 : 1][SKIP ? NW : 1][4];  // per tile parity and warp: min/max X', Y'
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int unit = blockIdx.x / CL;
@@ -329,14 +337,75 @@ __global__ void __launch_bounds__(32 * NW, min_blocks<NW, K>()) compat_kernel(co
       continue;
     }
     // whiten raw tile -> AoS (X', Y', w 2^-64, w)
-    for (int idx = tid; idx < np; idx += kThreads) {
-      const float lx = X[idx] - cx, ly = Y[idx] - cy;
-      A[idx] = make_float4(fmaf(a.a2, ly, a.a1 * lx), a.b2 * ly, W[idx] * kTwoM64, W[idx]);
+    if constexpr (!SKIP) {
+      for (int idx = tid; idx < np; idx += kThreads) {
+        const float lx = X[idx] - cx, ly = Y[idx] - cy;
+        A[idx] = make_float4(fmaf(a.a2, ly, a.a1 * lx), a.b2 * ly, W[idx] * kTwoM64, W[idx]);
+      }
+    } else {
+      float bx0 = INFINITY, bx1 = -INFINITY, by0 = INFINITY, by1 = -INFINITY;
+      for (int idx = tid; idx < np; idx += kThreads) {
+        const float lx = X[idx] - cx, ly = Y[idx] - cy;
+        const float qx = fmaf(a.a2, ly, a.a1 * lx), qy = a.b2 * ly;
+        A[idx] = make_float4(qx, qy, W[idx] * kTwoM64, W[idx]);
+        bx0 = fminf(bx0, qx);
+        bx1 = fmaxf(bx1, qx);
+        by0 = fminf(by0, qy);
+        by1 = fmaxf(by1, qy);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        bx0 = fminf(bx0, __shfl_xor_sync(0xffffffffu, bx0, o));
+        bx1 = fmaxf(bx1, __shfl_xor_sync(0xffffffffu, bx1, o));
+        by0 = fminf(by0, __shfl_xor_sync(0xffffffffu, by0, o));
+        by1 = fmaxf(by1, __shfl_xor_sync(0xffffffffu, by1, o));
+      }
+      if (lane == 0) {
+        tbox[t & 1][warp][0] = bx0;
+        tbox[t & 1][warp][1] = bx1;
+        tbox[t & 1][warp][2] = by0;
+        tbox[t & 1][warp][3] = by1;
+      }
     }
     fence_proxy_async_smem();  // the raw stage was read through the generic proxy; TMA rewrites it next
     __syncthreads();           // AoS tile t complete; every warp is done with tile t-1
     if (tid == 0 && t + 1 < t_end) issue_tile(a, xs, ys, ws, smem, &bars[0], t + 1);
-    if (hv > 0) tile_dispatch<K, EMU_PERIOD>(hv, A, np, m);
+    if constexpr (!SKIP) {
+      if (hv > 0) tile_dispatch<K, EMU_PERIOD>(hv, A, np, m);
+    } else if (hv > 0) {
+      {
+        float x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          x0 = fminf(x0, tbox[t & 1][w][0]);
+          x1 = fmaxf(x1, tbox[t & 1][w][1]);
+          y0 = fminf(y0, tbox[t & 1][w][2]);
+          y1 = fmaxf(y1, tbox[t & 1][w][3]);
+        }
+        bool far = true;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const int i = wbase + k * 32 + lane;
+          if (i < a.M) {
+            float zx, zy, z1x, z1y;
+            f2_unpack(m.zx2[k >> 1], zx, z1x);
+            f2_unpack(m.zy2[k >> 1], zy, z1y);
+            if (k & 1) {
+              zx = z1x;
+              zy = z1y;
+            }
+            zx *= 0.5f;
+            zy *= 0.5f;
+            const float dx = fmaxf(0.0f, fmaxf(x0 - zx, zx - x1)), dy = fmaxf(0.0f, fmaxf(y0 - zy, zy - y1));
+            far &= fmaf(dx, dx, dy * dy) >= kSkipD2;
+          }
+        }
+        const bool skip = __all_sync(0xffffffffu, far);
+        if (skip && lane == 0 && a.skip_count != nullptr)
+          atomicAdd(a.skip_count, static_cast<unsigned long long>(np) * static_cast<unsigned long long>(min(32 * K, a.M - wbase)));
+        if (!skip) tile_dispatch<K, EMU_PERIOD>(hv, A, np, m);
+      }
+    }
   }
 
   if constexpr (CL > 1) {  // rank 0 adds the ranks' partial sums in rank order (DSMEM)
@@ -388,11 +457,11 @@ __global__ void clutter_fill_kernel(float *c, int32_t M, float kappa) {
   if (i < M) c[i] = kappa;
 }
 
-template <int NW, int K, int EMU_PERIOD, int CL>
+template <int NW, int K, int EMU_PERIOD, int CL, bool SKIP>
 cudaError_t launch_kc(const CompatArgs &a, cudaStream_t s) {
   const int64_t grid = static_cast<int64_t>(a.T) * a.n_mtiles * CL;
   if (CL == 1)
-    return launch_pdl(compat_kernel<NW, K, EMU_PERIOD, CL>, dim3(static_cast<unsigned>(grid)), dim3(32 * NW),
+    return launch_pdl(compat_kernel<NW, K, EMU_PERIOD, CL, SKIP>, dim3(static_cast<unsigned>(grid)), dim3(32 * NW),
                       kSmemBytes, s, a);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
@@ -408,12 +477,26 @@ cudaError_t launch_kc(const CompatArgs &a, cudaStream_t s) {
   attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, compat_kernel<NW, K, EMU_PERIOD, CL>, a);
+  return cudaLaunchKernelEx(&cfg, compat_kernel<NW, K, EMU_PERIOD, CL, SKIP>, a);
+}
+
+// GLMB_COMPAT_SKIP=1: exact zero-tile skipping (opt-in; the dense pass is the default
+// and the measured headline).  Built for the default exp split only.
+bool skip_enabled() {
+  static const bool v = [] {
+    const char *e = std::getenv("GLMB_COMPAT_SKIP");
+    return e && std::atoi(e) == 1;
+  }();
+  return v;
 }
 
 template <int NW, int K, int EMU_PERIOD>
 cudaError_t launch_k(const CompatArgs &a, cudaStream_t s) {
-  return a.CL == 2 ? launch_kc<NW, K, EMU_PERIOD, 2>(a, s) : launch_kc<NW, K, EMU_PERIOD, 1>(a, s);
+  if constexpr (EMU_PERIOD == -10) {
+    if (skip_enabled())
+      return a.CL == 2 ? launch_kc<NW, K, EMU_PERIOD, 2, true>(a, s) : launch_kc<NW, K, EMU_PERIOD, 1, true>(a, s);
+  }
+  return a.CL == 2 ? launch_kc<NW, K, EMU_PERIOD, 2, false>(a, s) : launch_kc<NW, K, EMU_PERIOD, 1, false>(a, s);
 }
 
 // Share of the exps evaluated on the FMA pipe: one particle in |EMU| (negative:

@@ -72,6 +72,9 @@ struct CompatArgs {
   uint32_t *const *peer_G;
   int32_t n_peers;
   int64_t peer_row0;
+  // exact zero-tile skipping (GLMB_COMPAT_SKIP=1, opt-in): optional device counter of the
+  // particle-measurement pairs skipped because their contribution is exactly +0
+  unsigned long long *skip_count;
 };
 
 struct ReweightArgs {

@@ -608,3 +608,24 @@ def test_step_host_csr_matches_dense(L, orc):
     np.testing.assert_array_equal(val2.numpy()[:nnz], val_h.numpy()[:nnz])
     np.testing.assert_array_equal(ln2.numpy(), ln_a.numpy())
     np.testing.assert_array_equal(d.weights().cpu().numpy(), c.weights().cpu().numpy())
+
+
+@pytest.mark.parametrize("cfg_id,n_rows,n_pred", [(1, 64, 0), (3, 96, 0), (3, 96, 12)])
+def test_compat_exact_skip(cfg_id, n_rows, n_pred, tmp_path):
+    """GLMB_COMPAT_SKIP=1 (warps skip particle tiles whose every pair has q >= 200, where both
+    exp paths give exactly +0) reproduces the dense pass bit for bit: C and the gate words
+    from two child processes, one per setting (compact and diffused clouds)."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    outs = {}
+    for skip in ("0", "1"):
+        out = str(tmp_path / f"c{skip}.npz")
+        env = dict(os.environ, GLMB_COMPAT_SKIP=skip, PYTHONPATH=os.path.dirname(here))
+        r = subprocess.run([sys.executable, os.path.join(here, "_compat_dump.py"), str(cfg_id), str(n_rows),
+                            str(n_pred), out], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        outs[skip] = np.load(out)
+    np.testing.assert_array_equal(outs["0"]["C"].view(np.uint32), outs["1"]["C"].view(np.uint32))
+    np.testing.assert_array_equal(outs["0"]["G"], outs["1"]["G"])
