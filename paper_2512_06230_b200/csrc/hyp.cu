@@ -693,7 +693,7 @@ __global__ void __launch_bounds__(kPruneThreads) prune_kernel(PruneArgs a) {
   __shared__ int32_t si[32];
   __shared__ uint32_t hist[256];
   __shared__ unsigned long long prefix_s;
-  __shared__ int32_t need_s;
+  __shared__ int32_t need_s, done_s;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int32_t n = a.n;
 
@@ -776,7 +776,7 @@ __global__ void __launch_bounds__(kPruneThreads) prune_kernel(PruneArgs a) {
   int32_t ties = 0;
   bool select = K > a.h_max;
   if (select) {
-    if (threadIdx.x == 0) { prefix_s = 0ull; need_s = a.h_max; }
+    if (threadIdx.x == 0) { prefix_s = 0ull; need_s = a.h_max; done_s = 0; }
     __syncthreads();
     for (int shift = 56; shift >= 0; shift -= 8) {
       for (int b = threadIdx.x; b < 256; b += kPruneThreads) hist[b] = 0u;
@@ -810,20 +810,32 @@ __global__ void __launch_bounds__(kPruneThreads) prune_kernel(PruneArgs a) {
           int b = 255 - 8 * l - 7;
           int32_t rem = need - above;
 #pragma unroll
+          int32_t hbb = 0;
           for (int k = 0; k < 8; ++k) {
             if (hb[k] >= need - above) {
               b = 255 - 8 * l - k;
               rem = need - above;
+              hbb = hb[k];
               break;
             }
             above += hb[k];
             rem = need - above;
           }
-          need_s = rem;
-          prefix_s = pre | (static_cast<unsigned long long>(b) << shift);
+          const unsigned long long pb = pre | (static_cast<unsigned long long>(b) << shift);
+          if (hbb == rem && shift > 0) {
+            // the whole bin is kept: every key >= pb (its lowest possible value) and none
+            // below -- threshold pb - 1 with no ties, the remaining digits need no pass
+            need_s = 0;
+            prefix_s = pb - 1ull;
+            done_s = 1;
+          } else {
+            need_s = rem;
+            prefix_s = pb;
+          }
         }
       }
       __syncthreads();
+      if (done_s) break;
     }
     thr = prefix_s;
     ties = need_s;  // how many keys == thr to keep
