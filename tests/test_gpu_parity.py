@@ -325,9 +325,10 @@ def test_reweight_paths_and_multi_detection(L, orc, P):
     np.testing.assert_array_equal(fl, 0)
 
 
-def test_reweight_degenerate_and_many_assigned(L, orc):
+@pytest.mark.parametrize("P", [256, 8192])   # cluster kernel / flat two-pass kernel
+def test_reweight_degenerate_and_many_assigned(L, orc, P):
     r = np.random.default_rng(3)
-    T, P, M = 2, 256, 1500          # > 256 assigned measurements: generic S path
+    T, M = 2, 1500                  # > 256 assigned measurements: generic S path
     x = r.normal(0, 1, (T, P)).astype(np.float32)
     y = r.normal(0, 1, (T, P)).astype(np.float32)
     w = r.dirichlet(np.ones(P), T).astype(np.float32)
