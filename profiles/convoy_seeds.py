@@ -18,7 +18,13 @@ N = int(sys.argv[1]) if len(sys.argv) > 1 else 20
 H = int(sys.argv[2]) if len(sys.argv) > 2 else 100
 seeds = [int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else list(range(10))
 extra = dict(a.split("=") for a in sys.argv[4].split(";")) if len(sys.argv) > 4 and sys.argv[4] else {}
-extra = {k: (float(v) if "." in v or "e" in v else int(v)) for k, v in extra.items()}
+def _conv(v):
+    if "," in v:
+        return tuple(float(x) for x in v.split(","))
+    return float(v) if "." in v or "e" in v else int(v)
+
+
+extra = {k: _conv(v) for k, v in extra.items()}
 for seed in seeds:
     cfg = ConvoyConfig(N=N, H_max=H, seed=seed, **extra)
     recs, ests, truth = run_convoy(cfg, K_cap=4096)
