@@ -258,8 +258,8 @@ def make_line(*, cfg_id, cfg, world, steps, warmup, elapsed_ms, evals_total, pai
         "data": "synthetic",
         "config": {"workload": f"cfg{cfg_id} ({cfg.name})", "T": cfg.T, "B": cfg.B, "P": cfg.P,
                    "M_mean": M_mean, "parallelism": f"tracks sharded x{world}",
-                   "l2": "inputs larger than L2: particle state 24 B x T_k x P (204 MB at cfg3) "
-                         "streams from HBM every step",
+                   "l2": f"inputs larger than L2: particle state 24 B x T_k x P "
+                         f"({24 * (cfg.T + cfg.B) * cfg.P / 1e6:.0f} MB) streams from HBM every step",
                    "evals_per_step": evals_total / steps,
                    "schedule": "predict, birth; then compat overlapped with reweight on a second stream "
                                "(double-buffered weights); stages_ms timed in a separate serialised pass"},
