@@ -428,11 +428,25 @@ def bench_update(a, st, scene, cfg, dev, stream, L):
     rp = hu.row_ptr[:M + 1].cpu().numpy()
     row_len = np.diff(rp)
     fl = pu.flags[:n_pairs].cpu().numpy()
+    n_res = int(((fl >> 1) & 1).sum())
+    stage_mean = {n: statistics.mean(v) for n, v in stage.items()}
+    P = st.P
+    hbm = hbm_peak()
+
+    def hbm_stage(name, nbytes):
+        gbps = nbytes / (stage_mean[name] * 1e-3) / 1e9 if stage_mean[name] > 0 else 0.0
+        return {"bytes": int(nbytes), "achieved_GBps": gbps, "peak_GBps": hbm, "frac": gbps / hbm}
+
+    # algorithmic bytes: reweight_pairs reads x, y, w and writes w' (16 B per particle and
+    # pair); resample reads w' (4 B) and, per resampled pair, gathers 5 state fields (20 B)
+    # and writes 6 (24 B), per kept pair copies 6 fields (24 + 24 B)
+    hbm_f2 = {"reweight_pairs": hbm_stage("reweight_pairs", 16 * P * n_pairs),
+              "resample": hbm_stage("resample", P * (4 * n_pairs + 44 * n_res + 48 * (n_pairs - n_res)))}
     return {"workload": f"cfg{a.config if a.config is not None else 3} C_k (T_k={T}, M={M}) + particles; "
                         f"H_old={a.h_old} x H_up={a.h_up}, tau=1e-5, H_max={a.h_max} (P:186)",
-            "ms": statistics.mean(total), "stages_ms": {n: statistics.mean(v) for n, v in stage.items()},
+            "ms": statistics.mean(total), "stages_ms": stage_mean, "hbm_kernels": hbm_f2,
             "n_samples": a.h_old * a.h_up, "n_unique": int(hu.unique.sum().item()), "n_kept": n_kept,
-            "n_pairs": n_pairs, "n_resampled": int(((fl >> 1) & 1).sum()),
+            "n_pairs": n_pairs, "n_resampled": n_res,
             "gated_entries": int(rp[-1]), "row_len_max": int(row_len.max()) if M else 0,
             "rows_empty": int((row_len == 0).sum()),
             "gpu_launches_per_update": 14,
