@@ -164,11 +164,18 @@ class OracleSample:
                 f"P={c.P} (predict+compat+reweight, fp64, OpenMP over tracks), {dt:.2f} s")
 
 
-def oracle_sample(cfg_id: int, seconds: float, cores: int):
+def oracle_sample(cfg_id: int, seconds: float, cores: int, single_core: bool = True):
+    """The oracle on all `cores` host threads (the reported baseline) and, beside it, on one
+    thread with a third of the time budget (oracle at 1 and all host cores)."""
     smp = OracleSample(cfg_id, seconds, cores)
     dt, evals = smp.run()
-    return {"value": evals / dt, "unit": "evals/s", "cores": cores, "kind": "oracle",
-            "sample": smp.describe(dt)}
+    out = {"value": evals / dt, "unit": "evals/s", "cores": cores, "kind": "oracle",
+           "sample": smp.describe(dt)}
+    if single_core and cores > 1:
+        one = OracleSample(cfg_id, seconds / 3, 1)
+        dt1, ev1 = one.run()
+        out["single_core"] = {"value": ev1 / dt1, "unit": "evals/s", "cores": 1, "sample": one.describe(dt1)}
+    return out
 
 
 def reference_arm(a, cfg_id):
