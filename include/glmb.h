@@ -522,6 +522,9 @@ glmb_status glmb_resample(const glmb_particles *src, int32_t K,
  * the pairs pair_of[r][j] >= 0 with index < K_cap (their rows in the new
  * particle set) and of the birth columns birth_col0 .. birth_col0+B-1;
  * parent_logw[r] = ln keep_w[r]; *n_parents = min(*n_kept, n_hyp_cap).
+ * birth_col0_dev (optional, device): when non-NULL the birth columns start at
+ * min(*birth_col0_dev, K_cap) instead (e.g. glmb_assoc_pairs' *n_pairs, so
+ * the call can be enqueued before the host reads the pair count).
  * Rows r >= *n_kept are not written.  All pointers device memory.
  * Errors: INVALID_ARG on negative sizes, K_cap or birth columns beyond
  * 32*ldt, ldt > 12288, NULL pointers. */
@@ -530,7 +533,9 @@ glmb_status glmb_next_parents(int32_t n_hyp_cap, const int32_t *n_kept,
                               int32_t T, int32_t K_cap, int32_t B,
                               int32_t birth_col0, uint32_t *parent_mask,
                               int32_t ldt, double *parent_logw,
-                              int32_t *n_parents, glmb_stream_t stream);
+                              int32_t *n_parents,
+                              const int32_t *birth_col0_dev,
+                              glmb_stream_t stream);
 
 /* glmb_map_estimate -- the state estimate of the most likely hypothesis
  * (R34): for every old track j < T with k = pair_of0[j] >= 0 (row 0 of

@@ -98,7 +98,7 @@ def load(path: str = LIB_PATH):
         L.glmb_assoc_sample.argtypes = [i32, vp, i32, i32, i32, vp, i32, vp, vp, vp, f32, f32, vp, vp, vp,
                                         vp, vp, i32, u64, u32, vp, vp, i64, vp, vp, vp]
         L.glmb_dedup.argtypes = [i32, vp, i32, i32, vp, i32, vp, i64, vp, vp, vp]
-        L.glmb_next_parents.argtypes = [i32, vp, vp, vp, i32, i32, i32, i32, vp, i32, vp, vp, vp]
+        L.glmb_next_parents.argtypes = [i32, vp, vp, vp, i32, i32, i32, i32, vp, i32, vp, vp, vp, vp]
         L.glmb_map_estimate.argtypes = [vp, vp, i32, PP, vp, vp]
         L.glmb_update.argtypes = [C.POINTER(glmb_update_params), vp]
         L.glmb_step_host_csr.argtypes = [SP, vp, i32, vp, vp, vp, vp, i64, vp, i64, vp, vp, vp, vp, vp, vp,
@@ -348,12 +348,13 @@ def glmb_resample(src: Particles, K, n_pairs, pair_track, w, out: Particles, see
 
 # --------------------------------------------------------------- tracker loop (f4)
 def glmb_next_parents(n_kept, keep_w, pair_of, K_cap, B, birth_col0, parent_mask, parent_logw, n_parents,
-                      stream=None):
-    """pair_of [n_hyp_cap, T] int32; parent_mask [n_hyp_cap, ldt] int32 words (outputs on device)."""
+                      stream=None, birth_col0_dev=None):
+    """pair_of [n_hyp_cap, T] int32; parent_mask [n_hyp_cap, ldt] int32 words (outputs on device).
+    birth_col0_dev: optional device int32 (e.g. n_pairs) overriding birth_col0."""
     n_hyp_cap, T = pair_of.shape
     _check(load().glmb_next_parents(n_hyp_cap, _ptr(n_kept), _ptr(keep_w), _ptr(pair_of), T, int(K_cap), int(B),
                                     int(birth_col0), _ptr(parent_mask), parent_mask.shape[1], _ptr(parent_logw),
-                                    _ptr(n_parents), _stream(stream)))
+                                    _ptr(n_parents), _ptr(birth_col0_dev), _stream(stream)))
 
 
 def glmb_map_estimate(n_kept, pair_of0, new_set: Particles, est, stream=None):

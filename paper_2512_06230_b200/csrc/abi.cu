@@ -527,10 +527,11 @@ glmb_status glmb_resample(const glmb_particles *src, int32_t K, const int32_t *n
 // ------------------------------------------------------------------ tracker loop (f4)
 glmb_status glmb_next_parents(int32_t n_hyp_cap, const int32_t *n_kept, const double *keep_w, const int32_t *pair_of,
                               int32_t T, int32_t K_cap, int32_t B, int32_t birth_col0, uint32_t *parent_mask,
-                              int32_t ldt, double *parent_logw, int32_t *n_parents, glmb_stream_t stream) {
+                              int32_t ldt, double *parent_logw, int32_t *n_parents, const int32_t *birth_col0_dev,
+                              glmb_stream_t stream) {
   if (n_hyp_cap < 0 || T < 0 || K_cap < 0 || B < 0 || birth_col0 < 0 || ldt < 1) return GLMB_ERR_INVALID_ARG;
-  if (static_cast<int64_t>(K_cap) > 32LL * ldt || static_cast<int64_t>(birth_col0) + B > 32LL * ldt ||
-      ldt > 12 * 1024)
+  const int64_t col_max = birth_col0_dev != nullptr ? static_cast<int64_t>(K_cap) : static_cast<int64_t>(birth_col0);
+  if (static_cast<int64_t>(K_cap) > 32LL * ldt || col_max + B > 32LL * ldt || ldt > 12 * 1024)
     return GLMB_ERR_INVALID_ARG;
   if (n_kept == nullptr || n_parents == nullptr) return GLMB_ERR_INVALID_ARG;
   if (n_hyp_cap > 0 && (keep_w == nullptr || parent_mask == nullptr || parent_logw == nullptr ||
@@ -539,7 +540,7 @@ glmb_status glmb_next_parents(int32_t n_hyp_cap, const int32_t *n_kept, const do
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   GLMB_TRY(bind_stream(s, nullptr));
   glmb::NextParentsArgs a{n_hyp_cap, n_kept, keep_w, pair_of, T, K_cap, B, birth_col0, ldt, parent_mask,
-                          parent_logw, n_parents};
+                          parent_logw, n_parents, birth_col0_dev};
   return from_cuda(glmb::launch_next_parents(a, s));
 }
 

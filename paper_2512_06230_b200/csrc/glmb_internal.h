@@ -232,6 +232,7 @@ struct NextParentsArgs {
   uint32_t *parent_mask;   // [n_hyp_cap][ldt]
   double *parent_logw;
   int32_t *n_parents;
+  const int32_t *birth_col0_dev;  // optional: birth columns start at min(*birth_col0_dev, K_cap)
 };
 cudaError_t launch_next_parents(const NextParentsArgs &a, cudaStream_t s);
 

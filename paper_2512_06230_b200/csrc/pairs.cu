@@ -535,8 +535,9 @@ __global__ void __launch_bounds__(128) next_parents_kernel(NextParentsArgs a) {
     const int32_t k = __ldg(po + j);
     if (k >= 0 && k < a.K_cap) atomicOr(msk + (k >> 5), 1u << (k & 31));
   }
+  const int32_t col0 = a.birth_col0_dev != nullptr ? min(__ldg(a.birth_col0_dev), a.K_cap) : a.birth_col0;
   for (int32_t b = threadIdx.x; b < a.B; b += blockDim.x) {
-    const int32_t c = a.birth_col0 + b;
+    const int32_t c = col0 + b;
     atomicOr(msk + (c >> 5), 1u << (c & 31));
   }
   __syncthreads();

@@ -178,14 +178,16 @@ class ConvoyTracker:
                 _lib.glmb_update(self._update_params(trk, Tk, M, k), s)
             self.counts_host.copy_(self.counts, non_blocking=True)   # (n_pairs, n_kept, n_parents)
             e1.record(s)
+            # kept hypotheses -> parents over the new rows [0, K) and the next births at
+            # [K, K + B), K read on the device (enqueued before the host waits for K)
+            _lib.glmb_next_parents(hu.n_kept, hu.keep_w, po, self.K_cap, B, 0,
+                                   self.parent_mask, self.parent_logw, self.n_parents, s,
+                                   birth_col0_dev=pu.n_pairs)
         s.synchronize()
         self.last_events = evs
         K, n_kept, n_par = (int(v) for v in self.counts_host)
         if K > self.K_cap:
             raise RuntimeError(f"step {k}: {K} unique pairs exceed K_cap = {self.K_cap}")
-        # kept hypotheses -> parents over the new rows [0, K) and the next births at [K, K + B)
-        _lib.glmb_next_parents(hu.n_kept, hu.keep_w, po, self.K_cap, B, K,
-                               self.parent_mask, self.parent_logw, self.n_parents, s)
         wall = (time.perf_counter() - t0) * 1e3
         self.n_surv = K
         self.cur = 1 - self.cur

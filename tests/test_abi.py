@@ -140,5 +140,6 @@ def test_validation_hypothesis_calls_without_gpu():
     assert L.glmb_resample(C.byref(p), 2, None, fake, fake, 6, C.byref(p), 0, 0, None, None) == -2   # ldw % 4
     assert L.glmb_resample(C.byref(p), 3, None, fake, fake, 8, C.byref(p), 0, 0, None, None) == -1   # out too small
     # tracker loop
-    assert L.glmb_next_parents(4, fake, fake, fake, 10, 64, 1, 0, fake, 1, fake, fake, None) == -1  # K_cap > 32 ldt
+    assert L.glmb_next_parents(4, fake, fake, fake, 10, 64, 1, 0, fake, 1, fake, fake, None, None) == -1  # K_cap > 32 ldt
+    assert L.glmb_next_parents(4, fake, fake, fake, 10, 32, 1, 0, fake, 1, fake, fake, fake, None) == -1  # K_cap + B > 32 ldt (device col0)
     assert L.glmb_map_estimate(None, fake, 3, C.byref(p), fake, None) == -1

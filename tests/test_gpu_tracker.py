@@ -55,6 +55,11 @@ def test_next_parents_vs_oracle(L, orc, H, T, K_cap, B, col0, n_kept):
     assert np.all(m[n_kept:] == 0xFFFFFFFF)                    # rows past n_kept untouched
     np.testing.assert_allclose(_host(lw)[:n_kept], r_lw, rtol=1e-15)
     assert int(_host(npar)[0]) == n_kept
+    # the same with the birth column read on the device (e.g. glmb_assoc_pairs' n_pairs)
+    mask2 = torch.full((H, ldt), -1, dtype=torch.int32, device="cuda")
+    L.glmb_next_parents(_dev(np.array([n_kept], np.int32)), _dev(keep_w), _dev(pair_of), K_cap, B, 0,
+                        mask2, lw, npar, birth_col0_dev=_dev(np.array([col0], np.int32)))
+    np.testing.assert_array_equal(_host(mask2).view(np.uint32)[:n_kept], r_mask)
 
 
 @pytest.mark.parametrize("P", [4, 1024, 8192])
