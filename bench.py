@@ -287,7 +287,7 @@ def make_line(*, cfg_id, cfg, world, steps, warmup, elapsed_ms, evals_total, pai
         "clocks": clocks,
         "e2e": e2e,
         "cpu_baseline": None if cpu is None else
-        {k: v for k, v in cpu.items() if k in ("value", "unit", "cores", "kind", "sample")},
+        {k: v for k, v in cpu.items() if k in ("value", "unit", "cores", "kind", "sample", "single_core")},
     }
 
 
