@@ -493,17 +493,20 @@ __global__ void __launch_bounds__(kThreads, R == 1 ? 5 : (R == 2 ? 3 : 2)) rewei
 // triples merge in a fixed order.  Pass 2 re-reads x, y, w (L2-resident by then),
 // recomputes l_p bit for bit and writes w'_p = 2^(l_p - m) / s.  Nothing waits at a
 // cluster barrier holding registers, so ~8 CTAs per SM stream concurrently.
-__device__ __forceinline__ void online_add(double l, double &m, double &s, double &s2) {
+// The per-thread sums stay fp32 (at most P / 256 terms of at most 1 each, rel. error
+// ~1e-6); the conversions fp32 <-> fp64 run on the XU pipe beside MUFU, so keeping the
+// running sums out of fp64 halves them per particle.
+__device__ __forceinline__ void online_add(double l, double &m, float &s, float &s2) {
   if (l == -INFINITY) return;
   if (l > m) {
-    const double f = m == -INFINITY ? 0.0 : static_cast<double>(ex2_approx(static_cast<float>(m - l)));
-    s = s * f + 1.0;
-    s2 = s2 * (f * f) + 1.0;
+    const float f = m == -INFINITY ? 0.0f : ex2_approx(static_cast<float>(m - l));
+    s = fmaf(s, f, 1.0f);
+    s2 = fmaf(s2, f * f, 1.0f);
     m = l;
   } else {
-    const double e = ex2_approx(static_cast<float>(l - m));
+    const float e = ex2_approx(static_cast<float>(l - m));
     s += e;
-    s2 += e * e;
+    s2 = fmaf(e, e, s2);
   }
 }
 
@@ -558,7 +561,8 @@ __device__ __forceinline__ void reweight_flat_unit(const ReweightArgs &a, const 
 
   // pass 1: online (m, s, s2) per thread; the next quad's loads are issued before this
   // quad's arithmetic
-  double m = -INFINITY, sm = 0.0, sm2 = 0.0;
+  double m = -INFINITY;
+  float sm = 0.0f, sm2 = 0.0f;
   {
     int g = threadIdx.x;
     float4 X = X0, Y = Y0, W = W0;
@@ -585,7 +589,8 @@ __device__ __forceinline__ void reweight_flat_unit(const ReweightArgs &a, const 
   // warp: max by shuffles, the lanes' sums rescaled to it; CTA: thread 0 merges the warps
   const double mw = warp_max_d(m);
   const double f = mw == -INFINITY || m == -INFINITY ? 0.0 : static_cast<double>(ex2_approx(static_cast<float>(m - mw)));
-  double sw = warp_sum_d(sm * f), sw2 = a.ess != nullptr ? warp_sum_d(sm2 * (f * f)) : 0.0;
+  double sw = warp_sum_d(static_cast<double>(sm) * f),
+         sw2 = a.ess != nullptr ? warp_sum_d(static_cast<double>(sm2) * (f * f)) : 0.0;
   if (lane == 0) {
     red[0][warp] = mw;
     red[1][warp] = sw;
