@@ -383,3 +383,19 @@ def test_assoc_sample_small_pool(pool):
                         "-m", "gpu"], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert "passed" in r.stdout
+
+
+def test_plain_launches_without_pdl():
+    """GLMB_PDL=0 (plain launches, no programmatic serialization): the sampler, update-chain
+    and tracker parity tests pass unchanged (child process: the knob is read once)."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, GLMB_PDL="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_hyp.py"), os.path.join(here, "test_gpu_tracker.py"),
+                        "-k", "assoc_sample_vs_oracle or hypothesis_update_chain or one_call or convoy",
+                        "-m", "gpu"], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "passed" in r.stdout
