@@ -12,6 +12,7 @@
 // prefix sums, the ESS decision and the ancestors are exact integers: the same
 // on any hardware and in any summation order.
 #include <algorithm>
+#include <cstdlib>
 
 #include "glmb_device.cuh"
 #include "glmb_internal.h"
@@ -509,7 +510,7 @@ __device__ __forceinline__ void resample_unit(const ResampleArgs &a, const int k
 // Grid-stride over the device count of pairs (the grid is capped near the resident
 // CTA count: a capacity-sized grid of mostly empty 1024-thread CTAs cost ~0.1 ms).
 template <int kResThreads>
-__global__ void __launch_bounds__(kResThreads) resample_kernel(ResampleArgs a) {
+__global__ void __launch_bounds__(kResThreads, kResThreads == 512 ? 2 : (kResThreads == 256 ? 4 : 1)) resample_kernel(ResampleArgs a) {
   grid_dep_wait();
   const int n = a.n_units_dev != nullptr ? min(a.K, __ldg(a.n_units_dev)) : a.K;
   for (int k = blockIdx.x; k < n; k += gridDim.x) {
@@ -642,15 +643,24 @@ cudaError_t launch_resample(const ResampleArgs &a, int sm_count, cudaStream_t s)
   const int per_sm = a.P <= 2048 ? std::max(1, std::min(8, static_cast<int>((200 * 1024) / (smem + 1024))))
                                  : std::max(1, std::min(2, static_cast<int>((200 * 1024) / (smem + 1024))));
   const int grid = std::min(a.K, 2 * sms * per_sm);
+  // threads per pair above P = 2048: 512 (two CTAs per SM under the 64-register budget;
+  // a 1024-thread CTA held a whole SM's register file) unless GLMB_RESAMPLE_NT=1024
+  static const int res_nt = [] {
+    const char *e = std::getenv("GLMB_RESAMPLE_NT");
+    return e && std::atoi(e) == 1024 ? 1024 : 512;
+  }();
   if (smem > 40 * 1024) {
     cudaError_t e = a.P <= 2048 ? cudaFuncSetAttribute(resample_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       static_cast<int>(smem))
+                    : res_nt == 512 ? cudaFuncSetAttribute(resample_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                        static_cast<int>(smem))
                                 : cudaFuncSetAttribute(resample_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                        static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  cudaError_t e2 = a.P <= 2048 ? launch_pdl(resample_kernel<256>, dim3(grid), dim3(256), smem, s, a)
-                                : launch_pdl(resample_kernel<1024>, dim3(grid), dim3(1024), smem, s, a);
+  cudaError_t e2 = a.P <= 2048  ? launch_pdl(resample_kernel<256>, dim3(grid), dim3(256), smem, s, a)
+                   : res_nt == 512 ? launch_pdl(resample_kernel<512>, dim3(grid), dim3(512), smem, s, a)
+                                   : launch_pdl(resample_kernel<1024>, dim3(grid), dim3(1024), smem, s, a);
   if (e2 != cudaSuccess) return e2;
   return cudaGetLastError();
 }
