@@ -559,10 +559,22 @@ glmb_status glmb_map_estimate(const int32_t *n_kept, const int32_t *pair_of0, in
 glmb_status glmb_update(const glmb_update_params *u, glmb_stream_t stream) {
   if (u == nullptr) return GLMB_ERR_INVALID_ARG;
   const int64_t n = static_cast<int64_t>(u->H_old) * u->H_up;
-  GLMB_TRY(glmb_death_prob(u->T, u->M, u->C_tracks, u->ldc, u->gate, u->ldg, u->p_d, u->kappa, u->p_s, u->d_prob,
-                           stream));
-  GLMB_TRY(glmb_compat_rows(u->T, u->M, u->C_tracks, u->ldc, u->gate, u->ldg, u->row_ptr, u->col, u->val, u->ln_val,
-                            u->rows_cap, stream));
+  {  // glmb_death_prob + glmb_compat_rows (same validation), the first two in one grid
+    const int32_t T = u->T, M = u->M;
+    if (T < 0 || M < 0 || u->rows_cap < 0 || u->row_ptr == nullptr) return GLMB_ERR_INVALID_ARG;
+    if (!(u->p_d > 0.f && u->p_d <= 1.f) || !(u->kappa >= 0.f)) return GLMB_ERR_INVALID_ARG;
+    if (T > 0 && (u->d_prob == nullptr || u->p_s == nullptr)) return GLMB_ERR_INVALID_ARG;
+    if (T > 0 && M > 0 && (u->C_tracks == nullptr || u->gate == nullptr || u->ldc < M || u->ldg < (M + 31) / 32))
+      return GLMB_ERR_INVALID_ARG;
+    if (u->rows_cap > 0 && (u->col == nullptr || u->val == nullptr || u->ln_val == nullptr))
+      return GLMB_ERR_INVALID_ARG;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int dev = 0;
+    GLMB_TRY(bind_stream(s, &dev));
+    glmb::DeathArgs d{T, M, u->C_tracks, u->ldc, u->gate, u->ldg, u->p_d, u->kappa, u->p_s, u->d_prob};
+    glmb::RowsArgs r{T, M, u->gate, u->ldg, u->C_tracks, u->ldc, u->row_ptr, u->col, u->val, u->ln_val, u->rows_cap};
+    GLMB_TRY(from_cuda(glmb::launch_death_and_rows(d, r, g_sm_count[dev], s)));
+  }
   GLMB_TRY(glmb_assoc_sample(u->H_old, u->n_parents, u->H_up, u->T, u->M, u->parent_mask, u->ldt, u->parent_logw,
                              u->d_prob, u->p_s, u->p_d, u->kappa, u->row_ptr, u->col, u->val, u->ln_val, u->count_lp,
                              u->n_count, u->seed, u->step, u->alive, u->theta, u->ldm, u->logw, u->hash, stream));

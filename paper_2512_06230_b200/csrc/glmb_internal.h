@@ -185,6 +185,8 @@ cudaError_t launch_clutter_fill(float *C_clutter, int32_t M, float kappa, cudaSt
 cudaError_t launch_reweight(const ReweightArgs &a, cudaStream_t s);
 cudaError_t launch_death_prob(const DeathArgs &a, cudaStream_t s);
 cudaError_t launch_compat_rows(const RowsArgs &a, int sm_count, cudaStream_t s);
+// glmb_update: death_prob and the CSR row counts in one grid, then the scan and the fill
+cudaError_t launch_death_and_rows(const DeathArgs &d, const RowsArgs &a, int sm_count, cudaStream_t s);
 cudaError_t launch_assoc_sample(const SampleArgs &a, int sm_count, cudaStream_t s);
 cudaError_t launch_dedup(const DedupArgs &a, cudaStream_t s);
 int32_t prune_capacity(int32_t h_max);

@@ -26,10 +26,7 @@ constexpr uint32_t kDomainSurvive = 2u, kDomainAssoc = 3u;
 // One warp per track column: e_j = max over gated i of r_i = C[i, j+1] / (C[i, j+1] + kappa),
 // then d_j = (1 - P_S) / ((1 - P_S) + P_S ((1 - P_D) + P_D e_j)).  fp64 with explicitly
 // rounded operations (no FMA contraction): IEEE-exact steps, so d_j is reproducible.
-__global__ void __launch_bounds__(256) death_prob_kernel(DeathArgs a) {
-  grid_dep_wait();
-  const int32_t j = blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
+__device__ __forceinline__ void death_prob_warp(const DeathArgs &a, const int32_t j, const int lane) {
   if (j >= a.T) return;
   const float *col = a.C_tracks + static_cast<int64_t>(j) * a.ldc;
   const uint32_t *g = a.gate + static_cast<int64_t>(j) * a.ldg;
@@ -60,6 +57,11 @@ __global__ void __launch_bounds__(256) death_prob_kernel(DeathArgs a) {
   }
 }
 
+__global__ void __launch_bounds__(256) death_prob_kernel(DeathArgs a) {
+  grid_dep_wait();
+  death_prob_warp(a, blockIdx.x * 8 + (threadIdx.x >> 5), threadIdx.x & 31);
+}
+
 // ------------------------------------------------------------------ CSR of the gated entries
 // CTA (w, c) = 32 consecutive rows (gate word column w) x the c-th of gridDim.y track
 // chunks; warp k owns the contiguous sub-chunk k of it, so entries come out in
@@ -73,19 +75,14 @@ __device__ __forceinline__ void range_part(int32_t lo, int32_t hi, int parts, in
   j1 = min(hi, j0 + ch);
 }
 
-__device__ __forceinline__ void row_chunk(int32_t T, int k, int32_t &j0, int32_t &j1) {
-  int32_t c0, c1;
-  range_part(0, T, gridDim.y, blockIdx.y, c0, c1);
-  range_part(c0, c1, kRowWarps, k, j0, j1);
-}
 
 // row totals: each CTA adds its chunk's counts (row_ptr zeroed by the launcher)
-__global__ void __launch_bounds__(kRowWarps * 32) rows_count_kernel(RowsArgs a) {
-  grid_dep_wait();
+__device__ __forceinline__ void rows_count_block(const RowsArgs &a, const int w, const int chunk, const int n_chunks) {
   __shared__ int32_t cnt[kRowWarps][32];
-  const int w = blockIdx.x, lane = threadIdx.x & 31, k = threadIdx.x >> 5;
-  int32_t j0, j1;
-  row_chunk(a.T, k, j0, j1);
+  const int lane = threadIdx.x & 31, k = threadIdx.x >> 5;
+  int32_t c0, c1, j0, j1;
+  range_part(0, a.T, n_chunks, chunk, c0, c1);
+  range_part(c0, c1, kRowWarps, k, j0, j1);
   int32_t c = 0;
   for (int32_t j = j0; j < j1; ++j) c += (__ldg(a.gate + static_cast<int64_t>(j) * a.ldg + w) >> lane) & 1u;
   cnt[k][lane] = c;
@@ -96,10 +93,29 @@ __global__ void __launch_bounds__(kRowWarps * 32) rows_count_kernel(RowsArgs a) 
     for (int q = 0; q < kRowWarps; ++q) s += cnt[q][lane];
     const int32_t i = w * 32 + lane;
     if (i < a.M) {
-      if (gridDim.y == 1) a.row_ptr[i] = s;
+      if (n_chunks == 1) a.row_ptr[i] = s;
       else if (s) atomicAdd(a.row_ptr + i, s);
     }
   }
+}
+
+__global__ void __launch_bounds__(kRowWarps * 32) rows_count_kernel(RowsArgs a) {
+  grid_dep_wait();
+  rows_count_block(a, blockIdx.x, blockIdx.y, gridDim.y);
+}
+
+// glmb_update's first launch: death probabilities (a warp per column, the first
+// n_death_blocks CTAs) and the CSR row counts (the rest) read the same C_k and gate words
+// and write disjoint outputs, so one grid does both
+__global__ void __launch_bounds__(kRowWarps * 32) death_and_count_kernel(DeathArgs d, RowsArgs r, int n_death_blocks,
+                                                                         int words, int n_chunks) {
+  grid_dep_wait();
+  if (static_cast<int>(blockIdx.x) < n_death_blocks) {
+    death_prob_warp(d, static_cast<int32_t>(blockIdx.x) * kRowWarps + (threadIdx.x >> 5), threadIdx.x & 31);
+    return;
+  }
+  const int b = static_cast<int>(blockIdx.x) - n_death_blocks;
+  rows_count_block(r, b % words, b / words, n_chunks);
 }
 
 // exclusive scan of row_ptr[0..M) in place, row_ptr[M] = total (one CTA)
@@ -936,6 +952,28 @@ __global__ void __launch_bounds__(kPruneThreads) prune_kernel(PruneArgs a) {
 cudaError_t launch_death_prob(const DeathArgs &a, cudaStream_t s) {
   cudaError_t e0 = launch_pdl(death_prob_kernel, dim3((a.T + 7) / 8), dim3(256), 0, s, a);
   if (e0 != cudaSuccess) return e0;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_death_and_rows(const DeathArgs &d, const RowsArgs &a, int sm_count, cudaStream_t s) {
+  const int32_t words = (a.M + 31) / 32;
+  const int sms = sm_count > 0 ? sm_count : 148;
+  const int32_t chunks = std::max<int32_t>(1, std::min<int32_t>((sms + words - 1) / std::max<int32_t>(words, 1),
+                                                                (a.T + 63) / 64));
+  if (a.M > 0 && (chunks > 1 || a.T == 0)) {
+    cudaError_t e = cudaMemsetAsync(a.row_ptr, 0, sizeof(int32_t) * a.M, s);
+    if (e != cudaSuccess) return e;
+  }
+  const int n_death = (d.T + kRowWarps - 1) / kRowWarps;
+  const int n_count = (a.T > 0 && words > 0) ? words * chunks : 0;
+  cudaError_t e = cudaSuccess;
+  if (n_death + n_count > 0)
+    e = launch_pdl(death_and_count_kernel, dim3(n_death + n_count), dim3(kRowWarps * 32), 0, s, d, a, n_death,
+                   std::max<int32_t>(words, 1), chunks);
+  if (e == cudaSuccess) e = launch_pdl(rows_scan_kernel, dim3(1), dim3(1024), 0, s, a.row_ptr, a.M);
+  if (e == cudaSuccess && n_count > 0)
+    e = launch_pdl(rows_fill_kernel, dim3(words, chunks), dim3(kRowWarps * 32), 0, s, a);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
