@@ -549,13 +549,14 @@ glmb_status glmb_map_estimate(const int32_t *n_kept, const int32_t *pair_of0,
 
 /* ---------------------------------------------------------------------
  * glmb_update -- the whole update after C_k in one call: the
- * calls glmb_death_prob -> glmb_compat_rows -> glmb_assoc_sample ->
+ * work of glmb_death_prob -> glmb_compat_rows -> glmb_assoc_sample ->
  * glmb_dedup -> glmb_prune -> glmb_assoc_pairs -> glmb_reweight_pairs ->
  * glmb_resample (-> glmb_map_estimate when est != NULL), enqueued in that
  * order on `stream` with the counts passed between them on the device (no
- * host round trip).  Each field has the meaning, layout and requirements of
- * the same argument of those calls; the first failing call's status is
- * returned (earlier calls stay enqueued).
+ * host round trip); the death probabilities and the CSR row counts share one
+ * grid (identical outputs).  Each field has the meaning, layout and
+ * requirements of the same argument of those calls; the first failing call's
+ * status is returned (earlier calls stay enqueued).
  * --------------------------------------------------------------------- */
 typedef struct {
   /* sizes and model */
