@@ -78,7 +78,9 @@ class ConvoyTracker:
             b.data.zero_()
         self.cur = 0
         self.gid = torch.arange(rows, dtype=torch.int32, device=dev)
-        self.p_s = torch.empty(rows, dtype=torch.float32, device=dev)
+        # survival prior per column: P_S everywhere; each update sets its birth columns to r_b
+        # and restores them after its kernels (enqueued before the host waits)
+        self.p_s = torch.full((rows,), cfg.p_s, dtype=torch.float32, device=dev)
         self.ldc = max(32, (M_max + 31) // 32 * 32)
         self.ldg = max(1, (M_max + 31) // 32)
         self.C_clutter = torch.empty(max(M_max, 1), dtype=torch.float32, device=dev)
@@ -152,7 +154,6 @@ class ConvoyTracker:
             e0.record(s)
             self.Z[:M].copy_(self.Z_host[:M], non_blocking=True)
             Zk = self.Z[:M]
-            self.p_s[:T].fill_(cfg.p_s)
             self.p_s[T:Tk].fill_(cfg.r_birth)
             mark("start")
             if T:
@@ -178,6 +179,7 @@ class ConvoyTracker:
                 _lib.glmb_update(self._update_params(trk, Tk, M, k), s)
             self.counts_host.copy_(self.counts, non_blocking=True)   # (n_pairs, n_kept, n_parents)
             e1.record(s)
+            self.p_s[T:Tk].fill_(cfg.p_s)   # these columns are survivors' rows next update
             # kept hypotheses -> parents over the new rows [0, K) and the next births at
             # [K, K + B), K read on the device (enqueued before the host waits for K)
             _lib.glmb_next_parents(hu.n_kept, hu.keep_w, po, self.K_cap, B, 0,
