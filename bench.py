@@ -430,6 +430,20 @@ def bench_update(a, st, scene, cfg, dev, stream, L):
             stage[n].append(prev.elapsed_time(evs[n]))
             prev = evs[n]
         total.append(evs["start"].elapsed_time(evs["resample"]))
+    # the same chain as one glmb_update call (the tracker's path: one argument block, the
+    # death probabilities and row counts in one grid), timed end to end with two events
+    from paper_2512_06230_b200.hyp import update_params
+    one = []
+    for k in range(a.warmup, a.warmup + a.steps):
+        prm = update_params(hu, pu, st.particles, st.out.C_tracks, st.out.gate, M, Z, st.R, ps_d, pm_d, plw_d,
+                            cfg.p_d, cfg.kappa, 1e-5, cfg.seed, k, out=pu.out)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        L.glmb_update(prm, stream)
+        e1.record(stream)
+        one.append((e0, e1))
+    torch.cuda.synchronize(dev)
+    one_ms = statistics.mean(x.elapsed_time(y) for x, y in one)
     n_kept = int(hu.n_kept.item())
     n_pairs = pu.n_pairs_checked()
     rp = hu.row_ptr[:M + 1].cpu().numpy()
@@ -451,7 +465,7 @@ def bench_update(a, st, scene, cfg, dev, stream, L):
               "resample": hbm_stage("resample", P * (4 * n_pairs + 44 * n_res + 48 * (n_pairs - n_res)))}
     return {"workload": f"cfg{a.config if a.config is not None else 3} C_k (T_k={T}, M={M}) + particles; "
                         f"H_old={a.h_old} x H_up={a.h_up}, tau=1e-5, H_max={a.h_max} (P:186)",
-            "ms": statistics.mean(total), "stages_ms": stage_mean, "hbm_kernels": hbm_f2,
+            "ms": statistics.mean(total), "one_call_ms": one_ms, "stages_ms": stage_mean, "hbm_kernels": hbm_f2,
             "n_samples": a.h_old * a.h_up, "n_unique": int(hu.unique.sum().item()), "n_kept": n_kept,
             "n_pairs": n_pairs, "n_resampled": n_res,
             "gated_entries": int(rp[-1]), "row_len_max": int(row_len.max()) if M else 0,
