@@ -664,7 +664,7 @@ __device__ __forceinline__ void reweight_flat_unit(const ReweightArgs &a, const 
 }
 
 template <bool LC>
-__global__ void __launch_bounds__(kThreads, 4) reweight_flat_kernel(const ReweightArgs a) {
+__global__ void __launch_bounds__(kThreads, 3) reweight_flat_kernel(const ReweightArgs a) {
   grid_dep_wait();
   const int n_units = a.n_units_dev != nullptr ? min(a.T, __ldg(a.n_units_dev)) : a.T;
   for (int u = blockIdx.x; u < n_units; u += gridDim.x) reweight_flat_unit<LC>(a, u);
