@@ -510,7 +510,7 @@ __device__ __forceinline__ void resample_unit(const ResampleArgs &a, const int k
 // Grid-stride over the device count of pairs (the grid is capped near the resident
 // CTA count: a capacity-sized grid of mostly empty 1024-thread CTAs cost ~0.1 ms).
 template <int kResThreads>
-__global__ void __launch_bounds__(kResThreads, kResThreads == 512 ? 2 : (kResThreads == 256 ? 4 : 1)) resample_kernel(ResampleArgs a) {
+__global__ void __launch_bounds__(kResThreads, kResThreads == 512 ? 3 : (kResThreads == 256 ? 4 : 1)) resample_kernel(ResampleArgs a) {
   grid_dep_wait();
   const int n = a.n_units_dev != nullptr ? min(a.K, __ldg(a.n_units_dev)) : a.K;
   for (int k = blockIdx.x; k < n; k += gridDim.x) {
@@ -641,9 +641,9 @@ cudaError_t launch_resample(const ResampleArgs &a, int sm_count, cudaStream_t s)
   // about two waves of resident CTAs (shared memory bounds residency at large P)
   const int sms = sm_count > 0 ? sm_count : 148;
   const int per_sm = a.P <= 2048 ? std::max(1, std::min(8, static_cast<int>((200 * 1024) / (smem + 1024))))
-                                 : std::max(1, std::min(2, static_cast<int>((200 * 1024) / (smem + 1024))));
+                                 : std::max(1, std::min(3, static_cast<int>((200 * 1024) / (smem + 1024))));
   const int grid = std::min(a.K, 2 * sms * per_sm);
-  // threads per pair above P = 2048: 512 (two CTAs per SM under the 64-register budget;
+  // threads per pair above P = 2048: 512 (three CTAs per SM at 40 registers;
   // a 1024-thread CTA held a whole SM's register file) unless GLMB_RESAMPLE_NT=1024
   static const int res_nt = [] {
     const char *e = std::getenv("GLMB_RESAMPLE_NT");
