@@ -221,6 +221,22 @@ def reweight(x, y, w, Z, R, theta, col_offset=0):
     return wo, lz, fl
 
 
+def nearest_gate_theta(ref_compat) -> np.ndarray:
+    """Nearest-gate association map of BASELINE.json configs[2] ("A nearest-gate association map
+    theta is supplied for reweighting each step"), computed from the ORACLE's C_k (a dict returned
+    by ``compat``): theta_i = 1 + argmax_j {C[i, j+1] : g_ij = 1} (ties -> lowest j), 0 when row i
+    has no gated track (the clutter column).  Test/bench harness input (reading R22)."""
+    C = np.asarray(ref_compat["C_tracks"], np.float64)       # [T][M]
+    T, M = C.shape
+    if T == 0 or M == 0:
+        return np.zeros(M, np.int32)
+    g = ((np.asarray(ref_compat["gate"], np.uint32)[:, np.arange(M) // 32]
+          >> (np.arange(M) % 32).astype(np.uint32)) & 1).astype(bool)      # [T][M]
+    Cg = np.where(g, C, -np.inf)
+    j = np.argmax(Cg, axis=0)                                  # first maximiser = lowest j
+    return np.where(g.any(axis=0), j + 1, 0).astype(np.int32)
+
+
 # ----------------------------------------------------------------- O9-O13 (hypothesis machinery)
 def _gate_words(gate, T, M):
     ldg = (M + 31) // 32

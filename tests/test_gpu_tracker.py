@@ -177,3 +177,126 @@ def test_glmb_update_one_call_equals_stages(L, orc):
     a, b = outs
     for x, y in zip(a, b):
         np.testing.assert_array_equal(x, y)
+
+
+def test_convoy_loop_stagewise_vs_oracle_chain(L, orc):
+    """The tracker loop itself against the oracle chain (SURVEY 8(c) protocol 1 applied to f4):
+    a convoy of N = 5 objects for 30 updates through ConvoyTracker.update (one glmb_update call
+    per step, the tracker's real path).  At every step each stage's GPU input buffers are copied
+    to the host and the oracle recomputes that stage from exactly those values: predict (O5),
+    birth (O6), compat (O7), death_prob (O9), compat_rows (O10), assoc_sample (O11), dedup (O12),
+    prune (O13), assoc_pairs (O14), reweight_pairs (O15), resample (O16, on the GPU's weights),
+    map_estimate (O18) and next_parents (O17).  Integer outcomes (gate bits outside the gamma
+    band, survival bits, theta, uniqueness, kept indices, pairs, resampling decisions and
+    ancestors, parent masks) must match bit for bit; weights and estimates within contract."""
+    import torch
+    from _parity import check_compat, check_log_norm, check_state, check_weights
+    from paper_2512_06230_b200.scenes import ConvoyConfig, convoy_scene
+    from paper_2512_06230_b200.tracker import ConvoyTracker, count_log_prior
+    cfg = ConvoyConfig(N=5, K=30, seed=4)
+    Zs, truth, bm, bc = convoy_scene(cfg)
+    M_max = max(len(z) for z in Zs)
+    tr = ConvoyTracker(cfg, M_max, K_cap=512)
+    tr.reset(bm, bc)
+    lc = count_log_prior(cfg, M_max)
+    P, B, H, H_up = cfg.P, cfg.B, cfg.H_max, cfg.H_up
+    seen_multi_parent = seen_resampled = 0
+    for k in range(cfg.K):
+        torch.cuda.synchronize()
+        T = tr.n_surv
+        Tk = T + B
+        src = tr.bufs[tr.cur]
+        pre = src.data[:, :T].cpu().numpy()
+        npar = int(tr.counts[2].item())
+        pm = tr.parent_mask[:npar].cpu().numpy().view(np.uint32)
+        plw = tr.parent_logw[:npar].cpu().numpy()
+        gid = tr.gid[:Tk].cpu().numpy()
+        Z = Zs[k]
+        M = len(Z)
+        rec = tr.update(k, Z)
+        torch.cuda.synchronize()
+        dst = tr.bufs[tr.cur]
+        post = src.data[:, :Tk].cpu().numpy()
+        # a1/a3: predict and birth
+        if T:
+            ref = orc.predict(*pre[:5], gid[:T], cfg.dt, cfg.sigma_a, cfg.sigma_w, cfg.seed, k)
+            check_state([a[:T] for a in post[:5]], ref)
+            np.testing.assert_array_equal(post[5][:T], pre[5])
+        bref = orc.birth(bm, bc, gid[T:Tk], P, cfg.seed, k)
+        check_state([a[T:Tk] for a in post[:5]], bref[:5])
+        # a4/a5: compat
+        C = tr.C_tracks[:Tk, :M].cpu().numpy()
+        G = tr.gate[:Tk, :(M + 31) // 32].cpu().numpy().view(np.uint32)
+        ref_c = orc.compat(post[0], post[1], post[5], Z, cfg.R, cfg.p_d, cfg.kappa, cfg.gamma)
+        check_compat(C, G, tr.C_clutter.cpu().numpy(), ref_c, cfg.gamma, M)
+        # f1: death probabilities, CSR rows, the two-stage sampler, dedup (on the GPU's C_k)
+        ps = np.concatenate([np.full(T, cfg.p_s), np.full(B, cfg.r_birth)]).astype(np.float32)
+        hu, pu = tr.hu, tr.pu
+        d = hu.d[:Tk].cpu().numpy()
+        np.testing.assert_array_equal(d, orc.death_prob(C, G, cfg.p_d, cfg.kappa, ps).astype(np.float32))
+        rp, col, val, lv = orc.compat_rows(C, G, M)
+        nnz = int(rp[M])
+        np.testing.assert_array_equal(hu.row_ptr[:M + 1].cpu().numpy(), rp)
+        np.testing.assert_array_equal(hu.col[:nnz].cpu().numpy(), col)
+        np.testing.assert_array_equal(hu.val[:nnz].cpu().numpy(), val)
+        np.testing.assert_allclose(hu.ln_val[:nnz].cpu().numpy(), lv, rtol=1e-15)
+        n = npar * H_up
+        al, th, lw = orc.assoc_sample(pm, plw, H_up, d, ps, cfg.p_d, cfg.kappa, (rp, col, val, lv), M,
+                                      cfg.seed, k, count_lp=lc)
+        g_al = hu.alive[:n].cpu().numpy().view(np.uint32)
+        g_th = hu.theta[:n, :M].cpu().numpy()
+        g_lw = hu.logw[:n].cpu().numpy()
+        np.testing.assert_array_equal(g_al, al)
+        np.testing.assert_array_equal(g_th, th)
+        np.testing.assert_allclose(g_lw, lw, rtol=1e-9, atol=1e-9)
+        u = hu.unique[:H * H_up].cpu().numpy()
+        np.testing.assert_array_equal(u[:n], orc.dedup(g_al, g_th, npar, H_up))
+        assert not u[n:].any()
+        # f3: normalisation, tau, H_max (on the GPU's log-weights)
+        idx, kw = orc.prune(g_lw, u[:n], cfg.tau, H)
+        nk = rec.n_kept
+        np.testing.assert_array_equal(hu.keep_idx[:nk].cpu().numpy(), idx)
+        g_kw = hu.keep_w[:nk].cpu().numpy()
+        np.testing.assert_allclose(g_kw, kw, rtol=1e-9)
+        # f2: pairs, per-pair update, resampling (on the GPU's kept set and weights)
+        r_pt, r_pp, r_pm, r_po = orc.assoc_pairs(idx, g_al, g_th, Tk, M)
+        K = rec.n_pairs
+        assert K == len(r_pt)
+        np.testing.assert_array_equal(pu.pair_track[:K].cpu().numpy(), r_pt)
+        np.testing.assert_array_equal(pu.pair_ptr[:K + 1].cpu().numpy(), r_pp)
+        np.testing.assert_array_equal(pu.pair_meas[:len(r_pm)].cpu().numpy(), r_pm)
+        po = pu.pair_of.view(-1)[:H * Tk].view(H, Tk)[:nk].cpu().numpy()
+        np.testing.assert_array_equal(po, r_po)
+        r_w, r_lz, r_fl, r_es = orc.reweight_pairs(post[0], post[1], post[5], Z, cfg.R, r_pt, r_pp, r_pm)
+        g_w = pu.w_new[:K].cpu().numpy()
+        fl = pu.flags[:K].cpu().numpy().view(np.uint32)
+        check_weights(g_w, r_w)
+        check_log_norm(pu.log_norm[:K].cpu().numpy(), r_lz)
+        np.testing.assert_array_equal(fl & 1, r_fl)
+        np.testing.assert_allclose(pu.ess[:K].cpu().numpy(), r_es, rtol=1e-4)
+        out = dst.data[:, :K].cpu().numpy()
+        for q in range(K):
+            res, anc = orc.resample(g_w[q], cfg.seed, k, q)
+            assert bool(fl[q] & 2) == res, (k, q)
+            rows = post[:5, r_pt[q]]
+            if res:
+                seen_resampled += 1
+                np.testing.assert_array_equal(out[:5, q], rows[:, anc])
+                assert np.all(out[5, q] == np.float32(1.0 / P))
+            else:
+                np.testing.assert_array_equal(out[:5, q], rows)
+                np.testing.assert_array_equal(out[5, q], g_w[q])
+        # f4: MAP estimate and the next parents
+        est = tr.est[:Tk].cpu().numpy()
+        r_est = orc.map_estimate(nk, po[0], out[0], out[1], out[5])
+        np.testing.assert_array_equal(est[:, 2], r_est[:, 2])
+        ok = r_est[:, 2] > 0
+        np.testing.assert_allclose(est[ok, :2], r_est[ok, :2], rtol=1e-12)
+        r_mask, r_plw = orc.next_parents(g_kw, po, Tk, tr.K_cap, B, K, tr.ldt)
+        np.testing.assert_array_equal(tr.parent_mask[:nk].cpu().numpy().view(np.uint32), r_mask)
+        np.testing.assert_allclose(tr.parent_logw[:nk].cpu().numpy(), r_plw, rtol=1e-15)
+        assert int(tr.counts[2].item()) == nk
+        seen_multi_parent += npar > 1
+    # the run exercised the interesting paths: several parents, resampled pairs, all objects in
+    assert seen_multi_parent > 10 and seen_resampled > 0
+    assert tr.n_surv >= cfg.N

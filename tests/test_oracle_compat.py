@@ -125,3 +125,18 @@ def test_likelihood_integrates_to_one(orc):
     Z = np.stack([gx.ravel(), gy.ravel()], 1).astype(np.float32)
     out = orc.compat(x, y, w, Z, (0.6, 0.2, 0.9), 1.0, 0.0, 1e-30)
     assert out["L"].sum() * h * h == pytest.approx(1.0, abs=1e-6)
+
+
+def test_nearest_gate_theta_hand_example(orc):
+    """BASELINE.json configs[2]'s nearest-gate map from the oracle's C_k (R22), worked by hand:
+    3 tracks at x = 0, 3, 30 (one particle each, R = I, P_D = 1, gamma = 1e-6, gate radius
+    4.894 m).  z0 = (1, 0): tracks 0 (d = 1) and 1 (d = 2) gated, the nearer one wins -> 1;
+    z1 = (1.5, 0): equidistant from tracks 0 and 1, an exact tie -> the lower column, 1;
+    z2 = (30, 4): only track 2 (d = 4) -> 3; z3 = (15, 0): nothing within the gate -> 0."""
+    x, y, w = (np.asarray([[0.0], [3.0], [30.0]], np.float32), np.zeros((3, 1), np.float32),
+               np.ones((3, 1), np.float32))
+    Z = np.asarray([[1.0, 0.0], [1.5, 0.0], [30.0, 4.0], [15.0, 0.0]], np.float32)
+    ref = orc.compat(x, y, w, Z, (1.0, 0.0, 1.0), 1.0, 1e-4, 1e-6)
+    assert ref["C_tracks"][0, 1] == ref["C_tracks"][1, 1]           # the tie is exact
+    np.testing.assert_array_equal(orc.nearest_gate_theta(ref), [1, 1, 3, 0])
+    assert orc.nearest_gate_theta(orc.compat(x[:0], y[:0], w[:0], Z, (1, 0, 1), 1.0, 1e-4, 1e-6)).tolist() == [0] * 4
