@@ -737,21 +737,21 @@ def main():
         col_d = torch.empty(cap, dtype=torch.int32, device=dev)
         val_d = torch.empty(cap, dtype=torch.float32, device=dev)
         lv_d = torch.empty(cap, dtype=torch.float64, device=dev)
-        cap_h = 4 * M_max                              # host CSR capacity = the speculative first copy
-                                                       # (a second, exact copy if the entries exceed it)
+        first_h = 4 * M_max                            # the speculative first copy (entries); a second,
+                                                       # exact copy if the gated entries exceed it
         rp_h = pin(torch.empty(M_max + 1, dtype=torch.int32))
-        col_h = pin(torch.empty(cap_h, dtype=torch.int32))
-        val_h = pin(torch.empty(cap_h))
+        col_h = pin(torch.empty(cap, dtype=torch.int32))   # host capacity = the device capacity
+        val_h = pin(torch.empty(cap))
 
         def host_step_csr(k):
             """C_k read back as the CSR of its gated entries (glmb_step_host_csr)."""
             zi = k % len(Zh)
             nnz = L.glmb_step_host_csr(st.step_params(k, out_of_place=True), Zh[zi], thh[zi], Zd, thd,
                                        o.C_tracks, o.gate, o.log_norm, o.flags, rp_d, col_d, val_d, lv_d, rp_h,
-                                       col_h, val_h, ln_h, fl_h, stream, aux_stream=copy_stream)
+                                       col_h, val_h, ln_h, fl_h, stream, aux_stream=copy_stream, first_copy=first_h)
             st.swap_weights()
             M = Zh[zi].shape[0]
-            first = min(cap_h, cap)                    # entries copied speculatively, then the rest
+            first = min(first_h, cap)                  # entries copied speculatively, then the rest
             return M * 12, (M + 1) * 4 + max(first, nnz) * 8 + st.T_local * 8
 
         def host_step_dense(k):

@@ -276,9 +276,11 @@ glmb_status glmb_step_host(const glmb_step_params *prm, const float *Z_host,
  * glmb_compat_rows defines them; C[i][0] = kappa and every other entry is 0)
  * -- plus log_norm and flags.  C_k is ~0.1 % dense at the BASELINE scenes, so
  * this moves kilobytes over PCIe instead of T_k x ldc floats.  cap: device
- * capacity of col/val/ln_val; cap_host: host capacity of col_host/val_host.
- * The first min(cap, cap_host) entries come back with row_ptr; more (when
- * nnz exceeds it) in a second exact-size copy.  With prm->w_out set and an
+ * capacity of col/val/ln_val; cap_host: host capacity of col_host/val_host;
+ * first_host: how many entries to copy speculatively with row_ptr (before nnz
+ * is known on the host).  The first min(first_host, cap_host, cap) entries come
+ * back with row_ptr; the rest (when nnz exceeds that) in a second exact-size
+ * copy after one synchronisation.  With prm->w_out set and an
  * aux_stream (and a non-NULL stream), reweight runs on aux_stream beside
  * compat (out of place: the caller swaps weight buffers afterwards); else the
  * four calls run in order on `stream`.  Errors: INVALID_ARG when nnz exceeds
@@ -293,8 +295,9 @@ glmb_status glmb_step_host_csr(const glmb_step_params *prm, const float *Z_host,
                                float *val_dev, double *ln_val_dev, int32_t cap,
                                int32_t *row_ptr_host, int32_t *col_host,
                                float *val_host, int32_t cap_host,
-                               float *log_norm_host, uint32_t *flags_host,
-                               glmb_stream_t stream, glmb_stream_t aux_stream);
+                               int32_t first_host, float *log_norm_host,
+                               uint32_t *flags_host, glmb_stream_t stream,
+                               glmb_stream_t aux_stream);
 
 /* =====================================================================
  * Hypothesis machinery: the consumers of C_k.
@@ -538,8 +541,9 @@ glmb_status glmb_next_parents(int32_t n_hyp_cap, const int32_t *n_kept,
                               glmb_stream_t stream);
 
 /* glmb_map_estimate -- the state estimate of the most likely hypothesis
- * (R34): for every old track j < T with k = pair_of0[j] >= 0 (row 0 of
- * glmb_assoc_pairs' pair_of, i.e. the best kept hypothesis) and *n_kept > 0,
+ * (R34): for every old track j < T with 0 <= k = pair_of0[j] < set->n_tracks
+ * (row 0 of glmb_assoc_pairs' pair_of, i.e. the best kept hypothesis; a pair
+ * past the set's rows -- a K_cap overflow -- counts as none) and *n_kept > 0,
  * est[j] = (sum_p w_p x_p / sum_p w_p, ... y ..., 1) over row k of `set` (the
  * new particle set); otherwise est[j] = (NaN, NaN, 0).  est: [T][3] fp64,
  * sums in fp64.  Errors: INVALID_ARG on NULL pointers / bad particle set. */

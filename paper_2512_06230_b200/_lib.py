@@ -102,7 +102,7 @@ def load(path: str = LIB_PATH):
         L.glmb_map_estimate.argtypes = [vp, vp, i32, PP, vp, vp]
         L.glmb_update.argtypes = [C.POINTER(glmb_update_params), vp]
         L.glmb_step_host_csr.argtypes = [SP, vp, i32, vp, vp, vp, vp, i64, vp, i64, vp, vp, vp, vp, vp, vp,
-                                         i32, vp, vp, vp, i32, vp, vp, vp, vp]
+                                         i32, vp, vp, vp, i32, i32, vp, vp, vp, vp]
         L.glmb_compat_peers.argtypes = [PP, vp, i32, f32, f32, f32, f32, f32, f32, vp, vp, vp, i32, i64, i64,
                                         i64, vp]
         L.glmb_prune.argtypes = [i32, vp, vp, C.c_double, i32, vp, vp, vp, vp, vp]
@@ -381,15 +381,17 @@ def glmb_compat_peers(trk: Particles, Z, R, p_d, kappa, gamma, C_clutter, peer_C
 
 def glmb_step_host_csr(prm: glmb_step_params, Z_host, theta_host, Z_dev, theta_dev, C_tracks, gate, log_norm,
                        flags, row_ptr, col, val, ln_val, row_ptr_host, col_host, val_host, log_norm_host,
-                       flags_host, stream=None, aux_stream=None):
+                       flags_host, stream=None, aux_stream=None, first_copy=None):
     """End-to-end step with C_k read back as the CSR of its gated entries (include/glmb.h).
-    Host tensors pinned; returns nnz.  aux_stream (with prm.w_out set): reweight beside compat."""
+    Host tensors pinned; returns nnz.  aux_stream (with prm.w_out set): reweight beside compat.
+    first_copy: entries copied speculatively with row_ptr (default: the host capacity); more,
+    up to the host capacity, in a second exact copy."""
     hp = lambda t: None if t is None else t.data_ptr()
     M = Z_host.shape[0]
     _check(load().glmb_step_host_csr(C.byref(prm), hp(Z_host), M, hp(theta_host), _ptr(Z_dev), _ptr(theta_dev),
                                      _ptr(C_tracks), C_tracks.shape[1], _ptr(gate), gate.shape[1], _ptr(log_norm),
                                      _ptr(flags), _ptr(row_ptr), _ptr(col), _ptr(val), _ptr(ln_val), col.shape[0],
                                      hp(row_ptr_host), hp(col_host), hp(val_host), col_host.shape[0],
-                                     hp(log_norm_host), hp(flags_host), _stream(stream),
+                                     col_host.shape[0] if first_copy is None else int(first_copy), hp(log_norm_host), hp(flags_host), _stream(stream),
                                      None if aux_stream is None else aux_stream.cuda_stream))
     return int(row_ptr_host[M])

@@ -552,7 +552,7 @@ glmb_status glmb_map_estimate(const int32_t *n_kept, const int32_t *pair_of0, in
   if (pair_of0 == nullptr || est == nullptr || set->n_tracks == 0) return GLMB_ERR_INVALID_ARG;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   GLMB_TRY(bind_stream(s, nullptr));
-  glmb::MapEstimateArgs a{n_kept, pair_of0, T, set->n_particles, set->ld, set->x, set->y, set->w, est};
+  glmb::MapEstimateArgs a{n_kept, pair_of0, T, set->n_particles, set->n_tracks, set->ld, set->x, set->y, set->w, est};
   return from_cuda(glmb::launch_map_estimate(a, s));
 }
 
@@ -600,9 +600,9 @@ glmb_status glmb_step_host_csr(const glmb_step_params *prm, const float *Z_host,
                                int64_t ldc, uint32_t *gate_dev, int64_t ldg, float *log_norm_dev, uint32_t *flags_dev,
                                int32_t *row_ptr_dev, int32_t *col_dev, float *val_dev, double *ln_val_dev,
                                int32_t cap, int32_t *row_ptr_host, int32_t *col_host, float *val_host,
-                               int32_t cap_host, float *log_norm_host, uint32_t *flags_host, glmb_stream_t stream,
-                               glmb_stream_t aux_stream) {
-  if (prm == nullptr || M < 0 || cap < 0 || cap_host < 0) return GLMB_ERR_INVALID_ARG;
+                               int32_t cap_host, int32_t first_host, float *log_norm_host, uint32_t *flags_host,
+                               glmb_stream_t stream, glmb_stream_t aux_stream) {
+  if (prm == nullptr || M < 0 || cap < 0 || cap_host < 0 || first_host < 0) return GLMB_ERR_INVALID_ARG;
   if (M > 0 && (Z_host == nullptr || theta_host == nullptr || Z_dev == nullptr || theta_dev == nullptr))
     return GLMB_ERR_INVALID_ARG;
   if (row_ptr_dev == nullptr || row_ptr_host == nullptr) return GLMB_ERR_INVALID_ARG;
@@ -653,9 +653,9 @@ glmb_status glmb_step_host_csr(const glmb_step_params *prm, const float *Z_host,
   }
   GLMB_TRY(glmb_compat_rows(Tk, M, C_tracks_dev, ldc, gate_dev, ldg, row_ptr_dev, col_dev, val_dev, ln_val_dev, cap,
                             stream));
-  // one read-back: row_ptr, the first cap_host entries, log_norm, flags; the rest only if
-  // the gated entries outnumber cap_host (then a second, exact-size copy)
-  const int32_t first = std::min(cap_host, cap);
+  // one read-back: row_ptr, the first first_host entries (speculative), log_norm, flags; the
+  // rest only if the gated entries outnumber them (then a second, exact-size copy, up to cap_host)
+  const int32_t first = std::min(std::min(first_host, cap_host), cap);
   if (cudaMemcpyAsync(row_ptr_host, row_ptr_dev, sizeof(int32_t) * (M + 1), cudaMemcpyDeviceToHost, s) != cudaSuccess)
     return GLMB_ERR_CUDA;
   if (first > 0 &&

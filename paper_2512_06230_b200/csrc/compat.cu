@@ -15,7 +15,7 @@
 //    is bit-identical for any sharding of the tracks and any permutation of
 //    Z's rows.  Warps past M skip the arithmetic; the ragged last measurement
 //    tiles are scheduled last (unit = mt*T + j) to fill the tail.  K = 2 and
-//    40 registers give 16 resident CTAs (64 warps) per SM.
+//    40 registers give 12 resident CTAs (48 warps) per SM.
 //  * The track's particles stream through shared memory in tiles of kTileP,
 //    moved by the TMA bulk-copy engine (cp.async.bulk + mbarrier) and reused
 //    by all 128*K measurements of the CTA; one tile of arithmetic (~50 us per
@@ -30,10 +30,10 @@
 //    packed in pairs (fp32x2), the particle's values are scalar operands that
 //    FFMA2 broadcasts: dx, dy = z' - p' exactly as in the definition (no
 //    |z|^2 - 2z.p + |p|^2 expansion, whose cancellation grows with the cloud
-//    width), q = dx^2 + dy^2, acc += w 2^-q.  One particle in 12 evaluates its
-//    exps on the FMA pipe instead of MUFU (round-to-nearest range reduction
-//    with the 1.5*2^23 trick, degree-5 minimax polynomial, rel. error 2.4e-7
-//    ~ MUFU's, exponent added with an integer shift-add, scaled by 2^64 so
+//    width), q = dx^2 + dy^2, acc += w 2^-q.  One particle in 10 (default;
+//    GLMB_COMPAT_EMU) evaluates its exps on the FMA pipe instead of MUFU
+//    (round-to-nearest range reduction with the 1.5*2^23 trick, degree-4
+//    near-minimax polynomial, rel. error 2.7e-6, exponent added with an integer shift-add, scaled by 2^64 so
 //    tiny results flush to zero like MUFU.EX2.FTZ), which offloads the MUFU
 //    pipe.  The choice is by particle index, so
 //    every measurement sees the same arithmetic (row-permutation bit-exact).
@@ -63,7 +63,7 @@ constexpr int kSmemBytes = kStages * kRawFloats * 4 + 2 * kTileP * 16;  // raw r
 
 // degree-4 near-minimax fit of 2^f on [-1/2, 1/2] (max rel. error 2.6e-6, 2.7e-6 in fp32
 // Horner): one FFMA2 fewer than degree 5 on the FMA pipe; the polynomial covers 1 particle in
-// 12, so C's relative error from it is <= 2.7e-6 (the contract is 1e-4)
+// 10, so C's relative error from it is <= 2.7e-6 (the contract is 1e-4)
 constexpr float kC0 = 0.999999261416315f, kC1 = 0.6931218155360352f, kC2 = 0.24024745060218355f,
                 kC3 = 0.05591785367459349f, kC4 = 0.009570086922274257f;
 constexpr float kRound64 = 12582976.0f;  // 1.5 * 2^23 + 64: x + kRound64 = round(x) + 64 in the low bits

@@ -241,6 +241,7 @@ cudaError_t launch_next_parents(const NextParentsArgs &a, cudaStream_t s);
 struct MapEstimateArgs {
   const int32_t *n_kept, *pair_of0;
   int32_t T, P;
+  int32_t n_rows;  // rows of the particle set: a pair index k >= n_rows is treated like k < 0
   int64_t ld;
   const float *x, *y, *w;
   double *est;  // [T][3]

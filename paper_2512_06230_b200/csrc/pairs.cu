@@ -326,7 +326,8 @@ __global__ void __launch_bounds__(256) finish_kernel(PairsArgs a) {
 // word 0 -- found particle-parallel (range starts marked, then a prefix max; see
 // below).  Ancestors are non-decreasing in n, so the gathers of consecutive slots
 // hit neighbouring addresses.  NT threads per pair: 256 for P <= 2048 (short CTAs),
-// 1024 above (more gathers in flight).
+// 512 above, three CTAs per SM at 40 registers (a 1024-thread CTA at 64 registers held a
+// whole SM's register file).
 // nf(c) = min{n >= 0 : n S + V >= c P}, capped at P; exact (fp64 estimate, integer
 // fix-up; c P, n S <= 2^55 for S <= P 2^26, P <= 2^14)
 __device__ __forceinline__ int res_first_slot(unsigned long long c, unsigned long long P, unsigned long long V,
@@ -554,7 +555,7 @@ __global__ void __launch_bounds__(256) map_estimate_kernel(MapEstimateArgs a) {
   const int32_t j = blockIdx.x;
   const int32_t k = __ldg(a.n_kept) > 0 ? __ldg(a.pair_of0 + j) : -1;
   double *e = a.est + 3 * static_cast<int64_t>(j);
-  if (k < 0) {
+  if (k < 0 || k >= a.n_rows) {  // no pair, or a pair past the set's rows (K_cap overflow)
     if (threadIdx.x == 0) {
       e[0] = __longlong_as_double(0x7ff8000000000000ll);
       e[1] = e[0];

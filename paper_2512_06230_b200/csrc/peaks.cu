@@ -157,7 +157,7 @@ void run_mix(int sms, float *out, long long *cyc) {
 }
 
 template <typename F>
-void run(const char *name, F kern, int sms, float *out, long long *cyc, bool last) {
+void run(const char *name, F kern, int sms, int clk_khz, float *out, long long *cyc, bool last) {
   const int threads = 256, blocks_per_sm = 8, iters = 4096;
   const int blocks = sms * blocks_per_sm;
   kern<<<blocks, threads>>>(out, 16, 1.0f, cyc);  // warm up
@@ -170,13 +170,12 @@ void run(const char *name, F kern, int sms, float *out, long long *cyc, bool las
   cudaEventSynchronize(e1);
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
-  long long c = 0;
-  cudaMemcpy(&c, cyc, sizeof(c), cudaMemcpyDeviceToHost);
   const double ops = double(blocks) * threads * iters * kChains;  // thread-level instructions
-  const double per_sm_per_clk = ops / sms / double(c) * ((double)blocks_per_sm / blocks_per_sm);
-  // one block's clock64 span ~ the whole kernel when all blocks are co-resident
-  printf("  \"%s\": {\"ops_per_s\": %.6e, \"ms\": %.4f, \"block_cycles\": %lld, \"lanes_per_clk_per_sm\": %.3f}%s\n",
-         name, ops / (ms * 1e-3), ms, c, per_sm_per_clk, last ? "" : ",");
+  const double per_s = ops / (ms * 1e-3);
+  // thread-level instructions per clock per SM at the attribute (max) clock: an FFMA2 is one
+  // instruction doing two FP32 lanes, MUFU.EX2 / FFMA one
+  printf("  \"%s\": {\"ops_per_s\": %.6e, \"ms\": %.4f, \"thread_instr_per_clk_per_sm\": %.3f}%s\n", name, per_s,
+         ms, per_s / sms / (clk_khz * 1e3), last ? "" : ",");
 }
 
 int main() {
@@ -196,9 +195,9 @@ int main() {
   run_mix<8, 12>(sms, out, cyc);
   run_mix<8, 16>(sms, out, cyc);
   run_mix<4, 16>(sms, out, cyc);
-  run("mufu_ex2", ex2_kernel, sms, out, cyc, false);
-  run("ffma2_f32x2", ffma2_kernel, sms, out, cyc, false);
-  run("ffma", ffma_kernel, sms, out, cyc, true);
+  run("mufu_ex2", ex2_kernel, sms, clk_khz, out, cyc, false);
+  run("ffma2_f32x2", ffma2_kernel, sms, clk_khz, out, cyc, false);
+  run("ffma", ffma_kernel, sms, clk_khz, out, cyc, true);
   printf("}\n");
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }

@@ -109,6 +109,9 @@ class ConvoyTracker:
         self._ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
         self._prm = [None, None]   # cached glmb_update argument blocks, one per particle buffer
         self.est_host = torch.zeros(rows, 3, dtype=torch.float64).pin_memory()
+        # every buffer above was filled on the current stream; the tracker's kernels run on
+        # self.stream (a non-blocking pool stream), so order it after those fills explicitly
+        self.stream.wait_stream(torch.cuda.current_stream(dev))
 
     def reset(self, birth_mean: np.ndarray, birth_chol: np.ndarray):
         """Empty track set; one parent (the empty hypothesis, weight 1) over the birth columns."""

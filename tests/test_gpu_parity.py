@@ -583,8 +583,11 @@ def test_step_host_csr_matches_dense(L, orc):
                              b.out.flags, rp, col, val, lv, rp_h, col_h, val_h, ln_b, fl_b)
     c = GlmbStep(s)
     col_h, val_h = pin(torch.empty(4096, dtype=torch.int32)), pin(torch.empty(4096))
+    # a speculative first copy of 8 entries: the rest (nnz > 8, within the host capacity) in
+    # the second, exact-size copy
     nnz = L.glmb_step_host_csr(c.step_params(0), Zh, th, Zd, thd, c.out.C_tracks, c.out.gate, c.out.log_norm,
-                               c.out.flags, rp, col, val, lv, rp_h, col_h, val_h, ln_b, fl_b)
+                               c.out.flags, rp, col, val, lv, rp_h, col_h, val_h, ln_b, fl_b, first_copy=8)
+    assert nnz > 8
     C = Ct_h.numpy()[:, :M]
     G = np.unpackbits(G_h.numpy().view(np.uint8), bitorder="little").reshape(a.T_local, -1)[:, :M].astype(bool)
     rows = [np.nonzero(G[:, i])[0] for i in range(M)]

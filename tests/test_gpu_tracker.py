@@ -81,6 +81,12 @@ def test_map_estimate_vs_oracle(L, orc, P):
     assert np.all(np.isnan(got[~ok, :2]))
     L.glmb_map_estimate(_dev(np.array([0], np.int32)), _dev(pair_of0), s, est)
     assert np.all(_host(est)[:, 2] == 0)
+    # a set of 4 rows: pairs 5 (past the rows, a K_cap overflow) count as none
+    L.glmb_map_estimate(_dev(np.array([4], np.int32)), _dev(pair_of0), s.rows(0, 4), est)
+    got4 = _host(est)
+    past = pair_of0 >= 4
+    assert np.all(got4[past, 2] == 0) and np.all(np.isnan(got4[past, :2]))
+    np.testing.assert_array_equal(got4[~past], got[~past])
 
 
 def test_sampler_parent_count(L, orc):
