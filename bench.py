@@ -235,7 +235,8 @@ def compat_traffic(T: int, P: int, M: int):
 
 
 def make_line(*, cfg_id, cfg, world, steps, warmup, elapsed_ms, evals_total, pairs_per_launch,
-              stage_ms, sm_count, clocks, T_surv, B_local, T_local, P, M_mean, traffic, e2e, cpu):
+              stage_ms, sm_count, clocks, T_surv, B_local, T_local, P, M_mean, traffic, e2e, cpu,
+              reweight_launches=1):
     """The one JSON line of the GPU arm (pure function of the measurements)."""
     f_max = (clocks.get("sm_max_mhz") or 1965.0) * 1e6
     peak = sm_count * COMPAT_PAIRS_PER_CLK_PER_SM * f_max
@@ -283,7 +284,7 @@ def make_line(*, cfg_id, cfg, world, steps, warmup, elapsed_ms, evals_total, pai
                         "birth": hbm_kernel("birth", B_local * P * 24),
                         "reweight": hbm_kernel("reweight", T_local * P * 16)},
         "stages_ms": stage_mean,
-        "gpu_launches": ((1 if T_surv else 0) + (1 if B_local else 0) + 2) * steps,
+        "gpu_launches": ((1 if T_surv else 0) + (1 if B_local else 0) + 1 + reweight_launches) * steps,
         "clocks": clocks,
         "e2e": e2e,
         "cpu_baseline": None if cpu is None else
@@ -343,34 +344,33 @@ def skip_probe(cfg_id: int) -> dict:
     return out
 
 
-def verify_fused_gather(st, symm_cols, C_full, G_full, plan, rank, world, dev, stream) -> bool:
+def verify_fused_gather(sh, dev, stream) -> bool:
     """Before timing (N > 1): the fused compat + peer-store gather must give every rank
     exactly the C_k / gate words an NCCL all-gather of glmb_compat's local columns gives
     (bit-identical by construction).  All ranks agree on the outcome (all_reduce MIN)."""
     import torch
     import torch.distributed as dist
     from paper_2512_06230_b200 import _lib as L
-    from paper_2512_06230_b200.dist import allgather_columns
-    Zk = st.Z[0]
-    M = Zk.shape[0]
+    st = sh.st
+    M = sh.load_measurements(0, stream=stream)
     ok = True
     try:
         with torch.cuda.stream(stream):
-            symm_cols.compat(st.particles, Zk, st.R, st.cfg.p_d, st.cfg.kappa, st.cfg.gamma, st.out.C_clutter, stream)
-            symm_cols.barrier(stream)
+            sh._broadcast(M)
+            Zk = sh.Z(M)
+            for k in (0, 1):                  # both symmetric copies
+                sh._compat(st.particles, Zk, k, stream)
+                sh.symm.barrier(k, stream)
             L.glmb_compat(st.particles, Zk, st.R, st.cfg.p_d, st.cfg.kappa, st.cfg.gamma, st.out.C_clutter,
-                          st.out.C_tracks, st.out.gate, stream)
+                          sh.local_C()[:st.T_local], sh.local_gate()[:st.T_local], stream)
         torch.cuda.synchronize(dev)
-        allgather_columns(st.out.C_tracks, C_full)
-        allgather_columns(st.out.gate, G_full)
+        dist.all_gather_into_tensor(sh.gathered, sh.block)
         torch.cuda.synchronize(dev)
         ldg_used = (M + 31) // 32
-        for r in range(world):
-            c = plan.cols(r)
-            n_r = len(c)
-            rows = slice(r * plan.per_rank, r * plan.per_rank + n_r)
-            ok &= bool(torch.equal(symm_cols.C[rows, :M], C_full[rows, :M]))
-            ok &= bool(torch.equal(symm_cols.G[rows, :ldg_used], G_full[rows, :ldg_used]))
+        for k in (0, 1):
+            buf = sh.symm.buffer(k)
+            ok &= bool(torch.equal(buf[:, :M], sh.gathered[:, :M]))
+            ok &= bool(torch.equal(buf[:, sh.ldc:sh.ldc + ldg_used], sh.gathered[:, sh.ldc:sh.ldc + ldg_used]))
     except Exception as e:  # noqa: BLE001
         print(f"[bench] fused gather check raised {e!r}", file=sys.stderr)
         ok = False
@@ -560,7 +560,7 @@ def main():
     from paper_2512_06230_b200 import _lib as L
     from paper_2512_06230_b200.build import build
     from paper_2512_06230_b200.scenes import CONFIGS, make_scene
-    from paper_2512_06230_b200.dist import ShardPlan, allgather_columns, broadcast_measurements
+    from paper_2512_06230_b200.dist import ShardedStep
     from paper_2512_06230_b200.step import GlmbStep
 
     torch.cuda.set_device(local)   # before NCCL init: each rank's communicator binds its own GPU
@@ -573,54 +573,47 @@ def main():
     L.glmb_init(local)
     dev = torch.device("cuda", local)
     cfg = CONFIGS[cfg_id]
-    Tk = cfg.T + cfg.B
-    plan = ShardPlan(Tk, world)
-    cols = plan.cols(rank)
-    per = plan.per_rank
     n_steps_scene = min(cfg.steps, a.warmup + a.steps)
-    scene = make_scene(cfg_id, rows=range(cols.start, min(cols.stop, cfg.T)), steps=n_steps_scene)
-    st = GlmbStep(scene, cols=cols, device=dev, rows_alloc=per)
     stream = torch.cuda.Stream(device=dev)
-    # W>1: Z/theta live on rank 0 and are broadcast inside the timed region;
-    # column blocks of C (+ gate words) are all-gathered into the full matrix.
-    if world > 1:
-        Zbuf = torch.zeros(st.M_max, 2, device=dev)
-        thbuf = torch.zeros(st.M_max, dtype=torch.int32, device=dev)
-        C_full = torch.empty(per * world, st.ldc, device=dev)
-        G_full = torch.empty(per * world, st.ldg, dtype=torch.int32, device=dev)
-    # fused compat + all-gather: compat stores each column into every rank's symmetric-memory
-    # copy of C_k over NVLink, then one device barrier (GLMB_FUSED_GATHER=0: NCCL all-gather)
-    symm_cols = None
+    side = torch.cuda.Stream(device=dev)   # reweight overlaps compat (double-buffered weights)
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    sh = None
     gather = "none (one rank)"
     if world > 1:
-        gather = "NCCL all_gather_into_tensor of the column blocks"
-        if os.environ.get("GLMB_FUSED_GATHER", "1") != "0":
-            try:
-                from paper_2512_06230_b200.symm import SymmetricColumns
-                symm_cols = SymmetricColumns(per, st.ldc, st.ldg, dev)
-                gather = "fused: compat stores its columns into every rank's symmetric-memory C_k (NVLink), device barrier"
-            except Exception as e:  # noqa: BLE001
-                print(f"[bench] symmetric memory unavailable ({e}); NCCL all-gather", file=sys.stderr)
-
-    ev = lambda: torch.cuda.Event(enable_timing=True)
+        # W > 1 (dist.ShardedStep): Z_k / theta_k live on rank 0 and are broadcast inside the
+        # timed region (one packed collective); survivors and births split evenly over the
+        # ranks; C_k's column blocks + gate words all-gathered (one collective) with the
+        # log-normalisers and flags -- or, fused, stored by compat into every rank's
+        # symmetric-memory copy over NVLink (GLMB_FUSED_GATHER=0: NCCL all-gather)
+        fused = os.environ.get("GLMB_FUSED_GATHER", "1") != "0"
+        try:
+            sh = ShardedStep(cfg_id, device=dev, steps=n_steps_scene, fused=fused)
+        except Exception as e:  # noqa: BLE001
+            if not fused:
+                raise
+            print(f"[bench] symmetric memory unavailable ({e}); NCCL all-gather", file=sys.stderr)
+            sh = ShardedStep(cfg_id, device=dev, steps=n_steps_scene, fused=False)
+        gather = ("fused: compat stores its columns into every rank's symmetric-memory C_k (NVLink), device barrier"
+                  if sh.symm is not None else "NCCL all_gather_into_tensor of the column blocks")
+        st, scene = sh.st, sh.scene
+    else:
+        scene = make_scene(cfg_id, steps=n_steps_scene)
+        st = GlmbStep(scene, device=dev)
     stage_names = ["predict", "birth", "compat", "reweight"]
     stage_ms = {n: [] for n in stage_names}
 
-    side = torch.cuda.Stream(device=dev)   # reweight overlaps compat (double-buffered weights)
     def one_step(k):
         """One step as timed: predict -> birth on `stream`, then compat on `stream`
         overlapped with reweight on `side` (reweight writes the spare weight buffer,
-        compat reads the current one)."""
+        compat reads the current one); at W > 1 with the broadcast before and the
+        gather after (ShardedStep.step)."""
+        if sh is not None:
+            M = sh.load_measurements(k, stream=stream)
+            sh.step(k, M, stream=stream, side=side)
+            return
         zi = k % len(st.Z)
         with torch.cuda.stream(stream):
-            if world > 1:
-                M = st.Z[zi].shape[0]
-                if rank == 0:
-                    Zbuf[:M].copy_(st.Z[zi]); thbuf[:M].copy_(st.theta[zi])
-                broadcast_measurements(Zbuf[:M], thbuf[:M], src=0)
-                Zk, thk = Zbuf[:M], thbuf[:M]
-            else:
-                Zk, thk = st.Z[zi], st.theta[zi]
+            Zk, thk = st.Z[zi], st.theta[zi]
             st.predict(k, stream)
             st.birth(k, stream)
             ready = ev()
@@ -631,17 +624,9 @@ def main():
                 st.reweight(k, side, Z=Zk, theta=thk, out_of_place=True)
                 done = ev()
                 done.record(side)
-            if symm_cols is not None:
-                symm_cols.compat(p_now, Zk, st.R, st.cfg.p_d, st.cfg.kappa, st.cfg.gamma, st.out.C_clutter, stream)
-            else:
-                L.glmb_compat(p_now, Zk, st.R, st.cfg.p_d, st.cfg.kappa, st.cfg.gamma,
-                              st.out.C_clutter, st.out.C_tracks, st.out.gate, stream)
+            L.glmb_compat(p_now, Zk, st.R, st.cfg.p_d, st.cfg.kappa, st.cfg.gamma,
+                          st.out.C_clutter, st.out.C_tracks, st.out.gate, stream)
             stream.wait_event(done)
-            if symm_cols is not None:
-                symm_cols.barrier(stream)
-            elif world > 1:
-                allgather_columns(st.out.C_tracks, C_full)
-                allgather_columns(st.out.gate, G_full)
 
     def isolated_step(k):
         """The same four calls serialised on `stream`, with an event between each, so
@@ -664,9 +649,8 @@ def main():
     for k in range(a.warmup):
         one_step(k)
     torch.cuda.synchronize(dev)
-    if symm_cols is not None and not verify_fused_gather(st, symm_cols, C_full, G_full, plan, rank, world, dev,
-                                                         stream):
-        symm_cols = None   # every rank falls back together (collective decision)
+    if sh is not None and sh.symm is not None and not verify_fused_gather(sh, dev, stream):
+        sh.symm = None   # every rank falls back together (collective decision)
         gather = "NCCL all_gather_into_tensor of the column blocks (fused gather failed its check)"
         print("[bench] fused gather disagreed with the NCCL all-gather; using NCCL", file=sys.stderr)
     sampler = ClockSampler(local)
@@ -782,6 +766,23 @@ def main():
                 sec = float(t[0])
             return sec, h2d // a.steps, d2h // a.steps
 
+        def host_step_dist(k):
+            """W > 1: ShardedStep.step_host_csr -- rank 0's pinned Z_k / theta_k H2D, the broadcast,
+            every rank's shard, the gathers, and rank 0's CSR read-back of the gathered C_k."""
+            zi = k % len(Zh)
+            _, hb, db = sh.step_host_csr(k, Zh[zi], thh[zi], stream=stream, side=side)
+            return hb, db
+
+        if sh is not None:
+            e2e_s, h2d, d2h = timed(host_step_dist)
+            e2e = {"value": evals_total / e2e_s, "unit": "evals/s",
+                   "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                   "ms_per_step": e2e_s * 1e3 / a.steps,
+                   "note": "dist.ShardedStep.step_host_csr: rank 0's pinned H2D of Z_k, theta_k; the broadcast; "
+                           "every rank's predict/birth/compat/reweight; the C_k + gate all-gather (or fused peer "
+                           "stores) and the log_norm/flags gather; rank 0 builds the CSR of the gathered C_k and "
+                           "reads it back with log_norm and flags; synchronised each step; max over ranks"}
+    if not a.no_e2e and sh is None:
         e2e_s, h2d, d2h = timed(host_step_csr)
         dn_s, dn_h2d, dn_d2h = timed(host_step_dense)
         e2e = {"value": evals_total / e2e_s, "unit": "evals/s",
@@ -816,7 +817,8 @@ def main():
         elapsed_ms=elapsed_ms, evals_total=evals_total, pairs_per_launch=pairs_local / a.steps,
         stage_ms=stage_ms, sm_count=L.glmb_sm_count(local), clocks=sampler.summary(),
         T_surv=st.T_surv, B_local=st.B_local, T_local=st.T_local, P=st.P, M_mean=float(np.mean(Ms)),
-        traffic=compat_traffic(st.T_local, st.P, len(scene.Z[0])), e2e=e2e, cpu=cpu)
+        traffic=compat_traffic(st.T_local, st.P, len(scene.Z[0])), e2e=e2e, cpu=cpu,
+        reweight_launches=1 if st.contiguous else 2)
     line["config"]["gather"] = gather
     line["ms_per_step_p50"] = float(np.percentile(per_step, 50))
     line["ms_per_step_p95"] = float(np.percentile(per_step, 95))

@@ -136,6 +136,18 @@ def _ptr(t) -> int:
     return t.data_ptr()
 
 
+def _mat(t):
+    """(pointer, leading dimension) of a row-major 2-D CUDA matrix whose rows may be strided
+    (e.g. the C columns / gate words of a packed row, dist.ShardedStep); None -> (None, 0)."""
+    if t is None:
+        return None, 0
+    if not t.is_cuda:
+        raise GlmbError(-1, "expected a CUDA tensor (the GLMB path has no CPU fallback)")
+    if t.dim() != 2 or (t.shape[1] > 1 and t.stride(1) != 1):
+        raise GlmbError(-1, "expected a 2-D matrix with unit column stride")
+    return t.data_ptr(), (t.stride(0) if t.shape[0] > 1 else t.shape[1])
+
+
 def _stream(stream):
     s = stream if stream is not None else torch.cuda.current_stream()
     return s.cuda_stream
@@ -221,9 +233,9 @@ def glmb_compat(trk: Particles, Z, R, p_d, kappa, gamma, C_clutter, C_tracks, ga
     """Z [M,2] fp32; C_tracks [T, ldc] fp32; gate [T, ldg] int32 (u32 words); C_clutter [M] or None."""
     t = trk.struct()
     M = Z.shape[0]
+    (pc, ldc), (pg, ldg) = _mat(C_tracks), _mat(gate)
     _check(load().glmb_compat(C.byref(t), _ptr(Z), M, R[0], R[1], R[2], p_d, kappa, gamma,
-                              _ptr(C_clutter), _ptr(C_tracks), C_tracks.shape[1], _ptr(gate),
-                              gate.shape[1], _stream(stream)))
+                              _ptr(C_clutter), pc, ldc, pg, ldg, _stream(stream)))
 
 
 def glmb_reweight(trk: Particles, Z, R, theta, col_offset, log_norm, flags, stream=None, w_out=None):
@@ -278,15 +290,16 @@ def glmb_normals_dump(seed, ctr, out, stream=None):
 def glmb_death_prob(C_tracks, gate, M, p_d, kappa, p_s, d_out, stream=None):
     """C_tracks [T, ldc] fp32, gate [T, ldg] int32 words, p_s [T] fp32 -> d_out [T] fp32."""
     T = C_tracks.shape[0]
-    _check(load().glmb_death_prob(T, int(M), _ptr(C_tracks), C_tracks.shape[1], _ptr(gate), gate.shape[1],
-                                  p_d, kappa, _ptr(p_s), _ptr(d_out), _stream(stream)))
+    (pc, ldc), (pg, ldg) = _mat(C_tracks), _mat(gate)
+    _check(load().glmb_death_prob(T, int(M), pc, ldc, pg, ldg, p_d, kappa, _ptr(p_s), _ptr(d_out),
+                                  _stream(stream)))
 
 
 def glmb_compat_rows(C_tracks, gate, M, row_ptr, col, val, ln_val, stream=None):
     """CSR of the gated entries: row_ptr [M+1] int32, col [cap] int32, val [cap] fp32, ln_val [cap] fp64."""
     T = C_tracks.shape[0]
-    _check(load().glmb_compat_rows(T, int(M), _ptr(C_tracks), C_tracks.shape[1], _ptr(gate), gate.shape[1],
-                                   _ptr(row_ptr), _ptr(col), _ptr(val), _ptr(ln_val), col.shape[0],
+    (pc, ldc), (pg, ldg) = _mat(C_tracks), _mat(gate)
+    _check(load().glmb_compat_rows(T, int(M), pc, ldc, pg, ldg, _ptr(row_ptr), _ptr(col), _ptr(val), _ptr(ln_val), col.shape[0],
                                    _stream(stream)))
 
 

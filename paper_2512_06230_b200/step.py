@@ -19,12 +19,6 @@ from . import _lib as L
 from .scenes import Scene
 
 
-def shard_range(n: int, rank: int, world: int) -> range:
-    """Contiguous block of the n global columns owned by rank (dist.ShardPlan)."""
-    from .dist import ShardPlan
-    return ShardPlan(n, world).cols(rank)
-
-
 @dataclasses.dataclass
 class StepOutputs:
     C_clutter: torch.Tensor
@@ -37,26 +31,44 @@ class StepOutputs:
 class GlmbStep:
     """Buffers + launch sequence for one rank.
 
-    scene: generated with rows = this rank's survivor rows (global ids in scene.gid).
-    cols:  this rank's global column block [lo, hi) of the T_k columns.
+    scene:  generated with rows = this rank's survivor rows (global ids in scene.gid).
+    cols:   a contiguous block [lo, hi) of the T_k global columns (survivors, then births);
+    births: or, with cols holding survivor columns only, this rank's births as birth indices
+            [b0, b1) (global columns T + b) -- SURVEY 8(e)'s even split of the births
+            (dist.ShardPlan).  The local rows are [survivors | births] either way.
     """
 
     def __init__(self, scene: Scene, cols: Optional[range] = None, device="cuda",
-                 seed: Optional[int] = None, rows_alloc: Optional[int] = None):
+                 seed: Optional[int] = None, rows_alloc: Optional[int] = None,
+                 births: Optional[range] = None):
         cfg = scene.cfg
         self.scene = scene
         self.cfg = cfg
         self.device = torch.device(device)
         Tk = cfg.T + cfg.B
-        self.cols = range(0, Tk) if cols is None else cols
-        lo, hi = self.cols.start, self.cols.stop
-        surv = range(lo, min(hi, cfg.T))
-        births = range(max(lo, cfg.T), hi)
+        cols = range(0, Tk) if cols is None else cols
+        lo, hi = cols.start, cols.stop
+        if births is None:
+            surv = range(lo, min(hi, cfg.T))
+            births = range(max(lo, cfg.T) - cfg.T, max(hi, cfg.T) - cfg.T)
+        else:
+            if hi > cfg.T or births.start < 0 or births.stop > cfg.B:
+                raise ValueError("with births given, cols must be survivor columns")
+            surv = cols
         if list(scene.gid) != list(surv):
             raise ValueError("scene rows must equal this rank's survivor columns")
+        self.surv_cols = surv
+        self.birth_idx = births
         self.T_surv = len(surv)
         self.B_local = len(births)
         self.T_local = self.T_surv + self.B_local
+        # global column (0-based track index) of every local row
+        self.col_of_row = np.concatenate([np.arange(surv.start, surv.stop),
+                                          cfg.T + np.arange(births.start, births.stop)]).astype(np.int64)
+        # one reweight launch when the local rows are consecutive global columns, else two
+        self.contiguous = (self.T_surv == 0 or self.B_local == 0
+                           or (surv.stop == cfg.T and births.start == 0))
+        self.col_offset = int(self.col_of_row[0]) if self.T_local else 0
         P = cfg.P
         self.P = P
         dev = self.device
@@ -68,7 +80,7 @@ class GlmbStep:
         # reads the current one on another stream (glmb_reweight's w_out)
         self.w_bufs = [self.particles.data[5], torch.empty_like(self.particles.data[5])]
         self.w_cur = 0
-        b_idx = [b - cfg.T for b in births]
+        b_idx = list(births)
         gid = np.concatenate([np.asarray(scene.gid, np.int32),
                               scene.birth_gid[b_idx].astype(np.int32)])
         self.gid = torch.from_numpy(gid).to(dev)
@@ -91,6 +103,13 @@ class GlmbStep:
             flags=torch.zeros(self.T_local, dtype=torch.int32, device=dev))
         self.seed = cfg.seed if seed is None else seed
         self.R = cfg.R
+
+    @property
+    def cols(self) -> range:
+        """The contiguous global column block of this rank (only when its rows are contiguous)."""
+        if not self.contiguous:
+            raise ValueError("this rank's columns are two blocks (survivors, births): use col_of_row")
+        return range(self.col_offset, self.col_offset + self.T_local)
 
     # ---- the four stages (each is one C-ABI call) ----
     def survivors(self) -> L.Particles:
@@ -121,9 +140,16 @@ class GlmbStep:
         zi = k % len(self.Z)
         o = self.out
         w_out = self.w_bufs[1 - self.w_cur] if out_of_place else None
-        L.glmb_reweight(self.particles, self.Z[zi] if Z is None else Z, self.R,
-                        self.theta[zi] if theta is None else theta, self.cols.start,
-                        o.log_norm, o.flags, stream, w_out=w_out)
+        Zk = self.Z[zi] if Z is None else Z
+        thk = self.theta[zi] if theta is None else theta
+        if self.contiguous:
+            L.glmb_reweight(self.particles, Zk, self.R, thk, self.col_offset, o.log_norm, o.flags, stream,
+                            w_out=w_out)
+        else:   # survivors and births are two global column blocks: one launch per block
+            for a, b, off in ((0, self.T_surv, self.surv_cols.start),
+                              (self.T_surv, self.T_local, self.cfg.T + self.birth_idx.start)):
+                L.glmb_reweight(self.particles.rows(a, b), Zk, self.R, thk, off, o.log_norm[a:b], o.flags[a:b],
+                                stream, w_out=None if w_out is None else w_out[a:b])
         if out_of_place:
             self.w_cur = 1 - self.w_cur
             self.particles = L.Particles(self.particles.data, self.P, self.w_bufs[self.w_cur])
@@ -133,6 +159,8 @@ class GlmbStep:
 
     def run(self, k: int, stream=None):
         """One whole step through the fused glmb_step entry point."""
+        if not self.contiguous:
+            raise ValueError("glmb_step takes one column offset: run the four stages instead")
         zi = k % len(self.Z)
         o = self.out
         prm = self.step_params(k)
@@ -159,5 +187,5 @@ class GlmbStep:
         zi = k % len(self.Z)
         M = len(self.scene.Z[zi])
         th = self.scene.theta[zi]
-        n_assigned = int(((th >= self.cols.start + 1) & (th <= self.cols.stop)).sum())
+        n_assigned = int(np.isin(th - 1, self.col_of_row).sum())
         return M * self.T_local * self.P + self.P * n_assigned

@@ -31,18 +31,18 @@ def _worker(rank, world, port, cfg_id, out_q):
         full = make_scene(cfg_id, steps=1)
         c = full.cfg
         Tk = c.T + c.B
-        plan = ShardPlan(Tk, world)
-        cols = plan.cols(rank)
+        plan = ShardPlan(Tk, world, c.B)
+        surv, births = plan.surv(rank), plan.births(rank)
+        cols = list(surv) + [c.T + b for b in births]
         # Z_k, theta_k live on rank 0 and are broadcast
         M = len(full.Z[0])
         Z = torch.from_numpy(full.Z[0].copy()) if rank == 0 else torch.zeros(M, 2)
         th = torch.from_numpy(full.theta[0].copy()) if rank == 0 else torch.zeros(M, dtype=torch.int32)
         broadcast_measurements(Z, th, src=0)
         Z, th = Z.numpy(), th.numpy()
-        # this rank's particles: survivors from the generator, births from the oracle
-        surv = range(cols.start, min(cols.stop, c.T))
+        # this rank's particles: survivors from the generator, births (split evenly) from the oracle
         s = make_scene(cfg_id, rows=surv, steps=1)
-        bidx = [b - c.T for b in range(max(cols.start, c.T), cols.stop)]
+        bidx = list(births)
         xs, ys, ws = [s.x], [s.y], [s.w]
         if bidx:
             bo = oracle.birth(full.birth_mean[bidx], full.birth_chol[bidx], full.birth_gid[bidx],
@@ -57,13 +57,18 @@ def _worker(rank, world, port, cfg_id, out_q):
         block[:len(cols)] = torch.from_numpy(loc["C_tracks"])
         gathered = torch.zeros(plan.per_rank * world, ldc, dtype=torch.float64)
         allgather_columns(block, gathered)
-        _, ln, _ = oracle.reweight(x, y, w, Z, c.R, th, col_offset=cols.start) if len(cols) else (None, np.zeros(0), None)
+        # the reweight block per contiguous run of global columns (survivors, then births)
+        ln = np.zeros(len(cols))
+        for a, b, off in ((0, len(surv), surv.start), (len(surv), len(cols), c.T + births.start)):
+            if b > a:
+                ln[a:b] = oracle.reweight(x[a:b], y[a:b], w[a:b], Z, c.R, th, col_offset=off)[1]
         lnb = torch.zeros(plan.per_rank, dtype=torch.float64)
         lnb[:len(cols)] = torch.from_numpy(ln)
         lng = torch.zeros(plan.per_rank * world, dtype=torch.float64)
         allgather_columns(lnb, lng)
         if rank == 0:
-            out_q.put((gathered[:Tk].numpy(), lng[:Tk].numpy(), list(cols), plan.per_rank))
+            rows = plan.global_rows()
+            out_q.put((gathered.numpy()[rows], lng.numpy()[rows], cols, plan.per_rank))
     finally:
         dist.destroy_process_group()
 
@@ -92,16 +97,24 @@ def test_sharded_C_equals_single_process(orc, cfg_id, world):
     np.testing.assert_array_equal(gathered, ref["C_tracks"])
     _, ln_ref, _ = orc.reweight(x, y, w, full.Z[0], c.R, full.theta[0], 0)
     np.testing.assert_array_equal(ln_g, ln_ref)
-    assert cols0 == list(range(0, per))
+    assert cols0[0] == 0 and len(cols0) <= per
 
 
 def test_shard_plan_covers_columns_once():
     from paper_2512_06230_b200.dist import ShardPlan
-    for n in (0, 1, 7, 64, 68, 1040, 4096):
+    for n, B in ((0, 0), (1, 0), (7, 0), (64, 0), (68, 4), (1040, 16), (4096, 0), (21, 5), (3, 3)):
         for world in (1, 2, 3, 4, 8):
-            plan = ShardPlan(n, world)
-            seen = [c for r in range(world) for c in plan.cols(r)]
+            plan = ShardPlan(n, world, B)
+            seen = sorted(c for r in range(world) for c in plan.cols(r))
             assert seen == list(range(n))
             assert all(len(plan.cols(r)) <= plan.per_rank for r in range(world))
+            # births split evenly: no rank holds more than ceil(B / W)
+            assert all(len(plan.births(r)) <= -(-B // world) for r in range(world))
+            rows = plan.global_rows()
+            assert len(set(rows.tolist())) == n and (rows < world * plan.per_rank).all()
             for col in range(n):
-                assert col in plan.cols(plan.owner(col))
+                r = plan.owner(col)
+                assert col in list(plan.cols(r))
+                assert rows[col] == r * plan.per_rank + list(plan.cols(r)).index(col)
+            if B == 0 or world == 1:      # one contiguous block per rank: gathered = global order
+                assert (rows == np.arange(n)).all()

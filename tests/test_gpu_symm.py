@@ -33,17 +33,21 @@ def test_symmetric_columns_world1():
         Z = torch.from_numpy(sc.Z[0]).cuda()
         M = Z.shape[0]
         ldc, ldg = (M + 31) // 32 * 32, (M + 31) // 32
+        S = ldc + (ldg + 31) // 32 * 32                  # dist.ShardedStep's packed row
         try:
-            cols = SymmetricColumns(p.T, ldc, ldg, torch.device("cuda", 0))
+            cols = SymmetricColumns(p.T, S, ldc, torch.device("cuda", 0))
         except Exception as e:  # noqa: BLE001
             pytest.skip(f"symmetric memory unavailable: {e}")
-        cols.compat(p, Z, cfg.R, cfg.p_d, cfg.kappa, cfg.gamma, None)
-        cols.barrier()
         C0 = torch.zeros(p.T, ldc, device="cuda")
         G0 = torch.zeros(p.T, ldg, dtype=torch.int32, device="cuda")
         L.glmb_compat(p, Z, cfg.R, cfg.p_d, cfg.kappa, cfg.gamma, None, C0, G0)
-        torch.cuda.synchronize()
-        np.testing.assert_array_equal(cols.C.cpu().numpy()[:, :M], C0.cpu().numpy()[:, :M])
-        np.testing.assert_array_equal(cols.G.cpu().numpy(), G0.cpu().numpy())
+        for k in (0, 1):                                 # both copies of the double buffer
+            cols.compat(p, Z, cfg.R, cfg.p_d, cfg.kappa, cfg.gamma, None, 0, k)
+            cols.barrier(k)
+            torch.cuda.synchronize()
+            buf = cols.buffer(k)
+            np.testing.assert_array_equal(buf.cpu().numpy()[:, :M], C0.cpu().numpy()[:, :M])
+            np.testing.assert_array_equal(buf.view(torch.int32)[:, ldc:ldc + ldg].cpu().numpy(), G0.cpu().numpy())
+        assert cols.buffer(0).data_ptr() != cols.buffer(1).data_ptr()
     finally:
         dist.destroy_process_group()
