@@ -31,8 +31,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "particle-measurement likelihood evals/s (GLMB step: predict+birth+compat+reweight)"
-SFU_EX2_PER_CLK_PER_SM = 16          # MUFU.EX2 lanes/clk/SM on sm_100 (measured: glmb_peaks)
-FMA_LANES_PER_CLK_PER_SM = 128       # FP32 FMA lanes/clk/SM (FFMA or FFMA2 x 2), measured: glmb_peaks
+# measured on B200 by glmb_peaks (profiles/r01_peaks.json, at the 1965 MHz max clock):
+SFU_EX2_PER_CLK_PER_SM = 15.94       # MUFU.EX2 results/clk/SM (nominal 16)
+FMA_LANES_PER_CLK_PER_SM = 124.0     # FP32 lanes/clk/SM issued as FFMA2 (nominal 128; plain FFMA 120.4)
 # compat, per pair (exact-difference form): 5 FP32 lane-ops (dx, dy, dx^2, +dy^2, acc) + one exp;
 # an exp moved to the FMA pipe costs 8 FP32 lane-ops.
 # Best split f of exps on the FMA pipe: x(1-f) = E, x(5+8f) = F  ->  x = (F + 8E) / 13 pairs/clk/SM.
@@ -178,38 +179,108 @@ def oracle_sample(cfg_id: int, seconds: float, cores: int, single_core: bool = T
     return out
 
 
-def reference_arm(a, cfg_id):
+def workload_config(cfg_id, cfg, world, M_mean, evals_per_step):
+    """The `config` object both arms print (same keys and values for the same workload)."""
+    return {"workload": f"cfg{cfg_id} ({cfg.name})", "T": cfg.T, "B": cfg.B, "P": cfg.P, "M_mean": M_mean,
+            "parallelism": f"tracks sharded x{world}",
+            "l2": f"inputs larger than L2: particle state 24 B x T_k x P "
+                  f"({24 * (cfg.T + cfg.B) * cfg.P / 1e6:.0f} MB) streams from HBM every step",
+            "evals_per_step": evals_per_step}
+
+
+class OracleStep:
+    """The fp64 oracle running the bench's workload step by step (the reference arm): predict
+    of the survivors (O5), births (O6), compat over [survivors | births] x all M_k (O7),
+    reweight under theta_k (O8), the state (fp32-rounded, as the GPU keeps it) carried from
+    step to step -- the same steps, step indices and measurements the GPU arm times.  n_tracks
+    < T samples the first n survivor tracks (and all births) when the whole step would not fit
+    the time budget; at config 3 on the box's 16 cores the whole step fits (~6 s)."""
+
+    def __init__(self, cfg_id: int, n_steps: int, n_tracks: int, cores: int):
+        import oracle
+        from paper_2512_06230_b200.scenes import make_scene
+        self.o = oracle
+        oracle.set_num_threads(cores)
+        self.cfg_id, self.cores = cfg_id, cores
+        s = make_scene(cfg_id, rows=range(n_tracks), steps=n_steps)
+        self.s, self.c, self.n = s, s.cfg, n_tracks
+        self.state = [a.astype(np.float32) for a in (s.x, s.y, s.v, s.psi, s.omega, s.w)]
+
+    def step(self, k: int):
+        s, c, o = self.s, self.c, self.o
+        zi = k % len(s.Z)
+        Z, th = s.Z[zi], s.theta[zi]
+        t0 = time.perf_counter()
+        x, y, v, psi, om, w = self.state
+        pred = [a.astype(np.float32) for a in o.predict(x, y, v, psi, om, s.gid, c.dt, c.sigma_a, c.sigma_w,
+                                                         c.seed, k)]
+        if c.B:
+            b = [a.astype(np.float32) for a in o.birth(s.birth_mean, s.birth_chol, s.birth_gid, c.P, c.seed, k)]
+            cols = [np.concatenate([pa, ba]) for pa, ba in zip(pred + [w], b)]
+        else:
+            cols = pred + [w]
+        o.compat(cols[0], cols[1], cols[5], Z, c.R, c.p_d, c.kappa, c.gamma)
+        # theta's columns are global: the sampled survivors keep theirs, births sit at T + b
+        th_s = np.where((th >= 1) & (th <= self.n), th,
+                        np.where(th > c.T, th - (c.T - self.n), 0)).astype(np.int32)
+        w_new = o.reweight(cols[0], cols[1], cols[5], Z, c.R, th_s, 0)[0].astype(np.float32)
+        dt = time.perf_counter() - t0
+        self.state = pred + [w_new[:self.n]]
+        n_cols = self.n + c.B
+        n_assigned = int((th_s != 0).sum())
+        return dt, len(Z) * n_cols * c.P + c.P * n_assigned
+
+    def describe(self):
+        c = self.c
+        what = "every track" if self.n == c.T else f"the first {self.n} of {c.T} survivor tracks + all {c.B} births"
+        return (f"cfg{self.cfg_id}: {what} x all M_k x P={c.P}; predict + birth + compat + reweight per step, "
+                f"state carried, fp64, OpenMP over tracks on {self.cores} threads")
+
+
+def reference_arm(a, cfg_id, budget_s: float = 240.0):
     """--impl reference: this tier's reference is the fp64 oracle (there is no reference
-    implementation, only the paper).  Rank 0 alone runs it; other ranks exit 0."""
+    implementation, only the paper), timed as it stands on the host's cores over the same
+    workload steps as the GPU arm.  The whole step is run when K + W steps fit `budget_s`
+    (config 3), else the first n survivor tracks (config 4 at N > 1).  Rank 0 alone runs it;
+    the other ranks exit 0."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    from paper_2512_06230_b200.scenes import make_scene
+    from paper_2512_06230_b200.scenes import CONFIGS
+    cfg = CONFIGS[cfg_id]
     cores = host_cores()
-    full = make_scene(cfg_id, rows=range(0), steps=1)
-    c = full.cfg
-    th = full.theta[0]
-    full_evals = len(full.Z[0]) * (c.T + c.B) * c.P + c.P * int((th != 0).sum())
-    per_step = min(20.0, max(1.0, 150.0 / max(1, a.steps + a.warmup)))
-    smp = OracleSample(cfg_id, per_step, cores)
-    times, evals = [], []
+    n_steps = min(cfg.steps, a.warmup + a.steps)
+    # calibrate on a few tracks: seconds per track-step
+    n0 = max(1, min(cfg.T, cores))
+    cal = OracleStep(cfg_id, n_steps, n0, cores)
+    t_cal, _ = cal.step(0)
+    per_track = t_cal / (n0 + cfg.B)
+    per_step_budget = budget_s / max(1, a.steps + a.warmup)
+    n = cfg.T if per_track * (cfg.T + cfg.B) <= per_step_budget else \
+        max(n0, min(cfg.T, int(per_step_budget / per_track) - cfg.B))
+    smp = OracleStep(cfg_id, n_steps, n, cores)
+    times, evals, Ms, full_ev = [], [], [], []
     for k in range(a.warmup + a.steps):
-        dt, ev = smp.run()
+        dt, ev = smp.step(k)
         if k >= a.warmup:
             times.append(dt)
             evals.append(ev)
+            zi = k % len(smp.s.Z)
+            Ms.append(len(smp.s.Z[zi]))
+            full_ev.append(len(smp.s.Z[zi]) * (cfg.T + cfg.B) * cfg.P + cfg.P * int((smp.s.theta[zi] != 0).sum()))
     value = sum(evals) / sum(times)
-    ms = full_evals / value * 1e3
-    sample = smp.describe(statistics.mean(times)) + " per step"
+    M_mean = float(np.mean(Ms))
+    full_evals = M_mean * (cfg.T + cfg.B) * cfg.P
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s",
-            "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
+            "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
             "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"cfg{cfg_id} ({c.name})", "T": c.T, "B": c.B, "P": c.P,
-                       "M": len(full.Z[0]), "note": "fp64 CPU oracle on a bounded sample per step; "
-                       "ms_per_step extrapolated to the full step at the sampled rate"},
+            "config": workload_config(cfg_id, cfg, world, M_mean, float(sum(full_ev)) / a.steps),
+            "sample": smp.describe() + ("" if n == cfg.T else
+                                        f"; ms_per_step is the sampled step's (the whole step would be "
+                                        f"~{1e3 * full_evals / value:.0f} ms at this rate)"),
             "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "oracle",
-                             "sample": sample},
+                             "sample": smp.describe()},
             "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -264,18 +335,15 @@ def make_line(*, cfg_id, cfg, world, steps, warmup, elapsed_ms, evals_total, pai
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": f"cfg{cfg_id} ({cfg.name})", "T": cfg.T, "B": cfg.B, "P": cfg.P,
-                   "M_mean": M_mean, "parallelism": f"tracks sharded x{world}",
-                   "l2": f"inputs larger than L2: particle state 24 B x T_k x P "
-                         f"({24 * (cfg.T + cfg.B) * cfg.P / 1e6:.0f} MB) streams from HBM every step",
-                   "evals_per_step": evals_total / steps,
-                   "schedule": "predict, birth; then compat overlapped with reweight on a second stream "
-                               "(double-buffered weights); stages_ms timed in a separate serialised pass"},
+        "config": workload_config(cfg_id, cfg, world, M_mean, evals_total / steps),
+        "schedule": "predict, birth; then compat overlapped with reweight on a second stream "
+                    "(double-buffered weights); stages_ms timed in a separate serialised pass",
         "roofline": {"bound": "alu", "kernel": "compat (exp: MUFU.EX2 + FMA-pipe polynomial)",
                      "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Geval/s",
                      "frac": achieved / peak,
                      "peak_basis": f"{sm_count} SM x {COMPAT_PAIRS_PER_CLK_PER_SM:.2f} pairs/clk "
-                                   f"(16 ex2/clk + 128 FP32 lanes/clk, measured; 5 lanes + 1 exp per pair) x {f_max / 1e6:.0f} MHz",
+                                   f"({SFU_EX2_PER_CLK_PER_SM} ex2/clk + {FMA_LANES_PER_CLK_PER_SM} FP32 lanes/clk, measured by "
+                                   f"glmb_peaks; 5 lanes + 1 exp per pair) x {f_max / 1e6:.0f} MHz",
                      "frac_of_mufu_only_bound": achieved / peak_sfu,
                      "frac_at_measured_clock": (achieved / (sm_count * COMPAT_PAIRS_PER_CLK_PER_SM * sm_mhz * 1e6)
                                                 if sm_mhz else None),
@@ -518,29 +586,46 @@ def bench_graphs(dev, reps: int = 200):
 
 
 # ------------------------------------------------------------------ the paper's convoy
-def bench_convoy(dev):
+def bench_convoy(dev, seeds=range(10)):
     """The paper's own benchmark shape: N = 20 objects, D = 5, sigma = 0.25, delta = 2,
     H_up = 100, tau = 1e-5, H_max = 100, 548 updates, through tracker.ConvoyTracker (every stage a
-    libglmb kernel; the host copies Z_k in and reads one count per update).  Per-update time is
+    libglmb kernel; the host copies Z_k in and reads one count per update).  The paper's protocol
+    (P:186): 10 runs (seeds 0-9), reported as mean +- SEM over the runs.  Per-update time is
     wall clock around the whole update (what the paper's 0.1 s real-time line refers to),
     plus the device time between the first and last kernel; accuracy by P:213-215's metrics."""
     from paper_2512_06230_b200.scenes import ConvoyConfig
     from paper_2512_06230_b200.tracker import convoy_metrics, run_convoy
-    cfg = ConvoyConfig(N=20, H_max=100)
     run_convoy(ConvoyConfig(N=2, H_max=10, K=20), K_cap=256, device=dev)     # warm-up (module load, allocator)
-    recs, ests, truth = run_convoy(cfg, K_cap=4096, device=dev)
-    card, dist = convoy_metrics(ests, truth)
+    per_seed = []
+    wall_all, dev_all = [], []
+    for sd in seeds:
+        cfg = ConvoyConfig(N=20, H_max=100, seed=sd)
+        recs, ests, truth = run_convoy(cfg, K_cap=4096, device=dev)
+        card, dist = convoy_metrics(ests, truth)
+        wall = np.array([r.wall_ms for r in recs])
+        devms = np.array([r.device_ms for r in recs])
+        wall_all.append(wall)
+        dev_all.append(devms)
+        per_seed.append({"seed": sd, "card_err": card, "track_err_m": dist, "update_ms_mean": float(wall.mean()),
+                         "device_ms_mean": float(devms.mean()), "pairs_max": max(r.n_pairs for r in recs)})
     stages = {}
-    run_convoy(cfg, K_cap=4096, device=dev, with_estimates=False, stage_ms=stages)   # per-stage pass
-    wall = np.array([r.wall_ms for r in recs])
-    devms = np.array([r.device_ms for r in recs])
+    run_convoy(ConvoyConfig(N=20, H_max=100, seed=0), K_cap=4096, device=dev, with_estimates=False,
+               stage_ms=stages)   # per-stage pass
+    wall, devms = np.concatenate(wall_all), np.concatenate(dev_all)
+    mse = lambda key: (float(np.mean([p[key] for p in per_seed])),
+                       float(np.std([p[key] for p in per_seed], ddof=1) / np.sqrt(len(per_seed))))
+    card_m, card_sem = mse("card_err")
+    dist_m, dist_sem = mse("track_err_m")
     return {"workload": "convoy N=20, D=5, sigma=0.25 m, delta=2, lambda=0, H_up=100, tau=1e-5, H_max=100, "
-                        "548 updates (P:182-186; synthetic figure-eight ground track, R35)",
+                        f"548 updates (P:182-186; synthetic figure-eight ground track, R35); {len(per_seed)} runs "
+                        "(seeds), mean +- SEM (P:186)",
             "update_ms_mean": float(wall.mean()), "update_ms_p95": float(np.percentile(wall, 95)),
             "update_ms_max": float(wall.max()), "device_ms_mean": float(devms.mean()),
-            "realtime_budget_ms": 100.0, "card_err": card, "track_err_m": dist,
-            "pairs_max": max(r.n_pairs for r in recs),
-            "stages_ms": stages, "stages_note": "a second pass with a CUDA event after every stage",
+            "realtime_budget_ms": 100.0,
+            "card_err_mean": card_m, "card_err_sem": card_sem,
+            "track_err_m_mean": dist_m, "track_err_m_sem": dist_sem,
+            "per_seed": per_seed,
+            "stages_ms": stages, "stages_note": "seed 0, a second pass with a CUDA event after every stage",
             "paper": "L40S: 'under the threshold of 0.1 seconds per update ... almost always' (P:211), "
                      "card. error low at H_max=100, matched error < 0.15 m (P:213-215)"}
 
@@ -819,7 +904,7 @@ def main():
         T_surv=st.T_surv, B_local=st.B_local, T_local=st.T_local, P=st.P, M_mean=float(np.mean(Ms)),
         traffic=compat_traffic(st.T_local, st.P, len(scene.Z[0])), e2e=e2e, cpu=cpu,
         reweight_launches=1 if st.contiguous else 2)
-    line["config"]["gather"] = gather
+    line["gather"] = gather
     line["ms_per_step_p50"] = float(np.percentile(per_step, 50))
     line["ms_per_step_p95"] = float(np.percentile(per_step, 95))
     if graphs is not None:

@@ -29,7 +29,7 @@ def test_make_line_contract():
     assert line["ms_per_step"] == pytest.approx(2.5)
     r = line["roofline"]
     assert r["bound"] == "alu" and 0 < r["frac"] < 1 and r["frac"] == pytest.approx(r["achieved"] / r["peak"])
-    assert r["peak"] == pytest.approx(148 * (128 + 8 * 16) / 13 * 1.965e9 / 1e9)   # 5 lanes + 1 exp per pair
+    assert r["peak"] == pytest.approx(148 * (124.0 + 8 * 15.94) / 13 * 1.965e9 / 1e9)   # 5 lanes + 1 exp per pair
     assert line["gpu_launches"] == 16
     assert line["cpu_baseline"]["cores"] == 8 and "seconds" not in line["cpu_baseline"]
     assert "workload" in line["config"]
@@ -46,3 +46,8 @@ def test_reference_arm_runs_on_cpu():
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "oracle"
     assert line["e2e"]["h2d_bytes_per_step"] == 0
+    # the same config object as the GPU arm prints for this workload (bench.workload_config)
+    import bench
+    assert set(line["config"]) == set(bench.workload_config(0, None.__class__ and __import__(
+        "paper_2512_06230_b200.scenes", fromlist=["CONFIGS"]).CONFIGS[0], 1, 6.0, 1.0))
+    assert "every track" in line["sample"]
