@@ -48,6 +48,6 @@ def test_reference_arm_runs_on_cpu():
     assert line["e2e"]["h2d_bytes_per_step"] == 0
     # the same config object as the GPU arm prints for this workload (bench.workload_config)
     import bench
-    assert set(line["config"]) == set(bench.workload_config(0, None.__class__ and __import__(
-        "paper_2512_06230_b200.scenes", fromlist=["CONFIGS"]).CONFIGS[0], 1, 6.0, 1.0))
+    from paper_2512_06230_b200.scenes import CONFIGS
+    assert set(line["config"]) == set(bench.workload_config(0, CONFIGS[0], 1, 6.0, 1.0))
     assert "every track" in line["sample"]
