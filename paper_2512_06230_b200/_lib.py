@@ -143,9 +143,13 @@ def _mat(t):
         return None, 0
     if not t.is_cuda:
         raise GlmbError(-1, "expected a CUDA tensor (the GLMB path has no CPU fallback)")
-    if t.dim() != 2 or (t.shape[1] > 1 and t.stride(1) != 1):
+    if t.dim() != 2:
+        raise GlmbError(-1, "expected a 2-D matrix")
+    if t.numel() == 0 or t.shape[0] == 1:
+        return t.data_ptr(), t.shape[1]
+    if t.shape[1] > 1 and t.stride(1) != 1:
         raise GlmbError(-1, "expected a 2-D matrix with unit column stride")
-    return t.data_ptr(), (t.stride(0) if t.shape[0] > 1 else t.shape[1])
+    return t.data_ptr(), t.stride(0)
 
 
 def _stream(stream):

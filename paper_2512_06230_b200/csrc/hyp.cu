@@ -192,22 +192,23 @@ __global__ void __launch_bounds__(kRowWarps * 32) rows_fill_kernel(RowsArgs a) {
 }
 
 // ------------------------------------------------------------------ two-stage sampler
-// One CTA per sample q = h * H_up + s.  Shared memory: the sample's alive set
-// and its detected-track set (ldt words each).
-constexpr int kSampThreads = 128;
+// CTA = (parent h, group of spc samples), kSampWarps warps; a WARP draws one sample at a
+// time (samples s0 + warp, s0 + warp + kSampWarps, ...) with no CTA barrier inside the
+// per-sample loop: its alive / detected sets live in the warp's own shared-memory
+// words, reductions are shuffles, and __syncwarp orders the lanes.
+constexpr int kSampWarps = 8;
+constexpr int kSampThreads = 32 * kSampWarps;
 
-__device__ __forceinline__ uint64_t mix64(uint64_t z) {  // SplitMix64 finaliser
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+// one fingerprint term (summed mod 2^64 over a sample's detected rows and alive words):
+// any deterministic function works -- dedup compares the words exactly when two
+// fingerprints agree -- so one multiply-xorshift round stands in for a full finaliser
+__device__ __forceinline__ uint64_t fp_term(uint32_t v, uint64_t idx) {
+  uint64_t z = ((idx << 32) | v) * 0xBF58476D1CE4E5B9ull;
   return z ^ (z >> 31);
 }
-__device__ __forceinline__ uint64_t fp_term(uint32_t v, uint64_t idx) {
-  return mix64((idx << 32) ^ v ^ 0x9E3779B97F4A7C15ull);
-}
-
 
 // Block-wide exclusive scan of one int32 per thread (kSampThreads threads).
-__device__ __forceinline__ int32_t block_excl_scan_128(int32_t v, int32_t *red, int32_t &total) {
+__device__ __forceinline__ int32_t block_excl_scan(int32_t v, int32_t *red, int32_t &total) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int32_t x = v;
 #pragma unroll
@@ -217,24 +218,29 @@ __device__ __forceinline__ int32_t block_excl_scan_128(int32_t v, int32_t *red, 
   }
   if (lane == 31) red[wid] = x;
   __syncthreads();
-  const int32_t w0 = red[0], w1 = red[1], w2 = red[2], w3 = red[3];
-  total = w0 + w1 + w2 + w3;
-  const int32_t before = wid == 0 ? 0 : wid == 1 ? w0 : wid == 2 ? w0 + w1 : w0 + w1 + w2;
+  int32_t before = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < kSampWarps; ++w) {
+    const int32_t r = red[w];
+    before += w < wid ? r : 0;
+    tot += r;
+  }
+  total = tot;
   __syncthreads();
   return before + x - v;
 }
 
-// CTA = (parent h, group of kSampPerCta samples).  Once per CTA: the parent's rows of
-// C'_k -- the gated entries whose column is in the parent, in ascending column order --
-// are filtered into shared memory (when they fit, else the CTA walks the global CSR),
-// and the parent's track quads are listed, the first quad_cap of them with ln P_S,
-// ln(1 - P_S) of their tracks (later ones take the logs inline), and the rows holding
-// a parent entry are listed by Philox quad.  Per sample, stage 1 visits only the
-// parent's quads and stage 2 only those rows (a thread per quad, or per row when M <
-// 256).  Same draws and the same fp32 operation order as a walk of the full
-// rows (columns outside the parent are never alive), so the integer outcomes do not
-// depend on any of this.
-constexpr int kSampPerCtaMax = 16;
+// Once per CTA: the parent's rows of C'_k -- the gated entries whose column is in the
+// parent, in ascending column order -- are filtered into shared memory (when they fit,
+// else the warps walk the global CSR), the parent's track quads are listed, and the row
+// quads are split into those holding a parent entry (with the mask of their non-empty
+// rows) and the rest.  Per sample, stage 1 visits only the parent's quads, stage 2 only
+// the non-empty rows (a lane per row when they are sparse, else per quad); the other rows
+// draw theta_i = 0 with ln kappa whatever their uniform (see draw_row) and are stored as
+// zeros.  ln P_S / ln(1 - P_S) are memoised per lane (tracks share a few P_S values).  Same
+// draws and the same fp32 operation order as a walk of the full rows (columns outside
+// the parent are never alive), so the integer outcomes do not depend on any of this.
+constexpr int kSampPerCtaMax = 64;
 constexpr int kFilterBatch = 8;  // CSR words (32 entries) a warp loads per round of the row filter
 
 __device__ __forceinline__ uint32_t word_of(const u32x4 &r, int e) {
@@ -291,19 +297,17 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
   extern __shared__ __align__(16) unsigned char smraw[];
   // a.pool bytes at the front, carved at run time (below); fixed arrays after it
   unsigned char *pool = smraw;
-  double *slc = reinterpret_cast<double *>(smraw + a.pool);         // [n_count] count prior
+  double *slc = reinterpret_cast<double *>(smraw + a.pool);            // [n_count] count prior
   int32_t *frp = reinterpret_cast<int32_t *>(slc + max(a.n_count, 0));  // [M + 1]
-  int32_t *pq = frp + a.M + 1;                                     // [(T + 3) / 4]
-  int32_t *nzq = pq + ((a.T + 3) >> 2);                            // [(M + 3) / 4]
-  const bool row_mode = a.M < 2 * kSampThreads;
-  int32_t *nzr = nzq + ((a.M + 3) >> 2);                            // [M] in row mode
-  uint32_t *pmask = reinterpret_cast<uint32_t *>(nzr + (row_mode ? a.M : 0));  // [ldt]
-  uint32_t *alive = pmask + a.ldt, *det = alive + a.ldt;            // [ldt] each
-  int32_t *cnt = reinterpret_cast<int32_t *>(det + a.ldt);         // [T] when a count prior is given
-  __shared__ double red_d[4];
-  __shared__ unsigned long long red_u[4];
-  __shared__ int32_t red_i[4];
-  __shared__ int32_t use_smem, n_quads, n_nzq, n_nzr;
+  int32_t *pq = frp + a.M + 1;                                          // [(T + 3) / 4]
+  int32_t *nzq = pq + ((a.T + 3) >> 2);                                 // [(M + 3) / 4]
+  int32_t *zq = nzq + ((a.M + 3) >> 2);                                 // [(M + 3) / 4]
+  int32_t *nzr = zq + ((a.M + 3) >> 2);                                 // [M]
+  uint32_t *pmask = reinterpret_cast<uint32_t *>(nzr + a.M);           // [ldt]
+  // per warp: alive [ldt], det [ldt], cnt [T] (count prior only)
+  const int32_t wstride = 2 * a.ldt + (a.n_count > 0 ? a.T : 0);
+  __shared__ int32_t red_i[kSampWarps];
+  __shared__ int32_t use_smem, n_quads, n_nzq, n_zq, n_nzr;
   const int n_groups = (a.H_up + a.spc - 1) / a.spc;
   const int32_t h = static_cast<int32_t>(blockIdx.x / n_groups);
   const int32_t s0 = static_cast<int32_t>(blockIdx.x - static_cast<int64_t>(h) * n_groups) * a.spc;
@@ -323,13 +327,16 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
   // entry x's slot K(x).  Rows too many for the bitmap: a count and a fill pass per row.
   const int32_t r0 = __ldg(a.row_ptr), r1 = __ldg(a.row_ptr + a.M);
   const int32_t nwords = (r1 - r0 + 31) >> 5;
+  // the warps' sets sit at the end of the pool; the rest (avail) holds the rows and logs
+  const size_t warps_bytes = sizeof(uint32_t) * static_cast<size_t>(wstride) * kSampWarps;
+  const int64_t avail = static_cast<int64_t>(a.pool) - static_cast<int64_t>(warps_bytes);
   size_t rows_at = 0;  // pool offset of the filtered rows
   int32_t kept = 0;
-  if (8 * static_cast<int64_t>(nwords) <= a.pool / 2) {
+  if (8 * static_cast<int64_t>(nwords) <= avail / 2) {
     uint32_t *kb = reinterpret_cast<uint32_t *>(pool);
     int32_t *kbp = reinterpret_cast<int32_t *>(kb + nwords);
     // a warp takes kFilterBatch consecutive words per round, all loads issued first
-    for (int32_t w0 = wid * kFilterBatch; w0 < nwords; w0 += kSampThreads / 32 * kFilterBatch) {
+    for (int32_t w0 = wid * kFilterBatch; w0 < nwords; w0 += kSampWarps * kFilterBatch) {
       int32_t jj[kFilterBatch];
 #pragma unroll
       for (int u = 0; u < kFilterBatch; ++u) {
@@ -346,7 +353,7 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
     for (int32_t w0 = 0; w0 < nwords; w0 += kSampThreads) {
       const int32_t w = w0 + threadIdx.x;
       int32_t tot;
-      const int32_t ex = block_excl_scan_128(w < nwords ? __popc(kb[w]) : 0, red_i, tot);
+      const int32_t ex = block_excl_scan(w < nwords ? __popc(kb[w]) : 0, red_i, tot);
       if (w < nwords) kbp[w] = kept + ex;
       kept += tot;
     }
@@ -358,11 +365,11 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
     };
     for (int32_t i = threadIdx.x; i <= a.M; i += kSampThreads) frp[i] = K(__ldg(a.row_ptr + i));
     rows_at = static_cast<size_t>(8) * nwords;
-    if (rows_at + 16 * static_cast<size_t>(kept) <= static_cast<size_t>(a.pool)) {
+    if (static_cast<int64_t>(rows_at + 16 * static_cast<size_t>(kept)) <= avail) {
       double *flv = reinterpret_cast<double *>(pool + rows_at);
       float *fval = reinterpret_cast<float *>(flv + kept);
       int32_t *fcol = reinterpret_cast<int32_t *>(fval + kept);
-      for (int32_t w = wid; w < nwords; w += kSampThreads / 32) {
+      for (int32_t w = wid; w < nwords; w += kSampWarps) {
         const uint32_t word = kb[w];
         if (!((word >> lane) & 1u)) continue;
         const int32_t x = r0 + 32 * w + lane;
@@ -381,13 +388,13 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
         for (int32_t x = __ldg(a.row_ptr + i); x < e1; ++x) c += in_parent(__ldg(a.col + x));
       }
       int32_t tot;
-      const int32_t ex = block_excl_scan_128(c, red_i, tot);
+      const int32_t ex = block_excl_scan(c, red_i, tot);
       if (i < a.M) frp[i] = kept + ex;
       kept += tot;
     }
     if (threadIdx.x == 0) frp[a.M] = kept;
     __syncthreads();
-    if (16 * static_cast<size_t>(kept) <= static_cast<size_t>(a.pool)) {
+    if (static_cast<int64_t>(16 * static_cast<size_t>(kept)) <= avail) {
       double *flv = reinterpret_cast<double *>(pool);
       float *fval = reinterpret_cast<float *>(flv + kept);
       int32_t *fcol = reinterpret_cast<int32_t *>(fval + kept);
@@ -406,33 +413,20 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
       }
     }
   }
-  if (threadIdx.x == 0) use_smem = rows_at + 16 * static_cast<size_t>(kept) <= static_cast<size_t>(a.pool);
+  if (threadIdx.x == 0) use_smem = static_cast<int64_t>(rows_at + 16 * static_cast<size_t>(kept)) <= avail;
   __syncthreads();
 
-  // ---- the parent's track quads (ascending) with the logs of their tracks (the first
-  // quad_cap of them, in the pool after the rows)
-  const size_t quads_at = use_smem ? rows_at + 16 * static_cast<size_t>(kept) : 0;
-  const int32_t quad_cap = static_cast<int32_t>((static_cast<size_t>(a.pool) - quads_at) / 64);
-  double *qls = reinterpret_cast<double *>(pool + quads_at);   // [4 quad_cap] ln P_S
-  double *qld = qls + 4 * quad_cap;                            // [4 quad_cap] ln(1 - P_S)
+  // ---- the parent's track quads (ascending); the per-warp sets at the pool's end
+  uint32_t *wsets = reinterpret_cast<uint32_t *>(pool + a.pool - warps_bytes);
   {
     int32_t carry = 0;
     for (int32_t t0 = 0; t0 < tquads; t0 += kSampThreads) {
       const int32_t t = t0 + threadIdx.x;
       const uint32_t qbits = t < tquads ? (pmask[t >> 3] >> (4 * (t & 7))) & 0xFu : 0u;
       int32_t tot;
-      const int32_t ex = block_excl_scan_128(qbits != 0u, red_i, tot);
+      const int32_t ex = block_excl_scan(qbits != 0u, red_i, tot);
       const int32_t slot = carry + ex;
       if (qbits != 0u) pq[slot] = t;
-      if (qbits != 0u && slot < quad_cap) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          if (!((qbits >> e) & 1u)) continue;
-          const double ps = static_cast<double>(__ldg(a.p_s + 4 * t + e));
-          qls[4 * slot + e] = log(ps);
-          qld[4 * slot + e] = log(1.0 - ps);
-        }
-      }
       carry += tot;
     }
     if (threadIdx.x == 0) n_quads = carry;
@@ -448,12 +442,10 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
   const double ln_kappa = log(static_cast<double>(a.kappa));
   const double ln_miss = log(1.0 - static_cast<double>(a.p_d));
   const int32_t rquads = (a.M + 3) >> 2;
-  // ---- rows holding a parent entry, grouped by their Philox quad: nzq = (quad << 4 |
-  // mask of its non-empty rows); in row mode (few rows) also the rows themselves.  A row
-  // without one draws theta_i = 0 with ln kappa whatever its uniform (see draw_row), so
-  // the sampler only visits these.
+  // ---- row quads split into those holding a parent entry, nzq = (quad << 4 | mask of its
+  // non-empty rows), and the rest (zq: theta stored as zeros)
   {
-    int32_t cq = 0, cr = 0;
+    int32_t cq = 0, cz = 0, cr = 0;
     for (int32_t t0 = 0; t0 < rquads; t0 += kSampThreads) {
       const int32_t t = t0 + threadIdx.x;
       uint32_t mask = 0u;
@@ -464,38 +456,53 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
           if (i < a.M && rp[i + 1] > rp[i]) mask |= 1u << e;
         }
       }
-      int32_t tq, tr;
-      const int32_t exq = block_excl_scan_128(mask != 0u, red_i, tq);
-      const int32_t exr = block_excl_scan_128(__popc(mask), red_i, tr);
+      int32_t tq, tz, tr;
+      const int32_t exq = block_excl_scan(mask != 0u, red_i, tq);
+      const int32_t exz = block_excl_scan(t < rquads && mask == 0u, red_i, tz);
+      const int32_t exr = block_excl_scan(__popc(mask), red_i, tr);
       if (mask != 0u) {
         nzq[cq + exq] = static_cast<int32_t>((static_cast<uint32_t>(t) << 4) | mask);
-        if (row_mode) {
-          int32_t k = cr + exr;
-          for (uint32_t m = mask; m != 0u; m &= m - 1u) nzr[k++] = 4 * t + __ffs(m) - 1;
-        }
+        int32_t k = cr + exr;
+        for (uint32_t m = mask; m != 0u; m &= m - 1u) nzr[k++] = 4 * t + __ffs(m) - 1;
+      } else if (t < rquads) {
+        zq[cz + exz] = t;
       }
       cq += tq;
+      cz += tz;
       cr += tr;
     }
     if (threadIdx.x == 0) {
       n_nzq = cq;
+      n_zq = cz;
       n_nzr = cr;
     }
     __syncthreads();
   }
-  const int32_t nzq_n = n_nzq, nzr_n = n_nzr, nq = n_quads;
+  const int32_t nzq_n = n_nzq, zq_n = n_zq, nzr_n = n_nzr, nq = n_quads;
+  // a lane per non-empty row when the rows are sparse (<= 1.5 per non-empty quad: every
+  // row's draw is then one uniform body instead of four divergent ones), else per quad
+  const bool row_mode = 2 * nzr_n <= 3 * nzq_n;
   const bool vec_store = ((a.ldm & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.theta) & 15) == 0);
-  for (int32_t s = s0; s < s1; ++s) {
+  uint32_t *alive = wsets + static_cast<size_t>(wid) * wstride;
+  uint32_t *det = alive + a.ldt;
+  int32_t *cnt = reinterpret_cast<int32_t *>(det + a.ldt);
+  // rows without a parent entry: theta_i = 0 with ln kappa each
+  const int32_t n_empty = a.M - nzr_n;
+  const double l_empty = n_empty > 0 ? static_cast<double>(n_empty) * ln_kappa : 0.0;
+
+  float memo_ps = -1.0f;             // P_S of the memoised logs (none yet)
+  double memo_ls = 0.0, memo_ld = 0.0;
+  for (int32_t s = s0 + wid; s < s1; s += kSampWarps) {
     const int64_t q = static_cast<int64_t>(h) * a.H_up + s;
-    // stage 1 (P:44): track j of the parent survives iff u_j < 1 - d_j (fp32, R25);
-    // Philox block (j/4, h, step, 2<<24 | s), word j%4 -- only quads holding parent tracks
-    double lw = 0.0;
-    for (int32_t k = threadIdx.x; k < a.ldt; k += kSampThreads) {
+    for (int32_t k = lane; k < a.ldt; k += 32) {
       alive[k] = 0u;
       det[k] = 0u;
     }
-    __syncthreads();
-    for (int32_t v = threadIdx.x; v < nq; v += kSampThreads) {
+    __syncwarp();
+    // stage 1 (P:44): track j of the parent survives iff u_j < 1 - d_j (fp32, R25);
+    // Philox block (j/4, h, step, 2<<24 | s), word j%4 -- only quads holding parent tracks
+    double lw = 0.0;
+    for (int32_t v = lane; v < nq; v += 32) {
       const int32_t t = pq[v];
       const uint32_t qbits = (pmask[t >> 3] >> (4 * (t & 7))) & 0xFu;
       const u32x4 r = philox4x32_10(
@@ -508,86 +515,117 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
         const int32_t j = 4 * t + e;
         const float thr = __fsub_rn(1.0f, __ldg(a.d_prob + j));
         const bool al = uniform24(word_of(r, e)) < thr;
-        if (v < quad_cap) {
-          lw += al ? qls[4 * v + e] : qld[4 * v + e];
-        } else {
-          const double ps = static_cast<double>(__ldg(a.p_s + j));
-          lw += al ? log(ps) : log(1.0 - ps);
+        const float ps = __ldg(a.p_s + j);
+        if (ps != memo_ps) {  // tracks mostly share a few P_S values: logs memoised per lane
+          memo_ps = ps;
+          memo_ls = log(static_cast<double>(ps));
+          memo_ld = log(1.0 - static_cast<double>(ps));
         }
+        lw += al ? memo_ls : memo_ld;
         bits |= static_cast<uint32_t>(al) << e;
         if (a.n_count > 0) cnt[j] = 0;
       }
       if (bits) atomicOr(alive + (t >> 3), bits << (4 * (t & 7)));
     }
-    // theta_i = 0 for every row; stage 2 (after the barrier) stores the detections
     int32_t *th = a.theta + q * a.ldm;
-    for (int32_t t = threadIdx.x; t < rquads; t += kSampThreads) {
-      if (vec_store && 4 * t + 3 < a.M) {
-        *reinterpret_cast<int4 *>(th + 4 * t) = make_int4(0, 0, 0, 0);
-      } else {
-        for (int32_t i = 4 * t; i < min(a.M, 4 * t + 4); ++i) th[i] = 0;
-      }
-    }
-    __syncthreads();
-
+    uint64_t fp = 0ull;
     // stage 2: each row i draws theta_i from the row of C'_k (clutter kappa,
     // surviving gated columns in ascending order), inverse CDF in fp32 (R26);
-    // Philox block (i/4, h, step, 3<<24 | s), word i%4.  Rows with a parent entry only.
-    uint64_t fp = 0ull;
-    auto row = [&](int32_t i, uint32_t word) {
-      const int32_t pick = draw_row(rp, cl, vl, lvl, alive, a.kappa, ln_kappa, i, word, lw);
+    // Philox block (i/4, h, step, 3<<24 | s), word i%4.  Returns theta_i; updates the
+    // log-weight, the detected set, the counts and the fingerprint.
+    auto draw = [&](int32_t i, uint32_t word) -> int32_t {
+      const int32_t e0 = rp[i];
+      int32_t pick;
+      if (rp[i + 1] - e0 == 1) {
+        // one gated parent entry (the common case): draw_row's walk reduces to
+        // pick = j + 1 iff track j is alive and u (kappa + C) does not fall below kappa
+        const int32_t j = cl[e0];
+        const bool al = ((alive[j >> 5] >> (j & 31)) & 1u) != 0u;
+        const float tot = al ? __fadd_rn(a.kappa, vl[e0]) : a.kappa;
+        const bool hit = al && !(__fmul_rn(uniform24(word), tot) < a.kappa);
+        pick = hit ? j + 1 : 0;
+        lw += hit ? lvl[e0] : ln_kappa;
+      } else {
+        pick = draw_row(rp, cl, vl, lvl, alive, a.kappa, ln_kappa, i, word, lw);
+      }
       if (pick > 0) {
         atomicOr(det + ((pick - 1) >> 5), 1u << ((pick - 1) & 31));
         if (a.n_count > 0) atomicAdd(cnt + pick - 1, 1);
         // fingerprint over the detected rows only (theta is 0 elsewhere)
         fp += fp_term(static_cast<uint32_t>(pick), static_cast<uint64_t>(a.ldt) + i);
-        th[i] = pick;
       }
+      return pick;
     };
     if (row_mode) {
-      // thread = one row (its own Philox block: latency over issue when rows are few)
-      for (int32_t k = threadIdx.x; k < nzr_n; k += kSampThreads) {
+      // few non-empty rows per quad: theta zero-filled, then a lane per non-empty row
+      // (its quad's Philox block recomputed per row) stores its pick
+      for (int32_t t = lane; t < rquads; t += 32) {
+        if (vec_store && 4 * t + 3 < a.M) {
+          *reinterpret_cast<int4 *>(th + 4 * t) = make_int4(0, 0, 0, 0);
+        } else {
+          for (int32_t i = 4 * t; i < min(a.M, 4 * t + 4); ++i) th[i] = 0;
+        }
+      }
+      __syncwarp();   // the alive set is complete; the zeros land before the picks
+      for (int32_t k = lane; k < nzr_n; k += 32) {
         const int32_t i = nzr[k];
         const u32x4 r = philox4x32_10(u32x4{static_cast<uint32_t>(i >> 2), static_cast<uint32_t>(h), a.step,
                                             (kDomainAssoc << 24) | static_cast<uint32_t>(s)},
                                       a.key0, a.key1);
-        row(i, word_of(r, i & 3));
+        const int32_t pick = draw(i, word_of(r, i & 3));
+        if (pick > 0) th[i] = pick;
       }
     } else {
-      // thread = one quad of rows (one Philox block), its non-empty rows in turn
-      for (int32_t v = threadIdx.x; v < nzq_n; v += kSampThreads) {
+      // rows of quads without a parent entry: theta_i = 0
+      for (int32_t v = lane; v < zq_n; v += 32) {
+        const int32_t t = zq[v];
+        if (vec_store && 4 * t + 3 < a.M) {
+          *reinterpret_cast<int4 *>(th + 4 * t) = make_int4(0, 0, 0, 0);
+        } else {
+          for (int32_t i = 4 * t; i < min(a.M, 4 * t + 4); ++i) th[i] = 0;
+        }
+      }
+      __syncwarp();   // the alive set is complete
+      // a lane per non-empty row quad, its four theta entries stored at once
+      for (int32_t v = lane; v < nzq_n; v += 32) {
         const uint32_t ent = static_cast<uint32_t>(nzq[v]);
         const int32_t t = static_cast<int32_t>(ent >> 4);
         const u32x4 r = philox4x32_10(u32x4{static_cast<uint32_t>(t), static_cast<uint32_t>(h), a.step,
                                             (kDomainAssoc << 24) | static_cast<uint32_t>(s)},
                                       a.key0, a.key1);
-        for (uint32_t m = ent & 0xFu; m != 0u; m &= m - 1u) {
-          const int e = __ffs(m) - 1;
-          row(4 * t + e, word_of(r, e));
+        int32_t pk[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if ((ent >> e) & 1u) pk[e] = draw(4 * t + e, word_of(r, e));
+        if (vec_store && 4 * t + 3 < a.M) {
+          *reinterpret_cast<int4 *>(th + 4 * t) = make_int4(pk[0], pk[1], pk[2], pk[3]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (4 * t + e < a.M) th[4 * t + e] = pk[e];
         }
       }
     }
-    __syncthreads();
+    __syncwarp();   // det / cnt complete
 
     // missed detections (alive tracks with no measurement) or, with a count prior,
     // lc(n_j) for every alive track; fingerprint of the alive words
     int32_t missed = 0;
     uint32_t *al_out = a.alive + q * a.ldt;
-    for (int32_t k = threadIdx.x; k < a.ldt; k += kSampThreads) {
+    for (int32_t k = lane; k < a.ldt; k += 32) {
       const uint32_t av = alive[k];
       al_out[k] = av;
       fp += fp_term(av, static_cast<uint64_t>(k));
       if (a.n_count == 0) missed += __popc(av & ~det[k]);
     }
-    if (a.n_count > 0) {  // lc(n_j) of every alive track, a thread per parent quad
-      for (int32_t v = threadIdx.x; v < nq; v += kSampThreads) {
+    if (a.n_count > 0) {  // lc(n_j) of every alive track, a lane per parent quad
+      for (int32_t v = lane; v < nq; v += 32) {
         const int32_t t = pq[v];
         const uint32_t abits = (alive[t >> 3] >> (4 * (t & 7))) & 0xFu;
         for (uint32_t rest = abits; rest != 0u; rest &= rest - 1u)
           lw += slc[min(cnt[4 * t + __ffs(rest) - 1], a.n_count - 1)];
       }
     }
-    // one reduction round for (lw, fingerprint, missed): shuffles, one barrier, thread 0
     unsigned long long fpu = static_cast<unsigned long long>(fp);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -595,21 +633,11 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
       fpu += __shfl_xor_sync(0xffffffffu, fpu, o);
       missed += __shfl_xor_sync(0xffffffffu, missed, o);
     }
-    if ((threadIdx.x & 31) == 0) {
-      red_d[threadIdx.x >> 5] = lw;
-      red_u[threadIdx.x >> 5] = fpu;
-      red_i[threadIdx.x >> 5] = missed;
+    if (lane == 0) {
+      a.logw[q] = __ldg(a.parent_logw + h) + (lw + l_empty) + static_cast<double>(missed) * ln_miss;
+      if (a.hash) a.hash[q] = fpu;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const double lws = (red_d[0] + red_d[1]) + (red_d[2] + red_d[3]);
-      const int32_t ms = (red_i[0] + red_i[1]) + (red_i[2] + red_i[3]);
-      // rows without a parent entry: theta_i = 0 with ln kappa each
-      const int32_t n_empty = a.M - nzr_n;
-      const double l_empty = n_empty > 0 ? static_cast<double>(n_empty) * ln_kappa : 0.0;
-      a.logw[q] = __ldg(a.parent_logw + h) + (lws + l_empty) + static_cast<double>(ms) * ln_miss;
-      if (a.hash) a.hash[q] = (red_u[0] + red_u[1]) + (red_u[2] + red_u[3]);
-    }
+    __syncwarp();   // the warp's sets are reused by its next sample
   }
 }
 
@@ -833,8 +861,8 @@ __global__ void __launch_bounds__(kPruneThreads) prune_kernel(PruneArgs a) {
           int32_t above = incl - sl;  // bins above this lane's first bin
           int b = 255 - 8 * l - 7;
           int32_t rem = need - above;
-#pragma unroll
           int32_t hbb = 0;
+#pragma unroll
           for (int k = 0; k < 8; ++k) {
             if (hb[k] >= need - above) {
               b = 255 - 8 * l - k;
@@ -1006,38 +1034,40 @@ bool pdl_enabled() {
 
 cudaError_t launch_assoc_sample(const SampleArgs &a, int sm_count, cudaStream_t s) {
   SampleArgs b = a;
-  // samples per CTA: enough CTAs to fill the GPU ~8 deep, at most kSampPerCtaMax (the
-  // parent's rows are filtered once per CTA)
+  // samples per CTA (a warp draws one sample at a time): enough CTAs for ~6 per SM, at
+  // least one sample per warp, at most kSampPerCtaMax (the parent's rows are filtered once
+  // per CTA)
   static const int spc_env = [] {
     const char *e = std::getenv("GLMB_SAMPLES_PER_CTA");
     return e ? std::atoi(e) : 0;
   }();
   const int64_t total = static_cast<int64_t>(a.H_old) * a.H_up;
-  // (~8 CTAs per SM in all: measured best at both the cfg3 update and the convoy, 8
-  // samples per CTA, against 16 at ~4 CTAs per SM: -6 % and -4.5 %)
-  int64_t spc = spc_env > 0 ? spc_env : total / (static_cast<int64_t>(sm_count > 0 ? sm_count : 148) * 8);
-  b.spc = static_cast<int32_t>(spc < 1 ? 1 : spc > kSampPerCtaMax ? kSampPerCtaMax : spc);
+  const int64_t sms = sm_count > 0 ? sm_count : 148;
+  int64_t spc = spc_env > 0 ? spc_env : total / (sms * 6);
+  spc = (spc + kSampWarps - 1) / kSampWarps * kSampWarps;
+  b.spc = static_cast<int32_t>(spc < kSampWarps ? kSampWarps : spc > kSampPerCtaMax ? kSampPerCtaMax : spc);
   const int64_t groups = (a.H_up + b.spc - 1) / b.spc;
   const int64_t n = static_cast<int64_t>(a.H_old) * groups;
   const size_t tquads = (static_cast<size_t>(a.T) + 3) / 4;
-  const size_t fixed = sizeof(int32_t) * (static_cast<size_t>(a.M) + 1) + sizeof(uint32_t) * 3 * static_cast<size_t>(a.ldt) +
-                       sizeof(int32_t) * tquads + sizeof(int32_t) * ((static_cast<size_t>(a.M) + 3) / 4) +
-                       (a.M < 2 * kSampThreads ? sizeof(int32_t) * static_cast<size_t>(a.M) : 0) +
-                       (a.n_count > 0 ? (sizeof(int32_t) * static_cast<size_t>(a.T) +
-                                         sizeof(double) * static_cast<size_t>(a.n_count)) : 0) + 16;
-  if (fixed > 200 * 1024) return cudaErrorInvalidValue;
+  const size_t rquads = (static_cast<size_t>(a.M) + 3) / 4;
+  const size_t fixed = sizeof(int32_t) * (static_cast<size_t>(a.M) + 1) + sizeof(uint32_t) * static_cast<size_t>(a.ldt) +
+                       sizeof(int32_t) * tquads + 2 * sizeof(int32_t) * rquads + sizeof(int32_t) * static_cast<size_t>(a.M) +
+                       (a.n_count > 0 ? sizeof(double) * static_cast<size_t>(a.n_count) : 0) + 16;
+  const size_t warps_bytes = sizeof(uint32_t) * kSampWarps *
+                             (2 * static_cast<size_t>(a.ldt) + (a.n_count > 0 ? static_cast<size_t>(a.T) : 0));
+  if (fixed + warps_bytes + 1024 > 220 * 1024) return cudaErrorInvalidValue;
   // shared memory per CTA sized so the grid runs in one wave where it can; the pool
-  // beyond the fixed arrays holds the kept-entry bitmap, the parent's rows and the
-  // parent quads' logs, carved by the kernel
-  const int64_t sms = sm_count > 0 ? sm_count : 148;
-  const int64_t per_sm = std::min<int64_t>(16, std::max<int64_t>(1, (n + sms - 1) / sms));
-  const size_t target = std::min<size_t>(200 * 1024, (227 * 1024) / per_sm - 2048);
+  // beyond the fixed arrays holds the kept-entry bitmap, the parent's rows, the parent
+  // quads' logs and (at its end) the warps' sets, carved by the kernel
+  const int64_t per_sm = std::min<int64_t>(8, std::max<int64_t>(1, (n + sms - 1) / sms));
+  const size_t target = std::min<size_t>(220 * 1024, (227 * 1024) / per_sm - 2048);
   static const int pool_env = [] {  // test hook: force a small pool (every fallback path)
     const char *e = std::getenv("GLMB_SAMPLER_POOL");
     return e ? std::atoi(e) : 0;
   }();
-  size_t pool = target > fixed + 1024 ? (target - fixed) & ~static_cast<size_t>(15) : 1024;
-  if (pool_env > 0) pool = static_cast<size_t>(pool_env) & ~static_cast<size_t>(15);
+  size_t pool = target > fixed + warps_bytes + 1024 ? (target - fixed) & ~static_cast<size_t>(15)
+                                                    : (warps_bytes + 1024 + 15) & ~static_cast<size_t>(15);
+  if (pool_env > 0) pool = (warps_bytes + static_cast<size_t>(pool_env) + 15) & ~static_cast<size_t>(15);
   b.pool = static_cast<int32_t>(pool);
   const size_t smem = pool + fixed;
   cudaError_t e = cudaFuncSetAttribute(assoc_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
