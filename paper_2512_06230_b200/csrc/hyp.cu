@@ -192,10 +192,12 @@ __global__ void __launch_bounds__(kRowWarps * 32) rows_fill_kernel(RowsArgs a) {
 }
 
 // ------------------------------------------------------------------ two-stage sampler
-// CTA = (parent h, group of spc samples), kSampWarps warps; a WARP draws one sample at a
-// time (samples s0 + warp, s0 + warp + kSampWarps, ...) with no CTA barrier inside the
-// per-sample loop: its alive / detected sets live in the warp's own shared-memory
-// words, reductions are shuffles, and __syncwarp orders the lanes.
+// CTA = (parent h, group of 32 samples): LANE l of every warp is sample s = 32 g + l, and
+// the warps split the work items -- stage 1 the parent's track words, stage 2 the row
+// quads holding a parent entry.  Every lane of a warp thus walks the same track quad or
+// the same row at the same time (uniform control flow, the row's entries read from shared
+// memory as broadcasts); only the uniforms, and hence the alive bits and picks, differ
+// per lane.  The samples' alive / detected sets live in shared memory as [word][lane].
 constexpr int kSampWarps = 8;
 constexpr int kSampThreads = 32 * kSampWarps;
 
@@ -232,61 +234,94 @@ __device__ __forceinline__ int32_t block_excl_scan(int32_t v, int32_t *red, int3
 
 // Once per CTA: the parent's rows of C'_k -- the gated entries whose column is in the
 // parent, in ascending column order -- are filtered into shared memory (when they fit,
-// else the warps walk the global CSR), the parent's track quads are listed, and the row
-// quads are split into those holding a parent entry (with the mask of their non-empty
-// rows) and the rest.  Per sample, stage 1 visits only the parent's quads, stage 2 only
-// the non-empty rows (a lane per row when they are sparse, else per quad); the other rows
-// draw theta_i = 0 with ln kappa whatever their uniform (see draw_row) and are stored as
-// zeros.  ln P_S / ln(1 - P_S) are memoised per lane (tracks share a few P_S values).  Same
-// draws and the same fp32 operation order as a walk of the full rows (columns outside
-// the parent are never alive), so the integer outcomes do not depend on any of this.
-constexpr int kSampPerCtaMax = 64;
+// else the CTA walks the global CSR), the parent's track words are listed, and the row
+// quads holding a parent entry are listed with the mask of their non-empty rows.  The
+// other rows draw theta_i = 0 with ln kappa whatever their uniform (see draw_row) and are
+// stored as zeros.  Same draws and the same fp32 operation order as a walk of the full
+// rows (columns outside the parent are never alive), so the integer outcomes do not
+// depend on any of this.
 constexpr int kFilterBatch = 8;  // CSR words (32 entries) a warp loads per round of the row filter
 
 __device__ __forceinline__ uint32_t word_of(const u32x4 &r, int e) {
   return e == 0 ? r.a : e == 1 ? r.b : e == 2 ? r.c : r.d;
 }
 
-// Row i's categorical draw (R26): clutter kappa, then the alive gated columns
-// in ascending order; inverse CDF in fp32 with the word's 24-bit uniform.  Adds the
-// picked entry's ln value to lw and returns theta_i (0 = clutter).  An empty row draws
-// the clutter entry whatever u is (u * kappa rounds to at most kappa, and the walk past
-// it falls back to column 0 as well).
+// Row i's categorical draw for this lane's sample (R26): clutter kappa, then the
+// alive gated columns in ascending order; inverse CDF in fp32 with the word's 24-bit
+// uniform.  The entries are the same for every lane (broadcast reads); the walk visits
+// all of them without an early exit, so the control flow stays uniform across the warp.
+// Adds the picked entry's ln value to lw and returns theta_i (0 = clutter).  An empty
+// row draws the clutter entry whatever u is.  al_of(j): bit j of this lane's alive set.
+template <class AliveOf>
 __device__ __forceinline__ int32_t draw_row(const int32_t *rp, const int32_t *cl, const float *vl,
-                                            const double *lvl, const uint32_t *alive, float kappa,
+                                            const double *lvl, const AliveOf &al_of, float kappa,
                                             double ln_kappa, int32_t i, uint32_t word, double &lw) {
   const int32_t e0 = rp[i], e1 = rp[i + 1];
-  int32_t pick = 0;
-  double lpick = ln_kappa;
-  if (e0 < e1) {
+  constexpr int kShort = 4;
+  if (e1 - e0 <= kShort) {
+    // short rows (almost all): the entries in registers, both passes unrolled and predicated
+    int32_t jj[kShort];
+    float vv[kShort];
+    bool al[kShort];
+#pragma unroll
+    for (int k = 0; k < kShort; ++k) {
+      const bool in = e0 + k < e1;
+      jj[k] = in ? cl[e0 + k] : 0;
+      vv[k] = in ? vl[e0 + k] : 0.0f;
+      al[k] = in && al_of(jj[k]);
+    }
     float total = kappa;
-    for (int32_t x = e0; x < e1; ++x) {
-      const int32_t j = cl[x];
-      if ((alive[j >> 5] >> (j & 31)) & 1u) total = __fadd_rn(total, vl[x]);
-    }
+#pragma unroll
+    for (int k = 0; k < kShort; ++k)
+      if (al[k]) total = __fadd_rn(total, vv[k]);
     const float tt = __fmul_rn(uniform24(word), total);
+    bool found = !(tt >= kappa);
     float acc = kappa;
-    if (!(tt < acc)) {
-      int32_t last = 0;
-      double llast = ln_kappa;
-      pick = -1;
-      for (int32_t x = e0; x < e1; ++x) {
-        const int32_t j = cl[x];
-        if (!((alive[j >> 5] >> (j & 31)) & 1u)) continue;
-        acc = __fadd_rn(acc, vl[x]);
-        last = j + 1;
-        llast = lvl[x];
-        if (tt < acc) {
-          pick = j + 1;
-          lpick = llast;
-          break;
-        }
-      }
-      if (pick < 0) {
+    int32_t pick = 0, last = 0, kpick = -1, klast = -1;
+#pragma unroll
+    for (int k = 0; k < kShort; ++k) {
+      if (!al[k]) continue;
+      acc = __fadd_rn(acc, vv[k]);
+      last = jj[k] + 1;
+      klast = k;
+      if (!found && tt < acc) {
         pick = last;
-        lpick = llast;
+        kpick = k;
+        found = true;
       }
     }
+    if (!found) {
+      pick = last;
+      kpick = klast;
+    }
+    lw += kpick >= 0 ? lvl[e0 + kpick] : ln_kappa;
+    return pick;
+  }
+  float total = kappa;
+  for (int32_t x = e0; x < e1; ++x)
+    if (al_of(cl[x])) total = __fadd_rn(total, vl[x]);
+  const float tt = __fmul_rn(uniform24(word), total);
+  // pick = the first alive column whose running sum (from kappa) exceeds tt; if rounding
+  // leaves none although tt >= kappa, the last alive column; tt < kappa: clutter
+  int32_t pick = 0, last = 0;
+  double lpick = ln_kappa, llast = ln_kappa;
+  bool found = !(tt >= kappa);
+  float acc = kappa;
+  for (int32_t x = e0; x < e1; ++x) {
+    const int32_t j = cl[x];
+    if (!al_of(j)) continue;
+    acc = __fadd_rn(acc, vl[x]);
+    last = j + 1;
+    llast = lvl[x];
+    if (!found && tt < acc) {
+      pick = j + 1;
+      lpick = llast;
+      found = true;
+    }
+  }
+  if (!found) {
+    pick = last;
+    lpick = llast;
   }
   lw += lpick;
   return pick;
@@ -295,30 +330,39 @@ __device__ __forceinline__ int32_t draw_row(const int32_t *rp, const int32_t *cl
 __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a) {
   grid_dep_wait();
   extern __shared__ __align__(16) unsigned char smraw[];
-  // a.pool bytes at the front, carved at run time (below); fixed arrays after it
+  // a.pool bytes at the front (the kept-entry bitmap, then the parent's rows), carved
+  // at run time; fixed arrays after it
   unsigned char *pool = smraw;
   double *slc = reinterpret_cast<double *>(smraw + a.pool);            // [n_count] count prior
-  int32_t *frp = reinterpret_cast<int32_t *>(slc + max(a.n_count, 0));  // [M + 1]
-  int32_t *pq = frp + a.M + 1;                                          // [(T + 3) / 4]
-  int32_t *nzq = pq + ((a.T + 3) >> 2);                                 // [(M + 3) / 4]
-  int32_t *zq = nzq + ((a.M + 3) >> 2);                                 // [(M + 3) / 4]
-  int32_t *nzr = zq + ((a.M + 3) >> 2);                                 // [M]
-  uint32_t *pmask = reinterpret_cast<uint32_t *>(nzr + a.M);           // [ldt]
-  // per warp: alive [ldt], det [ldt], cnt [T] (count prior only)
-  const int32_t wstride = 2 * a.ldt + (a.n_count > 0 ? a.T : 0);
+  double *red_lw = slc + max(a.n_count, 0);                             // [kSampWarps][32]
+  unsigned long long *red_fp = reinterpret_cast<unsigned long long *>(red_lw + 32 * kSampWarps);  // [W][32]
+  int32_t *red_ms = reinterpret_cast<int32_t *>(red_fp + 32 * kSampWarps);  // [W][32]
+  uint32_t *alive = reinterpret_cast<uint32_t *>(red_ms + 32 * kSampWarps);  // [ldt][32]
+  uint32_t *det = alive + 32 * a.ldt;                                   // [ldt][32]
+  uint32_t *cnt = det + 32 * a.ldt;                                     // [(T+1)/2][32] u16 pairs (count prior)
+  int32_t *frp = reinterpret_cast<int32_t *>(cnt + (a.n_count > 0 ? 32 * ((a.T + 1) >> 1) : 0));  // [M + 1]
+  int32_t *nzq = frp + a.M + 1;                                         // [(M + 3) / 4]
+  int32_t *pw = nzq + ((a.M + 3) >> 2);                                 // [ldt] parent words
+  uint32_t *pmask = reinterpret_cast<uint32_t *>(pw + a.ldt);           // [ldt]
   __shared__ int32_t red_i[kSampWarps];
-  __shared__ int32_t use_smem, n_quads, n_nzq, n_zq, n_nzr;
-  const int n_groups = (a.H_up + a.spc - 1) / a.spc;
+  __shared__ int32_t use_smem, n_pw, n_nzq, n_nzr;
+  const int n_groups = (a.H_up + 31) >> 5;
   const int32_t h = static_cast<int32_t>(blockIdx.x / n_groups);
-  const int32_t s0 = static_cast<int32_t>(blockIdx.x - static_cast<int64_t>(h) * n_groups) * a.spc;
-  const int32_t s1 = min(a.H_up, s0 + a.spc);
+  const int32_t g = static_cast<int32_t>(blockIdx.x - static_cast<int64_t>(h) * n_groups);
   if (a.n_parents != nullptr && h >= __ldg(a.n_parents)) return;  // inactive parent slot
-  const uint32_t *pm = a.parent_mask + static_cast<int64_t>(h) * a.ldt;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int32_t s = 32 * g + lane;          // this lane's sample
+  const bool valid = s < a.H_up;
+  const uint32_t* pm = a.parent_mask + static_cast<int64_t>(h) * a.ldt;
   for (int32_t k = threadIdx.x; k < a.ldt; k += kSampThreads) pmask[k] = __ldg(pm + k);
   for (int32_t k = threadIdx.x; k < a.n_count; k += kSampThreads) slc[k] = __ldg(a.count_lp + k);
+  for (int32_t k = threadIdx.x; k < 32 * a.ldt; k += kSampThreads) {
+    alive[k] = 0u;
+    det[k] = 0u;
+  }
+  if (a.n_count > 0)
+    for (int32_t k = threadIdx.x; k < 32 * ((a.T + 1) >> 1); k += kSampThreads) cnt[k] = 0u;
   __syncthreads();
-  const int32_t tquads = (a.T + 3) >> 2;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   auto in_parent = [&](int32_t j) { return ((pmask[j >> 5] >> (j & 31)) & 1u) != 0u; };
 
   // ---- the parent's rows (pool), filtered in ascending column order.  A stable
@@ -327,9 +371,7 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
   // entry x's slot K(x).  Rows too many for the bitmap: a count and a fill pass per row.
   const int32_t r0 = __ldg(a.row_ptr), r1 = __ldg(a.row_ptr + a.M);
   const int32_t nwords = (r1 - r0 + 31) >> 5;
-  // the warps' sets sit at the end of the pool; the rest (avail) holds the rows and logs
-  const size_t warps_bytes = sizeof(uint32_t) * static_cast<size_t>(wstride) * kSampWarps;
-  const int64_t avail = static_cast<int64_t>(a.pool) - static_cast<int64_t>(warps_bytes);
+  const int64_t avail = a.pool;
   size_t rows_at = 0;  // pool offset of the filtered rows
   int32_t kept = 0;
   if (8 * static_cast<int64_t>(nwords) <= avail / 2) {
@@ -416,21 +458,6 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
   if (threadIdx.x == 0) use_smem = static_cast<int64_t>(rows_at + 16 * static_cast<size_t>(kept)) <= avail;
   __syncthreads();
 
-  // ---- the parent's track quads (ascending); the per-warp sets at the pool's end
-  uint32_t *wsets = reinterpret_cast<uint32_t *>(pool + a.pool - warps_bytes);
-  {
-    int32_t carry = 0;
-    for (int32_t t0 = 0; t0 < tquads; t0 += kSampThreads) {
-      const int32_t t = t0 + threadIdx.x;
-      const uint32_t qbits = t < tquads ? (pmask[t >> 3] >> (4 * (t & 7))) & 0xFu : 0u;
-      int32_t tot;
-      const int32_t ex = block_excl_scan(qbits != 0u, red_i, tot);
-      const int32_t slot = carry + ex;
-      if (qbits != 0u) pq[slot] = t;
-      carry += tot;
-    }
-    if (threadIdx.x == 0) n_quads = carry;
-  }
   const bool sm_rows = use_smem;
   const double *flv = reinterpret_cast<const double *>(pool + rows_at);
   const float *fval = reinterpret_cast<const float *>(flv + kept);
@@ -442,10 +469,19 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
   const double ln_kappa = log(static_cast<double>(a.kappa));
   const double ln_miss = log(1.0 - static_cast<double>(a.p_d));
   const int32_t rquads = (a.M + 3) >> 2;
-  // ---- row quads split into those holding a parent entry, nzq = (quad << 4 | mask of its
-  // non-empty rows), and the rest (zq: theta stored as zeros)
+  // ---- the parent's track words (ascending) and the row quads holding a parent entry
+  // (quad << 4 | mask of its non-empty rows)
   {
-    int32_t cq = 0, cz = 0, cr = 0;
+    int32_t cw = 0;
+    for (int32_t w0 = 0; w0 < a.ldt; w0 += kSampThreads) {
+      const int32_t w = w0 + threadIdx.x;
+      const bool any = w < a.ldt && pmask[w] != 0u;
+      int32_t tot;
+      const int32_t ex = block_excl_scan(any, red_i, tot);
+      if (any) pw[cw + ex] = w;
+      cw += tot;
+    }
+    int32_t cq = 0, cr = 0;
     for (int32_t t0 = 0; t0 < rquads; t0 += kSampThreads) {
       const int32_t t = t0 + threadIdx.x;
       uint32_t mask = 0u;
@@ -456,59 +492,57 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
           if (i < a.M && rp[i + 1] > rp[i]) mask |= 1u << e;
         }
       }
-      int32_t tq, tz, tr;
+      int32_t tq, tr;
       const int32_t exq = block_excl_scan(mask != 0u, red_i, tq);
-      const int32_t exz = block_excl_scan(t < rquads && mask == 0u, red_i, tz);
       const int32_t exr = block_excl_scan(__popc(mask), red_i, tr);
-      if (mask != 0u) {
-        nzq[cq + exq] = static_cast<int32_t>((static_cast<uint32_t>(t) << 4) | mask);
-        int32_t k = cr + exr;
-        for (uint32_t m = mask; m != 0u; m &= m - 1u) nzr[k++] = 4 * t + __ffs(m) - 1;
-      } else if (t < rquads) {
-        zq[cz + exz] = t;
-      }
+      (void)exr;
+      if (mask != 0u) nzq[cq + exq] = static_cast<int32_t>((static_cast<uint32_t>(t) << 4) | mask);
       cq += tq;
-      cz += tz;
       cr += tr;
     }
     if (threadIdx.x == 0) {
+      n_pw = cw;
       n_nzq = cq;
-      n_zq = cz;
       n_nzr = cr;
     }
-    __syncthreads();
   }
-  const int32_t nzq_n = n_nzq, zq_n = n_zq, nzr_n = n_nzr, nq = n_quads;
-  // a lane per non-empty row when the rows are sparse (<= 1.5 per non-empty quad: every
-  // row's draw is then one uniform body instead of four divergent ones), else per quad
-  const bool row_mode = 2 * nzr_n <= 3 * nzq_n;
+  // ---- theta rows of the CTA's samples zero-filled (coalesced); stage 2 stores the picks
   const bool vec_store = ((a.ldm & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.theta) & 15) == 0);
-  uint32_t *alive = wsets + static_cast<size_t>(wid) * wstride;
-  uint32_t *det = alive + a.ldt;
-  int32_t *cnt = reinterpret_cast<int32_t *>(det + a.ldt);
-  // rows without a parent entry: theta_i = 0 with ln kappa each
-  const int32_t n_empty = a.M - nzr_n;
-  const double l_empty = n_empty > 0 ? static_cast<double>(n_empty) * ln_kappa : 0.0;
-
-  float memo_ps = -1.0f;             // P_S of the memoised logs (none yet)
-  double memo_ls = 0.0, memo_ld = 0.0;
-  for (int32_t s = s0 + wid; s < s1; s += kSampWarps) {
-    const int64_t q = static_cast<int64_t>(h) * a.H_up + s;
-    for (int32_t k = lane; k < a.ldt; k += 32) {
-      alive[k] = 0u;
-      det[k] = 0u;
+  const int32_t n_s = min(32, a.H_up - 32 * g);
+  {
+    int32_t *th0 = a.theta + (static_cast<int64_t>(h) * a.H_up + 32 * g) * a.ldm;
+    for (int32_t ss = wid; ss < n_s; ss += kSampWarps) {   // a warp per sample row
+      int32_t *th = th0 + static_cast<int64_t>(ss) * a.ldm;
+      if (vec_store) {
+        for (int32_t t = lane; t < rquads; t += 32) {
+          if (4 * t + 3 < a.M) *reinterpret_cast<int4 *>(th + 4 * t) = make_int4(0, 0, 0, 0);
+          else for (int32_t i = 4 * t; i < a.M; ++i) th[i] = 0;
+        }
+      } else {
+        for (int32_t i = lane; i < a.M; i += 32) th[i] = 0;
+      }
     }
-    __syncwarp();
-    // stage 1: track j of the parent survives iff u_j < 1 - d_j (fp32, R25);
-    // Philox block (j/4, h, step, 2<<24 | s), word j%4 -- only quads holding parent tracks
-    double lw = 0.0;
-    for (int32_t v = lane; v < nq; v += 32) {
-      const int32_t t = pq[v];
-      const uint32_t qbits = (pmask[t >> 3] >> (4 * (t & 7))) & 0xFu;
+  }
+  __syncthreads();
+  const int32_t npw = n_pw, nzq_n = n_nzq, nzr_n = n_nzr;
+
+  // ---- stage 1: track j of the parent survives iff u_j < 1 - d_j (fp32, R25);
+  // Philox block (j/4, h, step, 2<<24 | s), word j%4.  A warp per parent word (8 quads):
+  // the word's alive bits of every lane's sample are stored once, no atomics.
+  double lw = 0.0;
+  float memo_ps = -1.0f;              // P_S of the memoised logs (none yet)
+  double memo_ls = 0.0, memo_ld = 0.0;
+  for (int32_t v = wid; v < npw; v += kSampWarps) {
+    const int32_t w = pw[v];
+    const uint32_t pbits = pmask[w];
+    uint32_t abits = 0u;
+    for (int32_t qq = 0; qq < 8; ++qq) {
+      const uint32_t qbits = (pbits >> (4 * qq)) & 0xFu;
+      if (qbits == 0u) continue;
+      const int32_t t = 8 * w + qq;
       const u32x4 r = philox4x32_10(
           u32x4{static_cast<uint32_t>(t), static_cast<uint32_t>(h), a.step, (kDomainSurvive << 24) | static_cast<uint32_t>(s)},
           a.key0, a.key1);
-      uint32_t bits = 0u;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         if (!((qbits >> e) & 1u)) continue;
@@ -516,128 +550,85 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
         const float thr = __fsub_rn(1.0f, __ldg(a.d_prob + j));
         const bool al = uniform24(word_of(r, e)) < thr;
         const float ps = __ldg(a.p_s + j);
-        if (ps != memo_ps) {  // tracks mostly share a few P_S values: logs memoised per lane
+        if (ps != memo_ps) {  // tracks mostly share a few P_S values: logs memoised (warp-uniform)
           memo_ps = ps;
           memo_ls = log(static_cast<double>(ps));
           memo_ld = log(1.0 - static_cast<double>(ps));
         }
         lw += al ? memo_ls : memo_ld;
-        bits |= static_cast<uint32_t>(al) << e;
-        if (a.n_count > 0) cnt[j] = 0;
+        abits |= static_cast<uint32_t>(al) << (4 * qq + e);
       }
-      if (bits) atomicOr(alive + (t >> 3), bits << (4 * (t & 7)));
     }
-    int32_t *th = a.theta + q * a.ldm;
-    uint64_t fp = 0ull;
-    // stage 2: each row i draws theta_i from the row of C'_k (clutter kappa,
-    // surviving gated columns in ascending order), inverse CDF in fp32 (R26);
-    // Philox block (i/4, h, step, 3<<24 | s), word i%4.  Returns theta_i; updates the
-    // log-weight, the detected set, the counts and the fingerprint.
-    auto draw = [&](int32_t i, uint32_t word) -> int32_t {
-      const int32_t e0 = rp[i];
-      int32_t pick;
-      if (rp[i + 1] - e0 == 1) {
-        // one gated parent entry (the common case): draw_row's walk reduces to
-        // pick = j + 1 iff track j is alive and u (kappa + C) does not fall below kappa
-        const int32_t j = cl[e0];
-        const bool al = ((alive[j >> 5] >> (j & 31)) & 1u) != 0u;
-        const float tot = al ? __fadd_rn(a.kappa, vl[e0]) : a.kappa;
-        const bool hit = al && !(__fmul_rn(uniform24(word), tot) < a.kappa);
-        pick = hit ? j + 1 : 0;
-        lw += hit ? lvl[e0] : ln_kappa;
-      } else {
-        pick = draw_row(rp, cl, vl, lvl, alive, a.kappa, ln_kappa, i, word, lw);
-      }
+    alive[32 * w + lane] = abits;
+  }
+  __syncthreads();   // every sample's alive set is complete
+
+  // ---- stage 2: each row i draws theta_i from the row of C'_k (clutter kappa,
+  // surviving gated columns in ascending order), inverse CDF in fp32 (R26);
+  // Philox block (i/4, h, step, 3<<24 | s), word i%4.  A warp per non-empty row quad.
+  uint64_t fp = 0ull;
+  auto al_of = [&](int32_t j) { return ((alive[32 * (j >> 5) + lane] >> (j & 31)) & 1u) != 0u; };
+  int32_t *th = a.theta + (static_cast<int64_t>(h) * a.H_up + s) * a.ldm;
+  for (int32_t v = wid; v < nzq_n; v += kSampWarps) {
+    const uint32_t ent = static_cast<uint32_t>(nzq[v]);
+    const int32_t t = static_cast<int32_t>(ent >> 4);
+    const u32x4 r = philox4x32_10(u32x4{static_cast<uint32_t>(t), static_cast<uint32_t>(h), a.step,
+                                        (kDomainAssoc << 24) | static_cast<uint32_t>(s)},
+                                  a.key0, a.key1);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (!((ent >> e) & 1u)) continue;
+      const int32_t i = 4 * t + e;
+      const int32_t pick = draw_row(rp, cl, vl, lvl, al_of, a.kappa, ln_kappa, i, word_of(r, e), lw);
       if (pick > 0) {
-        atomicOr(det + ((pick - 1) >> 5), 1u << ((pick - 1) & 31));
-        if (a.n_count > 0) atomicAdd(cnt + pick - 1, 1);
+        atomicOr(det + 32 * ((pick - 1) >> 5) + lane, 1u << ((pick - 1) & 31));
+        if (a.n_count > 0) atomicAdd(cnt + 32 * ((pick - 1) >> 1) + lane, 1u << (16 * ((pick - 1) & 1)));
         // fingerprint over the detected rows only (theta is 0 elsewhere)
         fp += fp_term(static_cast<uint32_t>(pick), static_cast<uint64_t>(a.ldt) + i);
-      }
-      return pick;
-    };
-    if (row_mode) {
-      // few non-empty rows per quad: theta zero-filled, then a lane per non-empty row
-      // (its quad's Philox block recomputed per row) stores its pick
-      for (int32_t t = lane; t < rquads; t += 32) {
-        if (vec_store && 4 * t + 3 < a.M) {
-          *reinterpret_cast<int4 *>(th + 4 * t) = make_int4(0, 0, 0, 0);
-        } else {
-          for (int32_t i = 4 * t; i < min(a.M, 4 * t + 4); ++i) th[i] = 0;
-        }
-      }
-      __syncwarp();   // the alive set is complete; the zeros land before the picks
-      for (int32_t k = lane; k < nzr_n; k += 32) {
-        const int32_t i = nzr[k];
-        const u32x4 r = philox4x32_10(u32x4{static_cast<uint32_t>(i >> 2), static_cast<uint32_t>(h), a.step,
-                                            (kDomainAssoc << 24) | static_cast<uint32_t>(s)},
-                                      a.key0, a.key1);
-        const int32_t pick = draw(i, word_of(r, i & 3));
-        if (pick > 0) th[i] = pick;
-      }
-    } else {
-      // rows of quads without a parent entry: theta_i = 0
-      for (int32_t v = lane; v < zq_n; v += 32) {
-        const int32_t t = zq[v];
-        if (vec_store && 4 * t + 3 < a.M) {
-          *reinterpret_cast<int4 *>(th + 4 * t) = make_int4(0, 0, 0, 0);
-        } else {
-          for (int32_t i = 4 * t; i < min(a.M, 4 * t + 4); ++i) th[i] = 0;
-        }
-      }
-      __syncwarp();   // the alive set is complete
-      // a lane per non-empty row quad, its four theta entries stored at once
-      for (int32_t v = lane; v < nzq_n; v += 32) {
-        const uint32_t ent = static_cast<uint32_t>(nzq[v]);
-        const int32_t t = static_cast<int32_t>(ent >> 4);
-        const u32x4 r = philox4x32_10(u32x4{static_cast<uint32_t>(t), static_cast<uint32_t>(h), a.step,
-                                            (kDomainAssoc << 24) | static_cast<uint32_t>(s)},
-                                      a.key0, a.key1);
-        int32_t pk[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if ((ent >> e) & 1u) pk[e] = draw(4 * t + e, word_of(r, e));
-        if (vec_store && 4 * t + 3 < a.M) {
-          *reinterpret_cast<int4 *>(th + 4 * t) = make_int4(pk[0], pk[1], pk[2], pk[3]);
-        } else {
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if (4 * t + e < a.M) th[4 * t + e] = pk[e];
-        }
+        if (valid) th[i] = pick;
       }
     }
-    __syncwarp();   // det / cnt complete
+  }
+  __syncthreads();   // det / cnt complete
 
-    // missed detections (alive tracks with no measurement) or, with a count prior,
-    // lc(n_j) for every alive track; fingerprint of the alive words
-    int32_t missed = 0;
-    uint32_t *al_out = a.alive + q * a.ldt;
-    for (int32_t k = lane; k < a.ldt; k += 32) {
-      const uint32_t av = alive[k];
-      al_out[k] = av;
-      fp += fp_term(av, static_cast<uint64_t>(k));
-      if (a.n_count == 0) missed += __popc(av & ~det[k]);
-    }
-    if (a.n_count > 0) {  // lc(n_j) of every alive track, a lane per parent quad
-      for (int32_t v = lane; v < nq; v += 32) {
-        const int32_t t = pq[v];
-        const uint32_t abits = (alive[t >> 3] >> (4 * (t & 7))) & 0xFu;
-        for (uint32_t rest = abits; rest != 0u; rest &= rest - 1u)
-          lw += slc[min(cnt[4 * t + __ffs(rest) - 1], a.n_count - 1)];
+  // ---- missed detections (alive tracks with no measurement) or, with a count prior,
+  // lc(n_j) for every alive track; fingerprint of the alive words; alive words out
+  int32_t missed = 0;
+  uint32_t *al_out = a.alive + (static_cast<int64_t>(h) * a.H_up + s) * a.ldt;
+  for (int32_t k = wid; k < a.ldt; k += kSampWarps) {
+    const uint32_t av = alive[32 * k + lane];
+    if (valid) al_out[k] = av;
+    fp += fp_term(av, static_cast<uint64_t>(k));
+    if (a.n_count == 0) {
+      missed += __popc(av & ~det[32 * k + lane]);
+    } else {
+      for (uint32_t rest = av; rest != 0u; rest &= rest - 1u) {
+        const int32_t j = 32 * k + __ffs(rest) - 1;
+        const uint32_t n = (cnt[32 * (j >> 1) + lane] >> (16 * (j & 1))) & 0xFFFFu;
+        lw += slc[min(static_cast<int32_t>(n), a.n_count - 1)];
       }
     }
-    unsigned long long fpu = static_cast<unsigned long long>(fp);
+  }
+  red_lw[32 * wid + lane] = lw;
+  red_fp[32 * wid + lane] = static_cast<unsigned long long>(fp);
+  red_ms[32 * wid + lane] = missed;
+  __syncthreads();
+  if (wid == 0 && valid) {
+    double lws = 0.0;
+    unsigned long long fps = 0ull;
+    int32_t ms = 0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      lw += __shfl_xor_sync(0xffffffffu, lw, o);
-      fpu += __shfl_xor_sync(0xffffffffu, fpu, o);
-      missed += __shfl_xor_sync(0xffffffffu, missed, o);
+    for (int w = 0; w < kSampWarps; ++w) {
+      lws += red_lw[32 * w + lane];
+      fps += red_fp[32 * w + lane];
+      ms += red_ms[32 * w + lane];
     }
-    if (lane == 0) {
-      a.logw[q] = __ldg(a.parent_logw + h) + (lw + l_empty) + static_cast<double>(missed) * ln_miss;
-      if (a.hash) a.hash[q] = fpu;
-    }
-    __syncwarp();   // the warp's sets are reused by its next sample
+    // rows without a parent entry: theta_i = 0 with ln kappa each
+    const int32_t n_empty = a.M - nzr_n;
+    const double l_empty = n_empty > 0 ? static_cast<double>(n_empty) * ln_kappa : 0.0;
+    const int64_t q = static_cast<int64_t>(h) * a.H_up + s;
+    a.logw[q] = __ldg(a.parent_logw + h) + (lws + l_empty) + static_cast<double>(ms) * ln_miss;
+    if (a.hash) a.hash[q] = fps;
   }
 }
 
@@ -1034,40 +1025,28 @@ bool pdl_enabled() {
 
 cudaError_t launch_assoc_sample(const SampleArgs &a, int sm_count, cudaStream_t s) {
   SampleArgs b = a;
-  // samples per CTA (a warp draws one sample at a time): enough CTAs for ~6 per SM, at
-  // least one sample per warp, at most kSampPerCtaMax (the parent's rows are filtered once
-  // per CTA)
-  static const int spc_env = [] {
-    const char *e = std::getenv("GLMB_SAMPLES_PER_CTA");
-    return e ? std::atoi(e) : 0;
-  }();
-  const int64_t total = static_cast<int64_t>(a.H_old) * a.H_up;
-  const int64_t sms = sm_count > 0 ? sm_count : 148;
-  int64_t spc = spc_env > 0 ? spc_env : total / (sms * 6);
-  spc = (spc + kSampWarps - 1) / kSampWarps * kSampWarps;
-  b.spc = static_cast<int32_t>(spc < kSampWarps ? kSampWarps : spc > kSampPerCtaMax ? kSampPerCtaMax : spc);
-  const int64_t groups = (a.H_up + b.spc - 1) / b.spc;
+  b.spc = 32;   // samples per CTA: one per lane
+  const int64_t groups = (a.H_up + 31) / 32;
   const int64_t n = static_cast<int64_t>(a.H_old) * groups;
-  const size_t tquads = (static_cast<size_t>(a.T) + 3) / 4;
-  const size_t rquads = (static_cast<size_t>(a.M) + 3) / 4;
-  const size_t fixed = sizeof(int32_t) * (static_cast<size_t>(a.M) + 1) + sizeof(uint32_t) * static_cast<size_t>(a.ldt) +
-                       sizeof(int32_t) * tquads + 2 * sizeof(int32_t) * rquads + sizeof(int32_t) * static_cast<size_t>(a.M) +
-                       (a.n_count > 0 ? sizeof(double) * static_cast<size_t>(a.n_count) : 0) + 16;
-  const size_t warps_bytes = sizeof(uint32_t) * kSampWarps *
-                             (2 * static_cast<size_t>(a.ldt) + (a.n_count > 0 ? static_cast<size_t>(a.T) : 0));
-  if (fixed + warps_bytes + 1024 > 220 * 1024) return cudaErrorInvalidValue;
+  const size_t fixed =
+      sizeof(double) * static_cast<size_t>(max(a.n_count, 0)) +
+      (sizeof(double) + sizeof(unsigned long long) + sizeof(int32_t)) * 32 * kSampWarps +
+      sizeof(uint32_t) * 32 * 2 * static_cast<size_t>(a.ldt) +
+      (a.n_count > 0 ? sizeof(uint32_t) * 32 * ((static_cast<size_t>(a.T) + 1) / 2) : 0) +
+      sizeof(int32_t) * (static_cast<size_t>(a.M) + 1) + sizeof(int32_t) * ((static_cast<size_t>(a.M) + 3) / 4) +
+      2 * sizeof(uint32_t) * static_cast<size_t>(a.ldt) + 16;
+  if (fixed + 1024 > 220 * 1024) return cudaErrorInvalidValue;
   // shared memory per CTA sized so the grid runs in one wave where it can; the pool
-  // beyond the fixed arrays holds the kept-entry bitmap, the parent's rows, the parent
-  // quads' logs and (at its end) the warps' sets, carved by the kernel
+  // beyond the fixed arrays holds the kept-entry bitmap and the parent's rows
+  const int64_t sms = sm_count > 0 ? sm_count : 148;
   const int64_t per_sm = std::min<int64_t>(8, std::max<int64_t>(1, (n + sms - 1) / sms));
   const size_t target = std::min<size_t>(220 * 1024, (227 * 1024) / per_sm - 2048);
   static const int pool_env = [] {  // test hook: force a small pool (every fallback path)
     const char *e = std::getenv("GLMB_SAMPLER_POOL");
     return e ? std::atoi(e) : 0;
   }();
-  size_t pool = target > fixed + warps_bytes + 1024 ? (target - fixed) & ~static_cast<size_t>(15)
-                                                    : (warps_bytes + 1024 + 15) & ~static_cast<size_t>(15);
-  if (pool_env > 0) pool = (warps_bytes + static_cast<size_t>(pool_env) + 15) & ~static_cast<size_t>(15);
+  size_t pool = target > fixed + 1024 ? (target - fixed) & ~static_cast<size_t>(15) : 1024;
+  if (pool_env > 0) pool = static_cast<size_t>(pool_env) & ~static_cast<size_t>(15);
   b.pool = static_cast<int32_t>(pool);
   const size_t smem = pool + fixed;
   cudaError_t e = cudaFuncSetAttribute(assoc_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
