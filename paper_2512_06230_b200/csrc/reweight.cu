@@ -6,14 +6,16 @@
 //   m = max_p l_p,  s = sum_p 2^(l_p - m),  w'_p = 2^(l_p - m) / s
 //   log_norm_j = (m + log2 s) ln 2 - |S_j| ln(2 pi sqrt(det R))
 //
-// One CTA (256 threads) per track.  HBM-bound: x, y, w are read once and w
-// written once (16 B per particle).  The exponent l_p is accumulated in fp64
-// (a handful of DFMA per particle-measurement, negligible next to the HBM
-// time) so the max-shift l_p - m keeps full relative accuracy even when the
-// assigned measurement is far from the cloud; 2^(l-m) itself is fp32 MUFU.
-// Particles are cached in registers (R float4 quads per thread, P <= 1024 R)
-// so the two passes (block max, then block sum) read HBM once; larger P uses
-// the generic path that recomputes l_p in the second pass.
+// HBM-bound: x, y, w are read once and w written once (16 B per particle).
+// Launch variants by P (shape depends on P only: shard-invariant results):
+//  * 2048 <= P <= 25600: the e-cache kernel (reweight_ecache_unit below): the
+//    centred quadratic form (O(1) per particle for any |S_j|), an fp32 pass with
+//    a checked error budget and an fp64 rerun otherwise, e_p parked in shared
+//    memory between the two passes;
+//  * smaller P: thread-block clusters holding the particles in registers;
+//  * larger P: the generic path recomputing l_p (fp64) in the second pass.
+// Where l_p is fp64 the max shift l_p - m keeps full relative accuracy even when
+// the assigned measurement is far from the cloud; 2^(l-m) itself is fp32 MUFU.
 // Block reductions run in a fixed order -> deterministic, shard-invariant.
 #include <cfloat>
 #include <cstdlib>
@@ -28,6 +30,9 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+#ifndef GLMB_RW_ECACHE_BLOCKS
+#define GLMB_RW_ECACHE_BLOCKS 4
+#endif
 constexpr int kSCap = 256;   // assigned measurements held in shared memory (more: global rescan)
 
 struct SList {
@@ -59,21 +64,23 @@ __device__ void collect_S_pair(const ReweightArgs &a, int k, SList &S) {
 // masks -- already in ascending-i order -- into list positions with a
 // warp-shuffle prefix sum and fetches the hit measurements.
 constexpr int kRows = 8;
-__device__ void collect_S(const ReweightArgs &a, int col, SList &S, uint32_t *masks /* [kRows * kWarps] */) {
-  static_assert(kRows * kWarps == 64, "warp 0 scans two masks per lane");
+template <int NT = kThreads>
+__device__ void collect_S(const ReweightArgs &a, int col, SList &S, uint32_t *masks /* [64] */) {
+  constexpr int kW = NT / 32, kR = 64 / kW;  // kR rows of NT indices per chunk: 64 (row, warp) masks
+  static_assert(kR * kW == 64, "warp 0 scans two masks per lane");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int total = 0;  // maintained by warp 0
-  for (int base = 0; base < a.M; base += kRows * kThreads) {
-    int th[kRows];
+  for (int base = 0; base < a.M; base += kR * NT) {
+    int th[kR];
 #pragma unroll
-    for (int r = 0; r < kRows; ++r) {
-      const int i = base + r * kThreads + threadIdx.x;
+    for (int r = 0; r < kR; ++r) {
+      const int i = base + r * NT + threadIdx.x;
       th[r] = i < a.M ? __ldg(a.theta + i) : -1;
     }
 #pragma unroll
-    for (int r = 0; r < kRows; ++r) {
+    for (int r = 0; r < kR; ++r) {
       const uint32_t m = __ballot_sync(0xffffffffu, th[r] == col);
-      if (lane == 0) masks[r * kWarps + warp] = m;
+      if (lane == 0) masks[r * kW + warp] = m;
     }
     __syncthreads();
     if (warp == 0) {
@@ -670,6 +677,304 @@ __global__ void __launch_bounds__(kThreads, 3) reweight_flat_kernel(const Reweig
   for (int u = blockIdx.x; u < n_units; u += gridDim.x) reweight_flat_unit<LC>(a, u);
 }
 
+// E-cache variant (the default for 2048 <= P <= 25600): one 256-thread CTA per unit, 4
+// per SM (62 registers: the fp32 pass keeps two quads of loads in flight).  (1) When S_j fits in shared memory, sum_{s in S} q'(z_s - p) is evaluated as
+// C0 + n q'(zbar - p) (zbar the mean of S_j's measurements, C0 = sum q'(z_s - zbar): the
+// cross terms vanish), so every particle costs one fp64 quadratic form whatever |S_j| is;
+// C0 is added back into log_norm only.  (2) Pass 1 parks e_p = 2^(l_p - m_t) in fp32 in
+// shared memory (4 B per particle), m_t being the thread's running max (fp64), and
+// rescales the thread's parked entries whenever a quad raises it; pass 2 writes
+// w'_p = e_p 2^(m_t - m) / s from shared memory.  Pass 1 runs in fp32 (ecache_pass1_f32)
+// and is kept when the unit's max shows every weight that matters is inside the fp32
+// error budget; otherwise (far measurements, tiny weights, S_j past shared memory) it is
+// rerun with l_p in fp64, so the max shift keeps full accuracy.
+//
+// Pass 1 of the e-cache variant: per quad l_p (fp64; CENTRED: the centred quadratic form,
+// else the general per-measurement loop); the thread's running max m rises to the quad's
+// max (its parked e's, s and s2 rescaled by 2^(m_old - m_new)); e_p parked in shared memory.
+template <bool CENTRED>
+__device__ __forceinline__ void ecache_pass1(const ReweightArgs &a, const SList &S, int col, const float4 *xs,
+                                             const float4 *ys, const float4 *ws, float4 *e4, int quads, float4 X,
+                                             float4 Y, float4 W, const double *cq, double &m, float &sm,
+                                             float &sm2) {
+  int g = threadIdx.x;
+#pragma unroll 1
+  for (; g < quads; g += kThreads) {
+    if (g != static_cast<int>(threadIdx.x)) {   // the first quad was loaded before the S scan
+      X = __ldg(xs + g);
+      Y = __ldg(ys + g);
+      W = __ldg(ws + g);
+    }
+    double l[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float px = q4(X, q), py = q4(Y, q), w = q4(W, q);
+      if constexpr (CENTRED) {   // the unit's constants re-read from shared memory (registers are scarce)
+        const double dx = cq[0] - static_cast<double>(px), dy = cq[1] - static_cast<double>(py);
+        const double lw = w > 0.f ? static_cast<double>(__log2f(w)) : -INFINITY;
+        l[q] = lw - fma(dx, fma(cq[2], dx, cq[3] * dy), cq[4] * dy * dy);
+      } else {
+        l[q] = log_weight(a, S, col, px, py, w);
+      }
+    }
+    const double lq = fmax(fmax(l[0], l[1]), fmax(l[2], l[3]));
+    if (lq > m) {
+      if (m != -INFINITY) {
+        const float f = ex2_approx(static_cast<float>(m - lq));
+        sm *= f;
+        sm2 *= f * f;
+        for (int gp = threadIdx.x; gp < g; gp += kThreads) {
+          float4 e = e4[gp];
+          e.x *= f;
+          e.y *= f;
+          e.z *= f;
+          e.w *= f;
+          e4[gp] = e;
+        }
+      }
+      m = lq;
+    }
+    float4 e;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) q4(e, q) = l[q] == -INFINITY ? 0.0f : ex2_approx(static_cast<float>(l[q] - m));
+    sm += (e.x + e.y) + (e.z + e.w);
+    sm2 = fmaf(e.x, e.x, fmaf(e.y, e.y, fmaf(e.z, e.z, fmaf(e.w, e.w, sm2))));
+    e4[g] = e;
+  }
+}
+
+// Fast pass 1 of the e-cache variant, all fp32 (MUFU.LG2 + MUFU.EX2 per particle, no
+// fp64 conversions): d = (p - zhi) - zlo with zbar = zhi + zlo split into two floats
+// (p - zhi is exact by Sterbenz for nearby coordinates), q' = n d^T A d in fp32.  Its
+// error is ~q' 2^-22; a weight matters only if l_p >= m - 100 (below that 2^(l - m) <
+// 1e-30, the absolute tolerance), i.e. q' <= 100 - m, so once the unit's max m >= -300
+// every weight that matters has q' <= 400 and a relative error <= 1e-4 / 2 -- the caller
+// checks that and otherwise reruns pass 1 in fp64 (far measurements, tiny weights).
+// The thread's running max starts at the warp's max over the first quads.
+__device__ __forceinline__ void ecache_pass1_f32(const float4 *xs, const float4 *ys, const float4 *ws, float4 *e4,
+                                                 int quads, float4 X, float4 Y, float4 W, const float *c32,
+                                                 float &m, float &sm, float &sm2) {
+  const float zhx = c32[0], zlx = c32[1], zhy = c32[2], zly = c32[3], na = c32[4], nb = c32[5], nc = c32[6];
+  bool first = true;   // quads >= kThreads (P >= 1024): every lane has a first quad
+  // two quads in flight ahead of the one computed (the loads of one thread are a serial
+  // chain otherwise: one quad of prefetch left each iteration waiting on memory latency)
+  float4 Xn, Yn, Wn, Xm, Ym, Wm;
+  if (static_cast<int>(threadIdx.x) + kThreads < quads) {
+    Xn = __ldg(xs + threadIdx.x + kThreads);
+    Yn = __ldg(ys + threadIdx.x + kThreads);
+    Wn = __ldg(ws + threadIdx.x + kThreads);
+  }
+#pragma unroll 1
+  for (int g = threadIdx.x; g < quads; g += kThreads) {
+    const int gm = g + 2 * kThreads;
+    if (gm < quads) {
+      Xm = __ldg(xs + gm);
+      Ym = __ldg(ys + gm);
+      Wm = __ldg(ws + gm);
+    }
+    float l[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float dx = (q4(X, q) - zhx) - zlx, dy = (q4(Y, q) - zhy) - zly;
+      const float w = q4(W, q);
+      l[q] = w > 0.f ? __log2f(w) - fmaf(dx, fmaf(na, dx, nb * dy), nc * dy * dy) : -INFINITY;
+    }
+    const float lq = fmaxf(fmaxf(l[0], l[1]), fmaxf(l[2], l[3]));
+    if (first) {
+      float wm = lq;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+      m = wm;
+      first = false;
+    }
+    if (lq > m) {
+      if (m != -INFINITY) {
+        const float f = ex2_approx(m - lq);
+        sm *= f;
+        sm2 *= f * f;
+        for (int gp = threadIdx.x; gp < g; gp += kThreads) {
+          float4 e = e4[gp];
+          e.x *= f;
+          e.y *= f;
+          e.z *= f;
+          e.w *= f;
+          e4[gp] = e;
+        }
+      }
+      m = lq;
+    }
+    float4 e;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) q4(e, q) = l[q] == -INFINITY ? 0.0f : ex2_approx(l[q] - m);
+    sm += (e.x + e.y) + (e.z + e.w);
+    sm2 = fmaf(e.x, e.x, fmaf(e.y, e.y, fmaf(e.z, e.z, fmaf(e.w, e.w, sm2))));
+    e4[g] = e;
+    X = Xn;
+    Y = Yn;
+    W = Wn;
+    Xn = Xm;
+    Yn = Ym;
+    Wn = Wm;
+  }
+}
+
+__device__ __forceinline__ void reweight_ecache_unit(const ReweightArgs &a, const int u) {
+  extern __shared__ __align__(16) float ec[];  // [P] e_p
+  __shared__ SList S;
+  __shared__ double red[3][kWarps];
+  __shared__ uint32_t masks[kRows * kWarps];
+  __shared__ double bc[3];
+  __shared__ double cq[6];   // zbar x, y; n qa, n qb, n qc; C0
+  __shared__ float c32[7];   // zbar split into (hi, lo) floats for x and y; n qa, n qb, n qc
+  const bool pairs = a.pair_track != nullptr;
+  const int j = pairs ? __ldg(a.pair_track + u) : u;
+  const int col = a.col_offset + j + 1;
+  const int64_t base = static_cast<int64_t>(j) * a.ld;
+  const float4 *xs = reinterpret_cast<const float4 *>(a.x + base);
+  const float4 *ys = reinterpret_cast<const float4 *>(a.y + base);
+  const float4 *ws = reinterpret_cast<const float4 *>(a.w + base);
+  float4 *wo = reinterpret_cast<float4 *>(a.w_out + static_cast<int64_t>(u) * a.ld_out);
+  float4 *e4 = reinterpret_cast<float4 *>(ec);
+  const bool copy_out = pairs || a.w_out != a.w;
+  const int quads = a.P >> 2;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // the first quad's loads are issued before the S scan, so the two latencies overlap
+  float4 X0, Y0, W0;
+  if (static_cast<int>(threadIdx.x) < quads) {
+    X0 = __ldg(xs + threadIdx.x);
+    Y0 = __ldg(ys + threadIdx.x);
+    W0 = __ldg(ws + threadIdx.x);
+  }
+  if (pairs) collect_S_pair(a, u, S);
+  else collect_S(a, col, S, masks);
+  const int nS = S.n;
+
+  if (nS == 0) {  // untouched; log_norm = ln sum w; ESS = (sum w)^2 / sum w^2
+    double sw = 0.0, sw2 = 0.0;
+    for (int g = threadIdx.x; g < quads; g += kThreads) {
+      const float4 w4 = __ldcs(ws + g);
+      if (copy_out) __stcs(wo + g, w4);
+      sw += (static_cast<double>(w4.x) + w4.y) + (static_cast<double>(w4.z) + w4.w);
+      sw2 += (static_cast<double>(w4.x) * w4.x + static_cast<double>(w4.y) * w4.y) +
+             (static_cast<double>(w4.z) * w4.z + static_cast<double>(w4.w) * w4.w);
+    }
+    sw = block_sum(sw, red[0]);
+    if (a.ess != nullptr) sw2 = block_sum(sw2, red[1]);
+    if (threadIdx.x == 0) {
+      a.log_norm[u] = static_cast<float>(log(sw));
+      a.flags[u] = 0u;
+      if (a.ess != nullptr) a.ess[u] = sw2 > 0.0 ? static_cast<float>(sw * sw / sw2) : 0.0f;
+    }
+    __syncthreads();
+    return;
+  }
+  const bool centred = S.in_smem;
+  if (centred && threadIdx.x == 0) {
+    double sx = 0.0, sy = 0.0;
+    for (int k = 0; k < nS; ++k) {
+      sx += S.z[k].x;
+      sy += S.z[k].y;
+    }
+    const double zx = sx / nS, zy = sy / nS;
+    double c0 = 0.0;
+    for (int k = 0; k < nS; ++k) c0 += qform(a, S.z[k].x, S.z[k].y, zx, zy);
+    cq[0] = zx;
+    cq[1] = zy;
+    cq[2] = nS * a.qa;
+    cq[3] = nS * a.qb;
+    cq[4] = nS * a.qc;
+    cq[5] = c0;
+    const float hx = static_cast<float>(zx), hy = static_cast<float>(zy);
+    c32[0] = hx;
+    c32[1] = static_cast<float>(zx - hx);
+    c32[2] = hy;
+    c32[3] = static_cast<float>(zy - hy);
+    c32[4] = static_cast<float>(cq[2]);
+    c32[5] = static_cast<float>(cq[3]);
+    c32[6] = static_cast<float>(cq[4]);
+  }
+  __syncthreads();
+  // warp: max by shuffles, the lanes' sums rescaled to it; CTA: thread 0 merges the warps
+  auto merge = [&](double m, float sm, float sm2) {
+    const double mw = warp_max_d(m);
+    const double f = mw == -INFINITY || m == -INFINITY ? 0.0 : static_cast<double>(ex2_approx(static_cast<float>(m - mw)));
+    double sw = warp_sum_d(static_cast<double>(sm) * f),
+           sw2 = a.ess != nullptr ? warp_sum_d(static_cast<double>(sm2) * (f * f)) : 0.0;
+    if (lane == 0) {
+      red[0][warp] = mw;
+      red[1][warp] = sw;
+      red[2][warp] = sw2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double mb = red[0][0], sb = red[1][0], s2b = red[2][0];
+#pragma unroll
+      for (int k = 1; k < kWarps; ++k) ms_merge(mb, sb, s2b, red[0][k], red[1][k], red[2][k]);
+      bc[0] = mb;
+      bc[1] = sb;
+      bc[2] = s2b;
+    }
+    __syncthreads();
+  };
+  // pass 1: fp32 when the centred form applies, kept when the unit's max shows every weight
+  // that matters is within the fp32 error budget (see ecache_pass1_f32); else fp64
+  double m = -INFINITY;
+  float sm = 0.0f, sm2 = 0.0f;
+  bool fp64 = !centred;
+  if (centred) {
+    float m32 = -INFINITY;
+    ecache_pass1_f32(xs, ys, ws, e4, quads, X0, Y0, W0, c32, m32, sm, sm2);
+    m = m32;
+    merge(m, sm, sm2);
+    fp64 = bc[0] != -INFINITY && bc[0] < -300.0;
+    __syncthreads();   // every thread has read bc before a rerun overwrites it
+  }
+  if (fp64) {
+    m = -INFINITY;
+    sm = sm2 = 0.0f;
+    if (static_cast<int>(threadIdx.x) < quads) {
+      X0 = __ldg(xs + threadIdx.x);
+      Y0 = __ldg(ys + threadIdx.x);
+      W0 = __ldg(ws + threadIdx.x);
+    }
+    if (centred) ecache_pass1<true>(a, S, col, xs, ys, ws, e4, quads, X0, Y0, W0, cq, m, sm, sm2);
+    else ecache_pass1<false>(a, S, col, xs, ys, ws, e4, quads, X0, Y0, W0, cq, m, sm, sm2);
+    merge(m, sm, sm2);
+  }
+  const double mc = bc[0], sc = bc[1], s2c = bc[2];
+  if (mc == -INFINITY) {  // every weight zero: uniform reset, flagged (never abort)
+    const float uw = 1.0f / static_cast<float>(a.P);
+    for (int g = threadIdx.x; g < quads; g += kThreads) __stcs(wo + g, make_float4(uw, uw, uw, uw));
+    if (threadIdx.x == 0) {
+      a.log_norm[u] = -INFINITY;
+      a.flags[u] = 1u;
+      if (a.ess != nullptr) a.ess[u] = static_cast<float>(a.P);
+    }
+    __syncthreads();
+    return;
+  }
+  // pass 2: w'_p = e_p 2^(m_t - m) / s from the thread's own parked entries
+  const float ft = m == -INFINITY ? 0.0f : ex2_approx(static_cast<float>(m - mc)) * static_cast<float>(1.0 / sc);
+  for (int g = threadIdx.x; g < quads; g += kThreads) {
+    const float4 e = e4[g];
+    __stcs(wo + g, make_float4(e.x * ft, e.y * ft, e.z * ft, e.w * ft));
+  }
+  if (threadIdx.x == 0) {
+    const double ln2 = 0.69314718055994530942;
+    const double c0 = centred ? cq[5] : 0.0;   // the centred form's constant term
+    a.log_norm[u] = static_cast<float>((mc - c0 + log2(sc)) * ln2 - nS * a.log_norm1);
+    a.flags[u] = 0u;
+    if (a.ess != nullptr) a.ess[u] = static_cast<float>(sc * sc / s2c);
+  }
+  __syncthreads();  // S, red, bc and cq are reused by the next unit
+}
+
+__global__ void __launch_bounds__(kThreads, GLMB_RW_ECACHE_BLOCKS) reweight_ecache_kernel(const ReweightArgs a) {
+  grid_dep_wait();
+  const int n_units = a.n_units_dev != nullptr ? min(a.T, __ldg(a.n_units_dev)) : a.T;
+  for (int u = blockIdx.x; u < n_units; u += gridDim.x) reweight_ecache_unit(a, u);
+}
+
 template <int CL, int R>
 cudaError_t launch_cluster(const ReweightArgs &a, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
@@ -703,8 +1008,26 @@ cudaError_t launch_reweight(const ReweightArgs &a, cudaStream_t s) {
     const char *e = std::getenv("GLMB_REWEIGHT_FLAT");
     return e ? std::atoi(e) : -1;
   }();
-  const bool flat_default = flat_env < 0 && a.P >= 2048 && static_cast<size_t>(a.P) * 8 <= kMaxCacheBytes;
-  if (flat_env == 1 || flat_env == 2 || flat_default) {
+  const bool ecache_ok = a.P >= 4 * kThreads && static_cast<size_t>(a.P) * 4 <= kMaxCacheBytes;
+  const bool ecache_default = flat_env < 0 && a.P >= 2048 && ecache_ok;
+  if ((flat_env == 3 && ecache_ok) || ecache_default) {
+    const int units = a.units_cap > 0 ? min(a.T, a.units_cap) : a.T;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(units));
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = s;
+    cfg.dynamicSmemBytes = static_cast<size_t>(a.P) * 4;
+    cudaError_t e = cudaFuncSetAttribute(reweight_ecache_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kMaxCacheBytes);
+    if (e != cudaSuccess) return e;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = (a.pair_track != nullptr && pdl_enabled()) ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, reweight_ecache_kernel, a);
+  }
+  if (flat_env == 1 || flat_env == 2) {
     const int units = a.units_cap > 0 ? min(a.T, a.units_cap) : a.T;
     const bool lcache = flat_env != 1 && static_cast<size_t>(a.P) * 8 <= kMaxCacheBytes;
     cudaLaunchConfig_t cfg = {};
