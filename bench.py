@@ -58,7 +58,6 @@ def parse():
     ap.add_argument("--no-convoy", action="store_true", help="skip the paper-shaped convoy run (f4)")
     ap.add_argument("--no-graphs", action="store_true", help="skip the CUDA-graph timing of configs 0-2")
     ap.add_argument("--no-skip-probe", action="store_true", help="skip the exact zero-tile skipping probe")
-    ap.add_argument("--compat-probe", type=int, default=None, help=argparse.SUPPRESS)  # child: predicts
     return ap.parse_args()
 
 
@@ -361,54 +360,54 @@ def make_line(*, cfg_id, cfg, world, steps, warmup, elapsed_ms, evals_total, pai
 
 
 # ------------------------------------------------------------------ GLMB update
-def compat_probe_child(cfg_id: int, n_pred: int, reps: int = 10) -> None:
-    """Child process of skip_probe: glmb_compat on config cfg_id after n_pred predicts, mean
-    launch time over `reps` (CUDA events) and a checksum of C and the gate words."""
-    import hashlib
+def skip_probe(st, dev, L, reps: int = 10) -> dict:
+    """Exact zero-tile skipping (glmb_compat_skipping, opt-in, not the headline): compat dense and
+    skipping on the step-0 clouds (a fresh copy of the scene, births drawn) and on the bench's
+    own state after its timed steps (diffused clouds), CUDA-event means over `reps` launches;
+    evaluated pairs = dense pairs - the device count of skipped pairs, with their rate against
+    the same combined exp-pipe bound as the headline; bit-identity of C and the gate words.
+    late_state = the bench's particles after its timed and end-to-end steps (diffused clouds)."""
     import torch
-    from paper_2512_06230_b200 import _lib as L
-    from paper_2512_06230_b200.scenes import make_scene
     from paper_2512_06230_b200.step import GlmbStep
-    torch.cuda.set_device(0)
-    L.glmb_init(0)
-    sc = make_scene(cfg_id, steps=1)
-    st = GlmbStep(sc, device="cuda:0")
-    for k in range(n_pred):
-        st.predict(k)
-    for _ in range(2):
-        st.compat(0)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
-        st.compat(0)
-    e1.record()
-    torch.cuda.synchronize()
-    M = len(sc.Z[0])
-    h = hashlib.sha256(st.out.C_tracks[:, :M].cpu().numpy().tobytes() + st.out.gate.cpu().numpy().tobytes())
-    print(json.dumps({"ms": e0.elapsed_time(e1) / reps, "sha": h.hexdigest()[:16]}), flush=True)
-
-
-def skip_probe(cfg_id: int) -> dict:
-    """Exact zero-tile skipping (GLMB_COMPAT_SKIP=1, opt-in, not the headline): compat with and
-    without it on the step-0 clouds and after 25 predicts (the timed steps' diffused clouds),
-    each setting in its own process; bit-identity by checksum of C and the gate words."""
-    import subprocess
-    out = {"note": "GLMB_COMPAT_SKIP=1: a warp skips a particle tile when all its measurements are >= 200 "
-                   "whitened units^2 from the tile's bounding box (contributions exactly +0 on both exp "
-                   "paths); opt-in, the headline is the dense pass"}
-    for pred in (0, 25):
-        r = {}
-        for skip in ("0", "1"):
-            env = dict(os.environ, GLMB_COMPAT_SKIP=skip)
-            p = subprocess.run([sys.executable, os.path.abspath(__file__), "--compat-probe", str(pred),
-                                "--config", str(cfg_id)], env=env, capture_output=True, text=True, timeout=600)
-            line = [l for l in p.stdout.splitlines() if l.startswith("{")]
-            if p.returncode != 0 or not line:
-                return {"error": (p.stderr or p.stdout)[-300:]}
-            r[skip] = json.loads(line[-1])
-        out[f"pred{pred}"] = {"dense_ms": r["0"]["ms"], "skip_ms": r["1"]["ms"],
-                              "speedup": r["0"]["ms"] / r["1"]["ms"], "bit_identical": r["0"]["sha"] == r["1"]["sha"]}
+    fresh = GlmbStep(st.scene, device=dev)
+    fresh.birth(0)
+    out = {"note": "glmb_compat_skipping: a warp skips a particle tile when all its measurements are >= 200 "
+                   "whitened units^2 from the tile's bounding box (contributions exactly +0 on both exp paths); "
+                   "opt-in, the headline is the dense pass and counts the dense pairs"}
+    sm = L.glmb_sm_count(dev.index or 0)
+    for name, g in (("step0", fresh), ("late_state", st)):
+        Z = g.Z[0]
+        M = Z.shape[0]
+        c = g.cfg
+        Cs, Gs = torch.empty_like(g.out.C_tracks), torch.empty_like(g.out.gate)
+        cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        for _ in range(2):
+            g.compat(0, Z=Z)
+            L.glmb_compat_skipping(g.particles, Z, c.R, c.p_d, c.kappa, c.gamma, None, Cs, Gs, cnt)
+        torch.cuda.synchronize(dev)
+        e[0].record()
+        for _ in range(reps):
+            g.compat(0, Z=Z)
+        e[1].record()
+        cnt.zero_()
+        e[2].record()
+        for _ in range(reps):
+            L.glmb_compat_skipping(g.particles, Z, c.R, c.p_d, c.kappa, c.gamma, None, Cs, Gs, cnt)
+        e[3].record()
+        torch.cuda.synchronize(dev)
+        dense_ms, skip_ms = e[0].elapsed_time(e[1]) / reps, e[2].elapsed_time(e[3]) / reps
+        pairs = M * g.T_local * g.P
+        evaluated = pairs - int(cnt.item()) // reps
+        ldg = (M + 31) // 32
+        same = bool(torch.equal(Cs[:, :M], g.out.C_tracks[:, :M]) and torch.equal(Gs[:, :ldg], g.out.gate[:, :ldg]))
+        peak = sm * COMPAT_PAIRS_PER_CLK_PER_SM * 1.965e9
+        out[name] = {"dense_ms": dense_ms, "skip_ms": skip_ms, "speedup": dense_ms / skip_ms,
+                     "pairs": pairs, "evaluated_pairs": evaluated, "evaluated_frac": evaluated / pairs,
+                     "evaluated_pairs_per_s": evaluated / (skip_ms * 1e-3),
+                     "frac_of_combined_bound": evaluated / (skip_ms * 1e-3) / peak,
+                     "bit_identical": same}
+    del fresh
     return out
 
 
@@ -531,9 +530,37 @@ def bench_update(a, st, scene, cfg, dev, stream, L):
     # and writes 6 (24 B), per kept pair copies 6 fields (24 + 24 B)
     hbm_f2 = {"reweight_pairs": hbm_stage("reweight_pairs", 16 * P * n_pairs),
               "resample": hbm_stage("resample", P * (4 * n_pairs + 44 * n_res + 48 * (n_pairs - n_res)))}
+    # the two-stage sampler's bound (R24): one Philox4x32-10 block per (sample, parent track quad)
+    # and per (sample, row quad holding a parent entry) -- 10 rounds of 2 IMAD.WIDE.U32 (FMA-heavy
+    # pipe, 64 lanes/clk/SM) and 2 LOP3 (ALU pipe, 64 lanes/clk/SM), the two pipes in parallel --
+    # against the theta / alive / log-weight / fingerprint writes at the HBM peak
+    col = hu.col[:int(rp[-1])].cpu().numpy()
+    row_of = np.repeat(np.arange(M), row_len)
+    ldt = pm.shape[1]
+    blocks = 0
+    for h in range(a.h_old):
+        bits = np.zeros(32 * ldt, bool)
+        bits[:] = np.unpackbits(pm[h].astype("<u4").view(np.uint8), bitorder="little").astype(bool)
+        bits[T:] = False
+        tq = int(bits[:(T + 3) // 4 * 4].reshape(-1, 4).any(axis=1).sum())
+        rows_h = np.unique(row_of[bits[col]] // 4) if len(col) else np.zeros(0)
+        blocks += a.h_up * (tq + len(rows_h))
+    f_clk = 1.965e9
+    sm = L.glmb_sm_count(dev.index or 0)
+    alu_s = blocks * 20.0 / (64.0 * sm * f_clk)
+    n_s = a.h_old * a.h_up
+    bytes_s = n_s * (4 * M + 4 * ldt + 8 + 8)
+    hbm_s = bytes_s / (hbm * 1e9)
+    t_s = stage_mean["assoc_sample"] * 1e-3
+    sampler = {"philox_blocks": blocks, "alu_bound_us": alu_s * 1e6, "bytes_written": bytes_s,
+               "hbm_bound_us": hbm_s * 1e6, "bound": "hbm" if hbm_s >= alu_s else "alu",
+               "frac": max(alu_s, hbm_s) / t_s,
+               "basis": "Philox: 20 IMAD.WIDE + 20 LOP3 per block on two 64-lane/clk/SM pipes; theta, alive, "
+                        "log-weight and fingerprint bytes at the measured HBM peak"}
     return {"workload": f"cfg{a.config if a.config is not None else 3} C_k (T_k={T}, M={M}) + particles; "
                         f"H_old={a.h_old} x H_up={a.h_up}, tau=1e-5, H_max={a.h_max} (P:186)",
             "ms": statistics.mean(total), "one_call_ms": one_ms, "stages_ms": stage_mean, "hbm_kernels": hbm_f2,
+            "assoc_sample_roofline": sampler,
             "n_samples": a.h_old * a.h_up, "n_unique": int(hu.unique.sum().item()), "n_kept": n_kept,
             "n_pairs": n_pairs, "n_resampled": n_res,
             "gated_entries": int(rp[-1]), "row_len_max": int(row_len.max()) if M else 0,
@@ -637,8 +664,6 @@ def main():
     cfg_id = a.config if a.config is not None else (3 if world == 1 else 4)
     if a.impl == "reference":
         return reference_arm(a, cfg_id)
-    if a.compat_probe is not None:
-        return compat_probe_child(cfg_id, a.compat_probe)
 
     import torch
     import torch.distributed as dist
@@ -891,7 +916,7 @@ def main():
         convoy = bench_convoy(dev)
     skipped = None
     if world == 1 and not a.no_skip_probe:
-        skipped = skip_probe(cfg_id)
+        skipped = skip_probe(st, dev, L)
 
     cpu = None
     if world == 1 and not a.no_cpu_baseline:

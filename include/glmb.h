@@ -175,6 +175,26 @@ glmb_status glmb_compat(const glmb_particles *trk, const float *Z, int32_t M,
                         int64_t ldg, glmb_stream_t stream);
 
 /* ---------------------------------------------------------------------
+ * glmb_compat_skipping -- glmb_compat with exact zero-tile skipping (opt-in;
+ * an optimisation of a4/a5, not the method's definition): a warp skips a
+ * particle tile when every one of its measurements lies >= 200 whitened
+ * units^2 (q' = 1/2 log2(e) d^T R^-1 d >= 200) from the tile's bounding box.
+ * Every skipped pair's contribution is exactly +0 on both exp paths
+ * (2^-200 flushes to zero in fp32), so C, the gate words and C_clutter are
+ * bit-identical to glmb_compat's.  skipped_pairs (DEVICE uint64, may be NULL):
+ * incremented by the number of particle-measurement pairs skipped (for
+ * reporting evaluated pairs; the caller zeroes it).  Arguments, layout and
+ * errors as glmb_compat.  (GLMB_COMPAT_SKIP=1 in the environment makes
+ * glmb_compat itself skip, for A/B runs.)
+ * --------------------------------------------------------------------- */
+glmb_status glmb_compat_skipping(const glmb_particles *trk, const float *Z,
+                                 int32_t M, float Rxx, float Rxy, float Ryy,
+                                 float p_d, float kappa, float gamma,
+                                 float *C_clutter, float *C_tracks, int64_t ldc,
+                                 uint32_t *gate, int64_t ldg,
+                                 uint64_t *skipped_pairs, glmb_stream_t stream);
+
+/* ---------------------------------------------------------------------
  * glmb_compat_peers -- glmb_compat fused with the all-gather of C_k's column
  * blocks across ranks: the epilogue stores column j of this
  * rank's tracks to row row0 + j of EVERY peer_C[r] [.][ldc] and its gate words

@@ -63,7 +63,7 @@ EXPORTED = ["glmb_version", "glmb_status_string", "glmb_init", "glmb_sm_count", 
             "glmb_philox_dump", "glmb_normals_dump", "glmb_death_prob", "glmb_compat_rows",
             "glmb_assoc_sample", "glmb_dedup", "glmb_prune", "glmb_assoc_pairs_workspace_size",
             "glmb_assoc_pairs", "glmb_reweight_pairs", "glmb_resample", "glmb_next_parents",
-            "glmb_map_estimate", "glmb_update", "glmb_compat_peers", "glmb_step_host_csr"]
+            "glmb_map_estimate", "glmb_update", "glmb_compat_peers", "glmb_step_host_csr", "glmb_compat_skipping"]
 
 
 def load(path: str = LIB_PATH):
@@ -86,6 +86,7 @@ def load(path: str = LIB_PATH):
         L.glmb_predict.argtypes = [PP, PP, vp, f32, f32, f32, u64, u32, vp]
         L.glmb_birth.argtypes = [PP, vp, vp, vp, u64, u32, vp]
         L.glmb_compat.argtypes = [PP, vp, i32, f32, f32, f32, f32, f32, f32, vp, vp, i64, vp, i64, vp]
+        L.glmb_compat_skipping.argtypes = [PP, vp, i32, f32, f32, f32, f32, f32, f32, vp, vp, i64, vp, i64, vp, vp]
         L.glmb_reweight.argtypes = [PP, vp, vp, i32, f32, f32, f32, vp, i32, vp, vp, vp]
         SP = C.POINTER(glmb_step_params)
         L.glmb_step.argtypes = [SP, vp, i32, vp, vp, vp, i64, vp, i64, vp, vp, vp]
@@ -240,6 +241,17 @@ def glmb_compat(trk: Particles, Z, R, p_d, kappa, gamma, C_clutter, C_tracks, ga
     (pc, ldc), (pg, ldg) = _mat(C_tracks), _mat(gate)
     _check(load().glmb_compat(C.byref(t), _ptr(Z), M, R[0], R[1], R[2], p_d, kappa, gamma,
                               _ptr(C_clutter), pc, ldc, pg, ldg, _stream(stream)))
+
+
+def glmb_compat_skipping(trk: Particles, Z, R, p_d, kappa, gamma, C_clutter, C_tracks, gate, skipped=None,
+                         stream=None):
+    """glmb_compat with exact zero-tile skipping (include/glmb.h); skipped: optional device uint64 [1]
+    (int64 tensor) incremented by the number of skipped pairs."""
+    t = trk.struct()
+    M = Z.shape[0]
+    (pc, ldc), (pg, ldg) = _mat(C_tracks), _mat(gate)
+    _check(load().glmb_compat_skipping(C.byref(t), _ptr(Z), M, R[0], R[1], R[2], p_d, kappa, gamma,
+                                       _ptr(C_clutter), pc, ldc, pg, ldg, _ptr(skipped), _stream(stream)))
 
 
 def glmb_reweight(trk: Particles, Z, R, theta, col_offset, log_norm, flags, stream=None, w_out=None):

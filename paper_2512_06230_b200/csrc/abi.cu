@@ -173,9 +173,10 @@ glmb_status glmb_birth(const glmb_particles *out, const int32_t *gid, const floa
   return from_cuda(glmb::launch_birth(a, g_sm_count[dev], s));
 }
 
-glmb_status glmb_compat(const glmb_particles *trk, const float *Z, int32_t M, float Rxx, float Rxy, float Ryy,
+namespace {
+glmb_status compat_impl(const glmb_particles *trk, const float *Z, int32_t M, float Rxx, float Rxy, float Ryy,
                         float p_d, float kappa, float gamma, float *C_clutter, float *C_tracks, int64_t ldc,
-                        uint32_t *gate, int64_t ldg, glmb_stream_t stream) {
+                        uint32_t *gate, int64_t ldg, bool skip, unsigned long long *skipped, glmb_stream_t stream) {
   GLMB_TRY(check_particles(trk, true, false));
   if (M < 0) return GLMB_ERR_INVALID_ARG;
   if (!spd(Rxx, Rxy, Ryy) || !(p_d > 0.f && p_d <= 1.f) || !(kappa >= 0.f) || !(gamma >= 1e-30f))
@@ -206,9 +207,27 @@ glmb_status glmb_compat(const glmb_particles *trk, const float *Z, int32_t M, fl
   a.norm = static_cast<float>(1.0 / (2.0 * 3.14159265358979323846 * std::sqrt(det)));
   a.p_d = p_d; a.kappa = kappa; a.gamma = gamma;
   a.C_clutter = C_clutter; a.C_tracks = C_tracks; a.ldc = ldc; a.gate = gate; a.ldg = ldg;
+  a.skip = skip ? 1 : 0;
+  a.skip_count = skipped;
   glmb::compat_plan(M, a.P, &a.K, &a.NW, &a.CL, &a.n_mtiles);
   if (static_cast<int64_t>(T) * a.n_mtiles * a.CL > 0x7fffffffLL) return GLMB_ERR_INVALID_ARG;
   return from_cuda(glmb::launch_compat(a, s));
+}
+}  // namespace
+
+glmb_status glmb_compat(const glmb_particles *trk, const float *Z, int32_t M, float Rxx, float Rxy, float Ryy,
+                        float p_d, float kappa, float gamma, float *C_clutter, float *C_tracks, int64_t ldc,
+                        uint32_t *gate, int64_t ldg, glmb_stream_t stream) {
+  return compat_impl(trk, Z, M, Rxx, Rxy, Ryy, p_d, kappa, gamma, C_clutter, C_tracks, ldc, gate, ldg,
+                     glmb::compat_skip_env(), nullptr, stream);
+}
+
+glmb_status glmb_compat_skipping(const glmb_particles *trk, const float *Z, int32_t M, float Rxx, float Rxy,
+                                 float Ryy, float p_d, float kappa, float gamma, float *C_clutter, float *C_tracks,
+                                 int64_t ldc, uint32_t *gate, int64_t ldg, uint64_t *skipped_pairs,
+                                 glmb_stream_t stream) {
+  return compat_impl(trk, Z, M, Rxx, Rxy, Ryy, p_d, kappa, gamma, C_clutter, C_tracks, ldc, gate, ldg, true,
+                     reinterpret_cast<unsigned long long *>(skipped_pairs), stream);
 }
 
 glmb_status glmb_compat_peers(const glmb_particles *trk, const float *Z, int32_t M, float Rxx, float Rxy,
@@ -240,6 +259,7 @@ glmb_status glmb_compat_peers(const glmb_particles *trk, const float *Z, int32_t
   a.p_d = p_d; a.kappa = kappa; a.gamma = gamma;
   a.C_clutter = C_clutter; a.C_tracks = nullptr; a.ldc = ldc; a.gate = nullptr; a.ldg = ldg;
   a.peer_C = peer_C; a.peer_G = peer_G; a.n_peers = n_peers; a.peer_row0 = row0;
+  a.skip = glmb::compat_skip_env() ? 1 : 0;
   glmb::compat_plan(M, a.P, &a.K, &a.NW, &a.CL, &a.n_mtiles);
   if (static_cast<int64_t>(T) * a.n_mtiles * a.CL > 0x7fffffffLL) return GLMB_ERR_INVALID_ARG;
   return from_cuda(glmb::launch_compat(a, s));

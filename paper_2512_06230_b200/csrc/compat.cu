@@ -480,20 +480,12 @@ cudaError_t launch_kc(const CompatArgs &a, cudaStream_t s) {
   return cudaLaunchKernelEx(&cfg, compat_kernel<NW, K, EMU_PERIOD, CL, SKIP>, a);
 }
 
-// GLMB_COMPAT_SKIP=1: exact zero-tile skipping (opt-in; the dense pass is the default
-// and the measured headline).  Built for the default exp split only.
-bool skip_enabled() {
-  static const bool v = [] {
-    const char *e = std::getenv("GLMB_COMPAT_SKIP");
-    return e && std::atoi(e) == 1;
-  }();
-  return v;
-}
-
 template <int NW, int K, int EMU_PERIOD>
 cudaError_t launch_k(const CompatArgs &a, cudaStream_t s) {
+  // exact zero-tile skipping (a.skip, opt-in; the dense pass is the default and the measured
+  // headline).  Built for the default exp split only.
   if constexpr (EMU_PERIOD == -10) {
-    if (skip_enabled())
+    if (a.skip)
       return a.CL == 2 ? launch_kc<NW, K, EMU_PERIOD, 2, true>(a, s) : launch_kc<NW, K, EMU_PERIOD, 1, true>(a, s);
   }
   return a.CL == 2 ? launch_kc<NW, K, EMU_PERIOD, 2, false>(a, s) : launch_kc<NW, K, EMU_PERIOD, 1, false>(a, s);
@@ -579,6 +571,15 @@ cudaError_t launch_compat(const CompatArgs &a_in, cudaStream_t s) {
     case 2: return launch_e<4, 2>(a, s);
     default: return cudaErrorInvalidValue;
   }
+}
+
+// GLMB_COMPAT_SKIP=1 turns glmb_compat into the skipping variant (A/B runs and tests)
+bool compat_skip_env() {
+  static const bool v = [] {
+    const char *e = std::getenv("GLMB_COMPAT_SKIP");
+    return e && std::atoi(e) == 1;
+  }();
+  return v;
 }
 
 cudaError_t launch_clutter_fill(float *C_clutter, int32_t M, float kappa, cudaStream_t s) {

@@ -72,8 +72,10 @@ struct CompatArgs {
   uint32_t *const *peer_G;
   int32_t n_peers;
   int64_t peer_row0;
-  // exact zero-tile skipping (GLMB_COMPAT_SKIP=1, opt-in): optional device counter of the
-  // particle-measurement pairs skipped because their contribution is exactly +0
+  // exact zero-tile skipping (opt-in: glmb_compat_skipping, or GLMB_COMPAT_SKIP=1 for
+  // glmb_compat): skip = 1 selects the skipping kernel; skip_count (optional) is a device
+  // counter of the particle-measurement pairs skipped because their contribution is exactly +0
+  int32_t skip;
   unsigned long long *skip_count;
 };
 
@@ -181,6 +183,7 @@ cudaError_t launch_normals_dump(uint32_t k0, uint32_t k1, const uint32_t *ctr, i
 // chooses K / n_mtiles from (M, P) only (never from T: bit-identical sharding)
 void compat_plan(int32_t M, int32_t P, int32_t *K, int32_t *NW, int32_t *CL, int32_t *n_mtiles);
 cudaError_t launch_compat(const CompatArgs &a, cudaStream_t s);
+bool compat_skip_env();
 cudaError_t launch_clutter_fill(float *C_clutter, int32_t M, float kappa, cudaStream_t s);
 cudaError_t launch_reweight(const ReweightArgs &a, cudaStream_t s);
 cudaError_t launch_death_prob(const DeathArgs &a, cudaStream_t s);

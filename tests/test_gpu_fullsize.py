@@ -134,27 +134,39 @@ def test_cfg4_full_size_rank_blocks(L, orc):
 
 
 @pytest.mark.parametrize("n_pred", [0, 25])
-def test_cfg3_exact_skip_vs_oracle(orc, n_pred, tmp_path):
-    """GLMB_COMPAT_SKIP=1 at the full config 3 (1024 survivors + 16 births, every column) against
-    the oracle directly -- not only against the dense pass: compact (step-0) clouds, where most
-    tiles are skipped, and the diffused clouds after 25 predicts (the bench's timed steps)."""
-    import os
-    import subprocess
-    import sys
+def test_cfg3_exact_skip_vs_oracle(L, orc, n_pred):
+    """glmb_compat_skipping at the full config 3 (1024 survivors + 16 births, every column)
+    against the oracle directly -- not only against the dense pass -- on compact (step-0)
+    clouds, where most tiles are skipped, and on the diffused clouds after 25 predicts (the
+    bench's timed steps).  C and the gate words are bit-identical to glmb_compat's, and the
+    device counter reports how many pairs were skipped (the bench's evaluated-pair count)."""
     from paper_2512_06230_b200.scenes import make_scene
-    here = os.path.dirname(os.path.abspath(__file__))
-    out = str(tmp_path / "skip.npz")
-    env = dict(os.environ, GLMB_COMPAT_SKIP="1", PYTHONPATH=os.path.dirname(here))
-    r = subprocess.run([sys.executable, os.path.join(here, "_compat_dump.py"), "3", "1024", str(n_pred), out,
-                        "1040"], env=env, capture_output=True, text=True, timeout=900)
-    assert r.returncode == 0, r.stderr[-3000:]
-    d = np.load(out)
-    s = make_scene(3, rows=range(0), steps=1)
+    from paper_2512_06230_b200.step import GlmbStep
+    s = make_scene(3, steps=1)
     c = s.cfg
+    st = GlmbStep(s)
+    for k in range(n_pred):
+        st.predict(k)
+    st.birth(0)
+    st.compat(0)
     M = len(s.Z[0])
-    ref = orc.compat(d["x"], d["y"], d["w"], s.Z[0], c.R, c.p_d, c.kappa, c.gamma)
-    nband, rel = check_compat(d["C"], d["G"].view(np.uint32), None, ref, c.gamma, M)
+    Cs = torch.full_like(st.out.C_tracks, -1.0)
+    Gs = torch.full_like(st.out.gate, -1)
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    L.glmb_compat_skipping(st.particles, st.Z[0], c.R, c.p_d, c.kappa, c.gamma, None, Cs, Gs, cnt)
+    torch.cuda.synchronize()
+    ldg = (M + 31) // 32
+    np.testing.assert_array_equal(Cs.cpu().numpy()[:, :M].view(np.uint32),
+                                  st.out.C_tracks.cpu().numpy()[:, :M].view(np.uint32))
+    np.testing.assert_array_equal(Gs.cpu().numpy()[:, :ldg], st.out.gate.cpu().numpy()[:, :ldg])
+    skipped = int(cnt.item())
+    total = M * st.T_local * c.P
+    assert 0 < skipped < total
+    d = st.particles.data.cpu().numpy()
+    ref = orc.compat(d[0], d[1], d[5], s.Z[0], c.R, c.p_d, c.kappa, c.gamma)
+    nband, rel = check_compat(Cs.cpu().numpy(), Gs.cpu().numpy().view(np.uint32), None, ref, c.gamma, M)
     _gated_band_bound(nband, ref, c.gamma)
+    print(f"cfg3 exact skip after {n_pred} predicts: {skipped / total:.3f} of the pairs skipped")
 
 
 def test_cfg2_sequence_stagewise_vs_oracle(L, orc):

@@ -325,6 +325,35 @@ def test_reweight_paths_and_multi_detection(L, orc, P):
     np.testing.assert_array_equal(fl, 0)
 
 
+@pytest.mark.parametrize("P", [2048, 8192])
+def test_reweight_fp32_budget_edge(L, orc, P):
+    """The e-cache kernel's fp32 pass is kept only while the unit's max log-weight m >= -300
+    (every weight that matters then has q' <= 400 and an fp32 error under the contract),
+    else pass 1 is rerun in fp64.  Tracks with a measurement 12-32 m from a 1.5 m cloud and
+    Dirichlet weights put m on both sides of the threshold (the 28-32 m tracks past it);
+    all of them must meet the 1e-4 contract against the oracle, 1e-30 absolute for the tiny
+    weights.  Also 4 km coordinates, where z - p is formed from the split (hi, lo) mean."""
+    r = np.random.default_rng(P + 7)
+    ds = [12.0, 18.0, 22.0, 25.0, 28.0, 30.0, 32.0]
+    T = len(ds)
+    for base in (0.0, 4000.0):
+        x = (base + r.normal(0, 1.5, (T, P))).astype(np.float32)
+        y = (base + r.normal(0, 1.5, (T, P))).astype(np.float32)
+        w = r.dirichlet(np.full(P, 0.5), T).astype(np.float32)
+        Z = np.array([[base + d, base + 0.3] for d in ds], np.float32)
+        theta = np.arange(1, T + 1, dtype=np.int32)
+        wg, ln, fl = _reweight_gpu(L, x, y, w, Z, (1.0, 0.0, 1.0), theta)
+        rw, rln, rfl = orc.reweight(x, y, w, Z, (1.0, 0.0, 1.0), theta)
+        check_weights(wg, rw)
+        check_log_norm(ln, rln)
+        np.testing.assert_array_equal(fl.view(np.uint32), rfl)
+        # the threshold is crossed inside the set: m_j = max_p log2 w' before normalising
+        lw = np.log2(np.maximum(w.astype(np.float64), 1e-300))
+        q = 0.5 / np.log(2) * ((Z[:, 0:1] - x.astype(np.float64)) ** 2 + (Z[:, 1:2] - y.astype(np.float64)) ** 2)
+        m = (lw - q).max(axis=1)
+        assert (m > -300).any() and (m < -300).any(), m
+
+
 @pytest.mark.parametrize("P", [256, 8192])   # cluster kernel / flat two-pass kernel
 def test_reweight_degenerate_and_many_assigned(L, orc, P):
     r = np.random.default_rng(3)
