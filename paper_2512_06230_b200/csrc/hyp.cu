@@ -337,10 +337,16 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
   double *red_lw = slc + max(a.n_count, 0);                             // [kSampWarps][32]
   unsigned long long *red_fp = reinterpret_cast<unsigned long long *>(red_lw + 32 * kSampWarps);  // [W][32]
   int32_t *red_ms = reinterpret_cast<int32_t *>(red_fp + 32 * kSampWarps);  // [W][32]
-  uint32_t *alive = reinterpret_cast<uint32_t *>(red_ms + 32 * kSampWarps);  // [ldt][32]
-  uint32_t *det = alive + 32 * a.ldt;                                   // [ldt][32]
-  uint32_t *cnt = det + 32 * a.ldt;                                     // [(T+1)/2][32] u16 pairs (count prior)
-  int32_t *frp = reinterpret_cast<int32_t *>(cnt + (a.n_count > 0 ? 32 * ((a.T + 1) >> 1) : 0));  // [M + 1]
+  const int32_t tw = (a.T + 31) >> 5;                                   // track words in use (<= ldt)
+  uint32_t *alive = reinterpret_cast<uint32_t *>(red_ms + 32 * kSampWarps);  // [tw][32]
+  uint32_t *det = alive + 32 * tw;                                      // [tw][32]
+  // count prior: per (track, lane) counts packed 4 x u8 per word when M < 256 (a count never
+  // exceeds M), else 2 x u16 -- [(T + per - 1) / per][32]
+  const int cbits = a.M < 256 ? 8 : 16, cper = 32 / cbits;
+  const uint32_t cmask = (1u << cbits) - 1u;
+  const int32_t cwords = a.n_count > 0 ? (a.T + cper - 1) / cper : 0;
+  uint32_t *cnt = det + 32 * tw;
+  int32_t *frp = reinterpret_cast<int32_t *>(cnt + 32 * cwords);        // [M + 1]
   int32_t *nzq = frp + a.M + 1;                                         // [(M + 3) / 4]
   int32_t *pw = nzq + ((a.M + 3) >> 2);                                 // [ldt] parent words
   uint32_t *pmask = reinterpret_cast<uint32_t *>(pw + a.ldt);           // [ldt]
@@ -356,12 +362,12 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
   const uint32_t* pm = a.parent_mask + static_cast<int64_t>(h) * a.ldt;
   for (int32_t k = threadIdx.x; k < a.ldt; k += kSampThreads) pmask[k] = __ldg(pm + k);
   for (int32_t k = threadIdx.x; k < a.n_count; k += kSampThreads) slc[k] = __ldg(a.count_lp + k);
-  for (int32_t k = threadIdx.x; k < 32 * a.ldt; k += kSampThreads) {
+  for (int32_t k = threadIdx.x; k < 32 * tw; k += kSampThreads) {
     alive[k] = 0u;
     det[k] = 0u;
   }
   if (a.n_count > 0)
-    for (int32_t k = threadIdx.x; k < 32 * ((a.T + 1) >> 1); k += kSampThreads) cnt[k] = 0u;
+    for (int32_t k = threadIdx.x; k < 32 * cwords; k += kSampThreads) cnt[k] = 0u;
   __syncthreads();
   auto in_parent = [&](int32_t j) { return ((pmask[j >> 5] >> (j & 31)) & 1u) != 0u; };
 
@@ -473,9 +479,9 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
   // (quad << 4 | mask of its non-empty rows)
   {
     int32_t cw = 0;
-    for (int32_t w0 = 0; w0 < a.ldt; w0 += kSampThreads) {
+    for (int32_t w0 = 0; w0 < tw; w0 += kSampThreads) {
       const int32_t w = w0 + threadIdx.x;
-      const bool any = w < a.ldt && pmask[w] != 0u;
+      const bool any = w < tw && pmask[w] != 0u;
       int32_t tot;
       const int32_t ex = block_excl_scan(any, red_i, tot);
       if (any) pw[cw + ex] = w;
@@ -582,7 +588,7 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
       const int32_t pick = draw_row(rp, cl, vl, lvl, al_of, a.kappa, ln_kappa, i, word_of(r, e), lw);
       if (pick > 0) {
         atomicOr(det + 32 * ((pick - 1) >> 5) + lane, 1u << ((pick - 1) & 31));
-        if (a.n_count > 0) atomicAdd(cnt + 32 * ((pick - 1) >> 1) + lane, 1u << (16 * ((pick - 1) & 1)));
+        if (a.n_count > 0) atomicAdd(cnt + 32 * ((pick - 1) / cper) + lane, 1u << (cbits * ((pick - 1) % cper)));
         // fingerprint over the detected rows only (theta is 0 elsewhere)
         fp += fp_term(static_cast<uint32_t>(pick), static_cast<uint64_t>(a.ldt) + i);
         if (valid) th[i] = pick;
@@ -596,15 +602,15 @@ __global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a
   int32_t missed = 0;
   uint32_t *al_out = a.alive + (static_cast<int64_t>(h) * a.H_up + s) * a.ldt;
   for (int32_t k = wid; k < a.ldt; k += kSampWarps) {
-    const uint32_t av = alive[32 * k + lane];
+    const uint32_t av = k < tw ? alive[32 * k + lane] : 0u;   // words past the tracks: 0
     if (valid) al_out[k] = av;
     fp += fp_term(av, static_cast<uint64_t>(k));
     if (a.n_count == 0) {
-      missed += __popc(av & ~det[32 * k + lane]);
+      if (k < tw) missed += __popc(av & ~det[32 * k + lane]);
     } else {
       for (uint32_t rest = av; rest != 0u; rest &= rest - 1u) {
         const int32_t j = 32 * k + __ffs(rest) - 1;
-        const uint32_t n = (cnt[32 * (j >> 1) + lane] >> (16 * (j & 1))) & 0xFFFFu;
+        const uint32_t n = (cnt[32 * (j / cper) + lane] >> (cbits * (j % cper))) & cmask;
         lw += slc[min(static_cast<int32_t>(n), a.n_count - 1)];
       }
     }
@@ -1031,15 +1037,19 @@ cudaError_t launch_assoc_sample(const SampleArgs &a, int sm_count, cudaStream_t 
   const size_t fixed =
       sizeof(double) * static_cast<size_t>(max(a.n_count, 0)) +
       (sizeof(double) + sizeof(unsigned long long) + sizeof(int32_t)) * 32 * kSampWarps +
-      sizeof(uint32_t) * 32 * 2 * static_cast<size_t>(a.ldt) +
-      (a.n_count > 0 ? sizeof(uint32_t) * 32 * ((static_cast<size_t>(a.T) + 1) / 2) : 0) +
+      sizeof(uint32_t) * 32 * 2 * ((static_cast<size_t>(a.T) + 31) / 32) +
+      (a.n_count > 0 ? sizeof(uint32_t) * 32 * ((static_cast<size_t>(a.T) + (a.M < 256 ? 3 : 1)) / (a.M < 256 ? 4 : 2))
+                     : 0) +
       sizeof(int32_t) * (static_cast<size_t>(a.M) + 1) + sizeof(int32_t) * ((static_cast<size_t>(a.M) + 3) / 4) +
       2 * sizeof(uint32_t) * static_cast<size_t>(a.ldt) + 16;
   if (fixed + 1024 > 220 * 1024) return cudaErrorInvalidValue;
   // shared memory per CTA sized so the grid runs in one wave where it can; the pool
   // beyond the fixed arrays holds the kept-entry bitmap and the parent's rows
   const int64_t sms = sm_count > 0 ? sm_count : 148;
-  const int64_t per_sm = std::min<int64_t>(8, std::max<int64_t>(1, (n + sms - 1) / sms));
+  int64_t per_sm = std::min<int64_t>(8, std::max<int64_t>(1, (n + sms - 1) / sms));
+  // fewer CTAs per SM rather than a pool too small for the parent's rows (the fallback
+  // walks the whole global CSR)
+  while (per_sm > 1 && (227 * 1024) / per_sm - 2048 < fixed + 24 * 1024) --per_sm;
   const size_t target = std::min<size_t>(220 * 1024, (227 * 1024) / per_sm - 2048);
   static const int pool_env = [] {  // test hook: force a small pool (every fallback path)
     const char *e = std::getenv("GLMB_SAMPLER_POOL");
