@@ -335,8 +335,10 @@ def make_line(*, cfg_id, cfg, world, steps, warmup, elapsed_ms, evals_total, pai
         "dtype": "f32",
         "data": "synthetic",
         "config": workload_config(cfg_id, cfg, world, M_mean, evals_total / steps),
-        "schedule": "predict, birth; then compat overlapped with reweight on a second stream "
-                    "(double-buffered weights); stages_ms timed in a separate serialised pass",
+        "schedule": "software-pipelined steps: predict + birth of step k into a spare state buffer on a "
+                    "high-priority stream beside compat of step k-1, reweight beside compat on a second stream "
+                    "(double-buffered state and weights, event-ordered); stages_ms timed in a separate "
+                    "serialised pass",
         "roofline": {"bound": "alu", "kernel": "compat (exp: MUFU.EX2 + FMA-pipe polynomial)",
                      "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Geval/s",
                      "frac": achieved / peak,
@@ -671,7 +673,7 @@ def main():
     from paper_2512_06230_b200.build import build
     from paper_2512_06230_b200.scenes import CONFIGS, make_scene
     from paper_2512_06230_b200.dist import ShardedStep
-    from paper_2512_06230_b200.step import GlmbStep
+    from paper_2512_06230_b200.step import GlmbStep, PipelinedSteps
 
     torch.cuda.set_device(local)   # before NCCL init: each rank's communicator binds its own GPU
     if rank == 0:
@@ -712,31 +714,23 @@ def main():
     stage_names = ["predict", "birth", "compat", "reweight"]
     stage_ms = {n: [] for n in stage_names}
 
+    # N = 1: software-pipelined steps (step.PipelinedSteps): predict + birth of step k into the
+    # spare state buffer on a high-priority stream beside compat of step k-1, reweight beside compat
+    pipe = PipelinedSteps(st, stream, side) if sh is None else None
+
     def one_step(k):
-        """One step as timed: predict -> birth on `stream`, then compat on `stream`
-        overlapped with reweight on `side` (reweight writes the spare weight buffer,
-        compat reads the current one); at W > 1 with the broadcast before and the
-        gather after (ShardedStep.step)."""
+        """One step as timed (PipelinedSteps at N = 1); at W > 1 the broadcast, the four calls
+        and the gather in order (ShardedStep.step, reweight beside compat)."""
         if sh is not None:
             M = sh.load_measurements(k, stream=stream)
             sh.step(k, M, stream=stream, side=side)
             return
-        zi = k % len(st.Z)
-        with torch.cuda.stream(stream):
-            Zk, thk = st.Z[zi], st.theta[zi]
-            st.predict(k, stream)
-            st.birth(k, stream)
-            ready = ev()
-            ready.record(stream)
-            side.wait_event(ready)
-            p_now = st.particles          # compat reads these weights; reweight writes the spare
-            with torch.cuda.stream(side):
-                st.reweight(k, side, Z=Zk, theta=thk, out_of_place=True)
-                done = ev()
-                done.record(side)
-            L.glmb_compat(p_now, Zk, st.R, st.cfg.p_d, st.cfg.kappa, st.cfg.gamma,
-                          st.out.C_clutter, st.out.C_tracks, st.out.gate, stream)
-            stream.wait_event(done)
+        pipe.step(k)
+
+    def join_streams():
+        """The timed region ends when every stream's last step work is done."""
+        if pipe is not None:
+            pipe.join()
 
     def isolated_step(k):
         """The same four calls serialised on `stream`, with an event between each, so
@@ -771,11 +765,14 @@ def main():
     step_marks = []
     with sampler:
         t_start.record(stream)
+        if pipe is not None:
+            pipe.start_after(t_start)
         for k in range(a.warmup, a.warmup + a.steps):
             one_step(k)
             e = ev()
             e.record(stream)
             step_marks.append(e)
+        join_streams()
         t_end.record(stream)
         torch.cuda.synchronize(dev)
     per_step = [(step_marks[0] if i == 0 else step_marks[i - 1]).elapsed_time(step_marks[i]) if i else
@@ -930,6 +927,9 @@ def main():
         traffic=compat_traffic(st.T_local, st.P, len(scene.Z[0])), e2e=e2e, cpu=cpu,
         reweight_launches=1 if st.contiguous else 2)
     line["gather"] = gather
+    if world > 1:
+        line["schedule"] = ("per step: the packed Z_k/theta_k broadcast, predict, birth, compat with reweight "
+                            "beside it on a second stream, the C_k/gate and log_norm gathers")
     line["ms_per_step_p50"] = float(np.percentile(per_step, 50))
     line["ms_per_step_p95"] = float(np.percentile(per_step, 95))
     if graphs is not None:

@@ -123,6 +123,25 @@ class GlmbStep:
         L.glmb_predict(s, s, self.gid[:self.T_surv], self.cfg.dt, self.cfg.sigma_a,
                        self.cfg.sigma_w, self.seed, k, stream)
 
+    def predict_to_spare(self, k: int, stream=None):
+        """Out-of-place step start (software pipelining across steps): predict the survivors
+        from the current state into a spare state buffer and draw the births there, then make
+        the spare current (the weights are shared).  The old state stays readable by a compat
+        still running on another stream; the spare must no longer be read by one (the caller
+        orders that, e.g. with events)."""
+        if not hasattr(self, "spare"):
+            self.spare = torch.empty_like(self.particles.data)
+        src = L.Particles(self.particles.data, self.P, self.w_bufs[self.w_cur])
+        dst = L.Particles(self.spare, self.P, self.w_bufs[self.w_cur])
+        if self.T_surv:
+            L.glmb_predict(src.rows(0, self.T_surv), dst.rows(0, self.T_surv), self.gid[:self.T_surv],
+                           self.cfg.dt, self.cfg.sigma_a, self.cfg.sigma_w, self.seed, k, stream)
+        if self.B_local:
+            L.glmb_birth(dst.rows(self.T_surv, self.T_local), self.gid[self.T_surv:], self.birth_mean,
+                         self.birth_chol, self.seed, k, stream)
+        self.spare = self.particles.data
+        self.particles = dst
+
     def birth(self, k: int, stream=None):
         if self.B_local:
             L.glmb_birth(self.births(), self.gid[self.T_surv:], self.birth_mean, self.birth_chol,
@@ -189,3 +208,63 @@ class GlmbStep:
         th = self.scene.theta[zi]
         n_assigned = int(np.isin(th - 1, self.col_of_row).sum())
         return M * self.T_local * self.P + self.P * n_assigned
+
+
+class PipelinedSteps:
+    """Software-pipelined GLMB steps on one rank (what bench.py times at N = 1): step k's
+    predict + birth write the spare state buffer (GlmbStep.predict_to_spare) on a high-priority
+    stream, so they run while step k-1's compat still reads the other buffer; reweight_k writes
+    the spare weight buffer on `side` beside compat_k on `main`.  Event order: predict_k after
+    compat_{k-2} and reweight_{k-2} (the readers of the buffer it overwrites); reweight_k after
+    predict_k and compat_{k-1} (the reader of the weights it overwrites); compat_k after
+    predict_k and reweight_{k-1} (its weights).  Every step does all of its work; the results
+    are those of the sequential steps (tests/test_gpu_parity.py)."""
+
+    def __init__(self, st: GlmbStep, main, side, pred=None):
+        self.st, self.main, self.side = st, main, side
+        self.pred = pred if pred is not None else torch.cuda.Stream(device=st.device, priority=-1)
+        self.c = [None, None]    # compat events of steps k-1, k-2
+        self.rw = [None, None]   # reweight events of steps k-1, k-2
+
+    def start_after(self, event):
+        self.pred.wait_event(event)
+        self.side.wait_event(event)
+
+    def step(self, k: int):
+        st = self.st
+        zi = k % len(st.Z)
+        Zk, thk = st.Z[zi], st.theta[zi]
+        c1, c2 = self.c
+        r1, r2 = self.rw
+        ev = lambda: torch.cuda.Event()
+        with torch.cuda.stream(self.pred):
+            for e in (c2, r2):
+                if e is not None:
+                    self.pred.wait_event(e)
+            st.predict_to_spare(k, self.pred)
+            ready = ev()
+            ready.record(self.pred)
+        p_now = st.particles          # compat reads these weights; reweight writes the spare
+        self.side.wait_event(ready)
+        if c1 is not None:
+            self.side.wait_event(c1)
+        with torch.cuda.stream(self.side):
+            st.reweight(k, self.side, Z=Zk, theta=thk, out_of_place=True)
+            rdone = ev()
+            rdone.record(self.side)
+        self.main.wait_event(ready)
+        if r1 is not None:
+            self.main.wait_event(r1)
+        with torch.cuda.stream(self.main):
+            o = st.out
+            L.glmb_compat(p_now, Zk, st.R, st.cfg.p_d, st.cfg.kappa, st.cfg.gamma, o.C_clutter, o.C_tracks,
+                          o.gate, self.main)
+            cdone = ev()
+            cdone.record(self.main)
+        self.c = [cdone, c1]
+        self.rw = [rdone, r1]
+
+    def join(self):
+        """Make `main` wait for every stream's last work (then one event on main ends the steps)."""
+        if self.rw[0] is not None:
+            self.main.wait_event(self.rw[0])

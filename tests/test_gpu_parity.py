@@ -662,3 +662,29 @@ def test_compat_exact_skip(cfg_id, n_rows, n_pred, tmp_path):
         outs[skip] = np.load(out)
     np.testing.assert_array_equal(outs["0"]["C"].view(np.uint32), outs["1"]["C"].view(np.uint32))
     np.testing.assert_array_equal(outs["0"]["G"], outs["1"]["G"])
+
+
+@pytest.mark.parametrize("cfg_id", [1, 2])
+def test_pipelined_steps_equal_sequential(L, cfg_id):
+    """step.PipelinedSteps (bench.py's N = 1 schedule: predict + birth of step k into the spare
+    state buffer beside compat of step k-1, reweight beside compat, event-ordered) gives the
+    sequential steps' results bit for bit: state, weights, C_k, gate words, log-normalisers."""
+    import torch
+    from paper_2512_06230_b200.scenes import make_scene
+    from paper_2512_06230_b200.step import GlmbStep, PipelinedSteps
+    s = make_scene(cfg_id, steps=6)
+    a, b = GlmbStep(s), GlmbStep(s)
+    main, side = torch.cuda.Stream(), torch.cuda.Stream()
+    pipe = PipelinedSteps(b, main, side)
+    for k in range(6):
+        a.predict(k)
+        a.birth(k)
+        a.compat(k)
+        a.reweight(k)
+        pipe.step(k)
+    pipe.join()
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(a.particles.data[:5].cpu().numpy(), b.particles.data[:5].cpu().numpy())
+    np.testing.assert_array_equal(a.particles.data[5].cpu().numpy(), b.weights().cpu().numpy())
+    for f in ("C_tracks", "gate", "log_norm", "flags"):
+        np.testing.assert_array_equal(getattr(a.out, f).cpu().numpy(), getattr(b.out, f).cpu().numpy())

@@ -148,3 +148,38 @@ def test_birth_moments(orc):
     # ranks of different births / steps draw different particles
     out2 = orc.birth(mean, chol, np.array([12], np.int32), 16, seed=5, step=2)
     assert not np.array_equal(out2[0][0], out[0][0][:16])
+
+
+def test_predict_keying_properties(orc):
+    """R9's keying pinned by what it must guarantee, not by its formula (BJ north_star: noise
+    "keyed by (seed, step, track, particle)"): the draws of a track follow its global id, not its
+    row (rows permuted with their gids -> outputs permuted exactly; the same track alone in a
+    one-row call -> the same output); a different step, seed or gid changes every particle's
+    draw; the two particles sharing a Philox block (p = 2q, 2q + 1) get different noise; and the
+    noise-free flow is recovered with sigma = 0."""
+    T, P = 4, 16
+    r = np.random.default_rng(5)
+    st = [r.uniform(0, 50, (T, P)).astype(np.float32), r.uniform(0, 50, (T, P)).astype(np.float32),
+          r.uniform(2, 20, (T, P)).astype(np.float32), r.uniform(-3, 3, (T, P)).astype(np.float32),
+          r.normal(0, 0.3, (T, P)).astype(np.float32)]
+    gid = np.array([11, 4, 700, 9], np.int32)
+    base = orc.predict(*st, gid, 0.1, 1.0, 0.1, seed=3, step=2)
+    perm = np.array([2, 0, 3, 1])
+    swapped = orc.predict(*[a[perm] for a in st], gid[perm], 0.1, 1.0, 0.1, seed=3, step=2)
+    for b, s_ in zip(base, swapped):
+        np.testing.assert_array_equal(b[perm], s_)
+    alone = orc.predict(*[a[2:3] for a in st], gid[2:3], 0.1, 1.0, 0.1, seed=3, step=2)
+    for b, s_ in zip(base, alone):
+        np.testing.assert_array_equal(b[2:3], s_)
+    clean = orc.predict(*st, gid, 0.1, 0.0, 0.0, seed=3, step=2)
+    dv = base[2] - clean[2]                                  # dt * nu_a: the drawn acceleration
+    for kw in ({"seed": 4, "step": 2}, {"seed": 3, "step": 3}):
+        other = orc.predict(*st, gid, 0.1, 1.0, 0.1, **kw)
+        assert np.all(other[2] - clean[2] != dv)
+    other = orc.predict(*st, gid + 1, 0.1, 1.0, 0.1, seed=3, step=2)
+    assert np.all(other[2] - clean[2] != dv)
+    assert np.all(dv[:, 0::2] != dv[:, 1::2])                # block-sharing particle pairs differ
+    for j in range(T):                                       # clean = the noise-free CTRV flow
+        s = [float(a[j, 5]) for a in st]
+        np.testing.assert_allclose([c[j, 5] for c in clean[:2]], orc.ctrv(s, float(np.float32(0.1)))[:2],
+                                   rtol=0, atol=1e-12)
