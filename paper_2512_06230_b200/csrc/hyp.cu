@@ -198,7 +198,13 @@ __global__ void __launch_bounds__(kRowWarps * 32) rows_fill_kernel(RowsArgs a) {
 // the same row at the same time (uniform control flow, the row's entries read from shared
 // memory as broadcasts); only the uniforms, and hence the alive bits and picks, differ
 // per lane.  The samples' alive / detected sets live in shared memory as [word][lane].
-constexpr int kSampWarps = 8;
+#ifndef GLMB_SAMP_WARPS
+#define GLMB_SAMP_WARPS 16
+#endif
+#ifndef GLMB_SAMP_BLOCKS
+#define GLMB_SAMP_BLOCKS 3
+#endif
+constexpr int kSampWarps = GLMB_SAMP_WARPS;
 constexpr int kSampThreads = 32 * kSampWarps;
 
 // one fingerprint term (summed mod 2^64 over a sample's detected rows and alive words):
@@ -257,45 +263,17 @@ __device__ __forceinline__ int32_t draw_row(const int32_t *rp, const int32_t *cl
                                             const double *lvl, const AliveOf &al_of, float kappa,
                                             double ln_kappa, int32_t i, uint32_t word, double &lw) {
   const int32_t e0 = rp[i], e1 = rp[i + 1];
-  constexpr int kShort = 4;
-  if (e1 - e0 <= kShort) {
-    // short rows (almost all): the entries in registers, both passes unrolled and predicated
-    int32_t jj[kShort];
-    float vv[kShort];
-    bool al[kShort];
-#pragma unroll
-    for (int k = 0; k < kShort; ++k) {
-      const bool in = e0 + k < e1;
-      jj[k] = in ? cl[e0 + k] : 0;
-      vv[k] = in ? vl[e0 + k] : 0.0f;
-      al[k] = in && al_of(jj[k]);
-    }
-    float total = kappa;
-#pragma unroll
-    for (int k = 0; k < kShort; ++k)
-      if (al[k]) total = __fadd_rn(total, vv[k]);
-    const float tt = __fmul_rn(uniform24(word), total);
-    bool found = !(tt >= kappa);
-    float acc = kappa;
-    int32_t pick = 0, last = 0, kpick = -1, klast = -1;
-#pragma unroll
-    for (int k = 0; k < kShort; ++k) {
-      if (!al[k]) continue;
-      acc = __fadd_rn(acc, vv[k]);
-      last = jj[k] + 1;
-      klast = k;
-      if (!found && tt < acc) {
-        pick = last;
-        kpick = k;
-        found = true;
-      }
-    }
-    if (!found) {
-      pick = last;
-      kpick = klast;
-    }
-    lw += kpick >= 0 ? lvl[e0 + kpick] : ln_kappa;
-    return pick;
+  // the row is the same for every lane of the warp, so the entry count -- and every
+  // branch on it below -- is warp-uniform
+  if (e1 - e0 == 1) {
+    // one gated parent entry (most rows): the walk reduces to pick = j + 1 iff track j is
+    // alive and u (kappa + C) does not fall below kappa
+    const int32_t j = cl[e0];
+    const bool al = al_of(j);
+    const float tot = al ? __fadd_rn(kappa, vl[e0]) : kappa;
+    const bool hit = al && !(__fmul_rn(uniform24(word), tot) < kappa);
+    lw += hit ? lvl[e0] : ln_kappa;
+    return hit ? j + 1 : 0;
   }
   float total = kappa;
   for (int32_t x = e0; x < e1; ++x)
@@ -327,7 +305,7 @@ __device__ __forceinline__ int32_t draw_row(const int32_t *rp, const int32_t *cl
   return pick;
 }
 
-__global__ void __launch_bounds__(kSampThreads) assoc_sample_kernel(SampleArgs a) {
+__global__ void __launch_bounds__(kSampThreads, GLMB_SAMP_BLOCKS) assoc_sample_kernel(SampleArgs a) {
   grid_dep_wait();
   extern __shared__ __align__(16) unsigned char smraw[];
   // a.pool bytes at the front (the kept-entry bitmap, then the parent's rows), carved
