@@ -675,12 +675,27 @@ def main():
     from paper_2512_06230_b200.dist import ShardedStep
     from paper_2512_06230_b200.step import GlmbStep, PipelinedSteps
 
+    # GLMB_BENCH_BACKEND=gloo (test hook): the N > 1 path with gloo collectives on host-staged
+    # copies, ranks mapped onto the available GPUs -- a dry run of this code path on a box
+    # with fewer GPUs than ranks (the kernels of the ranks never wait on each other)
+    backend = os.environ.get("GLMB_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend == "gloo" else local
     torch.cuda.set_device(local)   # before NCCL init: each rank's communicator binds its own GPU
     if rank == 0:
         build()
+    coll_dev = torch.device("cuda", local) if backend == "nccl" else torch.device("cpu")
+
+    def barrier():
+        if backend == "nccl":
+            dist.barrier(device_ids=[local])
+        else:
+            dist.barrier()
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        dist.barrier(device_ids=[local])
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+        barrier()
         build()  # no-op once rank 0 has built
     L.glmb_init(local)
     dev = torch.device("cuda", local)
@@ -697,16 +712,18 @@ def main():
         # ranks; C_k's column blocks + gate words all-gathered (one collective) with the
         # log-normalisers and flags -- or, fused, stored by compat into every rank's
         # symmetric-memory copy over NVLink (GLMB_FUSED_GATHER=0: NCCL all-gather)
-        fused = os.environ.get("GLMB_FUSED_GATHER", "1") != "0"
+        fused = os.environ.get("GLMB_FUSED_GATHER", "1") != "0" and backend == "nccl"
         try:
-            sh = ShardedStep(cfg_id, device=dev, steps=n_steps_scene, fused=fused)
+            sh = ShardedStep(cfg_id, device=dev, steps=n_steps_scene, fused=fused,
+                             stage_on_host=backend != "nccl")
         except Exception as e:  # noqa: BLE001
             if not fused:
                 raise
             print(f"[bench] symmetric memory unavailable ({e}); NCCL all-gather", file=sys.stderr)
             sh = ShardedStep(cfg_id, device=dev, steps=n_steps_scene, fused=False)
         gather = ("fused: compat stores its columns into every rank's symmetric-memory C_k (NVLink), device barrier"
-                  if sh.symm is not None else "NCCL all_gather_into_tensor of the column blocks")
+                  if sh.symm is not None else "NCCL all_gather_into_tensor of the column blocks"
+                  if backend == "nccl" else "gloo all_gather of host-staged column blocks (dry-run test hook)")
         st, scene = sh.st, sh.scene
     else:
         scene = make_scene(cfg_id, steps=n_steps_scene)
@@ -759,7 +776,7 @@ def main():
         print("[bench] fused gather disagreed with the NCCL all-gather; using NCCL", file=sys.stderr)
     sampler = ClockSampler(local)
     if world > 1:
-        dist.barrier(device_ids=[local])
+        barrier()
     torch.cuda.synchronize(dev)
     t_start, t_end = ev(), ev()
     step_marks = []
@@ -778,7 +795,7 @@ def main():
     per_step = [(step_marks[0] if i == 0 else step_marks[i - 1]).elapsed_time(step_marks[i]) if i else
                 t_start.elapsed_time(step_marks[0]) for i in range(len(step_marks))]
     if world > 1:
-        dist.barrier(device_ids=[local])
+        barrier()
     elapsed_ms = t_start.elapsed_time(t_end)
     # per-kernel durations: the same steps again, serialised (outside the timed region)
     all_marks = [isolated_step(k) for k in range(a.warmup, a.warmup + a.steps)]
@@ -790,7 +807,7 @@ def main():
     pairs_local = sum(len(scene.Z[k % len(scene.Z)]) * st.T_local * st.P
                       for k in range(a.warmup, a.warmup + a.steps))
     if world > 1:
-        t = torch.tensor([elapsed_ms, float(evals_local)], dtype=torch.float64, device=dev)
+        t = torch.tensor([elapsed_ms, float(evals_local)], dtype=torch.float64, device=coll_dev)
         tmax = t.clone(); dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
         tsum = t.clone(); dist.all_reduce(tsum[1:], op=dist.ReduceOp.SUM)
         elapsed_ms, evals_total = float(tmax[0]), float(tsum[1])
@@ -859,7 +876,7 @@ def main():
             for k in range(a.warmup):
                 fn(k)
             if world > 1:
-                dist.barrier(device_ids=[local])
+                barrier()
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
             for k in range(a.warmup, a.warmup + a.steps):
@@ -868,7 +885,7 @@ def main():
                 d2h += db
             sec = time.perf_counter() - t0
             if world > 1:
-                t = torch.tensor([sec], dtype=torch.float64, device=dev)
+                t = torch.tensor([sec], dtype=torch.float64, device=coll_dev)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 sec = float(t[0])
             return sec, h2d // a.steps, d2h // a.steps
