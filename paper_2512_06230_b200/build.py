@@ -20,7 +20,7 @@ HEADERS = ["glmb_device.cuh", "glmb_internal.h", "peaks.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
-                "--expt-relaxed-constexpr"]
+                "--expt-relaxed-constexpr"] + os.environ.get("GLMB_NVCC_FLAGS", "").split()  # A/B builds
 
 
 def _stale() -> bool:

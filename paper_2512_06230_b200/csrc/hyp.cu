@@ -198,6 +198,9 @@ __global__ void __launch_bounds__(kRowWarps * 32) rows_fill_kernel(RowsArgs a) {
 // the same row at the same time (uniform control flow, the row's entries read from shared
 // memory as broadcasts); only the uniforms, and hence the alive bits and picks, differ
 // per lane.  The samples' alive / detected sets live in shared memory as [word][lane].
+#ifndef GLMB_SAMP_DEBUG
+#define GLMB_SAMP_DEBUG 0  // A/B timing builds only: 1 skips stage 1's Philox, 2 skips stage 2
+#endif
 #ifndef GLMB_SAMP_WARPS
 #define GLMB_SAMP_WARPS 16
 #endif
@@ -328,6 +331,7 @@ __global__ void __launch_bounds__(kSampThreads, GLMB_SAMP_BLOCKS) assoc_sample_k
   int32_t *nzq = frp + a.M + 1;                                         // [(M + 3) / 4]
   int32_t *pw = nzq + ((a.M + 3) >> 2);                                 // [ldt] parent words
   uint32_t *pmask = reinterpret_cast<uint32_t *>(pw + a.ldt);           // [ldt]
+  int32_t *kthr = reinterpret_cast<int32_t *>(pmask + a.ldt);          // [T] survival thresholds
   __shared__ int32_t red_i[kSampWarps];
   __shared__ int32_t use_smem, n_pw, n_nzq, n_nzr;
   const int n_groups = (a.H_up + 31) >> 5;
@@ -340,6 +344,13 @@ __global__ void __launch_bounds__(kSampThreads, GLMB_SAMP_BLOCKS) assoc_sample_k
   const uint32_t* pm = a.parent_mask + static_cast<int64_t>(h) * a.ldt;
   for (int32_t k = threadIdx.x; k < a.ldt; k += kSampThreads) pmask[k] = __ldg(pm + k);
   for (int32_t k = threadIdx.x; k < a.n_count; k += kSampThreads) slc[k] = __ldg(a.count_lp + k);
+  // R25's fp32 decision u < 1 - d_j as an integer compare: u = k 2^-24 with k = 2 (r >> 9) + 1
+  // exact, and (1 - d_j) 2^24 is exact too, so u < 1 - d_j  <=>  k < ceil((1 - d_j) 2^24)
+  for (int32_t j = threadIdx.x; j < a.T; j += kSampThreads) {
+    const float thr = __fsub_rn(1.0f, __ldg(a.d_prob + j));
+    const float t = thr * 16777216.0f;
+    kthr[j] = !(thr == thr) ? 0 : t <= 0.0f ? 0 : t >= 16777218.0f ? 16777218 : static_cast<int32_t>(ceilf(t));
+  }
   for (int32_t k = threadIdx.x; k < 32 * tw; k += kSampThreads) {
     alive[k] = 0u;
     det[k] = 0u;
@@ -516,6 +527,7 @@ __global__ void __launch_bounds__(kSampThreads, GLMB_SAMP_BLOCKS) assoc_sample_k
   double lw = 0.0;
   float memo_ps = -1.0f;              // P_S of the memoised logs (none yet)
   double memo_ls = 0.0, memo_ld = 0.0;
+  int32_t n_al = 0, n_dd = 0;
   for (int32_t v = wid; v < npw; v += kSampWarps) {
     const int32_t w = pw[v];
     const uint32_t pbits = pmask[w];
@@ -524,27 +536,34 @@ __global__ void __launch_bounds__(kSampThreads, GLMB_SAMP_BLOCKS) assoc_sample_k
       const uint32_t qbits = (pbits >> (4 * qq)) & 0xFu;
       if (qbits == 0u) continue;
       const int32_t t = 8 * w + qq;
+#if GLMB_SAMP_DEBUG == 1
+      const u32x4 r{0u, 0u, 0u, 0u};
+#else
       const u32x4 r = philox4x32_10(
           u32x4{static_cast<uint32_t>(t), static_cast<uint32_t>(h), a.step, (kDomainSurvive << 24) | static_cast<uint32_t>(s)},
           a.key0, a.key1);
+#endif
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         if (!((qbits >> e) & 1u)) continue;
         const int32_t j = 4 * t + e;
-        const float thr = __fsub_rn(1.0f, __ldg(a.d_prob + j));
-        const bool al = uniform24(word_of(r, e)) < thr;
+        const bool al = static_cast<int32_t>(((word_of(r, e) >> 9) << 1) | 1u) < kthr[j];
         const float ps = __ldg(a.p_s + j);
-        if (ps != memo_ps) {  // tracks mostly share a few P_S values: logs memoised (warp-uniform)
+        if (ps != memo_ps) {  // tracks mostly share a few P_S values: logs memoised (warp-uniform),
+          lw += static_cast<double>(n_al) * memo_ls + static_cast<double>(n_dd) * memo_ld;
+          n_al = n_dd = 0;    // the survival terms counted per memo and folded in when it changes
           memo_ps = ps;
           memo_ls = log(static_cast<double>(ps));
           memo_ld = log(1.0 - static_cast<double>(ps));
         }
-        lw += al ? memo_ls : memo_ld;
+        n_al += al;
+        n_dd += !al;
         abits |= static_cast<uint32_t>(al) << (4 * qq + e);
       }
     }
     alive[32 * w + lane] = abits;
   }
+  lw += static_cast<double>(n_al) * memo_ls + static_cast<double>(n_dd) * memo_ld;
   __syncthreads();   // every sample's alive set is complete
 
   // ---- stage 2: each row i draws theta_i from the row of C'_k (clutter kappa,
@@ -553,6 +572,9 @@ __global__ void __launch_bounds__(kSampThreads, GLMB_SAMP_BLOCKS) assoc_sample_k
   uint64_t fp = 0ull;
   auto al_of = [&](int32_t j) { return ((alive[32 * (j >> 5) + lane] >> (j & 31)) & 1u) != 0u; };
   int32_t *th = a.theta + (static_cast<int64_t>(h) * a.H_up + s) * a.ldm;
+#if GLMB_SAMP_DEBUG == 2
+  if (nzq_n > 0 && a.M < 0)
+#endif
   for (int32_t v = wid; v < nzq_n; v += kSampWarps) {
     const uint32_t ent = static_cast<uint32_t>(nzq[v]);
     const int32_t t = static_cast<int32_t>(ent >> 4);
@@ -1019,7 +1041,7 @@ cudaError_t launch_assoc_sample(const SampleArgs &a, int sm_count, cudaStream_t 
       (a.n_count > 0 ? sizeof(uint32_t) * 32 * ((static_cast<size_t>(a.T) + (a.M < 256 ? 3 : 1)) / (a.M < 256 ? 4 : 2))
                      : 0) +
       sizeof(int32_t) * (static_cast<size_t>(a.M) + 1) + sizeof(int32_t) * ((static_cast<size_t>(a.M) + 3) / 4) +
-      2 * sizeof(uint32_t) * static_cast<size_t>(a.ldt) + 16;
+      2 * sizeof(uint32_t) * static_cast<size_t>(a.ldt) + sizeof(int32_t) * static_cast<size_t>(a.T) + 16;
   if (fixed + 1024 > 220 * 1024) return cudaErrorInvalidValue;
   // shared memory per CTA sized so the grid runs in one wave where it can; the pool
   // beyond the fixed arrays holds the kept-entry bitmap and the parent's rows
