@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) rows_fill_kernel(RowsArgs a) {
 // memory as broadcasts); only the uniforms, and hence the alive bits and picks, differ
 // per lane.  The samples' alive / detected sets live in shared memory as [word][lane].
 #ifndef GLMB_SAMP_DEBUG
-#define GLMB_SAMP_DEBUG 0  // A/B timing builds only: 1 skips stage 1's Philox, 2 skips stage 2
+#define GLMB_SAMP_DEBUG 0  // A/B timing builds only: 1 skips stage 1's Philox, 2 skips stage 2, 3 stamps phases
 #endif
 #ifndef GLMB_SAMP_WARPS
 #define GLMB_SAMP_WARPS 16
@@ -340,6 +340,19 @@ __global__ void __launch_bounds__(kSampThreads, GLMB_SAMP_BLOCKS) assoc_sample_k
   if (a.n_parents != nullptr && h >= __ldg(a.n_parents)) return;  // inactive parent slot
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int32_t s = 32 * g + lane;          // this lane's sample
+#if GLMB_SAMP_DEBUG == 3   // A/B timing build: %globaltimer per CTA phase into the fingerprint output
+  auto stamp = [&](int k) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.hash[6 * blockIdx.x + k] = t;
+    }
+  };
+  stamp(0);
+#else
+  auto stamp = [](int) {};
+#endif
   const bool valid = s < a.H_up;
   const uint32_t* pm = a.parent_mask + static_cast<int64_t>(h) * a.ldt;
   for (int32_t k = threadIdx.x; k < a.ldt; k += kSampThreads) pmask[k] = __ldg(pm + k);
@@ -520,6 +533,7 @@ __global__ void __launch_bounds__(kSampThreads, GLMB_SAMP_BLOCKS) assoc_sample_k
   }
   __syncthreads();
   const int32_t npw = n_pw, nzq_n = n_nzq, nzr_n = n_nzr;
+  stamp(1);
 
   // ---- stage 1: track j of the parent survives iff u_j < 1 - d_j (fp32, R25);
   // Philox block (j/4, h, step, 2<<24 | s), word j%4.  A warp per parent word (8 quads):
@@ -565,6 +579,7 @@ __global__ void __launch_bounds__(kSampThreads, GLMB_SAMP_BLOCKS) assoc_sample_k
   }
   lw += static_cast<double>(n_al) * memo_ls + static_cast<double>(n_dd) * memo_ld;
   __syncthreads();   // every sample's alive set is complete
+  stamp(2);
 
   // ---- stage 2: each row i draws theta_i from the row of C'_k (clutter kappa,
   // surviving gated columns in ascending order), inverse CDF in fp32 (R26);
@@ -596,6 +611,7 @@ __global__ void __launch_bounds__(kSampThreads, GLMB_SAMP_BLOCKS) assoc_sample_k
     }
   }
   __syncthreads();   // det / cnt complete
+  stamp(3);
 
   // ---- missed detections (alive tracks with no measurement) or, with a count prior,
   // lc(n_j) for every alive track; fingerprint of the alive words; alive words out
@@ -634,8 +650,11 @@ __global__ void __launch_bounds__(kSampThreads, GLMB_SAMP_BLOCKS) assoc_sample_k
     const double l_empty = n_empty > 0 ? static_cast<double>(n_empty) * ln_kappa : 0.0;
     const int64_t q = static_cast<int64_t>(h) * a.H_up + s;
     a.logw[q] = __ldg(a.parent_logw + h) + (lws + l_empty) + static_cast<double>(ms) * ln_miss;
+#if GLMB_SAMP_DEBUG != 3
     if (a.hash) a.hash[q] = fps;
+#endif
   }
+  stamp(4);
 }
 
 // ------------------------------------------------------------------ dedup
