@@ -304,9 +304,63 @@ def compat_traffic(T: int, P: int, M: int):
         return None
 
 
+def reweight_bytes(st, k: int) -> int:
+    """Algorithmic bytes of step k's reweight on this rank: x, y, w read and w written (16 B per
+    particle) for a track with an assigned measurement, w copied (8 B) for one without."""
+    th = np.asarray(st.scene.theta[k % len(st.scene.theta)])
+    cols = set(int(c) - 1 for c in th[th > 0])
+    hit = sum(1 for c in st.col_of_row if int(c) in cols)
+    return st.P * (16 * hit + 8 * (st.T_local - hit))
+
+
+def hbm_back_to_back(st, stream, dev, k: int):
+    """Back-to-back launch durations of the step's HBM-bound kernels on the current state:
+    predict (survivors into a scratch state) and reweight (new weights into a scratch
+    buffer) -- every launch reads the same inputs and writes the same scratch, so the
+    state of the timed steps is untouched."""
+    import torch
+    from paper_2512_06230_b200 import _lib as L
+    out = {}
+    scratch = L.Particles(torch.empty_like(st.particles.data), st.P)
+    if st.T_surv:
+        src, dst = st.survivors(), scratch.rows(0, st.T_surv)
+        out["predict"] = back_to_back_ms(
+            lambda: L.glmb_predict(src, dst, st.gid[:st.T_surv], st.cfg.dt, st.cfg.sigma_a, st.cfg.sigma_w,
+                                   st.seed, k, stream), stream, dev)
+    if st.contiguous and st.T_local:
+        zi = k % len(st.Z)
+        w_out = torch.empty_like(st.weights())
+        ln, fl = torch.empty_like(st.out.log_norm), torch.empty_like(st.out.flags)
+        out["reweight"] = back_to_back_ms(
+            lambda: L.glmb_reweight(st.particles, st.Z[zi], st.R, st.theta[zi], st.col_offset, ln, fl, stream,
+                                    w_out=w_out), stream, dev)
+    del scratch
+    return out
+
+
+def back_to_back_ms(fn, stream, dev, reps: int = 10, trials: int = 5) -> float:
+    """Mean launch duration of `fn` (one kernel launch on `stream`) over `reps` launches back to
+    back between two events, queued behind a busy GPU so no host gap enters; median of
+    `trials`.  A single launch between two events also carries a fixed ~8 us of event and
+    launch overhead (profiles/reweight_time.py), which this amortises."""
+    import torch
+    out = []
+    for _ in range(trials):
+        with torch.cuda.stream(stream):
+            torch.cuda._sleep(1_000_000)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(reps):
+                fn()
+            e1.record(stream)
+        torch.cuda.synchronize(dev)
+        out.append(e0.elapsed_time(e1) / reps)
+    return float(statistics.median(out))
+
+
 def make_line(*, cfg_id, cfg, world, steps, warmup, elapsed_ms, evals_total, pairs_per_launch,
               stage_ms, sm_count, clocks, T_surv, B_local, T_local, P, M_mean, traffic, e2e, cpu,
-              reweight_launches=1):
+              reweight_launches=1, b2b_ms=None, reweight_bytes=None):
     """The one JSON line of the GPU arm (pure function of the measurements)."""
     f_max = (clocks.get("sm_max_mhz") or 1965.0) * 1e6
     peak = sm_count * COMPAT_PAIRS_PER_CLK_PER_SM * f_max
@@ -316,9 +370,17 @@ def make_line(*, cfg_id, cfg, world, steps, warmup, elapsed_ms, evals_total, pai
     hbm = hbm_peak()
 
     def hbm_kernel(name, nbytes):
-        gbps = nbytes / (stage_mean[name] * 1e-3) / 1e9 if stage_mean[name] > 0 else 0.0
-        return {"bound": "hbm", "bytes_per_launch": nbytes, "achieved_GBps": gbps,
-                "peak_GBps": hbm, "frac": gbps / hbm}
+        nbytes = int(nbytes)
+        gbps1 = nbytes / (stage_mean[name] * 1e-3) / 1e9 if stage_mean[name] > 0 else 0.0
+        ms = (b2b_ms or {}).get(name)
+        if ms is None:   # only the serialised step's single launches were timed
+            return {"bound": "hbm", "bytes_per_launch": nbytes, "achieved_GBps": gbps1,
+                    "peak_GBps": hbm, "frac": gbps1 / hbm}
+        gbps = nbytes / (ms * 1e-3) / 1e9
+        return {"bound": "hbm", "bytes_per_launch": nbytes, "achieved_GBps": gbps, "peak_GBps": hbm,
+                "frac": gbps / hbm, "ms_per_launch": ms,
+                "timing": "mean of 10 launches back to back between two events (same inputs)",
+                "single_launch_frac": gbps1 / hbm}
 
     sm_mhz = clocks.get("sm_mhz")
     return {
@@ -351,7 +413,10 @@ def make_line(*, cfg_id, cfg, world, steps, warmup, elapsed_ms, evals_total, pai
                      "traffic": traffic},
         "hbm_kernels": {"predict": hbm_kernel("predict", T_surv * P * 40),
                         "birth": hbm_kernel("birth", B_local * P * 24),
-                        "reweight": hbm_kernel("reweight", T_local * P * 16)},
+                        "reweight": dict(hbm_kernel("reweight", reweight_bytes if reweight_bytes is not None
+                                                    else T_local * P * 16),
+                                         bytes_basis="16 B per particle of a track with a measurement (x, y, w "
+                                                     "read, w written), 8 B of one without (w copied)")},
         "stages_ms": stage_mean,
         "gpu_launches": ((1 if T_surv else 0) + (1 if B_local else 0) + 1 + reweight_launches) * steps,
         "clocks": clocks,
@@ -523,15 +588,30 @@ def bench_update(a, st, scene, cfg, dev, stream, L):
     P = st.P
     hbm = hbm_peak()
 
+    def hbm_stage_ms(nbytes, ms):
+        gbps = nbytes / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
+        return {"bytes": int(nbytes), "achieved_GBps": gbps, "peak_GBps": hbm, "frac": gbps / hbm, "ms_per_launch": ms}
+
     def hbm_stage(name, nbytes):
-        gbps = nbytes / (stage_mean[name] * 1e-3) / 1e9 if stage_mean[name] > 0 else 0.0
-        return {"bytes": int(nbytes), "achieved_GBps": gbps, "peak_GBps": hbm, "frac": gbps / hbm}
+        return hbm_stage_ms(nbytes, stage_mean[name])
 
     # algorithmic bytes: reweight_pairs reads x, y, w and writes w' (16 B per particle and
     # pair); resample reads w' (4 B) and, per resampled pair, gathers 5 state fields (20 B)
     # and writes 6 (24 B), per kept pair copies 6 fields (24 + 24 B)
-    hbm_f2 = {"reweight_pairs": hbm_stage("reweight_pairs", 16 * P * n_pairs),
+    plen = np.diff(pu.pair_ptr[:n_pairs + 1].cpu().numpy()) if n_pairs else np.zeros(0, np.int64)
+    rp_bytes = P * (16 * int((plen > 0).sum()) + 8 * int((plen == 0).sum()))
+    hbm_f2 = {"reweight_pairs": hbm_stage("reweight_pairs", rp_bytes),
               "resample": hbm_stage("resample", P * (4 * n_pairs + 44 * n_res + 48 * (n_pairs - n_res)))}
+    # the pair update again, 10 launches back to back on the last update's pair lists (idempotent:
+    # reads the predicted particles, writes w_new); the headline frac, the single launch beside it
+    K = min(pu.K_cap, max(1, a.h_max * T))
+    ms_rp = back_to_back_ms(lambda: L.glmb_reweight_pairs(st.particles, Z, st.R, K, pu.n_pairs, pu.pair_track,
+                                                          pu.pair_ptr, pu.pair_meas, pu.w_new[:K], pu.log_norm,
+                                                          pu.flags, pu.ess, stream), stream, dev)
+    rp_single = hbm_f2["reweight_pairs"]["frac"]
+    hbm_f2["reweight_pairs"] = dict(hbm_stage_ms(rp_bytes, ms_rp), single_launch_frac=rp_single,
+                                    pairs_without_measurement=int((plen == 0).sum()),
+                                    timing="mean of 10 launches back to back between two events (same inputs)")
     # the two-stage sampler's bound (R24): one Philox4x32-10 block per (sample, parent track quad)
     # and per (sample, row quad holding a parent entry) -- 10 rounds of 2 IMAD.WIDE.U32 (FMA-heavy
     # pipe, 64 lanes/clk/SM) and 2 LOP3 (ALU pipe, 64 lanes/clk/SM), the two pipes in parallel --
@@ -803,6 +883,7 @@ def main():
     for m in all_marks:
         for n, (m0, m1) in zip(stage_names, zip(m[:-1], m[1:])):
             stage_ms[n].append(m0.elapsed_time(m1))
+    b2b = hbm_back_to_back(st, stream, dev, a.warmup)
     evals_local = sum(st.evals(k) for k in range(a.warmup, a.warmup + a.steps))
     pairs_local = sum(len(scene.Z[k % len(scene.Z)]) * st.T_local * st.P
                       for k in range(a.warmup, a.warmup + a.steps))
@@ -942,7 +1023,8 @@ def main():
         stage_ms=stage_ms, sm_count=L.glmb_sm_count(local), clocks=sampler.summary(),
         T_surv=st.T_surv, B_local=st.B_local, T_local=st.T_local, P=st.P, M_mean=float(np.mean(Ms)),
         traffic=compat_traffic(st.T_local, st.P, len(scene.Z[0])), e2e=e2e, cpu=cpu,
-        reweight_launches=1 if st.contiguous else 2)
+        reweight_launches=1 if st.contiguous else 2, b2b_ms=b2b,
+        reweight_bytes=statistics.mean(reweight_bytes(st, k) for k in range(a.warmup, a.warmup + a.steps)))
     line["gather"] = gather
     if world > 1:
         line["schedule"] = ("per step: the packed Z_k/theta_k broadcast, predict, birth, compat with reweight "

@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) rows_fill_kernel(RowsArgs a) {
 // per lane.  The samples' alive / detected sets live in shared memory as [word][lane].
 #ifndef GLMB_SAMP_DEBUG
 #define GLMB_SAMP_DEBUG 0  // A/B timing builds only: 1 skips stage 1's Philox, 2 skips stage 2, 3 stamps phases
+                           // (16 %globaltimer slots per CTA in the fingerprint output: profiles/sampler_phases.py)
 #endif
 #ifndef GLMB_SAMP_WARPS
 #define GLMB_SAMP_WARPS 16
@@ -346,7 +347,7 @@ __global__ void __launch_bounds__(kSampThreads, GLMB_SAMP_BLOCKS) assoc_sample_k
     if (threadIdx.x == 0) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      a.hash[6 * blockIdx.x + k] = t;
+      a.hash[16 * blockIdx.x + k] = t;
     }
   };
   stamp(0);
@@ -371,6 +372,7 @@ __global__ void __launch_bounds__(kSampThreads, GLMB_SAMP_BLOCKS) assoc_sample_k
   if (a.n_count > 0)
     for (int32_t k = threadIdx.x; k < 32 * cwords; k += kSampThreads) cnt[k] = 0u;
   __syncthreads();
+  stamp(10);
   auto in_parent = [&](int32_t j) { return ((pmask[j >> 5] >> (j & 31)) & 1u) != 0u; };
 
   // ---- the parent's rows (pool), filtered in ascending column order.  A stable
@@ -400,6 +402,7 @@ __global__ void __launch_bounds__(kSampThreads, GLMB_SAMP_BLOCKS) assoc_sample_k
       }
     }
     __syncthreads();
+    stamp(11);
     for (int32_t w0 = 0; w0 < nwords; w0 += kSampThreads) {
       const int32_t w = w0 + threadIdx.x;
       int32_t tot;
@@ -408,6 +411,7 @@ __global__ void __launch_bounds__(kSampThreads, GLMB_SAMP_BLOCKS) assoc_sample_k
       kept += tot;
     }
     __syncthreads();
+    stamp(12);
     const int32_t total = kept;
     auto K = [&](int32_t x) -> int32_t {
       const int32_t d = x - r0, w = d >> 5;
@@ -465,6 +469,7 @@ __global__ void __launch_bounds__(kSampThreads, GLMB_SAMP_BLOCKS) assoc_sample_k
   }
   if (threadIdx.x == 0) use_smem = static_cast<int64_t>(rows_at + 16 * static_cast<size_t>(kept)) <= avail;
   __syncthreads();
+  stamp(13);
 
   const bool sm_rows = use_smem;
   const double *flv = reinterpret_cast<const double *>(pool + rows_at);
@@ -514,6 +519,7 @@ __global__ void __launch_bounds__(kSampThreads, GLMB_SAMP_BLOCKS) assoc_sample_k
       n_nzr = cr;
     }
   }
+  stamp(14);
   // ---- theta rows of the CTA's samples zero-filled (coalesced); stage 2 stores the picks
   const bool vec_store = ((a.ldm & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.theta) & 15) == 0);
   const int32_t n_s = min(32, a.H_up - 32 * g);

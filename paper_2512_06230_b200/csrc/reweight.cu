@@ -30,6 +30,9 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+#ifndef GLMB_RW_DEBUG
+#define GLMB_RW_DEBUG 0   // A/B timing builds only: 3 stamps the e-cache kernel's phases into w_out
+#endif
 #ifndef GLMB_RW_ECACHE_BLOCKS
 #define GLMB_RW_ECACHE_BLOCKS 4
 #endif
@@ -823,7 +826,6 @@ __device__ __forceinline__ void reweight_ecache_unit(const ReweightArgs &a, cons
   __shared__ SList S;
   __shared__ double red[3][kWarps];
   __shared__ uint32_t masks[kRows * kWarps];
-  __shared__ double bc[3];
   __shared__ double cq[6];   // zbar x, y; n qa, n qb, n qc; C0
   __shared__ float c32[7];   // zbar split into (hi, lo) floats for x and y; n qa, n qb, n qc
   const bool pairs = a.pair_track != nullptr;
@@ -838,6 +840,20 @@ __device__ __forceinline__ void reweight_ecache_unit(const ReweightArgs &a, cons
   const bool copy_out = pairs || a.w_out != a.w;
   const int quads = a.P >> 2;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#if GLMB_RW_DEBUG == 3   // A/B timing build: %globaltimer per phase, stored over the unit's first weights at the end
+  __shared__ unsigned long long tst[8];
+  auto stamp = [&](int k) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      tst[k] = t;
+    }
+  };
+  stamp(0);
+#else
+  auto stamp = [](int) {};
+#endif
   // the first quad's loads are issued before the S scan, so the two latencies overlap
   float4 X0, Y0, W0;
   if (static_cast<int>(threadIdx.x) < quads) {
@@ -865,7 +881,6 @@ __device__ __forceinline__ void reweight_ecache_unit(const ReweightArgs &a, cons
       a.flags[u] = 0u;
       if (a.ess != nullptr) a.ess[u] = sw2 > 0.0 ? static_cast<float>(sw * sw / sw2) : 0.0f;
     }
-    __syncthreads();
     return;
   }
   const bool centred = S.in_smem;
@@ -894,7 +909,10 @@ __device__ __forceinline__ void reweight_ecache_unit(const ReweightArgs &a, cons
     c32[6] = static_cast<float>(cq[4]);
   }
   __syncthreads();
-  // warp: max by shuffles, the lanes' sums rescaled to it; CTA: thread 0 merges the warps
+  stamp(1);
+  // warp: max by shuffles, the lanes' sums rescaled to it; CTA: after one barrier every
+  // thread merges the warps' partials itself (same order everywhere: identical results)
+  double mc = -INFINITY, sc = 0.0, s2c = 0.0;
   auto merge = [&](double m, float sm, float sm2) {
     const double mw = warp_max_d(m);
     const double f = mw == -INFINITY || m == -INFINITY ? 0.0 : static_cast<double>(ex2_approx(static_cast<float>(m - mw)));
@@ -906,15 +924,11 @@ __device__ __forceinline__ void reweight_ecache_unit(const ReweightArgs &a, cons
       red[2][warp] = sw2;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      double mb = red[0][0], sb = red[1][0], s2b = red[2][0];
+    mc = red[0][0];
+    sc = red[1][0];
+    s2c = red[2][0];
 #pragma unroll
-      for (int k = 1; k < kWarps; ++k) ms_merge(mb, sb, s2b, red[0][k], red[1][k], red[2][k]);
-      bc[0] = mb;
-      bc[1] = sb;
-      bc[2] = s2b;
-    }
-    __syncthreads();
+    for (int k = 1; k < kWarps; ++k) ms_merge(mc, sc, s2c, red[0][k], red[1][k], red[2][k]);
   };
   // pass 1: fp32 when the centred form applies, kept when the unit's max shows every weight
   // that matters is within the fp32 error budget (see ecache_pass1_f32); else fp64
@@ -925,9 +939,11 @@ __device__ __forceinline__ void reweight_ecache_unit(const ReweightArgs &a, cons
     float m32 = -INFINITY;
     ecache_pass1_f32(xs, ys, ws, e4, quads, X0, Y0, W0, c32, m32, sm, sm2);
     m = m32;
+    stamp(2);
     merge(m, sm, sm2);
-    fp64 = bc[0] != -INFINITY && bc[0] < -300.0;
-    __syncthreads();   // every thread has read bc before a rerun overwrites it
+    stamp(3);
+    fp64 = mc != -INFINITY && mc < -300.0;   // CTA-uniform
+    if (fp64) __syncthreads();   // every thread has read red before the rerun's merge overwrites it
   }
   if (fp64) {
     m = -INFINITY;
@@ -941,7 +957,6 @@ __device__ __forceinline__ void reweight_ecache_unit(const ReweightArgs &a, cons
     else ecache_pass1<false>(a, S, col, xs, ys, ws, e4, quads, X0, Y0, W0, cq, m, sm, sm2);
     merge(m, sm, sm2);
   }
-  const double mc = bc[0], sc = bc[1], s2c = bc[2];
   if (mc == -INFINITY) {  // every weight zero: uniform reset, flagged (never abort)
     const float uw = 1.0f / static_cast<float>(a.P);
     for (int g = threadIdx.x; g < quads; g += kThreads) __stcs(wo + g, make_float4(uw, uw, uw, uw));
@@ -950,7 +965,6 @@ __device__ __forceinline__ void reweight_ecache_unit(const ReweightArgs &a, cons
       a.flags[u] = 1u;
       if (a.ess != nullptr) a.ess[u] = static_cast<float>(a.P);
     }
-    __syncthreads();
     return;
   }
   // pass 2: w'_p = e_p 2^(m_t - m) / s from the thread's own parked entries
@@ -959,6 +973,15 @@ __device__ __forceinline__ void reweight_ecache_unit(const ReweightArgs &a, cons
     const float4 e = e4[g];
     __stcs(wo + g, make_float4(e.x * ft, e.y * ft, e.z * ft, e.w * ft));
   }
+#if GLMB_RW_DEBUG == 3
+  stamp(4);
+  if (threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    tst[5] = smid;
+    for (int k = 0; k < 6; ++k) reinterpret_cast<unsigned long long *>(wo)[k] = tst[k];
+  }
+#endif
   if (threadIdx.x == 0) {
     const double ln2 = 0.69314718055994530942;
     const double c0 = centred ? cq[5] : 0.0;   // the centred form's constant term
@@ -966,13 +989,15 @@ __device__ __forceinline__ void reweight_ecache_unit(const ReweightArgs &a, cons
     a.flags[u] = 0u;
     if (a.ess != nullptr) a.ess[u] = static_cast<float>(sc * sc / s2c);
   }
-  __syncthreads();  // S, red, bc and cq are reused by the next unit
 }
 
 __global__ void __launch_bounds__(kThreads, GLMB_RW_ECACHE_BLOCKS) reweight_ecache_kernel(const ReweightArgs a) {
   grid_dep_wait();
   const int n_units = a.n_units_dev != nullptr ? min(a.T, __ldg(a.n_units_dev)) : a.T;
-  for (int u = blockIdx.x; u < n_units; u += gridDim.x) reweight_ecache_unit(a, u);
+  for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+    if (u != static_cast<int>(blockIdx.x)) __syncthreads();   // S, red, cq reused by the next unit
+    reweight_ecache_unit(a, u);
+  }
 }
 
 template <int CL, int R>

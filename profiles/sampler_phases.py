@@ -32,11 +32,15 @@ hu = HypothesisUpdate(T, st.M_max, 100, 100, 100)
 for _ in range(3):
     hu.run(st.out.C_tracks, st.out.gate, M, dv(ps), dv(pm.view(np.int32)), dv(plw), c.p_d, c.kappa, 1e-5, c.seed, 0)
 torch.cuda.synchronize()
-ts = hu.hash[:400 * 6].cpu().numpy().astype(np.int64).reshape(400, 6)[:, :5]
+raw = hu.hash[:400 * 16].cpu().numpy().astype(np.int64).reshape(400, 16)
+order = [0, 10, 11, 12, 13, 14, 1, 2, 3, 4]
+names = ["init+zero smem", "filter ballot", "scan", "rows fill", "pw/nzq scans", "theta zero-fill",
+         "stage1", "stage2", "finalize"]
+ts = raw[:, order]
 t0 = ts[:, 0].min()
 ts = (ts - t0) / 1e3
 d = np.diff(ts, axis=1)
 print("CTA start  min/median/max us:", ts[:, 0].min(), np.median(ts[:, 0]), ts[:, 0].max())
-print("CTA end    min/median/max us:", ts[:, 4].min(), np.median(ts[:, 4]), ts[:, 4].max())
-for name, col in zip(("setup", "stage1", "stage2", "finalize"), d.T):
-    print(f"{name:9s} mean {col.mean():7.2f} us  median {np.median(col):7.2f}  max {col.max():7.2f}")
+print("CTA end    min/median/max us:", ts[:, -1].min(), np.median(ts[:, -1]), ts[:, -1].max())
+for name, col in zip(names, d.T):
+    print(f"{name:16s} mean {col.mean():7.2f} us  median {np.median(col):7.2f}  max {col.max():7.2f}")
