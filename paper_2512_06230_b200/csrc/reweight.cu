@@ -979,7 +979,8 @@ __device__ __forceinline__ void reweight_ecache_unit(const ReweightArgs &a, cons
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     tst[5] = smid;
-    for (int k = 0; k < 6; ++k) reinterpret_cast<unsigned long long *>(wo)[k] = tst[k];
+    tst[6] = fp64 ? 1ull : 0ull;
+    for (int k = 0; k < 7; ++k) reinterpret_cast<unsigned long long *>(wo)[k] = tst[k];
   }
 #endif
   if (threadIdx.x == 0) {

@@ -17,26 +17,36 @@ from paper_2512_06230_b200.step import GlmbStep  # noqa: E402
 
 torch.cuda.set_device(0)
 L.glmb_init(0)
-sc = make_scene(3, steps=1)
+# argv[1] = N: the state after N steps of predict + reweight (the bench's late-step state), else fresh
+N = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+sc = make_scene(3, steps=max(N, 1) + 1)
 st = GlmbStep(sc)
-for k in range(6):
-    st.predict(k)
-st.birth(0)
+if N == 0:
+    for k in range(6):
+        st.predict(k)
+else:
+    for k in range(N):
+        st.predict(k)
+        st.birth(k)
+        st.reweight(k, out_of_place=True)
+K = N
+st.birth(K)
 for rep in range(4):
-    st.reweight(0, out_of_place=True)
+    st.reweight(K, out_of_place=True)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
-st.reweight(0, out_of_place=True)
+st.reweight(K, out_of_place=True)
 e1.record()
 torch.cuda.synchronize()
 print(f"launch {e0.elapsed_time(e1) * 1e3:.1f} us (stamped build)")
 w = st.weights()
 T = st.T_local
-ts = w[:, :12].contiguous().view(torch.int64).cpu().numpy()[:, :6]
+ts = w[:, :14].contiguous().view(torch.int64).cpu().numpy()[:, :7]
 ok = (np.abs(ts[:, 0] - np.median(ts[:, 0])) < 10**7) & (np.abs(ts[:, 4] - np.median(ts[:, 0])) < 10**7)
 print(f"units with stamps: {ok.sum()} of {len(ok)} (the rest took the |S_j| = 0 path)")
 ts = ts[ok]
+print(f"units rerun in fp64: {int(ts[:, 6].sum())} of {len(ts)}")
 sm = ts[:, 5]
 ts = ts[:, :5]
 t0 = ts[:, 0].min()
