@@ -248,7 +248,7 @@ def reference_arm(a, cfg_id, budget_s: float = 240.0):
     from paper_2512_06230_b200.scenes import CONFIGS
     cfg = CONFIGS[cfg_id]
     cores = host_cores()
-    n_steps = min(cfg.steps, a.warmup + a.steps)
+    n_steps = max(cfg.steps, a.warmup + a.steps)   # the GPU arm's steps use the same Z_k (prefix-stable)
     # calibrate on a few tracks: seconds per track-step
     n0 = max(1, min(cfg.T, cores))
     cal = OracleStep(cfg_id, n_steps, n0, cores)
@@ -360,7 +360,7 @@ def back_to_back_ms(fn, stream, dev, reps: int = 10, trials: int = 5) -> float:
 
 def make_line(*, cfg_id, cfg, world, steps, warmup, elapsed_ms, evals_total, pairs_per_launch,
               stage_ms, sm_count, clocks, T_surv, B_local, T_local, P, M_mean, traffic, e2e, cpu,
-              reweight_launches=1, b2b_ms=None, reweight_bytes=None):
+              reweight_launches=1, b2b_ms=None, reweight_bytes=None, reweight_bytes_b2b=None):
     """The one JSON line of the GPU arm (pure function of the measurements)."""
     f_max = (clocks.get("sm_max_mhz") or 1965.0) * 1e6
     peak = sm_count * COMPAT_PAIRS_PER_CLK_PER_SM * f_max
@@ -369,13 +369,14 @@ def make_line(*, cfg_id, cfg, world, steps, warmup, elapsed_ms, evals_total, pai
     achieved = pairs_per_launch / (stage_mean["compat"] * 1e-3)
     hbm = hbm_peak()
 
-    def hbm_kernel(name, nbytes):
+    def hbm_kernel(name, nbytes, nbytes_b2b=None):
         nbytes = int(nbytes)
         gbps1 = nbytes / (stage_mean[name] * 1e-3) / 1e9 if stage_mean[name] > 0 else 0.0
         ms = (b2b_ms or {}).get(name)
         if ms is None:   # only the serialised step's single launches were timed
             return {"bound": "hbm", "bytes_per_launch": nbytes, "achieved_GBps": gbps1,
                     "peak_GBps": hbm, "frac": gbps1 / hbm}
+        nbytes = int(nbytes_b2b) if nbytes_b2b is not None else nbytes
         gbps = nbytes / (ms * 1e-3) / 1e9
         return {"bound": "hbm", "bytes_per_launch": nbytes, "achieved_GBps": gbps, "peak_GBps": hbm,
                 "frac": gbps / hbm, "ms_per_launch": ms,
@@ -414,7 +415,7 @@ def make_line(*, cfg_id, cfg, world, steps, warmup, elapsed_ms, evals_total, pai
         "hbm_kernels": {"predict": hbm_kernel("predict", T_surv * P * 40),
                         "birth": hbm_kernel("birth", B_local * P * 24),
                         "reweight": dict(hbm_kernel("reweight", reweight_bytes if reweight_bytes is not None
-                                                    else T_local * P * 16),
+                                                    else T_local * P * 16, reweight_bytes_b2b),
                                          bytes_basis="16 B per particle of a track with a measurement (x, y, w "
                                                      "read, w written), 8 B of one without (w copied)")},
         "stages_ms": stage_mean,
@@ -427,7 +428,7 @@ def make_line(*, cfg_id, cfg, world, steps, warmup, elapsed_ms, evals_total, pai
 
 
 # ------------------------------------------------------------------ GLMB update
-def skip_probe(st, dev, L, reps: int = 10) -> dict:
+def skip_probe(st, dev, L, reps: int = 10, k_late: int = 0) -> dict:
     """Exact zero-tile skipping (glmb_compat_skipping, opt-in, not the headline): compat dense and
     skipping on the step-0 clouds (a fresh copy of the scene, births drawn) and on the bench's
     own state after its timed steps (diffused clouds), CUDA-event means over `reps` launches;
@@ -442,8 +443,8 @@ def skip_probe(st, dev, L, reps: int = 10) -> dict:
                    "whitened units^2 from the tile's bounding box (contributions exactly +0 on both exp paths); "
                    "opt-in, the headline is the dense pass and counts the dense pairs"}
     sm = L.glmb_sm_count(dev.index or 0)
-    for name, g in (("step0", fresh), ("late_state", st)):
-        Z = g.Z[0]
+    for name, g, kz in (("step0", fresh, 0), ("late_state", st, k_late)):
+        Z = g.Z[kz % len(g.Z)]   # the measurements of the step the clouds were last predicted to
         M = Z.shape[0]
         c = g.cfg
         Cs, Gs = torch.empty_like(g.out.C_tracks), torch.empty_like(g.out.gate)
@@ -513,7 +514,7 @@ def verify_fused_gather(sh, dev, stream) -> bool:
     return bool(flag.item())
 
 
-def bench_update(a, st, scene, cfg, dev, stream, L):
+def bench_update(a, st, scene, cfg, dev, stream, L, k_last: int):
     """The hypothesis update and particle loop that consume the step's C_k:
     death_prob -> compat_rows -> assoc_sample -> dedup -> prune -> assoc_pairs ->
     reweight_pairs -> resample, on the device-resident C_k / particles of the last timed
@@ -523,7 +524,7 @@ def bench_update(a, st, scene, cfg, dev, stream, L):
     from paper_2512_06230_b200.hyp import HypothesisUpdate, ParticleUpdate
     from paper_2512_06230_b200.scenes import hypothesis_inputs
     T = st.T_local
-    zi = (a.warmup + a.steps - 1) % len(st.Z)
+    zi = k_last % len(st.Z)    # the step whose C_k and particles the update consumes
     Z = st.Z[zi]
     M = Z.shape[0]
     pm, plw, ps = hypothesis_inputs(cfg.T, cfg.B, a.h_old, seed=cfg.seed)
@@ -780,7 +781,14 @@ def main():
     L.glmb_init(local)
     dev = torch.device("cuda", local)
     cfg = CONFIGS[cfg_id]
-    n_steps_scene = min(cfg.steps, a.warmup + a.steps)
+    # Every executed step k uses the scene's own Z_k, theta_k (the truth moves on with the
+    # predicted clouds): the timed loop runs steps [0, W + K), the serialised per-kernel pass
+    # [W + K, W + 2K), the end-to-end legs (W + K) each after that -- the sequence is generated
+    # that long (prefix-stable: step k's data do not depend on the length), past BASELINE's
+    # own step count where that is shorter.
+    k_iso = a.warmup + a.steps                  # first step of the serialised pass
+    k_e2e = k_iso + a.steps                     # first step of the end-to-end legs
+    n_steps_scene = max(cfg.steps, k_e2e + 2 * (a.warmup + a.steps))
     stream = torch.cuda.Stream(device=dev)
     side = torch.cuda.Stream(device=dev)   # reweight overlaps compat (double-buffered weights)
     ev = lambda: torch.cuda.Event(enable_timing=True)
@@ -878,12 +886,12 @@ def main():
         barrier()
     elapsed_ms = t_start.elapsed_time(t_end)
     # per-kernel durations: the same steps again, serialised (outside the timed region)
-    all_marks = [isolated_step(k) for k in range(a.warmup, a.warmup + a.steps)]
+    all_marks = [isolated_step(k) for k in range(k_iso, k_e2e)]
     torch.cuda.synchronize(dev)
     for m in all_marks:
         for n, (m0, m1) in zip(stage_names, zip(m[:-1], m[1:])):
             stage_ms[n].append(m0.elapsed_time(m1))
-    b2b = hbm_back_to_back(st, stream, dev, a.warmup)
+    b2b = hbm_back_to_back(st, stream, dev, k_e2e - 1)
     evals_local = sum(st.evals(k) for k in range(a.warmup, a.warmup + a.steps))
     pairs_local = sum(len(scene.Z[k % len(scene.Z)]) * st.T_local * st.P
                       for k in range(a.warmup, a.warmup + a.steps))
@@ -898,7 +906,7 @@ def main():
     # ---- the hypothesis update on this step's C_k (before the e2e legs step the particles on)
     update = None
     if world == 1 and not a.no_update:
-        update = bench_update(a, st, scene, cfg, dev, stream, L)
+        update = bench_update(a, st, scene, cfg, dev, stream, L, k_e2e - 1)
 
     # ---- launch-bound small configs: one whole step (glmb_step) captured in a CUDA graph
     graphs = None
@@ -952,24 +960,28 @@ def main():
             M = Zh[zi].shape[0]
             return M * 12, M * 4 + st.T_local * st.ldc * 4 + st.T_local * st.ldg * 4 + st.T_local * 8
 
-        def timed(fn):
+        def timed(fn, k0):
+            """W warm-up then K timed steps of the leg from scene step k0; returns the seconds,
+            the bytes per step and the whole job's evals of the timed steps."""
             h2d = d2h = 0
-            for k in range(a.warmup):
+            for k in range(k0, k0 + a.warmup):
                 fn(k)
             if world > 1:
                 barrier()
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
-            for k in range(a.warmup, a.warmup + a.steps):
+            for k in range(k0 + a.warmup, k0 + a.warmup + a.steps):
                 hb, db = fn(k)
                 h2d += hb
                 d2h += db
             sec = time.perf_counter() - t0
+            ev_loc = float(sum(st.evals(k) for k in range(k0 + a.warmup, k0 + a.warmup + a.steps)))
             if world > 1:
-                t = torch.tensor([sec], dtype=torch.float64, device=coll_dev)
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                sec = float(t[0])
-            return sec, h2d // a.steps, d2h // a.steps
+                t = torch.tensor([sec, ev_loc], dtype=torch.float64, device=coll_dev)
+                tmax = t.clone(); dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
+                tsum = t.clone(); dist.all_reduce(tsum[1:], op=dist.ReduceOp.SUM)
+                sec, ev_loc = float(tmax[0]), float(tsum[1])
+            return sec, h2d // a.steps, d2h // a.steps, ev_loc
 
         def host_step_dist(k):
             """W > 1: ShardedStep.step_host_csr -- rank 0's pinned Z_k / theta_k H2D, the broadcast,
@@ -979,8 +991,8 @@ def main():
             return hb, db
 
         if sh is not None:
-            e2e_s, h2d, d2h = timed(host_step_dist)
-            e2e = {"value": evals_total / e2e_s, "unit": "evals/s",
+            e2e_s, h2d, d2h, e2e_ev = timed(host_step_dist, k_e2e)
+            e2e = {"value": e2e_ev / e2e_s, "unit": "evals/s",
                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                    "ms_per_step": e2e_s * 1e3 / a.steps,
                    "note": "dist.ShardedStep.step_host_csr: rank 0's pinned H2D of Z_k, theta_k; the broadcast; "
@@ -988,15 +1000,15 @@ def main():
                            "stores) and the log_norm/flags gather; rank 0 builds the CSR of the gathered C_k and "
                            "reads it back with log_norm and flags; synchronised each step; max over ranks"}
     if not a.no_e2e and sh is None:
-        e2e_s, h2d, d2h = timed(host_step_csr)
-        dn_s, dn_h2d, dn_d2h = timed(host_step_dense)
-        e2e = {"value": evals_total / e2e_s, "unit": "evals/s",
+        e2e_s, h2d, d2h, e2e_ev = timed(host_step_csr, k_e2e)
+        dn_s, dn_h2d, dn_d2h, dn_ev = timed(host_step_dense, k_e2e + a.warmup + a.steps)
+        e2e = {"value": e2e_ev / e2e_s, "unit": "evals/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": e2e_s * 1e3 / a.steps,
                "note": "glmb_step_host_csr: pinned H2D of Z_k, theta_k; the step (reweight into the spare "
                        "weights beside compat); C_k's gated entries as CSR (row_ptr, col, val) + log_norm, "
                        "flags D2H; synchronised each step; particle state resident on the device",
-               "dense": {"value": evals_total / dn_s, "ms_per_step": dn_s * 1e3 / a.steps,
+               "dense": {"value": dn_ev / dn_s, "ms_per_step": dn_s * 1e3 / a.steps,
                          "h2d_bytes_per_step": dn_h2d, "d2h_bytes_per_step": dn_d2h,
                          "note": "glmb_step_host: the same with C_k and the gate words read back dense "
                                  "(on a copy stream overlapping reweight)"}}
@@ -1011,7 +1023,8 @@ def main():
         convoy = bench_convoy(dev)
     skipped = None
     if world == 1 and not a.no_skip_probe:
-        skipped = skip_probe(st, dev, L)
+        k_done = k_e2e + (0 if a.no_e2e else (a.warmup + a.steps) * (1 if sh is not None else 2)) - 1
+        skipped = skip_probe(st, dev, L, k_late=k_done if not a.no_e2e else k_e2e - 1)
 
     cpu = None
     if world == 1 and not a.no_cpu_baseline:
@@ -1024,7 +1037,8 @@ def main():
         T_surv=st.T_surv, B_local=st.B_local, T_local=st.T_local, P=st.P, M_mean=float(np.mean(Ms)),
         traffic=compat_traffic(st.T_local, st.P, len(scene.Z[0])), e2e=e2e, cpu=cpu,
         reweight_launches=1 if st.contiguous else 2, b2b_ms=b2b,
-        reweight_bytes=statistics.mean(reweight_bytes(st, k) for k in range(a.warmup, a.warmup + a.steps)))
+        reweight_bytes=statistics.mean(reweight_bytes(st, k) for k in range(k_iso, k_e2e)),
+        reweight_bytes_b2b=reweight_bytes(st, k_e2e - 1))
     line["gather"] = gather
     if world > 1:
         line["schedule"] = ("per step: the packed Z_k/theta_k broadcast, predict, birth, compat with reweight "
