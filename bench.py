@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--no-convoy", action="store_true", help="skip the paper-shaped convoy run (f4)")
     ap.add_argument("--no-graphs", action="store_true", help="skip the CUDA-graph timing of configs 0-2")
     ap.add_argument("--no-skip-probe", action="store_true", help="skip the exact zero-tile skipping probe")
+    ap.add_argument("--no-b2b", action="store_true",
+                    help="skip the back-to-back launch timing of the HBM-bound kernels (ncu launch lists)")
     return ap.parse_args()
 
 
@@ -606,13 +608,14 @@ def bench_update(a, st, scene, cfg, dev, stream, L, k_last: int):
     # the pair update again, 10 launches back to back on the last update's pair lists (idempotent:
     # reads the predicted particles, writes w_new); the headline frac, the single launch beside it
     K = min(pu.K_cap, max(1, a.h_max * T))
-    ms_rp = back_to_back_ms(lambda: L.glmb_reweight_pairs(st.particles, Z, st.R, K, pu.n_pairs, pu.pair_track,
-                                                          pu.pair_ptr, pu.pair_meas, pu.w_new[:K], pu.log_norm,
-                                                          pu.flags, pu.ess, stream), stream, dev)
+    rp_call = lambda: L.glmb_reweight_pairs(st.particles, Z, st.R, K, pu.n_pairs, pu.pair_track, pu.pair_ptr,  # noqa: E731
+                                            pu.pair_meas, pu.w_new[:K], pu.log_norm, pu.flags, pu.ess, stream)
+    ms_rp = stage_mean["reweight_pairs"] if a.no_b2b else back_to_back_ms(rp_call, stream, dev)
     rp_single = hbm_f2["reweight_pairs"]["frac"]
     hbm_f2["reweight_pairs"] = dict(hbm_stage_ms(rp_bytes, ms_rp), single_launch_frac=rp_single,
                                     pairs_without_measurement=int((plen == 0).sum()),
-                                    timing="mean of 10 launches back to back between two events (same inputs)")
+                                    timing="single launches (--no-b2b)" if a.no_b2b else
+                                    "mean of 10 launches back to back between two events (same inputs)")
     # the two-stage sampler's bound (R24): one Philox4x32-10 block per (sample, parent track quad)
     # and per (sample, row quad holding a parent entry) -- 10 rounds of 2 IMAD.WIDE.U32 (FMA-heavy
     # pipe, 64 lanes/clk/SM) and 2 LOP3 (ALU pipe, 64 lanes/clk/SM), the two pipes in parallel --
@@ -891,7 +894,7 @@ def main():
     for m in all_marks:
         for n, (m0, m1) in zip(stage_names, zip(m[:-1], m[1:])):
             stage_ms[n].append(m0.elapsed_time(m1))
-    b2b = hbm_back_to_back(st, stream, dev, k_e2e - 1)
+    b2b = None if a.no_b2b else hbm_back_to_back(st, stream, dev, k_e2e - 1)
     evals_local = sum(st.evals(k) for k in range(a.warmup, a.warmup + a.steps))
     pairs_local = sum(len(scene.Z[k % len(scene.Z)]) * st.T_local * st.P
                       for k in range(a.warmup, a.warmup + a.steps))

@@ -18,19 +18,19 @@ timeout 900 python bench.py --impl reference > $OUT/${TAG}_bench_ref.json 2> $OU
 echo "bench reference exit $?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file $OUT/${TAG}_launches.csv python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline \
-    --no-convoy --no-graphs --no-skip-probe > $OUT/${TAG}_ncu_list.log 2>&1
+    --no-convoy --no-graphs --no-skip-probe --no-b2b > $OUT/${TAG}_ncu_list.log 2>&1
 echo "ncu list exit $?"
 python profiles/launch_summary.py $OUT/${TAG}_launches.csv > $OUT/${TAG}_launch_summary.txt 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on \
     -k regex:'compat_kernel|reweight_ecache|predict|birth' -s 8 -c 4 -o $OUT/${TAG}_full -f \
-    python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-convoy --no-graphs --no-skip-probe \
+    python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-convoy --no-graphs --no-skip-probe --no-b2b \
     --no-update > $OUT/${TAG}_ncu_full.log 2>&1
 echo "ncu full exit $?"
 python profiles/ncu_summary.py $OUT/${TAG}_full.ncu-rep > $OUT/${TAG}_ncu_full_summary.txt 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on \
     -k regex:'assoc_sample|resample_kernel|prune_kernel|invert_kernel|dedup_kernel|rows_fill|death_prob' \
     -s 14 -c 7 -o $OUT/${TAG}_upd -f \
-    python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-convoy --no-graphs --no-skip-probe \
+    python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-convoy --no-graphs --no-skip-probe --no-b2b \
     > $OUT/${TAG}_ncu_upd.log 2>&1
 echo "ncu update exit $?"
 # reweight_pairs (the e-cache kernel in pair mode): the first launch after the step's 9 theta-mode ones
