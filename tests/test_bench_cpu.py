@@ -51,3 +51,19 @@ def test_reference_arm_runs_on_cpu():
     from paper_2512_06230_b200.scenes import CONFIGS
     assert set(line["config"]) == set(bench.workload_config(0, CONFIGS[0], 1, 6.0, 1.0))
     assert "every track" in line["sample"]
+
+
+def test_reweight_bytes_counts_tracks_with_a_measurement():
+    """bench.reweight_bytes: 16 B per particle for a local track with an assigned measurement,
+    8 B (w copied) for one without; theta_i = global column + 1 (0 clutter)."""
+    import types
+
+    import numpy as np
+
+    import bench
+    th = np.array([0, 3, 3, 1, 0, 7], np.int32)          # columns 2 (twice), 0, 6
+    scene = types.SimpleNamespace(theta=[th])
+    st = types.SimpleNamespace(scene=scene, P=8, T_local=4, col_of_row=np.array([0, 1, 2, 6]))
+    assert bench.reweight_bytes(st, 0) == 8 * (16 * 3 + 8 * 1)
+    st2 = types.SimpleNamespace(scene=scene, P=8, T_local=2, col_of_row=np.array([3, 4]))   # another rank
+    assert bench.reweight_bytes(st2, 5) == 8 * (8 * 2)
