@@ -1,5 +1,6 @@
 """Every libglmb kernel once on small inputs (configs 0-1 shapes) -- the workload that
-profiles/sanitize.sh runs under compute-sanitizer memcheck / racecheck / synccheck / initcheck."""
+written to run under `compute-sanitizer --tool memcheck|racecheck|synccheck|initcheck python
+profiles/sanitize_run.py` (the tool is closed on this pool; profiles/README.md)."""
 import sys
 
 import numpy as np
