@@ -1,5 +1,4 @@
-"""Every libglmb kernel once on small inputs (configs 0-1 shapes) -- the workload that
-written to run under `compute-sanitizer --tool memcheck|racecheck|synccheck|initcheck python
+"""Every libglmb kernel once on small inputs (configs 0-1 shapes), written to run under `compute-sanitizer --tool memcheck|racecheck|synccheck|initcheck python
 profiles/sanitize_run.py` (the tool is closed on this pool; profiles/README.md)."""
 import sys
 
