@@ -415,7 +415,9 @@ def make_line(*, cfg_id, cfg, world, steps, warmup, elapsed_ms, evals_total, pai
                                                 if sm_mhz else None),
                      "traffic": traffic},
         "hbm_kernels": {"predict": hbm_kernel("predict", T_surv * P * 40),
-                        "birth": hbm_kernel("birth", B_local * P * 24),
+                        "birth": dict(hbm_kernel("birth", B_local * P * 24), bound="launch",
+                                      note="3 MB per launch at cfg3 (16 tracks): the launch and its ramp, "
+                                           "not HBM, set its time; the fraction is for reference"),
                         "reweight": dict(hbm_kernel("reweight", reweight_bytes if reweight_bytes is not None
                                                     else T_local * P * 16, reweight_bytes_b2b),
                                          bytes_basis="16 B per particle of a track with a measurement (x, y, w "
