@@ -486,8 +486,10 @@ cudaError_t launch_k(const CompatArgs &a, cudaStream_t s) {
   // headline).  Built for the default exp split only.
   if constexpr (EMU_PERIOD == -10) {
     if (a.skip)
-      return a.CL == 2 ? launch_kc<NW, K, EMU_PERIOD, 2, true>(a, s) : launch_kc<NW, K, EMU_PERIOD, 1, true>(a, s);
+      return a.CL == 4 ? launch_kc<NW, K, EMU_PERIOD, 4, true>(a, s)
+             : a.CL == 2 ? launch_kc<NW, K, EMU_PERIOD, 2, true>(a, s) : launch_kc<NW, K, EMU_PERIOD, 1, true>(a, s);
   }
+  if (a.CL == 4) return launch_kc<NW, K, EMU_PERIOD, 4, false>(a, s);
   return a.CL == 2 ? launch_kc<NW, K, EMU_PERIOD, 2, false>(a, s) : launch_kc<NW, K, EMU_PERIOD, 1, false>(a, s);
 }
 
@@ -524,14 +526,16 @@ void compat_plan(int32_t M, int32_t P, int32_t *K, int32_t *NW, int32_t *CL, int
   //   M > 128: NW = 4, K = kDefaultK (GLMB_COMPAT_K overrides: A/B runs)
   //   64 < M <= 128: NW = 2, K = 2;  32 < M <= 64: NW = 1, K = 2;  M <= 32: NW = 1, K = 1
   // CL: particle chunks per (track, measurement tile), a thread-block cluster (>= 8
-  // particle tiles per CTA); GLMB_COMPAT_CL overrides (A/B runs)
+  // particle tiles per CTA, or one each at P = 1024); GLMB_COMPAT_CL overrides (A/B runs)
   static const int32_t cl_env = [] {
     const char *e = std::getenv("GLMB_COMPAT_CL");
     return e ? std::atoi(e) : 0;
   }();
   const int32_t ptiles = (P + kTileP - 1) / kTileP;
-  int32_t cl = ptiles >= 16 ? 2 : 1;  // measured (cfg3): CL = 1 14.5, 2 15.3, 4 14.9 pairs/clk/SM
-  if (cl_env == 1 || cl_env == 2) cl = cl_env;
+  // measured (cfg3): CL = 1 14.5, 2 15.3, 4 14.9 pairs/clk/SM; at P = 1024 (4 tiles) a tile per
+  // rank: cfg1 (T_k = 68) 34 -> 23 us, the convoy (T_k ~ 800) unchanged -- small grids fill more SMs
+  int32_t cl = ptiles >= 16 ? 2 : ptiles == 4 ? 4 : 1;
+  if (cl_env == 1 || cl_env == 2 || cl_env == 4) cl = cl_env;
   *CL = cl;
   static const int32_t kmax = [] {
     const char *e = std::getenv("GLMB_COMPAT_K");
