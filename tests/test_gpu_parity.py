@@ -688,3 +688,27 @@ def test_pipelined_steps_equal_sequential(L, cfg_id):
     np.testing.assert_array_equal(a.particles.data[5].cpu().numpy(), b.weights().cpu().numpy())
     for f in ("C_tracks", "gate", "log_norm", "flags"):
         np.testing.assert_array_equal(getattr(a.out, f).cpu().numpy(), getattr(b.out, f).cpu().numpy())
+
+
+def test_compat_p1024_split_bit_identical(tmp_path):
+    """At P = 1024 (four particle tiles) compat runs a 4-CTA cluster per unit, one tile per
+    rank; rank 0's ordered merge adds the tile sums in the order one CTA would, so C and the
+    gate words equal the unsplit kernel's (GLMB_COMPAT_CL=1) bit for bit (config 1: P = 1024,
+    births included)."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    outs = {}
+    for cl in ("", "1"):
+        out = str(tmp_path / f"cl{cl or 'd'}.npz")
+        env = dict(os.environ, PYTHONPATH=os.path.dirname(here))
+        env.pop("GLMB_COMPAT_CL", None)
+        if cl:
+            env["GLMB_COMPAT_CL"] = cl
+        r = subprocess.run([sys.executable, os.path.join(here, "_compat_dump.py"), "1", "64", "3", out, "68"],
+                           env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        outs[cl] = np.load(out)
+    np.testing.assert_array_equal(outs[""]["C"].view(np.uint32), outs["1"]["C"].view(np.uint32))
+    np.testing.assert_array_equal(outs[""]["G"], outs["1"]["G"])
