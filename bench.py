@@ -77,7 +77,7 @@ def host_cores() -> int:
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """Polls NVML every 5 ms while active: SM clock, max clock, throttle reasons."""
+    """Polls NVML every 2 ms while active: SM clock, max clock, throttle reasons."""
 
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
                0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
@@ -106,10 +106,14 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:  # noqa: BLE001
                 pass
-            time.sleep(0.005)
+            time.sleep(0.002)
 
     def __enter__(self):
         if self.ok:
+            # the main thread spends the timed region enqueueing steps from Python: a short
+            # GIL switch interval lets the poller run every few ms (one sample otherwise)
+            self._switch = sys.getswitchinterval()
+            sys.setswitchinterval(0.0005)
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         return self
@@ -118,6 +122,7 @@ class ClockSampler:
         if self.ok:
             self._stop.set()
             self.t.join()
+            sys.setswitchinterval(self._switch)
 
     def summary(self):
         if not self.ok or not self.samples:
