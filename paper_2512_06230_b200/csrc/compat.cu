@@ -93,6 +93,40 @@ __device__ __forceinline__ f2 exp2_poly2_x64_neg(f2 q) {
   return f2_pack(p0, p1);
 }
 
+// Scalar mirrors of the packed ops (the same PTX rounding, no contraction): one lane of a
+// packed pair computed alone gives the packed result's bits for that lane.
+__device__ __forceinline__ float f1_add(float a, float b) {
+  float r;
+  asm("add.rn.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float f1_sub(float a, float b) {
+  float r;
+  asm("sub.rn.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float f1_mul(float a, float b) {
+  float r;
+  asm("mul.rn.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float f1_fma(float a, float b, float c) {
+  float r;
+  asm("fma.rn.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+// exp2_poly2_x64_neg for one lane
+__device__ __forceinline__ float exp2_poly1_x64_neg(float q) {
+  const float e = -fminf(q, 189.0f);
+  const float t = f1_add(e, kRound64);
+  const float f = f1_sub(e, f1_sub(t, kRound64));
+  float p = f1_fma(kC4, f, kC3);
+  p = f1_fma(p, f, kC2);
+  p = f1_fma(p, f, kC1);
+  p = f1_fma(p, f, kC0);
+  return __uint_as_float(__float_as_uint(p) + (__float_as_uint(t) << 23));
+}
+
 // 2^-q on MUFU.EX2 (the negation is an operand modifier)
 __device__ __forceinline__ f2 exp2_mufu2_neg(f2 q) {
   float q0, q1;
@@ -124,9 +158,21 @@ struct Meas {
 // AoS entry p = (X', Y', w 2^-64, w).  e = -|z' - p'|^2 from the exact difference
 // (z' = zx2 / 2 exactly): dx, dy by FFMA2, q by FMUL2 + FFMA2; the sign of -q is
 // an operand modifier of MUFU / the polynomial's adds.
-template <int H, int POLY_MASK>
+template <int H, int POLY_MASK, bool LO = false>
 __device__ __forceinline__ void particle_step(const float4 p, const f2 (&zx2)[H], const f2 (&zy2)[H],
                                               f2 (&acc)[H], int hv) {
+  if constexpr (LO) {   // H == 1 and only the pair's low slot holds measurements: that lane alone
+    float zx, zxh, zy, zyh, a0, a1;
+    f2_unpack(zx2[0], zx, zxh);
+    f2_unpack(zy2[0], zy, zyh);
+    f2_unpack(acc[0], a0, a1);
+    const float dx = f1_fma(zx, 0.5f, -p.x), dy = f1_fma(zy, 0.5f, -p.y);
+    const float q = f1_fma(dy, dy, f1_mul(dx, dx));
+    if (POLY_MASK & 1) a0 = f1_fma(p.z, exp2_poly1_x64_neg(q), a0);
+    else a0 = f1_fma(p.w, ex2_approx(-q), a0);
+    acc[0] = f2_pack(a0, a1);
+    return;
+  }
   const f2 pw = f2_pack(p.w, p.w);
   const f2 half = f2_pack(0.5f, 0.5f);
   const f2 npx = f2_pack(-p.x, -p.x), npy = f2_pack(-p.y, -p.y);
@@ -161,18 +207,18 @@ constexpr int poly_mask(int u) {
   return m;
 }
 
-template <int H, int EMU_PERIOD, int U = 0>
+template <int H, int EMU_PERIOD, bool LO, int U = 0>
 __device__ __forceinline__ void step_u(int u, const float4 p, const f2 (&zx2)[H], const f2 (&zy2)[H],
                                        f2 (&acc)[H], int hv) {
   // u is a compile-time constant after unrolling; recurse to turn it into a template argument
   if constexpr (U < (EMU_PERIOD > 0 ? EMU_PERIOD : -EMU_PERIOD)) {
-    if (u == U) particle_step<H, poly_mask<EMU_PERIOD, H>(U)>(p, zx2, zy2, acc, hv);
-    else step_u<H, EMU_PERIOD, U + 1>(u, p, zx2, zy2, acc, hv);
+    if (u == U) particle_step<H, poly_mask<EMU_PERIOD, H>(U), LO>(p, zx2, zy2, acc, hv);
+    else step_u<H, EMU_PERIOD, LO, U + 1>(u, p, zx2, zy2, acc, hv);
   }
 }
 
 // Sum over one AoS tile for this warp's first HV measurement pairs.
-template <int K, int HV, int EMU_PERIOD>
+template <int K, int HV, int EMU_PERIOD, bool LO = false>
 __device__ __forceinline__ void tile_sum(const float4 *__restrict__ A, int np, Meas<K> &m) {
   constexpr int H = Meas<K>::H;
   f2 acc[H];
@@ -184,11 +230,11 @@ __device__ __forceinline__ void tile_sum(const float4 *__restrict__ A, int np, M
 #pragma unroll 1
     for (; p + PER <= np; p += PER) {
 #pragma unroll
-      for (int u = 0; u < PER; ++u) step_u<H, EMU_PERIOD>(u, A[p + u], m.zx2, m.zy2, acc, HV);
+      for (int u = 0; u < PER; ++u) step_u<H, EMU_PERIOD, LO>(u, A[p + u], m.zx2, m.zy2, acc, HV);
     }
   }
 #pragma unroll 4
-  for (; p < np; ++p) particle_step<H, 0>(A[p], m.zx2, m.zy2, acc, HV);
+  for (; p < np; ++p) particle_step<H, 0, LO>(A[p], m.zx2, m.zy2, acc, HV);
 #pragma unroll
   for (int h = 0; h < H; ++h) {
     float lo, hi;
@@ -198,9 +244,19 @@ __device__ __forceinline__ void tile_sum(const float4 *__restrict__ A, int np, M
   }
 }
 
+// kv: measurement slots with a valid lane.  K = 2 with only the first slot valid (the
+// ragged last warp of a tile when M mod 64 <= 32) evaluates that slot alone: half the exps,
+// bit-identical sums (the packed ops lane for lane).
 template <int K, int EMU_PERIOD>
-__device__ __forceinline__ void tile_dispatch(int hv, const float4 *A, int np, Meas<K> &m) {
+__device__ __forceinline__ void tile_dispatch(int kv, bool lo, const float4 *A, int np, Meas<K> &m) {
   constexpr int H = Meas<K>::H;
+  const int hv = (kv + 1) >> 1;
+  if constexpr (K == 2) {
+    if (kv == 1 && lo) {
+      tile_sum<K, 1, EMU_PERIOD, true>(A, np, m);
+      return;
+    }
+  }
   if (hv == H) tile_sum<K, H, EMU_PERIOD>(A, np, m);
   else if constexpr (H > 1) {
     if (hv == 1) tile_sum<K, 1, EMU_PERIOD>(A, np, m);
@@ -371,7 +427,7 @@ __global__ void __launch_bounds__(32 * NW, min_blocks<NW, K>()) compat_kernel(co
     __syncthreads();           // AoS tile t complete; every warp is done with tile t-1
     if (tid == 0 && t + 1 < t_end) issue_tile(a, xs, ys, ws, smem, &bars[0], t + 1);
     if constexpr (!SKIP) {
-      if (hv > 0) tile_dispatch<K, EMU_PERIOD>(hv, A, np, m);
+      if (hv > 0) tile_dispatch<K, EMU_PERIOD>(kv, a.lo_slot != 0, A, np, m);
     } else if (hv > 0) {
       {
         float x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY;
@@ -403,7 +459,7 @@ __global__ void __launch_bounds__(32 * NW, min_blocks<NW, K>()) compat_kernel(co
         const bool skip = __all_sync(0xffffffffu, far);
         if (skip && lane == 0 && a.skip_count != nullptr)
           atomicAdd(a.skip_count, static_cast<unsigned long long>(np) * static_cast<unsigned long long>(min(32 * K, a.M - wbase)));
-        if (!skip) tile_dispatch<K, EMU_PERIOD>(hv, A, np, m);
+        if (!skip) tile_dispatch<K, EMU_PERIOD>(kv, a.lo_slot != 0, A, np, m);
       }
     }
   }
@@ -568,6 +624,11 @@ cudaError_t launch_compat(const CompatArgs &a_in, cudaStream_t s) {
   }();
   CompatArgs a = a_in;
   a.track_major = order_env;
+  static const int lo_env = [] {   // GLMB_COMPAT_LO=0: the packed pair always (A/B; same C bits)
+    const char *e = std::getenv("GLMB_COMPAT_LO");
+    return e ? std::atoi(e) : 1;
+  }();
+  a.lo_slot = lo_env != 0;
   if (a.NW == 1) return a.K == 1 ? launch_e<1, 1>(a, s) : launch_e<1, 2>(a, s);
   if (a.NW == 2) return launch_e<2, 2>(a, s);
   switch (a.K) {

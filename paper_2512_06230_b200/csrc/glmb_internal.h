@@ -65,6 +65,7 @@ struct CompatArgs {
   int32_t NW;        // warps per CTA
   int32_t CL;        // CTAs (particle chunks) per (track, measurement tile): cluster size
   int32_t track_major;  // unit order: 1 = a track's measurement tiles adjacent, 0 = tile-major
+  int32_t lo_slot;      // 1: a warp whose only valid slot is the pair's low one evaluates it alone
   // fused all-gather (glmb_compat_peers): n_peers > 0 writes column j to row peer_row0 + j of
   // every peer_C[r] / peer_G[r] (device arrays of n_peers pointers, e.g. symmetric memory
   // mapped over NVLink) instead of C_tracks / gate

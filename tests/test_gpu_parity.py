@@ -712,3 +712,25 @@ def test_compat_p1024_split_bit_identical(tmp_path):
         outs[cl] = np.load(out)
     np.testing.assert_array_equal(outs[""]["C"].view(np.uint32), outs["1"]["C"].view(np.uint32))
     np.testing.assert_array_equal(outs[""]["G"], outs["1"]["G"])
+
+
+def test_compat_low_slot_path_bit_identical(tmp_path):
+    """A warp whose only valid measurement slot is its packed pair's low one (the ragged last
+    warp of a tile when M mod 64 <= 32: config 1, M = 81) evaluates that lane alone with
+    scalar mirrors of the packed ops; C and the gate words equal the packed evaluation's
+    (GLMB_COMPAT_LO=0) bit for bit, births included."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    outs = {}
+    for lo in ("1", "0"):
+        out = str(tmp_path / f"lo{lo}.npz")
+        env = dict(os.environ, GLMB_COMPAT_LO=lo, PYTHONPATH=os.path.dirname(here))
+        r = subprocess.run([sys.executable, os.path.join(here, "_compat_dump.py"), "1", "64", "3", out, "68"],
+                           env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        outs[lo] = np.load(out)
+    assert outs["1"]["C"].shape[1] % 64 <= 32   # the low-slot path is exercised
+    np.testing.assert_array_equal(outs["1"]["C"].view(np.uint32), outs["0"]["C"].view(np.uint32))
+    np.testing.assert_array_equal(outs["1"]["G"], outs["0"]["G"])
